@@ -1,0 +1,163 @@
+/* tcudb.h — C ABI of the B200-native TCUDB join + group-by hot path.
+ *
+ * The operation (Fig. 4; §3.1; §3.3):
+ *
+ *     SELECT A.g, B.h, SUM(A.v * B.w)        -- or COUNT(*)
+ *     FROM A JOIN B ON A.k = B.k
+ *     GROUP BY A.g, B.h
+ *
+ * evaluated as C = A_op · B_opᵀ on the sm_100a tensor cores, where A_op[g][k]
+ * aggregates A's tuples of group g and join key k (the "adjacency over value
+ * domains" form, with the 1^{1×n} reduction of P:808-810 folded into
+ * the fill) and B_op likewise. The result is the list of (g, h, agg) for every
+ * group with at least one joined pair (existence = COUNT > 0; R3),
+ * sorted ascending by (g, h) (the ORDER BY-for-free reading of §3.4).
+ *
+ * Everything here is plain C: pointers, sizes, status codes. No torch types.
+ * All column/result pointers are DEVICE pointers on the context's device unless
+ * the entry point says HOST. The stream argument is a cudaStream_t passed as
+ * void* (NULL = the legacy default stream).
+ */
+#ifndef TCUDB_H_
+#define TCUDB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. On any error the result is empty (n = 0, NULL pointers): there
+ * are never partial results. E_CUDA is sticky: destroy the context. */
+typedef enum {
+  TCUDB_OK = 0,
+  TCUDB_E_INVALID = -1,     /* NULL / negative / mismatched arguments */
+  TCUDB_E_UNSUPPORTED = -2, /* float keys or groups, mixed int/float values, key span of 2^64 */
+  TCUDB_E_PRECISION = -3,   /* reserved: no exact or toleranced plan exists */
+  TCUDB_E_OVERFLOW = -4,    /* the precision guard proves an int64 result could overflow */
+  TCUDB_E_NOMEM = -5,       /* device memory for operands / C / result exhausted */
+  TCUDB_E_CUDA = -6,        /* CUDA runtime / launch error (sticky) */
+  TCUDB_E_COMM = -7         /* reserved for the collective path */
+} tcudb_status;
+
+typedef enum { TCUDB_I32 = 0, TCUDB_I64 = 1, TCUDB_F32 = 2, TCUDB_F64 = 3 } tcudb_dtype;
+typedef enum { TCUDB_COUNT = 0, TCUDB_SUM = 1 } tcudb_agg;
+
+/* One column: data == NULL means "absent". A value column that is absent means
+ * the factor 1 (so SUM with both values absent equals COUNT). */
+typedef struct {
+  const void* data;
+  int32_t type; /* tcudb_dtype. Keys/groups: I32 or I64. Values: I32, I64 or F32. */
+} tcudb_col;
+
+/* A table in column-store layout: n_rows entries per column. */
+typedef struct {
+  int64_t n_rows;
+  tcudb_col key;   /* join key k (required) */
+  tcudb_col group; /* group key: A.g or B.h (required) */
+  tcudb_col value; /* A.v or B.w (optional) */
+} tcudb_table;
+
+/* Query flags (default 0: selector chooses the path, results sorted by (g,h)). */
+enum {
+  TCUDB_FORCE_DENSE = 1u << 0,  /* tensor-core GEMM path (a5, a6) */
+  TCUDB_FORCE_SPARSE = 1u << 1, /* sparse-operand expand path (a7) */
+  TCUDB_GATHER_NONE = 1u << 2,  /* reserved (multi-GPU: keep row shards) */
+  TCUDB_UNORDERED = 1u << 3,    /* reserved: output order unspecified */
+  TCUDB_FORCE_WIDE = 1u << 4    /* test hook: skip the packed-u8 COUNT fill, use the
+                                   32-bit scratch + digit-plane guard path */
+};
+
+typedef struct {
+  int32_t agg;    /* tcudb_agg */
+  uint32_t flags; /* TCUDB_* flags above */
+} tcudb_query;
+
+/* Result tuples (SoA). g has A.group's type, h has B.group's type, agg is I64
+ * for COUNT and integer SUM, F64 for float SUM. Owned by the caller; release
+ * with tcudb_result_free (device) — or tcudb_result_free_host for results of
+ * tcudb_join_agg_host. */
+typedef struct {
+  int64_t n;
+  void* g;
+  void* h;
+  void* agg;
+  int32_t g_type, h_type, agg_type;
+  int32_t on_host; /* 1 if the arrays are pinned host memory */
+} tcudb_result;
+
+/* Plan and stage breakdown of one query (cf. SPEC ExecutionReport S:502-505 and
+ * the paper's stage breakdowns P:1531-1546). Times are CUDA-event milliseconds
+ * on the query stream; ms_total is host wall clock of the whole call. */
+typedef struct {
+  int32_t path;       /* 0 dense (tensor cores), 1 sparse expand */
+  int32_t elem;       /* dense operand type: 0 u8/s8 (kind::i8), 1 bf16, 2 bf16x3 split */
+  int32_t planes_a;   /* base-256 digit planes of A_op (int SUM) */
+  int32_t planes_b;
+  int32_t existence;  /* 0: existence from C itself, 1: separate COUNT plane */
+  int32_t kchunks;    /* K chunks accumulated in int64 (1 = single int32 pass) */
+  int32_t key_mode;   /* 0 direct-offset dictionary, 1 hash dictionary (join key) */
+  int32_t n_launches; /* kernels launched by this call */
+  int64_t G, H, K, K_union, join_pairs, n_result;
+  double density_union; /* nnz cells / (G * K_union): the paper's density */
+  double gemm_ops;      /* 2 * Gp * Hp * Kp summed over GEMM launches (dense path) */
+  float ms_stats, ms_encode, ms_fill, ms_gemm, ms_sparse, ms_compact, ms_total;
+} tcudb_stats;
+
+typedef struct tcudb_ctx tcudb_ctx;
+
+/* Optional stream-ordered allocator callbacks for RESULT arrays (e.g. a caching
+ * allocator). NULL: the library uses cudaMallocAsync from its own pool. */
+typedef void* (*tcudb_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*tcudb_free_fn)(void* ptr, void* stream, void* user);
+
+/* Create a context on `device`. nccl_comm is reserved (pass NULL); the
+ * multi-GPU row sharding lives in the Python layer. Returns E_CUDA if the
+ * device is not sm_100 or the CUDA runtime fails. */
+tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_alloc_fn alloc_fn,
+                          tcudb_free_fn free_fn, void* user);
+
+/* The join + group-by query. A, B: device columns, read-only,
+ * any alignment. On success *out holds device arrays (caller owns). Blocks the
+ * host on at most 4 small device->host reads (statistics, sizes, join size,
+ * nnz); results are valid once `stream` passes the call. One query in flight
+ * per context. `stats` may be NULL. */
+tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B,
+                            const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, void* stream);
+
+/* Same query with HOST columns: copies the columns host->device (pinned or
+ * pageable), runs tcudb_join_agg and copies the result tuples back into pinned
+ * host arrays (out->on_host = 1; release with tcudb_result_free_host). */
+tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B,
+                                 const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, void* stream);
+
+/* Triangle count of the simple undirected graph of an edge list (self-loops
+ * dropped, duplicates and direction ignored): T = trace(A³)/6 over the
+ * symmetrised 0/1 adjacency A, evaluated as the 2-hop GEMM A·A with an epilogue
+ * that multiplies each accumulator tile by the matching A tile and reduces to
+ * one int64 (§3.2 chain exception P:751-756). src/dst:
+ * device I32 or I64 columns of n_edges entries. */
+tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* src, const void* dst,
+                                  int32_t id_type, int64_t* triangles_out, tcudb_stats* stats, void* stream);
+
+/* Step a6 on its own (for kernel tests and calibration): C[M][N] = A[M][K]·B[N][K]ᵀ
+ * with K-major device operands. elem 0: int8 (a_signed/b_signed select s8 vs
+ * u8), C int32; elem 1: bf16, C fp32. Requirements: M % 128 == 0,
+ * N % 256 == 0, K*elem_bytes % 128 == 0, row strides lda/ldb/ldc in elements
+ * with lda*elem_bytes % 16 == 0, 16-byte aligned base pointers. */
+tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t b_signed, int64_t M, int64_t N,
+                        int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                        void* stream);
+
+void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r);
+void tcudb_result_free_host(tcudb_ctx* ctx, tcudb_result* r);
+const char* tcudb_last_error(const tcudb_ctx* ctx);
+/* Kernel launches recorded since the context was created (evidence counter). */
+int64_t tcudb_launch_count(const tcudb_ctx* ctx);
+void tcudb_destroy(tcudb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCUDB_H_ */

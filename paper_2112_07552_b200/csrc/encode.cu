@@ -1,0 +1,371 @@
+// encode.cu — steps a1/a2: column statistics and key-domain encoding.
+//
+// PAPER.md §3.1: dom(ID) = dom(A.ID) ∪ dom(B.ID) = {v_1..v_k},
+// v_j ↦ column j; §4.2.1 per-column metadata (min, max,
+// #distinct). Readings: codes are dense ranks (R2); the join-key
+// domain keeps only keys present on BOTH sides (∩ ⊆ ∪ gives the same result —
+// a key on one side only yields a zero column; R1).
+//
+// Two dictionary mechanisms, chosen per domain from the min/max statistics:
+//   direct-offset (span <= 4n): presence flags over [min, max], codes = exclusive
+//     scan of the flags (ascending by construction);
+//   hash (otherwise): open-addressing table of 2^ceil(log2 2n) slots keyed by
+//     (x - min) with warp-aggregated inserts (__match_any_sync de-duplicates
+//     equal keys inside a warp before the CAS), side flags, compaction by scan,
+//     and — for the group domains — an LSD radix sort of the distinct values so
+//     codes are ascending ranks (result order = (g,h) order).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tcudb {
+namespace {
+
+constexpr int T = 256;
+
+TCUDB_DEV unsigned long long fmix64(unsigned long long k) {
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+// ------------------------------------------------------------------ a1: statistics
+// blockIdx.y = column id. Integer columns: min / max (int64). Float columns:
+// min / max / min |x| (ordered-int encodings of fp32).
+__global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColDesc c4, ColDesc c5,
+                            ColStats* __restrict__ st) {
+  ColDesc c = blockIdx.y == 0 ? c0 : blockIdx.y == 1 ? c1 : blockIdx.y == 2 ? c2 : blockIdx.y == 3 ? c3
+             : blockIdx.y == 4 ? c4 : c5;
+  if (!c.data || c.n <= 0) return;
+  ColStats* s = st + blockIdx.y;
+  const int64_t stride = (int64_t)gridDim.x * T;
+  if (c.type == 2) {  // fp32
+    float mn = INFINITY, mx = -INFINITY, mabs = INFINITY;
+    int nonfinite = 0;
+    const float* p = static_cast<const float*>(c.data);
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < c.n; i += stride) {
+      const float x = __ldg(p + i);
+      if (!isfinite(x)) nonfinite = 1;
+      mn = fminf(mn, x); mx = fmaxf(mx, x); mabs = fminf(mabs, fabsf(x));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mabs = fminf(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+    }
+    nonfinite = __any_sync(0xffffffffu, nonfinite);
+    if (lane_id() == 0) {
+      // fp32 -> order-preserving int: flip for negatives
+      auto ord = [](float f) { int b = __float_as_int(f); return b >= 0 ? (long long)b : (long long)(b ^ 0x7fffffff); };
+      atomicMin(&s->mn, ord(mn));
+      atomicMax(&s->mx, ord(mx));
+      atomicMin(&s->min_abs, ord(mabs));
+      if (nonfinite) atomicOr(&s->flags, 1);
+    }
+    return;
+  }
+  long long mn = LLONG_MAX, mx = LLONG_MIN, mabs = LLONG_MAX;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < c.n; i += stride) {
+    const long long x = ld_int(c.data, c.type, i);
+    mn = min(mn, x); mx = max(mx, x);
+    const long long a = x < 0 ? (x == LLONG_MIN ? LLONG_MAX : -x) : x;
+    mabs = min(mabs, a);
+  }
+  mn = warp_min_ll(mn); mx = warp_max_ll(mx); mabs = warp_min_ll(mabs);
+  if (lane_id() == 0) { atomicMin(&s->mn, mn); atomicMax(&s->mx, mx); atomicMin(&s->min_abs, mabs); }
+}
+
+__global__ void k_init_stats(ColStats* st, int n) {
+  const int i = threadIdx.x;
+  if (i < n) { st[i].mn = LLONG_MAX; st[i].mx = LLONG_MIN; st[i].min_abs = LLONG_MAX; st[i].flags = 0; }
+}
+
+// ------------------------------------------------------------------ direct-offset dictionary
+__global__ void k_mark_direct(ColDesc c, long long minv, uint8_t* __restrict__ flags) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < c.n; i += stride)
+    flags[(unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv] = 1;
+}
+
+// ------------------------------------------------------------------ hash dictionary
+// Slot key = (x - min) as u64; EMPTY = ~0. Linear probing; equal keys in a warp
+// are inserted once (warp aggregation). flags[slot] = 1 marks the side.
+__global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __restrict__ slots,
+                              unsigned long long mask, uint8_t* __restrict__ flags) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  const int64_t n_round = (c.n + 31) & ~int64_t(31);
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_round; i += stride) {
+    const bool ok = i < c.n;
+    const unsigned long long off = ok ? (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv
+                                      : ~0ull - 1 - lane_id();
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    const unsigned peers = __match_any_sync(0xffffffffu, off) & act;
+    if (!ok || (__ffs(peers) - 1) != lane_id()) continue;  // lowest active peer lane inserts
+    unsigned long long h = fmix64(off) & mask;
+    while (true) {
+      const unsigned long long prev = atomicCAS(slots + h, ~0ull, off);
+      if (prev == ~0ull || prev == off) break;
+      h = (h + 1) & mask;
+    }
+    if (!flags[h]) flags[h] = 1;
+  }
+}
+
+// ------------------------------------------------------------------ predicate scan -> codes
+// pred(i) = fa[i] && (fb ? fb[i] : 1). Tile = 4096 flags per 256-thread block.
+constexpr int PT = 4096;
+__global__ void k_pred_count(const uint8_t* __restrict__ fa, const uint8_t* __restrict__ fb, int64_t n,
+                             int32_t* __restrict__ tile_cnt, unsigned long long* __restrict__ union_cnt) {
+  const int64_t base = (int64_t)blockIdx.x * PT + threadIdx.x * 16;
+  int c = 0, u = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t i = base + j;
+    if (i < n) {
+      const int a = fa[i], b = fb ? fb[i] : 1;
+      c += a & b;
+      if (fb) u += a | b;
+    }
+  }
+  c = warp_sum(c); u = warp_sum(u);
+  __shared__ int sc[T / 32], su[T / 32];
+  if (lane_id() == 0) { sc[warp_id()] = c; su[warp_id()] = u; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tc = 0, tu = 0;
+    for (int w = 0; w < T / 32; ++w) { tc += sc[w]; tu += su[w]; }
+    tile_cnt[blockIdx.x] = tc;
+    if (union_cnt && tu) atomicAdd(union_cnt, (unsigned long long)tu);
+  }
+}
+
+__global__ void k_pred_codes(const uint8_t* __restrict__ fa, const uint8_t* __restrict__ fb, int64_t n,
+                             const int64_t* __restrict__ tile_off, int32_t* __restrict__ code) {
+  const int64_t base = (int64_t)blockIdx.x * PT + threadIdx.x * 16;
+  uint8_t p[16];
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t i = base + j;
+    p[j] = (i < n) ? (uint8_t)(fa[i] & (fb ? fb[i] : 1)) : 0;
+    c += p[j];
+  }
+  // block exclusive scan of c
+  int x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane_id() >= o) x += y; }
+  __shared__ int wt[T / 32];
+  if (lane_id() == 31) wt[warp_id()] = x;
+  __syncthreads();
+  int wp = 0;
+  for (int w = 0; w < warp_id(); ++w) wp += wt[w];
+  int64_t run = tile_off[blockIdx.x] + wp + x - c;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t i = base + j;
+    if (i < n) { code[i] = p[j] ? (int32_t)run : -1; run += p[j]; }
+  }
+}
+
+// ------------------------------------------------------------------ group dictionaries
+// direct: dict[code[x]] = min + x
+__global__ void k_direct_dict(const int32_t* __restrict__ code, int64_t range, long long minv,
+                              long long* __restrict__ dict) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t x = (int64_t)blockIdx.x * T + threadIdx.x; x < range; x += stride) {
+    const int32_t c = code[x];
+    if (c >= 0) dict[c] = minv + (long long)x;
+  }
+}
+// hash: gather (slot key, slot) pairs of occupied slots into compaction order
+__global__ void k_gather_slots(const int32_t* __restrict__ tmp_code, const unsigned long long* __restrict__ slots,
+                               int64_t cap, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t s = (int64_t)blockIdx.x * T + threadIdx.x; s < cap; s += stride) {
+    const int32_t c = tmp_code[s];
+    if (c >= 0) { keys[c] = slots[s]; vals[c] = (uint32_t)s; }
+  }
+}
+// hash: after sorting by key, rank i -> slot_code[slot] = i, dict[i] = min + key
+__global__ void k_rank_write(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
+                             int64_t n, long long minv, int32_t* __restrict__ slot_code,
+                             long long* __restrict__ dict) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    slot_code[vals[i]] = (int32_t)i;
+    dict[i] = (long long)(keys[i] + (unsigned long long)minv);
+  }
+}
+
+// ------------------------------------------------------------------ probe (codes per tuple)
+TCUDB_DEV int32_t dict_lookup(const DictView& d, long long x) {
+  const unsigned long long off = (unsigned long long)x - (unsigned long long)d.minv;
+  if (d.mode == 0) return off < d.size ? d.code[off] : -1;
+  unsigned long long h = fmix64(off) & d.size;  // size = mask in hash mode
+  while (true) {
+    const unsigned long long k = d.slots[h];
+    if (k == off) return d.code[h];
+    if (k == ~0ull) return -1;
+    h = (h + 1) & d.size;
+  }
+}
+
+// kcode / gcode per tuple; per-key counts (warp-aggregated); per-group tuple
+// counts and sum |v| of tuples whose key survives the ∩ (guard bounds, a3).
+__global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, DictView gd,
+                        int32_t* __restrict__ kcode, int32_t* __restrict__ gcode, int32_t* __restrict__ cnt_k,
+                        double* __restrict__ rowabs_g) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  const int64_t n_round = (key.n + 31) & ~int64_t(31);
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_round; i += stride) {
+    const bool ok = i < key.n;
+    int32_t kc = -1, gc = -1;
+    if (ok) {
+      kc = dict_lookup(kd, ld_int(key.data, key.type, i));
+      gc = dict_lookup(gd, ld_int(grp.data, grp.type, i));
+      kcode[i] = kc;
+      gcode[i] = gc;
+    }
+    const int32_t kk = (ok && kc >= 0) ? kc : -2 - lane_id();
+    const unsigned peers = __match_any_sync(0xffffffffu, kk);
+    if (ok && kc >= 0 && (__ffs(peers) - 1) == lane_id()) atomicAdd(cnt_k + kc, __popc(peers));
+    if (ok && kc >= 0 && rowabs_g) {
+      // sum |v| per group in fp64 (a bound only: no wrap-around, relative rounding ~1e-16 * n)
+      double a = 1.0;
+      if (val.data) {
+        if (val.type == 2) a = 0.0;  // float: bound not needed
+        else a = fabs((double)ld_int(val.data, val.type, i));
+      }
+      atomicAdd(rowabs_g + gc, a);
+    }
+  }
+}
+
+// J = sum_k cntA[k] * cntB[k] (join size, a4) and max per-key counts.
+__global__ void k_join_size(const int32_t* __restrict__ ca, const int32_t* __restrict__ cb, int64_t K,
+                            unsigned long long* __restrict__ J) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  unsigned long long s = 0;
+  for (int64_t k = (int64_t)blockIdx.x * T + threadIdx.x; k < K; k += stride)
+    s += (unsigned long long)ca[k] * (unsigned long long)cb[k];
+  s = warp_sum(s);
+  if (lane_id() == 0 && s) atomicAdd(J, s);
+}
+
+__global__ void k_max_u64(const unsigned long long* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  unsigned long long m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) m = max(m, x[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(out, m);
+}
+
+inline int grid_for(int64_t n, int per_block = T * 4) {
+  int64_t g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > kNumSMs * 16) g = kNumSMs * 16;
+  return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, int64_t* launches) {
+  k_init_stats<<<1, 32, 0, s>>>(st, 6);
+  int64_t nmax = 1;
+  for (int i = 0; i < 6; ++i) if (cols[i].data && cols[i].n > nmax) nmax = cols[i].n;
+  dim3 grid(grid_for(nmax, T * 8), 6);
+  k_col_stats<<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, cudaStream_t s, int64_t* launches) {
+  if (c.n <= 0) return cudaSuccess;
+  k_mark_direct<<<grid_for(c.n), T, 0, s>>>(c, minv, flags);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
+                               uint8_t* flags, cudaStream_t s, int64_t* launches) {
+  if (c.n <= 0) return cudaSuccess;
+  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+size_t pred_temp_bytes(int64_t n) {
+  const int64_t nt = (n + PT - 1) / PT;
+  return ((size_t)nt * 4 + 15) / 16 * 16 + (size_t)nt * 8 + scan_temp_bytes(nt) + 64;
+}
+
+cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, int32_t* code, int64_t* count_dev,
+                              unsigned long long* union_dev, void* temp, cudaStream_t s, int64_t* launches) {
+  const int64_t nt = (n + PT - 1) / PT;
+  if (n <= 0) return exclusive_scan_i32(nullptr, nullptr, 0, count_dev, temp, s, launches);
+  int32_t* tc = static_cast<int32_t*>(temp);
+  int64_t* toff = reinterpret_cast<int64_t*>(static_cast<char*>(temp) + ((size_t)nt * 4 + 15) / 16 * 16);
+  void* st = toff + nt;
+  k_pred_count<<<(unsigned)nt, T, 0, s>>>(fa, fb, n, tc, union_dev);
+  if (launches) ++*launches;
+  cudaError_t e = exclusive_scan_i32(tc, toff, nt, count_dev, st, s, launches);
+  if (e != cudaSuccess) return e;
+  k_pred_codes<<<(unsigned)nt, T, 0, s>>>(fa, fb, n, toff, code);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct_dict(const int32_t* code, int64_t range, long long minv, long long* dict, cudaStream_t s,
+                               int64_t* launches) {
+  k_direct_dict<<<grid_for(range), T, 0, s>>>(code, range, minv, dict);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_slots(const int32_t* tmp_code, const unsigned long long* slots, int64_t cap,
+                                unsigned long long* keys, uint32_t* vals, cudaStream_t s, int64_t* launches) {
+  k_gather_slots<<<grid_for(cap), T, 0, s>>>(tmp_code, slots, cap, keys, vals);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* vals, int64_t n, long long minv,
+                              int32_t* slot_code, long long* dict, cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_rank_write<<<grid_for(n), T, 0, s>>>(keys, vals, n, minv, slot_code, dict);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
+                         const DictView& gd, int32_t* kcode, int32_t* gcode, int32_t* cnt_k,
+                         double* rowabs_g, cudaStream_t s, int64_t* launches) {
+  if (key.n <= 0) return cudaSuccess;
+  k_probe<<<grid_for(key.n), T, 0, s>>>(key, grp, val, kd, gd, kcode, gcode, cnt_k, rowabs_g);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* J, cudaStream_t s,
+                             int64_t* launches) {
+  if (K <= 0) return cudaSuccess;
+  k_join_size<<<grid_for(K), T, 0, s>>>(ca, cb, K, J);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_u64(const unsigned long long* x, int64_t n, unsigned long long* out, cudaStream_t s,
+                           int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_max_u64<<<grid_for(n), T, 0, s>>>(x, n, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace tcudb

@@ -1,0 +1,267 @@
+// gemm_tc.cu — step a6: the tensor-core GEMM C = A_op · B_opᵀ on sm_100a.
+//
+// PAPER.md §3.1 "C = mat(A) × mat(B)^T", §3.3 the
+// group-by aggregate as a product, Eq. 3 CT = 2MNK / peak.
+// The paper ran WMMA/cuBLAS fp16 on Turing/Ampere; here:
+//   * tcgen05.mma kind::i8 (u8/s8 -> s32, exact) or kind::f16 (bf16 -> f32),
+//     issued by one thread, accumulators in TMEM (2 x 256 columns: the epilogue
+//     of tile t overlaps the main loop of tile t+1);
+//   * TMA 2D tile loads with 128-byte swizzle into a 4-stage mbarrier ring;
+//   * persistent CTAs (grid = #SMs) walking a grouped tile order;
+//   * warp roles: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-5 epilogue.
+// Tile 128 x 256 x (128 bytes of K) per stage.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tcudb {
+namespace {
+
+constexpr int BM = kGemmBM, BN = kGemmBN, BKB = kGemmBKBytes;
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BKB;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BKB;  // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int NUM_THREADS = 192;         // 6 warps
+constexpr int TMEM_COLS = 512;           // 2 accumulators x 256 fp32/s32 columns
+constexpr int GROUP_M = 16;              // tile raster: 16 M-blocks per band
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct KParams {
+  int64_t M, N;
+  int tiles_m, tiles_n;
+  int num_kb;        // K blocks of 128 bytes
+  int kb_begin;      // first K block (elements / elems_per_kb)
+  int elems_per_kb;  // 128 (i8) or 64 (bf16)
+  int is_bf16;
+  uint32_t idesc;
+  int epi;
+  void* C; int64_t ldc; int shift;
+  const uint8_t* mask; int64_t ldm, mask_rows, mask_cols;
+  unsigned long long* tri_out;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
+  const int band = t / (GROUP_M * tiles_n);
+  const int first_m = band * GROUP_M;
+  const int gsz = min(tiles_m - first_m, GROUP_M);
+  const int r = t - band * GROUP_M * tiles_n;
+  mb = first_m + r % gsz;
+  nb = r / gsz;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment required by the 128B swizzle atoms.
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int num_tiles = p.tiles_m * p.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          const int kc = (p.kb_begin + kb) * p.elems_per_kb;
+          tma_load_2d(&tmA, sA + stage * A_STAGE_BYTES, &full[stage], kc, mb * BM, pol);
+          tma_load_2d(&tmB, sB + stage * B_STAGE_BYTES, &full[stage], kc, nb * BN, pol);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A_STAGE_BYTES));
+          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * B_STAGE_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 bytes of K per 128-byte stage
+            const uint32_t accum = (kb | kk) != 0;
+            if (p.is_bf16) mma_f16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
+            else mma_i8(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);      // accumulator ready for the epilogue
+        acc ^= 1; if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 =====================
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0; uint32_t acc_phase = 0;
+    long long tri = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_wait();
+        const int64_t col = (int64_t)nb * BN + c * 32;
+        if (p.epi == EPI_STORE32) {
+          int4* dst = reinterpret_cast<int4*>(reinterpret_cast<uint32_t*>(p.C) + row * p.ldc + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dst[i] = make_int4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+        } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
+          long long* dst = reinterpret_cast<long long*>(p.C) + row * p.ldc + col;
+          longlong2* d2 = reinterpret_cast<longlong2*>(dst);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            long long x0 = (long long)(int)r[2 * i] << p.shift, x1 = (long long)(int)r[2 * i + 1] << p.shift;
+            if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += o.x; x1 += o.y; }
+            d2[i] = make_longlong2(x0, x1);
+          }
+        } else {  // EPI_TRI
+          if (row < p.mask_rows && col < p.mask_cols) {
+            const uint4* m4 = reinterpret_cast<const uint4*>(p.mask + row * p.ldm + col);
+            const uint4 ma = m4[0], mb4 = m4[1];
+            const uint32_t mw[8] = {ma.x, ma.y, ma.z, ma.w, mb4.x, mb4.y, mb4.z, mb4.w};
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tri += (long long)(int)r[i] * (long long)((mw[i >> 2] >> (8 * (i & 3))) & 0xFF);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1; if (acc == 0) acc_phase ^= 1;
+    }
+    if (p.epi == EPI_TRI) {
+      tri = warp_sum(tri);
+      if (lane == 0 && tri != 0) atomicAdd(p.tri_out, (unsigned long long)tri);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int elem, int64_t rows, int64_t cols_elems, int64_t ld_elems,
+              int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  const int esz = elem == ELEM_BF16 ? 2 : 1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)(BKB / esz), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, elem == ELEM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
+  const int esz = a.elem == ELEM_BF16 ? 2 : 1;
+  if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
+  if (a.M % BM || a.N % BN || (a.k_len * esz) % BKB || (a.k_begin * esz) % BKB) return cudaErrorInvalidValue;
+  if ((a.lda * esz) % 16 || (a.ldb * esz) % 16) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t kcols = a.k_begin + a.k_len;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, a.elem, a.M, kcols, a.lda, BM) || !make_map(&mB, a.B, a.elem, a.N, kcols, a.ldb, BN))
+    return cudaErrorInvalidValue;
+  KParams p{};
+  p.M = a.M; p.N = a.N;
+  p.tiles_m = (int)(a.M / BM); p.tiles_n = (int)(a.N / BN);
+  p.elems_per_kb = BKB / esz;
+  p.num_kb = (int)(a.k_len / p.elems_per_kb);
+  p.kb_begin = (int)(a.k_begin / p.elems_per_kb);
+  p.is_bf16 = a.elem == ELEM_BF16;
+  // Instruction descriptor: D format (bits 4-5: 1 F32, 2 S32), A/B format (bits 7-9, 10-12:
+  // kind::i8 0 U8 / 1 S8; kind::f16 1 BF16), K-major A and B (bits 15, 16 = 0),
+  // N >> 3 (bits 17-22), M >> 4 (bits 24-28).
+  uint32_t idesc = 0;
+  if (p.is_bf16) idesc |= (1u << 4) | (1u << 7) | (1u << 10);
+  else idesc |= (2u << 4) | ((uint32_t)(a.a_signed != 0) << 7) | ((uint32_t)(a.b_signed != 0) << 10);
+  idesc |= (uint32_t)(BN >> 3) << 17;
+  idesc |= (uint32_t)(BM >> 4) << 24;
+  p.idesc = idesc;
+  p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = a.shift;
+  p.mask = a.mask; p.ldm = a.ldm; p.mask_rows = a.mask_rows; p.mask_cols = a.mask_cols; p.tri_out = a.tri_out;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  k_gemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace tcudb

@@ -1,0 +1,50 @@
+// internal.h — launchers shared between the kernel files and the host runtime.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tcudb {
+
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------- a6: tcgen05 GEMM
+enum GemmElem { ELEM_I8 = 0, ELEM_BF16 = 1 };
+enum GemmEpi {
+  EPI_STORE32 = 0,  // C32[r][c] = acc (int32 or fp32 bits)
+  EPI_SET64 = 1,    // C64[r][c] = (int64)acc << shift
+  EPI_ACC64 = 2,    // C64[r][c] += (int64)acc << shift
+  EPI_TRI = 3       // *tri_out += sum acc[r][c] * mask[r][c]   (triangle epilogue, a9)
+};
+constexpr int kGemmBM = 128;
+constexpr int kGemmBN = 256;
+constexpr int kGemmBKBytes = 128;
+
+struct GemmArgs {
+  int elem = ELEM_I8;
+  int a_signed = 0, b_signed = 0;
+  int64_t M = 0, N = 0;           // rows of A, rows of B (multiples of 128 / 256)
+  int64_t k_begin = 0, k_len = 0; // K range in elements (k_len * bytes % 128 == 0)
+  const void* A = nullptr; int64_t lda = 0;  // elements
+  const void* B = nullptr; int64_t ldb = 0;
+  int epi = EPI_STORE32;
+  void* C = nullptr; int64_t ldc = 0; int shift = 0;
+  const uint8_t* mask = nullptr; int64_t ldm = 0, mask_rows = 0, mask_cols = 0;
+  unsigned long long* tri_out = nullptr;
+};
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
+
+// ---------------------------------------------------------------- scan
+// Exclusive prefix sum of n int64 values (in -> out, out may alias in); total in *total_dev (optional).
+size_t scan_temp_bytes(int64_t n);
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* total_dev, void* temp,
+                               cudaStream_t s, int64_t* launches);
+cudaError_t exclusive_scan_i32(const int32_t* in, int64_t* out, int64_t n, int64_t* total_dev, void* temp,
+                               cudaStream_t s, int64_t* launches);
+
+// ---------------------------------------------------------------- radix sort (key u64, payload u32)
+size_t radix_temp_bytes(int64_t n);
+cudaError_t radix_sort_pairs(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt,
+                             uint32_t* vals_alt, int64_t n,
+                             int bits, void* temp, cudaStream_t s, int64_t* launches, bool* result_in_alt);
+
+}  // namespace tcudb

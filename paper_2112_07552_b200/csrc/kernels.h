@@ -1,0 +1,134 @@
+// kernels.h — device-side data descriptors and the launchers of encode / fill /
+// sparse / compaction kernels (host runtime in tcudb.cu drives them).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace tcudb {
+
+// One input column (device pointer; type: 0 I32, 1 I64, 2 F32; data == NULL absent).
+struct ColDesc {
+  const void* data;
+  int type;
+  int64_t n;
+};
+
+// Column statistics (a1 / D2). Integer columns: mn, mx, min_abs as int64.
+// Float columns: order-preserving int encodings of fp32 (see decode_ord), flags bit0 = non-finite seen.
+struct ColStats {
+  long long mn, mx, min_abs;
+  int flags;
+  int pad;
+};
+
+// Read-only view of one dictionary for lookups.
+//   mode 0 (direct): code[x - minv] for x - minv < size
+//   mode 1 (hash):   slots[] open addressing, size = capacity - 1 (mask), code[slot]
+struct DictView {
+  int mode;
+  long long minv;
+  unsigned long long size;
+  const int32_t* code;
+  const unsigned long long* slots;
+};
+
+// ---------------------------------------------------------------- encode.cu
+cudaError_t launch_col_stats(const ColDesc* cols6, ColStats* st, cudaStream_t s, int64_t* launches);
+cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, cudaStream_t s, int64_t* launches);
+cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
+                               uint8_t* flags, cudaStream_t s, int64_t* launches);
+size_t pred_temp_bytes(int64_t n);
+cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, int32_t* code, int64_t* count_dev,
+                              unsigned long long* union_dev, void* temp, cudaStream_t s, int64_t* launches);
+cudaError_t launch_direct_dict(const int32_t* code, int64_t range, long long minv, long long* dict, cudaStream_t s,
+                               int64_t* launches);
+cudaError_t launch_gather_slots(const int32_t* tmp_code, const unsigned long long* slots, int64_t cap,
+                                unsigned long long* keys, uint32_t* vals, cudaStream_t s, int64_t* launches);
+cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* vals, int64_t n, long long minv,
+                              int32_t* slot_code, long long* dict, cudaStream_t s, int64_t* launches);
+cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
+                         const DictView& gd, int32_t* kcode, int32_t* gcode, int32_t* cnt_k,
+                         double* rowabs_g, cudaStream_t s, int64_t* launches);
+cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* J, cudaStream_t s,
+                             int64_t* launches);
+cudaError_t launch_max_u64(const unsigned long long* x, int64_t n, unsigned long long* out, cudaStream_t s,
+                           int64_t* launches);
+
+// ---------------------------------------------------------------- fill.cu (a5)
+// Device-side fill statistics read by the precision guard (a3).
+struct FillStats {
+  unsigned long long max_abs;  // max |cell| (integer scratch) or packed-u8 max cell
+  unsigned long long nnz;      // non-zero cells
+  int overflow;                // packed-u8 carry or int32 scratch overflow seen
+  int inexact;                 // float: some cell is not bf16-exact
+  int neg;                     // some cell < 0
+  int pad;
+};
+// COUNT: packed u8 atomics directly into op[row][k] (row = code of the group).
+cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
+                                 FillStats* fs, cudaStream_t s, int64_t* launches);
+// Pattern plane op[r][k] = 1 where a cell holds >= 1 tuple; symmetric adjacency for triangles.
+cudaError_t launch_fill_pattern_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
+                                   cudaStream_t s, int64_t* launches);
+cudaError_t launch_fill_sym_pattern(const int32_t* u, const int32_t* v, int64_t n, uint8_t* op, int64_t ld,
+                                    cudaStream_t s, int64_t* launches);
+// Integer values (or 1) accumulated into an int64 scratch [rows][ld] (wrapping adds: exact
+// modulo 2^64, so exact whenever the guard has bounded the true cell value inside int64).
+cudaError_t launch_fill_i64(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                            long long* scr, int64_t ld, cudaStream_t s, int64_t* launches);
+// Float values accumulated into an fp32 scratch.
+cudaError_t launch_fill_f32(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n, float* scr,
+                            int64_t ld, cudaStream_t s, int64_t* launches);
+// Statistics of an int64 scratch (max |cell|, nnz, sign).
+cudaError_t launch_scratch_stats_i64(const long long* scr, int64_t count, FillStats* fs, cudaStream_t s,
+                                     int64_t* launches);
+// Base-256 digit planes from an int64 scratch: plane p at op + p*plane_stride (bytes);
+// digits 0..P-2 are u8, the top digit is s8 when top_signed, else u8.
+cudaError_t launch_pack_planes(const long long* scr, int64_t count, int planes, int top_signed, uint8_t* op,
+                               int64_t plane_stride, cudaStream_t s, int64_t* launches);
+// fp32 scratch [rows][ld] -> bf16 hi into op[row][seg_hi*ld + k], lo = bf16(x - hi) into
+// op[row][seg_lo*ld + k] (row stride ld_op elements); counts inexact cells.
+cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int seg_hi,
+                             int seg_lo, FillStats* fs, cudaStream_t s, int64_t* launches);
+
+// ---------------------------------------------------------------- sparse.cu (a7)
+cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const ColDesc& w, int64_t n,
+                               const int64_t* bstart, int32_t* cursor, int32_t* b_h, void* b_w, int w_kind,
+                               cudaStream_t s, int64_t* launches);
+cudaError_t launch_work(const int32_t* kcode, int64_t n, const int32_t* cnt_b, int32_t* work, cudaStream_t s,
+                        int64_t* launches);
+cudaError_t launch_flags_from_work(const int32_t* work, int64_t n, int32_t* flags, cudaStream_t s,
+                                   int64_t* launches);
+cudaError_t launch_compact_active(const int32_t* work, const int64_t* pos, int64_t n, int32_t* act_a,
+                                  int32_t* act_w, cudaStream_t s, int64_t* launches);
+struct ExpandArgs {
+  int64_t n_act, J;
+  const int32_t* act_a; const int64_t* act_off;
+  const int32_t* kcodeA; const int32_t* gcodeA; ColDesc va;
+  const int64_t* bstart; const int32_t* b_h; const void* b_w;
+  int w_kind;      // 0 none (1), 1 int64, 2 f32
+  int acc_kind;    // 0 COUNT int32, 1 COUNT int64, 2 int SUM int64, 3 float SUM f64
+  void* C; int64_t ldc;
+  int32_t* cnt;    // optional existence count plane (int32) or NULL
+};
+cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s, int64_t* launches);
+
+// ---------------------------------------------------------------- compact.cu (a8)
+// Existence matrix E (int32 count or the value matrix) -> tuples (g, h, agg), row-major.
+struct CompactArgs {
+  int64_t G, H;
+  const void* E; int e_kind; int64_t lde;       // e_kind: 0 int32, 1 int64, 2 f32, 3 f64
+  const void* V; int v_kind; int64_t ldv;       // value matrix (agg), same kinds
+  const long long* dict_g; const long long* dict_h;
+  int g_out_type, h_out_type;                    // 0 I32, 1 I64
+  int agg_out;                                   // 0 int64, 1 f64
+  void* out_g; void* out_h; void* out_agg;
+};
+size_t compact_temp_bytes(int64_t G, int64_t H);
+cudaError_t launch_compact_count(const CompactArgs& a, int64_t* nnz_dev, void* temp, cudaStream_t s,
+                                 int64_t* launches);
+cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t s, int64_t* launches);
+
+}  // namespace tcudb

@@ -1,0 +1,180 @@
+// sparse.cu — step a7: the sparse-operand path for low-density key domains.
+//
+// PAPER.md §4.2.4: below a density threshold a dense TCU product
+// wastes work on zero tiles; TCUDB's TCU-SpMM skipped all-zero 16x16 tiles. On
+// B200 with random keys at ~0.1% density nearly every MMA-sized tile is
+// non-empty, so instead each joined pair is expanded once (J = sum_k
+// cntA(k)·cntB(k) updates, the "output size of the join"):
+//   1. bucket B by join-key code (CSC-by-key): offsets = scan(cntB), entries (h, w);
+//   2. compact the A tuples that have work (kcode >= 0, cntB(kcode) > 0);
+//   3. load-balanced expand: each 256-thread block owns 2048 consecutive updates of
+//      the global update sequence (merge-path on the prefix of per-tuple work), so
+//      skewed buckets (Zipf hubs) split evenly across blocks; every update is an
+//      atomic C[g][h] += v·w (int32 / int64 wrapping / fp64) plus an optional
+//      COUNT plane for existence (reading R3).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tcudb {
+namespace {
+
+constexpr int T = 256;
+constexpr int UPB = 2048;           // updates per block
+constexpr int UPT = UPB / T;        // updates per thread (strided by T)
+
+inline int grid_for(int64_t n, int per_block = T * 4) {
+  int64_t g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > kNumSMs * 16) g = kNumSMs * 16;
+  return (int)g;
+}
+
+__global__ void k_bucket_fill(const int32_t* __restrict__ kcode, const int32_t* __restrict__ hcode, ColDesc w,
+                              int64_t n, const int64_t* __restrict__ bstart, int32_t* __restrict__ cursor,
+                              int32_t* __restrict__ b_h, void* __restrict__ b_w, int w_kind) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t kc = kcode[i];
+    if (kc < 0) continue;
+    const int64_t pos = bstart[kc] + atomicAdd(cursor + kc, 1);
+    b_h[pos] = hcode[i];
+    if (w_kind == 1) static_cast<long long*>(b_w)[pos] = ld_int(w.data, w.type, i);
+    else if (w_kind == 2) static_cast<float*>(b_w)[pos] = __ldg(static_cast<const float*>(w.data) + i);
+  }
+}
+
+__global__ void k_work(const int32_t* __restrict__ kcode, int64_t n, const int32_t* __restrict__ cnt_b,
+                       int32_t* __restrict__ work) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t kc = kcode[i];
+    work[i] = kc >= 0 ? cnt_b[kc] : 0;
+  }
+}
+
+// pos = exclusive scan of (work > 0) computed by the caller as a scan over flags;
+// here flags are recomputed from work.
+__global__ void k_compact_active(const int32_t* __restrict__ work, const int64_t* __restrict__ pos, int64_t n,
+                                 int32_t* __restrict__ act_a, int32_t* __restrict__ act_w) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t wk = work[i];
+    if (wk > 0) { act_a[pos[i]] = (int32_t)i; act_w[pos[i]] = wk; }
+  }
+}
+
+__global__ void k_flags_from_work(const int32_t* __restrict__ work, int64_t n, int32_t* __restrict__ flags) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) flags[i] = work[i] > 0;
+}
+
+__global__ void __launch_bounds__(T) k_expand(const ExpandArgs a) {
+  __shared__ int64_t s_off[UPB + 2];
+  __shared__ int64_t s_a0;
+  __shared__ int s_cnt;
+  const int64_t u0 = (int64_t)blockIdx.x * UPB;
+  const int64_t u1 = min(u0 + UPB, a.J);
+  if (threadIdx.x == 0) {
+    // last active index whose offset <= u0
+    int64_t lo = 0, hi = a.n_act - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (a.act_off[mid] <= u0) lo = mid; else hi = mid - 1;
+    }
+    s_a0 = lo;
+    // number of active tuples overlapping [u0, u1): at most UPB + 1
+    int64_t lo2 = lo, hi2 = a.n_act - 1;
+    while (lo2 < hi2) {
+      const int64_t mid = (lo2 + hi2 + 1) >> 1;
+      if (a.act_off[mid] < u1) lo2 = mid; else hi2 = mid - 1;
+    }
+    s_cnt = (int)(lo2 - lo + 1);
+  }
+  __syncthreads();
+  const int64_t a0 = s_a0;
+  const int cnt = s_cnt;
+  for (int i = threadIdx.x; i < cnt; i += T) s_off[i] = a.act_off[a0 + i];
+  __syncthreads();
+#pragma unroll 2
+  for (int j = 0; j < UPT; ++j) {
+    const int64_t u = u0 + (int64_t)j * T + threadIdx.x;
+    if (u >= u1) break;
+    // largest local index l with s_off[l] <= u
+    int lo = 0, hi = cnt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    const int32_t ai = a.act_a[a0 + lo];
+    const int32_t kc = a.kcodeA[ai];
+    const int32_t g = a.gcodeA[ai];
+    const int64_t pos = a.bstart[kc] + (u - s_off[lo]);
+    const int32_t h = a.b_h[pos];
+    const int64_t cell = (int64_t)g * a.ldc + h;
+    switch (a.acc_kind) {
+      case 0: atomicAdd(static_cast<int*>(a.C) + cell, 1); break;
+      case 1: atomicAdd(static_cast<unsigned long long*>(a.C) + cell, 1ull); break;
+      case 2: {
+        const long long v = a.va.data ? ld_int(a.va.data, a.va.type, ai) : 1;
+        const long long w = a.w_kind == 1 ? static_cast<const long long*>(a.b_w)[pos] : 1;
+        atomicAdd(static_cast<unsigned long long*>(a.C) + cell, (unsigned long long)v * (unsigned long long)w);
+        break;
+      }
+      default: {
+        const double v = a.va.data ? (double)__ldg(static_cast<const float*>(a.va.data) + ai) : 1.0;
+        const double w = a.w_kind == 2 ? (double)static_cast<const float*>(a.b_w)[pos] : 1.0;
+        atomicAdd(static_cast<double*>(a.C) + cell, v * w);
+      }
+    }
+    if (a.cnt) atomicAdd(a.cnt + cell, 1);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const ColDesc& w, int64_t n,
+                               const int64_t* bstart, int32_t* cursor, int32_t* b_h, void* b_w, int w_kind,
+                               cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_bucket_fill<<<grid_for(n), T, 0, s>>>(kcode, hcode, w, n, bstart, cursor, b_h, b_w, w_kind);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_work(const int32_t* kcode, int64_t n, const int32_t* cnt_b, int32_t* work, cudaStream_t s,
+                        int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_work<<<grid_for(n), T, 0, s>>>(kcode, n, cnt_b, work);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_active(const int32_t* work, const int64_t* pos, int64_t n, int32_t* act_a,
+                                  int32_t* act_w, cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_compact_active<<<grid_for(n), T, 0, s>>>(work, pos, n, act_a, act_w);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flags_from_work(const int32_t* work, int64_t n, int32_t* flags, cudaStream_t s,
+                                   int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_flags_from_work<<<grid_for(n), T, 0, s>>>(work, n, flags);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.J <= 0 || a.n_act <= 0) return cudaSuccess;
+  const int64_t nb = (a.J + UPB - 1) / UPB;
+  if (nb > 0x7fffffffLL) return cudaErrorInvalidValue;
+  k_expand<<<(unsigned)nb, T, 0, s>>>(a);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace tcudb

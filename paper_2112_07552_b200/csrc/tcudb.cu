@@ -1,0 +1,885 @@
+// tcudb.cu — host runtime behind the C ABI (include/tcudb.h).
+//
+// Drives the hot path of SURVEY §8 CS3 on one stream:
+//   a1 column statistics (P:1005-1008 metadata)            -> sync 1
+//   a2 key / group dictionaries                -> sync 2 (sizes)
+//      probe: per-tuple codes, per-key counts, group bounds
+//   a4 selector: join size J, density, cost model (Eq. 3) -> sync 3
+//   dense:  a5 fill -> a3 precision guard -> sync 4
+//           a6 tcgen05 GEMM(s)
+//   sparse: a7 bucket + load-balanced expand
+//   a8 compaction + decode                     -> sync 5 (nnz)
+// Scratch comes from a stream-ordered CUDA memory pool (cudaMallocAsync);
+// result arrays from the caller's allocator callbacks when given.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tcudb.h"
+#include "kernels.h"
+
+using namespace tcudb;
+
+struct tcudb_ctx {
+  int device = 0;
+  cudaMemPool_t pool = nullptr;
+  tcudb_alloc_fn afn = nullptr;
+  tcudb_free_fn ffn = nullptr;
+  void* user = nullptr;
+  std::string err;
+  bool sticky = false;
+  int64_t launches = 0;
+  void* pinned = nullptr;  // small D2H staging
+  cudaEvent_t ev[8] = {};
+  std::mutex mu;
+  // pinned host block cache for host-API results: size -> free blocks
+  std::multimap<size_t, void*> host_free;
+  std::map<void*, size_t> host_size;
+  std::map<void*, bool> dev_from_cb;  // result pointer -> allocated through afn
+};
+
+namespace {
+
+constexpr size_t kPinnedBytes = 4096;
+
+struct Fail {
+  tcudb_status st;
+  const char* what = nullptr;
+  cudaError_t cuda = cudaSuccess;
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Query-scoped arena: stream-ordered allocations, all released at scope exit.
+struct Arena {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t st) : s(st) {}
+  ~Arena() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* get(int64_t count) {
+    if (count <= 0) count = 1;
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocAsync(&p, (size_t)count * sizeof(T), s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Fail{e == cudaErrorMemoryAllocation ? TCUDB_E_NOMEM : TCUDB_E_CUDA, "cudaMallocAsync", e};
+    }
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* zeros(int64_t count) {
+    T* p = get<T>(count);
+    ck(cudaMemsetAsync(p, 0, (size_t)(count > 0 ? count : 1) * sizeof(T), s));
+    return p;
+  }
+  static void ck(cudaError_t e, const char* what = "cuda call") {
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Fail{e == cudaErrorMemoryAllocation ? TCUDB_E_NOMEM : TCUDB_E_CUDA, what, e};
+    }
+  }
+};
+#define CK_STR2(x) #x
+#define CK_STR(x) CK_STR2(x)
+#define CK(x) Arena::ck((x), #x " @tcudb.cu:" CK_STR(__LINE__))
+
+inline bool is_int_type(int t) { return t == TCUDB_I32 || t == TCUDB_I64; }
+
+inline float decode_ord(long long o) {
+  int b = (int)o;
+  b = b >= 0 ? b : (b ^ 0x7fffffff);
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+
+// One dictionary (device state) for a domain.
+struct Dict {
+  int mode = 0;              // 0 direct, 1 hash
+  long long minv = 0;
+  unsigned long long span = 0;  // direct: range; hash: capacity
+  int32_t* code = nullptr;
+  unsigned long long* slots = nullptr;
+  uint8_t* fa = nullptr;
+  uint8_t* fb = nullptr;
+  long long* dict = nullptr;  // sorted values (group domains)
+  int64_t* count_dev = nullptr;
+  int64_t count = 0;
+  int bits = 64;              // significant bits of (x - min) for the radix sort
+  DictView view() const {
+    DictView v;
+    v.mode = mode;
+    v.minv = minv;
+    v.size = mode == 0 ? span : span - 1;
+    v.code = code;
+    v.slots = slots;
+    return v;
+  }
+};
+
+unsigned long long next_pow2(unsigned long long x) {
+  unsigned long long p = 1024;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Build phase 1 of a dictionary over one or two columns (marks + codes / compaction).
+// two_sided: K domain, code only keys present on both sides (∩). union_only: vertex domain.
+void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long long mn, long long mx, bool intersect,
+                unsigned long long* union_dev, int64_t* launches) {
+  cudaStream_t s = ar.s;
+  const int64_t n = c1.n + (c2 ? c2->n : 0);
+  const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
+  d.minv = mn;
+  d.count_dev = ar.get<int64_t>(1);
+  {
+    const unsigned long long sm1 = (unsigned long long)mx - (unsigned long long)mn;
+    int b = 8;
+    while (b < 64 && (sm1 >> b)) b += 8;
+    d.bits = b;
+  }
+  const unsigned __int128 direct_cap = (unsigned __int128)std::max<int64_t>(4 * n, 1 << 16);
+  if (span <= direct_cap && span < ((unsigned __int128)1 << 31)) {
+    d.mode = 0;
+    d.span = (unsigned long long)span;
+    d.fa = ar.zeros<uint8_t>((int64_t)d.span);
+    CK(launch_mark_direct(c1, mn, d.fa, s, launches));
+    if (c2) {
+      if (intersect) { d.fb = ar.zeros<uint8_t>((int64_t)d.span); CK(launch_mark_direct(*c2, mn, d.fb, s, launches)); }
+      else CK(launch_mark_direct(*c2, mn, d.fa, s, launches));
+    }
+    d.code = ar.get<int32_t>((int64_t)d.span);
+    void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)d.span));
+    CK(launch_pred_codes(d.fa, d.fb, (int64_t)d.span, d.code, d.count_dev, union_dev, tmp, s, launches));
+  } else {
+    if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
+    d.mode = 1;
+    const unsigned long long cap = next_pow2((unsigned long long)(2 * n));
+    d.span = cap;
+    d.slots = ar.get<unsigned long long>((int64_t)cap);
+    CK(cudaMemsetAsync(d.slots, 0xFF, cap * sizeof(unsigned long long), s));
+    d.fa = ar.zeros<uint8_t>((int64_t)cap);
+    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, s, launches));
+    if (c2) {
+      if (intersect) { d.fb = ar.zeros<uint8_t>((int64_t)cap); CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, s, launches)); }
+      else CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, s, launches));
+    }
+    d.code = ar.get<int32_t>((int64_t)cap);
+    void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)cap));
+    CK(launch_pred_codes(d.fa, d.fb, (int64_t)cap, d.code, d.count_dev, union_dev, tmp, s, launches));
+  }
+}
+
+// Phase 2 for group domains: sorted value dictionary (ascending ranks).
+void dict_finish_group(Arena& ar, Dict& d, int64_t* launches) {
+  cudaStream_t s = ar.s;
+  d.dict = ar.get<long long>(d.count);
+  if (d.count == 0) return;
+  if (d.mode == 0) {
+    CK(launch_direct_dict(d.code, (int64_t)d.span, d.minv, d.dict, s, launches));
+    return;
+  }
+  unsigned long long* k0 = ar.get<unsigned long long>(d.count);
+  unsigned long long* k1 = ar.get<unsigned long long>(d.count);
+  uint32_t* v0 = ar.get<uint32_t>(d.count);
+  uint32_t* v1 = ar.get<uint32_t>(d.count);
+  CK(launch_gather_slots(d.code, d.slots, (int64_t)d.span, k0, v0, s, launches));
+  const int bits = d.bits;
+  void* tmp = ar.get<char>((int64_t)radix_temp_bytes(d.count));
+  bool alt = false;
+  CK(radix_sort_pairs(k0, v0, k1, v1, d.count, bits, tmp, s, launches, &alt));
+  CK(launch_rank_write(alt ? k1 : k0, alt ? v1 : v0, d.count, d.minv, d.code, d.dict, s, launches));
+}
+
+struct Timer {
+  tcudb_ctx* ctx;
+  cudaStream_t s;
+  bool on;
+  int n = 0;
+  float* slots[8] = {};
+  Timer(tcudb_ctx* c, cudaStream_t st, bool enable) : ctx(c), s(st), on(enable) {}
+  void mark(float* out_ms) {
+    if (!on || n >= 8) return;
+    cudaEventRecord(ctx->ev[n], s);
+    slots[n] = out_ms;
+    ++n;
+  }
+  // elapsed between consecutive marks is written into the slot of the later mark
+  void finish() {
+    if (!on) return;
+    for (int i = 1; i < n; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]);
+      if (slots[i]) *slots[i] += ms;
+    }
+  }
+};
+
+template <typename T>
+T* to_pinned(tcudb_ctx* ctx, const void* dev, cudaStream_t s) {
+  Arena::ck(cudaMemcpyAsync(ctx->pinned, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+  Arena::ck(cudaStreamSynchronize(s));
+  return static_cast<T*>(ctx->pinned);
+}
+
+void* result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 8;
+  void* p = nullptr;
+  if (ctx->afn) {
+    p = ctx->afn(bytes, s, ctx->user);
+    if (!p) throw Fail{TCUDB_E_NOMEM};
+    std::lock_guard<std::mutex> g(ctx->mu);
+    ctx->dev_from_cb[p] = true;
+  } else {
+    const cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) { cudaGetLastError(); throw Fail{TCUDB_E_NOMEM}; }
+  }
+  return p;
+}
+
+void result_release(tcudb_ctx* ctx, void* p) {
+  if (!p) return;
+  bool cb = false;
+  {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    auto it = ctx->dev_from_cb.find(p);
+    if (it != ctx->dev_from_cb.end()) { cb = true; ctx->dev_from_cb.erase(it); }
+  }
+  if (cb) { if (ctx->ffn) ctx->ffn(p, nullptr, ctx->user); }
+  else cudaFree(p);
+}
+
+// --------------------------------------------------------------------------- the query
+struct QueryOut {
+  int64_t n = 0;
+  void *g = nullptr, *h = nullptr, *agg = nullptr;
+};
+
+tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B, const tcudb_query* q,
+                          tcudb_result* out, tcudb_stats* st, cudaStream_t s) {
+  const auto t_host0 = std::chrono::steady_clock::now();
+  int64_t* L = &ctx->launches;
+  const int64_t launches0 = ctx->launches;
+  tcudb_stats local{};
+  tcudb_stats& S = st ? *st : local;
+  std::memset(&S, 0, sizeof(S));
+  Timer tm(ctx, s, st != nullptr);
+  const bool is_sum = q->agg == TCUDB_SUM;
+  const int64_t nA = A->n_rows, nB = B->n_rows;
+  ColDesc ak{A->key.data, A->key.type, nA}, ag{A->group.data, A->group.type, nA};
+  ColDesc bk{B->key.data, B->key.type, nB}, bh{B->group.data, B->group.type, nB};
+  ColDesc av{is_sum ? A->value.data : nullptr, A->value.type, nA};
+  ColDesc bw{is_sum ? B->value.data : nullptr, B->value.type, nB};
+  const bool is_float = is_sum && ((av.data && av.type == TCUDB_F32) || (bw.data && bw.type == TCUDB_F32));
+  out->g_type = A->group.type;
+  out->h_type = B->group.type;
+  out->agg_type = is_float ? TCUDB_F64 : TCUDB_I64;
+  if (nA == 0 || nB == 0) return TCUDB_OK;
+
+  Arena ar(s);
+  tm.mark(nullptr);
+  // ---------------- a1: statistics
+  ColDesc cols[6] = {ak, bk, ag, bh, av, bw};
+  ColStats* dstats = ar.get<ColStats>(6);
+  CK(launch_col_stats(cols, dstats, s, L));
+  CK(cudaMemcpyAsync(ctx->pinned, dstats, sizeof(ColStats) * 6, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ColStats hs[6];
+  std::memcpy(hs, ctx->pinned, sizeof(hs));
+  tm.mark(&S.ms_stats);
+  // float values: reject non-finite
+  for (int c = 4; c < 6; ++c)
+    if (cols[c].data && cols[c].type == TCUDB_F32 && (hs[c].flags & 1)) throw Fail{TCUDB_E_UNSUPPORTED};
+
+  // ---------------- a2: dictionaries
+  const long long kmin = std::min(hs[0].mn, hs[1].mn), kmax = std::max(hs[0].mx, hs[1].mx);
+  unsigned long long* d_union = ar.zeros<unsigned long long>(1);
+  Dict DK, DG, DH;
+  dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L);
+  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L);
+  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L);
+  {
+    int64_t* hp = static_cast<int64_t*>(ctx->pinned);
+    CK(cudaMemcpyAsync(hp + 0, DK.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 1, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 2, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 3, d_union, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    DK.count = hp[0]; DG.count = hp[1]; DH.count = hp[2];
+    S.K_union = hp[3];
+  }
+  const int64_t K = DK.count, G = DG.count, H = DH.count;
+  S.K = K; S.G = G; S.H = H;
+  S.key_mode = DK.mode;
+  dict_finish_group(ar, DG, L);
+  dict_finish_group(ar, DH, L);
+  if (K == 0) { tm.mark(&S.ms_encode); tm.finish(); return TCUDB_OK; }
+
+  // probe
+  int32_t* kA = ar.get<int32_t>(nA);
+  int32_t* gA = ar.get<int32_t>(nA);
+  int32_t* kB = ar.get<int32_t>(nB);
+  int32_t* hB = ar.get<int32_t>(nB);
+  int32_t* cntA = ar.zeros<int32_t>(K);
+  int32_t* cntB = ar.zeros<int32_t>(K);
+  double* rowA = ar.zeros<double>(G);  // sum |v| per group (fp64 bound; non-negative, so its
+  double* rowB = ar.zeros<double>(H);  // bit pattern orders like an unsigned integer for the max)
+  CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, s, L));
+  CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, s, L));
+  unsigned long long* d_misc = ar.zeros<unsigned long long>(4);  // J, max rowabs A, max rowabs B
+  CK(launch_join_size(cntA, cntB, K, d_misc + 0, s, L));
+  CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), G, d_misc + 1, s, L));
+  CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), H, d_misc + 2, s, L));
+  CK(cudaMemcpyAsync(ctx->pinned, d_misc, 32, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  unsigned long long misc[4];
+  std::memcpy(misc, ctx->pinned, 32);
+  tm.mark(&S.ms_encode);
+  const unsigned long long J = misc[0];
+  S.join_pairs = (int64_t)J;
+  if (J == 0) { tm.finish(); return TCUDB_OK; }
+
+  // ---------------- a3 (integer bound) + a4 selector
+  auto col_absmax = [&](int c) -> long double {
+    if (!cols[c].data) return 1.0L;
+    if (cols[c].type == TCUDB_F32) {
+      return std::max(std::fabs((long double)decode_ord(hs[c].mn)), std::fabs((long double)decode_ord(hs[c].mx)));
+    }
+    return std::max(std::fabs((long double)hs[c].mn), std::fabs((long double)hs[c].mx));
+  };
+  if (is_sum && !is_float) {
+    // |C_gh| <= min(rowabsA(g) * rowabsB(h), J * max|v| * max|w|)
+    double ra, rb;
+    std::memcpy(&ra, &misc[1], 8);
+    std::memcpy(&rb, &misc[2], 8);
+    const long double b1 = (long double)ra * (long double)rb * (1.0L + 1e-9L);
+    const long double b2 = (long double)J * col_absmax(4) * col_absmax(5);
+    if (std::min(b1, b2) >= 9.2e18L) throw Fail{TCUDB_E_OVERFLOW};
+  }
+  // sign consistency: C != 0 <=> COUNT > 0 when every product v*w has one strict sign
+  auto strict_sign = [&](int c) -> bool {
+    if (!cols[c].data) return true;
+    if (cols[c].type == TCUDB_F32) {
+      const float mn = decode_ord(hs[c].mn), mx = decode_ord(hs[c].mx);
+      const float mabs = decode_ord(hs[c].min_abs);
+      return (mn > 0.f || mx < 0.f) && mabs >= 1e-15f;
+    }
+    return hs[c].mn > 0 || hs[c].mx < 0;
+  };
+  const bool need_exist = is_sum && !(strict_sign(4) && strict_sign(5));
+  S.existence = need_exist ? 1 : 0;
+
+  const int esz = is_float ? 2 : 1;
+  const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256);
+  // K padded to 128 elements: 128-byte K blocks for the u8 planes (value, digit and pattern
+  // planes) and 2 x 128-byte blocks for bf16.
+  const int64_t Kp = round_up(K, 128);
+  const double dense_ops = 2.0 * (double)Gp * (double)Hp * (double)Kp;
+  // the paper's input-matrix density: nnz(mat(A)) / (|A rows| x |dom(ID)|), ∪ domain
+  S.density_union = S.K_union ? (double)nA / ((double)G * (double)S.K_union) : 0.0;
+  const double R_tc = is_float ? 1.0e15 : 2.0e15, BW = 5.5e12, R_sp = 1.2e10;
+  double planes_est = is_sum ? (is_float ? 1.0 : 2.0) : 1.0;
+  if (need_exist) planes_est += 1.0;
+  const double t_dense = planes_est * dense_ops / R_tc + ((double)(Gp + Hp) * Kp * esz * 3 + (double)Gp * Hp * 8) / BW;
+  const double csz = is_sum ? 8.0 : 4.0;
+  const double t_sparse = (double)J / R_sp + ((double)G * H * csz * 2 + (double)(nA + nB) * 24) / BW;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 3 : (is_sum ? 8 : 1)) +
+                             (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
+  const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
+  bool dense;
+  if (q->flags & TCUDB_FORCE_DENSE) dense = true;
+  else if (q->flags & TCUDB_FORCE_SPARSE) dense = false;
+  else {
+    dense = t_dense <= t_sparse;  // ties -> dense
+    if (dense && dense_bytes > 0.85 * free_b) dense = false;
+    if (!dense && sparse_bytes > 0.85 * free_b && dense_bytes <= 0.85 * free_b) dense = true;
+  }
+  S.path = dense ? 0 : 1;
+  S.elem = is_float ? 1 : 0;
+  S.planes_a = S.planes_b = 1;
+  S.kchunks = 1;
+
+  // result matrices for compaction
+  CompactArgs ca{};
+  ca.G = G; ca.H = H;
+  ca.dict_g = DG.dict; ca.dict_h = DH.dict;
+  ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
+  ca.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
+  ca.agg_out = is_float ? 1 : 0;
+
+  if (dense) {
+    // ---------------- a5 fill
+    uint8_t *opA = nullptr, *opB = nullptr;        // value planes (int8) or bf16 operands
+    uint8_t *patA = nullptr, *patB = nullptr;      // existence pattern planes
+    int PA = 1, PB = 1, sA = 0, sB = 0;
+    unsigned long long maxA = 1, maxB = 1;          // max |digit-plane value| for the int32 chunk bound
+    FillStats* fs = ar.zeros<FillStats>(2);
+    int64_t ldop = Kp;                              // elements per operand row
+    int64_t k_len = Kp;
+    const int64_t cellsA = Gp * Kp, cellsB = Hp * Kp;
+    if (!is_sum && !(q->flags & TCUDB_FORCE_WIDE)) {
+      opA = ar.zeros<uint8_t>(cellsA);
+      opB = ar.zeros<uint8_t>(cellsB);
+      CK(launch_fill_count_u8(kA, gA, nA, opA, Kp, fs + 0, s, L));
+      CK(launch_fill_count_u8(kB, hB, nB, opB, Kp, fs + 1, s, L));
+      CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      FillStats hf[2];
+      std::memcpy(hf, ctx->pinned, sizeof(hf));
+      if (hf[0].overflow || hf[1].overflow) { opA = opB = nullptr; CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s)); }
+      else { maxA = hf[0].max_abs; maxB = hf[1].max_abs; }
+    }
+    if (!opA && !is_float) {
+      // wide integer path: int64 scratch -> stats -> digit planes (guard a3)
+      long long* scrA = ar.zeros<long long>(cellsA);
+      long long* scrB = ar.zeros<long long>(cellsB);
+      CK(launch_fill_i64(kA, gA, av, nA, scrA, Kp, s, L));
+      CK(launch_fill_i64(kB, hB, bw, nB, scrB, Kp, s, L));
+      CK(launch_scratch_stats_i64(scrA, cellsA, fs + 0, s, L));
+      CK(launch_scratch_stats_i64(scrB, cellsB, fs + 1, s, L));
+      CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      FillStats hf[2];
+      std::memcpy(hf, ctx->pinned, sizeof(hf));
+      auto planes_for = [](const FillStats& f, int& signed_top) {
+        signed_top = f.neg ? 1 : 0;
+        int p = 1;
+        if (f.neg) { while (p < 8 && f.max_abs > ((1ull << (8 * p - 1)) - 1)) ++p; }
+        else { while (p < 8 && f.max_abs > ((1ull << (8 * p)) - 1)) ++p; }
+        return p;
+      };
+      PA = planes_for(hf[0], sA);
+      PB = planes_for(hf[1], sB);
+      maxA = PA == 1 ? hf[0].max_abs : 255;
+      maxB = PB == 1 ? hf[1].max_abs : 255;
+      if (PA > 1 && sA) maxA = 255;
+      if (PB > 1 && sB) maxB = 255;
+      opA = ar.get<uint8_t>(cellsA * PA);
+      opB = ar.get<uint8_t>(cellsB * PB);
+      CK(launch_pack_planes(scrA, cellsA, PA, sA, opA, cellsA, s, L));
+      CK(launch_pack_planes(scrB, cellsB, PB, sB, opB, cellsB, s, L));
+      S.planes_a = PA; S.planes_b = PB;
+    }
+    if (is_float) {
+      ldop = 3 * Kp;
+      float* scrA = ar.zeros<float>(cellsA);
+      float* scrB = ar.zeros<float>(cellsB);
+      CK(launch_fill_f32(kA, gA, av, nA, scrA, Kp, s, L));
+      CK(launch_fill_f32(kB, hB, bw, nB, scrB, Kp, s, L));
+      uint16_t* fA = ar.get<uint16_t>(Gp * ldop);
+      uint16_t* fB = ar.get<uint16_t>(Hp * ldop);
+      CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 0, -1, fs + 0, s, L));
+      CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 0, -1, fs + 1, s, L));
+      CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      FillStats hf[2];
+      std::memcpy(hf, ctx->pinned, sizeof(hf));
+      if (hf[0].inexact || hf[1].inexact) {
+        // 3-product split along K: A' = [hi | hi | lo], B' = [hi | lo | hi]
+        CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 1, 2, fs + 0, s, L));
+        CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 2, 1, fs + 1, s, L));
+        k_len = 3 * Kp;
+        S.elem = 2;
+      }
+      opA = reinterpret_cast<uint8_t*>(fA);
+      opB = reinterpret_cast<uint8_t*>(fB);
+    }
+    if (need_exist) {
+      patA = ar.zeros<uint8_t>(cellsA);
+      patB = ar.zeros<uint8_t>(cellsB);
+      CK(launch_fill_pattern_u8(kA, gA, nA, patA, Kp, s, L));
+      CK(launch_fill_pattern_u8(kB, hB, nB, patB, Kp, s, L));
+    }
+    tm.mark(&S.ms_fill);
+
+    // ---------------- a6 GEMM(s)
+    GemmArgs ga{};
+    ga.M = Gp; ga.N = Hp;
+    double ops = 0;
+    if (is_float) {
+      float* C = ar.get<float>(Gp * Hp);
+      ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop;
+      ga.k_begin = 0; ga.k_len = k_len; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
+      CK(launch_gemm(ga, s, L));
+      ops += 2.0 * Gp * Hp * k_len;
+      ca.E = C; ca.e_kind = 2; ca.lde = Hp; ca.V = C; ca.v_kind = 2; ca.ldv = Hp;
+    } else {
+      const unsigned long long prod = maxA * maxB ? maxA * maxB : 1;
+      int64_t kc = (int64_t)((2147483647ull / prod) / 128 * 128);
+      if (kc < 128) kc = 128;
+      const bool single = PA == 1 && PB == 1 && kc >= Kp;
+      if (single) {
+        int32_t* C = ar.get<int32_t>(Gp * Hp);
+        ga.elem = ELEM_I8; ga.a_signed = sA; ga.b_signed = sB;
+        ga.A = opA; ga.lda = Kp; ga.B = opB; ga.ldb = Kp;
+        ga.k_begin = 0; ga.k_len = Kp; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
+        CK(launch_gemm(ga, s, L));
+        ops += dense_ops;
+        ca.E = C; ca.e_kind = 0; ca.lde = Hp; ca.V = C; ca.v_kind = 0; ca.ldv = Hp;
+      } else {
+        long long* C = ar.get<long long>(Gp * Hp);
+        bool first = true;
+        int chunks = 0;
+        for (int i = 0; i < PA; ++i)
+          for (int j = 0; j < PB; ++j)
+            for (int64_t k0 = 0; k0 < Kp; k0 += kc) {
+              ga.elem = ELEM_I8;
+              ga.a_signed = (i == PA - 1) && sA; ga.b_signed = (j == PB - 1) && sB;
+              ga.A = opA + (int64_t)i * cellsA; ga.lda = Kp;
+              ga.B = opB + (int64_t)j * cellsB; ga.ldb = Kp;
+              ga.k_begin = k0; ga.k_len = std::min<int64_t>(kc, Kp - k0);
+              ga.epi = first ? EPI_SET64 : EPI_ACC64; ga.C = C; ga.ldc = Hp; ga.shift = 8 * (i + j);
+              CK(launch_gemm(ga, s, L));
+              ops += 2.0 * Gp * Hp * ga.k_len;
+              first = false;
+              ++chunks;
+            }
+        S.kchunks = (int)((Kp + kc - 1) / kc);
+        ca.E = C; ca.e_kind = 1; ca.lde = Hp; ca.V = C; ca.v_kind = 1; ca.ldv = Hp;
+      }
+    }
+    if (need_exist) {
+      int32_t* E = ar.get<int32_t>(Gp * Hp);
+      GemmArgs ge{};
+      ge.M = Gp; ge.N = Hp; ge.elem = ELEM_I8; ge.A = patA; ge.lda = Kp; ge.B = patB; ge.ldb = Kp;
+      ge.k_begin = 0; ge.k_len = Kp; ge.epi = EPI_STORE32; ge.C = E; ge.ldc = Hp;
+      CK(launch_gemm(ge, s, L));
+      ops += dense_ops;
+      ca.E = E; ca.e_kind = 0; ca.lde = Hp;
+    }
+    S.gemm_ops = ops;
+    tm.mark(&S.ms_gemm);
+  } else {
+    // ---------------- a7 sparse expand
+    int64_t* bstart = ar.get<int64_t>(K + 1);
+    void* tmp = ar.get<char>((int64_t)scan_temp_bytes(std::max<int64_t>(std::max(K, nA), 1)));
+    CK(exclusive_scan_i32(cntB, bstart, K, bstart + K, tmp, s, L));
+    int32_t* cursor = ar.zeros<int32_t>(K);
+    int32_t* b_h = ar.get<int32_t>(nB);
+    int w_kind = 0;
+    void* b_w = nullptr;
+    if (is_sum && bw.data) {
+      w_kind = is_float ? 2 : 1;
+      b_w = is_float ? (void*)ar.get<float>(nB) : (void*)ar.get<long long>(nB);
+    }
+    CK(launch_bucket_fill(kB, hB, bw, nB, bstart, cursor, b_h, b_w, w_kind, s, L));
+    int32_t* work = ar.get<int32_t>(nA);
+    int32_t* flg = ar.get<int32_t>(nA);
+    int64_t* pos = ar.get<int64_t>(nA);
+    CK(launch_work(kA, nA, cntB, work, s, L));
+    CK(launch_flags_from_work(work, nA, flg, s, L));
+    CK(exclusive_scan_i32(flg, pos, nA, nullptr, tmp, s, L));
+    int32_t* act_a = ar.get<int32_t>(nA);
+    int32_t* act_w = ar.zeros<int32_t>(nA);
+    CK(launch_compact_active(work, pos, nA, act_a, act_w, s, L));
+    int64_t* act_off = ar.get<int64_t>(nA);
+    CK(exclusive_scan_i32(act_w, act_off, nA, nullptr, tmp, s, L));
+    const int64_t ldc = round_up(H, 4);
+    ExpandArgs ea{};
+    ea.n_act = nA; ea.J = (int64_t)J;
+    ea.act_a = act_a; ea.act_off = act_off; ea.kcodeA = kA; ea.gcodeA = gA; ea.va = av;
+    ea.bstart = bstart; ea.b_h = b_h; ea.b_w = b_w; ea.w_kind = w_kind; ea.ldc = ldc;
+    if (!is_sum) {
+      if (J < (1ull << 31)) { ea.acc_kind = 0; ea.C = ar.zeros<int32_t>(G * ldc); ca.e_kind = 0; }
+      else { ea.acc_kind = 1; ea.C = ar.zeros<long long>(G * ldc); ca.e_kind = 1; }
+      ca.E = ea.C; ca.V = ea.C; ca.v_kind = ca.e_kind;
+    } else {
+      ea.acc_kind = is_float ? 3 : 2;
+      ea.C = is_float ? (void*)ar.zeros<double>(G * ldc) : (void*)ar.zeros<long long>(G * ldc);
+      ca.E = ea.C; ca.e_kind = is_float ? 3 : 1; ca.V = ea.C; ca.v_kind = ca.e_kind;
+      if (need_exist) { ea.cnt = ar.zeros<int32_t>(G * ldc); ca.E = ea.cnt; ca.e_kind = 0; }
+    }
+    ca.lde = ldc; ca.ldv = ldc;
+    CK(launch_expand(ea, s, L));
+    tm.mark(&S.ms_sparse);
+  }
+
+  // ---------------- a8 compaction
+  void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, H));
+  int64_t* d_nnz = ar.get<int64_t>(1);
+  CK(launch_compact_count(ca, d_nnz, ctmp, s, L));
+  const int64_t nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+  const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
+  QueryOut r;
+  r.n = nnz;
+  try {
+    r.g = result_alloc(ctx, (size_t)nnz * gb, s);
+    r.h = result_alloc(ctx, (size_t)nnz * hb, s);
+    r.agg = result_alloc(ctx, (size_t)nnz * 8, s);
+    ca.out_g = r.g; ca.out_h = r.h; ca.out_agg = r.agg;
+    CK(launch_compact_write(ca, ctmp, s, L));
+  } catch (...) {
+    result_release(ctx, r.g); result_release(ctx, r.h); result_release(ctx, r.agg);
+    throw;
+  }
+  tm.mark(&S.ms_compact);
+  CK(cudaStreamSynchronize(s));
+  tm.finish();
+  out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->on_host = 0;
+  S.n_result = nnz;
+  S.n_launches = (int32_t)(ctx->launches - launches0);
+  S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+  return TCUDB_OK;
+}
+
+tcudb_status check_table(const tcudb_table* t, bool need_value_ok) {
+  if (!t || t->n_rows < 0) return TCUDB_E_INVALID;
+  if (t->n_rows > 0 && (!t->key.data || !t->group.data)) return TCUDB_E_INVALID;
+  if (!is_int_type(t->key.type) || !is_int_type(t->group.type)) return TCUDB_E_UNSUPPORTED;
+  if (t->n_rows >= (1ll << 31)) return TCUDB_E_UNSUPPORTED;
+  if (need_value_ok && t->value.data && !(is_int_type(t->value.type) || t->value.type == TCUDB_F32))
+    return TCUDB_E_UNSUPPORTED;
+  return TCUDB_OK;
+}
+
+tcudb_status set_err(tcudb_ctx* ctx, tcudb_status st, const char* msg) {
+  ctx->err = msg;
+  if (st == TCUDB_E_CUDA) {
+    const cudaError_t e = cudaGetLastError();
+    ctx->err += ": ";
+    ctx->err += cudaGetErrorString(e);
+    ctx->sticky = true;
+  }
+  return st;
+}
+
+tcudb_status fail_err(tcudb_ctx* ctx, const Fail& f) {
+  std::string m = f.st == TCUDB_E_OVERFLOW      ? "int64 overflow possible (precision guard)"
+                  : f.st == TCUDB_E_NOMEM       ? "out of device memory"
+                  : f.st == TCUDB_E_UNSUPPORTED ? "unsupported input (non-finite value or 2^64 key span)"
+                                                : "CUDA error";
+  if (f.what) { m += " in "; m += f.what; }
+  if (f.cuda != cudaSuccess) { m += ": "; m += cudaGetErrorString(f.cuda); }
+  ctx->err = m;
+  if (f.st == TCUDB_E_CUDA && f.cuda != cudaErrorInvalidValue) ctx->sticky = true;
+  return f.st;
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+extern "C" {
+
+tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_alloc_fn alloc_fn,
+                          tcudb_free_fn free_fn, void* user) {
+  (void)nccl_comm;
+  if (!out) return TCUDB_E_INVALID;
+  *out = nullptr;
+  int major = 0, minor = 0;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return TCUDB_E_CUDA; }
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (major != 10 || minor != 0) return TCUDB_E_CUDA;  // built for sm_100a only
+  tcudb_ctx* c = new tcudb_ctx();
+  c->device = device;
+  c->afn = alloc_fn;
+  c->ffn = free_fn;
+  c->user = user;
+  if (cudaDeviceGetDefaultMemPool(&c->pool, device) != cudaSuccess) { delete c; return TCUDB_E_CUDA; }
+  unsigned long long thr = ~0ull;
+  cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  if (cudaMallocHost(&c->pinned, kPinnedBytes) != cudaSuccess) { delete c; return TCUDB_E_CUDA; }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  *out = c;
+  return TCUDB_OK;
+}
+
+tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B, const tcudb_query* q,
+                            tcudb_result* out, tcudb_stats* stats, void* stream) {
+  if (!ctx || !out) return TCUDB_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  if (ctx->sticky) return set_err(ctx, TCUDB_E_CUDA, "context has a sticky CUDA error");
+  if (!q || (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM)) return set_err(ctx, TCUDB_E_INVALID, "bad query");
+  if ((q->flags & TCUDB_FORCE_DENSE) && (q->flags & TCUDB_FORCE_SPARSE))
+    return set_err(ctx, TCUDB_E_INVALID, "FORCE_DENSE and FORCE_SPARSE are exclusive");
+  tcudb_status v = check_table(A, q->agg == TCUDB_SUM);
+  if (v == TCUDB_OK) v = check_table(B, q->agg == TCUDB_SUM);
+  if (v != TCUDB_OK) return set_err(ctx, v, "bad table arguments");
+  if (q->agg == TCUDB_SUM && A->value.data && B->value.data &&
+      ((A->value.type == TCUDB_F32) != (B->value.type == TCUDB_F32)))
+    return set_err(ctx, TCUDB_E_UNSUPPORTED, "mixed integer / float value columns");
+  cudaSetDevice(ctx->device);
+  try {
+    return run_join_agg(ctx, A, B, q, out, stats, static_cast<cudaStream_t>(stream));
+  } catch (const Fail& f) {
+    std::memset(out, 0, sizeof(*out));
+    return fail_err(ctx, f);
+  }
+}
+
+tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B, const tcudb_query* q,
+                                 tcudb_result* out, tcudb_stats* stats, void* stream) {
+  if (!ctx || !out || !A || !B || !q) return TCUDB_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaSetDevice(ctx->device);
+  std::vector<void*> dev;
+  auto up = [&](const tcudb_col& c, int64_t n, tcudb_col& d) -> bool {
+    d = c;
+    if (!c.data || n == 0) return true;
+    const size_t bytes = (size_t)n * ((c.type == TCUDB_I64 || c.type == TCUDB_F64) ? 8 : 4);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) { cudaGetLastError(); return false; }
+    dev.push_back(p);
+    if (cudaMemcpyAsync(p, c.data, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return false;
+    d.data = p;
+    return true;
+  };
+  tcudb_table dA = *A, dB = *B;
+  bool ok = up(A->key, A->n_rows, dA.key) && up(A->group, A->n_rows, dA.group) &&
+            up(A->value, A->n_rows, dA.value) && up(B->key, B->n_rows, dB.key) &&
+            up(B->group, B->n_rows, dB.group) && up(B->value, B->n_rows, dB.value);
+  tcudb_status st = ok ? TCUDB_OK : TCUDB_E_NOMEM;
+  tcudb_result dr{};
+  if (st == TCUDB_OK) st = tcudb_join_agg(ctx, &dA, &dB, q, &dr, stats, stream);
+  for (void* p : dev) cudaFreeAsync(p, s);
+  if (st != TCUDB_OK) return st;
+  // results -> pinned host blocks (cached across calls)
+  auto host_block = [&](size_t bytes) -> void* {
+    if (bytes == 0) bytes = 8;
+    std::lock_guard<std::mutex> g(ctx->mu);
+    auto it = ctx->host_free.lower_bound(bytes);
+    if (it != ctx->host_free.end() && it->first <= bytes * 2) {
+      void* p = it->second;
+      ctx->host_free.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    ctx->host_size[p] = bytes;
+    return p;
+  };
+  const size_t gb = dr.g_type == TCUDB_I64 ? 8 : 4, hb = dr.h_type == TCUDB_I64 ? 8 : 4;
+  out->n = dr.n; out->g_type = dr.g_type; out->h_type = dr.h_type; out->agg_type = dr.agg_type; out->on_host = 1;
+  out->g = host_block(dr.n * gb);
+  out->h = host_block(dr.n * hb);
+  out->agg = host_block(dr.n * 8);
+  if (!out->g || !out->h || !out->agg) { tcudb_result_free(ctx, &dr); tcudb_result_free_host(ctx, out); return TCUDB_E_NOMEM; }
+  if (dr.n) {
+    cudaMemcpyAsync(out->g, dr.g, dr.n * gb, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(out->h, dr.h, dr.n * hb, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(out->agg, dr.agg, dr.n * 8, cudaMemcpyDeviceToHost, s);
+  }
+  const cudaError_t e = cudaStreamSynchronize(s);
+  tcudb_result_free(ctx, &dr);
+  if (e != cudaSuccess) return set_err(ctx, TCUDB_E_CUDA, "D2H copy failed");
+  return TCUDB_OK;
+}
+
+tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* src, const void* dst,
+                                  int32_t id_type, int64_t* triangles_out, tcudb_stats* stats, void* stream) {
+  if (!ctx || !triangles_out || n_edges < 0 || (n_edges > 0 && (!src || !dst)) || !is_int_type(id_type))
+    return TCUDB_E_INVALID;
+  if (ctx->sticky) return set_err(ctx, TCUDB_E_CUDA, "context has a sticky CUDA error");
+  *triangles_out = 0;
+  if (n_edges == 0) return TCUDB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  tcudb_stats local{};
+  tcudb_stats& S = stats ? *stats : local;
+  std::memset(&S, 0, sizeof(S));
+  const int64_t launches0 = ctx->launches;
+  int64_t* L = &ctx->launches;
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    Arena ar(s);
+    ColDesc cs{src, id_type, n_edges}, cd{dst, id_type, n_edges}, none{nullptr, 0, 0};
+    ColDesc cols[6] = {cs, cd, none, none, none, none};
+    ColStats* dst_ = ar.get<ColStats>(6);
+    CK(launch_col_stats(cols, dst_, s, L));
+    CK(cudaMemcpyAsync(ctx->pinned, dst_, sizeof(ColStats) * 6, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ColStats hs[6];
+    std::memcpy(hs, ctx->pinned, sizeof(hs));
+    Dict DV;
+    dict_build(ar, DV, cs, &cd, std::min(hs[0].mn, hs[1].mn), std::max(hs[0].mx, hs[1].mx), false, nullptr, L);
+    const int64_t V = *to_pinned<int64_t>(ctx, DV.count_dev, s);
+    S.G = S.H = S.K = V;
+    int32_t* cu = ar.get<int32_t>(n_edges);
+    int32_t* cv = ar.get<int32_t>(n_edges);
+    int32_t* dummy = ar.zeros<int32_t>(V);
+    CK(launch_probe(cs, cd, none, DV.view(), DV.view(), cu, cv, dummy, nullptr, s, L));
+    const int64_t Vp = round_up(V, 256), Kp = round_up(V, 128);
+    uint8_t* adj = ar.zeros<uint8_t>(Vp * Kp);
+    CK(launch_fill_sym_pattern(cu, cv, n_edges, adj, Kp, s, L));
+    unsigned long long* tri = ar.zeros<unsigned long long>(1);
+    GemmArgs ga{};
+    ga.elem = ELEM_I8; ga.M = Vp; ga.N = Vp; ga.A = adj; ga.lda = Kp; ga.B = adj; ga.ldb = Kp;
+    ga.k_begin = 0; ga.k_len = Kp; ga.epi = EPI_TRI; ga.mask = adj; ga.ldm = Kp; ga.mask_rows = Vp;
+    ga.mask_cols = Kp; ga.tri_out = tri;
+    CK(launch_gemm(ga, s, L));
+    S.gemm_ops = 2.0 * Vp * Vp * Kp;
+    const unsigned long long t = *to_pinned<unsigned long long>(ctx, tri, s);
+    *triangles_out = (int64_t)(t / 6);
+    S.path = 0;
+    S.n_launches = (int32_t)(ctx->launches - launches0);
+    S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return TCUDB_OK;
+  } catch (const Fail& f) {
+    return fail_err(ctx, f);
+  }
+}
+
+tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t b_signed, int64_t M, int64_t N,
+                        int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                        void* stream) {
+  if (!ctx || !A || !B || !C || (elem != 0 && elem != 1)) return TCUDB_E_INVALID;
+  cudaSetDevice(ctx->device);
+  GemmArgs ga{};
+  ga.elem = elem; ga.a_signed = a_signed; ga.b_signed = b_signed; ga.M = M; ga.N = N; ga.k_begin = 0; ga.k_len = K;
+  ga.A = A; ga.lda = lda; ga.B = B; ga.ldb = ldb; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = ldc;
+  const cudaError_t e = launch_gemm(ga, static_cast<cudaStream_t>(stream), &ctx->launches);
+  if (e == cudaErrorInvalidValue) { cudaGetLastError(); return set_err(ctx, TCUDB_E_INVALID, "gemm shape/alignment"); }
+  if (e != cudaSuccess) return set_err(ctx, TCUDB_E_CUDA, "gemm launch");
+  return TCUDB_OK;
+}
+
+void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r) {
+  if (!ctx || !r) return;
+  if (r->on_host) { tcudb_result_free_host(ctx, r); return; }
+  result_release(ctx, r->g);
+  result_release(ctx, r->h);
+  result_release(ctx, r->agg);
+  std::memset(r, 0, sizeof(*r));
+}
+
+void tcudb_result_free_host(tcudb_ctx* ctx, tcudb_result* r) {
+  if (!ctx || !r) return;
+  std::lock_guard<std::mutex> g(ctx->mu);
+  for (void* p : {r->g, r->h, r->agg}) {
+    if (!p) continue;
+    auto it = ctx->host_size.find(p);
+    if (it != ctx->host_size.end()) ctx->host_free.emplace(it->second, p);
+  }
+  std::memset(r, 0, sizeof(*r));
+}
+
+const char* tcudb_last_error(const tcudb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t tcudb_launch_count(const tcudb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void tcudb_destroy(tcudb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : ctx->host_size) cudaFreeHost(kv.first);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Integer results (COUNT, integer SUM) must be bit-exact; float SUM within the
+floored 1e-3 relative tolerance of DESIGN.md R9. Every test calls
+libtcudb.so through paper_2112_07552_b200.Engine (ctypes -> C ABI).
+"""
+import numpy as np
+import pytest
+
+import datagen
+from parity_util import compare, res_np, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def engine(torch_mod):
+    from paper_2112_07552_b200 import Engine
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+def run(engine, torch_mod, A, B, agg, flags=0):
+    out, st = engine.join_agg(to_dev(A, torch_mod), to_dev(B, torch_mod), agg, flags=flags, with_stats=True)
+    return res_np(out), st
+
+
+# ---------------------------------------------------------------- a6: the GEMM alone
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 512, 384), (512, 768, 1024), (1152, 256, 2048)])
+@pytest.mark.parametrize("sa,sb", [(0, 0), (1, 1), (0, 1), (1, 0)])
+def test_gemm_int8_exact(engine, torch_mod, M, N, K, sa, sb):
+    torch = torch_mod
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + 3 * sa + sb)
+    def mk(r, signed):
+        x = torch.randint(-128 if signed else 0, 128 if signed else 256, (r, K), generator=g, device="cuda",
+                          dtype=torch.int32)
+        return x.to(torch.int8) if signed else x.to(torch.uint8)
+    A, B = mk(M, sa), mk(N, sb)
+    C = engine.gemm(A, B, a_signed=sa, b_signed=sb)
+    ref = (A.to(torch.float64) @ B.to(torch.float64).T)
+    assert torch.equal(C.to(torch.float64), ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (384, 512, 1024)])
+def test_gemm_bf16(engine, torch_mod, M, N, K):
+    torch = torch_mod
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, generator=g, device="cuda").to(torch.bfloat16)
+    C = engine.gemm(A, B)
+    ref = A.to(torch.float64) @ B.to(torch.float64).T
+    scale = (A.abs().to(torch.float64) @ B.abs().to(torch.float64).T)
+    assert torch.all((C.to(torch.float64) - ref).abs() <= 1e-5 * scale + 1e-6)
+
+
+# ---------------------------------------------------------------- random tiny instances
+@pytest.mark.parametrize("vkind", ["none", "int", "float"])
+@pytest.mark.parametrize("flags", [0, 1, 2])  # auto, FORCE_DENSE, FORCE_SPARSE
+def test_random_tiny_vs_oracle(engine, torch_mod, oracle_mod, vkind, flags):
+    rng = np.random.default_rng(100 + flags)
+    agg = "count" if vkind == "none" else "sum"
+    for _ in range(60):
+        A, B = datagen.random_tiny(rng, n_max=80, vkind=vkind, vmin=-20, vmax=20, allow_empty=True)
+        ref = oracle_mod.join_agg(A, B, agg)
+        out, _ = run(engine, torch_mod, A, B, agg, flags)
+        compare(out, ref, agg, float_vals=(vkind == "float"))
+
+
+def test_wide_count_path_matches(engine, torch_mod, oracle_mod):
+    """FORCE_WIDE: int64 scratch + digit-plane guard path for COUNT, and cells > 255
+    (a carry out of the packed u8 byte) — both exact."""
+    rng = np.random.default_rng(5)
+    A = datagen.Table(rng.integers(0, 3, 5000).astype(np.int32), rng.integers(0, 2, 5000).astype(np.int32))
+    B = datagen.Table(rng.integers(0, 3, 4000).astype(np.int32), rng.integers(0, 3, 4000).astype(np.int32))
+    ref = oracle_mod.join_agg(A, B, "count")
+    for flags in (1, 1 | 16):
+        out, st = run(engine, torch_mod, A, B, "count", flags)
+        compare(out, ref, "count")
+        assert st["path"] == 0
+
+
+def test_int_sum_digit_planes(engine, torch_mod, oracle_mod):
+    """Large integer values force multi-plane base-256 decompositions (s8 top digit)."""
+    rng = np.random.default_rng(6)
+    n = 3000
+    for lo, hi in ((-100, 100), (0, 5000), (-(2 ** 20), 2 ** 20), (-(2 ** 23), 2 ** 23)):
+        A = datagen.Table(rng.integers(0, 40, n), rng.integers(0, 30, n), rng.integers(lo, hi, n))
+        B = datagen.Table(rng.integers(0, 40, n), rng.integers(0, 20, n), rng.integers(lo, hi, n))
+        ref = oracle_mod.join_agg(A, B, "sum")
+        for flags in (1, 2):
+            out, st = run(engine, torch_mod, A, B, "sum", flags)
+            compare(out, ref, "sum")
+
+
+def test_overflow_reported(engine, torch_mod):
+    from paper_2112_07552_b200 import TcudbError
+    A = datagen.Table(np.zeros(4, np.int64), np.zeros(4, np.int64), np.full(4, 2 ** 62, np.int64))
+    B = datagen.Table(np.zeros(1, np.int64), np.zeros(1, np.int64), np.full(1, 2, np.int64))
+    with pytest.raises(TcudbError) as ei:
+        run(engine, torch_mod, A, B, "sum")
+    assert ei.value.status == -4
+
+
+def test_empty_and_disjoint(engine, torch_mod):
+    E = datagen.Table(np.zeros(0, np.int32), np.zeros(0, np.int32))
+    A = datagen.Table(np.array([1, 2], np.int32), np.array([0, 0], np.int32))
+    B = datagen.Table(np.array([3, 4], np.int32), np.array([0, 0], np.int32))
+    for X, Y in ((E, A), (A, E), (A, B)):
+        out, _ = run(engine, torch_mod, X, Y, "count")
+        assert len(out["g"]) == 0
+
+
+def test_int64_extreme_keys_hash_path(engine, torch_mod, oracle_mod):
+    rng = np.random.default_rng(8)
+    pool = np.array([-(2 ** 62), -5, 0, 7, 2 ** 62, 2 ** 61 + 3], dtype=np.int64)
+    A = datagen.Table(pool[rng.integers(0, 6, 500)], rng.integers(-(2 ** 40), 2 ** 40, 500) // 2 ** 30 * 2 ** 30)
+    B = datagen.Table(pool[rng.integers(0, 6, 400)], rng.integers(0, 7, 400).astype(np.int64) * (2 ** 50))
+    ref = oracle_mod.join_agg(A, B, "count")
+    for flags in (0, 1, 2):
+        out, st = run(engine, torch_mod, A, B, "count", flags)
+        compare(out, ref, "count")
+        assert st["key_mode"] == 1
+
+
+def test_zero_sum_groups_kept(engine, torch_mod, oracle_mod):
+    A = datagen.Table(np.array([1, 1, 2], np.int32), np.array([0, 0, 1], np.int32), np.array([3, -3, 0], np.int32))
+    B = datagen.Table(np.array([1, 2], np.int32), np.array([4, 4], np.int32), np.array([2, 5], np.int32))
+    ref = oracle_mod.join_agg(A, B, "sum")
+    for flags in (1, 2):
+        out, st = run(engine, torch_mod, A, B, "sum", flags)
+        compare(out, ref, "sum")
+        assert st["existence"] == 1
+
+
+# ---------------------------------------------------------------- configs (reduced + full)
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c1s", 1.0), ("c2", 0.1), ("c3", 1 / 16), ("c4", 1 / 1024),
+                                        ("c5", 1 / 256), ("c5s", 1 / 256)])
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_configs_small(engine, torch_mod, oracle_mod, name, scale, flags):
+    A, B, agg = datagen.make_config(name, scale)
+    ref = oracle_mod.join_agg(A, B, agg)
+    out, st = run(engine, torch_mod, A, B, agg, flags)
+    compare(out, ref, agg, float_vals=(name == "c4"))
+
+
+def test_dense_equals_sparse_bitwise(engine, torch_mod):
+    A, B, agg = datagen.make_config("c5s", 1 / 512)
+    d, _ = run(engine, torch_mod, A, B, agg, 1)
+    s, _ = run(engine, torch_mod, A, B, agg, 2)
+    for k in ("g", "h", "agg"):
+        assert np.array_equal(d[k], s[k])
+
+
+def test_triangles_textbook_and_random(engine, torch_mod, oracle_mod):
+    torch = torch_mod
+    import math
+    def tri(edges):
+        s, d = (np.array(x, dtype=np.int32) for x in zip(*edges))
+        return engine.triangle_count(torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
+    for n in (3, 5, 10, 40):
+        assert tri([(i, j) for i in range(n) for j in range(i + 1, n)]) == math.comb(n, 3)
+    for n in (4, 9):
+        rim = [(i, (i + 1) % n) for i in range(n)]
+        assert tri(rim) == 0
+        assert tri(rim + [(n, i) for i in range(n)]) == n
+    rng = np.random.default_rng(3)
+    s, d = rng.integers(0, 3000, 40000), rng.integers(0, 3000, 40000)
+    got = engine.triangle_count(torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
+    assert got == oracle_mod.triangles(s, d)
+
+
+def test_c3_triangles_reduced(engine, torch_mod, oracle_mod):
+    torch = torch_mod
+    s, d = datagen.c3_graph_edges(scale=12)
+    got = engine.triangle_count(torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
+    assert got == oracle_mod.triangles(s, d)
+
+
+# full-size configs in the launch configuration bench.py times (default flags)
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_configs_full_exact(engine, torch_mod, oracle_mod, name):
+    A, B, agg = datagen.make_config(name)
+    ref = oracle_mod.join_agg(A, B, agg)
+    out, st = run(engine, torch_mod, A, B, agg, 0)
+    compare(out, ref, agg)
+
+
+def test_c4_full_sampled_and_freivalds(engine, torch_mod, oracle_mod):
+    """c4 at full size: exact oracle on 64 sampled A rows + a Freivalds check
+    y = C x  vs  A_op (B_op^T x) in fp64 over the whole result."""
+    A, B, agg = datagen.make_config("c4")
+    out, st = run(engine, torch_mod, A, B, agg, 0)
+    n = 8192
+    assert len(out["g"]) == n * n
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(n, 64, replace=False))
+    sel = np.isin(A["g"], rows)
+    Asub = datagen.Table(A["k"][sel], A["g"][sel], A["v"][sel])
+    ref = oracle_mod.join_agg(Asub, B, "sum")
+    m = np.isin(out["g"], rows)
+    compare({k: v[m] for k, v in out.items()}, ref, "sum", float_vals=True)
+    # Freivalds: C is (i, j) -> value; compare C x with A (B^T x) computed from tuples
+    x = rng.standard_normal(n)
+    Cx = np.zeros(n)
+    np.add.at(Cx, out["g"].astype(np.int64), out["agg"] * x[out["h"].astype(np.int64)])
+    Btx = np.zeros(n)                       # (B^T x)[k] = sum_j B[k][j] x[j]
+    np.add.at(Btx, B["k"].astype(np.int64), B["v"].astype(np.float64) * x[B["g"].astype(np.int64)])
+    ABx = np.zeros(n)
+    np.add.at(ABx, A["g"].astype(np.int64), A["v"].astype(np.float64) * Btx[A["k"].astype(np.int64)])
+    assert np.allclose(Cx, ABx, rtol=1e-3, atol=1e-3 * np.abs(ABx).max())
