@@ -150,6 +150,24 @@ tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t 
                         int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                         void* stream);
 
+/* Multi-GPU row sharding helpers (output rows are sharded by A's
+ * group-key range; the exchange itself is NCCL through torch.distributed).
+ *
+ * tcudb_minmax: min / max of one device int column (I32 / I64) into host *mn, *mx
+ * (n == 0 leaves INT64_MAX / INT64_MIN). Blocks on one small device->host read.
+ *
+ * tcudb_partition: route the rows of a device table by its GROUP column into P
+ * destination ranges, dest(row) = #{ i < P-1 : bounds[i] <= group(row) } for the
+ * P-1 ascending host bounds (P <= 1024). The rows are written grouped by
+ * destination (destination 0 first; order inside a destination unspecified) into
+ * `out`, caller-allocated device columns of in->n_rows entries with the same
+ * types (out->value.data may be NULL iff in->value.data is NULL); counts[P] (host)
+ * receives the rows per destination. */
+tcudb_status tcudb_minmax(tcudb_ctx* ctx, const void* col, int32_t type, int64_t n, int64_t* mn, int64_t* mx,
+                          void* stream);
+tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_t* bounds, int32_t P,
+                             tcudb_table* out, int64_t* counts, void* stream);
+
 void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r);
 void tcudb_result_free_host(tcudb_ctx* ctx, tcudb_result* r);
 const char* tcudb_last_error(const tcudb_ctx* ctx);

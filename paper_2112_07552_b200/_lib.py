@@ -24,9 +24,9 @@ I32, I64, F32, F64 = 0, 1, 2, 3
 COUNT, SUM = 0, 1
 FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE = 1, 2, 4, 8, 16
 
-EXPORTS = ["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_triangle_count", "tcudb_gemm",
-           "tcudb_result_free", "tcudb_result_free_host", "tcudb_last_error", "tcudb_launch_count",
-           "tcudb_destroy"]
+EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_triangle_count", "tcudb_gemm",
+                  "tcudb_minmax", "tcudb_partition", "tcudb_result_free", "tcudb_result_free_host",
+                  "tcudb_last_error", "tcudb_launch_count", "tcudb_destroy"])
 
 
 class TcudbError(RuntimeError):
@@ -100,6 +100,12 @@ def load(build_if_missing: bool = True):
     lib.tcudb_gemm.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                                ctypes.c_int64, P, ctypes.c_int64, P, ctypes.c_int64, P, ctypes.c_int64, P]
     lib.tcudb_gemm.restype = ctypes.c_int
+    lib.tcudb_minmax.argtypes = [P, P, ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                 ctypes.POINTER(ctypes.c_int64), P]
+    lib.tcudb_minmax.restype = ctypes.c_int
+    lib.tcudb_partition.argtypes = [P, ctypes.POINTER(TableS), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
+                                    ctypes.POINTER(TableS), ctypes.POINTER(ctypes.c_int64), P]
+    lib.tcudb_partition.restype = ctypes.c_int
     lib.tcudb_result_free.argtypes = [P, ctypes.POINTER(Result)]
     lib.tcudb_result_free_host.argtypes = [P, ctypes.POINTER(Result)]
     lib.tcudb_last_error.argtypes = [P]
@@ -296,6 +302,31 @@ class Engine:
                                             self._stream(stream))
         self._check(st)
         return (int(out.value), stats.to_dict()) if with_stats else int(out.value)
+
+    def minmax(self, col, stream=None):
+        """(min, max) of a CUDA int32/int64 column (host ints)."""
+        mn, mx = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._lib.tcudb_minmax(self._ctx, col.data_ptr() if col.numel() else None, _dtype_code(col),
+                                           col.numel(), ctypes.byref(mn), ctypes.byref(mx), self._stream(stream)))
+        return int(mn.value), int(mx.value)
+
+    def partition(self, T, bounds, stream=None):
+        """Route a device table's rows into len(bounds)+1 group-key ranges.
+        Returns (table grouped by destination, list of rows per destination)."""
+        torch = self._torch
+        P = len(bounds) + 1
+        ts = self._table_dev(T)
+        out = {k: torch.empty_like(v) for k, v in T.items() if v is not None}
+        to = TableS()
+        to.n_rows = T["k"].numel()
+        to.key = Col(out["k"].data_ptr(), _dtype_code(out["k"]))
+        to.group = Col(out["g"].data_ptr(), _dtype_code(out["g"]))
+        to.value = Col(out["v"].data_ptr(), _dtype_code(out["v"])) if "v" in out else Col(None, 0)
+        b = (ctypes.c_int64 * max(1, P - 1))(*[int(x) for x in bounds])
+        counts = (ctypes.c_int64 * P)()
+        self._check(self._lib.tcudb_partition(self._ctx, ctypes.byref(ts), b, P, ctypes.byref(to), counts,
+                                              self._stream(stream)))
+        return out, [int(c) for c in counts]
 
     def gemm(self, A, B, a_signed=True, b_signed=True, stream=None):
         """C = A @ B.T on the tcgen05 kernel. A: [M,K], B: [N,K] int8/uint8 (-> int32) or bf16 (-> fp32)."""

@@ -115,6 +115,13 @@ struct ExpandArgs {
 };
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s, int64_t* launches);
 
+// ---------------------------------------------------------------- partition.cu (§8(e))
+cudaError_t launch_part_count(const ColDesc& grp, const long long* bounds, int P, unsigned long long* counts,
+                              cudaStream_t s, int64_t* launches);
+cudaError_t launch_part_scatter(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const long long* bounds,
+                                int P, unsigned long long* cursor, void* ok, void* og, void* ov, cudaStream_t s,
+                                int64_t* launches);
+
 // ---------------------------------------------------------------- compact.cu (a8)
 // Existence matrix E (int32 count or the value matrix) -> tuples (g, h, agg), row-major.
 struct CompactArgs {

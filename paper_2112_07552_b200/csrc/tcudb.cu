@@ -848,6 +848,69 @@ tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t 
   return TCUDB_OK;
 }
 
+tcudb_status tcudb_minmax(tcudb_ctx* ctx, const void* col, int32_t type, int64_t n, int64_t* mn, int64_t* mx,
+                          void* stream) {
+  if (!ctx || !mn || !mx || n < 0 || (n > 0 && !col) || !is_int_type(type)) return TCUDB_E_INVALID;
+  *mn = INT64_MAX;
+  *mx = INT64_MIN;
+  if (n == 0) return TCUDB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  try {
+    Arena ar(s);
+    ColDesc c{col, type, n}, none{nullptr, 0, 0};
+    ColDesc cols[6] = {c, none, none, none, none, none};
+    ColStats* d = ar.get<ColStats>(6);
+    CK(launch_col_stats(cols, d, s, &ctx->launches));
+    const ColStats h = *to_pinned<ColStats>(ctx, d, s);
+    *mn = h.mn;
+    *mx = h.mx;
+    return TCUDB_OK;
+  } catch (const Fail& f) {
+    return fail_err(ctx, f);
+  }
+}
+
+tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_t* bounds, int32_t P,
+                             tcudb_table* out, int64_t* counts, void* stream) {
+  if (!ctx || !in || !out || !counts || P < 1 || P > 1024 || (P > 1 && !bounds)) return TCUDB_E_INVALID;
+  if (check_table(in, true) != TCUDB_OK) return TCUDB_E_INVALID;
+  if (in->n_rows > 0 && (!out->key.data || !out->group.data || (in->value.data && !out->value.data)))
+    return TCUDB_E_INVALID;
+  for (int i = 0; i < P; ++i) counts[i] = 0;
+  if (in->n_rows == 0) return TCUDB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  try {
+    Arena ar(s);
+    const int64_t n = in->n_rows;
+    ColDesc k{in->key.data, in->key.type, n}, g{in->group.data, in->group.type, n};
+    ColDesc v{in->value.data, in->value.type, n};
+    long long* db = ar.get<long long>(P);
+    if (P > 1) CK(cudaMemcpyAsync(db, bounds, sizeof(long long) * (P - 1), cudaMemcpyHostToDevice, s));
+    unsigned long long* dc = ar.zeros<unsigned long long>(2 * P);
+    CK(launch_part_count(g, db, P, dc, s, &ctx->launches));
+    std::vector<unsigned long long> hc(P);
+    CK(cudaMemcpyAsync(hc.data(), dc, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> cur(P);
+    unsigned long long run = 0;
+    for (int i = 0; i < P; ++i) { cur[i] = run; run += hc[i]; counts[i] = (int64_t)hc[i]; }
+    CK(cudaMemcpyAsync(dc + P, cur.data(), sizeof(unsigned long long) * P, cudaMemcpyHostToDevice, s));
+    CK(launch_part_scatter(k, g, v, db, P, dc + P, const_cast<void*>(out->key.data),
+                           const_cast<void*>(out->group.data), const_cast<void*>(out->value.data), s,
+                           &ctx->launches));
+    CK(cudaStreamSynchronize(s));
+    out->n_rows = n;
+    out->key.type = in->key.type;
+    out->group.type = in->group.type;
+    out->value.type = in->value.type;
+    return TCUDB_OK;
+  } catch (const Fail& f) {
+    return fail_err(ctx, f);
+  }
+}
+
 void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r) {
   if (!ctx || !r) return;
   if (r->on_host) { tcudb_result_free_host(ctx, r); return; }

@@ -216,3 +216,46 @@ def test_c4_full_sampled_and_freivalds(engine, torch_mod, oracle_mod):
     ABx = np.zeros(n)
     np.add.at(ABx, A["g"].astype(np.int64), A["v"].astype(np.float64) * Btx[A["k"].astype(np.int64)])
     assert np.allclose(Cx, ABx, rtol=1e-3, atol=1e-3 * np.abs(ABx).max())
+
+
+# ---------------------------------------------------------------- multi-GPU building blocks (loopback)
+def test_minmax_and_partition(engine, torch_mod):
+    torch = torch_mod
+    rng = np.random.default_rng(4)
+    g = rng.integers(-1000, 5000, 100_000).astype(np.int64)
+    T = {"k": torch.from_numpy(rng.integers(0, 99, len(g)).astype(np.int32)).cuda(),
+         "g": torch.from_numpy(g).cuda(), "v": torch.from_numpy(rng.random(len(g)).astype(np.float32)).cuda()}
+    assert engine.minmax(T["g"]) == (int(g.min()), int(g.max()))
+    bounds = [0, 1000, 1001, 4000]
+    out, counts = engine.partition(T, bounds)
+    dest = np.searchsorted(np.array(bounds), g, side="right")
+    assert counts == np.bincount(dest, minlength=5).tolist()
+    og = out["g"].cpu().numpy()
+    off = np.concatenate([[0], np.cumsum(counts)])
+    for d in range(5):
+        seg = og[off[d]:off[d + 1]]
+        assert np.all(np.searchsorted(np.array(bounds), seg, side="right") == d)
+    # rows are permuted intact (multiset of (k, g, v) triples preserved)
+    trip = lambda T: np.sort(np.stack([T["k"].cpu().numpy().astype(np.float64), T["g"].cpu().numpy(),
+                                       T["v"].cpu().numpy().astype(np.float64)], 1), axis=0)
+    assert np.array_equal(trip(out), trip(T))
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_loopback_row_sharding(engine, torch_mod, P):
+    """the P-rank algorithm as P logical shards on one GPU (collectives
+    replaced by slicing): concatenated per-range results == the single query."""
+    from paper_2112_07552_b200.shard import range_bounds
+    torch = torch_mod
+    A, B, agg = datagen.make_config("c2", 0.2)
+    dA, dB = to_dev(A, torch), to_dev(B, torch)
+    full = res_np(engine.join_agg(dA, dB, agg))
+    mn, mx = engine.minmax(dA["g"])
+    Ap, counts = engine.partition(dA, range_bounds(mn, mx, P))
+    off = np.concatenate([[0], np.cumsum(counts)])
+    parts = []
+    for r in range(P):
+        Ar = {k: v[off[r]:off[r + 1]].contiguous() for k, v in Ap.items()}
+        parts.append(res_np(engine.join_agg(Ar, dB, agg)))
+    for k in ("g", "h", "agg"):
+        assert np.array_equal(np.concatenate([p[k] for p in parts]), full[k])
