@@ -157,6 +157,27 @@ class _Owner:
             pass
 
 
+class _HostOwner:
+    """Owns one host-side tcudb_result (pinned blocks of the context cache)."""
+
+    def __init__(self, engine, res):
+        self.engine, self.res = engine, res
+
+    def __del__(self):
+        try:
+            if self.engine._ctx:
+                self.engine._lib.tcudb_result_free_host(self.engine._ctx, ctypes.byref(self.res))
+        except Exception:
+            pass
+
+
+class _HostArray:
+    def __init__(self, owner, ptr, n, dt):
+        self._owner = owner
+        self.__array_interface__ = {"shape": (int(n),), "typestr": dt.str, "data": (int(ptr), False),
+                                    "version": 3}
+
+
 class _DevArray:
     def __init__(self, owner, ptr, n, code):
         self._owner = owner
@@ -277,18 +298,13 @@ class Engine:
         st = self._lib.tcudb_join_agg_host(self._ctx, ctypes.byref(ta), ctypes.byref(tb), ctypes.byref(q),
                                            ctypes.byref(res), ctypes.byref(stats), self._stream(stream))
         self._check(st)
-        try:
-            out = {}
-            for key, ptr, code in (("g", res.g, res.g_type), ("h", res.h, res.h_type),
-                                   ("agg", res.agg, res.agg_type)):
-                dt = np.dtype(_TYPESTR[code])
-                if res.n == 0:
-                    out[key] = np.zeros(0, dt)
-                else:
-                    buf = (ctypes.c_char * (res.n * dt.itemsize)).from_address(ptr)
-                    out[key] = np.frombuffer(buf, dtype=dt).copy()
-        finally:
-            self._lib.tcudb_result_free_host(self._ctx, ctypes.byref(res))
+        # zero-copy numpy views of the pinned result blocks; the blocks return to the
+        # context's pinned cache when the last view is garbage collected
+        owner = _HostOwner(self, res)
+        out = {}
+        for key, ptr, code in (("g", res.g, res.g_type), ("h", res.h, res.h_type), ("agg", res.agg, res.agg_type)):
+            dt = np.dtype(_TYPESTR[code])
+            out[key] = np.zeros(0, dt) if res.n == 0 else np.asarray(_HostArray(owner, ptr, res.n, dt))
         return (out, stats.to_dict()) if with_stats else out
 
     def triangle_count(self, src, dst, stream=None, with_stats=False):

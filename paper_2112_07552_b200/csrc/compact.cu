@@ -6,8 +6,13 @@
 // Existence is decided on a COUNT plane (or on C itself when the guard proved
 // that C != 0 <=> COUNT > 0; reading R3), so SUM = 0 groups are kept.
 //
-// Two passes over the G x H region (row-major tiles of 4096 columns per
-// 256-thread block, 16 consecutive cells per thread): count -> scan -> write.
+// Work unit: a segment = one row x 256 consecutive columns (the GEMM's N tile).
+//   count:  per-segment nonzero counts — produced by the GEMM epilogue for free
+//           on the dense path, or by k_seg_count (one warp per segment);
+//   scan:   exclusive prefix over G x nseg counts (row-major);
+//   write:  one warp per segment, 8 chunks of 32 columns; __ballot_sync +
+//           popc gives each nonzero its slot, so reads of C and dict_h and the
+//           writes of (g, h, agg) are all 32-wide contiguous (coalesced).
 // Codes are ascending dense ranks, so row-major order is (g, h) order and the
 // ORDER BY comes for free (§3.4). Decode: g = dict_g[i], h = dict_h[j].
 #include <cuda_runtime.h>
@@ -20,142 +25,113 @@ namespace tcudb {
 namespace {
 
 constexpr int T = 256;
-constexpr int PER = 16;
-constexpr int TW = T * PER;  // columns per block tile
+constexpr int WPB = T / 32;
 
-__device__ __forceinline__ void load16(const void* base, int kind, int64_t ld, int64_t row, int64_t col0,
-                                       int64_t H, double* out, bool* nz) {
-  // Reads 16 consecutive cells (col0 .. col0+15) of one row; cells >= H are zero.
-  const bool full = col0 + PER <= H;
-  if (kind == 0 || kind == 2) {
-    const uint32_t* p = static_cast<const uint32_t*>(base) + row * ld + col0;
-    uint32_t v[PER];
-    if (full) {
+__device__ __forceinline__ bool nz_at(const void* base, int kind, int64_t idx) {
+  switch (kind) {
+    case 0: return static_cast<const int*>(base)[idx] != 0;
+    case 1: return static_cast<const long long*>(base)[idx] != 0;
+    case 2: return static_cast<const float*>(base)[idx] != 0.f;
+    default: return static_cast<const double*>(base)[idx] != 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(T) k_seg_count(const CompactArgs a, int32_t* __restrict__ cnt) {
+  const int64_t nsegs = a.G * a.nseg;
+  const int lane = lane_id();
+  for (int64_t s = (int64_t)blockIdx.x * WPB + warp_id(); s < nsegs; s += (int64_t)gridDim.x * WPB) {
+    const int64_t row = s / a.nseg;
+    const int64_t col0 = (s - row * a.nseg) * 256;
+    int c = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 x = reinterpret_cast<const uint4*>(p)[q];
-        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t col = col0 + j * 32 + lane;
+      c += (col < a.H && nz_at(a.E, a.e_kind, row * a.lde + col)) ? 1 : 0;
+    }
+    c = warp_sum(c);
+    if (lane == 0) cnt[s] = c;
+  }
+}
+
+__global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int64_t* __restrict__ off) {
+  const int64_t nsegs = a.G * a.nseg;
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  for (int64_t s = (int64_t)blockIdx.x * WPB + warp_id(); s < nsegs; s += (int64_t)gridDim.x * WPB) {
+    const int64_t row = s / a.nseg;
+    const int64_t col0 = (s - row * a.nseg) * 256;
+    if (col0 >= a.H) continue;
+    int64_t base = off[s];
+    const long long gval = a.dict_g[row];
+#pragma unroll 2
+    for (int j = 0; j < 8; ++j) {
+      const int64_t col = col0 + j * 32 + lane;
+      const bool in = col < a.H;
+      const bool e = in && nz_at(a.E, a.e_kind, row * a.lde + col);
+      const uint32_t m = __ballot_sync(0xffffffffu, e);
+      if (e) {
+        const int64_t pos = base + __popc(m & lt);
+        const long long hval = a.dict_h[col];
+        if (a.g_out_type == 1) static_cast<long long*>(a.out_g)[pos] = gval;
+        else static_cast<int*>(a.out_g)[pos] = (int)gval;
+        if (a.h_out_type == 1) static_cast<long long*>(a.out_h)[pos] = hval;
+        else static_cast<int*>(a.out_h)[pos] = (int)hval;
+        const int64_t vi = row * a.ldv + col;
+        if (a.agg_out == 0) {
+          long long v;
+          switch (a.v_kind) {
+            case 0: v = static_cast<const int*>(a.V)[vi]; break;
+            case 1: v = static_cast<const long long*>(a.V)[vi]; break;
+            default: v = (long long)static_cast<const float*>(a.V)[vi];
+          }
+          static_cast<long long*>(a.out_agg)[pos] = v;
+        } else {
+          const double v = a.v_kind == 2 ? (double)static_cast<const float*>(a.V)[vi]
+                                         : static_cast<const double*>(a.V)[vi];
+          static_cast<double*>(a.out_agg)[pos] = v;
+        }
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < PER; ++j) v[j] = (col0 + j < H) ? p[j] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      if (kind == 0) { out[j] = (double)(int)v[j]; nz[j] = v[j] != 0u; }
-      else { const float f = __uint_as_float(v[j]); out[j] = (double)f; nz[j] = f != 0.f; }
-    }
-  } else {
-    const unsigned long long* p = static_cast<const unsigned long long*>(base) + row * ld + col0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const unsigned long long v = (col0 + j < H) ? p[j] : 0ull;
-      if (kind == 1) { out[j] = 0; nz[j] = v != 0ull; }
-      else { const double d = __longlong_as_double((long long)v); out[j] = d; nz[j] = d != 0.0; }
+      base += __popc(m);
     }
   }
 }
 
-__device__ __forceinline__ int exist16(const CompactArgs& a, int64_t row, int64_t col0, bool* nz) {
-  double tmp[PER];
-  load16(a.E, a.e_kind, a.lde, row, col0, a.H, tmp, nz);
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) c += nz[j];
-  return c;
-}
-
-__global__ void __launch_bounds__(T) k_compact_count(const CompactArgs a, int64_t tiles_per_row,
-                                                     int32_t* __restrict__ cnt) {
-  const int64_t b = blockIdx.x;
-  const int64_t row = b / tiles_per_row;
-  const int64_t col0 = (b - row * tiles_per_row) * TW + (int64_t)threadIdx.x * PER;
-  bool nz[PER];
-  int c = col0 < a.H ? exist16(a, row, col0, nz) : 0;
-  c = warp_sum(c);
-  __shared__ int s[T / 32];
-  if (lane_id() == 0) s[warp_id()] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < T / 32; ++w) t += s[w];
-    cnt[b] = t;
-  }
-}
-
-__global__ void __launch_bounds__(T) k_compact_write(const CompactArgs a, int64_t tiles_per_row,
-                                                     const int64_t* __restrict__ off) {
-  const int64_t b = blockIdx.x;
-  const int64_t row = b / tiles_per_row;
-  const int64_t col0 = (b - row * tiles_per_row) * TW + (int64_t)threadIdx.x * PER;
-  bool nz[PER];
-  int c = 0;
-  if (col0 < a.H) c = exist16(a, row, col0, nz);
-  else {
-#pragma unroll
-    for (int j = 0; j < PER; ++j) nz[j] = false;
-  }
-  int x = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane_id() >= o) x += y; }
-  __shared__ int wt[T / 32];
-  if (lane_id() == 31) wt[warp_id()] = x;
-  __syncthreads();
-  if (c == 0) return;
-  int wp = 0;
-  for (int w = 0; w < warp_id(); ++w) wp += wt[w];
-  int64_t pos = off[b] + wp + x - c;
-  double val[PER];
-  bool dummy[PER];
-  if (a.v_kind != 1) load16(a.V, a.v_kind, a.ldv, row, col0, a.H, val, dummy);
-  const long long gval = a.dict_g[row];
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    if (!nz[j]) continue;
-    const long long hval = a.dict_h[col0 + j];
-    if (a.g_out_type == 1) static_cast<long long*>(a.out_g)[pos] = gval;
-    else static_cast<int*>(a.out_g)[pos] = (int)gval;
-    if (a.h_out_type == 1) static_cast<long long*>(a.out_h)[pos] = hval;
-    else static_cast<int*>(a.out_h)[pos] = (int)hval;
-    if (a.agg_out == 0) {
-      long long v;
-      if (a.v_kind == 1) v = static_cast<const long long*>(a.V)[row * a.ldv + col0 + j];
-      else v = (long long)val[j];  // int32 / f32 paths are exact in double
-      static_cast<long long*>(a.out_agg)[pos] = v;
-    } else {
-      static_cast<double*>(a.out_agg)[pos] = val[j];
-    }
-    ++pos;
-  }
+inline int grid_for_segs(int64_t nsegs) {
+  int64_t g = (nsegs + WPB - 1) / WPB;
+  if (g < 1) g = 1;
+  if (g > kNumSMs * 32) g = kNumSMs * 32;
+  return (int)g;
 }
 
 }  // namespace
 
-size_t compact_temp_bytes(int64_t G, int64_t H) {
-  const int64_t tpr = (H + TW - 1) / TW;
-  const int64_t nb = G * tpr;
-  return ((size_t)nb * 4 + 15) / 16 * 16 + (size_t)nb * 8 + scan_temp_bytes(nb) + 64;
+size_t compact_temp_bytes(int64_t G, int64_t nseg) {
+  const int64_t n = G * nseg;
+  return ((size_t)n * 4 + 15) / 16 * 16 + (size_t)n * 8 + scan_temp_bytes(n) + 64;
 }
 
-cudaError_t launch_compact_count(const CompactArgs& a, int64_t* nnz_dev, void* temp, cudaStream_t s,
-                                 int64_t* launches) {
-  const int64_t tpr = (a.H + TW - 1) / TW;
-  const int64_t nb = a.G * tpr;
+// counts: if `precounted` != NULL the per-segment counts already exist (GEMM epilogue);
+// otherwise they are computed into the temp buffer.
+cudaError_t launch_compact_count(const CompactArgs& a, const int32_t* precounted, int64_t* nnz_dev, void* temp,
+                                 cudaStream_t s, int64_t* launches) {
+  const int64_t n = a.G * a.nseg;
   int32_t* cnt = static_cast<int32_t*>(temp);
-  int64_t* off = reinterpret_cast<int64_t*>(static_cast<char*>(temp) + ((size_t)nb * 4 + 15) / 16 * 16);
-  if (nb <= 0) return exclusive_scan_i32(nullptr, nullptr, 0, nnz_dev, off, s, launches);
-  if (nb > 0x7fffffffLL) return cudaErrorInvalidValue;
-  k_compact_count<<<(unsigned)nb, T, 0, s>>>(a, tpr, cnt);
-  if (launches) ++*launches;
-  return exclusive_scan_i32(cnt, off, nb, nnz_dev, off + nb, s, launches);
+  int64_t* off = reinterpret_cast<int64_t*>(static_cast<char*>(temp) + ((size_t)n * 4 + 15) / 16 * 16);
+  if (n <= 0) return exclusive_scan_i32(nullptr, nullptr, 0, nnz_dev, off, s, launches);
+  const int32_t* src = precounted;
+  if (!src) {
+    k_seg_count<<<grid_for_segs(n), T, 0, s>>>(a, cnt);
+    if (launches) ++*launches;
+    src = cnt;
+  }
+  return exclusive_scan_i32(src, off, n, nnz_dev, off + n, s, launches);
 }
 
 cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t s, int64_t* launches) {
-  const int64_t tpr = (a.H + TW - 1) / TW;
-  const int64_t nb = a.G * tpr;
-  if (nb <= 0) return cudaSuccess;
-  const int64_t* off = reinterpret_cast<const int64_t*>(static_cast<char*>(temp) + ((size_t)nb * 4 + 15) / 16 * 16);
-  k_compact_write<<<(unsigned)nb, T, 0, s>>>(a, tpr, off);
+  const int64_t n = a.G * a.nseg;
+  if (n <= 0) return cudaSuccess;
+  const int64_t* off = reinterpret_cast<const int64_t*>(static_cast<char*>(temp) + ((size_t)n * 4 + 15) / 16 * 16);
+  k_seg_write<<<grid_for_segs(n), T, 0, s>>>(a, off);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -43,6 +43,7 @@ struct KParams {
   void* C; int64_t ldc; int shift;
   const uint8_t* mask; int64_t ldm, mask_rows, mask_cols;
   unsigned long long* tri_out;
+  int32_t* cnt_out; int64_t ldcnt;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      int nzc = 0;  // nonzeros of this row inside the 256-column tile (compaction count, a8)
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -149,14 +151,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           int4* dst = reinterpret_cast<int4*>(reinterpret_cast<uint32_t*>(p.C) + row * p.ldc + col);
 #pragma unroll
           for (int i = 0; i < 8; ++i) dst[i] = make_int4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+          if (p.cnt_out) {
+            const uint32_t m = p.is_bf16 ? 0x7fffffffu : 0xffffffffu;  // fp32: +-0 are both zero
+#pragma unroll
+            for (int i = 0; i < 32; ++i) nzc += (r[i] & m) != 0u;
+          }
         } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
           long long* dst = reinterpret_cast<long long*>(p.C) + row * p.ldc + col;
           longlong2* d2 = reinterpret_cast<longlong2*>(dst);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            long long x0 = (long long)(int)r[2 * i] << p.shift, x1 = (long long)(int)r[2 * i + 1] << p.shift;
-            if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += o.x; x1 += o.y; }
-            d2[i] = make_longlong2(x0, x1);
+            // wrapping (mod 2^64) arithmetic: exact whenever the true sum fits int64 (guard a3)
+            unsigned long long x0 = (unsigned long long)(long long)(int)r[2 * i] << p.shift;
+            unsigned long long x1 = (unsigned long long)(long long)(int)r[2 * i + 1] << p.shift;
+            if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += (unsigned long long)o.x; x1 += (unsigned long long)o.y; }
+            d2[i] = make_longlong2((long long)x0, (long long)x1);
+            if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
           }
         } else {  // EPI_TRI
           if (row < p.mask_rows && col < p.mask_cols) {
@@ -171,6 +181,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (p.cnt_out) p.cnt_out[row * p.ldcnt + nb] = nzc;
       acc ^= 1; if (acc == 0) acc_phase ^= 1;
     }
     if (p.epi == EPI_TRI) {
@@ -257,6 +268,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   p.idesc = idesc;
   p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = a.shift;
   p.mask = a.mask; p.ldm = a.ldm; p.mask_rows = a.mask_rows; p.mask_cols = a.mask_cols; p.tri_out = a.tri_out;
+  p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   k_gemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);

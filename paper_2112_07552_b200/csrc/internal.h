@@ -30,6 +30,9 @@ struct GemmArgs {
   void* C = nullptr; int64_t ldc = 0; int shift = 0;
   const uint8_t* mask = nullptr; int64_t ldm = 0, mask_rows = 0, mask_cols = 0;
   unsigned long long* tri_out = nullptr;
+  // optional: per (row, 256-column N tile) count of nonzero results, cnt[row * ldcnt + n_tile]
+  // (feeds the compaction scan, a8; only on the launch that produces the final matrix)
+  int32_t* cnt_out = nullptr; int64_t ldcnt = 0;
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 

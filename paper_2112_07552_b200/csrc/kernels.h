@@ -126,6 +126,7 @@ cudaError_t launch_part_scatter(const ColDesc& key, const ColDesc& grp, const Co
 // Existence matrix E (int32 count or the value matrix) -> tuples (g, h, agg), row-major.
 struct CompactArgs {
   int64_t G, H;
+  int64_t nseg;                                  // 256-column segments per row (ceil(H/256) or Hp/256)
   const void* E; int e_kind; int64_t lde;       // e_kind: 0 int32, 1 int64, 2 f32, 3 f64
   const void* V; int v_kind; int64_t ldv;       // value matrix (agg), same kinds
   const long long* dict_g; const long long* dict_h;
@@ -133,9 +134,9 @@ struct CompactArgs {
   int agg_out;                                   // 0 int64, 1 f64
   void* out_g; void* out_h; void* out_agg;
 };
-size_t compact_temp_bytes(int64_t G, int64_t H);
-cudaError_t launch_compact_count(const CompactArgs& a, int64_t* nnz_dev, void* temp, cudaStream_t s,
-                                 int64_t* launches);
+size_t compact_temp_bytes(int64_t G, int64_t nseg);
+cudaError_t launch_compact_count(const CompactArgs& a, const int32_t* precounted, int64_t* nnz_dev, void* temp,
+                                 cudaStream_t s, int64_t* launches);
 cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t s, int64_t* launches);
 
 }  // namespace tcudb

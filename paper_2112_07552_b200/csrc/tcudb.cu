@@ -415,6 +415,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
 
   // result matrices for compaction
   CompactArgs ca{};
+  int32_t* seg_cnt = nullptr;  // per-segment counts from the GEMM epilogue (dense path)
   ca.G = G; ca.H = H;
   ca.dict_g = DG.dict; ca.dict_h = DH.dict;
   ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
@@ -510,10 +511,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     GemmArgs ga{};
     ga.M = Gp; ga.N = Hp;
     double ops = 0;
+    // the GEMM that produces the existence matrix also emits per-(row, 256-col) nonzero counts
+    ca.nseg = Hp / 256;
+    seg_cnt = ar.get<int32_t>(Gp * ca.nseg);
+    int32_t* value_cnt = need_exist ? nullptr : seg_cnt;
     if (is_float) {
       float* C = ar.get<float>(Gp * Hp);
       ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop;
       ga.k_begin = 0; ga.k_len = k_len; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
+      ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
       CK(launch_gemm(ga, s, L));
       ops += 2.0 * Gp * Hp * k_len;
       ca.E = C; ca.e_kind = 2; ca.lde = Hp; ca.V = C; ca.v_kind = 2; ca.ldv = Hp;
@@ -527,6 +533,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         ga.elem = ELEM_I8; ga.a_signed = sA; ga.b_signed = sB;
         ga.A = opA; ga.lda = Kp; ga.B = opB; ga.ldb = Kp;
         ga.k_begin = 0; ga.k_len = Kp; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
+        ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
         CK(launch_gemm(ga, s, L));
         ops += dense_ops;
         ca.E = C; ca.e_kind = 0; ca.lde = Hp; ca.V = C; ca.v_kind = 0; ca.ldv = Hp;
@@ -534,10 +541,13 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         long long* C = ar.get<long long>(Gp * Hp);
         bool first = true;
         int chunks = 0;
+        const int total = PA * PB * (int)((Kp + kc - 1) / kc);
         for (int i = 0; i < PA; ++i)
           for (int j = 0; j < PB; ++j)
             for (int64_t k0 = 0; k0 < Kp; k0 += kc) {
               ga.elem = ELEM_I8;
+              const bool last = chunks == total - 1;
+              ga.cnt_out = last ? value_cnt : nullptr; ga.ldcnt = ca.nseg;
               ga.a_signed = (i == PA - 1) && sA; ga.b_signed = (j == PB - 1) && sB;
               ga.A = opA + (int64_t)i * cellsA; ga.lda = Kp;
               ga.B = opB + (int64_t)j * cellsB; ga.ldb = Kp;
@@ -557,6 +567,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       GemmArgs ge{};
       ge.M = Gp; ge.N = Hp; ge.elem = ELEM_I8; ge.A = patA; ge.lda = Kp; ge.B = patB; ge.ldb = Kp;
       ge.k_begin = 0; ge.k_len = Kp; ge.epi = EPI_STORE32; ge.C = E; ge.ldc = Hp;
+      ge.cnt_out = seg_cnt; ge.ldcnt = ca.nseg;
       CK(launch_gemm(ge, s, L));
       ops += dense_ops;
       ca.E = E; ca.e_kind = 0; ca.lde = Hp;
@@ -604,14 +615,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       if (need_exist) { ea.cnt = ar.zeros<int32_t>(G * ldc); ca.E = ea.cnt; ca.e_kind = 0; }
     }
     ca.lde = ldc; ca.ldv = ldc;
+    ca.nseg = (H + 255) / 256;
     CK(launch_expand(ea, s, L));
     tm.mark(&S.ms_sparse);
   }
 
   // ---------------- a8 compaction
-  void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, H));
+  void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
   int64_t* d_nnz = ar.get<int64_t>(1);
-  CK(launch_compact_count(ca, d_nnz, ctmp, s, L));
+  CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
   const int64_t nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
   const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
   QueryOut r;
