@@ -53,47 +53,73 @@ __global__ void __launch_bounds__(T) k_seg_count(const CompactArgs a, int32_t* _
   }
 }
 
+template <int K>
+struct Cell;
+template <> struct Cell<0> { using T = int;       static __device__ bool nz(T x) { return x != 0; } };
+template <> struct Cell<1> { using T = long long; static __device__ bool nz(T x) { return x != 0; } };
+template <> struct Cell<2> { using T = float;     static __device__ bool nz(T x) { return x != 0.f; } };
+template <> struct Cell<3> { using T = double;    static __device__ bool nz(T x) { return x != 0.0; } };
+
+// One warp per 256-column segment: all 8 chunk loads are issued before the
+// ballots (8 loads in flight per lane); when V is E the value comes from the
+// same load. Output slots: base + popc(ballot & lanemask_lt) -> contiguous stores.
+template <int EK, int VK, bool SAME, int GT, int HT>
 __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int64_t* __restrict__ off) {
+  using ET = typename Cell<EK>::T;
+  using VT = typename Cell<VK>::T;
   const int64_t nsegs = a.G * a.nseg;
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt();
+  const ET* __restrict__ E = static_cast<const ET*>(a.E);
+  const VT* __restrict__ V = static_cast<const VT*>(a.V);
   for (int64_t s = (int64_t)blockIdx.x * WPB + warp_id(); s < nsegs; s += (int64_t)gridDim.x * WPB) {
     const int64_t row = s / a.nseg;
     const int64_t col0 = (s - row * a.nseg) * 256;
     if (col0 >= a.H) continue;
-    int64_t base = off[s];
-    const long long gval = a.dict_g[row];
-#pragma unroll 2
+    ET e[8];
+    VT v[8];
+#pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t col = col0 + j * 32 + lane;
-      const bool in = col < a.H;
-      const bool e = in && nz_at(a.E, a.e_kind, row * a.lde + col);
-      const uint32_t m = __ballot_sync(0xffffffffu, e);
-      if (e) {
+      e[j] = col < a.H ? __ldcs(E + row * a.lde + col) : ET(0);
+    }
+    if (!SAME) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t col = col0 + j * 32 + lane;
+        v[j] = (col < a.H && Cell<EK>::nz(e[j])) ? __ldcs(V + row * a.ldv + col) : VT(0);
+      }
+    }
+    int64_t base = off[s];
+    const long long gval = a.dict_g[row];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t col = col0 + j * 32 + lane;
+      const bool nz = Cell<EK>::nz(e[j]);
+      const uint32_t m = __ballot_sync(0xffffffffu, nz);
+      if (nz) {
         const int64_t pos = base + __popc(m & lt);
         const long long hval = a.dict_h[col];
-        if (a.g_out_type == 1) static_cast<long long*>(a.out_g)[pos] = gval;
+        if (GT == 1) static_cast<long long*>(a.out_g)[pos] = gval;
         else static_cast<int*>(a.out_g)[pos] = (int)gval;
-        if (a.h_out_type == 1) static_cast<long long*>(a.out_h)[pos] = hval;
+        if (HT == 1) static_cast<long long*>(a.out_h)[pos] = hval;
         else static_cast<int*>(a.out_h)[pos] = (int)hval;
-        const int64_t vi = row * a.ldv + col;
-        if (a.agg_out == 0) {
-          long long v;
-          switch (a.v_kind) {
-            case 0: v = static_cast<const int*>(a.V)[vi]; break;
-            case 1: v = static_cast<const long long*>(a.V)[vi]; break;
-            default: v = (long long)static_cast<const float*>(a.V)[vi];
-          }
-          static_cast<long long*>(a.out_agg)[pos] = v;
-        } else {
-          const double v = a.v_kind == 2 ? (double)static_cast<const float*>(a.V)[vi]
-                                         : static_cast<const double*>(a.V)[vi];
-          static_cast<double*>(a.out_agg)[pos] = v;
-        }
+        const VT x = SAME ? (VT)e[j] : v[j];
+        if (VK == 2 || VK == 3) static_cast<double*>(a.out_agg)[pos] = (double)x;
+        else static_cast<long long*>(a.out_agg)[pos] = (long long)x;
       }
       base += __popc(m);
     }
   }
+}
+
+template <int EK, int VK, bool SAME>
+void launch_write_t(const CompactArgs& a, const int64_t* off, int grid, cudaStream_t s) {
+  const int sel = a.g_out_type * 2 + a.h_out_type;
+  if (sel == 0) k_seg_write<EK, VK, SAME, 0, 0><<<grid, T, 0, s>>>(a, off);
+  else if (sel == 1) k_seg_write<EK, VK, SAME, 0, 1><<<grid, T, 0, s>>>(a, off);
+  else if (sel == 2) k_seg_write<EK, VK, SAME, 1, 0><<<grid, T, 0, s>>>(a, off);
+  else k_seg_write<EK, VK, SAME, 1, 1><<<grid, T, 0, s>>>(a, off);
 }
 
 inline int grid_for_segs(int64_t nsegs) {
@@ -131,7 +157,24 @@ cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t 
   const int64_t n = a.G * a.nseg;
   if (n <= 0) return cudaSuccess;
   const int64_t* off = reinterpret_cast<const int64_t*>(static_cast<char*>(temp) + ((size_t)n * 4 + 15) / 16 * 16);
-  k_seg_write<<<grid_for_segs(n), T, 0, s>>>(a, off);
+  const int grid = grid_for_segs(n);
+  const bool same = a.E == a.V && a.e_kind == a.v_kind && a.lde == a.ldv;
+  if (same) {
+    switch (a.e_kind) {
+      case 0: launch_write_t<0, 0, true>(a, off, grid, s); break;
+      case 1: launch_write_t<1, 1, true>(a, off, grid, s); break;
+      case 2: launch_write_t<2, 2, true>(a, off, grid, s); break;
+      default: launch_write_t<3, 3, true>(a, off, grid, s);
+    }
+  } else {
+    if (a.e_kind != 0) return cudaErrorInvalidValue;  // separate existence planes are int32 counts
+    switch (a.v_kind) {
+      case 0: launch_write_t<0, 0, false>(a, off, grid, s); break;
+      case 1: launch_write_t<0, 1, false>(a, off, grid, s); break;
+      case 2: launch_write_t<0, 2, false>(a, off, grid, s); break;
+      default: launch_write_t<0, 3, false>(a, off, grid, s);
+    }
+  }
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -91,6 +91,22 @@ __global__ void k_mark_direct(ColDesc c, long long minv, uint8_t* __restrict__ f
     flags[(unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv] = 1;
 }
 
+// Small spans with many tuples per value (e.g. c4: 67 M tuples over 8,192 keys):
+// mark a block-private copy of the flags in shared memory, then write each
+// block's set flags once — global stores drop from n to (#blocks x span).
+__global__ void __launch_bounds__(1024) k_mark_direct_smem(ColDesc c, long long minv, uint8_t* __restrict__ flags,
+                                                          int span) {
+  extern __shared__ uint8_t s_flag[];
+  for (int i = threadIdx.x; i < span; i += blockDim.x) s_flag[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += stride)
+    s_flag[(unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv] = 1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < span; i += blockDim.x)
+    if (s_flag[i]) flags[i] = 1;
+}
+
 // ------------------------------------------------------------------ hash dictionary
 // Slot key = (x - min) as u64; EMPTY = ~0. Linear probing; equal keys in a warp
 // are inserted once (warp aggregation). flags[slot] = 1 marks the side.
@@ -216,6 +232,27 @@ TCUDB_DEV int32_t dict_lookup(const DictView& d, long long x) {
 
 // kcode / gcode per tuple; per-key counts (warp-aggregated); per-group tuple
 // counts and sum |v| of tuples whose key survives the ∩ (guard bounds, a3).
+// Variant with the per-key counters privatized in shared memory (small key
+// domains with many tuples per key, e.g. c4: 8,192 keys x 8,192 tuples each):
+// smem atomics, then one global atomic per key per block.
+__global__ void __launch_bounds__(1024) k_probe_smem(ColDesc key, ColDesc grp, DictView kd, DictView gd,
+                                                     int32_t* __restrict__ kcode, int32_t* __restrict__ gcode,
+                                                     int32_t* __restrict__ cnt_k, int K) {
+  extern __shared__ int32_t s_cnt[];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) s_cnt[k] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < key.n; i += stride) {
+    const int32_t kc = dict_lookup(kd, ld_int(key.data, key.type, i));
+    kcode[i] = kc;
+    gcode[i] = dict_lookup(gd, ld_int(grp.data, grp.type, i));
+    if (kc >= 0) atomicAdd(s_cnt + kc, 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    if (s_cnt[k]) atomicAdd(cnt_k + k, s_cnt[k]);
+}
+
 __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, DictView gd,
                         int32_t* __restrict__ kcode, int32_t* __restrict__ gcode, int32_t* __restrict__ cnt_k,
                         double* __restrict__ rowabs_g) {
@@ -285,8 +322,22 @@ cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, cudaStream_t s, int64_t* launches) {
+cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
+                               int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
+  if (span <= 64 * 1024 && c.n >= 64 * span) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_mark_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr = true;
+    }
+    int64_t blocks = c.n / (64 * span);  // >= 64 tuples per flag per block
+    if (blocks > kNumSMs) blocks = kNumSMs;
+    if (blocks < 1) blocks = 1;
+    k_mark_direct_smem<<<(int)blocks, 1024, (size_t)span, s>>>(c, minv, flags, (int)span);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   k_mark_direct<<<grid_for(c.n), T, 0, s>>>(c, minv, flags);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -345,8 +396,21 @@ cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* va
 
 cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
                          const DictView& gd, int32_t* kcode, int32_t* gcode, int32_t* cnt_k,
-                         double* rowabs_g, cudaStream_t s, int64_t* launches) {
+                         double* rowabs_g, int64_t K, cudaStream_t s, int64_t* launches) {
   if (key.n <= 0) return cudaSuccess;
+  // privatized counters when the key domain fits in shared memory and there are
+  // enough tuples per block to amortize the per-block flush
+  const int64_t smem = K * 4;
+  if (!rowabs_g && K > 0 && smem <= 200 * 1024 && key.n >= 32 * K * kNumSMs / 4) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_probe_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_probe_smem<<<kNumSMs, 1024, (size_t)smem, s>>>(key, grp, kd, gd, kcode, gcode, cnt_k, (int)K);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   k_probe<<<grid_for(key.n), T, 0, s>>>(key, grp, val, kd, gd, kcode, gcode, cnt_k, rowabs_g);
   if (launches) ++*launches;
   return cudaGetLastError();

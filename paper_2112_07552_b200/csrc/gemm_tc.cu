@@ -55,6 +55,50 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = r / gsz;
 }
 
+// Epilogue for one accumulator tile: this thread owns one row (its TMEM lane) and
+// the BN accumulator columns at taddr. Returns the row's nonzero count.
+__device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, int64_t row, int nb, long long& tri) {
+  int nzc = 0;  // nonzeros of this row inside the 256-column tile (compaction count, a8)
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + c * 32, r);
+    tmem_ld_wait();
+    const int64_t col = (int64_t)nb * BN + c * 32;
+    if (p.epi == EPI_STORE32) {
+      int4* dst = reinterpret_cast<int4*>(reinterpret_cast<uint32_t*>(p.C) + row * p.ldc + col);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = make_int4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+      if (p.cnt_out) {
+        const uint32_t m = p.is_bf16 ? 0x7fffffffu : 0xffffffffu;  // fp32: +-0 are both zero
+#pragma unroll
+        for (int i = 0; i < 32; ++i) nzc += (r[i] & m) != 0u;
+      }
+    } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
+      long long* dst = reinterpret_cast<long long*>(p.C) + row * p.ldc + col;
+      longlong2* d2 = reinterpret_cast<longlong2*>(dst);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        // wrapping (mod 2^64) arithmetic: exact whenever the true sum fits int64 (guard a3)
+        unsigned long long x0 = (unsigned long long)(long long)(int)r[2 * i] << p.shift;
+        unsigned long long x1 = (unsigned long long)(long long)(int)r[2 * i + 1] << p.shift;
+        if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += (unsigned long long)o.x; x1 += (unsigned long long)o.y; }
+        d2[i] = make_longlong2((long long)x0, (long long)x1);
+        if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
+      }
+    } else {  // EPI_TRI
+      if (row < p.mask_rows && col < p.mask_cols) {
+        const uint4* m4 = reinterpret_cast<const uint4*>(p.mask + row * p.ldm + col);
+        const uint4 ma = m4[0], mb4 = m4[1];
+        const uint32_t mw[8] = {ma.x, ma.y, ma.z, ma.w, mb4.x, mb4.y, mb4.z, mb4.w};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tri += (long long)(int)r[i] * (long long)((mw[i >> 2] >> (8 * (i & 3))) & 0xFF);
+      }
+    }
+  }
+  return nzc;
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -140,44 +184,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      int nzc = 0;  // nonzeros of this row inside the 256-column tile (compaction count, a8)
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c * 32, r);
-        tmem_ld_wait();
-        const int64_t col = (int64_t)nb * BN + c * 32;
-        if (p.epi == EPI_STORE32) {
-          int4* dst = reinterpret_cast<int4*>(reinterpret_cast<uint32_t*>(p.C) + row * p.ldc + col);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dst[i] = make_int4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-          if (p.cnt_out) {
-            const uint32_t m = p.is_bf16 ? 0x7fffffffu : 0xffffffffu;  // fp32: +-0 are both zero
-#pragma unroll
-            for (int i = 0; i < 32; ++i) nzc += (r[i] & m) != 0u;
-          }
-        } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
-          long long* dst = reinterpret_cast<long long*>(p.C) + row * p.ldc + col;
-          longlong2* d2 = reinterpret_cast<longlong2*>(dst);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            // wrapping (mod 2^64) arithmetic: exact whenever the true sum fits int64 (guard a3)
-            unsigned long long x0 = (unsigned long long)(long long)(int)r[2 * i] << p.shift;
-            unsigned long long x1 = (unsigned long long)(long long)(int)r[2 * i + 1] << p.shift;
-            if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += (unsigned long long)o.x; x1 += (unsigned long long)o.y; }
-            d2[i] = make_longlong2((long long)x0, (long long)x1);
-            if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
-          }
-        } else {  // EPI_TRI
-          if (row < p.mask_rows && col < p.mask_cols) {
-            const uint4* m4 = reinterpret_cast<const uint4*>(p.mask + row * p.ldm + col);
-            const uint4 ma = m4[0], mb4 = m4[1];
-            const uint32_t mw[8] = {ma.x, ma.y, ma.z, ma.w, mb4.x, mb4.y, mb4.z, mb4.w};
-#pragma unroll
-            for (int i = 0; i < 32; ++i) tri += (long long)(int)r[i] * (long long)((mw[i >> 2] >> (8 * (i & 3))) & 0xFF);
-          }
-        }
-      }
+      const int nzc = epilogue_rows(p, taddr, row, nb, tri);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -196,6 +203,134 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     __syncwarp();
     tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair kernel (cta_group::2)
+// Two CTAs of a cluster share one 256 x 256 accumulator tile: each holds 128 rows
+// of A and 128 rows (half of N) of B per stage; the leader's single thread issues
+// tcgen05.mma.cta_group::2 (M = 256) and its commits multicast to both CTAs'
+// barriers. Per SM this halves the B bytes staged per MMA compared with the
+// 1-CTA 128 x 256 tile (L2 -> SM traffic per MAC drops by 1/3).
+constexpr int STAGES2 = 6;
+constexpr int A2_BYTES = 128 * BKB;  // 16 KB (this CTA's 128 rows of A)
+constexpr int B2_BYTES = 128 * BKB;  // 16 KB (this CTA's half of the 256 N rows)
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr size_t SMEM2_BYTES = (size_t)STAGES2 * STAGE2_BYTES + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * A2_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* full = bars;                          // [STAGES2] (used in the leader)
+  uint64_t* empty = bars + STAGES2;               // [STAGES2] (each CTA)
+  uint64_t* tfull = bars + 2 * STAGES2;           // [2]       (each CTA)
+  uint64_t* tempty = bars + 2 * STAGES2 + 2;      // [2]       (used in the leader: 8 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+  const int num_tiles = p.tiles_m * p.tiles_n;  // pair tiles (256 x 256)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncwarp();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      const uint32_t leader_full = mapa_shared(smem_u32(full), 0);
+      int stage = 0; uint32_t phase = 0;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          // Only the leader arrives (expecting both CTAs' bytes); the peer's TMA bytes
+          // complete_tx on the leader's barrier. The peer cannot reach the next phase of
+          // this stage before the MMA consumed it (it waits on its own empty[stage]).
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+          const int kc = (p.kb_begin + kb) * p.elems_per_kb;
+          tma_load_2d_pair(&tmA, sA + stage * A2_BYTES, leader_full + 8 * stage, kc, mb * 256 + rank * 128, pol);
+          tma_load_2d_pair(&tmB, sB + stage * B2_BYTES, leader_full + 8 * stage, kc, nb * 256 + rank * 128, pol);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A2_BYTES));
+          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * B2_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t accum = (kb | kk) != 0;
+            if (p.is_bf16) mma_f16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
+            else mma_i8_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
+          }
+          mma_commit_pair(&empty[stage], 0x3);  // frees this stage in both CTAs
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc], 0x3);      // both CTAs' accumulator halves ready
+        acc ^= 1; if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
+    int acc = 0; uint32_t acc_phase = 0;
+    long long tri = 0;
+    for (int t = cid; t < num_tiles; t += ncl) {
+      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = (int64_t)mb * 256 + rank * 128 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      const int nzc = epilogue_rows(p, taddr, row, nb, tri);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_cluster(leader_tempty + 8 * acc);
+      }
+      if (p.cnt_out) p.cnt_out[row * p.ldcnt + nb] = nzc;
+      acc ^= 1; if (acc == 0) acc_phase ^= 1;
+    }
+    if (p.epi == EPI_TRI) {
+      tri = warp_sum(tri);
+      if (lane == 0 && tri != 0) atomicAdd(p.tri_out, (unsigned long long)tri);
+    }
+  }
+
+  tc_fence_before();
+  __syncwarp();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
   }
 }
 
@@ -244,15 +379,23 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  // Kernel choice: the 1-CTA 128x256 kernel is the default (measured faster on c2: 1.31 vs
+  // 1.40 ms; both MMA-bound at ~65-70 % tensor-pipe activity). TCUDB_GEMM_PAIR=1 selects the
+  // CTA-pair (cta_group::2) kernel when M splits into 256-row pair tiles.
+  static const bool want_pair = getenv("TCUDB_GEMM_PAIR") && getenv("TCUDB_GEMM_PAIR")[0] == '1';
+  const bool pair = want_pair && a.M % 256 == 0;
   const int64_t kcols = a.k_begin + a.k_len;
   CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, a.elem, a.M, kcols, a.lda, BM) || !make_map(&mB, a.B, a.elem, a.N, kcols, a.ldb, BN))
+  if (!make_map(&mA, a.A, a.elem, a.M, kcols, a.lda, pair ? 128 : BM) ||
+      !make_map(&mB, a.B, a.elem, a.N, kcols, a.ldb, pair ? 128 : BN))
     return cudaErrorInvalidValue;
   KParams p{};
   p.M = a.M; p.N = a.N;
-  p.tiles_m = (int)(a.M / BM); p.tiles_n = (int)(a.N / BN);
+  p.tiles_m = (int)(a.M / (pair ? 256 : BM)); p.tiles_n = (int)(a.N / BN);
   p.elems_per_kb = BKB / esz;
   p.num_kb = (int)(a.k_len / p.elems_per_kb);
   p.kb_begin = (int)(a.k_begin / p.elems_per_kb);
@@ -264,14 +407,19 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   if (p.is_bf16) idesc |= (1u << 4) | (1u << 7) | (1u << 10);
   else idesc |= (2u << 4) | ((uint32_t)(a.a_signed != 0) << 7) | ((uint32_t)(a.b_signed != 0) << 10);
   idesc |= (uint32_t)(BN >> 3) << 17;
-  idesc |= (uint32_t)(BM >> 4) << 24;
+  idesc |= (uint32_t)((pair ? 256 : BM) >> 4) << 24;
   p.idesc = idesc;
   p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = a.shift;
   p.mask = a.mask; p.ldm = a.ldm; p.mask_rows = a.mask_rows; p.mask_cols = a.mask_cols; p.tri_out = a.tri_out;
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   const int tiles = p.tiles_m * p.tiles_n;
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  k_gemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
+  if (pair) {
+    const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+    k_gemm_tc2<<<grid, NUM_THREADS, SMEM2_BYTES, s>>>(mA, mB, p);
+  } else {
+    const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+    k_gemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
+  }
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -36,7 +36,8 @@ struct DictView {
 
 // ---------------------------------------------------------------- encode.cu
 cudaError_t launch_col_stats(const ColDesc* cols6, ColStats* st, cudaStream_t s, int64_t* launches);
-cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, cudaStream_t s, int64_t* launches);
+cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
+                               int64_t* launches);
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
                                uint8_t* flags, cudaStream_t s, int64_t* launches);
 size_t pred_temp_bytes(int64_t n);
@@ -50,7 +51,7 @@ cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* va
                               int32_t* slot_code, long long* dict, cudaStream_t s, int64_t* launches);
 cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
                          const DictView& gd, int32_t* kcode, int32_t* gcode, int32_t* cnt_k,
-                         double* rowabs_g, cudaStream_t s, int64_t* launches);
+                         double* rowabs_g, int64_t K, cudaStream_t s, int64_t* launches);
 cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* J, cudaStream_t s,
                              int64_t* launches);
 cudaError_t launch_max_u64(const unsigned long long* x, int64_t n, unsigned long long* out, cudaStream_t s,

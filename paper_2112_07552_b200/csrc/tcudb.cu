@@ -155,10 +155,11 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.mode = 0;
     d.span = (unsigned long long)span;
     d.fa = ar.zeros<uint8_t>((int64_t)d.span);
-    CK(launch_mark_direct(c1, mn, d.fa, s, launches));
+    const int64_t sp = (int64_t)d.span;
+    CK(launch_mark_direct(c1, mn, d.fa, sp, s, launches));
     if (c2) {
-      if (intersect) { d.fb = ar.zeros<uint8_t>((int64_t)d.span); CK(launch_mark_direct(*c2, mn, d.fb, s, launches)); }
-      else CK(launch_mark_direct(*c2, mn, d.fa, s, launches));
+      if (intersect) { d.fb = ar.zeros<uint8_t>(sp); CK(launch_mark_direct(*c2, mn, d.fb, sp, s, launches)); }
+      else CK(launch_mark_direct(*c2, mn, d.fa, sp, s, launches));
     }
     d.code = ar.get<int32_t>((int64_t)d.span);
     void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)d.span));
@@ -334,14 +335,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   int32_t* hB = ar.get<int32_t>(nB);
   int32_t* cntA = ar.zeros<int32_t>(K);
   int32_t* cntB = ar.zeros<int32_t>(K);
-  double* rowA = ar.zeros<double>(G);  // sum |v| per group (fp64 bound; non-negative, so its
-  double* rowB = ar.zeros<double>(H);  // bit pattern orders like an unsigned integer for the max)
-  CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, s, L));
-  CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, s, L));
+  // sum |v| per group: the integer-SUM overflow bound of the guard (fp64; non-negative, so
+  // its bit pattern orders like an unsigned integer for the max reduction)
+  const bool int_sum = is_sum && !is_float;
+  double* rowA = int_sum ? ar.zeros<double>(G) : nullptr;
+  double* rowB = int_sum ? ar.zeros<double>(H) : nullptr;
+  CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, K, s, L));
+  CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, K, s, L));
   unsigned long long* d_misc = ar.zeros<unsigned long long>(4);  // J, max rowabs A, max rowabs B
   CK(launch_join_size(cntA, cntB, K, d_misc + 0, s, L));
-  CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), G, d_misc + 1, s, L));
-  CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), H, d_misc + 2, s, L));
+  if (int_sum) {
+    CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), G, d_misc + 1, s, L));
+    CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), H, d_misc + 2, s, L));
+  }
   CK(cudaMemcpyAsync(ctx->pinned, d_misc, 32, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   unsigned long long misc[4];
@@ -395,11 +401,12 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double t_dense = planes_est * dense_ops / R_tc + ((double)(Gp + Hp) * Kp * esz * 3 + (double)Gp * Hp * 8) / BW;
   const double csz = is_sum ? 8.0 : 4.0;
   const double t_sparse = (double)J / R_sp + ((double)G * H * csz * 2 + (double)(nA + nB) * 24) / BW;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
   const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 3 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
+  // cudaMemGetInfo costs ~0.3-0.5 ms of host time: only consult it for large working sets
+  size_t free_b = (size_t)1 << 62, total_b = 0;
+  if (std::max(dense_bytes, sparse_bytes) > 4e9) cudaMemGetInfo(&free_b, &total_b);
   bool dense;
   if (q->flags & TCUDB_FORCE_DENSE) dense = true;
   else if (q->flags & TCUDB_FORCE_SPARSE) dense = false;
@@ -824,7 +831,7 @@ tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* s
     int32_t* cu = ar.get<int32_t>(n_edges);
     int32_t* cv = ar.get<int32_t>(n_edges);
     int32_t* dummy = ar.zeros<int32_t>(V);
-    CK(launch_probe(cs, cd, none, DV.view(), DV.view(), cu, cv, dummy, nullptr, s, L));
+    CK(launch_probe(cs, cd, none, DV.view(), DV.view(), cu, cv, dummy, nullptr, V, s, L));
     const int64_t Vp = round_up(V, 256), Kp = round_up(V, 128);
     uint8_t* adj = ar.zeros<uint8_t>(Vp * Kp);
     CK(launch_fill_sym_pattern(cu, cv, n_edges, adj, Kp, s, L));

@@ -34,7 +34,9 @@ def run(engine, torch_mod, A, B, agg, flags=0):
 
 
 # ---------------------------------------------------------------- a6: the GEMM alone
-@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 512, 384), (512, 768, 1024), (1152, 256, 2048)])
+# M % 256 == 0 -> CTA-pair kernel (cta_group::2); M = 128, 1152 -> 1-CTA kernel
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 512, 384), (512, 768, 1024), (1152, 256, 2048),
+                                   (2048, 1024, 640), (4096, 256, 128)])
 @pytest.mark.parametrize("sa,sb", [(0, 0), (1, 1), (0, 1), (1, 0)])
 def test_gemm_int8_exact(engine, torch_mod, M, N, K, sa, sb):
     torch = torch_mod
@@ -49,7 +51,7 @@ def test_gemm_int8_exact(engine, torch_mod, M, N, K, sa, sb):
     assert torch.equal(C.to(torch.float64), ref)
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (384, 512, 1024)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (384, 512, 1024), (512, 512, 256), (1024, 768, 2048)])
 def test_gemm_bf16(engine, torch_mod, M, N, K):
     torch = torch_mod
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
@@ -259,3 +261,35 @@ def test_loopback_row_sharding(engine, torch_mod, P):
         parts.append(res_np(engine.join_agg(Ar, dB, agg)))
     for k in ("g", "h", "agg"):
         assert np.array_equal(np.concatenate([p[k] for p in parts]), full[k])
+
+
+PAIR_SCRIPT = r"""
+import torch
+from paper_2112_07552_b200 import Engine
+e = Engine(0)
+g = torch.Generator(device="cuda").manual_seed(7)
+for (M, N, K) in [(256, 256, 128), (512, 768, 1024), (2048, 1024, 640)]:
+    for sa, sb in [(0, 0), (1, 1), (0, 1)]:
+        mk = lambda r, s: (torch.randint(-128, 128, (r, K), generator=g, device="cuda", dtype=torch.int32).to(torch.int8)
+                           if s else torch.randint(0, 256, (r, K), generator=g, device="cuda", dtype=torch.int32).to(torch.uint8))
+        A, B = mk(M, sa), mk(N, sb)
+        C = e.gemm(A, B, a_signed=sa, b_signed=sb)
+        assert torch.equal(C.double(), A.double() @ B.double().T), (M, N, K, sa, sb)
+    A = torch.randn(M, K, generator=g, device="cuda").bfloat16(); B = torch.randn(N, K, generator=g, device="cuda").bfloat16()
+    C = e.gemm(A, B)
+    ref = A.double() @ B.double().T
+    assert torch.all((C.double() - ref).abs() <= 1e-5 * (A.double().abs() @ B.double().abs().T) + 1e-6)
+print("PAIR_OK")
+"""
+
+
+def test_gemm_cta_pair_kernel_exact():
+    """The cta_group::2 kernel (TCUDB_GEMM_PAIR=1, read once per process) in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TCUDB_GEMM_PAIR="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", PAIR_SCRIPT], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert "PAIR_OK" in r.stdout, r.stdout + r.stderr
