@@ -111,11 +111,13 @@ def load_tables(config):
     return A, B, agg
 
 
-def gemm_traffic_from_profiles(config):
+def gemm_traffic_from_profiles(config, elem):
+    """DRAM bytes per GEMM launch from the committed ncu capture of this kernel variant."""
     p = os.path.join(ROOT, "profiles", f"gemm_traffic_{config}.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("dram_bytes_per_launch")
+        if d.get("elem", 0) == elem:
+            return d.get("dram_bytes_per_launch")
     return None
 
 
@@ -266,15 +268,21 @@ def main():
         ops = st["gemm_ops"]             # 2 * Gp * Hp * Kp per launch (SURVEY §8(d) per-unit figure)
         g_ms = statistics.mean(gemm_ms)
         achieved = ops / (g_ms * 1e-3) / 1e12
-        int8 = st["elem"] == 0
-        peak = peaks["bf16_tflops"] * (2.0 if int8 else 1.0)
-        peak_sus = peaks["bf16_tflops_sustained"] * (2.0 if int8 else 1.0)
-        roof = {"bound": "tensor", "kernel": "k_gemm_tc (tcgen05 kind::i8)" if int8 else "k_gemm_tc (tcgen05 kind::f16)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s" if not int8 else "TOP/s",
+        # the contraction's own dtype peak: measured bf16 x the nominal ratio (int8 / fp8 2x, fp4 4x)
+        kind, ratio, unit = {0: ("kind::i8 (u8/s8 -> s32)", 2.0, "TOP/s"),
+                             1: ("kind::f16 (bf16 -> f32)", 1.0, "TFLOP/s"),
+                             2: ("kind::f16 (bf16 hi/lo split)", 1.0, "TFLOP/s"),
+                             3: ("kind::mxf4 (e2m1 0/1 -> f32, unit scales)", 4.0, "TFLOP/s")}[st["elem"]]
+        peak = peaks["bf16_tflops"] * ratio
+        peak_sus = peaks["bf16_tflops_sustained"] * ratio
+        int8_peak = peaks["bf16_tflops"] * 2.0
+        roof = {"bound": "tensor", "kernel": f"k_gemm_tc (tcgen05 {kind})",
+                "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": achieved / peak, "peak_sustained": peak_sus, "frac_of_sustained": achieved / peak_sus,
-                "peak_source": f"{peaks['source']} bf16 x {'2 (int8/bf16 nominal ratio)' if int8 else '1'}",
+                "peak_source": f"{peaks['source']} bf16 x {ratio:g} (nominal {kind.split()[0]}/bf16 ratio)",
+                "vs_int8_peak": achieved / int8_peak,
                 "ops_per_launch": ops, "avg_launch_ms": g_ms,
-                "traffic": gemm_traffic_from_profiles(args.config)}
+                "traffic": gemm_traffic_from_profiles(args.config, st["elem"])}
     else:
         # sparse path: HBM-bound expand; algorithmic bytes = 16 B per update (read bucket entry + RMW C) approx.
         b = st["join_pairs"] * 16.0
@@ -296,7 +304,7 @@ def main():
         "metric": METRIC, "value": n_tuples * args.steps / (total_ms * 1e-3), "unit": "tuples/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u8" if (st["path"] == 0 and st["elem"] == 0) else ("bf16" if st["path"] == 0 else "int64"),
+        "dtype": ({0: "u8", 1: "bf16", 2: "bf16", 3: "e2m1"}[st["elem"]] if st["path"] == 0 else "int64"),
         "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "n_A": len(A["k"]), "n_B": len(B["k"]),
                    "G": st["G"], "H": st["H"], "K": st["K"], "join_pairs": st["join_pairs"],

@@ -65,8 +65,10 @@ enum {
   TCUDB_FORCE_SPARSE = 1u << 1, /* sparse-operand expand path (a7) */
   TCUDB_GATHER_NONE = 1u << 2,  /* reserved (multi-GPU: keep row shards) */
   TCUDB_UNORDERED = 1u << 3,    /* reserved: output order unspecified */
-  TCUDB_FORCE_WIDE = 1u << 4    /* test hook: skip the packed-u8 COUNT fill, use the
-                                   32-bit scratch + digit-plane guard path */
+  TCUDB_FORCE_WIDE = 1u << 4,   /* test hook: skip the packed fp4/u8 COUNT fills, use the
+                                   int64 scratch + digit-plane guard path */
+  TCUDB_NO_FP4 = 1u << 5        /* COUNT: do not use e2m1 (fp4) 0/1 operands (kind::mxf4);
+                                   use u8 operands (kind::i8) */
 };
 
 typedef struct {
@@ -92,7 +94,8 @@ typedef struct {
  * on the query stream; ms_total is host wall clock of the whole call. */
 typedef struct {
   int32_t path;       /* 0 dense (tensor cores), 1 sparse expand */
-  int32_t elem;       /* dense operand type: 0 u8/s8 (kind::i8), 1 bf16, 2 bf16x3 split */
+  int32_t elem;       /* dense operand type: 0 u8/s8 (kind::i8), 1 bf16, 2 bf16x3 split,
+                         3 e2m1 0/1 COUNT operands (kind::mxf4, unit scales) */
   int32_t planes_a;   /* base-256 digit planes of A_op (int SUM) */
   int32_t planes_b;
   int32_t existence;  /* 0: existence from C itself, 1: separate COUNT plane */
@@ -145,7 +148,10 @@ tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* s
  * with K-major device operands. elem 0: int8 (a_signed/b_signed select s8 vs
  * u8), C int32; elem 1: bf16, C fp32. Requirements: M % 128 == 0,
  * N % 256 == 0, K*elem_bytes % 128 == 0, row strides lda/ldb/ldc in elements
- * with lda*elem_bytes % 16 == 0, 16-byte aligned base pointers. */
+ * with lda*elem_bytes % 16 == 0, 16-byte aligned base pointers.
+ * elem 2: e2m1 (fp4) packed two per byte (kind::mxf4 with unit block scales), for
+ * integer-valued operands: K, lda, ldb count ELEMENTS (K % 256 == 0, lda/ldb even),
+ * N % 240 == 0, C int32 = the fp32 accumulator rounded to nearest. */
 tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t b_signed, int64_t M, int64_t N,
                         int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                         void* stream);

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "OK", -1: "E_INVALID", -2: "E_UNSUPPORTED", -3: "E_PRECISION"
                 -5: "E_NOMEM", -6: "E_CUDA", -7: "E_COMM"}
 I32, I64, F32, F64 = 0, 1, 2, 3
 COUNT, SUM = 0, 1
-FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE = 1, 2, 4, 8, 16
+FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE, NO_FP4 = 1, 2, 4, 8, 16, 32
 
 EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_triangle_count", "tcudb_gemm",
                   "tcudb_minmax", "tcudb_partition", "tcudb_result_free", "tcudb_result_free_host",
@@ -344,15 +344,19 @@ class Engine:
                                               self._stream(stream)))
         return out, [int(c) for c in counts]
 
-    def gemm(self, A, B, a_signed=True, b_signed=True, stream=None):
-        """C = A @ B.T on the tcgen05 kernel. A: [M,K], B: [N,K] int8/uint8 (-> int32) or bf16 (-> fp32)."""
+    def gemm(self, A, B, a_signed=True, b_signed=True, fp4=False, stream=None):
+        """C = A @ B.T on the tcgen05 kernel. A: [M,K], B: [N,K] int8/uint8 (-> int32) or bf16 (-> fp32).
+        fp4=True: A, B are uint8 [rows, K/2] of packed e2m1 pairs (kind::mxf4), C int32."""
         torch = self._torch
         M, K = A.shape
         N = B.shape[0]
-        elem = 1 if A.dtype == torch.bfloat16 else 0
-        C = torch.empty((M, N), dtype=torch.float32 if elem else torch.int32, device=A.device)
-        st = self._lib.tcudb_gemm(self._ctx, elem, int(a_signed), int(b_signed), M, N, K, A.data_ptr(), A.stride(0),
-                                  B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), self._stream(stream))
+        elem = 2 if fp4 else (1 if A.dtype == torch.bfloat16 else 0)
+        lda, ldb = A.stride(0), B.stride(0)
+        if fp4:
+            K, lda, ldb = 2 * K, 2 * lda, 2 * ldb
+        C = torch.empty((M, N), dtype=torch.float32 if elem == 1 else torch.int32, device=A.device)
+        st = self._lib.tcudb_gemm(self._ctx, elem, int(a_signed), int(b_signed), M, N, K, A.data_ptr(), lda,
+                                  B.data_ptr(), ldb, C.data_ptr(), C.stride(0), self._stream(stream))
         self._check(st)
         return C
 

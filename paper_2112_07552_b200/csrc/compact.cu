@@ -41,12 +41,13 @@ __global__ void __launch_bounds__(T) k_seg_count(const CompactArgs a, int32_t* _
   const int lane = lane_id();
   for (int64_t s = (int64_t)blockIdx.x * WPB + warp_id(); s < nsegs; s += (int64_t)gridDim.x * WPB) {
     const int64_t row = s / a.nseg;
-    const int64_t col0 = (s - row * a.nseg) * 256;
+    const int64_t col0 = (s - row * a.nseg) * a.seg_w;
+    const int64_t lim = min(a.H, col0 + a.seg_w);
     int c = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t col = col0 + j * 32 + lane;
-      c += (col < a.H && nz_at(a.E, a.e_kind, row * a.lde + col)) ? 1 : 0;
+      c += (col < lim && nz_at(a.E, a.e_kind, row * a.lde + col)) ? 1 : 0;
     }
     c = warp_sum(c);
     if (lane == 0) cnt[s] = c;
@@ -74,20 +75,21 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
   const VT* __restrict__ V = static_cast<const VT*>(a.V);
   for (int64_t s = (int64_t)blockIdx.x * WPB + warp_id(); s < nsegs; s += (int64_t)gridDim.x * WPB) {
     const int64_t row = s / a.nseg;
-    const int64_t col0 = (s - row * a.nseg) * 256;
+    const int64_t col0 = (s - row * a.nseg) * a.seg_w;
     if (col0 >= a.H) continue;
+    const int64_t lim = min(a.H, col0 + a.seg_w);
     ET e[8];
     VT v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t col = col0 + j * 32 + lane;
-      e[j] = col < a.H ? __ldcs(E + row * a.lde + col) : ET(0);
+      e[j] = col < lim ? __ldcs(E + row * a.lde + col) : ET(0);
     }
     if (!SAME) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int64_t col = col0 + j * 32 + lane;
-        v[j] = (col < a.H && Cell<EK>::nz(e[j])) ? __ldcs(V + row * a.ldv + col) : VT(0);
+        v[j] = (col < lim && Cell<EK>::nz(e[j])) ? __ldcs(V + row * a.ldv + col) : VT(0);
       }
     }
     int64_t base = off[s];

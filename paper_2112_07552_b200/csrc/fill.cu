@@ -58,6 +58,26 @@ __global__ void k_fill_count_u8(const int32_t* __restrict__ kcode, const int32_t
   }
 }
 
+// COUNT with 0/1 cells as e2m1 (fp4) nibbles, two per byte: 1.0 = 0b0010. The
+// atomicOr's return value tells whether the nibble was already set (a second
+// tuple in the same (row, k) cell) -> fs->overflow, and the guard falls back to
+// the exact u8 path. Only the set/unset pattern is written, so no carries exist.
+__global__ void k_fill_count_fp4(const int32_t* __restrict__ kcode, const int32_t* __restrict__ rcode, int64_t n,
+                                 uint8_t* __restrict__ op, int64_t ld_elems, FillStats* __restrict__ fs) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  int dup = 0;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t kc = kcode[i];
+    if (kc < 0) continue;
+    const int64_t e = (int64_t)rcode[i] * ld_elems + kc;  // element index (nibble)
+    const int sh = 4 * (int)(e & 7);
+    const unsigned old = atomicOr(reinterpret_cast<unsigned*>(op + ((e >> 1) & ~int64_t(3))), 0x2u << sh);
+    if ((old >> sh) & 0xFu) dup = 1;
+  }
+  dup = __any_sync(0xffffffffu, dup);
+  if (lane_id() == 0 && dup) atomicOr(&fs->overflow, 1);
+}
+
 // Wide integer fill into int64 scratch (COUNT: +1, SUM: +v), wrapping adds.
 __global__ void k_fill_i64(const int32_t* __restrict__ kcode, const int32_t* __restrict__ rcode, ColDesc val,
                            int64_t n, unsigned long long* __restrict__ scr, int64_t ld) {
@@ -194,6 +214,14 @@ cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int
                                  FillStats* fs, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
   k_fill_count_u8<<<grid_for(n), T, 0, s>>>(kcode, rcode, n, op, ld, fs);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,
+                                  int64_t ld_elems, FillStats* fs, cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_fill_count_fp4<<<grid_for(n), T, 0, s>>>(kcode, rcode, n, op, ld_elems, fs);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

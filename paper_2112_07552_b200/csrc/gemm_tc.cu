@@ -22,21 +22,28 @@ namespace tcudb {
 namespace {
 
 constexpr int BM = kGemmBM, BN = kGemmBN, BKB = kGemmBKBytes;
-constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BKB;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BKB;  // 32 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int NUM_THREADS = 192;         // 6 warps
-constexpr int TMEM_COLS = 512;           // 2 accumulators x 256 fp32/s32 columns
+constexpr int TMEM_COLS = 512;           // 2 accumulators x 256 fp32/s32 columns (fp4: 2 x 240 + scales)
 constexpr int GROUP_M = 16;              // tile raster: 16 M-blocks per band
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// Per-BN kernel geometry (BN = 256 for kind::i8 / kind::f16, 240 for kind::mxf4 so
+// that two accumulators plus the block-scale columns fit the 512 TMEM columns).
+template <int BN_>
+struct Geo {
+  static constexpr int B_STAGE_BYTES = BN_ * BKB;
+  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+  static constexpr int STAGES = 4;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+constexpr int SF_COL = 480;  // fp4: scale-factor columns [480, 512): SFA at 480, SFB at 496
 
 struct KParams {
   int64_t M, N;
   int tiles_m, tiles_n;
   int num_kb;        // K blocks of 128 bytes
   int kb_begin;      // first K block (elements / elems_per_kb)
-  int elems_per_kb;  // 128 (i8) or 64 (bf16)
+  int elems_per_kb;  // 128 (i8, fp4 bytes) or 64 (bf16)
   int is_bf16;
   uint32_t idesc;
   int epi;
@@ -55,58 +62,109 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nb = r / gsz;
 }
 
+TCUDB_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+TCUDB_DEV void tmem_st_32x32b_x16(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+TCUDB_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A·Bᵀ with e2m1 operands and UE8M0 block scales (32-element blocks) read from TMEM.
+TCUDB_DEV void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t sfa,
+                        uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+      : "memory");
+}
+
+// One W-column chunk (W = 32 or 16) of the epilogue for the row this thread owns.
+template <int W, bool FP4>
+__device__ __forceinline__ void epilogue_chunk(const KParams& p, const uint32_t* rr, int64_t row, int64_t col,
+                                               int& nzc, long long& tri) {
+  uint32_t r[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) r[i] = FP4 ? (uint32_t)__float2int_rn(__uint_as_float(rr[i])) : rr[i];
+  if (p.epi == EPI_STORE32) {
+    int4* dst = reinterpret_cast<int4*>(reinterpret_cast<uint32_t*>(p.C) + row * p.ldc + col);
+#pragma unroll
+    for (int i = 0; i < W / 4; ++i) dst[i] = make_int4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+    if (p.cnt_out) {
+      const uint32_t m = (p.is_bf16 && !FP4) ? 0x7fffffffu : 0xffffffffu;  // fp32: +-0 are both zero
+#pragma unroll
+      for (int i = 0; i < W; ++i) nzc += (r[i] & m) != 0u;
+    }
+  } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
+    longlong2* d2 = reinterpret_cast<longlong2*>(reinterpret_cast<long long*>(p.C) + row * p.ldc + col);
+#pragma unroll
+    for (int i = 0; i < W / 2; ++i) {
+      // wrapping (mod 2^64) arithmetic: exact whenever the true sum fits int64 (guard a3)
+      unsigned long long x0 = (unsigned long long)(long long)(int)r[2 * i] << p.shift;
+      unsigned long long x1 = (unsigned long long)(long long)(int)r[2 * i + 1] << p.shift;
+      if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += (unsigned long long)o.x; x1 += (unsigned long long)o.y; }
+      d2[i] = make_longlong2((long long)x0, (long long)x1);
+      if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
+    }
+  } else {  // EPI_TRI
+    if (row < p.mask_rows && col < p.mask_cols) {
+      const uint4* m4 = reinterpret_cast<const uint4*>(p.mask + row * p.ldm + col);
+#pragma unroll
+      for (int q = 0; q < W / 16; ++q) {
+        const uint4 ma = m4[q];
+        const uint32_t mw[4] = {ma.x, ma.y, ma.z, ma.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          tri += (long long)(int)r[16 * q + i] * (long long)((mw[i >> 2] >> (8 * (i & 3))) & 0xFF);
+      }
+    }
+  }
+}
+
 // Epilogue for one accumulator tile: this thread owns one row (its TMEM lane) and
-// the BN accumulator columns at taddr. Returns the row's nonzero count.
+// the BN_ accumulator columns at taddr. Returns the row's nonzero count.
+template <int BN_, bool FP4>
 __device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, int64_t row, int nb, long long& tri) {
-  int nzc = 0;  // nonzeros of this row inside the 256-column tile (compaction count, a8)
+  int nzc = 0;  // nonzeros of this row inside the BN_-column tile (compaction count, a8)
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = 0; c < BN_ / 32; ++c) {
     uint32_t r[32];
     tmem_ld_32x32b_x32(taddr + c * 32, r);
     tmem_ld_wait();
-    const int64_t col = (int64_t)nb * BN + c * 32;
-    if (p.epi == EPI_STORE32) {
-      int4* dst = reinterpret_cast<int4*>(reinterpret_cast<uint32_t*>(p.C) + row * p.ldc + col);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dst[i] = make_int4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-      if (p.cnt_out) {
-        const uint32_t m = p.is_bf16 ? 0x7fffffffu : 0xffffffffu;  // fp32: +-0 are both zero
-#pragma unroll
-        for (int i = 0; i < 32; ++i) nzc += (r[i] & m) != 0u;
-      }
-    } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
-      long long* dst = reinterpret_cast<long long*>(p.C) + row * p.ldc + col;
-      longlong2* d2 = reinterpret_cast<longlong2*>(dst);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        // wrapping (mod 2^64) arithmetic: exact whenever the true sum fits int64 (guard a3)
-        unsigned long long x0 = (unsigned long long)(long long)(int)r[2 * i] << p.shift;
-        unsigned long long x1 = (unsigned long long)(long long)(int)r[2 * i + 1] << p.shift;
-        if (p.epi == EPI_ACC64) { const longlong2 o = d2[i]; x0 += (unsigned long long)o.x; x1 += (unsigned long long)o.y; }
-        d2[i] = make_longlong2((long long)x0, (long long)x1);
-        if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
-      }
-    } else {  // EPI_TRI
-      if (row < p.mask_rows && col < p.mask_cols) {
-        const uint4* m4 = reinterpret_cast<const uint4*>(p.mask + row * p.ldm + col);
-        const uint4 ma = m4[0], mb4 = m4[1];
-        const uint32_t mw[8] = {ma.x, ma.y, ma.z, ma.w, mb4.x, mb4.y, mb4.z, mb4.w};
-#pragma unroll
-        for (int i = 0; i < 32; ++i) tri += (long long)(int)r[i] * (long long)((mw[i >> 2] >> (8 * (i & 3))) & 0xFF);
-      }
-    }
+    epilogue_chunk<32, FP4>(p, r, row, (int64_t)nb * BN_ + c * 32, nzc, tri);
+  }
+  if (BN_ % 32) {
+    uint32_t r[16];
+    tmem_ld_32x32b_x16(taddr + (BN_ / 32) * 32, r);
+    tmem_ld_wait();
+    epilogue_chunk<16, FP4>(p, r, row, (int64_t)nb * BN_ + (BN_ / 32) * 32, nzc, tri);
   }
   return nzc;
 }
 
+template <int BN_, bool FP4>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
+  using G = Geo<BN_>;
+  constexpr int STAGES = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment required by the 128B swizzle atoms.
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
@@ -128,6 +186,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (FP4) {
+    // all block scales = 2^0 (UE8M0 0x7F): the e2m1 operands carry the exact small
+    // integers themselves; written once into TMEM columns [480, 512) by the epilogue warps
+    if (warp >= 2) {
+      const uint32_t q = (uint32_t)((warp & 3) * 32) << 16;
+      tmem_st_32x32b_x16(tmem_base + q + SF_COL, 0x7F7F7F7Fu);
+      tmem_st_32x32b_x16(tmem_base + q + SF_COL + 16, 0x7F7F7F7Fu);
+      tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -138,10 +209,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
           const int kc = (p.kb_begin + kb) * p.elems_per_kb;
           tma_load_2d(&tmA, sA + stage * A_STAGE_BYTES, &full[stage], kc, mb * BM, pol);
-          tma_load_2d(&tmB, sB + stage * B_STAGE_BYTES, &full[stage], kc, nb * BN, pol);
+          tma_load_2d(&tmB, sB + stage * G::B_STAGE_BYTES, &full[stage], kc, nb * BN_, pol);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -154,16 +225,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BN_;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A_STAGE_BYTES));
-          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * B_STAGE_BYTES));
+          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * G::B_STAGE_BYTES));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 bytes of K per 128-byte stage
             const uint32_t accum = (kb | kk) != 0;
-            if (p.is_bf16) mma_f16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
+            if (FP4) mma_mxf4(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, tmem_base + SF_COL,
+                              tmem_base + SF_COL + 16, accum);
+            else if (p.is_bf16) mma_f16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
             else mma_i8(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
           }
           mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
@@ -183,8 +256,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      const int nzc = epilogue_rows(p, taddr, row, nb, tri);
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN_;
+      const int nzc = epilogue_rows<BN_, FP4>(p, taddr, row, nb, tri);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -308,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row = (int64_t)mb * 256 + rank * 128 + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      const int nzc = epilogue_rows(p, taddr, row, nb, tri);
+      const int nzc = epilogue_rows<BN, false>(p, taddr, row, nb, tri);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -370,14 +443,59 @@ bool make_map(CUtensorMap* m, const void* base, int elem, int64_t rows, int64_t 
 
 }  // namespace
 
+// kind::mxf4 path: e2m1 operands, two elements per byte. k_begin / k_len / lda / ldb
+// are in BYTES; the N tile is 240 (two 240-column accumulators + block scales in TMEM),
+// tiles_n = ceil(N / 240) with TMA zero-filling the rows past N; C must hold
+// ceil(N/240)*240 columns (ldc).
+cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
+  constexpr int BNF = kGemmBNFp4;
+  if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
+  if (a.M % BM || a.k_len % BKB || a.k_begin % BKB || a.lda % 16 || a.ldb % 16 || a.epi != EPI_STORE32)
+    return cudaErrorInvalidValue;
+  const int64_t tiles_n = (a.N + BNF - 1) / BNF;
+  if (a.ldc < tiles_n * BNF) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BNF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Geo<BNF>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t kcols = a.k_begin + a.k_len;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, ELEM_I8, a.M, kcols, a.lda, BM) || !make_map(&mB, a.B, ELEM_I8, a.N, kcols, a.ldb, BNF))
+    return cudaErrorInvalidValue;
+  KParams p{};
+  p.M = a.M; p.N = a.N;
+  p.tiles_m = (int)(a.M / BM); p.tiles_n = (int)tiles_n;
+  p.elems_per_kb = BKB;  // bytes
+  p.num_kb = (int)(a.k_len / BKB);
+  p.kb_begin = (int)(a.k_begin / BKB);
+  p.is_bf16 = 0;
+  // Block-scaled instruction descriptor (kind::mxf4): A/B format E2M1 = 1 (bits 7-9, 10-12),
+  // K-major, N >> 3 (bits 17-22), scale format UE8M0 (bit 23), M >> 4 (bits 24-28),
+  // scale-factor ids 0, K = 64 per MMA (bit 31 = 0).
+  uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BNF >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+  p.idesc = idesc;
+  p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = 0;
+  p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  k_gemm_tc<BNF, true><<<grid, NUM_THREADS, Geo<BNF>::SMEM_BYTES, s>>>(mA, mB, p);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.elem == ELEM_FP4) return launch_gemm_fp4(a, s, launches);
   const int esz = a.elem == ELEM_BF16 ? 2 : 1;
   if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
   if (a.M % BM || a.N % BN || (a.k_len * esz) % BKB || (a.k_begin * esz) % BKB) return cudaErrorInvalidValue;
   if ((a.lda * esz) % 16 || (a.ldb * esz) % 16) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Geo<BN>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
     if (e != cudaSuccess) return e;
@@ -418,7 +536,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
     k_gemm_tc2<<<grid, NUM_THREADS, SMEM2_BYTES, s>>>(mA, mB, p);
   } else {
     const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-    k_gemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
+    k_gemm_tc<BN, false><<<grid, NUM_THREADS, Geo<BN>::SMEM_BYTES, s>>>(mA, mB, p);
   }
   if (launches) ++*launches;
   return cudaGetLastError();

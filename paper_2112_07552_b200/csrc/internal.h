@@ -8,7 +8,7 @@ namespace tcudb {
 constexpr int kNumSMs = 148;
 
 // ---------------------------------------------------------------- a6: tcgen05 GEMM
-enum GemmElem { ELEM_I8 = 0, ELEM_BF16 = 1 };
+enum GemmElem { ELEM_I8 = 0, ELEM_BF16 = 1, ELEM_FP4 = 2 /* e2m1 x2 per byte, kind::mxf4, scales 1 */ };
 enum GemmEpi {
   EPI_STORE32 = 0,  // C32[r][c] = acc (int32 or fp32 bits)
   EPI_SET64 = 1,    // C64[r][c] = (int64)acc << shift
@@ -18,6 +18,7 @@ enum GemmEpi {
 constexpr int kGemmBM = 128;
 constexpr int kGemmBN = 256;
 constexpr int kGemmBKBytes = 128;
+constexpr int kGemmBNFp4 = 240;
 
 struct GemmArgs {
   int elem = ELEM_I8;

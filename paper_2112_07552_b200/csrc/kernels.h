@@ -70,6 +70,10 @@ struct FillStats {
 // COUNT: packed u8 atomics directly into op[row][k] (row = code of the group).
 cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
                                  FillStats* fs, cudaStream_t s, int64_t* launches);
+// COUNT with 0/1 cells straight into packed e2m1 nibbles (ld in elements); a second tuple in a
+// cell sets fs->overflow (the guard then uses the u8 path).
+cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,
+                                  int64_t ld_elems, FillStats* fs, cudaStream_t s, int64_t* launches);
 // Pattern plane op[r][k] = 1 where a cell holds >= 1 tuple; symmetric adjacency for triangles.
 cudaError_t launch_fill_pattern_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
                                    cudaStream_t s, int64_t* launches);
@@ -127,7 +131,8 @@ cudaError_t launch_part_scatter(const ColDesc& key, const ColDesc& grp, const Co
 // Existence matrix E (int32 count or the value matrix) -> tuples (g, h, agg), row-major.
 struct CompactArgs {
   int64_t G, H;
-  int64_t nseg;                                  // 256-column segments per row (ceil(H/256) or Hp/256)
+  int64_t nseg;                                  // segments per row (= GEMM N tiles on the dense path)
+  int64_t seg_w;                                 // columns per segment (<= 256; 256, or 240 for fp4)
   const void* E; int e_kind; int64_t lde;       // e_kind: 0 int32, 1 int64, 2 f32, 3 f64
   const void* V; int v_kind; int64_t ldv;       // value matrix (agg), same kinds
   const long long* dict_g; const long long* dict_h;

@@ -44,6 +44,7 @@ struct tcudb_ctx {
   std::multimap<size_t, void*> host_free;
   std::map<void*, size_t> host_size;
   std::map<void*, bool> dev_from_cb;  // result pointer -> allocated through afn
+  bool fp4 = true;                    // e2m1 COUNT operands allowed (env TCUDB_NO_FP4=1 disables)
 };
 
 namespace {
@@ -439,7 +440,24 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     int64_t ldop = Kp;                              // elements per operand row
     int64_t k_len = Kp;
     const int64_t cellsA = Gp * Kp, cellsB = Hp * Kp;
-    if (!is_sum && !(q->flags & TCUDB_FORCE_WIDE)) {
+    // Guard a3, most compact type ("int4"): COUNT with 0/1 cells fits e2m1
+    // (fp4) exactly; every product is 0 or 1 and every fp32 partial sum is an integer
+    // <= K < 2^24, so kind::mxf4 (unit block scales) is exact. A duplicate (g,k) tuple
+    // is detected by the fill and sends the query down the u8 path.
+    uint8_t *op4A = nullptr, *op4B = nullptr;
+    const int64_t Kp4 = round_up(K, 256);  // 128-byte K blocks of packed nibbles
+    if (!is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24)) {
+      op4A = ar.zeros<uint8_t>(Gp * Kp4 / 2);
+      op4B = ar.zeros<uint8_t>(Hp * Kp4 / 2);
+      CK(launch_fill_count_fp4(kA, gA, nA, op4A, Kp4, fs + 0, s, L));
+      CK(launch_fill_count_fp4(kB, hB, nB, op4B, Kp4, fs + 1, s, L));
+      CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      FillStats hf[2];
+      std::memcpy(hf, ctx->pinned, sizeof(hf));
+      if (hf[0].overflow || hf[1].overflow) { op4A = op4B = nullptr; CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s)); }
+    }
+    if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE)) {
       opA = ar.zeros<uint8_t>(cellsA);
       opB = ar.zeros<uint8_t>(cellsB);
       CK(launch_fill_count_u8(kA, gA, nA, opA, Kp, fs + 0, s, L));
@@ -451,7 +469,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       if (hf[0].overflow || hf[1].overflow) { opA = opB = nullptr; CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s)); }
       else { maxA = hf[0].max_abs; maxB = hf[1].max_abs; }
     }
-    if (!opA && !is_float) {
+    if (!op4A && !opA && !is_float) {
       // wide integer path: int64 scratch -> stats -> digit planes (guard a3)
       long long* scrA = ar.zeros<long long>(cellsA);
       long long* scrB = ar.zeros<long long>(cellsB);
@@ -518,11 +536,26 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     GemmArgs ga{};
     ga.M = Gp; ga.N = Hp;
     double ops = 0;
-    // the GEMM that produces the existence matrix also emits per-(row, 256-col) nonzero counts
+    // the GEMM that produces the existence matrix also emits per-(row, N-tile) nonzero counts
     ca.nseg = Hp / 256;
+    ca.seg_w = 256;
+    if (op4A) {
+      ca.nseg = (Hp + kGemmBNFp4 - 1) / kGemmBNFp4;
+      ca.seg_w = kGemmBNFp4;
+    }
     seg_cnt = ar.get<int32_t>(Gp * ca.nseg);
     int32_t* value_cnt = need_exist ? nullptr : seg_cnt;
-    if (is_float) {
+    if (op4A) {
+      const int64_t Hc = ca.nseg * kGemmBNFp4;
+      int32_t* C = ar.get<int32_t>(Gp * Hc);
+      ga.elem = ELEM_FP4; ga.A = op4A; ga.lda = Kp4 / 2; ga.B = op4B; ga.ldb = Kp4 / 2;
+      ga.k_begin = 0; ga.k_len = Kp4 / 2; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hc;
+      ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
+      CK(launch_gemm(ga, s, L));
+      ops += 2.0 * Gp * Hc * Kp4;
+      ca.E = C; ca.e_kind = 0; ca.lde = Hc; ca.V = C; ca.v_kind = 0; ca.ldv = Hc;
+      S.elem = 3;
+    } else if (is_float) {
       float* C = ar.get<float>(Gp * Hp);
       ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop;
       ga.k_begin = 0; ga.k_len = k_len; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
@@ -623,6 +656,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     }
     ca.lde = ldc; ca.ldv = ldc;
     ca.nseg = (H + 255) / 256;
+    ca.seg_w = 256;
     CK(launch_expand(ea, s, L));
     tm.mark(&S.ms_sparse);
   }
@@ -705,6 +739,7 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   if (major != 10 || minor != 0) return TCUDB_E_CUDA;  // built for sm_100a only
   tcudb_ctx* c = new tcudb_ctx();
   c->device = device;
+  c->fp4 = !(getenv("TCUDB_NO_FP4") && getenv("TCUDB_NO_FP4")[0] == '1');
   c->afn = alloc_fn;
   c->ffn = free_fn;
   c->user = user;
@@ -856,11 +891,13 @@ tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* s
 tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t b_signed, int64_t M, int64_t N,
                         int64_t K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                         void* stream) {
-  if (!ctx || !A || !B || !C || (elem != 0 && elem != 1)) return TCUDB_E_INVALID;
+  if (!ctx || !A || !B || !C || elem < 0 || elem > 2) return TCUDB_E_INVALID;
+  if (elem == 2 && (K % 256 || lda % 2 || ldb % 2 || N % kGemmBNFp4)) return TCUDB_E_INVALID;
   cudaSetDevice(ctx->device);
   GemmArgs ga{};
   ga.elem = elem; ga.a_signed = a_signed; ga.b_signed = b_signed; ga.M = M; ga.N = N; ga.k_begin = 0; ga.k_len = K;
   ga.A = A; ga.lda = lda; ga.B = B; ga.ldb = ldb; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = ldc;
+  if (elem == 2) { ga.k_len = K / 2; ga.lda = lda / 2; ga.ldb = ldb / 2; }  // fp4: bytes
   const cudaError_t e = launch_gemm(ga, static_cast<cudaStream_t>(stream), &ctx->launches);
   if (e == cudaErrorInvalidValue) { cudaGetLastError(); return set_err(ctx, TCUDB_E_INVALID, "gemm shape/alignment"); }
   if (e != cudaSuccess) return set_err(ctx, TCUDB_E_CUDA, "gemm launch");

@@ -293,3 +293,52 @@ def test_gemm_cta_pair_kernel_exact():
     r = subprocess.run([sys.executable, "-c", PAIR_SCRIPT], env=env, cwd=root, capture_output=True, text=True,
                        timeout=300)
     assert "PAIR_OK" in r.stdout, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- e2m1 (fp4) operands, kind::mxf4
+E2M1 = {0: 0, 1: 2, 2: 4, 3: 5, 4: 6, 6: 7}   # exact small integers in e2m1 (bias 1)
+
+
+def _pack_e2m1(vals, torch):
+    """uint8 [rows, K/2]: element 2j in the low nibble, 2j+1 in the high nibble."""
+    lut = torch.zeros(8, dtype=torch.uint8, device=vals.device)
+    for v, c in E2M1.items():
+        lut[v] = c
+    codes = lut[vals.long()]
+    return (codes[:, 0::2] | (codes[:, 1::2] << 4)).contiguous()
+
+
+@pytest.mark.parametrize("M,N,K,hi", [(128, 240, 256, 1), (256, 480, 1024, 4), (1024, 720, 2048, 6),
+                                      (384, 240, 4096, 2)])
+def test_gemm_fp4_exact_integers(engine, torch_mod, M, N, K, hi):
+    torch = torch_mod
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + hi)
+    allowed = torch.tensor([v for v in E2M1 if v <= hi], device="cuda")
+    A = allowed[torch.randint(0, len(allowed), (M, K), generator=g, device="cuda")]
+    B = allowed[torch.randint(0, len(allowed), (N, K), generator=g, device="cuda")]
+    C = engine.gemm(_pack_e2m1(A, torch), _pack_e2m1(B, torch), fp4=True)
+    assert torch.equal(C.double(), A.double() @ B.double().T)
+
+
+def test_gemm_fp4_large_sums_exact(engine, torch_mod):
+    """All-ones operands: every C = K; partial sums up to 20,480 stay exact in fp32."""
+    torch = torch_mod
+    K = 20480
+    A = torch.ones(128, K, dtype=torch.int32, device="cuda")
+    B = torch.ones(240, K, dtype=torch.int32, device="cuda")
+    C = engine.gemm(_pack_e2m1(A, torch), _pack_e2m1(B, torch), fp4=True)
+    assert torch.all(C == K)
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 0.1), ("c3", 1 / 16), ("c5", 1 / 256)])
+def test_count_fp4_vs_u8_vs_oracle(engine, torch_mod, oracle_mod, name, scale):
+    """Dense COUNT through e2m1 operands (default), u8 operands (NO_FP4) and the oracle agree."""
+    A, B, agg = datagen.make_config(name, scale)
+    ref = oracle_mod.join_agg(A, B, agg)
+    o4, s4 = run(engine, torch_mod, A, B, agg, 1)
+    o8, s8 = run(engine, torch_mod, A, B, agg, 1 | 32)
+    # c2 (token sets) and c3 (simple graph) have 0/1 cells -> e2m1; c5's random groups put
+    # several tuples in some (g, k) cells -> the fill detects it and falls back to u8
+    assert s4["elem"] == (0 if name == "c5" else 3) and s8["elem"] == 0
+    compare(o4, ref, agg)
+    compare(o8, ref, agg)
