@@ -79,7 +79,8 @@ typedef struct {
 /* Result tuples (SoA). g has A.group's type, h has B.group's type, agg is I64
  * for COUNT and integer SUM, F64 for float SUM. Owned by the caller; release
  * with tcudb_result_free (device) — or tcudb_result_free_host for results of
- * tcudb_join_agg_host. */
+ * tcudb_join_agg_host. Device results are ONE allocation (one allocator callback)
+ * with g at its base and h, agg at 256-byte aligned offsets: free through g only. */
 typedef struct {
   int64_t n;
   void* g;

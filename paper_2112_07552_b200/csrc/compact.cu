@@ -102,13 +102,14 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
       if (nz) {
         const int64_t pos = base + __popc(m & lt);
         const long long hval = a.dict_h[col];
-        if (GT == 1) static_cast<long long*>(a.out_g)[pos] = gval;
-        else static_cast<int*>(a.out_g)[pos] = (int)gval;
-        if (HT == 1) static_cast<long long*>(a.out_h)[pos] = hval;
-        else static_cast<int*>(a.out_h)[pos] = (int)hval;
+        // streaming (evict-first) stores: the result tuples are not re-read by the GPU
+        if (GT == 1) __stcs(static_cast<long long*>(a.out_g) + pos, gval);
+        else __stcs(static_cast<int*>(a.out_g) + pos, (int)gval);
+        if (HT == 1) __stcs(static_cast<long long*>(a.out_h) + pos, hval);
+        else __stcs(static_cast<int*>(a.out_h) + pos, (int)hval);
         const VT x = SAME ? (VT)e[j] : v[j];
-        if (VK == 2 || VK == 3) static_cast<double*>(a.out_agg)[pos] = (double)x;
-        else static_cast<long long*>(a.out_agg)[pos] = (long long)x;
+        if (VK == 2 || VK == 3) __stcs(static_cast<double*>(a.out_agg) + pos, (double)x);
+        else __stcs(static_cast<long long*>(a.out_agg) + pos, (long long)x);
       }
       base += __popc(m);
     }

@@ -159,8 +159,61 @@ __global__ void k_pred_count(const uint8_t* __restrict__ fa, const uint8_t* __re
   }
 }
 
+// Single-block variant for spans up to ~1 M flags (one launch instead of count +
+// scan + codes): 1024 threads sweep the flags in 16 K chunks with a running offset;
+// also writes the total, the ∪ count, and (direct group domains) dict[code] = min + x.
+__global__ void __launch_bounds__(1024) k_pred_codes_1blk(const uint8_t* __restrict__ fa,
+                                                          const uint8_t* __restrict__ fb, int64_t n,
+                                                          int32_t* __restrict__ code, int64_t* __restrict__ count,
+                                                          unsigned long long* __restrict__ union_cnt,
+                                                          long long* __restrict__ dict, long long minv) {
+  __shared__ int wt[32];
+  __shared__ long long s_run;
+  if (threadIdx.x == 0) s_run = 0;
+  long long u = 0;
+  for (int64_t base0 = 0; base0 < n; base0 += 1024 * 16) {
+    const int64_t base = base0 + (int64_t)threadIdx.x * 16;
+    uint8_t p[16];
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int64_t i = base + j;
+      const int a = i < n ? fa[i] : 0, b = (i < n) ? (fb ? fb[i] : 1) : 0;
+      p[j] = (uint8_t)(a & b);
+      c += p[j];
+      if (fb) u += a | b;
+    }
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane_id() >= o) x += y; }
+    if (lane_id() == 31) wt[warp_id()] = x;
+    __syncthreads();
+    int wp = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) { const int t = wt[w]; if (w < warp_id()) wp += t; tot += t; }
+    long long run = s_run + wp + x - c;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int64_t i = base + j;
+      if (i < n) {
+        code[i] = p[j] ? (int32_t)run : -1;
+        if (p[j] && dict) dict[run] = minv + (long long)i;
+        run += p[j];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_run += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = s_run;
+  if (union_cnt) {
+    u = warp_sum(u);
+    if (lane_id() == 0 && u) atomicAdd(union_cnt, (unsigned long long)u);
+  }
+}
+
 __global__ void k_pred_codes(const uint8_t* __restrict__ fa, const uint8_t* __restrict__ fb, int64_t n,
-                             const int64_t* __restrict__ tile_off, int32_t* __restrict__ code) {
+                             const int64_t* __restrict__ tile_off, int32_t* __restrict__ code,
+                             long long* __restrict__ dict, long long minv) {
   const int64_t base = (int64_t)blockIdx.x * PT + threadIdx.x * 16;
   uint8_t p[16];
   int c = 0;
@@ -183,7 +236,11 @@ __global__ void k_pred_codes(const uint8_t* __restrict__ fa, const uint8_t* __re
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int64_t i = base + j;
-    if (i < n) { code[i] = p[j] ? (int32_t)run : -1; run += p[j]; }
+    if (i < n) {
+      code[i] = p[j] ? (int32_t)run : -1;
+      if (p[j] && dict) dict[run] = minv + (long long)i;
+      run += p[j];
+    }
   }
 }
 
@@ -325,14 +382,18 @@ cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, 
 cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
                                int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
-  if (span <= 64 * 1024 && c.n >= 64 * span) {
+  // Same-address global stores serialize in L2 (a Zipf-hot key written by thousands of
+  // threads): mark in shared memory instead whenever the span fits, so each block
+  // stores each set flag once.
+  if (span <= 64 * 1024 && c.n >= 4096) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_mark_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
       attr = true;
     }
-    int64_t blocks = c.n / (64 * span);  // >= 64 tuples per flag per block
-    if (blocks > kNumSMs) blocks = kNumSMs;
+    // enough tuples per block to amortize zeroing and flushing the span
+    int64_t blocks = c.n / std::max<int64_t>(4096, span / 4);
+    if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
     if (blocks < 1) blocks = 1;
     k_mark_direct_smem<<<(int)blocks, 1024, (size_t)span, s>>>(c, minv, flags, (int)span);
     if (launches) ++*launches;
@@ -357,9 +418,15 @@ size_t pred_temp_bytes(int64_t n) {
 }
 
 cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, int32_t* code, int64_t* count_dev,
-                              unsigned long long* union_dev, void* temp, cudaStream_t s, int64_t* launches) {
+                              unsigned long long* union_dev, long long* dict, long long minv, void* temp,
+                              cudaStream_t s, int64_t* launches) {
   const int64_t nt = (n + PT - 1) / PT;
   if (n <= 0) return exclusive_scan_i32(nullptr, nullptr, 0, count_dev, temp, s, launches);
+  if (n <= (1 << 20)) {
+    k_pred_codes_1blk<<<1, 1024, 0, s>>>(fa, fb, n, code, count_dev, union_dev, dict, minv);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   int32_t* tc = static_cast<int32_t*>(temp);
   int64_t* toff = reinterpret_cast<int64_t*>(static_cast<char*>(temp) + ((size_t)nt * 4 + 15) / 16 * 16);
   void* st = toff + nt;
@@ -367,7 +434,7 @@ cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, i
   if (launches) ++*launches;
   cudaError_t e = exclusive_scan_i32(tc, toff, nt, count_dev, st, s, launches);
   if (e != cudaSuccess) return e;
-  k_pred_codes<<<(unsigned)nt, T, 0, s>>>(fa, fb, n, toff, code);
+  k_pred_codes<<<(unsigned)nt, T, 0, s>>>(fa, fb, n, toff, code, dict, minv);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -401,13 +468,16 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
   // privatized counters when the key domain fits in shared memory and there are
   // enough tuples per block to amortize the per-block flush
   const int64_t smem = K * 4;
-  if (!rowabs_g && K > 0 && smem <= 200 * 1024 && key.n >= 32 * K * kNumSMs / 4) {
+  if (!rowabs_g && K > 0 && smem <= 200 * 1024 && key.n >= 4 * K) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_probe_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    k_probe_smem<<<kNumSMs, 1024, (size_t)smem, s>>>(key, grp, kd, gd, kcode, gcode, cnt_k, (int)K);
+    int64_t blocks = key.n / std::max<int64_t>(2048, K / 2);  // tuples per block vs per-block flush of K
+    if (blocks > kNumSMs) blocks = kNumSMs;
+    if (blocks < 1) blocks = 1;
+    k_probe_smem<<<(int)blocks, 1024, (size_t)smem, s>>>(key, grp, kd, gd, kcode, gcode, cnt_k, (int)K);
     if (launches) ++*launches;
     return cudaGetLastError();
   }

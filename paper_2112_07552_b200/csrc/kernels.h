@@ -41,8 +41,11 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
                                uint8_t* flags, cudaStream_t s, int64_t* launches);
 size_t pred_temp_bytes(int64_t n);
+// codes = exclusive scan of pred(i) (-1 where false); optional dict[code] = minv + i (direct
+// group domains: the sorted value dictionary comes out of the same pass).
 cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, int32_t* code, int64_t* count_dev,
-                              unsigned long long* union_dev, void* temp, cudaStream_t s, int64_t* launches);
+                              unsigned long long* union_dev, long long* dict, long long minv, void* temp,
+                              cudaStream_t s, int64_t* launches);
 cudaError_t launch_direct_dict(const int32_t* code, int64_t range, long long minv, long long* dict, cudaStream_t s,
                                int64_t* launches);
 cudaError_t launch_gather_slots(const int32_t* tmp_code, const unsigned long long* slots, int64_t cap,

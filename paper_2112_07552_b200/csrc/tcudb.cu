@@ -164,7 +164,10 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     }
     d.code = ar.get<int32_t>((int64_t)d.span);
     void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)d.span));
-    CK(launch_pred_codes(d.fa, d.fb, (int64_t)d.span, d.code, d.count_dev, union_dev, tmp, s, launches));
+    // group domains (single column): the ascending value dictionary comes out of the same scan
+    if (!c2) d.dict = ar.get<long long>(sp);
+    CK(launch_pred_codes(d.fa, d.fb, (int64_t)d.span, d.code, d.count_dev, union_dev, d.dict, mn, tmp, s,
+                         launches));
   } else {
     if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
     d.mode = 1;
@@ -180,13 +183,14 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     }
     d.code = ar.get<int32_t>((int64_t)cap);
     void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)cap));
-    CK(launch_pred_codes(d.fa, d.fb, (int64_t)cap, d.code, d.count_dev, union_dev, tmp, s, launches));
+    CK(launch_pred_codes(d.fa, d.fb, (int64_t)cap, d.code, d.count_dev, union_dev, nullptr, 0, tmp, s, launches));
   }
 }
 
 // Phase 2 for group domains: sorted value dictionary (ascending ranks).
 void dict_finish_group(Arena& ar, Dict& d, int64_t* launches) {
   cudaStream_t s = ar.s;
+  if (d.mode == 0 && d.dict) return;  // written by the predicate scan
   d.dict = ar.get<long long>(d.count);
   if (d.count == 0) return;
   if (d.mode == 0) {
@@ -670,13 +674,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   QueryOut r;
   r.n = nnz;
   try {
-    r.g = result_alloc(ctx, (size_t)nnz * gb, s);
-    r.h = result_alloc(ctx, (size_t)nnz * hb, s);
-    r.agg = result_alloc(ctx, (size_t)nnz * 8, s);
+    // one allocation (one allocator callback) holding g | h | agg, 256-byte aligned parts
+    const size_t og = 0, oh = ((size_t)nnz * gb + 255) / 256 * 256;
+    const size_t oa = oh + ((size_t)nnz * hb + 255) / 256 * 256;
+    char* base = static_cast<char*>(result_alloc(ctx, oa + (size_t)nnz * 8, s));
+    r.g = base + og; r.h = base + oh; r.agg = base + oa;
     ca.out_g = r.g; ca.out_h = r.h; ca.out_agg = r.agg;
     CK(launch_compact_write(ca, ctmp, s, L));
   } catch (...) {
-    result_release(ctx, r.g); result_release(ctx, r.h); result_release(ctx, r.agg);
+    result_release(ctx, r.g);
     throw;
   }
   tm.mark(&S.ms_compact);
@@ -970,9 +976,7 @@ tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_
 void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r) {
   if (!ctx || !r) return;
   if (r->on_host) { tcudb_result_free_host(ctx, r); return; }
-  result_release(ctx, r->g);
-  result_release(ctx, r->h);
-  result_release(ctx, r->agg);
+  result_release(ctx, r->g);  // g is the base of the single g | h | agg allocation
   std::memset(r, 0, sizeof(*r));
 }
 
