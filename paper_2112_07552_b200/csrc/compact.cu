@@ -32,6 +32,7 @@ __device__ __forceinline__ bool nz_at(const void* base, int kind, int64_t idx) {
     case 0: return static_cast<const int*>(base)[idx] != 0;
     case 1: return static_cast<const long long*>(base)[idx] != 0;
     case 2: return static_cast<const float*>(base)[idx] != 0.f;
+    case 4: return static_cast<const unsigned short*>(base)[idx] != 0;
     default: return static_cast<const double*>(base)[idx] != 0.0;
   }
 }
@@ -60,6 +61,7 @@ template <> struct Cell<0> { using T = int;       static __device__ bool nz(T x)
 template <> struct Cell<1> { using T = long long; static __device__ bool nz(T x) { return x != 0; } };
 template <> struct Cell<2> { using T = float;     static __device__ bool nz(T x) { return x != 0.f; } };
 template <> struct Cell<3> { using T = double;    static __device__ bool nz(T x) { return x != 0.0; } };
+template <> struct Cell<4> { using T = unsigned short; static __device__ bool nz(T x) { return x != 0; } };
 
 // One warp per 256-column segment: all 8 chunk loads are issued before the
 // ballots (8 loads in flight per lane); when V is E the value comes from the
@@ -73,45 +75,60 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
   const uint32_t lt = lanemask_lt();
   const ET* __restrict__ E = static_cast<const ET*>(a.E);
   const VT* __restrict__ V = static_cast<const VT*>(a.V);
-  for (int64_t s = (int64_t)blockIdx.x * WPB + warp_id(); s < nsegs; s += (int64_t)gridDim.x * WPB) {
-    const int64_t row = s / a.nseg;
-    const int64_t col0 = (s - row * a.nseg) * a.seg_w;
-    if (col0 >= a.H) continue;
-    const int64_t lim = min(a.H, col0 + a.seg_w);
-    ET e[8];
-    VT v[8];
+  // Two segments per warp iteration: all 16 cell loads and 16 dict_h loads are in
+  // flight before the first ballot (the kernel is load-latency bound otherwise).
+  constexpr int P = 2;
+  const int64_t stride = (int64_t)gridDim.x * WPB;
+  for (int64_t s0 = (int64_t)blockIdx.x * WPB + warp_id(); s0 < nsegs; s0 += P * stride) {
+    ET e[P][8];
+    VT v[P][8];
+    long long hv[P][8];
+    int64_t row[P], col0[P], lim[P];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t col = col0 + j * 32 + lane;
-      e[j] = col < lim ? __ldcs(E + row * a.lde + col) : ET(0);
+    for (int q = 0; q < P; ++q) {
+      const int64_t s = s0 + q * stride;
+      row[q] = s < nsegs ? s / a.nseg : 0;
+      col0[q] = (s - row[q] * a.nseg) * a.seg_w;
+      lim[q] = s < nsegs ? min(a.H, col0[q] + a.seg_w) : 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t col = col0[q] + j * 32 + lane;
+        const bool in = col < lim[q];
+        e[q][j] = in ? __ldcs(E + row[q] * a.lde + col) : ET(0);
+        hv[q][j] = in ? __ldg(a.dict_h + col) : 0;
+      }
     }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const int64_t s = s0 + q * stride;
+      if (s >= nsegs || col0[q] >= a.H) continue;
     if (!SAME) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int64_t col = col0 + j * 32 + lane;
-        v[j] = (col < lim && Cell<EK>::nz(e[j])) ? __ldcs(V + row * a.ldv + col) : VT(0);
+        const int64_t col = col0[q] + j * 32 + lane;
+        v[q][j] = (col < lim[q] && Cell<EK>::nz(e[q][j])) ? __ldcs(V + row[q] * a.ldv + col) : VT(0);
       }
     }
     int64_t base = off[s];
-    const long long gval = a.dict_g[row];
+    const long long gval = a.dict_g[row[q]];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int64_t col = col0 + j * 32 + lane;
-      const bool nz = Cell<EK>::nz(e[j]);
+      const bool nz = Cell<EK>::nz(e[q][j]);
       const uint32_t m = __ballot_sync(0xffffffffu, nz);
       if (nz) {
         const int64_t pos = base + __popc(m & lt);
-        const long long hval = a.dict_h[col];
+        const long long hval = hv[q][j];
         // streaming (evict-first) stores: the result tuples are not re-read by the GPU
         if (GT == 1) __stcs(static_cast<long long*>(a.out_g) + pos, gval);
         else __stcs(static_cast<int*>(a.out_g) + pos, (int)gval);
         if (HT == 1) __stcs(static_cast<long long*>(a.out_h) + pos, hval);
         else __stcs(static_cast<int*>(a.out_h) + pos, (int)hval);
-        const VT x = SAME ? (VT)e[j] : v[j];
+        const VT x = SAME ? (VT)e[q][j] : v[q][j];
         if (VK == 2 || VK == 3) __stcs(static_cast<double*>(a.out_agg) + pos, (double)x);
         else __stcs(static_cast<long long*>(a.out_agg) + pos, (long long)x);
       }
       base += __popc(m);
+    }
     }
   }
 }
@@ -167,6 +184,7 @@ cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t 
       case 0: launch_write_t<0, 0, true>(a, off, grid, s); break;
       case 1: launch_write_t<1, 1, true>(a, off, grid, s); break;
       case 2: launch_write_t<2, 2, true>(a, off, grid, s); break;
+      case 4: launch_write_t<4, 4, true>(a, off, grid, s); break;
       default: launch_write_t<3, 3, true>(a, off, grid, s);
     }
   } else {

@@ -107,6 +107,16 @@ __device__ __forceinline__ void epilogue_chunk(const KParams& p, const uint32_t*
 #pragma unroll
       for (int i = 0; i < W; ++i) nzc += (r[i] & m) != 0u;
     }
+  } else if (p.epi == EPI_STORE16) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + col);
+#pragma unroll
+    for (int i = 0; i < W / 8; ++i)
+      dst[i] = make_uint4(r[8 * i] | (r[8 * i + 1] << 16), r[8 * i + 2] | (r[8 * i + 3] << 16),
+                          r[8 * i + 4] | (r[8 * i + 5] << 16), r[8 * i + 6] | (r[8 * i + 7] << 16));
+    if (p.cnt_out) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) nzc += r[i] != 0u;
+    }
   } else if (p.epi == EPI_SET64 || p.epi == EPI_ACC64) {
     longlong2* d2 = reinterpret_cast<longlong2*>(reinterpret_cast<long long*>(p.C) + row * p.ldc + col);
 #pragma unroll
@@ -450,7 +460,8 @@ bool make_map(CUtensorMap* m, const void* base, int elem, int64_t rows, int64_t 
 cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   constexpr int BNF = kGemmBNFp4;
   if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
-  if (a.M % BM || a.k_len % BKB || a.k_begin % BKB || a.lda % 16 || a.ldb % 16 || a.epi != EPI_STORE32)
+  if (a.M % BM || a.k_len % BKB || a.k_begin % BKB || a.lda % 16 || a.ldb % 16 ||
+      (a.epi != EPI_STORE32 && a.epi != EPI_STORE16))
     return cudaErrorInvalidValue;
   const int64_t tiles_n = (a.N + BNF - 1) / BNF;
   if (a.ldc < tiles_n * BNF) return cudaErrorInvalidValue;

@@ -13,7 +13,8 @@ enum GemmEpi {
   EPI_STORE32 = 0,  // C32[r][c] = acc (int32 or fp32 bits)
   EPI_SET64 = 1,    // C64[r][c] = (int64)acc << shift
   EPI_ACC64 = 2,    // C64[r][c] += (int64)acc << shift
-  EPI_TRI = 3       // *tri_out += sum acc[r][c] * mask[r][c]   (triangle epilogue, a9)
+  EPI_TRI = 3,      // *tri_out += sum acc[r][c] * mask[r][c]   (triangle epilogue, a9)
+  EPI_STORE16 = 4   // C16[r][c] = (uint16)acc — COUNT results the guard proved < 2^16 (fp4 path)
 };
 constexpr int kGemmBM = 128;
 constexpr int kGemmBN = 256;

@@ -136,7 +136,7 @@ struct CompactArgs {
   int64_t G, H;
   int64_t nseg;                                  // segments per row (= GEMM N tiles on the dense path)
   int64_t seg_w;                                 // columns per segment (<= 256; 256, or 240 for fp4)
-  const void* E; int e_kind; int64_t lde;       // e_kind: 0 int32, 1 int64, 2 f32, 3 f64
+  const void* E; int e_kind; int64_t lde;       // e_kind: 0 int32, 1 int64, 2 f32, 3 f64, 4 u16
   const void* V; int v_kind; int64_t ldv;       // value matrix (agg), same kinds
   const long long* dict_g; const long long* dict_h;
   int g_out_type, h_out_type;                    // 0 I32, 1 I64

@@ -551,13 +551,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     int32_t* value_cnt = need_exist ? nullptr : seg_cnt;
     if (op4A) {
       const int64_t Hc = ca.nseg * kGemmBNFp4;
-      int32_t* C = ar.get<int32_t>(Gp * Hc);
+      // 0/1 cells: every count <= K; below 2^16 the epilogue stores u16 (halves C traffic)
+      const bool c16 = K < 65536;
+      void* C = c16 ? (void*)ar.get<uint16_t>(Gp * Hc) : (void*)ar.get<int32_t>(Gp * Hc);
       ga.elem = ELEM_FP4; ga.A = op4A; ga.lda = Kp4 / 2; ga.B = op4B; ga.ldb = Kp4 / 2;
-      ga.k_begin = 0; ga.k_len = Kp4 / 2; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hc;
+      ga.k_begin = 0; ga.k_len = Kp4 / 2; ga.epi = c16 ? EPI_STORE16 : EPI_STORE32; ga.C = C; ga.ldc = Hc;
       ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
       CK(launch_gemm(ga, s, L));
       ops += 2.0 * Gp * Hc * Kp4;
-      ca.E = C; ca.e_kind = 0; ca.lde = Hc; ca.V = C; ca.v_kind = 0; ca.ldv = Hc;
+      ca.E = C; ca.e_kind = c16 ? 4 : 0; ca.lde = Hc; ca.V = C; ca.v_kind = ca.e_kind; ca.ldv = Hc;
       S.elem = 3;
     } else if (is_float) {
       float* C = ar.get<float>(Gp * Hp);
