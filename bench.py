@@ -65,6 +65,8 @@ class ClockSampler:
         self.p = None
 
     def __enter__(self):
+        if os.environ.get("TCUDB_BENCH_NO_CLOCKS") == "1":  # diagnosis: no sampler process
+            return self
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -179,6 +181,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the multi-GPU row-sharded path even on one rank (NCCL group of 1; test hook)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -187,7 +191,8 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    sharded = ws > 1 or args.force_shard
+    if sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     from paper_2112_07552_b200 import Engine
@@ -198,7 +203,7 @@ def main():
     eng = Engine(local)
     stream = torch.cuda.current_stream(dev)
     to_dev = lambda T: {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in T.items() if v is not None}
-    if ws == 1:
+    if not sharded:
         dA, dB = to_dev(A), to_dev(B)
         step = lambda: eng.join_agg(dA, dB, agg, with_stats=True)
     else:
@@ -215,7 +220,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     gemm_ms, stats_last = [], None
     with ClockSampler(local) as clk:
-        if ws > 1:
+        if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
@@ -227,20 +232,47 @@ def main():
             stats_last = st
             del out
         torch.cuda.synchronize()
-        if ws > 1:
+        if sharded:
             torch.distributed.barrier()
     launches = eng.launch_count - launches0
     step_ms = [s.elapsed_time(e) for s, e in ev]
     total_ms = sum(step_ms)
-    if ws > 1:
+    if sharded:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     clocks = clk.summary()
 
-    # ---- e2e: host (pinned) columns -> query through the C ABI host entry -> host result tuples
+    # ---- e2e: host (pinned) columns -> query through the public API -> host result tuples
     e2e = None
-    if ws == 1 and args.e2e_steps > 0:
+    if sharded and args.e2e_steps > 0:
+        # each rank: its pinned host slices -> device -> sharded query -> full result -> pinned host
+        hA = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in sA.items() if v is not None}
+        hB = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in sB.items() if v is not None}
+        h2d = sum(v.numel() * v.element_size() for v in list(hA.values()) + list(hB.values()))
+
+        def e2e_step():
+            gA = {k: v.to(dev, non_blocking=True) for k, v in hA.items()}
+            gB = {k: v.to(dev, non_blocking=True) for k, v in hB.items()}
+            r = shard_mod.sharded_join_agg(eng, gA, gB, agg)
+            return {k: v.to("cpu") for k, v in r.items()}
+        r = e2e_step()
+        d2h = sum(v.numel() * v.element_size() for v in r.values())
+        del r
+        ts = []
+        for _ in range(args.e2e_steps):
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = e2e_step()
+            ts.append(time.perf_counter() - t0)
+            del r
+        tmax = torch.tensor([statistics.mean(ts)], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": n_tuples / float(tmax.item()), "unit": "tuples/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(tmax.item()) * 1e3,
+               "note": "per rank: pinned host slices H2D, sharded query (NCCL exchange), full result D2H; max over ranks"}
+    if not sharded and args.e2e_steps > 0:
         pin = lambda T: {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy()
                          for k, v in T.items() if v is not None}
         hA, hB = pin(A), pin(B)
@@ -260,6 +292,8 @@ def main():
                "note": "tcudb_join_agg_host: pinned host columns in, pinned host result tuples out"}
 
     if rank != 0:
+        if sharded:
+            torch.distributed.destroy_process_group()
         return 0
     peaks = measured_peaks()
     st = stats_last
@@ -291,7 +325,7 @@ def main():
         roof = {"bound": "hbm", "kernel": "k_expand", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None}
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:  # the CPU baseline runs on rank 0 at N=1 only
         import oracle
         cores = len(os.sched_getaffinity(0))
         sample, A_s, frac = bounded_sample(args.config, A)
@@ -309,14 +343,16 @@ def main():
         "config": {"workload": WORKLOADS[args.config], "n_A": len(A["k"]), "n_B": len(B["k"]),
                    "G": st["G"], "H": st["H"], "K": st["K"], "join_pairs": st["join_pairs"],
                    "result_groups": st["n_result"], "path": "dense" if st["path"] == 0 else "sparse",
-                   "parallelism": f"row-shard x{ws}" if ws > 1 else "single GPU",
+                   "parallelism": f"row-shard x{ws} (A routed by g range, B allgathered, results allgathered; "
+                                  f"G/H/K/stage_ms are rank 0's local query)" if sharded else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps"},
         "stage_ms": {k: st[k] for k in ("ms_stats", "ms_encode", "ms_fill", "ms_gemm", "ms_sparse", "ms_compact")},
+        "step_ms": [round(x, 4) for x in step_ms],
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
         "context": PAPER_CONTEXT,
     }
     print(json.dumps(line))
-    if ws > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
     return 0
 

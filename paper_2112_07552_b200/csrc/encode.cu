@@ -84,6 +84,28 @@ __global__ void k_init_stats(ColStats* st, int n) {
   if (i < n) { st[i].mn = LLONG_MAX; st[i].mx = LLONG_MIN; st[i].min_abs = LLONG_MAX; st[i].flags = 0; }
 }
 
+// ------------------------------------------------------------------ #distinct sketch
+// PAPER.md §4.2.1 keeps "the number of distinct values" per column as
+// metadata. For hash-mode domains it is estimated on the device with a HyperLogLog
+// sketch (2^13 registers, ~1.2 % standard error) so the hash table is sized by the
+// distinct count (L2-resident when small) instead of by the tuple count.
+__global__ void __launch_bounds__(1024) k_hll(ColDesc c, unsigned* __restrict__ regs) {
+  __shared__ unsigned s_reg[kHllM];
+  for (int i = threadIdx.x; i < kHllM; i += blockDim.x) s_reg[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += stride) {
+    const unsigned long long h = fmix64((unsigned long long)ld_int(c.data, c.type, i) * 0x9E3779B97F4A7C15ull + 1);
+    const unsigned idx = (unsigned)(h >> (64 - kHllP));
+    const unsigned long long w = h << kHllP;
+    const unsigned rho = w ? (unsigned)__clzll(w) + 1u : (unsigned)(64 - kHllP + 1);
+    if (rho > s_reg[idx]) atomicMax(&s_reg[idx], rho);  // most updates stop at the read
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHllM; i += blockDim.x)
+    if (s_reg[i]) atomicMax(regs + i, s_reg[i]);
+}
+
 // ------------------------------------------------------------------ direct-offset dictionary
 __global__ void k_mark_direct(ColDesc c, long long minv, uint8_t* __restrict__ flags) {
   const int64_t stride = (int64_t)gridDim.x * T;
@@ -111,7 +133,7 @@ __global__ void __launch_bounds__(1024) k_mark_direct_smem(ColDesc c, long long 
 // Slot key = (x - min) as u64; EMPTY = ~0. Linear probing; equal keys in a warp
 // are inserted once (warp aggregation). flags[slot] = 1 marks the side.
 __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __restrict__ slots,
-                              unsigned long long mask, uint8_t* __restrict__ flags) {
+                              unsigned long long mask, uint8_t* __restrict__ flags, int* __restrict__ overflow) {
   const int64_t stride = (int64_t)gridDim.x * T;
   const int64_t n_round = (c.n + 31) & ~int64_t(31);
   for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_round; i += stride) {
@@ -122,11 +144,18 @@ __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __r
     const unsigned peers = __match_any_sync(0xffffffffu, off) & act;
     if (!ok || (__ffs(peers) - 1) != lane_id()) continue;  // lowest active peer lane inserts
     unsigned long long h = fmix64(off) & mask;
-    while (true) {
-      const unsigned long long prev = atomicCAS(slots + h, ~0ull, off);
-      if (prev == ~0ull || prev == off) break;
+    bool placed = false;
+    for (unsigned long long step = 0; step <= mask; ++step) {  // bounded: a full table is reported
+      // plain read first: a key already present (the common case for hot keys) costs no atomic
+      const unsigned long long cur = __ldcg(slots + h);
+      if (cur == off) { placed = true; break; }
+      if (cur == ~0ull) {
+        const unsigned long long prev = atomicCAS(slots + h, ~0ull, off);
+        if (prev == ~0ull || prev == off) { placed = true; break; }
+      }
       h = (h + 1) & mask;
     }
+    if (!placed) { *overflow = 1; continue; }
     if (!flags[h]) flags[h] = 1;
   }
 }
@@ -379,6 +408,15 @@ cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, 
   return cudaGetLastError();
 }
 
+cudaError_t launch_hll(const ColDesc& c, unsigned* regs, cudaStream_t s, int64_t* launches) {
+  if (c.n <= 0) return cudaSuccess;
+  int64_t blocks = (c.n + 16 * 1024 - 1) / (16 * 1024);
+  if (blocks > kNumSMs) blocks = kNumSMs;
+  k_hll<<<(int)blocks, 1024, 0, s>>>(c, regs);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
                                int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
@@ -405,9 +443,9 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 }
 
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, cudaStream_t s, int64_t* launches) {
+                               uint8_t* flags, int* overflow, cudaStream_t s, int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
-  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags);
+  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags, overflow);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

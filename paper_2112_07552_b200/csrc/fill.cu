@@ -78,6 +78,37 @@ __global__ void k_fill_count_fp4(const int32_t* __restrict__ kcode, const int32_
   if (lane_id() == 0 && dup) atomicOr(&fs->overflow, 1);
 }
 
+// Float SUM, optimistic direct fill: when every (row, k) cell holds at most one
+// tuple and every value is bf16-exact, the cell IS the bf16 of the value — no fp32
+// scratch, no atomics on values, no pack pass (c4: one tuple per cell). A 1-bit
+// occupancy map (atomicOr) detects a second tuple in a cell (fs->overflow) and a
+// value with nonzero low 16 bits is reported inexact (fs->inexact); either sends the
+// guard to the fp32-scratch path.
+__global__ void k_fill_bf16_direct(const int32_t* __restrict__ kcode, const int32_t* __restrict__ rcode,
+                                   const float* __restrict__ val, int64_t n, uint16_t* __restrict__ op,
+                                   int64_t ld_op, unsigned* __restrict__ occ, int64_t ld_occ,
+                                   FillStats* __restrict__ fs) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  int dup = 0, inexact = 0;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t kc = kcode[i];
+    if (kc < 0) continue;
+    const int64_t r = rcode[i];
+    const uint32_t b = val ? __float_as_uint(__ldg(val + i)) : 0x3F800000u;  // absent value = 1.0
+    inexact |= (b & 0xFFFFu) != 0u;
+    const int64_t bit = r * ld_occ + kc;
+    const unsigned old = atomicOr(occ + (bit >> 5), 1u << (bit & 31));
+    dup |= (old >> (bit & 31)) & 1u;
+    op[r * ld_op + kc] = (uint16_t)(b >> 16);
+  }
+  dup = __any_sync(0xffffffffu, dup);
+  inexact = __any_sync(0xffffffffu, inexact);
+  if (lane_id() == 0) {
+    if (dup) atomicOr(&fs->overflow, 1);
+    if (inexact) atomicOr(&fs->inexact, 1);
+  }
+}
+
 // Wide integer fill into int64 scratch (COUNT: +1, SUM: +v), wrapping adds.
 __global__ void k_fill_i64(const int32_t* __restrict__ kcode, const int32_t* __restrict__ rcode, ColDesc val,
                            int64_t n, unsigned long long* __restrict__ scr, int64_t ld) {
@@ -214,6 +245,16 @@ cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int
                                  FillStats* fs, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
   k_fill_count_u8<<<grid_for(n), T, 0, s>>>(kcode, rcode, n, op, ld, fs);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                    uint16_t* op, int64_t ld_op, unsigned* occ, int64_t ld_occ, FillStats* fs,
+                                    cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_fill_bf16_direct<<<grid_for(n), T, 0, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, op, ld_op,
+                                               occ, ld_occ, fs);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

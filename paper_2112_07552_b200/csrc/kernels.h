@@ -35,11 +35,15 @@ struct DictView {
 };
 
 // ---------------------------------------------------------------- encode.cu
+constexpr int kHllP = 13, kHllM = 1 << kHllP;  // HyperLogLog registers per sketch
+// max-merge the sketch of one int column into regs[kHllM] (regs zeroed by the caller)
+cudaError_t launch_hll(const ColDesc& c, unsigned* regs, cudaStream_t s, int64_t* launches);
 cudaError_t launch_col_stats(const ColDesc* cols6, ColStats* st, cudaStream_t s, int64_t* launches);
 cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
                                int64_t* launches);
+// Warp-aggregated open-addressing insert of (x - minv); *overflow = 1 if the table is full.
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, cudaStream_t s, int64_t* launches);
+                               uint8_t* flags, int* overflow, cudaStream_t s, int64_t* launches);
 size_t pred_temp_bytes(int64_t n);
 // codes = exclusive scan of pred(i) (-1 where false); optional dict[code] = minv + i (direct
 // group domains: the sorted value dictionary comes out of the same pass).
@@ -77,6 +81,12 @@ cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int
 // cell sets fs->overflow (the guard then uses the u8 path).
 cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,
                                   int64_t ld_elems, FillStats* fs, cudaStream_t s, int64_t* launches);
+// Float SUM with <= 1 tuple per cell and bf16-exact values: bf16 bits stored straight into
+// op[r][k]; occ is a zeroed 1-bit occupancy map [rows][ld_occ bits]; violations set
+// fs->overflow (second tuple in a cell) / fs->inexact (value not bf16-exact).
+cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                    uint16_t* op, int64_t ld_op, unsigned* occ, int64_t ld_occ, FillStats* fs,
+                                    cudaStream_t s, int64_t* launches);
 // Pattern plane op[r][k] = 1 where a cell holds >= 1 tuple; symmetric adjacency for triangles.
 cudaError_t launch_fill_pattern_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
                                    cudaStream_t s, int64_t* launches);
@@ -107,6 +117,11 @@ cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const
                                cudaStream_t s, int64_t* launches);
 cudaError_t launch_work(const int32_t* kcode, int64_t n, const int32_t* cnt_b, int32_t* work, cudaStream_t s,
                         int64_t* launches);
+// Active A tuples grouped by row g (counting sort): act_a[]/act_w[] (zeroed act_w tail),
+// gcnt (zeroed, G), goff (G), gcur (zeroed, G) are scratch.
+cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const int32_t* cnt_b, int64_t n, int G,
+                               int32_t* gcnt, int64_t* goff, int32_t* gcur, int32_t* act_a, int32_t* act_w,
+                               void* scan_tmp, cudaStream_t s, int64_t* launches);
 cudaError_t launch_flags_from_work(const int32_t* work, int64_t n, int32_t* flags, cudaStream_t s,
                                    int64_t* launches);
 cudaError_t launch_compact_active(const int32_t* work, const int64_t* pos, int64_t n, int32_t* act_a,
@@ -117,9 +132,10 @@ struct ExpandArgs {
   const int32_t* kcodeA; const int32_t* gcodeA; ColDesc va;
   const int64_t* bstart; const int32_t* b_h; const void* b_w;
   int w_kind;      // 0 none (1), 1 int64, 2 f32
-  int acc_kind;    // 0 COUNT int32, 1 COUNT int64, 2 int SUM int64, 3 float SUM f64
+  int acc_kind;    // 0 COUNT int32, 1 COUNT int64, 2 int SUM int64, 3 float SUM f64, 4 COUNT u16
   void* C; int64_t ldc;
   int32_t* cnt;    // optional existence count plane (int32) or NULL
+  int* ovf;        // acc_kind 4 (COUNT, packed u16, ldc even): set when a count passes 65535
 };
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s, int64_t* launches);
 

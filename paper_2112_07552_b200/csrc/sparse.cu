@@ -66,6 +66,48 @@ __global__ void k_compact_active(const int32_t* __restrict__ work, const int64_t
   }
 }
 
+// Active A tuples (kcode >= 0 and cntB(kcode) > 0) grouped by their row g (a counting
+// sort): consecutive updates of the expand then land in a narrow window of C rows,
+// which stays L2-resident instead of scattering atomics over the whole matrix.
+__global__ void __launch_bounds__(1024) k_active_g_count(const int32_t* __restrict__ kcode,
+                                                         const int32_t* __restrict__ gcode,
+                                                         const int32_t* __restrict__ cnt_b, int64_t n, int G,
+                                                         int32_t* __restrict__ gcnt, int use_smem) {
+  extern __shared__ int32_t s_cnt[];
+  if (use_smem) {
+    for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t kc = kcode[i];
+    if (kc < 0 || cnt_b[kc] == 0) continue;
+    atomicAdd((use_smem ? s_cnt : gcnt) + gcode[i], 1);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < G; i += blockDim.x)
+      if (s_cnt[i]) atomicAdd(gcnt + i, s_cnt[i]);
+  }
+}
+
+__global__ void k_active_g_scatter(const int32_t* __restrict__ kcode, const int32_t* __restrict__ gcode,
+                                   const int32_t* __restrict__ cnt_b, int64_t n, const int64_t* __restrict__ goff,
+                                   int32_t* __restrict__ gcur, int32_t* __restrict__ act_a,
+                                   int32_t* __restrict__ act_w) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t kc = kcode[i];
+    if (kc < 0) continue;
+    const int32_t w = cnt_b[kc];
+    if (w == 0) continue;
+    const int32_t g = gcode[i];
+    const int64_t pos = goff[g] + atomicAdd(gcur + g, 1);
+    act_a[pos] = (int32_t)i;
+    act_w[pos] = w;
+  }
+}
+
 __global__ void k_flags_from_work(const int32_t* __restrict__ work, int64_t n, int32_t* __restrict__ flags) {
   const int64_t stride = (int64_t)gridDim.x * T;
   for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) flags[i] = work[i] > 0;
@@ -115,6 +157,12 @@ __global__ void __launch_bounds__(T) k_expand(const ExpandArgs a) {
     const int32_t h = a.b_h[pos];
     const int64_t cell = (int64_t)g * a.ldc + h;
     switch (a.acc_kind) {
+      case 4: {  // COUNT in packed u16 pairs; a carry out of a half is detected from the return value
+        const int sh = 16 * (int)(cell & 1);
+        const unsigned old = atomicAdd(static_cast<unsigned*>(a.C) + (cell >> 1), 1u << sh);
+        if (((old >> sh) & 0xFFFFu) == 0xFFFFu) *a.ovf = 1;
+        break;
+      }
       case 0: atomicAdd(static_cast<int*>(a.C) + cell, 1); break;
       case 1: atomicAdd(static_cast<unsigned long long*>(a.C) + cell, 1ull); break;
       case 2: {
@@ -140,6 +188,28 @@ cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const
                                cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
   k_bucket_fill<<<grid_for(n), T, 0, s>>>(kcode, hcode, w, n, bstart, cursor, b_h, b_w, w_kind);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const int32_t* cnt_b, int64_t n, int G,
+                               int32_t* gcnt, int64_t* goff, int32_t* gcur, int32_t* act_a, int32_t* act_w,
+                               void* scan_tmp, cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  const bool smem = (int64_t)G * 4 <= 160 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_active_g_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  int64_t blocks = n / std::max<int64_t>(4096, G / 2);
+  if (blocks > kNumSMs) blocks = kNumSMs;
+  if (blocks < 1) blocks = 1;
+  k_active_g_count<<<(int)blocks, 1024, smem ? (size_t)G * 4 : 0, s>>>(kcode, gcode, cnt_b, n, G, gcnt, smem);
+  if (launches) ++*launches;
+  cudaError_t e = exclusive_scan_i32(gcnt, goff, G, nullptr, scan_tmp, s, launches);
+  if (e != cudaSuccess) return e;
+  k_active_g_scatter<<<grid_for(n), T, 0, s>>>(kcode, gcode, cnt_b, n, goff, gcur, act_a, act_w);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -37,7 +37,8 @@ struct tcudb_ctx {
   std::string err;
   bool sticky = false;
   int64_t launches = 0;
-  void* pinned = nullptr;  // small D2H staging
+  void* pinned = nullptr;      // small D2H staging
+  void* pinned_big = nullptr;  // sketch registers (3 x kHllM x 4 B)
   cudaEvent_t ev[8] = {};
   std::mutex mu;
   // pinned host block cache for host-API results: size -> free blocks
@@ -119,6 +120,7 @@ struct Dict {
   int64_t* count_dev = nullptr;
   int64_t count = 0;
   int bits = 64;              // significant bits of (x - min) for the radix sort
+  int* ovf = nullptr;         // hash mode: table-full flag (the estimate was too small)
   DictView view() const {
     DictView v;
     v.mode = mode;
@@ -136,10 +138,29 @@ unsigned long long next_pow2(unsigned long long x) {
   return p;
 }
 
+// Direct-offset dictionary when the value span is small relative to the tuples.
+bool dict_is_direct(int64_t n, long long mn, long long mx) {
+  const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
+  const unsigned __int128 direct_cap = (unsigned __int128)std::max<int64_t>(4 * n, 1 << 16);
+  return span <= direct_cap && span < ((unsigned __int128)1 << 31);
+}
+
+// HyperLogLog estimate from kHllM registers (bias-corrected, linear counting for small n).
+double hll_estimate(const unsigned* r) {
+  const double m = kHllM, alpha = 0.7213 / (1.0 + 1.079 / m);
+  double z = 0;
+  int zeros = 0;
+  for (int i = 0; i < kHllM; ++i) { z += std::ldexp(1.0, -(int)r[i]); zeros += r[i] == 0; }
+  const double e = alpha * m * m / z;
+  if (e <= 2.5 * m && zeros > 0) return m * std::log(m / zeros);
+  return e;
+}
+
 // Build phase 1 of a dictionary over one or two columns (marks + codes / compaction).
-// two_sided: K domain, code only keys present on both sides (∩). union_only: vertex domain.
+// intersect: K domain, code only keys present on both sides (∩); otherwise the union.
+// est_distinct (> 0) sizes the hash table: 2^ceil(log2(2.2 x estimate)), never above 2n.
 void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long long mn, long long mx, bool intersect,
-                unsigned long long* union_dev, int64_t* launches) {
+                unsigned long long* union_dev, int64_t* launches, double est_distinct = 0) {
   cudaStream_t s = ar.s;
   const int64_t n = c1.n + (c2 ? c2->n : 0);
   const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
@@ -151,8 +172,7 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     while (b < 64 && (sm1 >> b)) b += 8;
     d.bits = b;
   }
-  const unsigned __int128 direct_cap = (unsigned __int128)std::max<int64_t>(4 * n, 1 << 16);
-  if (span <= direct_cap && span < ((unsigned __int128)1 << 31)) {
+  if (dict_is_direct(n, mn, mx)) {
     d.mode = 0;
     d.span = (unsigned long long)span;
     d.fa = ar.zeros<uint8_t>((int64_t)d.span);
@@ -171,15 +191,22 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
   } else {
     if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
     d.mode = 1;
-    const unsigned long long cap = next_pow2((unsigned long long)(2 * n));
+    unsigned long long want = (unsigned long long)(2 * n);
+    if (est_distinct > 0) want = std::min(want, (unsigned long long)(2.2 * est_distinct) + 64);
+    const unsigned long long cap = next_pow2(want);
     d.span = cap;
     d.slots = ar.get<unsigned long long>((int64_t)cap);
     CK(cudaMemsetAsync(d.slots, 0xFF, cap * sizeof(unsigned long long), s));
     d.fa = ar.zeros<uint8_t>((int64_t)cap);
-    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, s, launches));
+    d.ovf = ar.zeros<int>(1);
+    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, s, launches));
     if (c2) {
-      if (intersect) { d.fb = ar.zeros<uint8_t>((int64_t)cap); CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, s, launches)); }
-      else CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, s, launches));
+      if (intersect) {
+        d.fb = ar.zeros<uint8_t>((int64_t)cap);
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, s, launches));
+      } else {
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, s, launches));
+      }
     }
     d.code = ar.get<int32_t>((int64_t)cap);
     void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)cap));
@@ -311,20 +338,51 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
 
   // ---------------- a2: dictionaries
   const long long kmin = std::min(hs[0].mn, hs[1].mn), kmax = std::max(hs[0].mx, hs[1].mx);
+  // #distinct metadata for the hash-mode domains: HyperLogLog sketches
+  double est[3] = {0, 0, 0};
+  {
+    // (small inputs size their tables by the tuple count: the sketch pass would cost more)
+    constexpr int64_t kSketchMin = 1 << 20;
+    const bool hk = nA + nB >= kSketchMin && !dict_is_direct(nA + nB, kmin, kmax);
+    const bool hg = nA >= kSketchMin && !dict_is_direct(nA, hs[2].mn, hs[2].mx);
+    const bool hh = nB >= kSketchMin && !dict_is_direct(nB, hs[3].mn, hs[3].mx);
+    if (hk || hg || hh) {
+      unsigned* regs = ar.zeros<unsigned>(3 * kHllM);
+      if (hk) { CK(launch_hll(ak, regs, s, L)); CK(launch_hll(bk, regs, s, L)); }  // union sketch
+      if (hg) CK(launch_hll(ag, regs + kHllM, s, L));
+      if (hh) CK(launch_hll(bh, regs + 2 * kHllM, s, L));
+      CK(cudaMemcpyAsync(ctx->pinned_big, regs, sizeof(unsigned) * 3 * kHllM, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const unsigned* hr = static_cast<const unsigned*>(ctx->pinned_big);
+      if (hk) est[0] = hll_estimate(hr);
+      if (hg) est[1] = hll_estimate(hr + kHllM);
+      if (hh) est[2] = hll_estimate(hr + 2 * kHllM);
+    }
+  }
   unsigned long long* d_union = ar.zeros<unsigned long long>(1);
   Dict DK, DG, DH;
-  dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L);
-  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L);
-  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L);
-  {
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0]);
+    dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
+    dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2]);
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
+    int* hov = reinterpret_cast<int*>(hp + 4);
+    hov[0] = hov[1] = hov[2] = 0;
     CK(cudaMemcpyAsync(hp + 0, DK.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 1, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 2, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 3, d_union, 8, cudaMemcpyDeviceToHost, s));
+    if (DK.ovf) CK(cudaMemcpyAsync(hov + 0, DK.ovf, 4, cudaMemcpyDeviceToHost, s));
+    if (DG.ovf) CK(cudaMemcpyAsync(hov + 1, DG.ovf, 4, cudaMemcpyDeviceToHost, s));
+    if (DH.ovf) CK(cudaMemcpyAsync(hov + 2, DH.ovf, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     DK.count = hp[0]; DG.count = hp[1]; DH.count = hp[2];
     S.K_union = hp[3];
+    if (!hov[0] && !hov[1] && !hov[2]) break;
+    // an estimate was far too small (table full): rebuild sized by the tuple counts
+    est[0] = est[1] = est[2] = 0;
+    CK(cudaMemsetAsync(d_union, 0, 8, s));
+    DK = Dict(); DG = Dict(); DH = Dict();
   }
   const int64_t K = DK.count, G = DG.count, H = DH.count;
   S.K = K; S.G = G; S.H = H;
@@ -428,6 +486,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   // result matrices for compaction
   CompactArgs ca{};
   int32_t* seg_cnt = nullptr;  // per-segment counts from the GEMM epilogue (dense path)
+  ExpandArgs sparse_u16{};     // sparse COUNT in u16 cells (kept to redo in int32 on overflow)
+  sparse_u16.acc_kind = -1;
   ca.G = G; ca.H = H;
   ca.dict_g = DG.dict; ca.dict_h = DH.dict;
   ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
@@ -504,14 +564,36 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       CK(launch_pack_planes(scrB, cellsB, PB, sB, opB, cellsB, s, L));
       S.planes_a = PA; S.planes_b = PB;
     }
+    bool bf16_direct = false;
+    uint16_t *fA = nullptr, *fB = nullptr;
     if (is_float) {
       ldop = 3 * Kp;
+      fA = ar.get<uint16_t>(Gp * ldop);
+      fB = ar.get<uint16_t>(Hp * ldop);
+      if (nA <= cellsA && nB <= cellsB) {
+        // optimistic: <= 1 tuple per cell and bf16-exact values -> the cells are the values
+        CK(cudaMemset2DAsync(fA, ldop * 2, 0, Kp * 2, Gp, s));
+        CK(cudaMemset2DAsync(fB, ldop * 2, 0, Kp * 2, Hp, s));
+        unsigned* occA = ar.zeros<unsigned>(cellsA / 32 + 1);
+        unsigned* occB = ar.zeros<unsigned>(cellsB / 32 + 1);
+        CK(launch_fill_bf16_direct(kA, gA, av, nA, fA, ldop, occA, Kp, fs + 0, s, L));
+        CK(launch_fill_bf16_direct(kB, hB, bw, nB, fB, ldop, occB, Kp, fs + 1, s, L));
+        CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        FillStats hf[2];
+        std::memcpy(hf, ctx->pinned, sizeof(hf));
+        bf16_direct = !(hf[0].overflow | hf[1].overflow | hf[0].inexact | hf[1].inexact);
+        if (!bf16_direct) CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
+      }
+    }
+    if (is_float && bf16_direct) {
+      opA = reinterpret_cast<uint8_t*>(fA);
+      opB = reinterpret_cast<uint8_t*>(fB);
+    } else if (is_float) {
       float* scrA = ar.zeros<float>(cellsA);
       float* scrB = ar.zeros<float>(cellsB);
       CK(launch_fill_f32(kA, gA, av, nA, scrA, Kp, s, L));
       CK(launch_fill_f32(kB, hB, bw, nB, scrB, Kp, s, L));
-      uint16_t* fA = ar.get<uint16_t>(Gp * ldop);
-      uint16_t* fB = ar.get<uint16_t>(Hp * ldop);
       CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 0, -1, fs + 0, s, L));
       CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 0, -1, fs + 1, s, L));
       CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
@@ -634,15 +716,27 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       b_w = is_float ? (void*)ar.get<float>(nB) : (void*)ar.get<long long>(nB);
     }
     CK(launch_bucket_fill(kB, hB, bw, nB, bstart, cursor, b_h, b_w, w_kind, s, L));
-    int32_t* work = ar.get<int32_t>(nA);
-    int32_t* flg = ar.get<int32_t>(nA);
-    int64_t* pos = ar.get<int64_t>(nA);
-    CK(launch_work(kA, nA, cntB, work, s, L));
-    CK(launch_flags_from_work(work, nA, flg, s, L));
-    CK(exclusive_scan_i32(flg, pos, nA, nullptr, tmp, s, L));
     int32_t* act_a = ar.get<int32_t>(nA);
     int32_t* act_w = ar.zeros<int32_t>(nA);
-    CK(launch_compact_active(work, pos, nA, act_a, act_w, s, L));
+    const int64_t ldc_ = round_up(H, 4);
+    const bool big_c = (double)G * ldc_ * csz > 64e6;
+    if (big_c) {
+      // C far larger than L2: active A tuples in row (g) order, so the expand's atomics walk
+      // C row by row and stay L2-local
+      int32_t* gcnt = ar.zeros<int32_t>(G);
+      int32_t* gcur = ar.zeros<int32_t>(G);
+      int64_t* goff = ar.get<int64_t>(G);
+      CK(launch_active_by_g(kA, gA, cntB, nA, (int)G, gcnt, goff, gcur, act_a, act_w, tmp, s, L));
+    } else {
+      // C fits in L2: keep the input order (atomics spread over all of C, no hot rows)
+      int32_t* work = ar.get<int32_t>(nA);
+      int32_t* flg = ar.get<int32_t>(nA);
+      int64_t* pos = ar.get<int64_t>(nA);
+      CK(launch_work(kA, nA, cntB, work, s, L));
+      CK(launch_flags_from_work(work, nA, flg, s, L));
+      CK(exclusive_scan_i32(flg, pos, nA, nullptr, tmp, s, L));
+      CK(launch_compact_active(work, pos, nA, act_a, act_w, s, L));
+    }
     int64_t* act_off = ar.get<int64_t>(nA);
     CK(exclusive_scan_i32(act_w, act_off, nA, nullptr, tmp, s, L));
     const int64_t ldc = round_up(H, 4);
@@ -650,7 +744,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     ea.n_act = nA; ea.J = (int64_t)J;
     ea.act_a = act_a; ea.act_off = act_off; ea.kcodeA = kA; ea.gcodeA = gA; ea.va = av;
     ea.bstart = bstart; ea.b_h = b_h; ea.b_w = b_w; ea.w_kind = w_kind; ea.ldc = ldc;
-    if (!is_sum) {
+    if (!is_sum && big_c) {
+      // COUNT in packed u16 cells (half the bytes of a C far larger than L2); the carry check
+      // needs the atomic's return value, so it is only used here; a count passing 65535 is
+      // detected and the expand is redone in int32 below
+      ea.acc_kind = 4; ea.C = ar.zeros<uint16_t>(G * ldc); ea.ovf = ar.zeros<int>(1); ca.e_kind = 4;
+      ca.E = ea.C; ca.V = ea.C; ca.v_kind = ca.e_kind;
+      sparse_u16 = ea;
+    } else if (!is_sum) {
+      // L2-resident C: fire-and-forget 32-bit reductions
       if (J < (1ull << 31)) { ea.acc_kind = 0; ea.C = ar.zeros<int32_t>(G * ldc); ca.e_kind = 0; }
       else { ea.acc_kind = 1; ea.C = ar.zeros<long long>(G * ldc); ca.e_kind = 1; }
       ca.E = ea.C; ca.V = ea.C; ca.v_kind = ca.e_kind;
@@ -671,7 +773,27 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
   int64_t* d_nnz = ar.get<int64_t>(1);
   CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
-  const int64_t nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+  int64_t nnz;
+  {
+    int64_t* hp = static_cast<int64_t*>(ctx->pinned);
+    int* hov = reinterpret_cast<int*>(hp + 1);
+    *hov = 0;
+    CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
+    if (sparse_u16.acc_kind == 4) CK(cudaMemcpyAsync(hov, sparse_u16.ovf, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nnz = hp[0];
+    if (*hov) {
+      // some (g, h) count passed 65535: redo the expand with 32/64-bit cells
+      ExpandArgs ea = sparse_u16;
+      ea.ovf = nullptr;
+      if (J < (1ull << 31)) { ea.acc_kind = 0; ea.C = ar.zeros<int32_t>(G * ea.ldc); ca.e_kind = 0; }
+      else { ea.acc_kind = 1; ea.C = ar.zeros<long long>(G * ea.ldc); ca.e_kind = 1; }
+      ca.E = ea.C; ca.V = ea.C; ca.v_kind = ca.e_kind;
+      CK(launch_expand(ea, s, L));
+      CK(launch_compact_count(ca, nullptr, d_nnz, ctmp, s, L));
+      nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+    }
+  }
   const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
   QueryOut r;
   r.n = nnz;
@@ -755,6 +877,11 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   unsigned long long thr = ~0ull;
   cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   if (cudaMallocHost(&c->pinned, kPinnedBytes) != cudaSuccess) { delete c; return TCUDB_E_CUDA; }
+  if (cudaMallocHost(&c->pinned_big, sizeof(unsigned) * 3 * kHllM) != cudaSuccess) {
+    cudaFreeHost(c->pinned);
+    delete c;
+    return TCUDB_E_CUDA;
+  }
   for (auto& e : c->ev) cudaEventCreate(&e);
   *out = c;
   return TCUDB_OK;
@@ -1003,6 +1130,7 @@ void tcudb_destroy(tcudb_ctx* ctx) {
   cudaDeviceSynchronize();
   for (auto& kv : ctx->host_size) cudaFreeHost(kv.first);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->pinned_big) cudaFreeHost(ctx->pinned_big);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   delete ctx;
 }

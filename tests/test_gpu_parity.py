@@ -342,3 +342,51 @@ def test_count_fp4_vs_u8_vs_oracle(engine, torch_mod, oracle_mod, name, scale):
     assert s4["elem"] == (0 if name == "c5" else 3) and s8["elem"] == 0
     compare(o4, ref, agg)
     compare(o8, ref, agg)
+
+
+SHARD_SCRIPT = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import datagen, oracle
+from paper_2112_07552_b200 import Engine
+from paper_2112_07552_b200.shard import local_slice, sharded_join_agg
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+e = Engine(0)
+for name, scale in (("c1", 1.0), ("c2", 0.1), ("c1s", 1.0)):
+    A, B, agg = datagen.make_config(name, scale)
+    ws, rk = dist.get_world_size(), dist.get_rank()
+    dev = lambda T: {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in local_slice(T, ws, rk).items() if v is not None}
+    out = sharded_join_agg(e, dev(A), dev(B), agg)
+    ref = oracle.join_agg(A, B, agg)
+    assert np.array_equal(out["g"].cpu().numpy(), ref["g"]) and np.array_equal(out["h"].cpu().numpy(), ref["h"])
+    assert np.array_equal(out["agg"].cpu().numpy(), ref["cnt"] if agg == "count" else ref["sum"])
+dist.destroy_process_group()
+print("SHARD_OK")
+"""
+
+
+def test_sharded_path_nccl_single_rank(tmp_path):
+    """The multi-GPU driver (tcudb_minmax, tcudb_partition, NCCL all_to_all / allgather) on a
+    1-rank NCCL group (one GPU in this environment), and bench.py --force-shard under torchrun."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "shard_check.py"
+    script.write_text(SHARD_SCRIPT)
+    def port():
+        s = socket.socket(); s.bind(("127.0.0.1", 0)); p = s.getsockname()[1]; s.close(); return p
+    base = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+            "--master-addr", "127.0.0.1"]
+    r = subprocess.run(base + ["--master-port", str(port()), str(script)], cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert "SHARD_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    r = subprocess.run(base + ["--master-port", str(port()), "bench.py", "--force-shard", "--config", "c1",
+                               "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert line, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads(line[-1])
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and "row-shard" in d["config"]["parallelism"]
