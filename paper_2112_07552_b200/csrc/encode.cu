@@ -293,13 +293,65 @@ __global__ void k_gather_slots(const int32_t* __restrict__ tmp_code, const unsig
   }
 }
 // hash: after sorting by key, rank i -> slot_code[slot] = i, dict[i] = min + key
+// remap (optional): remap[old compaction-order code] = rank, for codes already handed out
 __global__ void k_rank_write(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
                              int64_t n, long long minv, int32_t* __restrict__ slot_code,
-                             long long* __restrict__ dict) {
+                             long long* __restrict__ dict, int32_t* __restrict__ remap) {
   const int64_t stride = (int64_t)gridDim.x * T;
   for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    if (remap) remap[slot_code[vals[i]]] = (int32_t)i;
     slot_code[vals[i]] = (int32_t)i;
     dict[i] = (long long)(keys[i] + (unsigned long long)minv);
+  }
+}
+
+// Small hash-mode group domains (<= 4096 distinct values, <= 64 K slots): gather, bitonic
+// sort and rank write in ONE block (instead of a multi-launch radix sort).
+constexpr int SMALL_SORT = 4096;
+__global__ void __launch_bounds__(1024) k_small_rank(const int32_t* __restrict__ code_in,
+                                                     const unsigned long long* __restrict__ slots, int64_t cap,
+                                                     int count, long long minv, int32_t* __restrict__ slot_code,
+                                                     long long* __restrict__ dict, int32_t* __restrict__ remap) {
+  __shared__ unsigned long long sk[SMALL_SORT];
+  __shared__ int sv[SMALL_SORT];   // old (compaction-order) code
+  __shared__ int ss[SMALL_SORT];   // slot
+  int P = 1;
+  while (P < count) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) { sk[i] = ~0ull; sv[i] = -1; ss[i] = -1; }
+  __syncthreads();
+  for (int64_t s = threadIdx.x; s < cap; s += blockDim.x) {
+    const int32_t c = code_in[s];
+    if (c >= 0) { sk[c] = slots[s]; sv[c] = c; ss[c] = (int)s; }
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          if ((sk[i] > sk[l]) == up) {
+            unsigned long long tk = sk[i]; sk[i] = sk[l]; sk[l] = tk;
+            int tv = sv[i]; sv[i] = sv[l]; sv[l] = tv;
+            int ts = ss[i]; ss[i] = ss[l]; ss[l] = ts;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    remap[sv[i]] = i;
+    slot_code[ss[i]] = i;
+    dict[i] = (long long)(sk[i] + (unsigned long long)minv);
+  }
+}
+
+__global__ void k_remap_codes(int32_t* __restrict__ codes, int64_t n, const int32_t* __restrict__ remap) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
+    const int32_t c = codes[i];
+    if (c >= 0) codes[i] = remap[c];
   }
 }
 
@@ -460,7 +512,7 @@ cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, i
                               cudaStream_t s, int64_t* launches) {
   const int64_t nt = (n + PT - 1) / PT;
   if (n <= 0) return exclusive_scan_i32(nullptr, nullptr, 0, count_dev, temp, s, launches);
-  if (n <= (1 << 20)) {
+  if (n <= 8192) {  // small spans: one launch; larger ones need the parallel 3-pass scan
     k_pred_codes_1blk<<<1, 1024, 0, s>>>(fa, fb, n, code, count_dev, union_dev, dict, minv);
     if (launches) ++*launches;
     return cudaGetLastError();
@@ -492,9 +544,28 @@ cudaError_t launch_gather_slots(const int32_t* tmp_code, const unsigned long lon
 }
 
 cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* vals, int64_t n, long long minv,
-                              int32_t* slot_code, long long* dict, cudaStream_t s, int64_t* launches) {
+                              int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
+                              int64_t* launches) {
   if (n <= 0) return cudaSuccess;
-  k_rank_write<<<grid_for(n), T, 0, s>>>(keys, vals, n, minv, slot_code, dict);
+  k_rank_write<<<grid_for(n), T, 0, s>>>(keys, vals, n, minv, slot_code, dict, remap);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+bool small_rank_ok(int64_t count, int64_t cap) { return count <= SMALL_SORT && cap <= (1 << 16); }
+
+cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slots, int64_t cap, int64_t count,
+                              long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
+                              int64_t* launches) {
+  if (count <= 0) return cudaSuccess;
+  k_small_rank<<<1, 1024, 0, s>>>(code, slots, cap, (int)count, minv, slot_code, dict, remap);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remap_codes(int32_t* codes, int64_t n, const int32_t* remap, cudaStream_t s, int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_remap_codes<<<grid_for(n), T, 0, s>>>(codes, n, remap);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -512,7 +583,7 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
       cudaFuncSetAttribute(k_probe_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    int64_t blocks = key.n / std::max<int64_t>(2048, K / 2);  // tuples per block vs per-block flush of K
+    int64_t blocks = key.n / 2048;  // >= 2 tuples per thread; the flush is K / 1024 steps per block
     if (blocks > kNumSMs) blocks = kNumSMs;
     if (blocks < 1) blocks = 1;
     k_probe_smem<<<(int)blocks, 1024, (size_t)smem, s>>>(key, grp, kd, gd, kcode, gcode, cnt_k, (int)K);

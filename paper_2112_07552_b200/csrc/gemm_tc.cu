@@ -29,14 +29,24 @@ constexpr int GROUP_M = 16;              // tile raster: 16 M-blocks per band
 
 // Per-BN kernel geometry (BN = 256 for kind::i8 / kind::f16, 240 for kind::mxf4 so
 // that two accumulators plus the block-scale columns fit the 512 TMEM columns).
-template <int BN_>
+template <int BN_, int KB_ = 128>
 struct Geo {
-  static constexpr int B_STAGE_BYTES = BN_ * BKB;
-  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = BM * KB_;
+  static constexpr int B_STAGE_BYTES = BN_ * KB_;
+  static constexpr int STAGE_BYTES = A_BYTES + B_STAGE_BYTES;
+  static constexpr int STAGES = KB_ == 128 ? 4 : 8;  // same ~190 KB of smem in flight
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 constexpr int SF_COL = 480;  // fp4: scale-factor columns [480, 512): SFA at 480, SFB at 496
+
+// Shared-memory descriptor for a K-major tile with a KB-byte swizzle (128: SWIZZLE_128B,
+// 8-row atoms of 1024 B; 64: SWIZZLE_64B, 8-row atoms of 512 B).
+template <int KB_>
+TCUDB_DEV uint64_t sw_desc(uint32_t smem_addr) {
+  if (KB_ == 128) return sw128_desc(smem_addr);
+  return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | (1ull << 16) | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) |
+         (4ull << 61);
+}
 
 struct KParams {
   int64_t M, N;
@@ -51,13 +61,16 @@ struct KParams {
   const uint8_t* mask; int64_t ldm, mask_rows, mask_cols;
   unsigned long long* tri_out;
   int32_t* cnt_out; int64_t ldcnt;
+  int group_m;       // M-blocks per raster band
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  const int band = t / (GROUP_M * tiles_n);
-  const int first_m = band * GROUP_M;
-  const int gsz = min(tiles_m - first_m, GROUP_M);
-  const int r = t - band * GROUP_M * tiles_n;
+// Grouped raster: bands of group_m M-blocks, N-blocks swept inside a band, so a band's
+// A panel stays L2-resident while B streams through once per band.
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_m, int& mb, int& nb) {
+  const int band = t / (group_m * tiles_n);
+  const int first_m = band * group_m;
+  const int gsz = min(tiles_m - first_m, group_m);
+  const int r = t - band * group_m * tiles_n;
   mb = first_m + r % gsz;
   nb = r / gsz;
 }
@@ -164,10 +177,11 @@ __device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, i
   return nzc;
 }
 
-template <int BN_, bool FP4>
+template <int BN_, bool FP4, int KB_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
-  using G = Geo<BN_>;
+  using G = Geo<BN_, KB_>;
+  constexpr int A_STAGE_BYTES = G::A_BYTES;
   constexpr int STAGES = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment required by the 128B swizzle atoms.
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_last();
       int stage = 0; uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+        int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
@@ -239,10 +253,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A_STAGE_BYTES));
-          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * G::B_STAGE_BYTES));
+          const uint64_t adesc = sw_desc<KB_>(smem_u32(sA + stage * A_STAGE_BYTES));
+          const uint64_t bdesc = sw_desc<KB_>(smem_u32(sB + stage * G::B_STAGE_BYTES));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 bytes of K per 128-byte stage
+          for (int kk = 0; kk < KB_ / 32; ++kk) {  // 32 bytes of K per MMA
             const uint32_t accum = (kb | kk) != 0;
             if (FP4) mma_mxf4(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, tmem_base + SF_COL,
                               tmem_base + SF_COL + 16, accum);
@@ -262,7 +276,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0; uint32_t acc_phase = 0;
     long long tri = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
@@ -340,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t leader_full = mapa_shared(smem_u32(full), 0);
       int stage = 0; uint32_t phase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
-        int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+        int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           // Only the leader arrives (expecting both CTAs' bytes); the peer's TMA bytes
@@ -386,7 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int acc = 0; uint32_t acc_phase = 0;
     long long tri = 0;
     for (int t = cid; t < num_tiles; t += ncl) {
-      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, mb, nb);
+      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t row = (int64_t)mb * 256 + rank * 128 + quarter * 32 + lane;
@@ -435,23 +449,66 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+// 2D tensor map: box = kb_bytes of K x box_rows rows, swizzle matching kb_bytes (128 or 64).
 bool make_map(CUtensorMap* m, const void* base, int elem, int64_t rows, int64_t cols_elems, int64_t ld_elems,
-              int box_rows) {
+              int box_rows, int kb_bytes = BKB) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   const int esz = elem == ELEM_BF16 ? 2 : 1;
   cuuint64_t dims[2] = {(cuuint64_t)cols_elems, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)(BKB / esz), (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)(kb_bytes / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, elem == ELEM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   kb_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
+// K bytes per pipeline stage: 128 (4 stages) or 64 (8 stages; TCUDB_GEMM_KB=64).
+int pick_kb() {
+  static const int kb = (getenv("TCUDB_GEMM_KB") && atoi(getenv("TCUDB_GEMM_KB")) == 64) ? 64 : 128;
+  return kb;
+}
+
 }  // namespace
+
+// Raster band height: the band's A panel (rows x K bytes) should stay L2-resident while
+// B streams (126 MB L2; budget 48 MB). TCUDB_GEMM_GROUP_M overrides (experiments).
+int pick_group_m(int tiles_m, int64_t rows_per_mblock, int64_t k_bytes) {
+  static const int env = getenv("TCUDB_GEMM_GROUP_M") ? atoi(getenv("TCUDB_GEMM_GROUP_M")) : 0;
+  int64_t g = env > 0 ? env : (int64_t)(48e6 / (double)(rows_per_mblock * (k_bytes > 0 ? k_bytes : 1)));
+  if (g < 1) g = 1;
+  if (g > tiles_m) g = tiles_m;
+  return (int)g;
+}
+
+// Builds the tensor maps and launches the 1-CTA kernel for the chosen stage width.
+template <int BN_, bool FP4>
+cudaError_t run_1cta(const GemmArgs& a, const KParams& p, int map_elem, int kb, cudaStream_t s, int64_t* launches) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Geo<BN_, 128>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Geo<BN_, 64>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t kcols = a.k_begin + a.k_len;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, map_elem, a.M, kcols, a.lda, BM, kb) ||
+      !make_map(&mB, a.B, map_elem, a.N, kcols, a.ldb, BN_, kb))
+    return cudaErrorInvalidValue;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  if (kb == 64) k_gemm_tc<BN_, FP4, 64><<<grid, NUM_THREADS, Geo<BN_, 64>::SMEM_BYTES, s>>>(mA, mB, p);
+  else k_gemm_tc<BN_, FP4, 128><<<grid, NUM_THREADS, Geo<BN_, 128>::SMEM_BYTES, s>>>(mA, mB, p);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
 
 // kind::mxf4 path: e2m1 operands, two elements per byte. k_begin / k_len / lda / ldb
 // are in BYTES; the N tile is 240 (two 240-column accumulators + block scales in TMEM),
@@ -465,23 +522,13 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
     return cudaErrorInvalidValue;
   const int64_t tiles_n = (a.N + BNF - 1) / BNF;
   if (a.ldc < tiles_n * BNF) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BNF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Geo<BNF>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int64_t kcols = a.k_begin + a.k_len;
-  CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, ELEM_I8, a.M, kcols, a.lda, BM) || !make_map(&mB, a.B, ELEM_I8, a.N, kcols, a.ldb, BNF))
-    return cudaErrorInvalidValue;
+  const int kb = pick_kb();
   KParams p{};
   p.M = a.M; p.N = a.N;
   p.tiles_m = (int)(a.M / BM); p.tiles_n = (int)tiles_n;
-  p.elems_per_kb = BKB;  // bytes
-  p.num_kb = (int)(a.k_len / BKB);
-  p.kb_begin = (int)(a.k_begin / BKB);
+  p.elems_per_kb = kb;  // bytes
+  p.num_kb = (int)(a.k_len / kb);
+  p.kb_begin = (int)(a.k_begin / kb);
   p.is_bf16 = 0;
   // Block-scaled instruction descriptor (kind::mxf4): A/B format E2M1 = 1 (bits 7-9, 10-12),
   // K-major, N >> 3 (bits 17-22), scale format UE8M0 (bit 23), M >> 4 (bits 24-28),
@@ -490,11 +537,8 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   p.idesc = idesc;
   p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = 0;
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
-  const int tiles = p.tiles_m * p.tiles_n;
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  k_gemm_tc<BNF, true><<<grid, NUM_THREADS, Geo<BNF>::SMEM_BYTES, s>>>(mA, mB, p);
-  if (launches) ++*launches;
-  return cudaGetLastError();
+  p.group_m = pick_group_m(p.tiles_m, BM, a.k_len);
+  return run_1cta<BNF, true>(a, p, ELEM_I8, kb, s, launches);
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
@@ -505,10 +549,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   if ((a.lda * esz) % 16 || (a.ldb * esz) % 16) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Geo<BN>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -517,15 +558,11 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   // CTA-pair (cta_group::2) kernel when M splits into 256-row pair tiles.
   static const bool want_pair = getenv("TCUDB_GEMM_PAIR") && getenv("TCUDB_GEMM_PAIR")[0] == '1';
   const bool pair = want_pair && a.M % 256 == 0;
-  const int64_t kcols = a.k_begin + a.k_len;
-  CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, a.elem, a.M, kcols, a.lda, pair ? 128 : BM) ||
-      !make_map(&mB, a.B, a.elem, a.N, kcols, a.ldb, pair ? 128 : BN))
-    return cudaErrorInvalidValue;
+  const int kb = pair ? BKB : pick_kb();
   KParams p{};
   p.M = a.M; p.N = a.N;
   p.tiles_m = (int)(a.M / (pair ? 256 : BM)); p.tiles_n = (int)(a.N / BN);
-  p.elems_per_kb = BKB / esz;
+  p.elems_per_kb = kb / esz;
   p.num_kb = (int)(a.k_len / p.elems_per_kb);
   p.kb_begin = (int)(a.k_begin / p.elems_per_kb);
   p.is_bf16 = a.elem == ELEM_BF16;
@@ -541,14 +578,15 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = a.shift;
   p.mask = a.mask; p.ldm = a.ldm; p.mask_rows = a.mask_rows; p.mask_cols = a.mask_cols; p.tri_out = a.tri_out;
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
+  p.group_m = pick_group_m(p.tiles_m, pair ? 256 : BM, a.k_len * esz);
+  if (!pair) return run_1cta<BN, false>(a, p, a.elem, kb, s, launches);
+  const int64_t kcols = a.k_begin + a.k_len;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, a.elem, a.M, kcols, a.lda, 128) || !make_map(&mB, a.B, a.elem, a.N, kcols, a.ldb, 128))
+    return cudaErrorInvalidValue;
   const int tiles = p.tiles_m * p.tiles_n;
-  if (pair) {
-    const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-    k_gemm_tc2<<<grid, NUM_THREADS, SMEM2_BYTES, s>>>(mA, mB, p);
-  } else {
-    const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-    k_gemm_tc<BN, false><<<grid, NUM_THREADS, Geo<BN>::SMEM_BYTES, s>>>(mA, mB, p);
-  }
+  const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+  k_gemm_tc2<<<grid, NUM_THREADS, SMEM2_BYTES, s>>>(mA, mB, p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -55,7 +55,15 @@ cudaError_t launch_direct_dict(const int32_t* code, int64_t range, long long min
 cudaError_t launch_gather_slots(const int32_t* tmp_code, const unsigned long long* slots, int64_t cap,
                                 unsigned long long* keys, uint32_t* vals, cudaStream_t s, int64_t* launches);
 cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* vals, int64_t n, long long minv,
-                              int32_t* slot_code, long long* dict, cudaStream_t s, int64_t* launches);
+                              int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
+                              int64_t* launches);
+// One-block gather + bitonic sort + rank write for small hash domains (slot_code may alias code).
+bool small_rank_ok(int64_t count, int64_t cap);
+cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slots, int64_t cap, int64_t count,
+                              long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
+                              int64_t* launches);
+// codes[i] = remap[codes[i]] for codes >= 0 (per-tuple codes issued before the rank sort)
+cudaError_t launch_remap_codes(int32_t* codes, int64_t n, const int32_t* remap, cudaStream_t s, int64_t* launches);
 cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
                          const DictView& gd, int32_t* kcode, int32_t* gcode, int32_t* cnt_k,
                          double* rowabs_g, int64_t K, cudaStream_t s, int64_t* launches);

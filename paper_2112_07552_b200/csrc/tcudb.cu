@@ -215,13 +215,21 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
 }
 
 // Phase 2 for group domains: sorted value dictionary (ascending ranks).
-void dict_finish_group(Arena& ar, Dict& d, int64_t* launches) {
+// tuple_codes / n (optional): per-tuple codes already issued in compaction order; they
+// are remapped to the ascending ranks.
+void dict_finish_group(Arena& ar, Dict& d, int64_t* launches, int32_t* tuple_codes = nullptr, int64_t n = 0) {
   cudaStream_t s = ar.s;
   if (d.mode == 0 && d.dict) return;  // written by the predicate scan
   d.dict = ar.get<long long>(d.count);
   if (d.count == 0) return;
   if (d.mode == 0) {
     CK(launch_direct_dict(d.code, (int64_t)d.span, d.minv, d.dict, s, launches));
+    return;
+  }
+  if (small_rank_ok(d.count, (int64_t)d.span)) {
+    int32_t* remap = ar.get<int32_t>(d.count);
+    CK(launch_small_rank(d.code, d.slots, (int64_t)d.span, d.count, d.minv, d.code, d.dict, remap, s, launches));
+    if (tuple_codes) CK(launch_remap_codes(tuple_codes, n, remap, s, launches));
     return;
   }
   unsigned long long* k0 = ar.get<unsigned long long>(d.count);
@@ -233,7 +241,9 @@ void dict_finish_group(Arena& ar, Dict& d, int64_t* launches) {
   void* tmp = ar.get<char>((int64_t)radix_temp_bytes(d.count));
   bool alt = false;
   CK(radix_sort_pairs(k0, v0, k1, v1, d.count, bits, tmp, s, launches, &alt));
-  CK(launch_rank_write(alt ? k1 : k0, alt ? v1 : v0, d.count, d.minv, d.code, d.dict, s, launches));
+  int32_t* remap = tuple_codes ? ar.get<int32_t>(d.count) : nullptr;
+  CK(launch_rank_write(alt ? k1 : k0, alt ? v1 : v0, d.count, d.minv, d.code, d.dict, remap, s, launches));
+  if (tuple_codes) CK(launch_remap_codes(tuple_codes, n, remap, s, launches));
 }
 
 struct Timer {
@@ -361,23 +371,47 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   }
   unsigned long long* d_union = ar.zeros<unsigned long long>(1);
   Dict DK, DG, DH;
+  // sum |v| per group: the integer-SUM overflow bound of the guard (fp64; non-negative, so
+  // its bit pattern orders like an unsigned integer for the max reduction)
+  const bool int_sum = is_sum && !is_float;
+  int32_t *kA = ar.get<int32_t>(nA), *gA = ar.get<int32_t>(nA);
+  int32_t *kB = ar.get<int32_t>(nB), *hB = ar.get<int32_t>(nB);
+  int32_t *cntA = nullptr, *cntB = nullptr;
+  unsigned long long misc[4] = {0, 0, 0, 0};  // J, max rowabs A, max rowabs B
   for (int attempt = 0; attempt < 2; ++attempt) {
     dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0]);
     dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
     dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2]);
+    // probe right away with upper-bound sizes (codes < span / capacity), so the dictionary
+    // sizes and the join size J come back in ONE device->host read
+    const int64_t Ku = (int64_t)DK.span, Gu = (int64_t)DG.span, Hu = (int64_t)DH.span;
+    cntA = ar.zeros<int32_t>(Ku);
+    cntB = ar.zeros<int32_t>(Ku);
+    double* rowA = int_sum ? ar.zeros<double>(Gu) : nullptr;
+    double* rowB = int_sum ? ar.zeros<double>(Hu) : nullptr;
+    CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, Ku, s, L));
+    CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, Ku, s, L));
+    unsigned long long* d_misc = ar.zeros<unsigned long long>(4);
+    CK(launch_join_size(cntA, cntB, Ku, d_misc + 0, s, L));
+    if (int_sum) {
+      CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), Gu, d_misc + 1, s, L));
+      CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), Hu, d_misc + 2, s, L));
+    }
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
-    int* hov = reinterpret_cast<int*>(hp + 4);
+    int* hov = reinterpret_cast<int*>(hp + 8);
     hov[0] = hov[1] = hov[2] = 0;
     CK(cudaMemcpyAsync(hp + 0, DK.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 1, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 2, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 3, d_union, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 4, d_misc, 32, cudaMemcpyDeviceToHost, s));
     if (DK.ovf) CK(cudaMemcpyAsync(hov + 0, DK.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (DG.ovf) CK(cudaMemcpyAsync(hov + 1, DG.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (DH.ovf) CK(cudaMemcpyAsync(hov + 2, DH.ovf, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     DK.count = hp[0]; DG.count = hp[1]; DH.count = hp[2];
     S.K_union = hp[3];
+    std::memcpy(misc, hp + 4, 32);
     if (!hov[0] && !hov[1] && !hov[2]) break;
     // an estimate was far too small (table full): rebuild sized by the tuple counts
     est[0] = est[1] = est[2] = 0;
@@ -387,38 +421,14 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const int64_t K = DK.count, G = DG.count, H = DH.count;
   S.K = K; S.G = G; S.H = H;
   S.key_mode = DK.mode;
-  dict_finish_group(ar, DG, L);
-  dict_finish_group(ar, DH, L);
-  if (K == 0) { tm.mark(&S.ms_encode); tm.finish(); return TCUDB_OK; }
-
-  // probe
-  int32_t* kA = ar.get<int32_t>(nA);
-  int32_t* gA = ar.get<int32_t>(nA);
-  int32_t* kB = ar.get<int32_t>(nB);
-  int32_t* hB = ar.get<int32_t>(nB);
-  int32_t* cntA = ar.zeros<int32_t>(K);
-  int32_t* cntB = ar.zeros<int32_t>(K);
-  // sum |v| per group: the integer-SUM overflow bound of the guard (fp64; non-negative, so
-  // its bit pattern orders like an unsigned integer for the max reduction)
-  const bool int_sum = is_sum && !is_float;
-  double* rowA = int_sum ? ar.zeros<double>(G) : nullptr;
-  double* rowB = int_sum ? ar.zeros<double>(H) : nullptr;
-  CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, K, s, L));
-  CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, K, s, L));
-  unsigned long long* d_misc = ar.zeros<unsigned long long>(4);  // J, max rowabs A, max rowabs B
-  CK(launch_join_size(cntA, cntB, K, d_misc + 0, s, L));
-  if (int_sum) {
-    CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), G, d_misc + 1, s, L));
-    CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), H, d_misc + 2, s, L));
-  }
-  CK(cudaMemcpyAsync(ctx->pinned, d_misc, 32, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  unsigned long long misc[4];
-  std::memcpy(misc, ctx->pinned, 32);
   tm.mark(&S.ms_encode);
   const unsigned long long J = misc[0];
   S.join_pairs = (int64_t)J;
-  if (J == 0) { tm.finish(); return TCUDB_OK; }
+  if (K == 0 || J == 0) { tm.finish(); return TCUDB_OK; }
+  // hash-mode group domains: ascending ranks; the per-tuple codes issued by the probe
+  // (compaction order) are remapped so row/column order = (g, h) order
+  dict_finish_group(ar, DG, L, gA, nA);
+  dict_finish_group(ar, DH, L, hB, nB);
 
   // ---------------- a3 (integer bound) + a4 selector
   auto col_absmax = [&](int c) -> long double {
