@@ -312,9 +312,9 @@ __global__ void __launch_bounds__(1024) k_small_rank(const int32_t* __restrict__
                                                      const unsigned long long* __restrict__ slots, int64_t cap,
                                                      int count, long long minv, int32_t* __restrict__ slot_code,
                                                      long long* __restrict__ dict, int32_t* __restrict__ remap) {
-  __shared__ unsigned long long sk[SMALL_SORT];
-  __shared__ int sv[SMALL_SORT];   // old (compaction-order) code
-  __shared__ int ss[SMALL_SORT];   // slot
+  extern __shared__ unsigned long long sk[];               // [SMALL_SORT] keys
+  int* sv = reinterpret_cast<int*>(sk + SMALL_SORT);       // [SMALL_SORT] old (compaction-order) code
+  int* ss = sv + SMALL_SORT;                               // [SMALL_SORT] slot
   int P = 1;
   while (P < count) P <<= 1;
   for (int i = threadIdx.x; i < P; i += blockDim.x) { sk[i] = ~0ull; sv[i] = -1; ss[i] = -1; }
@@ -558,7 +558,13 @@ cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slo
                               long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
                               int64_t* launches) {
   if (count <= 0) return cudaSuccess;
-  k_small_rank<<<1, 1024, 0, s>>>(code, slots, cap, (int)count, minv, slot_code, dict, remap);
+  constexpr size_t smem = (size_t)SMALL_SORT * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_small_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_small_rank<<<1, 1024, smem, s>>>(code, slots, cap, (int)count, minv, slot_code, dict, remap);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
