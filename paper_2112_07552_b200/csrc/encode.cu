@@ -46,10 +46,20 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     float mn = INFINITY, mx = -INFINITY, mabs = INFINITY;
     int nonfinite = 0;
     const float* p = static_cast<const float*>(c.data);
-    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < c.n; i += stride) {
-      const float x = __ldg(p + i);
-      if (!isfinite(x)) nonfinite = 1;
-      mn = fminf(mn, x); mx = fmaxf(mx, x); mabs = fminf(mabs, fabsf(x));
+    // 4 independent loads in flight per thread (the scan is latency-bound otherwise)
+    for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < c.n; i0 += 4 * stride) {
+      float x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * stride;
+        x[u] = i < c.n ? __ldcs(p + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + u * stride >= c.n) break;
+        if (!isfinite(x[u])) nonfinite = 1;
+        mn = fminf(mn, x[u]); mx = fmaxf(mx, x[u]); mabs = fminf(mabs, fabsf(x[u]));
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -69,11 +79,20 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     return;
   }
   long long mn = LLONG_MAX, mx = LLONG_MIN, mabs = LLONG_MAX;
-  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < c.n; i += stride) {
-    const long long x = ld_int(c.data, c.type, i);
-    mn = min(mn, x); mx = max(mx, x);
-    const long long a = x < 0 ? (x == LLONG_MIN ? LLONG_MAX : -x) : x;
-    mabs = min(mabs, a);
+  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < c.n; i0 += 4 * stride) {
+    long long x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      x[u] = i < c.n ? ld_int(c.data, c.type, i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u * stride >= c.n) break;
+      mn = min(mn, x[u]); mx = max(mx, x[u]);
+      const long long a = x[u] < 0 ? (x[u] == LLONG_MIN ? LLONG_MAX : -x[u]) : x[u];
+      mabs = min(mabs, a);
+    }
   }
   mn = warp_min_ll(mn); mx = warp_max_ll(mx); mabs = warp_min_ll(mabs);
   if (lane_id() == 0) { atomicMin(&s->mn, mn); atomicMax(&s->mx, mx); atomicMin(&s->min_abs, mabs); }
@@ -134,29 +153,43 @@ __global__ void __launch_bounds__(1024) k_mark_direct_smem(ColDesc c, long long 
 // are inserted once (warp aggregation). flags[slot] = 1 marks the side.
 __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __restrict__ slots,
                               unsigned long long mask, uint8_t* __restrict__ flags, int* __restrict__ overflow) {
+  constexpr int U = 4;  // elements per thread per iteration: the first-probe loads overlap
   const int64_t stride = (int64_t)gridDim.x * T;
   const int64_t n_round = (c.n + 31) & ~int64_t(31);
-  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_round; i += stride) {
-    const bool ok = i < c.n;
-    const unsigned long long off = ok ? (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv
-                                      : ~0ull - 1 - lane_id();
-    const unsigned act = __ballot_sync(0xffffffffu, ok);
-    const unsigned peers = __match_any_sync(0xffffffffu, off) & act;
-    if (!ok || (__ffs(peers) - 1) != lane_id()) continue;  // lowest active peer lane inserts
-    unsigned long long h = fmix64(off) & mask;
-    bool placed = false;
-    for (unsigned long long step = 0; step <= mask; ++step) {  // bounded: a full table is reported
-      // plain read first: a key already present (the common case for hot keys) costs no atomic
-      const unsigned long long cur = __ldcg(slots + h);
-      if (cur == off) { placed = true; break; }
-      if (cur == ~0ull) {
-        const unsigned long long prev = atomicCAS(slots + h, ~0ull, off);
-        if (prev == ~0ull || prev == off) { placed = true; break; }
-      }
-      h = (h + 1) & mask;
+  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < n_round; i0 += U * stride) {
+    unsigned long long off[U], h[U], cur[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      ok[u] = i < c.n;
+      off[u] = ok[u] ? (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv
+                     : ~0ull - 1 - lane_id();
+      h[u] = fmix64(off[u]) & mask;
     }
-    if (!placed) { *overflow = 1; continue; }
-    if (!flags[h]) flags[h] = 1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = ok[u] ? __ldcg(slots + h[u]) : 0ull;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + u * stride >= n_round) break;  // warp-uniform (n_round is a multiple of 32)
+      const unsigned act = __ballot_sync(0xffffffffu, ok[u]);
+      const unsigned peers = __match_any_sync(0xffffffffu, off[u]) & act;
+      if (!ok[u] || (__ffs(peers) - 1) != lane_id()) continue;  // lowest active peer lane inserts
+      unsigned long long hh = h[u], cc = cur[u];
+      bool placed = false;
+      for (unsigned long long step = 0; step <= mask; ++step) {  // bounded: a full table is reported
+        // plain read first: a key already present (the common case for hot keys) costs no atomic
+        if (cc == off[u]) { placed = true; break; }
+        if (cc == ~0ull) {
+          const unsigned long long prev = atomicCAS(slots + hh, ~0ull, off[u]);
+          if (prev == ~0ull || prev == off[u]) { placed = true; break; }
+        }
+        hh = (hh + 1) & mask;
+        cc = __ldcg(slots + hh);
+      }
+      if (!placed) { *overflow = 1; continue; }
+      if (!flags[hh]) flags[hh] = 1;
+    }
   }
 }
 
@@ -368,6 +401,34 @@ TCUDB_DEV int32_t dict_lookup(const DictView& d, long long x) {
   }
 }
 
+// U lookups with their first loads issued together (the probe is latency-bound).
+template <int U>
+TCUDB_DEV void dict_lookup_batch(const DictView& d, const long long* x, const bool* ok, int32_t* out) {
+  unsigned long long off[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) off[u] = (unsigned long long)x[u] - (unsigned long long)d.minv;
+  if (d.mode == 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) out[u] = (ok[u] && off[u] < d.size) ? __ldg(d.code + off[u]) : -1;
+    return;
+  }
+  unsigned long long h[U], k[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    h[u] = fmix64(off[u]) & d.size;
+    k[u] = ok[u] ? __ldg(d.slots + h[u]) : off[u];
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    while (k[u] != off[u] && k[u] != ~0ull) {
+      h[u] = (h[u] + 1) & d.size;
+      k[u] = __ldg(d.slots + h[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) out[u] = (ok[u] && k[u] == off[u]) ? __ldg(d.code + h[u]) : -1;
+}
+
 // kcode / gcode per tuple; per-key counts (warp-aggregated); per-group tuple
 // counts and sum |v| of tuples whose key survives the ∩ (guard bounds, a3).
 // Variant with the per-key counters privatized in shared memory (small key
@@ -379,12 +440,29 @@ __global__ void __launch_bounds__(1024) k_probe_smem(ColDesc key, ColDesc grp, D
   extern __shared__ int32_t s_cnt[];
   for (int k = threadIdx.x; k < K; k += blockDim.x) s_cnt[k] = 0;
   __syncthreads();
+  constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < key.n; i += stride) {
-    const int32_t kc = dict_lookup(kd, ld_int(key.data, key.type, i));
-    kcode[i] = kc;
-    gcode[i] = dict_lookup(gd, ld_int(grp.data, grp.type, i));
-    if (kc >= 0) atomicAdd(s_cnt + kc, 1);
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < key.n; i0 += U * stride) {
+    long long xk[U], xg[U];
+    bool ok[U];
+    int32_t kc[U], gc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      ok[u] = i < key.n;
+      xk[u] = ok[u] ? ld_int(key.data, key.type, i) : 0;
+      xg[u] = ok[u] ? ld_int(grp.data, grp.type, i) : 0;
+    }
+    dict_lookup_batch<U>(kd, xk, ok, kc);
+    dict_lookup_batch<U>(gd, xg, ok, gc);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      const int64_t i = i0 + u * stride;
+      kcode[i] = kc[u];
+      gcode[i] = gc[u];
+      if (kc[u] >= 0) atomicAdd(s_cnt + kc[u], 1);
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < K; k += blockDim.x)
@@ -394,17 +472,29 @@ __global__ void __launch_bounds__(1024) k_probe_smem(ColDesc key, ColDesc grp, D
 __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, DictView gd,
                         int32_t* __restrict__ kcode, int32_t* __restrict__ gcode, int32_t* __restrict__ cnt_k,
                         double* __restrict__ rowabs_g) {
+  constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * T;
   const int64_t n_round = (key.n + 31) & ~int64_t(31);
-  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_round; i += stride) {
-    const bool ok = i < key.n;
-    int32_t kc = -1, gc = -1;
-    if (ok) {
-      kc = dict_lookup(kd, ld_int(key.data, key.type, i));
-      gc = dict_lookup(gd, ld_int(grp.data, grp.type, i));
-      kcode[i] = kc;
-      gcode[i] = gc;
-    }
+  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < n_round; i0 += U * stride) {
+  long long xk[U], xg[U];
+  bool okv[U];
+  int32_t kcv[U], gcv[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + u * stride;
+    okv[u] = i < key.n;
+    xk[u] = okv[u] ? ld_int(key.data, key.type, i) : 0;
+    xg[u] = okv[u] ? ld_int(grp.data, grp.type, i) : 0;
+  }
+  dict_lookup_batch<U>(kd, xk, okv, kcv);
+  dict_lookup_batch<U>(gd, xg, okv, gcv);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + u * stride;
+    if (i >= n_round) break;  // warp-uniform
+    const bool ok = okv[u];
+    const int32_t kc = ok ? kcv[u] : -1, gc = ok ? gcv[u] : -1;
+    if (ok) { kcode[i] = kc; gcode[i] = gc; }
     const int32_t kk = (ok && kc >= 0) ? kc : -2 - lane_id();
     const unsigned peers = __match_any_sync(0xffffffffu, kk);
     if (ok && kc >= 0 && (__ffs(peers) - 1) == lane_id()) atomicAdd(cnt_k + kc, __popc(peers));
@@ -418,17 +508,38 @@ __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, Dict
       atomicAdd(rowabs_g + gc, a);
     }
   }
+  }
 }
 
 // J = sum_k cntA[k] * cntB[k] (join size, a4) and max per-key counts.
+// out[0] = J = sum_k cntA[k]*cntB[k]; out[3] = sum cntA, out[4] = sum cntB (tuples with a
+// key in the ∩ domain on each side)
 __global__ void k_join_size(const int32_t* __restrict__ ca, const int32_t* __restrict__ cb, int64_t K,
-                            unsigned long long* __restrict__ J) {
+                            unsigned long long* __restrict__ out) {
   const int64_t stride = (int64_t)gridDim.x * T;
-  unsigned long long s = 0;
-  for (int64_t k = (int64_t)blockIdx.x * T + threadIdx.x; k < K; k += stride)
-    s += (unsigned long long)ca[k] * (unsigned long long)cb[k];
-  s = warp_sum(s);
-  if (lane_id() == 0 && s) atomicAdd(J, s);
+  unsigned long long s = 0, sa = 0, sb = 0;
+  for (int64_t k = (int64_t)blockIdx.x * T + threadIdx.x; k < K; k += stride) {
+    const unsigned long long a = (unsigned)ca[k], b = (unsigned)cb[k];
+    s += a * b;
+    if (b) sa += a;
+    if (a) sb += b;
+  }
+  s = warp_sum(s); sa = warp_sum(sa); sb = warp_sum(sb);
+  if (lane_id() == 0) {
+    if (s) atomicAdd(out, s);
+    if (sa) atomicAdd(out + 3, sa);
+    if (sb) atomicAdd(out + 4, sb);
+  }
+}
+
+// number of set bits of (w & mask) over n words (occupancy maps, fp4 nibble maps)
+__global__ void k_popcount(const unsigned* __restrict__ w, int64_t n, unsigned mask,
+                           unsigned long long* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * T;
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) c += __popc(__ldcs(w + i) & mask);
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
 }
 
 __global__ void k_max_u64(const unsigned long long* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
@@ -552,7 +663,8 @@ cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* va
   return cudaGetLastError();
 }
 
-bool small_rank_ok(int64_t count, int64_t cap) { return count <= SMALL_SORT && cap <= (1 << 16); }
+// (the one-block bitonic sort wins below ~1 K values; the radix sort above)
+bool small_rank_ok(int64_t count, int64_t cap) { return count <= 1024 && cap <= (1 << 16); }
 
 cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slots, int64_t cap, int64_t count,
                               long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
@@ -601,10 +713,18 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
   return cudaGetLastError();
 }
 
-cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* J, cudaStream_t s,
-                             int64_t* launches) {
+cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* out,
+                             cudaStream_t s, int64_t* launches) {
   if (K <= 0) return cudaSuccess;
-  k_join_size<<<grid_for(K), T, 0, s>>>(ca, cb, K, J);
+  k_join_size<<<grid_for(K), T, 0, s>>>(ca, cb, K, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_popcount(const unsigned* w, int64_t n, unsigned mask, unsigned long long* out, cudaStream_t s,
+                            int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_popcount<<<grid_for(n, T * 8), T, 0, s>>>(w, n, mask, out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

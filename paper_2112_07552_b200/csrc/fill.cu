@@ -71,8 +71,9 @@ __global__ void k_fill_count_fp4(const int32_t* __restrict__ kcode, const int32_
     if (kc < 0) continue;
     const int64_t e = (int64_t)rcode[i] * ld_elems + kc;  // element index (nibble)
     const int sh = 4 * (int)(e & 7);
+    // the OR's return value tells whether the nibble was already set: a duplicate cell
     const unsigned old = atomicOr(reinterpret_cast<unsigned*>(op + ((e >> 1) & ~int64_t(3))), 0x2u << sh);
-    if ((old >> sh) & 0xFu) dup = 1;
+    dup |= (old >> sh) & 0xFu;
   }
   dup = __any_sync(0xffffffffu, dup);
   if (lane_id() == 0 && dup) atomicOr(&fs->overflow, 1);
@@ -89,7 +90,7 @@ __global__ void k_fill_bf16_direct(const int32_t* __restrict__ kcode, const int3
                                    int64_t ld_op, unsigned* __restrict__ occ, int64_t ld_occ,
                                    FillStats* __restrict__ fs) {
   const int64_t stride = (int64_t)gridDim.x * T;
-  int dup = 0, inexact = 0;
+  int inexact = 0;
   for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
     const int32_t kc = kcode[i];
     if (kc < 0) continue;
@@ -97,16 +98,11 @@ __global__ void k_fill_bf16_direct(const int32_t* __restrict__ kcode, const int3
     const uint32_t b = val ? __float_as_uint(__ldg(val + i)) : 0x3F800000u;  // absent value = 1.0
     inexact |= (b & 0xFFFFu) != 0u;
     const int64_t bit = r * ld_occ + kc;
-    const unsigned old = atomicOr(occ + (bit >> 5), 1u << (bit & 31));
-    dup |= (old >> (bit & 31)) & 1u;
+    atomicOr(occ + (bit >> 5), 1u << (bit & 31));  // fire-and-forget; popcount checked afterwards
     op[r * ld_op + kc] = (uint16_t)(b >> 16);
   }
-  dup = __any_sync(0xffffffffu, dup);
   inexact = __any_sync(0xffffffffu, inexact);
-  if (lane_id() == 0) {
-    if (dup) atomicOr(&fs->overflow, 1);
-    if (inexact) atomicOr(&fs->inexact, 1);
-  }
+  if (lane_id() == 0 && inexact) atomicOr(&fs->inexact, 1);
 }
 
 // Wide integer fill into int64 scratch (COUNT: +1, SUM: +v), wrapping adds.

@@ -67,8 +67,12 @@ cudaError_t launch_remap_codes(int32_t* codes, int64_t n, const int32_t* remap, 
 cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
                          const DictView& gd, int32_t* kcode, int32_t* gcode, int32_t* cnt_k,
                          double* rowabs_g, int64_t K, cudaStream_t s, int64_t* launches);
-cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* J, cudaStream_t s,
-                             int64_t* launches);
+// out[0] += J = sum cntA*cntB, out[3] += sum cntA (keys also in B), out[4] += sum cntB
+cudaError_t launch_join_size(const int32_t* ca, const int32_t* cb, int64_t K, unsigned long long* out,
+                             cudaStream_t s, int64_t* launches);
+// *out += popcount(w[i] & mask) over n words
+cudaError_t launch_popcount(const unsigned* w, int64_t n, unsigned mask, unsigned long long* out, cudaStream_t s,
+                            int64_t* launches);
 cudaError_t launch_max_u64(const unsigned long long* x, int64_t n, unsigned long long* out, cudaStream_t s,
                            int64_t* launches);
 
@@ -86,12 +90,12 @@ struct FillStats {
 cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
                                  FillStats* fs, cudaStream_t s, int64_t* launches);
 // COUNT with 0/1 cells straight into packed e2m1 nibbles (ld in elements); a second tuple in a
-// cell sets fs->overflow (the guard then uses the u8 path).
+// cell sets fs->overflow (from the atomicOr's return value).
 cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,
                                   int64_t ld_elems, FillStats* fs, cudaStream_t s, int64_t* launches);
 // Float SUM with <= 1 tuple per cell and bf16-exact values: bf16 bits stored straight into
-// op[r][k]; occ is a zeroed 1-bit occupancy map [rows][ld_occ bits]; violations set
-// fs->overflow (second tuple in a cell) / fs->inexact (value not bf16-exact).
+// op[r][k]; occ is a zeroed 1-bit occupancy map [rows][ld_occ bits] (a second tuple in a cell:
+// popcount(occ) < tuples written, checked by the caller); fs->inexact: value not bf16-exact.
 cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                     uint16_t* op, int64_t ld_op, unsigned* occ, int64_t ld_occ, FillStats* fs,
                                     cudaStream_t s, int64_t* launches);

@@ -377,7 +377,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   int32_t *kA = ar.get<int32_t>(nA), *gA = ar.get<int32_t>(nA);
   int32_t *kB = ar.get<int32_t>(nB), *hB = ar.get<int32_t>(nB);
   int32_t *cntA = nullptr, *cntB = nullptr;
-  unsigned long long misc[4] = {0, 0, 0, 0};  // J, max rowabs A, max rowabs B
+  // J, max rowabs A, max rowabs B, A tuples with a ∩ key, B tuples with a ∩ key
+  unsigned long long misc[6] = {0, 0, 0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0]);
     dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
@@ -391,27 +392,27 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     double* rowB = int_sum ? ar.zeros<double>(Hu) : nullptr;
     CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, Ku, s, L));
     CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, Ku, s, L));
-    unsigned long long* d_misc = ar.zeros<unsigned long long>(4);
+    unsigned long long* d_misc = ar.zeros<unsigned long long>(6);
     CK(launch_join_size(cntA, cntB, Ku, d_misc + 0, s, L));
     if (int_sum) {
       CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), Gu, d_misc + 1, s, L));
       CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), Hu, d_misc + 2, s, L));
     }
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
-    int* hov = reinterpret_cast<int*>(hp + 8);
+    int* hov = reinterpret_cast<int*>(hp + 12);
     hov[0] = hov[1] = hov[2] = 0;
     CK(cudaMemcpyAsync(hp + 0, DK.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 1, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 2, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + 3, d_union, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 4, d_misc, 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 4, d_misc, 48, cudaMemcpyDeviceToHost, s));
     if (DK.ovf) CK(cudaMemcpyAsync(hov + 0, DK.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (DG.ovf) CK(cudaMemcpyAsync(hov + 1, DG.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (DH.ovf) CK(cudaMemcpyAsync(hov + 2, DH.ovf, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     DK.count = hp[0]; DG.count = hp[1]; DH.count = hp[2];
     S.K_union = hp[3];
-    std::memcpy(misc, hp + 4, 32);
+    std::memcpy(misc, hp + 4, 48);
     if (!hov[0] && !hov[1] && !hov[2]) break;
     // an estimate was far too small (table full): rebuild sized by the tuple counts
     est[0] = est[1] = est[2] = 0;
@@ -529,7 +530,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       CK(cudaStreamSynchronize(s));
       FillStats hf[2];
       std::memcpy(hf, ctx->pinned, sizeof(hf));
-      if (hf[0].overflow || hf[1].overflow) { op4A = op4B = nullptr; CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s)); }
+      if (hf[0].overflow || hf[1].overflow) {
+        op4A = op4B = nullptr;
+        CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
+      }
     }
     if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE)) {
       opA = ar.zeros<uint8_t>(cellsA);
@@ -588,11 +592,14 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         unsigned* occB = ar.zeros<unsigned>(cellsB / 32 + 1);
         CK(launch_fill_bf16_direct(kA, gA, av, nA, fA, ldop, occA, Kp, fs + 0, s, L));
         CK(launch_fill_bf16_direct(kB, hB, bw, nB, fB, ldop, occB, Kp, fs + 1, s, L));
+        CK(launch_popcount(occA, cellsA / 32 + 1, 0xFFFFFFFFu, &fs[0].nnz, s, L));
+        CK(launch_popcount(occB, cellsB / 32 + 1, 0xFFFFFFFFu, &fs[1].nnz, s, L));
         CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         FillStats hf[2];
         std::memcpy(hf, ctx->pinned, sizeof(hf));
-        bf16_direct = !(hf[0].overflow | hf[1].overflow | hf[0].inexact | hf[1].inexact);
+        // one set occupancy bit per written tuple <=> no cell holds two tuples
+        bf16_direct = hf[0].nnz == misc[3] && hf[1].nnz == misc[4] && !(hf[0].inexact | hf[1].inexact);
         if (!bf16_direct) CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
       }
     }
@@ -729,7 +736,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     int32_t* act_a = ar.get<int32_t>(nA);
     int32_t* act_w = ar.zeros<int32_t>(nA);
     const int64_t ldc_ = round_up(H, 4);
-    const bool big_c = (double)G * ldc_ * csz > 64e6;
+    const bool big_c = (double)G * ldc_ * csz > 100e6;  // vs the 126 MB L2
     if (big_c) {
       // C far larger than L2: active A tuples in row (g) order, so the expand's atomics walk
       // C row by row and stay L2-local
