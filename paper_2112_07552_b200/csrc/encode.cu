@@ -42,25 +42,26 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
   if (!c.data || c.n <= 0) return;
   ColStats* s = st + blockIdx.y;
   const int64_t stride = (int64_t)gridDim.x * T;
+  const int64_t gtid = (int64_t)blockIdx.x * T + threadIdx.x;
+  // 16-byte vector loads, two in flight per thread; the scalar tail (< 4 items) after
+  const int64_t n4 = (reinterpret_cast<uintptr_t>(c.data) & 15) ? 0 : c.n / 4;
   if (c.type == 2) {  // fp32
     float mn = INFINITY, mx = -INFINITY, mabs = INFINITY;
     int nonfinite = 0;
     const float* p = static_cast<const float*>(c.data);
-    // 4 independent loads in flight per thread (the scan is latency-bound otherwise)
-    for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < c.n; i0 += 4 * stride) {
-      float x[4];
+    const float4* p4 = static_cast<const float4*>(c.data);
+    auto take = [&](float x) {
+      if (!isfinite(x)) nonfinite = 1;
+      mn = fminf(mn, x); mx = fmaxf(mx, x); mabs = fminf(mabs, fabsf(x));
+    };
+    for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
+      float4 x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + u * stride;
-        x[u] = i < c.n ? __ldcs(p + i) : 0.f;
-      }
+      for (int u = 0; u < 4; ++u) x[u] = i0 + u * stride < n4 ? __ldcs(p4 + i0 + u * stride) : x[0];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i0 + u * stride >= c.n) break;
-        if (!isfinite(x[u])) nonfinite = 1;
-        mn = fminf(mn, x[u]); mx = fmaxf(mx, x[u]); mabs = fminf(mabs, fabsf(x[u]));
-      }
+      for (int u = 0; u < 4; ++u) { take(x[u].x); take(x[u].y); take(x[u].z); take(x[u].w); }
     }
+    for (int64_t i = n4 * 4 + gtid; i < c.n; i += stride) take(__ldcs(p + i));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -75,6 +76,36 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
       atomicMax(&s->mx, ord(mx));
       atomicMin(&s->min_abs, ord(mabs));
       if (nonfinite) atomicOr(&s->flags, 1);
+    }
+    return;
+  }
+  if (c.type == 0) {  // int32: 32-bit compares, widened once at the end
+    int mn = INT_MAX, mx = INT_MIN;
+    unsigned mabs = UINT_MAX;
+    const int* p = static_cast<const int*>(c.data);
+    const int4* p4 = static_cast<const int4*>(c.data);
+    auto take = [&](int x) {
+      mn = min(mn, x); mx = max(mx, x);
+      mabs = min(mabs, x < 0 ? 0u - (unsigned)x : (unsigned)x);
+    };
+    for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
+      int4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = i0 + u * stride < n4 ? __ldcs(p4 + i0 + u * stride) : x[0];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { take(x[u].x); take(x[u].y); take(x[u].z); take(x[u].w); }
+    }
+    for (int64_t i = n4 * 4 + gtid; i < c.n; i += stride) take(__ldcs(p + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mabs = min(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+    }
+    if (lane_id() == 0) {
+      atomicMin(&s->mn, (long long)mn);
+      atomicMax(&s->mx, (long long)mx);
+      atomicMin(&s->min_abs, (long long)mabs);
     }
     return;
   }
@@ -469,6 +500,59 @@ __global__ void __launch_bounds__(1024) k_probe_smem(ColDesc key, ColDesc grp, D
     if (s_cnt[k]) atomicAdd(cnt_k + k, s_cnt[k]);
 }
 
+// Same result as k_probe_smem for int32 columns whose key and group dictionaries are
+// both direct (code = table[x - min]) and small: the two code tables sit in shared
+// memory next to the counters (a random gather from shared memory costs a few bank
+// conflicts; from L1 it costs one wavefront per distinct 128-byte line), and each
+// thread moves 16-byte vectors: 4 keys + 4 groups in, 4 + 4 codes out.
+__global__ void __launch_bounds__(1024) k_probe_direct_smem(const int32_t* __restrict__ key,
+                                                            const int32_t* __restrict__ grp, int64_t n,
+                                                            DictView kd, DictView gd, int32_t* __restrict__ kcode,
+                                                            int32_t* __restrict__ gcode,
+                                                            int32_t* __restrict__ cnt_k, int K) {
+  extern __shared__ int32_t s_cnt[];
+  int32_t* s_kd = s_cnt + K;
+  int32_t* s_gd = s_kd + kd.size;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) s_cnt[k] = 0;
+  for (int i = threadIdx.x; i < (int)kd.size; i += blockDim.x) s_kd[i] = __ldg(kd.code + i);
+  for (int i = threadIdx.x; i < (int)gd.size; i += blockDim.x) s_gd[i] = __ldg(gd.code + i);
+  __syncthreads();
+  const unsigned ks = (unsigned)kd.size, gs = (unsigned)gd.size;
+  const int kmin = (int)kd.minv, gmin = (int)gd.minv;
+  auto one = [&](int x, int y, int& kc, int& gc) {
+    const unsigned ok = (unsigned)x - (unsigned)kmin, og = (unsigned)y - (unsigned)gmin;
+    kc = ok < ks ? s_kd[ok] : -1;
+    gc = og < gs ? s_gd[og] : -1;
+    if (kc >= 0) atomicAdd(s_cnt + kc, 1);
+  };
+  const int64_t n4 = n / 4;
+  const int4* k4 = reinterpret_cast<const int4*>(key);
+  const int4* g4 = reinterpret_cast<const int4*>(grp);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n4; v += 2 * stride) {
+    const bool two = v + stride < n4;
+    const int4 xa = __ldcs(k4 + v), ya = __ldcs(g4 + v);
+    int4 xb = xa, yb = ya;
+    if (two) { xb = __ldcs(k4 + v + stride); yb = __ldcs(g4 + v + stride); }
+    int4 ka, ga, kb, gb;
+    one(xa.x, ya.x, ka.x, ga.x); one(xa.y, ya.y, ka.y, ga.y);
+    one(xa.z, ya.z, ka.z, ga.z); one(xa.w, ya.w, ka.w, ga.w);
+    reinterpret_cast<int4*>(kcode)[v] = ka;
+    reinterpret_cast<int4*>(gcode)[v] = ga;
+    if (two) {
+      one(xb.x, yb.x, kb.x, gb.x); one(xb.y, yb.y, kb.y, gb.y);
+      one(xb.z, yb.z, kb.z, gb.z); one(xb.w, yb.w, kb.w, gb.w);
+      reinterpret_cast<int4*>(kcode)[v + stride] = kb;
+      reinterpret_cast<int4*>(gcode)[v + stride] = gb;
+    }
+  }
+  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    one(key[i], grp[i], kcode[i], gcode[i]);
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    if (s_cnt[k]) atomicAdd(cnt_k + k, s_cnt[k]);
+}
+
 __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, DictView gd,
                         int32_t* __restrict__ kcode, int32_t* __restrict__ gcode, int32_t* __restrict__ cnt_k,
                         double* __restrict__ rowabs_g) {
@@ -565,7 +649,7 @@ cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, 
   k_init_stats<<<1, 32, 0, s>>>(st, 6);
   int64_t nmax = 1;
   for (int i = 0; i < 6; ++i) if (cols[i].data && cols[i].n > nmax) nmax = cols[i].n;
-  dim3 grid(grid_for(nmax, T * 8), 6);
+  dim3 grid(grid_for(nmax, T * 16), 6);
   k_col_stats<<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st);
   if (launches) *launches += 2;
   return cudaGetLastError();
@@ -695,6 +779,26 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
   // privatized counters when the key domain fits in shared memory and there are
   // enough tuples per block to amortize the per-block flush
   const int64_t smem = K * 4;
+  auto fits_i32 = [](long long v) { return v >= INT_MIN && v <= INT_MAX; };
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const int64_t smem_d = smem + 4 * (int64_t)(kd.size + gd.size);
+  if (!rowabs_g && K > 0 && key.n >= 4 * K && key.type == 0 && grp.type == 0 && kd.mode == 0 && gd.mode == 0 &&
+      fits_i32(kd.minv) && fits_i32(gd.minv) && smem_d <= 100 * 1024 && al16(key.data) && al16(grp.data) &&
+      al16(kcode) && al16(gcode)) {
+    static bool attr_d = false;
+    if (!attr_d) {
+      cudaFuncSetAttribute(k_probe_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      attr_d = true;
+    }
+    int64_t blocks = key.n / 4096;
+    if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
+    if (blocks < 1) blocks = 1;
+    k_probe_direct_smem<<<(int)blocks, 1024, (size_t)smem_d, s>>>(static_cast<const int32_t*>(key.data),
+                                                                  static_cast<const int32_t*>(grp.data), key.n, kd,
+                                                                  gd, kcode, gcode, cnt_k, (int)K);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   if (!rowabs_g && K > 0 && smem <= 200 * 1024 && key.n >= 4 * K) {
     static bool attr = false;
     if (!attr) {

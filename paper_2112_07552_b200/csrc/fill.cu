@@ -17,6 +17,7 @@
 //                a second pass writes lo = bf16(x - hi) for the 3-product split.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -103,6 +104,213 @@ __global__ void k_fill_bf16_direct(const int32_t* __restrict__ kcode, const int3
   }
   inexact = __any_sync(0xffffffffu, inexact);
   if (lane_id() == 0 && inexact) atomicOr(&fs->inexact, 1);
+}
+
+// ---- binned bf16 direct fill: the same result as k_fill_bf16_direct without the
+// scattered 2-byte stores into HBM. Rows are grouped into bands of R rows (a band is one
+// shared-memory tile of R x Kp bf16) and bands into coarse bins of P bands:
+//   hist    per-(coarse bin, block) counts + global per-band totals
+//   scatter tuples -> 8-byte entries grouped by coarse bin, staged in shared memory per
+//           4096-tuple batch so the stores go out as runs (<= 256 coarse bins)
+//   split   one CTA per coarse bin -> 4-byte entries grouped by band (<= 64 write fronts)
+//   tile    one CTA per band builds its tile in shared memory and writes it out
+//           coalesced (zeros included, so no memset)
+// Coarse entry: band-in-bin << 32 | cell-in-band << 16 | bf16; band entry: the low 32 bits.
+constexpr int kBinThreads = 1024;
+constexpr int kBinBatch = 4 * kBinThreads;
+constexpr int kBinMaxCoarse = 256;
+
+__global__ void __launch_bounds__(kBinThreads) k_bin_hist(const int32_t* __restrict__ kcode,
+                                                          const int32_t* __restrict__ rcode, int64_t n,
+                                                          int64_t chunk, int R, int P, int nband, int ncoarse,
+                                                          int32_t* __restrict__ counts,
+                                                          int32_t* __restrict__ band_total) {
+  extern __shared__ int32_t hist[];  // per band
+  for (int b = threadIdx.x; b < nband; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = max(lo, min(n, lo + chunk));  // chunk % 4 == 0
+  auto one = [&](int kc, int r) { if (kc >= 0) atomicAdd(&hist[r / R], 1); };
+  const int64_t v1 = hi / 4;
+  for (int64_t v = lo / 4 + threadIdx.x; v < v1; v += blockDim.x) {
+    const int4 k = __ldg(reinterpret_cast<const int4*>(kcode) + v);
+    const int4 r = __ldg(reinterpret_cast<const int4*>(rcode) + v);
+    one(k.x, r.x); one(k.y, r.y); one(k.z, r.z); one(k.w, r.w);
+  }
+  for (int64_t i = v1 * 4 + threadIdx.x; i < hi; i += blockDim.x) one(kcode[i], rcode[i]);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nband; b += blockDim.x)
+    if (hist[b]) atomicAdd(band_total + b, hist[b]);
+  for (int c = threadIdx.x; c < ncoarse; c += blockDim.x) {
+    int sum = 0;
+    for (int b = c * P; b < min(nband, (c + 1) * P); ++b) sum += hist[b];
+    counts[(int64_t)c * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const int32_t* __restrict__ kcode,
+                                                             const int32_t* __restrict__ rcode,
+                                                             const float* __restrict__ val, int64_t n, int64_t chunk,
+                                                             int R, int P, int ncoarse, int64_t Kp,
+                                                             const int64_t* __restrict__ coffs,
+                                                             unsigned long long* __restrict__ ent,
+                                                             FillStats* __restrict__ fs) {
+  __shared__ unsigned long long stage[kBinBatch];
+  __shared__ uint8_t sbin[kBinBatch];
+  __shared__ int64_t gcur[kBinMaxCoarse];
+  __shared__ int cnt[kBinMaxCoarse], bstart[kBinMaxCoarse];
+  for (int c = threadIdx.x; c < ncoarse; c += blockDim.x) {
+    gcur[c] = coffs[(int64_t)c * gridDim.x + blockIdx.x];
+    cnt[c] = 0;
+  }
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = max(lo, min(n, lo + chunk));
+  const int RP = R * P;
+  const bool vec_val = val && (reinterpret_cast<uintptr_t>(val) & 15) == 0;
+  int inexact = 0;
+  for (int64_t i0 = lo; i0 < hi; i0 += kBinBatch) {
+    const int64_t i = i0 + 4 * threadIdx.x;
+    int kc[4] = {-1, -1, -1, -1}, r[4] = {0, 0, 0, 0};
+    uint32_t b[4] = {0x3F800000u, 0x3F800000u, 0x3F800000u, 0x3F800000u};  // absent value = 1.0
+    if (i + 3 < hi) {
+      const int4 k4 = __ldg(reinterpret_cast<const int4*>(kcode + i));
+      const int4 r4 = __ldg(reinterpret_cast<const int4*>(rcode + i));
+      kc[0] = k4.x; kc[1] = k4.y; kc[2] = k4.z; kc[3] = k4.w;
+      r[0] = r4.x; r[1] = r4.y; r[2] = r4.z; r[3] = r4.w;
+      if (vec_val) {
+        const uint4 b4 = __ldcs(reinterpret_cast<const uint4*>(val + i));
+        b[0] = b4.x; b[1] = b4.y; b[2] = b4.z; b[3] = b4.w;
+      } else if (val) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = __float_as_uint(val[i + u]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u < hi) {
+          kc[u] = kcode[i + u];
+          r[u] = rcode[i + u];
+          if (val) b[u] = __float_as_uint(val[i + u]);
+        }
+    }
+    int cb[4], rank[4];
+    unsigned long long e[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      cb[u] = -1;
+      if (kc[u] < 0) continue;
+      inexact |= (b[u] & 0xFFFFu) != 0u;
+      cb[u] = r[u] / RP;
+      const int band = r[u] / R;
+      const uint32_t cell = (uint32_t)((r[u] - band * R) * Kp + kc[u]);  // < R * Kp <= 65536
+      e[u] = ((unsigned long long)(band - cb[u] * P) << 32) | (cell << 16) | (b[u] >> 16);
+      rank[u] = atomicAdd(&cnt[cb[u]], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of <= 256 counts by one warp, 8 per lane
+      int v[8], s = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = threadIdx.x * 8 + j;
+        v[j] = c < ncoarse ? cnt[c] : 0;
+        s += v[j];
+      }
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)threadIdx.x >= o) incl += t;
+      }
+      int run = incl - s;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = threadIdx.x * 8 + j;
+        if (c < ncoarse) bstart[c] = run;
+        run += v[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (cb[u] >= 0) {
+        const int j = bstart[cb[u]] + rank[u];
+        stage[j] = e[u];
+        sbin[j] = (uint8_t)cb[u];
+      }
+    __syncthreads();
+    const int total = bstart[ncoarse - 1] + cnt[ncoarse - 1];
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      const int c = sbin[j];
+      ent[gcur[c] + (j - bstart[c])] = stage[j];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < ncoarse; c += blockDim.x) {
+      gcur[c] += cnt[c];
+      cnt[c] = 0;
+    }
+    __syncthreads();
+  }
+  inexact = __syncthreads_or(inexact);
+  if (threadIdx.x == 0 && inexact) atomicOr(&fs->inexact, 1);
+}
+
+// One CTA per coarse bin: its 8-byte entries -> 4-byte entries at their band's position.
+__global__ void __launch_bounds__(kBinThreads) k_bin_split(const unsigned long long* __restrict__ ent,
+                                                           const int64_t* __restrict__ coffs, int nblk, int P,
+                                                           int nband, const int64_t* __restrict__ boffs,
+                                                           uint32_t* __restrict__ out) {
+  __shared__ int64_t base[64];
+  __shared__ int cur[64];
+  const int c = blockIdx.x;
+  for (int f = threadIdx.x; f < P; f += blockDim.x) {
+    base[f] = c * P + f < nband ? boffs[c * P + f] : 0;
+    cur[f] = 0;
+  }
+  __syncthreads();
+  const int64_t lo = coffs[(int64_t)c * nblk], hi = coffs[(int64_t)(c + 1) * nblk];
+  // few write fronts (P bands) shared by the whole CTA: warp-aggregated cursor updates
+  for (int64_t i0 = lo + (threadIdx.x & ~31); i0 < hi; i0 += blockDim.x) {
+    const int64_t i = i0 + lane_id();
+    const unsigned long long e = i < hi ? __ldcs(ent + i) : 0ull;
+    const int f = i < hi ? (int)(e >> 32) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, f);
+    const int leader = __ffs(peers) - 1;
+    int rel = 0;
+    if (f >= 0 && lane_id() == leader) rel = atomicAdd(&cur[f], __popc(peers));
+    rel = __shfl_sync(0xffffffffu, rel, leader);
+    if (f >= 0) out[base[f] + rel + __popc(peers & lanemask_lt())] = (uint32_t)e;
+  }
+}
+
+// One CTA per band: tile in shared memory, occupancy bits detect a second tuple in a cell.
+__global__ void k_bin_tile(const uint32_t* __restrict__ ent, const int64_t* __restrict__ boffs, int R, int64_t Kp,
+                           int64_t rows, uint16_t* __restrict__ op, int64_t ld_op, FillStats* __restrict__ fs) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int cells = R * (int)Kp;
+  uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
+  unsigned* occ = reinterpret_cast<unsigned*>(smem + (size_t)cells * 2);
+  const int words = cells / 32;
+  for (int i = threadIdx.x; i < cells / 8; i += blockDim.x) reinterpret_cast<uint4*>(tile)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) occ[i] = 0;
+  __syncthreads();
+  const int band = blockIdx.x;
+  const int64_t lo = boffs[band], hi = boffs[band + 1];
+  int dup = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint32_t e = __ldcs(ent + i);
+    const uint32_t c = e >> 16;
+    tile[c] = (uint16_t)(e & 0xFFFFu);
+    dup |= (int)((atomicOr(&occ[c >> 5], 1u << (c & 31)) >> (c & 31)) & 1u);
+  }
+  __syncthreads();
+  const int64_t r0 = (int64_t)band * R;
+  const int nrow = (int)(rows - r0 < R ? rows - r0 : R);
+  const int v8 = (int)(Kp / 8);  // 16-byte vectors per row
+  for (int i = threadIdx.x; i < nrow * v8; i += blockDim.x) {
+    const int r = i / v8, c = i - r * v8;
+    __stcs(reinterpret_cast<uint4*>(op + (r0 + r) * ld_op) + c, reinterpret_cast<const uint4*>(tile + (int64_t)r * Kp)[c]);
+  }
+  dup = __syncthreads_or(dup);
+  if (threadIdx.x == 0 && dup) atomicOr(&fs->overflow, 1);
 }
 
 // Wide integer fill into int64 scratch (COUNT: +1, SUM: +v), wrapping adds.
@@ -252,6 +460,85 @@ cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, 
   k_fill_bf16_direct<<<grid_for(n), T, 0, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, op, ld_op,
                                                occ, ld_occ, fs);
   if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+namespace {
+constexpr int kBinTileBytes = 64 * 1024;  // 3 tiles per SM
+constexpr int kBinMaxBands = 8192;
+constexpr int kBinBlocks = kNumSMs * 2;  // 1024-thread blocks, 2 per SM
+constexpr int kBinTileThreads = 512;
+struct BinPlan {
+  int R = 0, P = 0, nband = 0, ncoarse = 0, nblk = 0;
+  int64_t chunk = 0;
+  size_t off_counts = 0, off_coffs = 0, off_btot = 0, off_boffs = 0, off_temp = 0, off_ent8 = 0, off_ent4 = 0,
+         bytes = 0;
+};
+inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+BinPlan bin_plan(int64_t n, int64_t rows, int64_t Kp) {
+  BinPlan p;
+  if (n < (1 << 20) || Kp * 2 > kBinTileBytes || Kp % 32) return p;
+  int R = 1;
+  while (2 * R * Kp * 2 <= kBinTileBytes && R < rows) R *= 2;
+  const int64_t nband = (rows + R - 1) / R;
+  if (nband > kBinMaxBands) return p;
+  int P = 1;
+  while ((nband + P - 1) / P > kBinMaxCoarse) P *= 2;
+  if (P > 64) return p;
+  p.R = R;
+  p.P = P;
+  p.nband = (int)nband;
+  p.ncoarse = (int)((nband + P - 1) / P);
+  p.nblk = (int)std::min<int64_t>(kBinBlocks, (n + 8191) / 8192);
+  p.chunk = ((n + p.nblk - 1) / p.nblk + 3) & ~int64_t(3);  // 16-byte aligned chunks
+  const int64_t m = (int64_t)p.ncoarse * p.nblk;
+  p.off_counts = 0;
+  p.off_coffs = al256(m * 4);
+  p.off_btot = p.off_coffs + al256((m + 1) * 8);
+  p.off_boffs = p.off_btot + al256(nband * 4);
+  p.off_temp = p.off_boffs + al256((nband + 1) * 8);
+  p.off_ent8 = p.off_temp + al256(std::max(scan_temp_bytes(m), scan_temp_bytes(nband)));
+  p.off_ent4 = p.off_ent8 + al256(n * 8);
+  p.bytes = p.off_ent4 + al256(n * 4);
+  return p;
+}
+}  // namespace
+
+size_t fill_bf16_binned_ws(int64_t n, int64_t rows, int64_t Kp) { return bin_plan(n, rows, Kp).bytes; }
+
+cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                    int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
+                                    cudaStream_t s, int64_t* launches) {
+  const BinPlan p = bin_plan(n, rows, Kp);
+  if (!p.bytes) return cudaErrorInvalidValue;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int32_t* counts = reinterpret_cast<int32_t*>(w + p.off_counts);
+  int64_t* coffs = reinterpret_cast<int64_t*>(w + p.off_coffs);
+  int32_t* btot = reinterpret_cast<int32_t*>(w + p.off_btot);
+  int64_t* boffs = reinterpret_cast<int64_t*>(w + p.off_boffs);
+  auto* ent8 = reinterpret_cast<unsigned long long*>(w + p.off_ent8);
+  uint32_t* ent4 = reinterpret_cast<uint32_t*>(w + p.off_ent4);
+  const int64_t m = (int64_t)p.ncoarse * p.nblk;
+  cudaError_t e = cudaMemsetAsync(btot, 0, (size_t)p.nband * 4, s);
+  if (e != cudaSuccess) return e;
+  k_bin_hist<<<p.nblk, kBinThreads, p.nband * 4, s>>>(kcode, rcode, n, p.chunk, p.R, p.P, p.nband, p.ncoarse,
+                                                      counts, btot);
+  if ((e = exclusive_scan_i32(counts, coffs, m, coffs + m, w + p.off_temp, s, launches)) != cudaSuccess) return e;
+  if ((e = exclusive_scan_i32(btot, boffs, p.nband, boffs + p.nband, w + p.off_temp, s, launches)) != cudaSuccess)
+    return e;
+  k_bin_scatter<<<p.nblk, kBinThreads, 0, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, p.chunk, p.R,
+                                               p.P, p.ncoarse, Kp, coffs, ent8, fs);
+  k_bin_split<<<p.ncoarse, kBinThreads, 0, s>>>(ent8, coffs, p.nblk, p.P, p.nband, boffs, ent4);
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_bin_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBinTileBytes + kBinTileBytes / 16);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tile_smem = (int)(p.R * Kp * 2 + p.R * Kp / 8);
+  k_bin_tile<<<p.nband, kBinTileThreads, tile_smem, s>>>(ent4, boffs, p.R, Kp, rows, op, ld_op, fs);
+  if (launches) *launches += 4;
   return cudaGetLastError();
 }
 

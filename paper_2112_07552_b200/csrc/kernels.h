@@ -99,6 +99,14 @@ cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, in
 cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                     uint16_t* op, int64_t ld_op, unsigned* occ, int64_t ld_occ, FillStats* fs,
                                     cudaStream_t s, int64_t* launches);
+// Binned variant of the bf16 direct fill (row bands built in shared memory, written out
+// coalesced including zeros). fill_bf16_binned_ws returns the workspace bytes, 0 when the
+// shape does not fit the scheme (caller uses the direct fill). Duplicate cells set
+// fs->overflow; inexact values set fs->inexact.
+size_t fill_bf16_binned_ws(int64_t n, int64_t rows, int64_t Kp);
+cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                    int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
+                                    cudaStream_t s, int64_t* launches);
 // Pattern plane op[r][k] = 1 where a cell holds >= 1 tuple; symmetric adjacency for triangles.
 cudaError_t launch_fill_pattern_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
                                    cudaStream_t s, int64_t* launches);

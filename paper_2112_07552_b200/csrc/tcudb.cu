@@ -586,20 +586,33 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       fB = ar.get<uint16_t>(Hp * ldop);
       if (nA <= cellsA && nB <= cellsB) {
         // optimistic: <= 1 tuple per cell and bf16-exact values -> the cells are the values
-        CK(cudaMemset2DAsync(fA, ldop * 2, 0, Kp * 2, Gp, s));
-        CK(cudaMemset2DAsync(fB, ldop * 2, 0, Kp * 2, Hp, s));
-        unsigned* occA = ar.zeros<unsigned>(cellsA / 32 + 1);
-        unsigned* occB = ar.zeros<unsigned>(cellsB / 32 + 1);
-        CK(launch_fill_bf16_direct(kA, gA, av, nA, fA, ldop, occA, Kp, fs + 0, s, L));
-        CK(launch_fill_bf16_direct(kB, hB, bw, nB, fB, ldop, occB, Kp, fs + 1, s, L));
-        CK(launch_popcount(occA, cellsA / 32 + 1, 0xFFFFFFFFu, &fs[0].nnz, s, L));
-        CK(launch_popcount(occB, cellsB / 32 + 1, 0xFFFFFFFFu, &fs[1].nnz, s, L));
+        // per side: binned (tile in shared memory, duplicate -> overflow) when the shape
+        // fits, else scattered stores + occupancy bits whose popcount must equal the tuples
+        bool binned[2];
+        auto direct_fill = [&](int side, const int32_t* kc, const int32_t* rc, const ColDesc& v, int64_t n,
+                               int64_t rows, uint16_t* op) {
+          const char* nb = getenv("TCUDB_NO_BINNED_FILL");
+          const size_t ws = (nb && nb[0] == '1') ? 0 : fill_bf16_binned_ws(n, rows, Kp);
+          binned[side] = ws != 0;
+          if (ws) {
+            CK(launch_fill_bf16_binned(kc, rc, v, n, rows, Kp, op, ldop, fs + side, ar.get<uint8_t>(ws), s, L));
+          } else {
+            CK(cudaMemset2DAsync(op, ldop * 2, 0, Kp * 2, rows, s));
+            unsigned* occ = ar.zeros<unsigned>(rows * Kp / 32 + 1);
+            CK(launch_fill_bf16_direct(kc, rc, v, n, op, ldop, occ, Kp, fs + side, s, L));
+            CK(launch_popcount(occ, rows * Kp / 32 + 1, 0xFFFFFFFFu, &fs[side].nnz, s, L));
+          }
+        };
+        direct_fill(0, kA, gA, av, nA, Gp, fA);
+        direct_fill(1, kB, hB, bw, nB, Hp, fB);
         CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         FillStats hf[2];
         std::memcpy(hf, ctx->pinned, sizeof(hf));
-        // one set occupancy bit per written tuple <=> no cell holds two tuples
-        bf16_direct = hf[0].nnz == misc[3] && hf[1].nnz == misc[4] && !(hf[0].inexact | hf[1].inexact);
+        auto no_dup = [&](int side, int64_t tuples) {
+          return binned[side] ? !hf[side].overflow : hf[side].nnz == tuples;
+        };
+        bf16_direct = no_dup(0, misc[3]) && no_dup(1, misc[4]) && !(hf[0].inexact | hf[1].inexact);
         if (!bf16_direct) CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
       }
     }

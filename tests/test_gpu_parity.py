@@ -142,6 +142,33 @@ def test_zero_sum_groups_kept(engine, torch_mod, oracle_mod):
         assert st["existence"] == 1
 
 
+@pytest.mark.parametrize("case", ["unique_exact", "dups_exact", "unique_inexact"])
+@pytest.mark.parametrize("G", [1024, 8576])  # 64 bands in 64 coarse bins; 536 bands, 4 per coarse bin
+def test_float_direct_fill_guard_large(engine, torch_mod, oracle_mod, case, G):
+    """float SUM with >= 2^20 A tuples: the binned bf16 direct fill (row bands in shared
+    memory) must detect a second tuple in a cell and non-bf16 values and hand over to the
+    fp32-scratch path; every case matches the oracle (R9 tolerance)."""
+    rng = np.random.default_rng({"unique_exact": 11, "dups_exact": 12, "unique_inexact": 13}[case] + G)
+    K, n = 2048, 1_200_000
+    if case == "dups_exact":
+        cell = rng.integers(0, G * K, n)
+    else:
+        cell = rng.permutation(G * K)[:n]
+    if case == "unique_inexact":
+        v = rng.standard_normal(n).astype(np.float32)
+    else:
+        v = (rng.integers(-64, 65, n) / 8).astype(np.float32)
+    A = datagen.Table((cell % K).astype(np.int32), (cell // K).astype(np.int32), v)
+    nb = 3000
+    B = datagen.Table(rng.integers(0, K, nb).astype(np.int32), rng.integers(0, 50, nb).astype(np.int32),
+                      (rng.integers(-8, 9, nb) / 4).astype(np.float32))
+    ref = oracle_mod.join_agg(A, B, "sum")
+    out, st = run(engine, torch_mod, A, B, "sum", 1)
+    compare(out, ref, "sum", float_vals=True)
+    if case == "unique_exact":
+        assert st["elem"] == 1
+
+
 # ---------------------------------------------------------------- configs (reduced + full)
 @pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c1s", 1.0), ("c2", 0.1), ("c3", 1 / 16), ("c4", 1 / 1024),
                                         ("c5", 1 / 256), ("c5s", 1 / 256)])
