@@ -22,6 +22,16 @@ TCUDB_DEV int64_t ld_int(const void* p, int type, int64_t i) {
                    : (int64_t)__ldg(reinterpret_cast<const int*>(p) + i);
 }
 
+// 16-byte streaming load as volatile asm: a batch of these stays batched (ptxas may
+// otherwise interleave each load with its consumers and serialize the latency).
+TCUDB_DEV int4 ld_stream_v4(const void* p) {
+  int4 v;
+  asm volatile("ld.global.cs.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // ------------------------------------------------------------------ mbarrier
 TCUDB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

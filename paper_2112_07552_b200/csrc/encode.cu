@@ -15,6 +15,7 @@
 //     and — for the group domains — an LSD radix sort of the distinct values so
 //     codes are ascending ranks (result order = (g,h) order).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -33,6 +34,27 @@ TCUDB_DEV unsigned long long fmix64(unsigned long long k) {
 }
 
 // ------------------------------------------------------------------ a1: statistics
+// Block-level reduction, then ONE set of atomics per block: same-address global
+// atomics serialize in L2 (~1 ns each), so per-warp atomics from thousands of warps
+// cost more than the column scan itself.
+__device__ __forceinline__ void col_stats_finish(ColStats* s, long long mn, long long mx, long long mabs, int flags) {
+  __shared__ long long smn[T / 32], smx[T / 32], sab[T / 32];
+  __shared__ int sfl[T / 32];
+  mn = warp_min_ll(mn); mx = warp_max_ll(mx); mabs = warp_min_ll(mabs);
+  flags = __any_sync(0xffffffffu, flags);
+  if (lane_id() == 0) { smn[warp_id()] = mn; smx[warp_id()] = mx; sab[warp_id()] = mabs; sfl[warp_id()] = flags; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < T / 32; ++w) {
+      mn = min(mn, smn[w]); mx = max(mx, smx[w]); mabs = min(mabs, sab[w]); flags |= sfl[w];
+    }
+    atomicMin(&s->mn, mn);
+    atomicMax(&s->mx, mx);
+    atomicMin(&s->min_abs, mabs);
+    if (flags) atomicOr(&s->flags, 1);
+  }
+}
+
 // blockIdx.y = column id. Integer columns: min / max (int64). Float columns:
 // min / max / min |x| (ordered-int encodings of fp32).
 __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColDesc c4, ColDesc c5,
@@ -57,26 +79,17 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
       float4 x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = i0 + u * stride < n4 ? __ldcs(p4 + i0 + u * stride) : x[0];
+      for (int u = 0; u < 4; ++u) {  // clamped index: a repeat is harmless for min/max
+        const int4 t = ld_stream_v4(p4 + min(i0 + u * stride, n4 - 1));
+        x[u] = make_float4(__int_as_float(t.x), __int_as_float(t.y), __int_as_float(t.z), __int_as_float(t.w));
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) { take(x[u].x); take(x[u].y); take(x[u].z); take(x[u].w); }
     }
     for (int64_t i = n4 * 4 + gtid; i < c.n; i += stride) take(__ldcs(p + i));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mabs = fminf(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
-    }
-    nonfinite = __any_sync(0xffffffffu, nonfinite);
-    if (lane_id() == 0) {
-      // fp32 -> order-preserving int: flip for negatives
-      auto ord = [](float f) { int b = __float_as_int(f); return b >= 0 ? (long long)b : (long long)(b ^ 0x7fffffff); };
-      atomicMin(&s->mn, ord(mn));
-      atomicMax(&s->mx, ord(mx));
-      atomicMin(&s->min_abs, ord(mabs));
-      if (nonfinite) atomicOr(&s->flags, 1);
-    }
+    // fp32 -> order-preserving int: flip for negatives
+    auto ord = [](float f) { int b = __float_as_int(f); return b >= 0 ? (long long)b : (long long)(b ^ 0x7fffffff); };
+    col_stats_finish(s, ord(mn), ord(mx), ord(mabs), nonfinite);
     return;
   }
   if (c.type == 0) {  // int32: 32-bit compares, widened once at the end
@@ -91,22 +104,12 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
       int4 x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = i0 + u * stride < n4 ? __ldcs(p4 + i0 + u * stride) : x[0];
+      for (int u = 0; u < 4; ++u) x[u] = ld_stream_v4(p4 + min(i0 + u * stride, n4 - 1));  // clamped: a repeat is harmless
 #pragma unroll
       for (int u = 0; u < 4; ++u) { take(x[u].x); take(x[u].y); take(x[u].z); take(x[u].w); }
     }
     for (int64_t i = n4 * 4 + gtid; i < c.n; i += stride) take(__ldcs(p + i));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mabs = min(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
-    }
-    if (lane_id() == 0) {
-      atomicMin(&s->mn, (long long)mn);
-      atomicMax(&s->mx, (long long)mx);
-      atomicMin(&s->min_abs, (long long)mabs);
-    }
+    col_stats_finish(s, (long long)mn, (long long)mx, (long long)mabs, 0);
     return;
   }
   long long mn = LLONG_MAX, mx = LLONG_MIN, mabs = LLONG_MAX;
@@ -125,8 +128,7 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
       mabs = min(mabs, a);
     }
   }
-  mn = warp_min_ll(mn); mx = warp_max_ll(mx); mabs = warp_min_ll(mabs);
-  if (lane_id() == 0) { atomicMin(&s->mn, mn); atomicMax(&s->mx, mx); atomicMin(&s->min_abs, mabs); }
+  col_stats_finish(s, mn, mx, mabs, 0);
 }
 
 __global__ void k_init_stats(ColStats* st, int n) {
@@ -649,7 +651,7 @@ cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, 
   k_init_stats<<<1, 32, 0, s>>>(st, 6);
   int64_t nmax = 1;
   for (int i = 0; i < 6; ++i) if (cols[i].data && cols[i].n > nmax) nmax = cols[i].n;
-  dim3 grid(grid_for(nmax, T * 16), 6);
+  dim3 grid((unsigned)std::min<int64_t>(2 * kNumSMs, (nmax + T * 16 - 1) / (T * 16)), 6);
   k_col_stats<<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st);
   if (launches) *launches += 2;
   return cudaGetLastError();

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(const int32_t* __restr
   }
 }
 
-__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const int32_t* __restrict__ kcode,
+__global__ void __launch_bounds__(kBinThreads, 2) k_bin_scatter(const int32_t* __restrict__ kcode,
                                                              const int32_t* __restrict__ rcode,
                                                              const float* __restrict__ val, int64_t n, int64_t chunk,
                                                              int R, int P, int ncoarse, int64_t Kp,
