@@ -10,8 +10,8 @@
 //   direct-offset (span <= 4n): presence flags over [min, max], codes = exclusive
 //     scan of the flags (ascending by construction);
 //   hash (otherwise): open-addressing table of 2^ceil(log2 2n) slots keyed by
-//     (x - min) with warp-aggregated inserts (__match_any_sync de-duplicates
-//     equal keys inside a warp before the CAS), side flags, compaction by scan,
+//     (x - min); an insert reads the slot first (a present key costs no atomic)
+//     and CASes only an empty slot; side flags, compaction by scan,
 //     and — for the group domains — an LSD radix sort of the distinct values so
 //     codes are ascending ranks (result order = (g,h) order).
 #include <cuda_runtime.h>
@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(1024) k_mark_direct_smem(ColDesc c, long long 
 // Slot key = (x - min) as u64; EMPTY = ~0. Linear probing; equal keys in a warp
 // are inserted once (warp aggregation). flags[slot] = 1 marks the side.
 __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __restrict__ slots,
-                              unsigned long long mask, uint8_t* __restrict__ flags, int* __restrict__ overflow) {
+                              unsigned long long mask, uint8_t* __restrict__ flags, int* __restrict__ overflow,
+                              int32_t* __restrict__ row_slot) {
   constexpr int U = 4;  // elements per thread per iteration: the first-probe loads overlap
   const int64_t stride = (int64_t)gridDim.x * T;
   const int64_t n_round = (c.n + 31) & ~int64_t(31);
@@ -204,10 +205,9 @@ __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __r
     for (int u = 0; u < U; ++u) cur[u] = ok[u] ? __ldcg(slots + h[u]) : 0ull;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (i0 + u * stride >= n_round) break;  // warp-uniform (n_round is a multiple of 32)
-      const unsigned act = __ballot_sync(0xffffffffu, ok[u]);
-      const unsigned peers = __match_any_sync(0xffffffffu, off[u]) & act;
-      if (!ok[u] || (__ffs(peers) - 1) != lane_id()) continue;  // lowest active peer lane inserts
+      // no warp de-duplication (match.any on 64-bit values costs more than it saves):
+      // equal keys in flight both find the slot by the plain read or by the CAS's return
+      if (!ok[u]) continue;
       unsigned long long hh = h[u], cc = cur[u];
       bool placed = false;
       for (unsigned long long step = 0; step <= mask; ++step) {  // bounded: a full table is reported
@@ -220,6 +220,7 @@ __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __r
         hh = (hh + 1) & mask;
         cc = __ldcg(slots + hh);
       }
+      if (row_slot) row_slot[i0 + u * stride] = placed ? (int32_t)hh : -1;
       if (!placed) { *overflow = 1; continue; }
       if (!flags[hh]) flags[hh] = 1;
     }
@@ -462,6 +463,22 @@ TCUDB_DEV void dict_lookup_batch(const DictView& d, const long long* x, const bo
   for (int u = 0; u < U; ++u) out[u] = (ok[u] && k[u] == off[u]) ? __ldg(d.code + h[u]) : -1;
 }
 
+// Codes of rows i0 + u * stride: through the insert's per-row slots when present
+// (code[row_slot[i]], one gather from an L2-sized table), else by value.
+template <int U>
+TCUDB_DEV void rows_lookup(const DictView& d, const long long* x, const bool* ok, int64_t i0, int64_t stride,
+                           int32_t* out) {
+  if (d.row_slot) {
+    int32_t sl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sl[u] = ok[u] ? __ldcs(d.row_slot + i0 + u * stride) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) out[u] = sl[u] >= 0 ? __ldg(d.code + sl[u]) : -1;
+    return;
+  }
+  dict_lookup_batch<U>(d, x, ok, out);
+}
+
 // kcode / gcode per tuple; per-key counts (warp-aggregated); per-group tuple
 // counts and sum |v| of tuples whose key survives the ∩ (guard bounds, a3).
 // Variant with the per-key counters privatized in shared memory (small key
@@ -569,11 +586,11 @@ __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, Dict
   for (int u = 0; u < U; ++u) {
     const int64_t i = i0 + u * stride;
     okv[u] = i < key.n;
-    xk[u] = okv[u] ? ld_int(key.data, key.type, i) : 0;
-    xg[u] = okv[u] ? ld_int(grp.data, grp.type, i) : 0;
+    xk[u] = okv[u] && !kd.row_slot ? ld_int(key.data, key.type, i) : 0;
+    xg[u] = okv[u] && !gd.row_slot ? ld_int(grp.data, grp.type, i) : 0;
   }
-  dict_lookup_batch<U>(kd, xk, okv, kcv);
-  dict_lookup_batch<U>(gd, xg, okv, gcv);
+  rows_lookup<U>(kd, xk, okv, i0, stride, kcv);
+  rows_lookup<U>(gd, xg, okv, i0, stride, gcv);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t i = i0 + u * stride;
@@ -692,9 +709,9 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 }
 
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, int* overflow, cudaStream_t s, int64_t* launches) {
+                               uint8_t* flags, int* overflow, int32_t* row_slot, cudaStream_t s, int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
-  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags, overflow);
+  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags, overflow, row_slot);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

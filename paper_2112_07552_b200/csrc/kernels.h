@@ -32,6 +32,9 @@ struct DictView {
   unsigned long long size;
   const int32_t* code;
   const unsigned long long* slots;
+  // hash mode, optional: slot of each row of the column this view is probed with (written
+  // by the insert): the lookup is then code[row_slot[i]], no rehash or table walk
+  const int32_t* row_slot;
 };
 
 // ---------------------------------------------------------------- encode.cu
@@ -41,9 +44,10 @@ cudaError_t launch_hll(const ColDesc& c, unsigned* regs, cudaStream_t s, int64_t
 cudaError_t launch_col_stats(const ColDesc* cols6, ColStats* st, cudaStream_t s, int64_t* launches);
 cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
                                int64_t* launches);
-// Warp-aggregated open-addressing insert of (x - minv); *overflow = 1 if the table is full.
+// Open-addressing insert of (x - minv); *overflow = 1 if the table is full; row_slot
+// (optional, c.n entries) receives each row's slot.
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, int* overflow, cudaStream_t s, int64_t* launches);
+                               uint8_t* flags, int* overflow, int32_t* row_slot, cudaStream_t s, int64_t* launches);
 size_t pred_temp_bytes(int64_t n);
 // codes = exclusive scan of pred(i) (-1 where false); optional dict[code] = minv + i (direct
 // group domains: the sorted value dictionary comes out of the same pass).
@@ -137,10 +141,13 @@ cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const
                                cudaStream_t s, int64_t* launches);
 cudaError_t launch_work(const int32_t* kcode, int64_t n, const int32_t* cnt_b, int32_t* work, cudaStream_t s,
                         int64_t* launches);
-// Active A tuples grouped by row g (counting sort): act_a[]/act_w[] (zeroed act_w tail),
-// gcnt (zeroed, G), goff (G), gcur (zeroed, G) are scratch.
-cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const int32_t* cnt_b, int64_t n, int G,
+// Active A tuples grouped by band g / R (counting sort): act_a[]/act_w[] (zeroed act_w
+// tail); with nb = ceil(G / R): gcnt (zeroed, nb), goff (nb + 1, total at goff[nb]), gcur
+// (zeroed, nb).
+// Optional (non-NULL bstart): act_b[] = bucket start of the tuple's key, act_g[] = its row.
+cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const int32_t* cnt_b, int64_t n, int G, int R,
                                int32_t* gcnt, int64_t* goff, int32_t* gcur, int32_t* act_a, int32_t* act_w,
+                               const int64_t* bstart, int64_t* act_b, int32_t* act_g,
                                void* scan_tmp, cudaStream_t s, int64_t* launches);
 cudaError_t launch_flags_from_work(const int32_t* work, int64_t n, int32_t* flags, cudaStream_t s,
                                    int64_t* launches);
@@ -158,6 +165,33 @@ struct ExpandArgs {
   int* ovf;        // acc_kind 4 (COUNT, packed u16, ldc even): set when a count passes 65535
 };
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s, int64_t* launches);
+
+// ---------------------------------------------------------------- spa.cu (a7 + a8 fused, sparse path)
+struct SpaArgs {
+  int64_t G, H;
+  const int64_t* goff;     // nbands + 1: active-tuple range of each band of `rows` rows (tuples grouped by band)
+  const int32_t* act_a;    // active A tuples (row index into A), g-ordered
+  const int64_t* act_off;  // n_act + 1: first update of each active tuple (exclusive scan of cntB[k])
+  const int64_t* act_b;    // bucket start of each active tuple's key
+  const int32_t* act_g;    // row (group code) of each active tuple
+  const int32_t* kcodeA; const int32_t* gcodeA; ColDesc va;
+  const int64_t* bstart; const int32_t* b_h; const void* b_w;
+  int w_kind;              // 0 none (1), 1 int64, 2 f32
+  int acc_kind;            // 0 COUNT int32, 1 COUNT int64, 2 int SUM int64 (wrapping), 3 float SUM f64
+  int64_t words;           // 32-bit bitmap words per row (set by spa_plan)
+  int rows;                // rows per band = per CTA of the write pass (set by spa_plan)
+  int64_t nbands;          // ceil(G / rows) (set by spa_plan)
+  int count_bands;         // bands per CTA of the count pass (set by spa_plan)
+  int32_t* row_nnz;        // count pass output (G)
+  const int64_t* row_out;  // write pass input: exclusive scan of row_nnz
+  const long long* dict_g; const long long* dict_h;
+  int g_out_type, h_out_type;  // 0 I32, 1 I64
+  void* out_g; void* out_h; void* out_agg;
+};
+// false when one result row does not fit in shared memory (the caller keeps the C path)
+bool spa_plan(SpaArgs& a);
+cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches);
+cudaError_t launch_spa_write(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 
 // ---------------------------------------------------------------- partition.cu (§8(e))
 cudaError_t launch_part_count(const ColDesc& grp, const long long* bounds, int P, unsigned long long* counts,

@@ -1,0 +1,311 @@
+// spa.cu — step a7 + a8 fused for the sparse path: row-wise expansion into
+// shared-memory accumulators (a sparse accumulator, "SPA", per result row) and
+// direct compaction from shared memory.
+//
+// PAPER.md §4.2.4 sends low-density joins to a sparse product; the
+// result matrix is then turned back into a table by nonzero() (§3.2).
+// Materializing C = G x H in HBM (zeroing it, scattering J atomics into it, and
+// reading it twice for count + write) dominates that path when G x H is large
+// (c3: 40k x 40k). Here no C exists:
+//   A tuples are ordered by group code g (counting sort, sparse.cu), so the
+//   updates of result rows [g0, g1) are one contiguous range of the update
+//   sequence (update u of active tuple t hits bucket entry bstart[k_t] + u - off_t).
+//   count pass: one CTA per band of rows; a presence bitmap per row in shared
+//               memory (atomicOr), then popcounts -> row_nnz[g];
+//   scan:       row_out = exclusive scan of row_nnz (the result allocation is
+//               exact: n_result = total);
+//   write pass: one CTA per (smaller) band; value cells + bitmap in shared
+//               memory (shared-memory atomics), then each row is written in h
+//               order straight to (g, h, agg) at row_out[g] — codes are ranks, so
+//               the output is in (g, h) order like the dense path's.
+// Both passes split each band's updates evenly over the CTA's warps; a warp maps 32
+// consecutive updates to their tuples with one ballot + one OR-reduction (spa_expand).
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tcudb {
+namespace {
+
+constexpr int NT = 1024;
+constexpr size_t kSmemMax = 216 * 1024;  // dynamic; + ~8.5 KB static (write pass) <= 227 KB
+
+__device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+  return (int64_t)__shfl_sync(0xffffffffu, (long long)v, src);
+}
+
+// Largest t in [lo, hi) with off[t] <= u (off ascending, off[lo] <= u): 32-way search,
+// one coalesced probe round per factor of 32.
+__device__ __forceinline__ int64_t warp_find(const int64_t* __restrict__ off, int64_t lo, int64_t hi, int64_t u) {
+  const int lane = lane_id();
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const unsigned m = __ballot_sync(0xffffffffu, p < hi && off[p] <= u);
+    lo = lo + (int64_t)(31 - __clz(m)) * step;
+    hi = min(hi, lo + step);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, lo + lane < hi && off[lo + lane] <= u);
+  return lo + (31 - __clz(m));
+}
+
+// Calls f(row_in_band, h, bucket_pos, a_index) for every update of the CTA's band of
+// rows [g0, g0 + rows) (active tuples are grouped by band: goff[band]).
+// The band's update range is split evenly over the CTA's warps; each warp then works
+// alone (no CTA barriers): a window of 32 consecutive active tuples sits one per lane,
+// and for 32 consecutive updates the owning tuple of update base + p is
+//   (last tuple starting <= base) + #(tuple starts in (base, base + p]),
+// from one ballot and one OR-reduction of the window's start bits.
+template <bool NEED_A, class F>
+__device__ __forceinline__ void spa_expand(const SpaArgs& a, int64_t t_begin, int64_t t_end, int64_t g0, F f) {
+  const int lane = lane_id(), wid = warp_id(), nw = (int)(blockDim.x >> 5);
+  if (t_begin >= t_end) return;
+  const int64_t U0 = a.act_off[t_begin], U1 = a.act_off[t_end];
+  const int64_t per = (U1 - U0 + nw - 1) / nw;
+  int64_t u = U0 + (int64_t)wid * per;
+  const int64_t uend = min(U1, u + per);
+  if (u >= uend) return;
+  int64_t t = warp_find(a.act_off, t_begin, t_end, u);
+  while (u < uend) {
+    const int64_t tl = t + lane;
+    const bool valid = tl < t_end;
+    const int64_t o = valid ? a.act_off[tl] : LLONG_MAX;
+    const int64_t b = valid ? a.act_b[tl] : 0;
+    const int gr = valid ? a.act_g[tl] - (int)g0 : 0;
+    const int ai = (NEED_A && valid) ? a.act_a[tl] : 0;
+    const int64_t wend = min(uend, t + 32 < t_end ? a.act_off[t + 32] : U1);
+    for (; u < wend; u += 128) {
+      int64_t pp[4];
+      int rr[4], aa[4], hh[4];
+      bool ok[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t base = u + 32 * j;  // warp-uniform
+        ok[j] = base + lane < wend;
+        const unsigned le = __ballot_sync(0xffffffffu, o <= base);
+        const int l0 = 31 - __clz(le);
+        const int64_t d = o - base;
+        const unsigned st = __reduce_or_sync(0xffffffffu, (d > 0 && d < 32) ? (1u << (int)d) : 0u);
+        const int l = (l0 + __popc(st & ((2u << lane) - 1u))) & 31;
+        const int64_t ol = shfl64(o, l), bl = shfl64(b, l);
+        rr[j] = __shfl_sync(0xffffffffu, gr, l);
+        aa[j] = NEED_A ? __shfl_sync(0xffffffffu, ai, l) : 0;
+        pp[j] = bl + (base + lane - ol);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) hh[j] = ok[j] ? __ldg(a.b_h + pp[j]) : 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ok[j]) f(rr[j], hh[j], pp[j], aa[j]);
+    }
+    u = wend;
+    t += 32;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_spa_count(const SpaArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  // count_bands consecutive bands per CTA (their tuples are contiguous)
+  const int64_t b0 = (int64_t)blockIdx.x * a.count_bands;
+  const int64_t b1 = min(a.nbands, b0 + a.count_bands);
+  const int64_t g0 = b0 * a.rows;
+  const int64_t g1 = min(a.G, b1 * a.rows);
+  const int nr = (int)(g1 - g0);
+  const int64_t W = a.words;
+  unsigned* bits = reinterpret_cast<unsigned*>(smem);
+  for (int i = threadIdx.x; i < nr * (int)W; i += NT) bits[i] = 0u;
+  __syncthreads();
+  spa_expand<false>(a, a.goff[b0], a.goff[b1], g0, [&](int r, int h, int64_t, int32_t) {
+    atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
+  });
+  __syncthreads();
+  for (int r = warp_id(); r < nr; r += NT / 32) {
+    int c = 0;
+    for (int64_t w = lane_id(); w < W; w += 32) c += __popc(bits[r * W + w]);
+    c = warp_sum(c);
+    if (lane_id() == 0) a.row_nnz[g0 + r] = c;
+  }
+}
+
+template <int ACC>
+struct AccT;
+template <> struct AccT<0> { using T = int; };
+template <> struct AccT<1> { using T = unsigned long long; };
+template <> struct AccT<2> { using T = unsigned long long; };
+template <> struct AccT<3> { using T = double; };
+
+template <int ACC>
+__global__ void __launch_bounds__(NT) k_spa_write(const SpaArgs a) {
+  using T = typename AccT<ACC>::T;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int64_t s_base[NT / 32 + 1];
+  __shared__ uint8_t s_stage[NT / 32][256];
+  const int64_t g0 = (int64_t)blockIdx.x * a.rows;
+  const int64_t g1 = min(a.G, g0 + a.rows);
+  const int nr = (int)(g1 - g0);
+  const int64_t W = a.words, ldc = W * 32;
+  T* acc = reinterpret_cast<T*>(smem);
+  unsigned* bits = reinterpret_cast<unsigned*>(acc + (size_t)a.rows * ldc);
+  {  // zero the cells with 16-byte stores (a row is a multiple of 128 bytes)
+    const int nv = (int)((size_t)nr * ldc * sizeof(T) / 16);
+    for (int i = threadIdx.x; i < nv; i += NT) reinterpret_cast<uint4*>(acc)[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = threadIdx.x; i < nr * (int)W; i += NT) bits[i] = 0u;
+  __syncthreads();
+  spa_expand<(ACC >= 2)>(a, a.goff[blockIdx.x], a.goff[blockIdx.x + 1], g0, [&](int r, int h, int64_t pos, int32_t ai) {
+    const int64_t cell = r * ldc + h;
+    if constexpr (ACC == 0) {
+      atomicAdd(acc + cell, 1);
+      atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
+    } else if constexpr (ACC == 1) {
+      atomicAdd(acc + cell, 1ull);
+      atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
+    } else if constexpr (ACC == 2) {
+      const long long v = a.va.data ? ld_int(a.va.data, a.va.type, ai) : 1;
+      const long long w = a.w_kind == 1 ? static_cast<const long long*>(a.b_w)[pos] : 1;
+      atomicAdd(acc + cell, (unsigned long long)v * (unsigned long long)w);  // wrapping, exact mod 2^64
+      atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
+    } else {
+      const double v = a.va.data ? (double)__ldg(static_cast<const float*>(a.va.data) + ai) : 1.0;
+      const double w = a.w_kind == 2 ? (double)static_cast<const float*>(a.b_w)[pos] : 1.0;
+      atomicAdd(acc + cell, v * w);
+      atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
+    }
+  });
+  __syncthreads();
+  // each row: warps own contiguous slices of 8-word (256-cell) groups. Per group, lane l
+  // takes byte l of the group's bitmap, the warp prefix-sums the byte popcounts, the set
+  // cells go to a per-warp staging list (u8 offsets), and the list is written out with
+  // all 32 lanes active (coalesced (g, h, agg) stores, one dict_h gather per output).
+  const int nw = NT / 32, wid = warp_id(), lane = lane_id();
+  uint8_t* stage = s_stage[wid];
+  const int ngrp = (int)((W + 7) / 8);
+  const int per = (ngrp + nw - 1) / nw;
+  const int q0 = min(ngrp, wid * per), q1 = min(ngrp, q0 + per);
+  for (int r = 0; r < nr; ++r) {
+    const int64_t g = g0 + r;
+    const unsigned* rb = bits + r * W;
+    const uint8_t* rbytes = reinterpret_cast<const uint8_t*>(rb);
+    const int nbytes = (int)W * 4;
+    int c = 0;
+    for (int i = q0 * 32 + lane; i < q1 * 32 && i < nbytes; i += 32) c += __popc(rbytes[i]);
+    c = warp_sum(c);
+    if (lane == 0) s_base[wid] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t run = a.row_out[g];
+      for (int i = 0; i < nw; ++i) { const int64_t x = s_base[i]; s_base[i] = run; run += x; }
+    }
+    __syncthreads();
+    int64_t base = s_base[wid];
+    const long long gv = a.dict_g[g];
+    const T* arow = acc + (int64_t)r * ldc;
+    for (int q = q0; q < q1; ++q) {
+      const int bi = q * 32 + lane;
+      unsigned m = bi < nbytes ? rbytes[bi] : 0u;
+      const int cnt = __popc(m);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) continue;
+      int p = incl - cnt;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        stage[p++] = (uint8_t)(lane * 8 + b);
+        m &= m - 1;
+      }
+      __syncwarp();
+      const int64_t hq = (int64_t)q * 256;
+      for (int j = lane; j < total; j += 32) {
+        const int64_t h = hq + stage[j];
+        const int64_t o = base + j;
+        const long long hv = __ldg(a.dict_h + h);
+        if (a.g_out_type) __stcs(static_cast<long long*>(a.out_g) + o, gv);
+        else __stcs(static_cast<int*>(a.out_g) + o, (int)gv);
+        if (a.h_out_type) __stcs(static_cast<long long*>(a.out_h) + o, hv);
+        else __stcs(static_cast<int*>(a.out_h) + o, (int)hv);
+        const T x = arow[h];
+        if constexpr (ACC == 3) __stcs(static_cast<double*>(a.out_agg) + o, x);
+        else __stcs(static_cast<long long*>(a.out_agg) + o, (long long)x);
+      }
+      __syncwarp();
+      base += total;
+    }
+    __syncthreads();  // s_base reuse
+  }
+}
+
+}  // namespace
+
+bool spa_plan(SpaArgs& a) {
+  a.words = (a.H + 31) / 32;
+  const size_t row_bits = (size_t)a.words * 4;
+  const size_t cell = a.acc_kind == 0 ? 4 : 8;
+  const size_t row_w = (size_t)a.words * 32 * cell + row_bits;
+  if (row_w + 1024 > kSmemMax) return false;
+  // one band of rows per CTA in both passes: ~2 waves of 1-CTA-per-SM bands
+  const int64_t want = std::max<int64_t>(1, (a.G + 2 * kNumSMs - 1) / (2 * kNumSMs));
+  a.rows = (int)std::min<int64_t>(want, (int64_t)((kSmemMax - 1024) / row_w));
+  if (a.rows < 1) return false;
+  a.nbands = (a.G + a.rows - 1) / a.rows;
+  // count pass: bitmaps only, so several bands per CTA (<= 48 KB, >= ~4 CTAs per SM of work)
+  const int64_t by_smem = std::max<int64_t>(1, (int64_t)(48 * 1024 / (row_bits * a.rows)));
+  const int64_t by_grid = std::max<int64_t>(1, a.nbands / (4 * kNumSMs));
+  a.count_bands = (int)std::min(by_smem, by_grid);
+  return true;
+}
+
+static size_t count_smem(const SpaArgs& a) { return (size_t)a.count_bands * a.rows * a.words * 4; }
+static size_t write_smem(const SpaArgs& a) {
+  const size_t cell = a.acc_kind == 0 ? 4 : 8;
+  return (size_t)a.rows * a.words * 32 * cell + (size_t)a.rows * a.words * 4;
+}
+
+cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.G <= 0) return cudaSuccess;
+  const size_t sm = count_smem(a);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_spa_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_spa_count<<<(unsigned)((a.nbands + a.count_bands - 1) / a.count_bands), NT, sm, s>>>(a);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+template <int ACC>
+static cudaError_t launch_write_t(const SpaArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_spa_write<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kSmemMax);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_spa_write<ACC><<<(unsigned)((a.G + a.rows - 1) / a.rows), NT, write_smem(a), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spa_write(const SpaArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.G <= 0) return cudaSuccess;
+  cudaError_t e;
+  switch (a.acc_kind) {
+    case 0: e = launch_write_t<0>(a, s); break;
+    case 1: e = launch_write_t<1>(a, s); break;
+    case 2: e = launch_write_t<2>(a, s); break;
+    default: e = launch_write_t<3>(a, s);
+  }
+  if (launches) ++*launches;
+  return e;
+}
+
+}  // namespace tcudb

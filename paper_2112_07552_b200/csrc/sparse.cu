@@ -13,6 +13,7 @@
 //      atomic C[g][h] += v·w (int32 / int64 wrapping / fp64) plus an optional
 //      COUNT plane for existence (reading R3).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -71,7 +72,7 @@ __global__ void k_compact_active(const int32_t* __restrict__ work, const int64_t
 // which stays L2-resident instead of scattering atomics over the whole matrix.
 __global__ void __launch_bounds__(1024) k_active_g_count(const int32_t* __restrict__ kcode,
                                                          const int32_t* __restrict__ gcode,
-                                                         const int32_t* __restrict__ cnt_b, int64_t n, int G,
+                                                         const int32_t* __restrict__ cnt_b, int64_t n, int G, int R,
                                                          int32_t* __restrict__ gcnt, int use_smem) {
   extern __shared__ int32_t s_cnt[];
   if (use_smem) {
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(1024) k_active_g_count(const int32_t* __restri
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int32_t kc = kcode[i];
     if (kc < 0 || cnt_b[kc] == 0) continue;
-    atomicAdd((use_smem ? s_cnt : gcnt) + gcode[i], 1);
+    atomicAdd((use_smem ? s_cnt : gcnt) + gcode[i] / R, 1);
   }
   if (use_smem) {
     __syncthreads();
@@ -92,9 +93,10 @@ __global__ void __launch_bounds__(1024) k_active_g_count(const int32_t* __restri
 }
 
 __global__ void k_active_g_scatter(const int32_t* __restrict__ kcode, const int32_t* __restrict__ gcode,
-                                   const int32_t* __restrict__ cnt_b, int64_t n, const int64_t* __restrict__ goff,
+                                   const int32_t* __restrict__ cnt_b, int64_t n, int R, const int64_t* __restrict__ goff,
                                    int32_t* __restrict__ gcur, int32_t* __restrict__ act_a,
-                                   int32_t* __restrict__ act_w) {
+                                   int32_t* __restrict__ act_w, const int64_t* __restrict__ bstart,
+                                   int64_t* __restrict__ act_b, int32_t* __restrict__ act_g) {
   const int64_t stride = (int64_t)gridDim.x * T;
   for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
     const int32_t kc = kcode[i];
@@ -102,9 +104,54 @@ __global__ void k_active_g_scatter(const int32_t* __restrict__ kcode, const int3
     const int32_t w = cnt_b[kc];
     if (w == 0) continue;
     const int32_t g = gcode[i];
-    const int64_t pos = goff[g] + atomicAdd(gcur + g, 1);
+    const int64_t pos = goff[g / R] + atomicAdd(gcur + g / R, 1);
     act_a[pos] = (int32_t)i;
     act_w[pos] = w;
+    if (bstart) {
+      act_b[pos] = bstart[kc];
+      act_g[pos] = g;
+    }
+  }
+}
+
+// Same output as k_active_g_scatter for small G, without same-address contention on
+// gcur[g] (c5: 16M tuples over 4,096 rows): each CTA counts its chunk per g in shared
+// memory, reserves each g's range with one global atomic, then places its tuples with
+// shared-memory cursors (a second read of the chunk, from L2).
+__global__ void __launch_bounds__(1024) k_active_g_scatter_smem(
+    const int32_t* __restrict__ kcode, const int32_t* __restrict__ gcode, const int32_t* __restrict__ cnt_b,
+    int64_t n, int64_t chunk, int G, int R, const int64_t* __restrict__ goff, int32_t* __restrict__ gcur,
+    int32_t* __restrict__ act_a, int32_t* __restrict__ act_w, const int64_t* __restrict__ bstart,
+    int64_t* __restrict__ act_b, int32_t* __restrict__ act_g) {
+  extern __shared__ int64_t s_base[];
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(s_base + G);
+  for (int g = threadIdx.x; g < G; g += blockDim.x) s_cnt[g] = 0;
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int32_t kc = kcode[i];
+    if (kc >= 0 && cnt_b[kc] > 0) atomicAdd(s_cnt + gcode[i] / R, 1);
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const int c = s_cnt[g];
+    s_base[g] = c ? goff[g] + atomicAdd(gcur + g, c) : 0;
+    s_cnt[g] = 0;
+  }
+  __syncthreads();
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int32_t kc = kcode[i];
+    if (kc < 0) continue;
+    const int32_t w = cnt_b[kc];
+    if (w == 0) continue;
+    const int32_t g = gcode[i];
+    const int64_t pos = s_base[g / R] + atomicAdd(s_cnt + g / R, 1);
+    act_a[pos] = (int32_t)i;
+    act_w[pos] = w;
+    if (bstart) {
+      act_b[pos] = bstart[kc];
+      act_g[pos] = g;
+    }
   }
 }
 
@@ -193,23 +240,41 @@ cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const
 }
 
 cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const int32_t* cnt_b, int64_t n, int G,
-                               int32_t* gcnt, int64_t* goff, int32_t* gcur, int32_t* act_a, int32_t* act_w,
+                               int R, int32_t* gcnt, int64_t* goff, int32_t* gcur, int32_t* act_a, int32_t* act_w,
+                               const int64_t* bstart, int64_t* act_b, int32_t* act_g,
                                void* scan_tmp, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
-  const bool smem = (int64_t)G * 4 <= 160 * 1024;
+  const int nb = (G + R - 1) / R;  // bands
+  const bool smem = (int64_t)nb * 4 <= 160 * 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_active_g_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
-  int64_t blocks = n / std::max<int64_t>(4096, G / 2);
+  int64_t blocks = n / std::max<int64_t>(4096, nb / 2);
   if (blocks > kNumSMs) blocks = kNumSMs;
   if (blocks < 1) blocks = 1;
-  k_active_g_count<<<(int)blocks, 1024, smem ? (size_t)G * 4 : 0, s>>>(kcode, gcode, cnt_b, n, G, gcnt, smem);
+  k_active_g_count<<<(int)blocks, 1024, smem ? (size_t)nb * 4 : 0, s>>>(kcode, gcode, cnt_b, n, nb, R, gcnt, smem);
   if (launches) ++*launches;
-  cudaError_t e = exclusive_scan_i32(gcnt, goff, G, nullptr, scan_tmp, s, launches);
+  cudaError_t e = exclusive_scan_i32(gcnt, goff, nb, goff + nb, scan_tmp, s, launches);
   if (e != cudaSuccess) return e;
-  k_active_g_scatter<<<grid_for(n), T, 0, s>>>(kcode, gcode, cnt_b, n, goff, gcur, act_a, act_w);
+  // few bands (<= 1024) and many tuples: per-CTA reservation (one global atomic per CTA and
+  // band; the CTA's run per band is long enough to fill whole sectors); else one global
+  // atomic per tuple (many bands: little contention)
+  if (nb <= 1024 && n >= (1 << 20)) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_active_g_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 1024);
+      attr2 = true;
+    }
+    const int64_t nblk = std::min<int64_t>(2 * kNumSMs, (n + 16383) / 16384);
+    const int64_t chunk = (n + nblk - 1) / nblk;
+    k_active_g_scatter_smem<<<(int)nblk, 1024, (size_t)nb * 12, s>>>(kcode, gcode, cnt_b, n, chunk, nb, R, goff,
+                                                                    gcur, act_a, act_w, bstart, act_b, act_g);
+  } else {
+    k_active_g_scatter<<<grid_for(n), T, 0, s>>>(kcode, gcode, cnt_b, n, R, goff, gcur, act_a, act_w, bstart, act_b,
+                                                  act_g);
+  }
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -39,6 +39,7 @@ struct tcudb_ctx {
   int64_t launches = 0;
   void* pinned = nullptr;      // small D2H staging
   void* pinned_big = nullptr;  // sketch registers (3 x kHllM x 4 B)
+  size_t mem_free0 = 0;        // free device memory at creation (path-selection budget)
   cudaEvent_t ev[8] = {};
   std::mutex mu;
   // pinned host block cache for host-API results: size -> free blocks
@@ -121,13 +122,16 @@ struct Dict {
   int64_t count = 0;
   int bits = 64;              // significant bits of (x - min) for the radix sort
   int* ovf = nullptr;         // hash mode: table-full flag (the estimate was too small)
-  DictView view() const {
+  int32_t* slot1 = nullptr;   // hash mode: slot of each row of the first / second column
+  int32_t* slot2 = nullptr;
+  DictView view(int col = 0) const {
     DictView v;
     v.mode = mode;
     v.minv = minv;
     v.size = mode == 0 ? span : span - 1;
     v.code = code;
     v.slots = slots;
+    v.row_slot = col == 1 ? slot1 : col == 2 ? slot2 : nullptr;
     return v;
   }
 };
@@ -199,13 +203,16 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     CK(cudaMemsetAsync(d.slots, 0xFF, cap * sizeof(unsigned long long), s));
     d.fa = ar.zeros<uint8_t>((int64_t)cap);
     d.ovf = ar.zeros<int>(1);
-    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, s, launches));
+    // per-row slots: the probe then reads code[slot] instead of rehashing and walking the table
+    d.slot1 = ar.get<int32_t>(c1.n);
+    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, s, launches));
     if (c2) {
+      d.slot2 = ar.get<int32_t>(c2->n);
       if (intersect) {
         d.fb = ar.zeros<uint8_t>((int64_t)cap);
-        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, s, launches));
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, d.slot2, s, launches));
       } else {
-        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, s, launches));
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot2, s, launches));
       }
     }
     d.code = ar.get<int32_t>((int64_t)cap);
@@ -390,8 +397,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     cntB = ar.zeros<int32_t>(Ku);
     double* rowA = int_sum ? ar.zeros<double>(Gu) : nullptr;
     double* rowB = int_sum ? ar.zeros<double>(Hu) : nullptr;
-    CK(launch_probe(ak, ag, av, DK.view(), DG.view(), kA, gA, cntA, rowA, Ku, s, L));
-    CK(launch_probe(bk, bh, bw, DK.view(), DH.view(), kB, hB, cntB, rowB, Ku, s, L));
+    CK(launch_probe(ak, ag, av, DK.view(1), DG.view(1), kA, gA, cntA, rowA, Ku, s, L));
+    CK(launch_probe(bk, bh, bw, DK.view(2), DH.view(1), kB, hB, cntB, rowB, Ku, s, L));
     unsigned long long* d_misc = ar.zeros<unsigned long long>(6);
     CK(launch_join_size(cntA, cntB, Ku, d_misc + 0, s, L));
     if (int_sum) {
@@ -478,9 +485,9 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 3 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
-  // cudaMemGetInfo costs ~0.3-0.5 ms of host time: only consult it for large working sets
-  size_t free_b = (size_t)1 << 62, total_b = 0;
-  if (std::max(dense_bytes, sparse_bytes) > 4e9) cudaMemGetInfo(&free_b, &total_b);
+  // memory budget: the device's free memory when the context was created (a live
+  // cudaMemGetInfo per query costs 0.3 ms to tens of ms of host time)
+  const size_t free_b = ctx->mem_free0;
   bool dense;
   if (q->flags & TCUDB_FORCE_DENSE) dense = true;
   else if (q->flags & TCUDB_FORCE_SPARSE) dense = false;
@@ -499,6 +506,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   int32_t* seg_cnt = nullptr;  // per-segment counts from the GEMM epilogue (dense path)
   ExpandArgs sparse_u16{};     // sparse COUNT in u16 cells (kept to redo in int32 on overflow)
   sparse_u16.acc_kind = -1;
+  bool spa = false;            // sparse path through spa.cu (no C matrix)
+  SpaArgs sa{};
   ca.G = G; ca.H = H;
   ca.dict_g = DG.dict; ca.dict_h = DH.dict;
   ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
@@ -750,13 +759,45 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     int32_t* act_w = ar.zeros<int32_t>(nA);
     const int64_t ldc_ = round_up(H, 4);
     const bool big_c = (double)G * ldc_ * csz > 100e6;  // vs the 126 MB L2
-    if (big_c) {
+    // fused row-wise expand + compaction in shared memory (spa.cu) whenever one result
+    // row fits in shared memory: no C in HBM at all
+    sa.G = G; sa.H = H;
+    sa.acc_kind = !is_sum ? (J < (1ull << 31) ? 0 : 1) : (is_float ? 3 : 2);
+    const char* no_spa = getenv("TCUDB_NO_SPA");
+    spa = !(no_spa && no_spa[0] == '1') && spa_plan(sa);
+    if (spa) {
+      const int64_t nb = (G + sa.rows - 1) / sa.rows;  // bands of sa.rows rows, one per CTA
+      int32_t* gcnt = ar.zeros<int32_t>(nb);
+      int32_t* gcur = ar.zeros<int32_t>(nb);
+      int64_t* goff = ar.get<int64_t>(nb + 1);
+      int64_t* act_b = ar.get<int64_t>(nA);
+      int32_t* act_g = ar.get<int32_t>(nA);
+      CK(launch_active_by_g(kA, gA, cntB, nA, (int)G, sa.rows, gcnt, goff, gcur, act_a, act_w, bstart, act_b, act_g,
+                            tmp, s, L));
+      sa.act_b = act_b; sa.act_g = act_g;
+      int64_t* act_off = ar.get<int64_t>(nA + 1);
+      CK(exclusive_scan_i32(act_w, act_off, nA, act_off + nA, tmp, s, L));
+      sa.goff = goff; sa.act_a = act_a; sa.act_off = act_off;
+      sa.kcodeA = kA; sa.gcodeA = gA; sa.va = av;
+      sa.bstart = bstart; sa.b_h = b_h; sa.b_w = b_w; sa.w_kind = w_kind;
+      sa.row_nnz = ar.get<int32_t>(G);
+      int64_t* row_out = ar.get<int64_t>(G + 1);
+      CK(launch_spa_count(sa, s, L));
+      void* tmpg = ar.get<char>((int64_t)scan_temp_bytes(std::max<int64_t>(G, 1)));
+      CK(exclusive_scan_i32(sa.row_nnz, row_out, G, row_out + G, tmpg, s, L));
+      sa.row_out = row_out;
+      sa.dict_g = DG.dict; sa.dict_h = DH.dict;
+      sa.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
+      sa.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
+      tm.mark(&S.ms_sparse);
+    } else if (big_c) {
       // C far larger than L2: active A tuples in row (g) order, so the expand's atomics walk
       // C row by row and stay L2-local
       int32_t* gcnt = ar.zeros<int32_t>(G);
       int32_t* gcur = ar.zeros<int32_t>(G);
-      int64_t* goff = ar.get<int64_t>(G);
-      CK(launch_active_by_g(kA, gA, cntB, nA, (int)G, gcnt, goff, gcur, act_a, act_w, tmp, s, L));
+      int64_t* goff = ar.get<int64_t>(G + 1);
+      CK(launch_active_by_g(kA, gA, cntB, nA, (int)G, 1, gcnt, goff, gcur, act_a, act_w, nullptr, nullptr, nullptr,
+                            tmp, s, L));
     } else {
       // C fits in L2: keep the input order (atomics spread over all of C, no hot rows)
       int32_t* work = ar.get<int32_t>(nA);
@@ -767,6 +808,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       CK(exclusive_scan_i32(flg, pos, nA, nullptr, tmp, s, L));
       CK(launch_compact_active(work, pos, nA, act_a, act_w, s, L));
     }
+    if (!spa) {
     int64_t* act_off = ar.get<int64_t>(nA);
     CK(exclusive_scan_i32(act_w, act_off, nA, nullptr, tmp, s, L));
     const int64_t ldc = round_up(H, 4);
@@ -797,12 +839,13 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     ca.seg_w = 256;
     CK(launch_expand(ea, s, L));
     tm.mark(&S.ms_sparse);
+    }  // !spa
   }
 
   // ---------------- a8 compaction
-  void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
-  int64_t* d_nnz = ar.get<int64_t>(1);
-  CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
+  void* ctmp = spa ? nullptr : ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
+  int64_t* d_nnz = spa ? const_cast<int64_t*>(sa.row_out) + G : ar.get<int64_t>(1);
+  if (!spa) CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
   int64_t nnz;
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
@@ -834,7 +877,12 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     char* base = static_cast<char*>(result_alloc(ctx, oa + (size_t)nnz * 8, s));
     r.g = base + og; r.h = base + oh; r.agg = base + oa;
     ca.out_g = r.g; ca.out_h = r.h; ca.out_agg = r.agg;
-    CK(launch_compact_write(ca, ctmp, s, L));
+    if (spa) {
+      sa.out_g = r.g; sa.out_h = r.h; sa.out_agg = r.agg;
+      CK(launch_spa_write(sa, s, L));
+    } else {
+      CK(launch_compact_write(ca, ctmp, s, L));
+    }
   } catch (...) {
     result_release(ctx, r.g);
     throw;
@@ -907,6 +955,11 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   unsigned long long thr = ~0ull;
   cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   if (cudaMallocHost(&c->pinned, kPinnedBytes) != cudaSuccess) { delete c; return TCUDB_E_CUDA; }
+  {
+    size_t fb = 0, tb = 0;
+    if (cudaMemGetInfo(&fb, &tb) != cudaSuccess) { cudaGetLastError(); fb = (size_t)1 << 62; }
+    c->mem_free0 = fb;
+  }
   if (cudaMallocHost(&c->pinned_big, sizeof(unsigned) * 3 * kHllM) != cudaSuccess) {
     cudaFreeHost(c->pinned);
     delete c;

@@ -169,6 +169,36 @@ def test_float_direct_fill_guard_large(engine, torch_mod, oracle_mod, case, G):
         assert st["elem"] == 1
 
 
+@pytest.mark.parametrize("spa", ["1", "0"])  # fused shared-memory SPA path / C-matrix path
+@pytest.mark.parametrize("case", ["c3", "c5", "c5s", "wide_h", "skew_sum_float", "skew_sum_int"])
+def test_sparse_spa_and_matrix_paths(engine, torch_mod, oracle_mod, monkeypatch, spa, case):
+    """The sparse path with and without the fused SPA kernels (TCUDB_NO_SPA=1 keeps C in
+    HBM) — both exact against the oracle; wide_h has H beyond one shared-memory row, so it
+    takes the C path either way; the skew cases put most updates in a few rows."""
+    monkeypatch.setenv("TCUDB_NO_SPA", "0" if spa == "1" else "1")
+    rng = np.random.default_rng(77)
+    if case in ("c3", "c5", "c5s"):
+        A, B, agg = datagen.make_config(case, {"c3": 1 / 16, "c5": 1 / 256, "c5s": 1 / 256}[case])
+    elif case == "wide_h":
+        n = 40000
+        A = datagen.Table(rng.integers(0, 5000, n), rng.integers(0, 300, n))
+        B = datagen.Table(rng.integers(0, 5000, n), rng.integers(0, 60000, n))
+        agg = "count"
+    else:
+        n = 30000
+        g = np.where(rng.random(n) < 0.5, 0, rng.integers(0, 3000, n))  # half the tuples in row 0
+        k = rng.zipf(1.3, n) % 20000
+        A = datagen.Table(k, g, rng.integers(-9, 10, n) if case == "skew_sum_int"
+                          else rng.uniform(-2, 2, n).astype(np.float32))
+        B = datagen.Table(rng.zipf(1.3, n) % 20000, rng.integers(0, 3000, n),
+                          rng.integers(-9, 10, n) if case == "skew_sum_int" else rng.uniform(-2, 2, n).astype(np.float32))
+        agg = "sum"
+    ref = oracle_mod.join_agg(A, B, agg)
+    out, st = run(engine, torch_mod, A, B, agg, 2)
+    assert st["path"] == 1
+    compare(out, ref, agg, float_vals=(case == "skew_sum_float"))
+
+
 # ---------------------------------------------------------------- configs (reduced + full)
 @pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c1s", 1.0), ("c2", 0.1), ("c3", 1 / 16), ("c4", 1 / 1024),
                                         ("c5", 1 / 256), ("c5s", 1 / 256)])
