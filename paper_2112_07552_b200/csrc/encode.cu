@@ -271,13 +271,26 @@ __global__ void __launch_bounds__(1024) k_pred_codes_1blk(const uint8_t* __restr
     const int64_t base = base0 + (int64_t)threadIdx.x * 16;
     uint8_t p[16];
     int c = 0;
+    if (base + 16 <= n) {  // 16 flags per thread as one 16-byte load (spans are 16-byte aligned allocations)
+      const uint4 va = *reinterpret_cast<const uint4*>(fa + base);
+      const uint4 vb = fb ? *reinterpret_cast<const uint4*>(fb + base) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int64_t i = base + j;
-      const int a = i < n ? fa[i] : 0, b = (i < n) ? (fb ? fb[i] : 1) : 0;
-      p[j] = (uint8_t)(a & b);
-      c += p[j];
-      if (fb) u += a | b;
+      for (int j = 0; j < 16; ++j) {
+        const int a = (wa[j >> 2] >> (8 * (j & 3))) & 1, b = (wb[j >> 2] >> (8 * (j & 3))) & 1;
+        p[j] = (uint8_t)(a & b);
+        c += p[j];
+        if (fb) u += a | b;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int64_t i = base + j;
+        const int a = i < n ? fa[i] : 0, b = (i < n) ? (fb ? fb[i] : 1) : 0;
+        p[j] = (uint8_t)(a & b);
+        c += p[j];
+        if (fb) u += a | b;
+      }
     }
     int x = c;
 #pragma unroll
@@ -287,14 +300,22 @@ __global__ void __launch_bounds__(1024) k_pred_codes_1blk(const uint8_t* __restr
     int wp = 0, tot = 0;
     for (int w = 0; w < 32; ++w) { const int t = wt[w]; if (w < warp_id()) wp += t; tot += t; }
     long long run = s_run + wp + x - c;
+    int32_t cv[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int64_t i = base + j;
-      if (i < n) {
-        code[i] = p[j] ? (int32_t)run : -1;
-        if (p[j] && dict) dict[run] = minv + (long long)i;
-        run += p[j];
-      }
+      cv[j] = p[j] ? (int32_t)run : -1;
+      if (i < n && p[j] && dict) dict[run] = minv + (long long)i;
+      run += p[j];
+    }
+    if (base + 16 <= n) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        reinterpret_cast<int4*>(code + base)[j] = make_int4(cv[4 * j], cv[4 * j + 1], cv[4 * j + 2], cv[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (base + j < n) code[base + j] = cv[j];
     }
     __syncthreads();
     if (threadIdx.x == 0) s_run += tot;

@@ -514,6 +514,18 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   ca.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
   ca.agg_out = is_float ? 1 : 0;
 
+  // The e2m1 COUNT fill is optimistic: its duplicate-cell flag is read together with the
+  // result size (one host sync fewer); on a duplicate the matrix stage reruns on u8.
+  void* ctmp = nullptr;
+  int64_t* d_nnz = nullptr;
+  int64_t nnz = 0;
+  FillStats* fs4 = nullptr;  // flags of the unchecked e2m1 fill
+  for (int attempt = 0; attempt < 2; ++attempt) {
+  const bool allow_fp4 = attempt == 0;
+  fs4 = nullptr;
+  S.elem = is_float ? 1 : 0;
+  S.planes_a = S.planes_b = 1;
+  S.kchunks = 1;
   if (dense) {
     // ---------------- a5 fill
     uint8_t *opA = nullptr, *opB = nullptr;        // value planes (int8) or bf16 operands
@@ -530,19 +542,12 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     // is detected by the fill and sends the query down the u8 path.
     uint8_t *op4A = nullptr, *op4B = nullptr;
     const int64_t Kp4 = round_up(K, 256);  // 128-byte K blocks of packed nibbles
-    if (!is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24)) {
+    if (allow_fp4 && !is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24)) {
       op4A = ar.zeros<uint8_t>(Gp * Kp4 / 2);
       op4B = ar.zeros<uint8_t>(Hp * Kp4 / 2);
       CK(launch_fill_count_fp4(kA, gA, nA, op4A, Kp4, fs + 0, s, L));
       CK(launch_fill_count_fp4(kB, hB, nB, op4B, Kp4, fs + 1, s, L));
-      CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      FillStats hf[2];
-      std::memcpy(hf, ctx->pinned, sizeof(hf));
-      if (hf[0].overflow || hf[1].overflow) {
-        op4A = op4B = nullptr;
-        CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
-      }
+      fs4 = fs;  // checked at the result-size read below
     }
     if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE)) {
       opA = ar.zeros<uint8_t>(cellsA);
@@ -843,18 +848,24 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   }
 
   // ---------------- a8 compaction
-  void* ctmp = spa ? nullptr : ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
-  int64_t* d_nnz = spa ? const_cast<int64_t*>(sa.row_out) + G : ar.get<int64_t>(1);
+  ctmp = spa ? nullptr : ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
+  d_nnz = spa ? const_cast<int64_t*>(sa.row_out) + G : ar.get<int64_t>(1);
   if (!spa) CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
-  int64_t nnz;
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
     int* hov = reinterpret_cast<int*>(hp + 1);
+    FillStats* hfs = reinterpret_cast<FillStats*>(hp + 2);
     *hov = 0;
     CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
     if (sparse_u16.acc_kind == 4) CK(cudaMemcpyAsync(hov, sparse_u16.ovf, 4, cudaMemcpyDeviceToHost, s));
+    if (fs4) CK(cudaMemcpyAsync(hfs, fs4, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     nnz = hp[0];
+    if (fs4 && (hfs[0].overflow || hfs[1].overflow)) {
+      // a (g, k) or (h, k) cell holds two tuples: not 0/1, so not e2m1 — rerun on u8
+      seg_cnt = nullptr;
+      continue;
+    }
     if (*hov) {
       // some (g, h) count passed 65535: redo the expand with 32/64-bit cells
       ExpandArgs ea = sparse_u16;
@@ -867,6 +878,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
     }
   }
+  break;
+  }  // attempt
   const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
   QueryOut r;
   r.n = nnz;
