@@ -107,6 +107,9 @@ typedef struct {
   double density_union; /* nnz cells / (G * K_union): the paper's density */
   double gemm_ops;      /* 2 * Gp * Hp * Kp summed over GEMM launches (dense path) */
   float ms_stats, ms_encode, ms_fill, ms_gemm, ms_sparse, ms_compact, ms_total;
+  int32_t spa_mode;     /* sparse path: 0 C matrix (or dense path), 1 count + write passes,
+                           2 count pass + persistent band writer, 3 one persistent pass */
+  int64_t spa_max_band; /* sparse path: most updates of one band of result rows */
 } tcudb_stats;
 
 typedef struct tcudb_ctx tcudb_ctx;

@@ -227,6 +227,75 @@ __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __r
   }
 }
 
+// Small domains with many tuples per value (c5: 16.7 M group values over 4,096
+// distinct): every tuple of k_hash_insert reads a slot of a tiny global table, and
+// those L2 requests (not bytes) bound it. Here each block first de-duplicates its
+// chunk in a shared-memory table (same key encoding and probing, capacity cap_s),
+// inserts only its distinct keys into the global table, and maps its tuples to global
+// slots from shared memory on a second read of the chunk. A block chunk with more
+// than cap_s / 2 distinct keys reports overflow (the caller rebuilds sized by n).
+__global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long minv,
+                                                          unsigned long long* __restrict__ slots,
+                                                          unsigned long long mask, uint8_t* __restrict__ flags,
+                                                          int* __restrict__ overflow, int32_t* __restrict__ row_slot,
+                                                          int cap_s, int64_t chunk) {
+  extern __shared__ unsigned long long s_key[];
+  int32_t* s_map = reinterpret_cast<int32_t*>(s_key + cap_s);
+  __shared__ int s_n, s_bad;
+  const unsigned smask = (unsigned)cap_s - 1u;
+  for (int i = threadIdx.x; i < cap_s; i += blockDim.x) s_key[i] = ~0ull;
+  if (threadIdx.x == 0) { s_n = 0; s_bad = 0; }
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(c.n, lo + chunk);
+  auto sfind = [&](unsigned long long off, bool insert) -> int {
+    unsigned h = (unsigned)fmix64(off) & smask;
+    for (int step = 0; step < cap_s; ++step) {
+      const unsigned long long cur = s_key[h];
+      if (cur == off) return (int)h;
+      if (cur == ~0ull) {
+        if (!insert) return -1;
+        const unsigned long long prev = atomicCAS(s_key + h, ~0ull, off);
+        if (prev == ~0ull) { atomicAdd(&s_n, 1); return (int)h; }
+        if (prev == off) return (int)h;
+      }
+      h = (h + 1) & smask;
+    }
+    return -1;
+  };
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const unsigned long long off = (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv;
+    if (sfind(off, true) < 0) s_bad = 1;
+  }
+  __syncthreads();
+  if (s_bad || s_n > cap_s / 2 + cap_s / 4) {
+    if (threadIdx.x == 0) *overflow = 1;
+    return;
+  }
+  for (int sidx = threadIdx.x; sidx < cap_s; sidx += blockDim.x) {
+    const unsigned long long off = s_key[sidx];
+    if (off == ~0ull) continue;
+    unsigned long long hh = fmix64(off) & mask;
+    int32_t placed = -1;
+    for (unsigned long long step = 0; step <= mask; ++step) {
+      const unsigned long long cc = __ldcg(slots + hh);
+      if (cc == off) { placed = (int32_t)hh; break; }
+      if (cc == ~0ull) {
+        const unsigned long long prev = atomicCAS(slots + hh, ~0ull, off);
+        if (prev == ~0ull || prev == off) { placed = (int32_t)hh; break; }
+      }
+      hh = (hh + 1) & mask;
+    }
+    s_map[sidx] = placed;
+    if (placed < 0) *overflow = 1;
+    else if (!flags[placed]) flags[placed] = 1;
+  }
+  __syncthreads();
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const unsigned long long off = (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv;
+    row_slot[i] = s_map[sfind(off, false)];
+  }
+}
+
 // ------------------------------------------------------------------ predicate scan -> codes
 // pred(i) = fa[i] && (fb ? fb[i] : 1). Tile = 4096 flags per 256-thread block.
 constexpr int PT = 4096;
@@ -730,8 +799,27 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 }
 
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, int* overflow, int32_t* row_slot, cudaStream_t s, int64_t* launches) {
+                               uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, cudaStream_t s,
+                               int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
+  // shared-memory pre-aggregation when the estimated distinct count is small and
+  // there are many tuples per distinct value (tables sized 2^ceil(log2(1.9 est)))
+  const int64_t cap = (int64_t)mask + 1;
+  if (est_distinct > 0 && row_slot && cap <= 16384 && c.n >= 64 * cap) {
+    const int cap_s = (int)cap;  // >= 1.9 x the global distinct count, so >= any block's
+    const size_t smem = (size_t)cap_s * 12;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_hash_insert_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 12);
+      attr = true;
+    }
+    const int per_sm = smem <= 96 * 1024 ? 2 : 1;
+    const int64_t nblk = std::min<int64_t>(per_sm * kNumSMs, (c.n + 32767) / 32768);
+    const int64_t chunk = (c.n + nblk - 1) / nblk;
+    k_hash_insert_smem<<<(int)nblk, 1024, smem, s>>>(c, minv, slots, mask, flags, overflow, row_slot, cap_s, chunk);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags, overflow, row_slot);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -787,8 +875,8 @@ cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* va
   return cudaGetLastError();
 }
 
-// (the one-block bitonic sort wins below ~1 K values; the radix sort above)
-bool small_rank_ok(int64_t count, int64_t cap) { return count <= 1024 && cap <= (1 << 16); }
+// (one block: gather + bitonic sort of <= 4 K values vs ~12 launches of the radix sort)
+bool small_rank_ok(int64_t count, int64_t cap) { return count <= SMALL_SORT && cap <= (1 << 16); }
 
 cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slots, int64_t cap, int64_t count,
                               long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,

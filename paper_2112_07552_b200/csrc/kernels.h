@@ -47,7 +47,8 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 // Open-addressing insert of (x - minv); *overflow = 1 if the table is full; row_slot
 // (optional, c.n entries) receives each row's slot.
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, int* overflow, int32_t* row_slot, cudaStream_t s, int64_t* launches);
+                               uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, cudaStream_t s,
+                               int64_t* launches);
 size_t pred_temp_bytes(int64_t n);
 // codes = exclusive scan of pred(i) (-1 where false); optional dict[code] = minv + i (direct
 // group domains: the sorted value dictionary comes out of the same pass).
@@ -187,9 +188,19 @@ struct SpaArgs {
   const long long* dict_g; const long long* dict_h;
   int g_out_type, h_out_type;  // 0 I32, 1 I64
   void* out_g; void* out_h; void* out_agg;
+  // one-pass kernel (spa_fused_plan / launch_spa_fused); acc_kind 4 = COUNT in packed u16
+  unsigned long long* ticket;  // 1, zeroed: band tickets
+  unsigned long long* lb_state;  // nbands, zeroed: look-back (flag | tuple count) per band
+  int64_t* total;              // out: number of result tuples
+  int* ovf;                    // out (zeroed): a u16 COUNT cell reached 65,535
 };
 // false when one result row does not fit in shared memory (the caller keeps the C path)
 bool spa_plan(SpaArgs& a);
+bool spa_fused_plan(SpaArgs& a);
+void spa_count_plan(SpaArgs& a);  // count_bands for the count pass at the current rows
+cudaError_t launch_spa_fused(const SpaArgs& a, cudaStream_t s, int64_t* launches);
+// *out = max over bands of the band's update count (out zeroed by the caller)
+cudaError_t launch_band_weight_max(const SpaArgs& a, unsigned long long* out, cudaStream_t s, int64_t* launches);
 cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_spa_write(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 

@@ -242,7 +242,244 @@ __global__ void __launch_bounds__(NT) k_spa_write(const SpaArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-pass variant: expansion, counting and writing of a band in ONE kernel.
+// Persistent CTAs (NTF threads, 2 per SM) take bands in ascending order from a
+// ticket counter; after expanding band b a CTA publishes its tuple count and finds
+// its output offset by a decoupled look-back over the bands before it (every band
+// with a smaller ticket is held by a running CTA, so the wait always ends). The
+// result buffer is sized by the upper bound min(G·H, J) tuples, so no count pass
+// and no second expansion are needed. Cells are zeroed as they are read, so shared
+// memory is cleared once per CTA, not once per band.
+// COUNT uses packed u16 cells (half the shared memory of int32, so twice the rows
+// per band or two CTAs per SM on wide rows); a count reaching 65,535 raises *ovf and
+// the caller reruns the kernel with int32 cells.
+constexpr int NTF = 512;
+constexpr size_t kSmemFused = 108 * 1024;  // 2 CTAs per SM
+
+template <int ACC> struct FusedCell;
+template <> struct FusedCell<0> { using T = uint16_t; };            // COUNT, packed u16
+template <> struct FusedCell<1> { using T = int; };                 // COUNT int32
+template <> struct FusedCell<2> { using T = unsigned long long; };  // integer SUM (wrapping)
+template <> struct FusedCell<3> { using T = double; };              // float SUM
+
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+template <int ACC>
+__global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
+  using T = typename FusedCell<ACC>::T;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int64_t s_base[NTF / 32 + 1];
+  __shared__ uint8_t s_stage[NTF / 32][256];
+  __shared__ int64_t s_rowbase[64];
+  __shared__ int s_rowcnt[64];
+  __shared__ int64_t s_band;
+  const int nw = NTF / 32, wid = warp_id(), lane = lane_id();
+  const int64_t W = a.words, ldc = W * 32;
+  T* acc = reinterpret_cast<T*>(smem);
+  unsigned* bits = reinterpret_cast<unsigned*>(smem + ((size_t)a.rows * ldc * sizeof(T) + 15) / 16 * 16);
+  {
+    const int nv = (int)(((size_t)a.rows * ldc * sizeof(T) + 15) / 16);
+    for (int i = threadIdx.x; i < nv; i += NTF) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < a.rows * (int)W; i += NTF) bits[i] = 0u;
+  }
+  volatile unsigned long long* state = reinterpret_cast<volatile unsigned long long*>(a.lb_state);
+  bool ovf = false;
+  for (;;) {
+    __syncthreads();  // smem clear / previous band finished before the ticket is replaced
+    if (threadIdx.x == 0) s_band = (int64_t)atomicAdd(a.ticket, 1ull);
+    __syncthreads();
+    const int64_t b = s_band;
+    if (b >= a.nbands) break;
+    const int64_t g0 = b * a.rows;
+    const int nr = (int)min((int64_t)a.rows, a.G - g0);
+    spa_expand<(ACC >= 2)>(a, a.goff[b], a.goff[b + 1], g0, [&](int r, int h, int64_t pos, int32_t ai) {
+      if constexpr (ACC == 0) {
+        const int sh = (h & 1) * 16;
+        const unsigned old = atomicAdd(reinterpret_cast<unsigned*>(acc) + ((r * ldc + h) >> 1), 1u << sh);
+        if (((old >> sh) & 0xFFFFu) == 0xFFFFu) ovf = true;
+      } else if constexpr (ACC == 1) {
+        atomicAdd(acc + r * ldc + h, 1);
+      } else if constexpr (ACC == 2) {
+        const long long v = a.va.data ? ld_int(a.va.data, a.va.type, ai) : 1;
+        const long long w = a.w_kind == 1 ? static_cast<const long long*>(a.b_w)[pos] : 1;
+        atomicAdd(acc + r * ldc + h, (unsigned long long)v * (unsigned long long)w);
+      } else {
+        const double v = a.va.data ? (double)__ldg(static_cast<const float*>(a.va.data) + ai) : 1.0;
+        const double w = a.w_kind == 2 ? (double)static_cast<const float*>(a.b_w)[pos] : 1.0;
+        atomicAdd(acc + r * ldc + h, v * w);
+      }
+      atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
+    });
+    __syncthreads();
+    // tuples per row of the band
+    for (int r = wid; r < nr && !a.row_out; r += nw) {
+      int c = 0;
+      for (int64_t w = lane; w < W; w += 32) c += __popc(bits[r * W + w]);
+      c = warp_sum(c);
+      if (lane == 0) s_rowcnt[r] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && a.row_out) {
+      // write pass of the two-pass schedule: offsets from the count pass
+      for (int r = 0; r < nr; ++r) s_rowbase[r] = a.row_out[g0 + r];
+    } else if (threadIdx.x == 0) {
+      int64_t cnt = 0;
+      for (int r = 0; r < nr; ++r) cnt += s_rowcnt[r];
+      // decoupled look-back: publish the aggregate, sum predecessors back to an inclusive prefix
+      int64_t prefix = 0;
+      if (b == 0) {
+        atomicExch(reinterpret_cast<unsigned long long*>(a.lb_state), kLbInc | (unsigned long long)cnt);
+      } else {
+        atomicExch(reinterpret_cast<unsigned long long*>(a.lb_state) + b, kLbAgg | (unsigned long long)cnt);
+        for (int64_t j = b - 1; j >= 0;) {
+          const unsigned long long v = state[j];
+          if ((v & ~kLbVal) == 0) continue;  // predecessor still expanding
+          prefix += (int64_t)(v & kLbVal);
+          if ((v & ~kLbVal) == kLbInc) break;
+          --j;
+        }
+        atomicExch(reinterpret_cast<unsigned long long*>(a.lb_state) + b, kLbInc | (unsigned long long)(prefix + cnt));
+      }
+      if (b == a.nbands - 1) *a.total = prefix + cnt;
+      int64_t run = prefix;
+      for (int r = 0; r < nr; ++r) { s_rowbase[r] = run; run += s_rowcnt[r]; }
+    }
+    __syncthreads();
+    // write: per row, warps own contiguous slices of 8-word (256-cell) groups (see k_spa_write)
+    const int ngrp = (int)((W + 7) / 8);
+    const int per = (ngrp + nw - 1) / nw;
+    const int q0 = min(ngrp, wid * per), q1 = min(ngrp, q0 + per);
+    uint8_t* stage = s_stage[wid];
+    const int nbytes = (int)W * 4;
+    for (int r = 0; r < nr; ++r) {
+      const int64_t g = g0 + r;
+      unsigned* rb = bits + r * W;
+      const uint8_t* rbytes = reinterpret_cast<const uint8_t*>(rb);
+      int c = 0;
+      for (int i = q0 * 32 + lane; i < q1 * 32 && i < nbytes; i += 32) c += __popc(rbytes[i]);
+      c = warp_sum(c);
+      if (lane == 0) s_base[wid] = c;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int64_t run = s_rowbase[r];
+        for (int i = 0; i < nw; ++i) { const int64_t x = s_base[i]; s_base[i] = run; run += x; }
+      }
+      __syncthreads();
+      int64_t base = s_base[wid];
+      const long long gv = a.dict_g[g];
+      T* arow = acc + (int64_t)r * ldc;
+      for (int q = q0; q < q1; ++q) {
+        const int bi = q * 32 + lane;
+        unsigned m = bi < nbytes ? rbytes[bi] : 0u;
+        const int cnt = __popc(m);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) continue;
+        int p = incl - cnt;
+        while (m) {
+          const int bb = __ffs(m) - 1;
+          stage[p++] = (uint8_t)(lane * 8 + bb);
+          m &= m - 1;
+        }
+        __syncwarp();
+        const int64_t hq = (int64_t)q * 256;
+        for (int j = lane; j < total; j += 32) {
+          const int64_t h = hq + stage[j];
+          const int64_t o = base + j;
+          const long long hv = __ldg(a.dict_h + h);
+          if (a.g_out_type) __stcs(static_cast<long long*>(a.out_g) + o, gv);
+          else __stcs(static_cast<int*>(a.out_g) + o, (int)gv);
+          if (a.h_out_type) __stcs(static_cast<long long*>(a.out_h) + o, hv);
+          else __stcs(static_cast<int*>(a.out_h) + o, (int)hv);
+          const T x = arow[h];
+          arow[h] = (T)0;  // zero on read: the next band starts from a clear accumulator
+          if constexpr (ACC == 3) __stcs(static_cast<double*>(a.out_agg) + o, x);
+          else __stcs(static_cast<long long*>(a.out_agg) + o, (long long)x);
+        }
+        __syncwarp();
+        base += total;
+      }
+      // clear this warp's slice of the row bitmap (all its bytes were read above)
+      for (int wq = q0 * 8 + lane; wq < q1 * 8 && wq < W; wq += 32) rb[wq] = 0u;
+      __syncthreads();  // s_base reuse
+    }
+  }
+  if (ovf) *a.ovf = 1;
+}
+
 }  // namespace
+
+__global__ void k_band_weight_max(const int64_t* __restrict__ goff, const int64_t* __restrict__ act_off,
+                                  int64_t nbands, unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbands; b += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(act_off[goff[b + 1]] - act_off[goff[b]]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(out, m);
+}
+
+cudaError_t launch_band_weight_max(const SpaArgs& a, unsigned long long* out, cudaStream_t s, int64_t* launches) {
+  if (a.nbands <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(2 * kNumSMs, (a.nbands + 255) / 256);
+  k_band_weight_max<<<(unsigned)blocks, 256, 0, s>>>(a.goff, a.act_off, a.nbands, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+// Fused one-pass plan: rows per band so that 2 CTAs fit per SM and there are >= ~4
+// bands per CTA for the ticket scheduler to balance. false: a row does not fit.
+bool spa_fused_plan(SpaArgs& a) {
+  a.words = (a.H + 31) / 32;
+  const size_t cell = a.acc_kind == 4 ? 2 : (a.acc_kind == 0 ? 4 : 8);
+  const size_t row_w = (size_t)a.words * 32 * cell + (size_t)a.words * 4;
+  const int fit = (int)std::min<size_t>(64, (kSmemFused - 16) / row_w);
+  if (fit < 1) return false;
+  const int64_t grid = 2 * kNumSMs;
+  const int64_t want = std::max<int64_t>(1, a.G / (4 * grid));
+  a.rows = (int)std::min<int64_t>(want, fit);
+  a.nbands = (a.G + a.rows - 1) / a.rows;
+  return true;
+}
+
+static size_t fused_smem(const SpaArgs& a) {
+  const size_t cell = a.acc_kind == 4 ? 2 : (a.acc_kind == 0 ? 4 : 8);
+  return ((size_t)a.rows * a.words * 32 * cell + 15) / 16 * 16 + (size_t)a.rows * a.words * 4;
+}
+
+template <int ACC>
+static cudaError_t launch_fused_t(const SpaArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_spa_fused<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kSmemFused);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t grid = std::min<int64_t>(a.nbands, 2 * kNumSMs);
+  k_spa_fused<ACC><<<(unsigned)grid, NTF, fused_smem(a), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spa_fused(const SpaArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.G <= 0) return cudaSuccess;
+  cudaError_t e;
+  switch (a.acc_kind) {
+    case 4: e = launch_fused_t<0>(a, s); break;
+    case 0: e = launch_fused_t<1>(a, s); break;
+    case 2: e = launch_fused_t<2>(a, s); break;
+    case 3: e = launch_fused_t<3>(a, s); break;
+    default: return cudaErrorInvalidValue;  // int64 COUNT cells: two-pass path
+  }
+  if (launches) ++*launches;
+  return e;
+}
 
 bool spa_plan(SpaArgs& a) {
   a.words = (a.H + 31) / 32;
@@ -260,6 +497,13 @@ bool spa_plan(SpaArgs& a) {
   const int64_t by_grid = std::max<int64_t>(1, a.nbands / (4 * kNumSMs));
   a.count_bands = (int)std::min(by_smem, by_grid);
   return true;
+}
+
+void spa_count_plan(SpaArgs& a) {
+  const size_t row_bits = (size_t)a.words * 4;
+  const int64_t by_smem = std::max<int64_t>(1, (int64_t)(48 * 1024 / (row_bits * a.rows)));
+  const int64_t by_grid = std::max<int64_t>(1, a.nbands / (4 * kNumSMs));
+  a.count_bands = (int)std::min(by_smem, by_grid);
 }
 
 static size_t count_smem(const SpaArgs& a) { return (size_t)a.count_bands * a.rows * a.words * 4; }

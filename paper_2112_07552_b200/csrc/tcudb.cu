@@ -162,7 +162,8 @@ double hll_estimate(const unsigned* r) {
 
 // Build phase 1 of a dictionary over one or two columns (marks + codes / compaction).
 // intersect: K domain, code only keys present on both sides (∩); otherwise the union.
-// est_distinct (> 0) sizes the hash table: 2^ceil(log2(2.2 x estimate)), never above 2n.
+// est_distinct (> 0) sizes the hash table: 2^ceil(log2(1.9 x estimate)), never above 2n
+// (load <= ~0.53; c5's 4.2 M keys fit 2^23 slots = 64 MB, L2-resident).
 void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long long mn, long long mx, bool intersect,
                 unsigned long long* union_dev, int64_t* launches, double est_distinct = 0) {
   cudaStream_t s = ar.s;
@@ -196,7 +197,7 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
     d.mode = 1;
     unsigned long long want = (unsigned long long)(2 * n);
-    if (est_distinct > 0) want = std::min(want, (unsigned long long)(2.2 * est_distinct) + 64);
+    if (est_distinct > 0) want = std::min(want, (unsigned long long)(1.9 * est_distinct) + 64);
     const unsigned long long cap = next_pow2(want);
     d.span = cap;
     d.slots = ar.get<unsigned long long>((int64_t)cap);
@@ -205,14 +206,14 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.ovf = ar.zeros<int>(1);
     // per-row slots: the probe then reads code[slot] instead of rehashing and walking the table
     d.slot1 = ar.get<int32_t>(c1.n);
-    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, s, launches));
+    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, s, launches));
     if (c2) {
       d.slot2 = ar.get<int32_t>(c2->n);
       if (intersect) {
         d.fb = ar.zeros<uint8_t>((int64_t)cap);
-        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, d.slot2, s, launches));
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, d.slot2, est_distinct, s, launches));
       } else {
-        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot2, s, launches));
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot2, est_distinct, s, launches));
       }
     }
     d.code = ar.get<int32_t>((int64_t)cap);
@@ -507,7 +508,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   ExpandArgs sparse_u16{};     // sparse COUNT in u16 cells (kept to redo in int32 on overflow)
   sparse_u16.acc_kind = -1;
   bool spa = false;            // sparse path through spa.cu (no C matrix)
+  bool spa_fw = false;         // ... on the persistent band kernel (spa.cu k_spa_fused)
+  bool spa_one = false;        // ... in one pass (no count pass)
   SpaArgs sa{};
+  const size_t res_gb = A->group.type == TCUDB_I64 ? 8 : 4, res_hb = B->group.type == TCUDB_I64 ? 8 : 4;
+  char* ub_base = nullptr;     // upper-bound result buffer of the one-pass kernel
+  struct ResultGuard {
+    tcudb_ctx* ctx; char** p; bool keep = false;
+    ~ResultGuard() { if (!keep && *p) result_release(ctx, *p); }
+  } ub_guard{ctx, &ub_base};
   ca.G = G; ca.H = H;
   ca.dict_g = DG.dict; ca.dict_h = DH.dict;
   ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
@@ -769,7 +778,14 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     sa.G = G; sa.H = H;
     sa.acc_kind = !is_sum ? (J < (1ull << 31) ? 0 : 1) : (is_float ? 3 : 2);
     const char* no_spa = getenv("TCUDB_NO_SPA");
-    spa = !(no_spa && no_spa[0] == '1') && spa_plan(sa);
+    const char* no_fused = getenv("TCUDB_NO_SPA_FUSED");
+    if (!(no_spa && no_spa[0] == '1') && !(no_fused && no_fused[0] == '1') && sa.acc_kind != 1) {
+      // persistent band kernel (spa.cu k_spa_fused): COUNT in packed u16 cells
+      SpaArgs fa = sa;
+      if (!is_sum) fa.acc_kind = 4;
+      if (spa_fused_plan(fa)) { sa = fa; spa_fw = true; }
+    }
+    spa = spa_fw || (!(no_spa && no_spa[0] == '1') && spa_plan(sa));
     if (spa) {
       const int64_t nb = (G + sa.rows - 1) / sa.rows;  // bands of sa.rows rows, one per CTA
       int32_t* gcnt = ar.zeros<int32_t>(nb);
@@ -785,15 +801,55 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       sa.goff = goff; sa.act_a = act_a; sa.act_off = act_off;
       sa.kcodeA = kA; sa.gcodeA = gA; sa.va = av;
       sa.bstart = bstart; sa.b_h = b_h; sa.b_w = b_w; sa.w_kind = w_kind;
-      sa.row_nnz = ar.get<int32_t>(G);
-      int64_t* row_out = ar.get<int64_t>(G + 1);
-      CK(launch_spa_count(sa, s, L));
-      void* tmpg = ar.get<char>((int64_t)scan_temp_bytes(std::max<int64_t>(G, 1)));
-      CK(exclusive_scan_i32(sa.row_nnz, row_out, G, row_out + G, tmpg, s, L));
-      sa.row_out = row_out;
       sa.dict_g = DG.dict; sa.dict_h = DH.dict;
       sa.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
       sa.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
+      if (spa_fw) {
+        // one pass (expand + count + look-back + ordered write, result buffer sized by the
+        // upper bound min(G·H, J)) unless a band carries far more updates than the average:
+        // its expansion would hold up the look-back of every later band
+        unsigned long long* d_w = ar.zeros<unsigned long long>(1);
+        CK(launch_band_weight_max(sa, d_w, s, L));
+        const unsigned long long max_w = *to_pinned<unsigned long long>(ctx, d_w, s);
+        const double avg_w = (double)J / (double)sa.nbands;
+        const double ub = std::min((double)G * (double)H, (double)J);
+        const double ub_bytes = ub * (double)(res_gb + res_hb + 8);
+        const bool u16_safe = max_w < 65535;  // a cell count never exceeds its band's updates
+        const char* force_one = getenv("TCUDB_SPA_ONE_PASS");
+        spa_one = ub_bytes <= 0.3 * (double)ctx->mem_free0 && (is_sum || u16_safe) &&
+                  ((double)max_w <= 4.0 * avg_w + 65536.0 || (force_one && force_one[0] == '1'));
+        S.spa_max_band = (int64_t)max_w;
+      }
+      if (spa_one) {
+        // expand + count + ordered write in one launch, into the upper-bound result buffer
+        const int64_t ub = (int64_t)std::min((double)G * (double)H, (double)J);
+        const size_t oh = ((size_t)ub * res_gb + 255) / 256 * 256;
+        const size_t oa = oh + ((size_t)ub * res_hb + 255) / 256 * 256;
+        ub_base = static_cast<char*>(result_alloc(ctx, oa + (size_t)ub * 8, s));
+        sa.out_g = ub_base;
+        sa.out_h = ub_base + oh;
+        sa.out_agg = ub_base + oa;
+        unsigned long long* lb = ar.zeros<unsigned long long>(sa.nbands + 1);
+        sa.ticket = lb + sa.nbands;
+        sa.lb_state = lb;
+        sa.total = ar.zeros<int64_t>(1);
+        sa.ovf = ar.zeros<int>(1);
+        sa.row_out = nullptr;
+        CK(launch_spa_fused(sa, s, L));
+      } else {
+        sa.row_nnz = ar.get<int32_t>(G);
+        int64_t* row_out = ar.get<int64_t>(G + 1);
+        spa_count_plan(sa);
+        CK(launch_spa_count(sa, s, L));
+        void* tmpg = ar.get<char>((int64_t)scan_temp_bytes(std::max<int64_t>(G, 1)));
+        CK(exclusive_scan_i32(sa.row_nnz, row_out, G, row_out + G, tmpg, s, L));
+        sa.row_out = row_out;
+        if (spa_fw) {
+          unsigned long long* tk = ar.zeros<unsigned long long>(1);
+          sa.ticket = tk;
+          sa.ovf = ar.zeros<int>(1);
+        }
+      }
       tm.mark(&S.ms_sparse);
     } else if (big_c) {
       // C far larger than L2: active A tuples in row (g) order, so the expand's atomics walk
@@ -849,7 +905,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
 
   // ---------------- a8 compaction
   ctmp = spa ? nullptr : ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
-  d_nnz = spa ? const_cast<int64_t*>(sa.row_out) + G : ar.get<int64_t>(1);
+  d_nnz = spa_one ? sa.total : spa ? const_cast<int64_t*>(sa.row_out) + G : ar.get<int64_t>(1);
   if (!spa) CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
@@ -883,7 +939,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
   QueryOut r;
   r.n = nnz;
-  try {
+  if (spa_one) {
+    r.g = sa.out_g; r.h = sa.out_h; r.agg = sa.out_agg;
+    ub_guard.keep = true;
+  } else try {
     // one allocation (one allocator callback) holding g | h | agg, 256-byte aligned parts
     const size_t og = 0, oh = ((size_t)nnz * gb + 255) / 256 * 256;
     const size_t oa = oh + ((size_t)nnz * hb + 255) / 256 * 256;
@@ -892,7 +951,17 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     ca.out_g = r.g; ca.out_h = r.h; ca.out_agg = r.agg;
     if (spa) {
       sa.out_g = r.g; sa.out_h = r.h; sa.out_agg = r.agg;
-      CK(launch_spa_write(sa, s, L));
+      if (spa_fw) {
+        // write pass on the persistent band kernel; a u16 COUNT cell reaching 65,535 is
+        // redone by the int32 write pass (same bands, same offsets)
+        CK(launch_spa_fused(sa, s, L));
+        if (sa.acc_kind == 4 && *to_pinned<int>(ctx, sa.ovf, s)) {
+          sa.acc_kind = 0;
+          CK(launch_spa_write(sa, s, L));
+        }
+      } else {
+        CK(launch_spa_write(sa, s, L));
+      }
     } else {
       CK(launch_compact_write(ca, ctmp, s, L));
     }
@@ -905,6 +974,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   tm.finish();
   out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->on_host = 0;
   S.n_result = nnz;
+  S.spa_mode = !spa ? 0 : spa_one ? 3 : spa_fw ? 2 : 1;
   S.n_launches = (int32_t)(ctx->launches - launches0);
   S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
   return TCUDB_OK;

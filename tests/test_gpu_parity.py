@@ -169,13 +169,19 @@ def test_float_direct_fill_guard_large(engine, torch_mod, oracle_mod, case, G):
         assert st["elem"] == 1
 
 
-@pytest.mark.parametrize("spa", ["1", "0"])  # fused shared-memory SPA path / C-matrix path
-@pytest.mark.parametrize("case", ["c3", "c5", "c5s", "wide_h", "skew_sum_float", "skew_sum_int"])
+# SPA schedules: "one" = one persistent pass with look-back (forced even when skewed),
+# "auto" = the selector's choice, "two" = count pass + legacy write kernel,
+# "0" = C matrix in HBM (no shared-memory SPA)
+@pytest.mark.parametrize("spa", ["one", "auto", "two", "0"])
+@pytest.mark.parametrize("case", ["c3", "c5", "c5s", "wide_h", "skew_sum_float", "skew_sum_int", "hot_cell"])
 def test_sparse_spa_and_matrix_paths(engine, torch_mod, oracle_mod, monkeypatch, spa, case):
-    """The sparse path with and without the fused SPA kernels (TCUDB_NO_SPA=1 keeps C in
-    HBM) — both exact against the oracle; wide_h has H beyond one shared-memory row, so it
-    takes the C path either way; the skew cases put most updates in a few rows."""
-    monkeypatch.setenv("TCUDB_NO_SPA", "0" if spa == "1" else "1")
+    """The sparse path under every schedule — all exact against the oracle. wide_h has a
+    wide H (~30 K groups: one u16 row per band); the skew cases put most updates
+    in a few rows; hot_cell drives one (g, h) COUNT past 65,535 (u16 cell overflow ->
+    int32 rerun)."""
+    monkeypatch.setenv("TCUDB_NO_SPA", "1" if spa == "0" else "0")
+    monkeypatch.setenv("TCUDB_NO_SPA_FUSED", "1" if spa == "two" else "0")
+    monkeypatch.setenv("TCUDB_SPA_ONE_PASS", "1" if spa == "one" else "0")
     rng = np.random.default_rng(77)
     if case in ("c3", "c5", "c5s"):
         A, B, agg = datagen.make_config(case, {"c3": 1 / 16, "c5": 1 / 256, "c5s": 1 / 256}[case])
@@ -184,6 +190,14 @@ def test_sparse_spa_and_matrix_paths(engine, torch_mod, oracle_mod, monkeypatch,
         A = datagen.Table(rng.integers(0, 5000, n), rng.integers(0, 300, n))
         B = datagen.Table(rng.integers(0, 5000, n), rng.integers(0, 60000, n))
         agg = "count"
+    elif case == "hot_cell":
+        # key 7 joins 400 A tuples of g=5 with 200 B tuples of h=9: COUNT(5, 9) = 80,000
+        n = 20000
+        ka = np.concatenate([np.full(400, 7), rng.integers(100, 900000, n)])
+        ga = np.concatenate([np.full(400, 5), rng.integers(0, 2000, n)])
+        kb = np.concatenate([np.full(200, 7), rng.integers(100, 900000, n)])
+        hb = np.concatenate([np.full(200, 9), rng.integers(0, 2000, n)])
+        A, B, agg = datagen.Table(ka, ga), datagen.Table(kb, hb), "count"
     else:
         n = 30000
         g = np.where(rng.random(n) < 0.5, 0, rng.integers(0, 3000, n))  # half the tuples in row 0
@@ -196,6 +210,12 @@ def test_sparse_spa_and_matrix_paths(engine, torch_mod, oracle_mod, monkeypatch,
     ref = oracle_mod.join_agg(A, B, agg)
     out, st = run(engine, torch_mod, A, B, agg, 2)
     assert st["path"] == 1
+    if spa == "0":
+        assert st["spa_mode"] == 0
+    elif spa == "two":
+        assert st["spa_mode"] in (1, 2)
+    elif spa == "one" and case != "hot_cell":  # a band past 65,535 updates: never one-pass COUNT
+        assert st["spa_mode"] == 3
     compare(out, ref, agg, float_vals=(case == "skew_sum_float"))
 
 
