@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long 
   __syncthreads();
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const unsigned long long off = (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv;
-    row_slot[i] = s_map[sfind(off, false)];
+    __stcs(row_slot + i, s_map[sfind(off, false)]);
   }
 }
 

@@ -36,14 +36,27 @@ inline int grid_for(int64_t n, int per_block = T * 4) {
 __global__ void k_bucket_fill(const int32_t* __restrict__ kcode, const int32_t* __restrict__ hcode, ColDesc w,
                               int64_t n, const int64_t* __restrict__ bstart, int32_t* __restrict__ cursor,
                               int32_t* __restrict__ b_h, void* __restrict__ b_w, int w_kind) {
+  constexpr int U = 4;  // independent tuples per thread per step (latency-bound gathers)
   const int64_t stride = (int64_t)gridDim.x * T;
-  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += stride) {
-    const int32_t kc = kcode[i];
-    if (kc < 0) continue;
-    const int64_t pos = bstart[kc] + atomicAdd(cursor + kc, 1);
-    b_h[pos] = hcode[i];
-    if (w_kind == 1) static_cast<long long*>(b_w)[pos] = ld_int(w.data, w.type, i);
-    else if (w_kind == 2) static_cast<float*>(b_w)[pos] = __ldg(static_cast<const float*>(w.data) + i);
+  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < n; i0 += U * stride) {
+    int32_t kc[U], hc[U];
+    int64_t pos[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      kc[u] = i < n ? __ldcs(kcode + i) : -1;
+      hc[u] = i < n ? __ldcs(hcode + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) pos[u] = kc[u] >= 0 ? __ldg(bstart + kc[u]) + atomicAdd(cursor + kc[u], 1) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (pos[u] < 0) continue;
+      const int64_t i = i0 + u * stride;
+      b_h[pos[u]] = hc[u];
+      if (w_kind == 1) static_cast<long long*>(b_w)[pos[u]] = ld_int(w.data, w.type, i);
+      else if (w_kind == 2) static_cast<float*>(b_w)[pos[u]] = __ldg(static_cast<const float*>(w.data) + i);
+    }
   }
 }
 
@@ -128,9 +141,22 @@ __global__ void __launch_bounds__(1024) k_active_g_scatter_smem(
   for (int g = threadIdx.x; g < G; g += blockDim.x) s_cnt[g] = 0;
   __syncthreads();
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const int32_t kc = kcode[i];
-    if (kc >= 0 && cnt_b[kc] > 0) atomicAdd(s_cnt + gcode[i] / R, 1);
+  // U tuples per thread per step: their loads and the dependent cnt_b gathers overlap
+  constexpr int U = 4;
+  const int64_t step = (int64_t)U * blockDim.x;
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
+    int32_t kc[U], gc[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      kc[u] = i < hi ? __ldcs(kcode + i) : -1;
+      gc[u] = i < hi ? __ldcs(gcode + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = kc[u] >= 0 ? __ldg(cnt_b + kc[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (w[u] > 0) atomicAdd(s_cnt + gc[u] / R, 1);
   }
   __syncthreads();
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
@@ -139,18 +165,30 @@ __global__ void __launch_bounds__(1024) k_active_g_scatter_smem(
     s_cnt[g] = 0;
   }
   __syncthreads();
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const int32_t kc = kcode[i];
-    if (kc < 0) continue;
-    const int32_t w = cnt_b[kc];
-    if (w == 0) continue;
-    const int32_t g = gcode[i];
-    const int64_t pos = s_base[g / R] + atomicAdd(s_cnt + g / R, 1);
-    act_a[pos] = (int32_t)i;
-    act_w[pos] = w;
-    if (bstart) {
-      act_b[pos] = bstart[kc];
-      act_g[pos] = g;
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
+    int32_t kc[U], gc[U], w[U];
+    int64_t bs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      kc[u] = i < hi ? __ldcs(kcode + i) : -1;
+      gc[u] = i < hi ? __ldcs(gcode + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      w[u] = kc[u] >= 0 ? __ldg(cnt_b + kc[u]) : 0;
+      bs[u] = (bstart && kc[u] >= 0) ? __ldg(bstart + kc[u]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (w[u] <= 0) continue;
+      const int64_t pos = s_base[gc[u] / R] + atomicAdd(s_cnt + gc[u] / R, 1);
+      act_a[pos] = (int32_t)(i0 + (int64_t)u * blockDim.x);
+      act_w[pos] = w[u];
+      if (bstart) {
+        act_b[pos] = bs[u];
+        act_g[pos] = gc[u];
+      }
     }
   }
 }
@@ -264,7 +302,7 @@ cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const
   if (nb <= 1024 && n >= (1 << 20)) {
     static bool attr2 = false;
     if (!attr2) {
-      cudaFuncSetAttribute(k_active_g_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 1024);
+      cudaFuncSetAttribute(k_active_g_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 12);
       attr2 = true;
     }
     const int64_t nblk = std::min<int64_t>(2 * kNumSMs, (n + 16383) / 16384);
