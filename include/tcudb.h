@@ -110,6 +110,7 @@ typedef struct {
   int32_t spa_mode;     /* sparse path: 0 C matrix (or dense path), 1 count + write passes,
                            2 count pass + persistent band writer, 3 one persistent pass */
   int64_t spa_max_band; /* sparse path: most updates of one band of result rows */
+  int32_t fused_compact; /* dense path: 1 if the compaction ran inside the GEMM kernel */
 } tcudb_stats;
 
 typedef struct tcudb_ctx tcudb_ctx;

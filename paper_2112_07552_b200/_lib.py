@@ -62,7 +62,8 @@ class Stats(ctypes.Structure):
                 ("density_union", ctypes.c_double), ("gemm_ops", ctypes.c_double),
                 ("ms_stats", ctypes.c_float), ("ms_encode", ctypes.c_float), ("ms_fill", ctypes.c_float),
                 ("ms_gemm", ctypes.c_float), ("ms_sparse", ctypes.c_float), ("ms_compact", ctypes.c_float),
-                ("ms_total", ctypes.c_float), ("spa_mode", ctypes.c_int32), ("spa_max_band", ctypes.c_int64)]
+                ("ms_total", ctypes.c_float), ("spa_mode", ctypes.c_int32), ("spa_max_band", ctypes.c_int64),
+                ("fused_compact", ctypes.c_int32)]
 
     def to_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

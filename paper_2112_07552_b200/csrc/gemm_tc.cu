@@ -62,6 +62,7 @@ struct KParams {
   unsigned long long* tri_out;
   int32_t* cnt_out; int64_t ldcnt;
   int group_m;       // M-blocks per raster band
+  FusedCompact fc;   // fused compaction (CMP kernels only)
 };
 
 // Grouped raster: bands of group_m M-blocks, N-blocks swept inside a band, so a band's
@@ -177,8 +178,143 @@ __device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, i
   return nzc;
 }
 
-template <int BN_, bool FP4, int KB_>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// ------------------------------------------------------------------ fused compaction (f1)
+// The ordered compaction (a8) runs inside the GEMM kernel: four extra warps per CTA
+// turn finished C tiles (u16, still L2-resident) into (g, h, COUNT) tuples while the
+// tensor cores work on later tiles, so the result write overlaps the MMA main loop.
+//   * Each epilogue warp stores its 32 rows of a tile plus their nonzero counts
+//     (tcnt[nb][row]) and arrives on the tile's M-block counter; the warp completing
+//     the M-block (4 x tiles_n arrivals) turns the counts into per-row offsets
+//     (exclusive along N tiles, rowbase = exclusive over the 128 rows) and publishes
+//     the M-block's tuple count (look-back state AGG). It never waits.
+//   * Compaction warps walk the CTA's own tiles in order; for a tile of M-block mb they
+//     need P(mb) = sum of the counts of M-blocks < mb, found by a decoupled look-back
+//     over the AGG / INC states (every AGG comes from an epilogue warp, so the wait ends).
+//     A row's tuples in the tile go to P(mb) + rowbase[row] + tcnt[nb][row], in column
+//     order: the output is (g, h)-sorted exactly as the separate compaction kernel's.
+constexpr int CMP_WARPS = 4;
+constexpr unsigned long long kMbAgg = 1ull << 62, kMbInc = 2ull << 62, kMbVal = (1ull << 62) - 1;
+
+__device__ __noinline__ void mblock_finish(const KParams& p, int mb) {
+  const FusedCompact& f = p.fc;
+  const int lane = lane_id();
+  const int64_t Mp = (int64_t)p.tiles_m * BM;
+  const int64_t r0 = (int64_t)mb * BM + lane * 4;  // this lane's 4 consecutive rows
+  int4 run = make_int4(0, 0, 0, 0);
+  for (int nb = 0; nb < p.tiles_n; nb += 4) {
+    int4 c[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      c[q] = nb + q < p.tiles_n ? __ldcg(reinterpret_cast<const int4*>(f.tcnt + (int64_t)(nb + q) * Mp + r0))
+                                : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (nb + q >= p.tiles_n) break;
+      __stcg(reinterpret_cast<int4*>(f.tcnt + (int64_t)(nb + q) * Mp + r0), run);
+      run.x += c[q].x; run.y += c[q].y; run.z += c[q].z; run.w += c[q].w;
+    }
+  }
+  const int tot = run.x + run.y + run.z + run.w;
+  int incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int ex = incl - tot;
+  __stcg(reinterpret_cast<int4*>(f.rowbase + r0),
+         make_int4(ex, ex + run.x, ex + run.x + run.y, ex + run.x + run.y + run.z));
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicExch(f.mstate + mb, kMbAgg | (unsigned long long)total);
+}
+
+// P(mb) (lane 0 of a compaction warp): waits for mb's own offsets, looks back over the
+// M-blocks before it, publishes INC(mb) and, for the last M-block, the result size.
+__device__ __noinline__ int64_t mblock_prefix(const KParams& p, int mb) {
+  volatile unsigned long long* st = p.fc.mstate;
+  unsigned long long v;
+  while (((v = st[mb]) >> 62) == 0) __nanosleep(200);
+  int64_t acc = 0;
+  for (int j = mb - 1; j >= 0;) {
+    const unsigned long long w = st[j];
+    const unsigned fl = (unsigned)(w >> 62);
+    if (fl == 0) { __nanosleep(100); continue; }
+    acc += (int64_t)(w & kMbVal);
+    if (fl == 2) break;
+    --j;
+  }
+  int64_t incl = (int64_t)(v & kMbVal);
+  if ((v >> 62) == 1) {
+    incl += acc;
+    atomicCAS(p.fc.mstate + mb, v, kMbInc | (unsigned long long)incl);
+  }
+  if (mb == p.tiles_m - 1) *p.fc.total = incl;
+  __threadfence();
+  return acc;
+}
+
+// Compacts this warp's 32 rows of tile (mb, nb): one row at a time, 8 chunks of 32
+// columns loaded before the ballots; stores are 32-wide contiguous.
+template <int BN_>
+__device__ __forceinline__ void compact_tile_rows(const KParams& p, int mb, int nb, int cw, int64_t P) {
+  const FusedCompact& f = p.fc;
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  const int64_t Mp = (int64_t)p.tiles_m * BM;
+  const int64_t rw0 = (int64_t)mb * BM + cw * 32;
+  if (rw0 >= f.G) return;
+  const int64_t my_row = rw0 + lane;
+  const int64_t my_off = P + __ldcg(f.rowbase + my_row) + __ldcg(f.tcnt + (int64_t)nb * Mp + my_row);
+  const long long my_g = my_row < f.G ? __ldg(f.dict_g + my_row) : 0;
+  const int64_t c0 = (int64_t)nb * BN_;
+  const int64_t lim = min(f.H, c0 + (int64_t)BN_);
+  const uint16_t* C = static_cast<const uint16_t*>(p.C);
+  long long hv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t col = c0 + j * 32 + lane;
+    hv[j] = col < lim ? __ldg(f.dict_h + col) : 0;
+  }
+  const int nrows = (int)min((int64_t)32, f.G - rw0);
+  constexpr int RB = 4;  // rows per batch: 32 cell loads in flight per lane before the ballots
+  for (int i0 = 0; i0 < nrows; i0 += RB) {
+    uint32_t e[RB][8];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int64_t row = rw0 + i0 + q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t col = c0 + j * 32 + lane;
+        e[q][j] = (i0 + q < nrows && col < lim) ? (uint32_t)__ldcg(C + row * p.ldc + col) : 0u;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      if (i0 + q >= nrows) break;
+      int64_t base = __shfl_sync(0xffffffffu, my_off, i0 + q);
+      const long long gv = __shfl_sync(0xffffffffu, my_g, i0 + q);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool nz = e[q][j] != 0u;
+        const uint32_t m = __ballot_sync(0xffffffffu, nz);
+        if (nz) {
+          const int64_t pos = base + __popc(m & lt);
+          if (f.g_out_type) __stcs(static_cast<long long*>(f.out_g) + pos, gv);
+          else __stcs(static_cast<int*>(f.out_g) + pos, (int)gv);
+          if (f.h_out_type) __stcs(static_cast<long long*>(f.out_h) + pos, hv[j]);
+          else __stcs(static_cast<int*>(f.out_h) + pos, (int)hv[j]);
+          __stcs(static_cast<long long*>(f.out_agg) + pos, (long long)e[q][j]);
+        }
+        base += __popc(m);
+      }
+    }
+  }
+}
+
+template <int BN_, bool FP4, int KB_, bool CMP = false>
+__global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
   using G = Geo<BN_, KB_>;
   constexpr int A_STAGE_BYTES = G::A_BYTES;
@@ -213,7 +349,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (FP4) {
     // all block scales = 2^0 (UE8M0 0x7F): the e2m1 operands carry the exact small
     // integers themselves; written once into TMEM columns [480, 512) by the epilogue warps
-    if (warp >= 2) {
+    if (warp >= 2 && warp < 6) {
       const uint32_t q = (uint32_t)((warp & 3) * 32) << 16;
       tmem_st_32x32b_x16(tmem_base + q + SF_COL, 0x7F7F7F7Fu);
       tmem_st_32x32b_x16(tmem_base + q + SF_COL + 16, 0x7F7F7F7Fu);
@@ -270,7 +406,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc ^= 1; if (acc == 0) acc_phase ^= 1;
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ===================== epilogue warps 2..5 =====================
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0; uint32_t acc_phase = 0;
@@ -285,12 +421,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (p.cnt_out) p.cnt_out[row * p.ldcnt + nb] = nzc;
+      if (CMP) {
+        p.fc.tcnt[(int64_t)nb * p.tiles_m * BM + row] = nzc;
+        __threadfence();  // this warp's C rows and counts before its arrival
+        __syncwarp();
+        unsigned old = 0;
+        if (lane == 0) old = atomicAdd(p.fc.mdone + mb, 1u);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == 4u * (unsigned)p.tiles_n - 1u) {
+          __threadfence();
+          mblock_finish(p, mb);
+        }
+      } else if (p.cnt_out) {
+        p.cnt_out[row * p.ldcnt + nb] = nzc;
+      }
       acc ^= 1; if (acc == 0) acc_phase ^= 1;
     }
     if (p.epi == EPI_TRI) {
       tri = warp_sum(tri);
       if (lane == 0 && tri != 0) atomicAdd(p.tri_out, (unsigned long long)tri);
+    }
+  } else if (CMP) {
+    // ===================== compaction warps 6..9 =====================
+    const int cw = warp - 6;
+    int cached_mb = -1;
+    int64_t P = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
+      if (mb != cached_mb) {
+        int64_t v = 0;
+        if (lane == 0) v = mblock_prefix(p, mb);
+        P = __shfl_sync(0xffffffffu, v, 0);
+        cached_mb = mb;
+        __threadfence();
+      }
+      compact_tile_rows<BN_>(p, mb, nb, cw, P);
     }
   }
 
@@ -485,18 +650,19 @@ int pick_group_m(int tiles_m, int64_t rows_per_mblock, int64_t k_bytes) {
 }
 
 // Builds the tensor maps and launches the 1-CTA kernel for the chosen stage width.
-template <int BN_, bool FP4>
+template <int BN_, bool FP4, bool CMP = false>
 cudaError_t run_1cta(const GemmArgs& a, const KParams& p, int map_elem, int kb, cudaStream_t s, int64_t* launches) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 128, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Geo<BN_, 128>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 64, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)Geo<BN_, 64>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  constexpr int NT_ = CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREADS;
   const int64_t kcols = a.k_begin + a.k_len;
   CUtensorMap mA, mB;
   if (!make_map(&mA, a.A, map_elem, a.M, kcols, a.lda, BM, kb) ||
@@ -504,8 +670,8 @@ cudaError_t run_1cta(const GemmArgs& a, const KParams& p, int map_elem, int kb, 
     return cudaErrorInvalidValue;
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  if (kb == 64) k_gemm_tc<BN_, FP4, 64><<<grid, NUM_THREADS, Geo<BN_, 64>::SMEM_BYTES, s>>>(mA, mB, p);
-  else k_gemm_tc<BN_, FP4, 128><<<grid, NUM_THREADS, Geo<BN_, 128>::SMEM_BYTES, s>>>(mA, mB, p);
+  if (kb == 64) k_gemm_tc<BN_, FP4, 64, CMP><<<grid, NT_, Geo<BN_, 64>::SMEM_BYTES, s>>>(mA, mB, p);
+  else k_gemm_tc<BN_, FP4, 128, CMP><<<grid, NT_, Geo<BN_, 128>::SMEM_BYTES, s>>>(mA, mB, p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -518,7 +684,7 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   constexpr int BNF = kGemmBNFp4;
   if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
   if (a.M % BM || a.k_len % BKB || a.k_begin % BKB || a.lda % 16 || a.ldb % 16 ||
-      (a.epi != EPI_STORE32 && a.epi != EPI_STORE16))
+      (a.epi != EPI_STORE32 && a.epi != EPI_STORE16) || (a.cmp && a.epi != EPI_STORE16))
     return cudaErrorInvalidValue;
   const int64_t tiles_n = (a.N + BNF - 1) / BNF;
   if (a.ldc < tiles_n * BNF) return cudaErrorInvalidValue;
@@ -538,6 +704,14 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = 0;
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   p.group_m = pick_group_m(p.tiles_m, BM, a.k_len);
+  if (a.cmp) {
+    // M-blocks must complete early for their compaction to overlap later tiles: bands of
+    // 2 M-blocks (measured best of 1..40 on c2)
+    if (!getenv("TCUDB_GEMM_GROUP_M")) p.group_m = p.tiles_m < 2 ? p.tiles_m : 2;
+    p.fc = *static_cast<const FusedCompact*>(a.cmp);
+    p.cnt_out = p.fc.tcnt;  // non-null: the epilogue counts nonzeros (stored as tcnt[nb][row])
+    return run_1cta<BNF, true, true>(a, p, ELEM_I8, kb, s, launches);
+  }
   return run_1cta<BNF, true>(a, p, ELEM_I8, kb, s, launches);
 }
 

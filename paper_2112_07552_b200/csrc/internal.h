@@ -35,6 +35,22 @@ struct GemmArgs {
   // optional: per (row, 256-column N tile) count of nonzero results, cnt[row * ldcnt + n_tile]
   // (feeds the compaction scan, a8; only on the launch that produces the final matrix)
   int32_t* cnt_out = nullptr; int64_t ldcnt = 0;
+  // optional (fp4 COUNT with EPI_STORE16): compaction (a8) fused into the GEMM kernel —
+  // the result tuples are written in (g, h) order by compaction warps while later tiles
+  // are still being multiplied (see gemm_tc.cu). Scratch arrays are zeroed by the caller.
+  const void* cmp = nullptr;        // const FusedCompact* (device-visible fields by value)
+};
+// Fused-compaction parameters (gemm_tc.cu, EPI_STORE16 + fp4 only).
+struct FusedCompact {
+  int64_t G, H;                     // valid rows / columns of C
+  const long long* dict_g; const long long* dict_h;
+  int g_out_type, h_out_type;       // 0 I32, 1 I64
+  void* out_g; void* out_h; void* out_agg;  // capacity >= nnz (agg int64)
+  int32_t* tcnt;                    // [tiles_n][Mp] per-(N tile, row) counts -> offsets in the row
+  int32_t* rowbase;                 // [Mp] row offset inside its 128-row M-block
+  unsigned* mdone;                  // [tiles_m] epilogue-warp arrivals per M-block (zeroed)
+  unsigned long long* mstate;       // [tiles_m] look-back state per M-block (zeroed)
+  int64_t* total;                   // out: number of result tuples
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches);
 

@@ -421,6 +421,51 @@ def test_count_fp4_vs_u8_vs_oracle(engine, torch_mod, oracle_mod, name, scale):
     compare(o8, ref, agg)
 
 
+@pytest.mark.parametrize("case", ["c2", "c3", "ragged", "many_tiles", "empty_rows"])
+def test_fused_compaction_matches(engine, torch_mod, oracle_mod, monkeypatch, case):
+    """f1: compaction inside the e2m1 GEMM kernel (TCUDB_FUSED_COMPACT=1) vs the separate
+    compaction kernels (default) vs the oracle — bit-identical, (g, h)-ordered.
+    ragged: G, H not multiples of the tiles; many_tiles: > 148 M-blocks x N-tiles with
+    int64 group values; empty_rows: most A groups join nothing."""
+    rng = np.random.default_rng(11)
+    if case in ("c2", "c3"):
+        A, B, agg = datagen.make_config(case, {"c2": 0.25, "c3": 1 / 8}[case])
+    elif case == "ragged":
+        def side(n_rec, vocab):
+            rec = np.repeat(np.arange(n_rec), 7)
+            tok = np.concatenate([rng.choice(vocab, 7, replace=False) for _ in range(n_rec)])
+            return tok, rec
+        ka, ga = side(1333, 700)
+        kb, hb = side(977, 700)
+        A, B, agg = datagen.Table(ka, ga * 3 + 5), datagen.Table(kb, hb - 400), "count"
+    elif case == "many_tiles":
+        def side(n_rec, vocab, L):
+            rec = np.repeat(np.arange(n_rec), L)
+            tok = np.concatenate([rng.choice(vocab, L, replace=False) for _ in range(n_rec)])
+            return tok, rec
+        ka, ga = side(9000, 4000, 5)
+        kb, hb = side(6000, 4000, 5)
+        A = datagen.Table(ka.astype(np.int64), (ga.astype(np.int64) << 33) + 1)
+        B = datagen.Table(kb.astype(np.int64), hb.astype(np.int64) * 7 - (1 << 40))
+        agg = "count"
+    else:
+        ka = rng.choice(50000, 30000, replace=False)
+        ga = rng.integers(0, 20000, 30000)
+        kb = np.concatenate([ka[:300], rng.integers(60000, 90000, 5000)])
+        hb = rng.integers(0, 3000, len(kb))
+        A, B, agg = datagen.Table(ka, ga), datagen.Table(kb, hb), "count"
+    ref = oracle_mod.join_agg(A, B, agg)
+    monkeypatch.setenv("TCUDB_FUSED_COMPACT", "1")
+    of, sf = run(engine, torch_mod, A, B, agg, 1)
+    assert sf["elem"] == 3 and sf["fused_compact"] == 1
+    compare(of, ref, agg)
+    monkeypatch.setenv("TCUDB_FUSED_COMPACT", "0")
+    ou, su = run(engine, torch_mod, A, B, agg, 1)
+    assert su["fused_compact"] == 0
+    for k in ("g", "h", "agg"):
+        assert np.array_equal(of[k], ou[k])
+
+
 SHARD_SCRIPT = r"""
 import os, sys, numpy as np, torch, torch.distributed as dist
 sys.path.insert(0, os.getcwd())
