@@ -20,12 +20,14 @@ __all__ = [
 
 
 def Table(k, g, v=None):
+    """Column-store table {"k", "g", "v"}; g None = the side is not grouped."""
     k = np.ascontiguousarray(k)
-    g = np.ascontiguousarray(g)
+    if g is not None:
+        g = np.ascontiguousarray(g)
+        assert len(k) == len(g)
     if v is not None:
         v = np.ascontiguousarray(v)
         assert len(v) == len(k)
-    assert len(k) == len(g)
     return {"k": k, "g": g, "v": v}
 
 

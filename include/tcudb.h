@@ -42,7 +42,8 @@ typedef enum {
 } tcudb_status;
 
 typedef enum { TCUDB_I32 = 0, TCUDB_I64 = 1, TCUDB_F32 = 2, TCUDB_F64 = 3 } tcudb_dtype;
-typedef enum { TCUDB_COUNT = 0, TCUDB_SUM = 1 } tcudb_agg;
+/* COUNT(*), SUM(A.v * B.w), AVG(A.v * B.w) = SUM / COUNT (§3.3). */
+typedef enum { TCUDB_COUNT = 0, TCUDB_SUM = 1, TCUDB_AVG = 2 } tcudb_agg;
 
 /* One column: data == NULL means "absent". A value column that is absent means
  * the factor 1 (so SUM with both values absent equals COUNT). */
@@ -55,7 +56,9 @@ typedef struct {
 typedef struct {
   int64_t n_rows;
   tcudb_col key;   /* join key k (required) */
-  tcudb_col group; /* group key: A.g or B.h (required) */
+  tcudb_col group; /* group key: A.g or B.h. Absent (data == NULL): this side is not
+                      grouped — GROUP BY B.h only is Q3, no GROUP BY at all is
+                      Q4 — and the result's g (or h) array is NULL. */
   tcudb_col value; /* A.v or B.w (optional) */
 } tcudb_table;
 
@@ -88,6 +91,7 @@ typedef struct {
   void* agg;
   int32_t g_type, h_type, agg_type;
   int32_t on_host; /* 1 if the arrays are pinned host memory */
+  void* base;      /* device results: the single allocation (g, unless g is absent) */
 } tcudb_result;
 
 /* Plan and stage breakdown of one query (cf. SPEC ExecutionReport S:502-505 and

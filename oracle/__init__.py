@@ -95,17 +95,40 @@ def _vcol(v):
     raise TypeError(f"unsupported value dtype {v.dtype}")
 
 
+def _ungrouped(A, B, out):
+    """Drop the output column of an ungrouped side (its group was the constant 0)."""
+    if A.get("g") is None:
+        out.pop("g")
+    if B.get("g") is None:
+        out.pop("h")
+    return out
+
+
+def _group_col(T, n):
+    g = T.get("g")
+    # an absent group column = the side is not grouped: every tuple in one group
+    # (GROUP BY B.h only is Q3, P:785-823; no GROUP BY at all is Q4, P:842-850)
+    return np.zeros(n, np.int64) if g is None else np.ascontiguousarray(g, dtype=np.int64)
+
+
 def join_agg(A, B, agg="count", threads: int = 0):
     """SELECT A.g, B.h, agg FROM A JOIN B ON A.k = B.k GROUP BY A.g, B.h.
 
     agg: "count" -> COUNT(*); "sum" -> SUM(A.v * B.w) (an absent value column
-    is the constant 1). Raises OracleOverflow if an integer SUM leaves int64.
+    is the constant 1); "avg" -> AVG(A.v * B.w) = SUM / COUNT as
+    "avg" (float64: the int64 SUM or the fp64 SUM divided by the count).
+    A table whose "g" is None is not grouped: its output column is omitted.
+    Raises OracleOverflow if an integer SUM leaves int64.
     """
+    if agg == "avg":
+        out = join_agg(A, B, "sum", threads)
+        out["avg"] = out["sum"].astype(np.float64) / out["cnt"].astype(np.float64)
+        return out
     lib = _load()
     ak = np.ascontiguousarray(A["k"], dtype=np.int64)
-    ag = np.ascontiguousarray(A["g"], dtype=np.int64)
+    ag = _group_col(A, len(ak))
     bk = np.ascontiguousarray(B["k"], dtype=np.int64)
-    bh = np.ascontiguousarray(B["g"], dtype=np.int64)
+    bh = _group_col(B, len(bk))
     av, avk = _vcol(A.get("v") if agg == "sum" else None)
     bw, bwk = _vcol(B.get("v") if agg == "sum" else None)
     res = _Result()
@@ -127,7 +150,7 @@ def join_agg(A, B, agg="count", threads: int = 0):
                 out["sum"] = cp(res.isum, np.int64)
         if st == 1:
             raise OracleOverflow("integer SUM exceeds int64")
-        return out
+        return _ungrouped(A, B, out)
     finally:
         lib.oracle_free(ctypes.byref(res))
 
@@ -148,10 +171,12 @@ def nested_loop(A, B, agg="count"):
     in fp64) — i.e. the correctly rounded sum of the exact products.
     """
     import math
-    ak, ag, bk, bh = (list(map(int, A["k"])), list(map(int, A["g"])),
-                      list(map(int, B["k"])), list(map(int, B["g"])))
-    av = A.get("v") if agg == "sum" else None
-    bw = B.get("v") if agg == "sum" else None
+    from fractions import Fraction
+    ak, bk = list(map(int, A["k"])), list(map(int, B["k"]))
+    ag = list(map(int, A["g"])) if A.get("g") is not None else [0] * len(ak)
+    bh = list(map(int, B["g"])) if B.get("g") is not None else [0] * len(bk)
+    av = A.get("v") if agg != "count" else None
+    bw = B.get("v") if agg != "count" else None
     is_float = (av is not None and np.asarray(av).dtype.kind == "f") or \
                (bw is not None and np.asarray(bw).dtype.kind == "f")
     conv = float if is_float else int
@@ -166,7 +191,7 @@ def nested_loop(A, B, agg="count"):
     out = {"g": np.array([k[0] for k in keys], dtype=np.int64),
            "h": np.array([k[1] for k in keys], dtype=np.int64),
            "cnt": np.array([len(groups[k]) for k in keys], dtype=np.int64)}
-    if agg == "sum":
+    if agg in ("sum", "avg"):
         if is_float:
             out["sum"] = np.array([math.fsum(groups[k]) for k in keys], dtype=np.float64)
             out["abs"] = np.array([math.fsum(abs(x) for x in groups[k]) for k in keys], dtype=np.float64)
@@ -175,4 +200,11 @@ def nested_loop(A, B, agg="count"):
             if any(s > 2**63 - 1 or s < -2**63 for s in sums):
                 raise OracleOverflow("integer SUM exceeds int64")
             out["sum"] = np.array(sums, dtype=np.int64)
-    return out
+    if agg == "avg":
+        # the mean of each group's products: exact rational, rounded once (integers);
+        # fsum of the exact products / count (floats)
+        if is_float:
+            out["avg"] = np.array([math.fsum(groups[k]) / len(groups[k]) for k in keys], dtype=np.float64)
+        else:
+            out["avg"] = np.array([float(Fraction(sum(groups[k]), len(groups[k]))) for k in keys], dtype=np.float64)
+    return _ungrouped(A, B, out)

@@ -21,7 +21,8 @@ TCUDB_E_OVERFLOW, TCUDB_E_NOMEM, TCUDB_E_CUDA, TCUDB_E_COMM = -4, -5, -6, -7
 STATUS_NAMES = {0: "OK", -1: "E_INVALID", -2: "E_UNSUPPORTED", -3: "E_PRECISION", -4: "E_OVERFLOW",
                 -5: "E_NOMEM", -6: "E_CUDA", -7: "E_COMM"}
 I32, I64, F32, F64 = 0, 1, 2, 3
-COUNT, SUM = 0, 1
+COUNT, SUM, AVG = 0, 1, 2
+_AGG = {"count": COUNT, "sum": SUM, "avg": AVG}
 FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE, NO_FP4 = 1, 2, 4, 8, 16, 32
 
 EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_triangle_count", "tcudb_gemm",
@@ -50,7 +51,7 @@ class Query(ctypes.Structure):
 class Result(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("g", ctypes.c_void_p), ("h", ctypes.c_void_p), ("agg", ctypes.c_void_p),
                 ("g_type", ctypes.c_int32), ("h_type", ctypes.c_int32), ("agg_type", ctypes.c_int32),
-                ("on_host", ctypes.c_int32)]
+                ("on_host", ctypes.c_int32), ("base", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):
@@ -235,27 +236,28 @@ class Engine:
 
     @staticmethod
     def _table_dev(T):
-        k, g = T["k"], T["g"]
-        v = T.get("v")
-        for t in (k, g) + ((v,) if v is not None else ()):
-            if not t.is_cuda or not t.is_contiguous():
+        k, g, v = T["k"], T.get("g"), T.get("v")
+        for t in (k, g, v):
+            if t is not None and (not t.is_cuda or not t.is_contiguous()):
                 raise ValueError("columns must be contiguous CUDA tensors")
         ts = TableS()
         ts.n_rows = k.numel()
         ts.key = Col(k.data_ptr(), _dtype_code(k))
-        ts.group = Col(g.data_ptr(), _dtype_code(g))
+        # absent group column: this side is not grouped (Q3 / Q4 of PAPER.md §3.3)
+        ts.group = Col(g.data_ptr(), _dtype_code(g)) if g is not None else Col(None, 0)
         ts.value = Col(v.data_ptr(), _dtype_code(v)) if v is not None else Col(None, 0)
         return ts
 
     @staticmethod
     def _table_host(T):
-        k, g = np.ascontiguousarray(T["k"]), np.ascontiguousarray(T["g"])
-        v = T.get("v")
+        k = np.ascontiguousarray(T["k"])
+        g, v = T.get("g"), T.get("v")
+        g = None if g is None else np.ascontiguousarray(g)
         v = None if v is None else np.ascontiguousarray(v)
         ts = TableS()
         ts.n_rows = len(k)
         ts.key = Col(k.ctypes.data, _np_dtype_code(k))
-        ts.group = Col(g.ctypes.data, _np_dtype_code(g))
+        ts.group = Col(g.ctypes.data, _np_dtype_code(g)) if g is not None else Col(None, 0)
         ts.value = Col(v.ctypes.data, _np_dtype_code(v)) if v is not None else Col(None, 0)
         return ts, (k, g, v)
 
@@ -272,7 +274,7 @@ class Engine:
         """
         torch = self._torch
         ta, tb = self._table_dev(A), self._table_dev(B)
-        q = Query(COUNT if agg == "count" else SUM, int(flags))
+        q = Query(_AGG[agg], int(flags))
         res = Result()
         stats = Stats()
         st = self._lib.tcudb_join_agg(self._ctx, ctypes.byref(ta), ctypes.byref(tb), ctypes.byref(q),
@@ -281,6 +283,8 @@ class Engine:
         owner = _Owner(self, res)
         out = {}
         for key, ptr, code in (("g", res.g, res.g_type), ("h", res.h, res.h_type), ("agg", res.agg, res.agg_type)):
+            if key != "agg" and (A if key == "g" else B).get("g") is None:
+                continue  # ungrouped side: no output column
             if res.n == 0 or not ptr:
                 dt = {I32: torch.int32, I64: torch.int64, F32: torch.float32, F64: torch.float64}[code]
                 out[key] = torch.empty(0, dtype=dt, device=f"cuda:{self.device}")
@@ -293,7 +297,7 @@ class Engine:
         result tuples into pinned host memory — all inside the C library."""
         ta, keep_a = self._table_host(A)
         tb, keep_b = self._table_host(B)
-        q = Query(COUNT if agg == "count" else SUM, int(flags))
+        q = Query(_AGG[agg], int(flags))
         res = Result()
         stats = Stats()
         st = self._lib.tcudb_join_agg_host(self._ctx, ctypes.byref(ta), ctypes.byref(tb), ctypes.byref(q),
@@ -304,6 +308,8 @@ class Engine:
         owner = _HostOwner(self, res)
         out = {}
         for key, ptr, code in (("g", res.g, res.g_type), ("h", res.h, res.h_type), ("agg", res.agg, res.agg_type)):
+            if key != "agg" and (A if key == "g" else B).get("g") is None:
+                continue  # ungrouped side: no output column
             dt = np.dtype(_TYPESTR[code])
             out[key] = np.zeros(0, dt) if res.n == 0 else np.asarray(_HostArray(owner, ptr, res.n, dt))
         return (out, stats.to_dict()) if with_stats else out

@@ -204,6 +204,31 @@ cudaError_t launch_band_weight_max(const SpaArgs& a, unsigned long long* out, cu
 cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_spa_write(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 
+// ---------------------------------------------------------------- reduce.cu (§8(f) f2)
+// One side ungrouped (Q3 P:785-823, Q4 P:842-850) or AVG: segmented reductions.
+struct SideOut {
+  const long long* dict_grp;          // grouped side's ascending value dictionary
+  void* grp_out; int grp_type;        // its output column (0 I32, 1 I64)
+  void* const_out; int const_type;    // the single-group side's output column (NULL: absent)
+  long long const_val;
+  void* agg;                          // I64 (COUNT, int SUM) or F64 (float SUM, AVG)
+};
+// sum_k[kcode[i]] += v[i]; kind 1: int64 (wrapping), 2: fp64 of fp32 values
+cudaError_t launch_key_sum(const int32_t* kcode, const ColDesc& v, int64_t n, int kind, void* sum_k, cudaStream_t s,
+                           int64_t* launches);
+// cnt_g[g] += cnt_o[k]; sum_g[g] += w · (sum_o ? sum_o[k] : cnt_o[k]); kind 0 COUNT, 1 int, 2 float
+cudaError_t launch_side_agg(const int32_t* kcode, const int32_t* gcode, const ColDesc& w, int64_t n,
+                            const int32_t* cnt_o, const void* sum_o, int kind, int64_t NG,
+                            unsigned long long* cnt_g, void* sum_g, cudaStream_t s, int64_t* launches);
+cudaError_t launch_side_flags(const unsigned long long* cnt_g, int64_t NG, int32_t* flags, cudaStream_t s,
+                              int64_t* launches);
+// agg_kind: 0 COUNT, 1 int SUM, 2 float SUM, 3 AVG of int, 4 AVG of float
+cudaError_t launch_side_write(const unsigned long long* cnt_g, const void* sum_g, const int64_t* pos, int64_t NG,
+                              int agg_kind, const SideOut& o, cudaStream_t s, int64_t* launches);
+// in place: sum (int64 or fp64) -> fp64 sum / cnt
+cudaError_t launch_avg_div(void* sum_inout, int sum_is_float, const long long* cnt, int64_t n, cudaStream_t s,
+                           int64_t* launches);
+
 // ---------------------------------------------------------------- partition.cu (§8(e))
 cudaError_t launch_part_count(const ColDesc& grp, const long long* bounds, int P, unsigned long long* counts,
                               cudaStream_t s, int64_t* launches);

@@ -318,8 +318,12 @@ struct QueryOut {
   void *g = nullptr, *h = nullptr, *agg = nullptr;
 };
 
+// internal status: AVG with both sides grouped -> the ABI entry composes SUM and COUNT
+constexpr tcudb_status kComposeAvg = static_cast<tcudb_status>(99);
+
+// absent: bit 0 = A.group absent, bit 1 = B.group absent (materialized as constant columns)
 tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B, const tcudb_query* q,
-                          tcudb_result* out, tcudb_stats* st, cudaStream_t s) {
+                          tcudb_result* out, tcudb_stats* st, cudaStream_t s, unsigned absent = 0) {
   const auto t_host0 = std::chrono::steady_clock::now();
   int64_t* L = &ctx->launches;
   const int64_t launches0 = ctx->launches;
@@ -327,7 +331,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   tcudb_stats& S = st ? *st : local;
   std::memset(&S, 0, sizeof(S));
   Timer tm(ctx, s, st != nullptr);
-  const bool is_sum = q->agg == TCUDB_SUM;
+  const bool is_sum = q->agg != TCUDB_COUNT;  // SUM or AVG: the values matter
+  const bool is_avg = q->agg == TCUDB_AVG;
   const int64_t nA = A->n_rows, nB = B->n_rows;
   ColDesc ak{A->key.data, A->key.type, nA}, ag{A->group.data, A->group.type, nA};
   ColDesc bk{B->key.data, B->key.type, nB}, bh{B->group.data, B->group.type, nB};
@@ -336,7 +341,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const bool is_float = is_sum && ((av.data && av.type == TCUDB_F32) || (bw.data && bw.type == TCUDB_F32));
   out->g_type = A->group.type;
   out->h_type = B->group.type;
-  out->agg_type = is_float ? TCUDB_F64 : TCUDB_I64;
+  out->agg_type = (is_float || is_avg) ? TCUDB_F64 : TCUDB_I64;
   if (nA == 0 || nB == 0) return TCUDB_OK;
 
   Arena ar(s);
@@ -456,6 +461,62 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     const long double b2 = (long double)J * col_absmax(4) * col_absmax(5);
     if (std::min(b1, b2) >= 9.2e18L) throw Fail{TCUDB_E_OVERFLOW};
   }
+  // ---------------- §8(f) f2: one side ungrouped (Q3 / Q4 shapes) -> segmented reduction
+  // (a single distinct group on a grouped side takes it too, unless a path is forced)
+  if (absent || ((G == 1 || H == 1) && !(q->flags & (TCUDB_FORCE_DENSE | TCUDB_FORCE_SPARSE)))) {
+    S.path = 2;
+    const bool by_h = G == 1;  // reduce B's tuples into H groups with A's per-key (count, sum)
+    const int32_t* k_this = by_h ? kB : kA;
+    const int32_t* g_this = by_h ? hB : gA;
+    const ColDesc& v_this = by_h ? bw : av;
+    const ColDesc& v_oth = by_h ? av : bw;
+    const int64_t n_this = by_h ? nB : nA, n_oth = by_h ? nA : nB;
+    const int64_t NG = by_h ? H : G;
+    const int kind = !is_sum ? 0 : (is_float ? 2 : 1);
+    void* sum_oth = nullptr;
+    if (kind && v_oth.data) {
+      sum_oth = ar.zeros<unsigned long long>(K);
+      CK(launch_key_sum(by_h ? kA : kB, v_oth, n_oth, kind, sum_oth, s, L));
+    }
+    unsigned long long* cnt_g = ar.zeros<unsigned long long>(NG);
+    void* sum_g = ar.zeros<unsigned long long>(NG);
+    CK(launch_side_agg(k_this, g_this, kind ? v_this : ColDesc{nullptr, 0, 0}, n_this, by_h ? cntA : cntB, sum_oth,
+                       kind, NG, cnt_g, sum_g, s, L));
+    int32_t* flg = ar.get<int32_t>(NG);
+    int64_t* pos = ar.get<int64_t>(NG + 1);
+    CK(launch_side_flags(cnt_g, NG, flg, s, L));
+    void* tmp = ar.get<char>((int64_t)scan_temp_bytes(NG));
+    CK(exclusive_scan_i32(flg, pos, NG, pos + NG, tmp, s, L));
+    const int64_t n_res = *to_pinned<int64_t>(ctx, pos + NG, s);
+    tm.mark(&S.ms_sparse);
+    const size_t gb = A->group.type == TCUDB_I64 ? 8 : 4, hb = B->group.type == TCUDB_I64 ? 8 : 4;
+    const bool g_abs = absent & 1u, h_abs = absent & 2u;
+    const size_t og = 0, oh = g_abs ? 0 : ((size_t)n_res * gb + 255) / 256 * 256;
+    const size_t oa = oh + (h_abs ? 0 : ((size_t)n_res * hb + 255) / 256 * 256);
+    char* base = static_cast<char*>(result_alloc(ctx, oa + (size_t)n_res * 8, s));
+    SideOut o{};
+    o.dict_grp = by_h ? DH.dict : DG.dict;
+    void* gp = g_abs ? nullptr : base + og;
+    void* hp_ = h_abs ? nullptr : base + oh;
+    o.grp_out = by_h ? hp_ : gp;
+    o.grp_type = by_h ? (hb == 8) : (gb == 8);
+    o.const_out = by_h ? gp : hp_;
+    o.const_type = by_h ? (gb == 8) : (hb == 8);
+    o.const_val = by_h ? hs[2].mn : hs[3].mn;  // the single distinct value of the other group column
+    o.agg = base + oa;
+    const int agg_kind = is_avg ? (kind == 2 ? 4 : 3) : kind;
+    CK(launch_side_write(cnt_g, sum_g, pos, NG, agg_kind, o, s, L));
+    tm.mark(&S.ms_compact);
+    CK(cudaStreamSynchronize(s));
+    tm.finish();
+    out->n = n_res; out->g = gp; out->h = hp_; out->agg = o.agg; out->base = base; out->on_host = 0;
+    S.n_result = n_res;
+    S.n_launches = (int32_t)(ctx->launches - launches0);
+    S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    return TCUDB_OK;
+  }
+  if (is_avg) return kComposeAvg;  // both sides grouped: SUM and COUNT queries, then divide
+
   // sign consistency: C != 0 <=> COUNT > 0 when every product v*w has one strict sign
   auto strict_sign = [&](int c) -> bool {
     if (!cols[c].data) return true;
@@ -1009,7 +1070,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   tm.mark(&S.ms_compact);
   CK(cudaStreamSynchronize(s));
   tm.finish();
-  out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->on_host = 0;
+  out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->base = r.g; out->on_host = 0;
   S.n_result = nnz;
   S.spa_mode = !spa ? 0 : spa_one ? 3 : spa_fw ? 2 : 1;
   S.fused_compact = dense_fc ? 1 : 0;
@@ -1020,8 +1081,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
 
 tcudb_status check_table(const tcudb_table* t, bool need_value_ok) {
   if (!t || t->n_rows < 0) return TCUDB_E_INVALID;
-  if (t->n_rows > 0 && (!t->key.data || !t->group.data)) return TCUDB_E_INVALID;
-  if (!is_int_type(t->key.type) || !is_int_type(t->group.type)) return TCUDB_E_UNSUPPORTED;
+  if (t->n_rows > 0 && !t->key.data) return TCUDB_E_INVALID;
+  if (!is_int_type(t->key.type) || (t->group.data && !is_int_type(t->group.type))) return TCUDB_E_UNSUPPORTED;
   if (t->n_rows >= (1ll << 31)) return TCUDB_E_UNSUPPORTED;
   if (need_value_ok && t->value.data && !(is_int_type(t->value.type) || t->value.type == TCUDB_F32))
     return TCUDB_E_UNSUPPORTED;
@@ -1096,18 +1157,67 @@ tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_ta
   if (!ctx || !out) return TCUDB_E_INVALID;
   std::memset(out, 0, sizeof(*out));
   if (ctx->sticky) return set_err(ctx, TCUDB_E_CUDA, "context has a sticky CUDA error");
-  if (!q || (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM)) return set_err(ctx, TCUDB_E_INVALID, "bad query");
+  if (!q || (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM && q->agg != TCUDB_AVG))
+    return set_err(ctx, TCUDB_E_INVALID, "bad query");
   if ((q->flags & TCUDB_FORCE_DENSE) && (q->flags & TCUDB_FORCE_SPARSE))
     return set_err(ctx, TCUDB_E_INVALID, "FORCE_DENSE and FORCE_SPARSE are exclusive");
-  tcudb_status v = check_table(A, q->agg == TCUDB_SUM);
-  if (v == TCUDB_OK) v = check_table(B, q->agg == TCUDB_SUM);
+  const bool vals = q->agg != TCUDB_COUNT;
+  tcudb_status v = check_table(A, vals);
+  if (v == TCUDB_OK) v = check_table(B, vals);
   if (v != TCUDB_OK) return set_err(ctx, v, "bad table arguments");
-  if (q->agg == TCUDB_SUM && A->value.data && B->value.data &&
-      ((A->value.type == TCUDB_F32) != (B->value.type == TCUDB_F32)))
+  if (vals && A->value.data && B->value.data && ((A->value.type == TCUDB_F32) != (B->value.type == TCUDB_F32)))
     return set_err(ctx, TCUDB_E_UNSUPPORTED, "mixed integer / float value columns");
   cudaSetDevice(ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // an absent group column = that side is not grouped (Q3 / Q4): a constant
+  // column stands in (one group), and the result omits that column
+  tcudb_table A2 = *A, B2 = *B;
+  unsigned absent = 0;
+  void* zcol[2] = {nullptr, nullptr};
+  for (int side = 0; side < 2; ++side) {
+    tcudb_table& t = side ? B2 : A2;
+    if (t.group.data) continue;
+    absent |= 1u << side;
+    t.group.type = TCUDB_I32;
+    if (t.n_rows == 0) continue;
+    if (cudaMallocAsync(&zcol[side], (size_t)t.n_rows * 4, s) != cudaSuccess ||
+        cudaMemsetAsync(zcol[side], 0, (size_t)t.n_rows * 4, s) != cudaSuccess) {
+      cudaGetLastError();
+      for (void* p : zcol) if (p) cudaFreeAsync(p, s);
+      return set_err(ctx, TCUDB_E_NOMEM, "constant group column");
+    }
+    t.group.data = zcol[side];
+  }
+  struct ZFree { void** z; cudaStream_t s; ~ZFree() { for (int i = 0; i < 2; ++i) if (z[i]) cudaFreeAsync(z[i], s); } } zf{zcol, s};
   try {
-    return run_join_agg(ctx, A, B, q, out, stats, static_cast<cudaStream_t>(stream));
+    tcudb_status st = run_join_agg(ctx, &A2, &B2, q, out, stats, s, absent);
+    if (st != kComposeAvg) return st;
+    // AVG = SUM / COUNT with both sides grouped: the SUM and COUNT results
+    // have the same groups in the same (g, h) order
+    tcudb_query qs = *q, qc = *q;
+    qs.agg = TCUDB_SUM;
+    qc.agg = TCUDB_COUNT;
+    tcudb_result rs{}, rc{};
+    st = run_join_agg(ctx, &A2, &B2, &qs, &rs, stats, s, absent);
+    if (st != TCUDB_OK) return st;
+    try {
+      st = run_join_agg(ctx, &A2, &B2, &qc, &rc, nullptr, s, absent);
+    } catch (...) {
+      tcudb_result_free(ctx, &rs);
+      throw;
+    }
+    if (st != TCUDB_OK) { tcudb_result_free(ctx, &rs); return st; }
+    const cudaError_t e1 = launch_avg_div(rs.agg, rs.agg_type == TCUDB_F64, static_cast<const long long*>(rc.agg),
+                                          rs.n, s, &ctx->launches);
+    const cudaError_t e2 = cudaStreamSynchronize(s);
+    tcudb_result_free(ctx, &rc);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      tcudb_result_free(ctx, &rs);
+      return set_err(ctx, TCUDB_E_CUDA, "AVG division failed");
+    }
+    rs.agg_type = TCUDB_F64;
+    *out = rs;
+    return TCUDB_OK;
   } catch (const Fail& f) {
     std::memset(out, 0, sizeof(*out));
     return fail_err(ctx, f);
@@ -1158,13 +1268,16 @@ tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcu
   };
   const size_t gb = dr.g_type == TCUDB_I64 ? 8 : 4, hb = dr.h_type == TCUDB_I64 ? 8 : 4;
   out->n = dr.n; out->g_type = dr.g_type; out->h_type = dr.h_type; out->agg_type = dr.agg_type; out->on_host = 1;
-  out->g = host_block(dr.n * gb);
-  out->h = host_block(dr.n * hb);
+  const bool has_g = dr.g || (dr.n == 0 && A->group.data), has_h = dr.h || (dr.n == 0 && B->group.data);
+  out->g = has_g ? host_block(dr.n * gb) : nullptr;
+  out->h = has_h ? host_block(dr.n * hb) : nullptr;
   out->agg = host_block(dr.n * 8);
-  if (!out->g || !out->h || !out->agg) { tcudb_result_free(ctx, &dr); tcudb_result_free_host(ctx, out); return TCUDB_E_NOMEM; }
+  if ((has_g && !out->g) || (has_h && !out->h) || !out->agg) {
+    tcudb_result_free(ctx, &dr); tcudb_result_free_host(ctx, out); return TCUDB_E_NOMEM;
+  }
   if (dr.n) {
-    cudaMemcpyAsync(out->g, dr.g, dr.n * gb, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(out->h, dr.h, dr.n * hb, cudaMemcpyDeviceToHost, s);
+    if (dr.g) cudaMemcpyAsync(out->g, dr.g, dr.n * gb, cudaMemcpyDeviceToHost, s);
+    if (dr.h) cudaMemcpyAsync(out->h, dr.h, dr.n * hb, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(out->agg, dr.agg, dr.n * 8, cudaMemcpyDeviceToHost, s);
   }
   const cudaError_t e = cudaStreamSynchronize(s);
@@ -1309,7 +1422,7 @@ tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_
 void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r) {
   if (!ctx || !r) return;
   if (r->on_host) { tcudb_result_free_host(ctx, r); return; }
-  result_release(ctx, r->g);  // g is the base of the single g | h | agg allocation
+  result_release(ctx, r->base ? r->base : r->g);  // base of the single g | h | agg allocation
   std::memset(r, 0, sizeof(*r));
 }
 

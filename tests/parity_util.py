@@ -12,8 +12,9 @@ FLOOR = 0.01
 
 
 def to_dev(T, torch, device="cuda:0"):
-    out = {"k": torch.from_numpy(np.ascontiguousarray(T["k"])).to(device),
-           "g": torch.from_numpy(np.ascontiguousarray(T["g"])).to(device)}
+    out = {"k": torch.from_numpy(np.ascontiguousarray(T["k"])).to(device)}
+    if T.get("g") is not None:  # absent: the side is not grouped (Q3 / Q4)
+        out["g"] = torch.from_numpy(np.ascontiguousarray(T["g"])).to(device)
     if T.get("v") is not None:
         out["v"] = torch.from_numpy(np.ascontiguousarray(T["v"])).to(device)
     return out
@@ -24,11 +25,25 @@ def res_np(r):
 
 
 def compare(gpu, ref, agg, float_vals=False):
-    """Assert GPU result == oracle result (see module docstring)."""
-    g, h, a = np.asarray(gpu["g"]), np.asarray(gpu["h"]), np.asarray(gpu["agg"])
-    assert len(g) == len(ref["g"]), f"group count {len(g)} != oracle {len(ref['g'])}"
-    assert np.array_equal(g.astype(np.int64), ref["g"]), "g keys / order differ"
-    assert np.array_equal(h.astype(np.int64), ref["h"]), "h keys / order differ"
+    """Assert GPU result == oracle result (see module docstring). AVG: integer inputs
+    bit-exact (both sides divide the exact int64 SUM by the COUNT in fp64); float inputs
+    within the SUM tolerance scaled by 1 / COUNT."""
+    a = np.asarray(gpu["agg"])
+    assert len(a) == len(ref["cnt"]), f"group count {len(a)} != oracle {len(ref['cnt'])}"
+    for col in ("g", "h"):
+        assert (col in gpu) == (col in ref), f"column {col}: present on one side only"
+        if col in ref:
+            assert np.array_equal(np.asarray(gpu[col]).astype(np.int64), ref[col]), f"{col} keys / order differ"
+    if agg == "avg":
+        assert a.dtype == np.float64
+        if not float_vals:
+            assert np.array_equal(a, ref["avg"]), "integer AVG differs"
+        else:
+            err = np.abs(a - ref["avg"])
+            tol = FLOAT_RTOL * np.maximum(np.abs(ref["avg"]), FLOOR * ref["abs"] / ref["cnt"])
+            bad = err > tol
+            assert not bad.any(), f"{bad.sum()} float AVG groups outside tolerance; worst err {err.max():.3g}"
+        return
     if agg == "count":
         assert np.array_equal(a.astype(np.int64), ref["cnt"]), "COUNT differs"
     elif not float_vals:

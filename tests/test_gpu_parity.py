@@ -76,6 +76,43 @@ def test_random_tiny_vs_oracle(engine, torch_mod, oracle_mod, vkind, flags):
         compare(out, ref, agg, float_vals=(vkind == "float"))
 
 
+# ---------------------------------------------------------------- §8(f) f2: AVG, Q3, Q4
+@pytest.mark.parametrize("vkind", ["none", "int", "float"])
+@pytest.mark.parametrize("shape", ["gh", "h_only", "g_only", "none"])
+def test_f2_random_tiny_vs_oracle(engine, torch_mod, oracle_mod, vkind, shape):
+    """COUNT / SUM / AVG with both sides grouped, one side ungrouped (Q3) or none (Q4)."""
+    rng = np.random.default_rng(300 + len(shape) + {"none": 0, "int": 1, "float": 2}[vkind])
+    for _ in range(25):
+        A, B = datagen.random_tiny(rng, n_max=80, vkind=vkind, vmin=-20, vmax=20, allow_empty=True)
+        if shape in ("h_only", "none"):
+            A = dict(A, g=None)
+        if shape in ("g_only", "none"):
+            B = dict(B, g=None)
+        for agg in ("count", "sum", "avg"):
+            ref = oracle_mod.join_agg(A, B, agg)
+            out, st = run(engine, torch_mod, A, B, agg, 0)
+            compare(out, ref, agg, float_vals=(vkind == "float"))
+
+
+@pytest.mark.parametrize("name,scale,shape,agg", [
+    ("c2", 0.1, "h_only", "count"), ("c5s", 1 / 64, "h_only", "sum"), ("c5s", 1 / 64, "g_only", "avg"),
+    ("c5s", 1 / 64, "none", "sum"), ("c4", 1 / 256, "h_only", "sum"), ("c4", 1 / 256, "none", "avg"),
+    ("c5s", 1 / 256, "gh", "avg"), ("c4", 1 / 1024, "gh", "avg"), ("c2", 0.05, "gh", "avg")])
+def test_f2_configs_vs_oracle(engine, torch_mod, oracle_mod, name, scale, shape, agg):
+    """f2 on the configs' distributions: Q3 / Q4 shapes take the segmented-reduction path
+    (stats path 2); two-sided AVG composes the SUM and COUNT queries."""
+    A, B, _ = datagen.make_config(name, scale)
+    if shape in ("h_only", "none"):
+        A = dict(A, g=None)
+    if shape in ("g_only", "none"):
+        B = dict(B, g=None)
+    ref = oracle_mod.join_agg(A, B, agg)
+    out, st = run(engine, torch_mod, A, B, agg, 0)
+    if shape != "gh":
+        assert st["path"] == 2
+    compare(out, ref, agg, float_vals=(name == "c4"))
+
+
 def test_wide_count_path_matches(engine, torch_mod, oracle_mod):
     """FORCE_WIDE: int64 scratch + digit-plane guard path for COUNT, and cells > 255
     (a carry out of the packed u8 byte) — both exact."""

@@ -295,3 +295,81 @@ def test_generators_shapes():
     assert np.all(s != d) and len(np.unique(np.stack([s, d], 1), axis=0)) == len(s)
     k = datagen.scramble(np.arange(10, dtype=np.uint64))
     assert len(np.unique(k)) == 10 and k.dtype == np.int64
+
+
+# ---------------------------------------------------------------- §8(f) f2: AVG, Q3, Q4
+def _drop_g(T):
+    return {"k": T["k"], "g": None, "v": T["v"]}
+
+
+@pytest.mark.parametrize("vkind", ["none", "int", "float"])
+@pytest.mark.parametrize("shape", ["gh", "h_only", "g_only", "none"])
+def test_avg_and_ungrouped_vs_nested_loop(oracle_mod, vkind, shape):
+    """AVG (= SUM / COUNT) and ungrouped sides (Q3 P:785-823, Q4 P:842-850):
+    the hash oracle equals the pure-Python nested loop (exact rational mean for
+    integers, math.fsum of exact products for floats) on random tiny instances."""
+    rng = np.random.default_rng({"none": 1, "int": 2, "float": 3}[vkind] * 10 + len(shape))
+    for _ in range(120):
+        A, B = datagen.random_tiny(rng, vkind=vkind)
+        if shape in ("h_only", "none"):
+            A = _drop_g(A)
+        if shape in ("g_only", "none"):
+            B = _drop_g(B)
+        for agg in ("count", "sum", "avg"):
+            got = oracle_mod.join_agg(A, B, agg)
+            ref = oracle_mod.nested_loop(A, B, agg)
+            assert set(got) == set(ref)
+            for col in ("g", "h", "cnt"):
+                if col in ref:
+                    assert np.array_equal(got[col], ref[col])
+            if agg != "count":
+                if vkind == "float":
+                    assert np.allclose(got["sum"], ref["sum"], rtol=1e-12, atol=1e-9)
+                else:
+                    assert np.array_equal(got["sum"], ref["sum"])
+            if agg == "avg":
+                if vkind == "float":
+                    assert np.allclose(got["avg"], ref["avg"], rtol=1e-12, atol=1e-9)
+                else:
+                    assert np.array_equal(got["avg"], ref["avg"])
+
+
+def test_q3_q4_spec_examples_ungrouped(oracle_mod):
+    """SPEC S:514 (Q3: GROUP BY B.Val only -> g1: 30) and S:515 (Q4: no GROUP BY -> 6)
+    with the constant group columns of the golden fixtures replaced by absent ones."""
+    A = {"k": np.array([1, 2]), "g": None, "v": np.array([10, 20])}
+    B = {"k": np.array([1, 2]), "g": np.array([1, 1]), "v": None}
+    r = oracle_mod.join_agg(A, B, "sum")
+    assert "g" not in r and r["h"].tolist() == [1] and r["sum"].tolist() == [30]
+    A = {"k": np.array([7]), "g": None, "v": np.array([2])}
+    B = {"k": np.array([7]), "g": None, "v": np.array([3])}
+    r = oracle_mod.join_agg(A, B, "sum")
+    assert "g" not in r and "h" not in r and r["sum"].tolist() == [6] and r["cnt"].tolist() == [1]
+    assert oracle_mod.join_agg(A, B, "avg")["avg"].tolist() == [6.0]
+
+
+def test_ungrouped_closed_forms(oracle_mod):
+    """Q3 with A ungrouped: SUM(h) = sum_{b.h=h} w_b * SA(b.k) and COUNT(h) =
+    sum_{b.h=h} cntA(b.k); Q4: SUM = sum_k SA(k) * SB(k), COUNT = J — computed here
+    with independent per-key dictionaries (the 1^{1xn} x mat(A) reduction)."""
+    rng = np.random.default_rng(21)
+    A = datagen.Table(rng.integers(0, 400, 20000), None, rng.integers(-50, 51, 20000))
+    B = datagen.Table(rng.integers(0, 400, 15000), rng.integers(0, 90, 15000), rng.integers(-50, 51, 15000))
+    SA, CA = {}, {}
+    for k, v in zip(A["k"].tolist(), A["v"].tolist()):
+        SA[k] = SA.get(k, 0) + v
+        CA[k] = CA.get(k, 0) + 1
+    per_h, cnt_h = {}, {}
+    for k, h, w in zip(B["k"].tolist(), B["g"].tolist(), B["v"].tolist()):
+        if k in CA:
+            per_h[h] = per_h.get(h, 0) + w * SA[k]
+            cnt_h[h] = cnt_h.get(h, 0) + CA[k]
+    r = oracle_mod.join_agg(A, B, "sum")
+    assert r["h"].tolist() == sorted(per_h)
+    assert r["sum"].tolist() == [per_h[h] for h in sorted(per_h)]
+    assert r["cnt"].tolist() == [cnt_h[h] for h in sorted(per_h)]
+    SB = {}
+    for k, w in zip(B["k"].tolist(), B["v"].tolist()):
+        SB[k] = SB.get(k, 0) + w
+    q4 = oracle_mod.join_agg(A, _drop_g(B), "sum")
+    assert q4["sum"].tolist() == [sum(SA[k] * SB.get(k, 0) for k in SA)]
