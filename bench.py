@@ -218,7 +218,7 @@ def main():
     torch.cuda.synchronize()
     launches0 = eng.launch_count
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    gemm_ms, stats_last = [], None
+    gemm_ms, kernel_ms, stats_last = [], [], None
     with ClockSampler(local) as clk:
         if sharded:
             torch.distributed.barrier()
@@ -229,6 +229,7 @@ def main():
             out, st = step()
             ev[i][1].record(stream)
             gemm_ms.append(st["ms_gemm"] if st["path"] == 0 else st["ms_sparse"])
+            kernel_ms.append(st["ms_kernel"])
             stats_last = st
             del out
         torch.cuda.synchronize()
@@ -317,13 +318,24 @@ def main():
                 "vs_int8_peak": achieved / int8_peak,
                 "ops_per_launch": ops, "avg_launch_ms": g_ms,
                 "traffic": gemm_traffic_from_profiles(args.config, st["elem"])}
+    elif st["ms_kernel"] > 0:
+        # sparse path: the persistent band kernel k_spa_fused (expand into shared-memory rows +
+        # ordered write), HBM-bound; algorithmic bytes per launch =
+        # 4 B per joined pair (bucket entry) + 20 B per active A tuple + the result tuples
+        k_ms = statistics.mean(kernel_ms)
+        achieved = st["kernel_bytes"] / (k_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_spa_fused (band SPA: expand + ordered write)", "achieved": achieved,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "peak_source": f"{peaks['source']} copy bandwidth", "bytes_per_launch": st["kernel_bytes"],
+                "avg_launch_ms": k_ms, "spa_mode": {2: "count pass + band writer", 3: "one pass (look-back)"}.get(
+                    st["spa_mode"], st["spa_mode"]), "traffic": None}
     else:
-        # sparse path: HBM-bound expand; algorithmic bytes = 16 B per update (read bucket entry + RMW C) approx.
+        # sparse or reduction path without the band kernel: stage time, 16 B per joined pair
         b = st["join_pairs"] * 16.0
         g_ms = statistics.mean(gemm_ms)
         achieved = b / (g_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "k_expand", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None}
+        roof = {"bound": "hbm", "kernel": "sparse stage", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:  # the CPU baseline runs on rank 0 at N=1 only
         import oracle

@@ -115,6 +115,8 @@ typedef struct {
                            2 count pass + persistent band writer, 3 one persistent pass */
   int64_t spa_max_band; /* sparse path: most updates of one band of result rows */
   int32_t fused_compact; /* dense path: 1 if the compaction ran inside the GEMM kernel */
+  float ms_kernel;       /* sparse path: CUDA-event time of the band kernel (k_spa_fused) */
+  double kernel_bytes;   /* ... and its algorithmic bytes (4 J + 20 n_active + result bytes) */
 } tcudb_stats;
 
 typedef struct tcudb_ctx tcudb_ctx;

@@ -41,6 +41,7 @@ struct tcudb_ctx {
   void* pinned_big = nullptr;  // sketch registers (3 x kHllM x 4 B)
   size_t mem_free0 = 0;        // free device memory at creation (path-selection budget)
   cudaEvent_t ev[8] = {};
+  cudaEvent_t evk[2] = {};   // the sparse path's band kernel (roofline timing)
   std::mutex mu;
   // pinned host block cache for host-API results: size -> free blocks
   std::multimap<size_t, void*> host_free;
@@ -571,6 +572,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   bool spa = false;            // sparse path through spa.cu (no C matrix)
   bool spa_fw = false;         // ... on the persistent band kernel (spa.cu k_spa_fused)
   bool spa_one = false;        // ... in one pass (no count pass)
+  bool spa_timed = false;      // evk[] bracket the band kernel
   bool dense_fc = false;       // dense path: compaction fused into the GEMM (f1)
   void* fc_out[3] = {nullptr, nullptr, nullptr};
   int64_t* d_fc_total = nullptr;
@@ -928,7 +930,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         sa.total = ar.zeros<int64_t>(1);
         sa.ovf = ar.zeros<int>(1);
         sa.row_out = nullptr;
+        if (st) cudaEventRecord(ctx->evk[0], s);
         CK(launch_spa_fused(sa, s, L));
+        if (st) cudaEventRecord(ctx->evk[1], s);
+        spa_timed = true;
       } else {
         sa.row_nnz = ar.get<int32_t>(G);
         int64_t* row_out = ar.get<int64_t>(G + 1);
@@ -1052,7 +1057,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       if (spa_fw) {
         // write pass on the persistent band kernel; a u16 COUNT cell reaching 65,535 is
         // redone by the int32 write pass (same bands, same offsets)
+        if (st) cudaEventRecord(ctx->evk[0], s);
         CK(launch_spa_fused(sa, s, L));
+        if (st) cudaEventRecord(ctx->evk[1], s);
+        spa_timed = true;
         if (sa.acc_kind == 4 && *to_pinned<int>(ctx, sa.ovf, s)) {
           sa.acc_kind = 0;
           CK(launch_spa_write(sa, s, L));
@@ -1073,6 +1081,12 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->base = r.g; out->on_host = 0;
   S.n_result = nnz;
   S.spa_mode = !spa ? 0 : spa_one ? 3 : spa_fw ? 2 : 1;
+  if (st && spa_timed) {
+    // band kernel: algorithmic bytes = bucket entries read (4 B per joined pair) + the
+    // active A tuples' (offset, bucket, row) read (20 B each) + result tuples written
+    cudaEventElapsedTime(&S.ms_kernel, ctx->evk[0], ctx->evk[1]);
+    S.kernel_bytes = 4.0 * (double)J + 20.0 * (double)misc[3] + (double)nnz * (double)(gb + hb + 8);
+  }
   S.fused_compact = dense_fc ? 1 : 0;
   S.n_launches = (int32_t)(ctx->launches - launches0);
   S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
@@ -1148,6 +1162,7 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
     return TCUDB_E_CUDA;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  for (auto& e : c->evk) cudaEventCreate(&e);
   *out = c;
   return TCUDB_OK;
 }
@@ -1449,6 +1464,7 @@ void tcudb_destroy(tcudb_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_big) cudaFreeHost(ctx->pinned_big);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->evk) if (e) cudaEventDestroy(e);
   delete ctx;
 }
 
