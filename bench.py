@@ -324,10 +324,13 @@ def main():
         # 4 B per joined pair (bucket entry) + 20 B per active A tuple + the result tuples
         k_ms = statistics.mean(kernel_ms)
         achieved = st["kernel_bytes"] / (k_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "k_spa_fused (band SPA: expand + ordered write)", "achieved": achieved,
+        kname = ("k_part_expand (hash-partitioned expand, one L2 reduction per joined pair)" if st["spa_mode"] == 4
+                 else "k_spa_fused (band SPA: expand + ordered write)")
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "peak_source": f"{peaks['source']} copy bandwidth", "bytes_per_launch": st["kernel_bytes"],
-                "avg_launch_ms": k_ms, "spa_mode": {2: "count pass + band writer", 3: "one pass (look-back)"}.get(
+                "avg_launch_ms": k_ms, "spa_mode": {2: "count pass + band writer", 3: "one pass (look-back)",
+                                                    4: "hash-partitioned"}.get(
                     st["spa_mode"], st["spa_mode"]), "traffic": None}
     else:
         # sparse or reduction path without the band kernel: stage time, 16 B per joined pair

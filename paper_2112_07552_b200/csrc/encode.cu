@@ -462,46 +462,36 @@ __global__ void k_rank_write(const unsigned long long* __restrict__ keys, const 
   }
 }
 
-// Small hash-mode group domains (<= 4096 distinct values, <= 64 K slots): gather, bitonic
-// sort and rank write in ONE block (instead of a multi-launch radix sort).
-constexpr int SMALL_SORT = 4096;
-__global__ void __launch_bounds__(1024) k_small_rank(const int32_t* __restrict__ code_in,
-                                                     const unsigned long long* __restrict__ slots, int64_t cap,
-                                                     int count, long long minv, int32_t* __restrict__ slot_code,
-                                                     long long* __restrict__ dict, int32_t* __restrict__ remap) {
-  extern __shared__ unsigned long long sk[];               // [SMALL_SORT] keys
-  int* sv = reinterpret_cast<int*>(sk + SMALL_SORT);       // [SMALL_SORT] old (compaction-order) code
-  int* ss = sv + SMALL_SORT;                               // [SMALL_SORT] slot
-  int P = 1;
-  while (P < count) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) { sk[i] = ~0ull; sv[i] = -1; ss[i] = -1; }
-  __syncthreads();
-  for (int64_t s = threadIdx.x; s < cap; s += blockDim.x) {
+constexpr int SMALL_SORT = 4096;  // small hash-mode group domains: rank by counting
+
+// Rank by counting for small domains (<= SMALL_SORT values): gather the distinct keys
+// (code_in[slot] >= 0) into code order, then every value's rank = #{keys < it}, computed
+// by many blocks against a shared-memory copy of all keys (keys are distinct).
+__global__ void k_small_gather(const int32_t* __restrict__ code_in, const unsigned long long* __restrict__ slots,
+                               int64_t cap, unsigned long long* __restrict__ keys, int32_t* __restrict__ slot_of) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += stride) {
     const int32_t c = code_in[s];
-    if (c >= 0) { sk[c] = slots[s]; sv[c] = c; ss[c] = (int)s; }
+    if (c >= 0) { keys[c] = slots[s]; slot_of[c] = (int32_t)s; }
   }
+}
+
+__global__ void __launch_bounds__(256) k_small_count_rank(const unsigned long long* __restrict__ keys,
+                                                          const int32_t* __restrict__ slot_of, int count,
+                                                          long long minv, int32_t* __restrict__ slot_code,
+                                                          long long* __restrict__ dict, int32_t* __restrict__ remap) {
+  __shared__ unsigned long long sk[SMALL_SORT];
+  for (int i = threadIdx.x; i < count; i += blockDim.x) sk[i] = keys[i];
   __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const bool up = (i & k) == 0;
-          if ((sk[i] > sk[l]) == up) {
-            unsigned long long tk = sk[i]; sk[i] = sk[l]; sk[l] = tk;
-            int tv = sv[i]; sv[i] = sv[l]; sv[l] = tv;
-            int ts = ss[i]; ss[i] = ss[l]; ss[l] = ts;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < count; i += blockDim.x) {
-    remap[sv[i]] = i;
-    slot_code[ss[i]] = i;
-    dict[i] = (long long)(sk[i] + (unsigned long long)minv);
-  }
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= count) return;
+  const unsigned long long x = sk[c];
+  int r = 0;
+#pragma unroll 8
+  for (int i = 0; i < count; ++i) r += sk[i] < x;  // broadcast reads: no bank conflicts
+  if (remap) remap[c] = r;
+  slot_code[slot_of[c]] = r;
+  dict[r] = (long long)(x + (unsigned long long)minv);
 }
 
 __global__ void k_remap_codes(int32_t* __restrict__ codes, int64_t n, const int32_t* __restrict__ remap) {
@@ -704,6 +694,27 @@ __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, Dict
   }
 }
 
+// Group codes only (the hash-partitioned sparse path encodes the join key itself).
+__global__ void k_group_codes(ColDesc grp, DictView gd, int32_t* __restrict__ gcode) {
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < grp.n; i0 += U * stride) {
+    long long x[U];
+    bool ok[U];
+    int32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      ok[u] = i < grp.n;
+      x[u] = ok[u] && !gd.row_slot ? ld_int(grp.data, grp.type, i) : 0;
+    }
+    rows_lookup<U>(gd, x, ok, i0, stride, c);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) gcode[i0 + u * stride] = c[u];
+  }
+}
+
 // J = sum_k cntA[k] * cntB[k] (join size, a4) and max per-key counts.
 // out[0] = J = sum_k cntA[k]*cntB[k]; out[3] = sum cntA, out[4] = sum cntB (tuples with a
 // key in the ∩ domain on each side)
@@ -875,21 +886,21 @@ cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* va
   return cudaGetLastError();
 }
 
-// (one block: gather + bitonic sort of <= 4 K values vs ~12 launches of the radix sort)
+// (gather + rank by counting of <= 4 K values vs ~12 launches of the radix sort)
 bool small_rank_ok(int64_t count, int64_t cap) { return count <= SMALL_SORT && cap <= (1 << 16); }
 
+size_t small_rank_temp_bytes() { return (size_t)SMALL_SORT * 12 + 256; }
+
 cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slots, int64_t cap, int64_t count,
-                              long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
-                              int64_t* launches) {
+                              long long minv, int32_t* slot_code, long long* dict, int32_t* remap, void* temp,
+                              cudaStream_t s, int64_t* launches) {
   if (count <= 0) return cudaSuccess;
-  constexpr size_t smem = (size_t)SMALL_SORT * 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_small_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_small_rank<<<1, 1024, smem, s>>>(code, slots, cap, (int)count, minv, slot_code, dict, remap);
-  if (launches) ++*launches;
+  unsigned long long* keys = static_cast<unsigned long long*>(temp);
+  int32_t* slot_of = reinterpret_cast<int32_t*>(keys + SMALL_SORT);
+  k_small_gather<<<grid_for(cap), T, 0, s>>>(code, slots, cap, keys, slot_of);
+  k_small_count_rank<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(keys, slot_of, (int)count, minv, slot_code, dict,
+                                                                    remap);
+  if (launches) *launches += 2;
   return cudaGetLastError();
 }
 
@@ -941,6 +952,14 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
     return cudaGetLastError();
   }
   k_probe<<<grid_for(key.n), T, 0, s>>>(key, grp, val, kd, gd, kcode, gcode, cnt_k, rowabs_g);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_codes(const ColDesc& grp, const DictView& gd, int32_t* gcode, cudaStream_t s,
+                               int64_t* launches) {
+  if (grp.n <= 0) return cudaSuccess;
+  k_group_codes<<<grid_for(grp.n), T, 0, s>>>(grp, gd, gcode);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

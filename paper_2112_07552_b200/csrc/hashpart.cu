@@ -1,0 +1,458 @@
+// hashpart.cu — steps a2 + a7 for large hash-mode key domains: a hash-partitioned
+// sparse COUNT.
+//
+// PAPER.md §3.1 encodes dom(ID) as matrix columns; §4.2.4
+// sends low-density joins (c5: 4 M keys, density < 0.1 %) to a sparse product. With
+// millions of distinct keys a global hash dictionary (hundreds of MB) and the
+// per-key buckets of B are random-access structures far larger than the SM's
+// caches. Here both tables are radix-partitioned on the key's hash first (two
+// passes of <= 7 bits, each staged in shared memory so the writes leave as runs),
+// until one partition's keys fit one CTA's shared memory. Per partition, a CTA then
+//   count:  builds the partition's key dictionary (slot = code; D_p keys on both
+//           sides), per-key counts cntA / cntB and J_p = sum cntA·cntB (the join
+//           size for the selector, a4);
+//   expand: rebuilds it, buckets B's group codes by key (counting sort in shared
+//           memory) and expands every A tuple over its key's bucket with one
+//           fire-and-forget reduction C[g][h] += 1 per joined pair (C: G x H u32,
+//           L2-resident at c5's 4,096 x 4,096).
+// The key dictionary is partition-local: a key's code is (partition, slot), a dense
+// code space of size K = sum_p D_p (reading R2: codes in hash order in hash mode).
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tcudb {
+namespace {
+
+constexpr int PT = 1024;       // threads per partitioning block
+constexpr int CH = 4 * PT;     // tuples per partitioning chunk
+constexpr int kMaxDigits = 128;
+
+TCUDB_DEV unsigned long long mix64(unsigned long long k) {
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+// chunk -> (segment, chunk in segment): chunk_start[s] = first global chunk of segment s
+TCUDB_DEV int find_seg(const int64_t* __restrict__ chunk_start, int nseg, int64_t c) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (chunk_start[mid] <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void k_chunk_starts(const int64_t* __restrict__ seg_off, int nseg, int64_t* __restrict__ chunk_start) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t c = 0;
+    for (int s = 0; s < nseg; ++s) {
+      chunk_start[s] = c;
+      c += (seg_off[s + 1] - seg_off[s] + CH - 1) / CH;
+    }
+    chunk_start[nseg] = c;
+  }
+}
+
+struct PassIO {
+  const void* raw; int raw_type; long long kmin; const int32_t* g_raw;  // pass 1 (raw column)
+  const unsigned long long* k_in; const int32_t* g_in;
+  const int64_t* seg_off; int nseg; int shift; int bits;
+  const int64_t* chunk_start;
+  int32_t* counts;  // [total_chunks * R] in (segment, digit, chunk) order
+  const int64_t* offs;  // exclusive scan of counts
+  unsigned long long* k_out; int32_t* g_out; int64_t* seg_out;
+};
+
+TCUDB_DEV void load_tuple(const PassIO& io, int64_t i, unsigned long long& k, int32_t& g) {
+  if (io.raw) {
+    k = (unsigned long long)ld_int(io.raw, io.raw_type, i) - (unsigned long long)io.kmin;
+    g = io.g_raw[i];
+  } else {
+    k = io.k_in[i];
+    g = io.g_in[i];
+  }
+}
+
+__global__ void __launch_bounds__(PT) k_part_hist(const PassIO io) {
+  __shared__ int h[kMaxDigits];
+  const int64_t c = blockIdx.x;
+  if (c >= io.chunk_start[io.nseg]) return;
+  const int s = find_seg(io.chunk_start, io.nseg, c);
+  const int64_t j = c - io.chunk_start[s];
+  const int64_t nch = io.chunk_start[s + 1] - io.chunk_start[s];
+  const int R = 1 << io.bits;
+  for (int d = threadIdx.x; d < R; d += PT) h[d] = 0;
+  __syncthreads();
+  const int64_t lo = io.seg_off[s] + j * CH, hi = min(io.seg_off[s + 1], lo + CH);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += PT) {
+    unsigned long long k; int32_t g;
+    load_tuple(io, i, k, g);
+    atomicAdd(&h[(int)((mix64(k) >> io.shift) & (unsigned)(R - 1))], 1);
+  }
+  __syncthreads();
+  const int64_t base = io.chunk_start[s] * R;
+  for (int d = threadIdx.x; d < R; d += PT) io.counts[base + (int64_t)d * nch + j] = h[d];
+}
+
+__global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
+  extern __shared__ __align__(16) uint8_t stage_raw[];
+  unsigned long long* sk = reinterpret_cast<unsigned long long*>(stage_raw);  // [CH]
+  int32_t* sg = reinterpret_cast<int32_t*>(sk + CH);                          // [CH]
+  __shared__ int cnt[kMaxDigits], lstart[kMaxDigits];
+  __shared__ int64_t gpos[kMaxDigits];
+  const int64_t c = blockIdx.x;
+  if (c >= io.chunk_start[io.nseg]) return;
+  const int s = find_seg(io.chunk_start, io.nseg, c);
+  const int64_t j = c - io.chunk_start[s];
+  const int64_t nch = io.chunk_start[s + 1] - io.chunk_start[s];
+  const int R = 1 << io.bits;
+  const int64_t base = io.chunk_start[s] * R;
+  for (int d = threadIdx.x; d < R; d += PT) {
+    cnt[d] = 0;
+    gpos[d] = io.offs[base + (int64_t)d * nch + j];
+  }
+  __syncthreads();
+  const int64_t lo = io.seg_off[s] + j * CH, hi = min(io.seg_off[s + 1], lo + CH);
+  unsigned long long k[4];
+  int32_t g[4];
+  int d[4], r[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = lo + threadIdx.x + u * PT;
+    d[u] = -1;
+    if (i < hi) {
+      load_tuple(io, i, k[u], g[u]);
+      d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
+      r[u] = atomicAdd(&cnt[d[u]], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of <= 128 digit counts, 4 per lane
+    int v[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int dd = threadIdx.x * 4 + q;
+      v[q] = dd < R ? cnt[dd] : 0;
+      sum += v[q];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)threadIdx.x >= o) incl += t;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int dd = threadIdx.x * 4 + q;
+      if (dd < R) lstart[dd] = run;
+      run += v[q];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (d[u] >= 0) {
+      const int p = lstart[d[u]] + r[u];
+      sk[p] = k[u];
+      sg[p] = g[u];
+    }
+  __syncthreads();
+  const int total = (int)(hi - lo);
+  for (int p = threadIdx.x; p < total; p += PT) {
+    // digit of staged entry p: the last digit whose local start is <= p (binary search)
+    int a = 0, b = R - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (lstart[m] <= p) a = m; else b = m - 1;
+    }
+    const int64_t o = gpos[a] + (p - lstart[a]);
+    io.k_out[o] = sk[p];
+    io.g_out[o] = sg[p];
+  }
+}
+
+// new segment offsets: seg_out[s * R + d] = start of digit d of segment s (empty segments
+// start where they are); seg_out[nseg * R] = end
+__global__ void k_seg_out(const PassIO io) {
+  const int R = 1 << io.bits;
+  const int64_t total = (int64_t)io.nseg * R;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= total; x += (int64_t)gridDim.x * blockDim.x) {
+    if (x == total) { io.seg_out[x] = io.seg_off[io.nseg]; continue; }
+    const int s = (int)(x / R), d = (int)(x - (int64_t)s * R);
+    const int64_t nch = io.chunk_start[s + 1] - io.chunk_start[s];
+    io.seg_out[x] = nch ? io.offs[io.chunk_start[s] * R + (int64_t)d * nch] : io.seg_off[s];
+  }
+}
+
+// ---- per-partition kernels: open-addressing table of TS slots in shared memory
+constexpr int QT = 512;
+
+TCUDB_DEV int slot_of(unsigned long long k, int ts_bits) {
+  return (int)((k * 0x9E3779B97F4A7C15ull) >> (64 - ts_bits));
+}
+
+// insert (or find) k; returns its slot
+TCUDB_DEV int tab_insert(unsigned long long* keys, int mask, int ts_bits, unsigned long long k) {
+  int h = slot_of(k, ts_bits);
+  while (true) {
+    const unsigned long long cur = keys[h];
+    if (cur == k) return h;
+    if (cur == ~0ull) {
+      const unsigned long long prev = atomicCAS(keys + h, ~0ull, k);
+      if (prev == ~0ull || prev == k) return h;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+TCUDB_DEV int tab_find(const unsigned long long* keys, int mask, int ts_bits, unsigned long long k) {
+  int h = slot_of(k, ts_bits);
+  while (true) {
+    const unsigned long long cur = keys[h];
+    if (cur == k) return h;
+    if (cur == ~0ull) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void __launch_bounds__(QT) k_part_count(const unsigned long long* __restrict__ ka,
+                                                   const int64_t* __restrict__ offa,
+                                                   const unsigned long long* __restrict__ kb,
+                                                   const int64_t* __restrict__ offb, int ts_bits,
+                                                   unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int TS = 1 << ts_bits, mask = TS - 1;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+  int* ca = reinterpret_cast<int*>(keys + TS);
+  int* cb = ca + TS;
+  for (int i = threadIdx.x; i < TS; i += QT) { keys[i] = ~0ull; ca[i] = 0; cb[i] = 0; }
+  __syncthreads();
+  const int p = blockIdx.x;
+  for (int64_t i = offb[p] + threadIdx.x; i < offb[p + 1]; i += QT)
+    atomicAdd(cb + tab_insert(keys, mask, ts_bits, __ldcs(kb + i)), 1);
+  __syncthreads();
+  for (int64_t i = offa[p] + threadIdx.x; i < offa[p + 1]; i += QT) {
+    const int h = tab_find(keys, mask, ts_bits, __ldcs(ka + i));
+    if (h >= 0) atomicAdd(ca + h, 1);
+  }
+  __syncthreads();
+  unsigned long long J = 0, D = 0, M = 0, U = 0;
+  for (int i = threadIdx.x; i < TS; i += QT) {
+    J += (unsigned long long)ca[i] * (unsigned long long)cb[i];
+    D += (ca[i] > 0 && cb[i] > 0);
+    M += cb[i] > 0 ? (unsigned long long)ca[i] : 0ull;
+    U += cb[i] > 0;
+  }
+  // per-partition totals (summed by k_part_sum: same-address atomics from every warp of
+  // 16 K CTAs would serialize in L2)
+  __shared__ unsigned long long red[4][QT / 32];
+  J = warp_sum(J); D = warp_sum(D); M = warp_sum(M); U = warp_sum(U);
+  if (lane_id() == 0) { red[0][warp_id()] = J; red[1][warp_id()] = D; red[2][warp_id()] = M; red[3][warp_id()] = U; }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    unsigned long long t = 0;
+    for (int w = 0; w < QT / 32; ++w) t += red[threadIdx.x][w];
+    out[(int64_t)p * 4 + threadIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_part_sum(const unsigned long long* __restrict__ per, int P,
+                                                   unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long red[4][32];
+  unsigned long long t[4] = {0, 0, 0, 0};
+  for (int p = threadIdx.x; p < P; p += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] += per[(int64_t)p * 4 + q];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    t[q] = warp_sum(t[q]);
+    if (lane_id() == 0) red[q][warp_id()] = t[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    unsigned long long x = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) x += red[threadIdx.x][w];
+    out[threadIdx.x] = x;
+  }
+}
+
+__global__ void __launch_bounds__(QT) k_part_expand(const unsigned long long* __restrict__ ka,
+                                                    const int32_t* __restrict__ ga,
+                                                    const int64_t* __restrict__ offa,
+                                                    const unsigned long long* __restrict__ kb,
+                                                    const int32_t* __restrict__ hb,
+                                                    const int64_t* __restrict__ offb, int ts_bits, int cap,
+                                                    unsigned* __restrict__ C, int64_t ldc) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int wsum[QT / 32];
+  const int TS = 1 << ts_bits, mask = TS - 1;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+  int* cnt = reinterpret_cast<int*>(keys + TS);   // per slot: B tuples, then the bucket cursor
+  int* start = cnt + TS;                          // per slot: bucket start
+  int* bslot = start + TS;                        // per B tuple of the partition: its slot
+  int* bh = bslot + cap;                          // B group codes bucketed by slot
+  for (int i = threadIdx.x; i < TS; i += QT) { keys[i] = ~0ull; cnt[i] = 0; }
+  __syncthreads();
+  const int p = blockIdx.x;
+  const int64_t b0 = offb[p];
+  const int nb = (int)(offb[p + 1] - b0);
+  for (int i = threadIdx.x; i < nb; i += QT) {
+    const int h = tab_insert(keys, mask, ts_bits, __ldcs(kb + b0 + i));
+    bslot[i] = h;
+    atomicAdd(cnt + h, 1);
+  }
+  __syncthreads();
+  // exclusive scan of cnt[0..TS) -> start (each thread a contiguous run of TS / QT slots)
+  {
+    const int per = TS / QT;
+    const int s0 = threadIdx.x * per;
+    int run = 0;
+    for (int q = 0; q < per; ++q) run += cnt[s0 + q];
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane_id() >= o) incl += t;
+    }
+    if (lane_id() == 31) wsum[warp_id()] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < warp_id(); ++w) wbase += wsum[w];
+    int x = wbase + incl - run;
+    for (int q = 0; q < per; ++q) { start[s0 + q] = x; x += cnt[s0 + q]; cnt[s0 + q] = 0; }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += QT) {
+    const int h = bslot[i];
+    bh[start[h] + atomicAdd(cnt + h, 1)] = __ldcs(hb + b0 + i);
+  }
+  __syncthreads();
+  for (int64_t i = offa[p] + threadIdx.x; i < offa[p + 1]; i += QT) {
+    const int h = tab_find(keys, mask, ts_bits, __ldcs(ka + i));
+    if (h < 0) continue;
+    const int n = cnt[h];
+    if (n == 0) continue;
+    unsigned* row = C + (int64_t)__ldcs(ga + i) * ldc;
+    const int e0 = start[h];
+    for (int e = 0; e < n; ++e) atomicAdd(row + bh[e0 + e], 1u);  // RED: no return value used
+  }
+}
+
+__global__ void k_part_max(const int64_t* __restrict__ offa, const int64_t* __restrict__ offb, int P,
+                           unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)max(offa[p + 1] - offa[p], offb[p + 1] - offb[p]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(out, m);
+}
+
+}  // namespace
+
+static int64_t max_chunks(int64_t n, int nseg) { return (n + CH - 1) / CH + nseg; }
+
+size_t hashpart_temp_bytes(int64_t n, int nseg, int bits) {
+  const int64_t cnts = max_chunks(n, nseg) * (1ll << bits);
+  return ((size_t)(nseg + 1) * 8 + 255) / 256 * 256 + ((size_t)cnts * 4 + 255) / 256 * 256 +
+         ((size_t)(cnts + 1) * 8 + 255) / 256 * 256 + scan_temp_bytes(cnts);
+}
+
+cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
+                             const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
+                             int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
+                             int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches) {
+  if (bits < 1 || bits > 7 || n <= 0) return cudaErrorInvalidValue;
+  const int R = 1 << bits;
+  const int64_t chunks = max_chunks(n, nseg);
+  const int64_t cnts = chunks * R;
+  char* t = static_cast<char*>(temp);
+  int64_t* chunk_start = reinterpret_cast<int64_t*>(t);
+  t += ((size_t)(nseg + 1) * 8 + 255) / 256 * 256;
+  int32_t* counts = reinterpret_cast<int32_t*>(t);
+  t += ((size_t)cnts * 4 + 255) / 256 * 256;
+  int64_t* offs = reinterpret_cast<int64_t*>(t);
+  t += ((size_t)(cnts + 1) * 8 + 255) / 256 * 256;
+  PassIO io{};
+  io.raw = raw ? raw->data : nullptr; io.raw_type = raw ? raw->type : 0; io.kmin = kmin; io.g_raw = g_raw;
+  io.k_in = k_in; io.g_in = g_in; io.seg_off = seg_off; io.nseg = nseg; io.shift = shift; io.bits = bits;
+  io.chunk_start = chunk_start; io.counts = counts; io.offs = offs;
+  io.k_out = k_out; io.g_out = g_out; io.seg_out = seg_out;
+  k_chunk_starts<<<1, 32, 0, s>>>(seg_off, nseg, chunk_start);
+  // unused count slots (chunks past the real total) must scan as zero
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cnts * 4, s);
+  if (e != cudaSuccess) return e;
+  k_part_hist<<<(unsigned)chunks, PT, 0, s>>>(io);
+  e = exclusive_scan_i32(counts, offs, cnts, nullptr, t, s, launches);
+  if (e != cudaSuccess) return e;
+  static bool attr = false;
+  constexpr int kStage = CH * 12;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kStage);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_part_scatter<<<(unsigned)chunks, PT, kStage, s>>>(io);
+  const int64_t so = (int64_t)nseg * R + 1;
+  k_seg_out<<<(unsigned)std::min<int64_t>((so + 255) / 256, 1024), 256, 0, s>>>(io);
+  if (launches) *launches += 4;
+  return cudaGetLastError();
+}
+
+static int ts_bits_for(int cap) {
+  int b = 11;
+  while ((1 << b) < 2 * cap) ++b;
+  return b;
+}
+
+cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa, const unsigned long long* kb,
+                              const int64_t* offb, int P, int cap, unsigned long long* out, cudaStream_t s,
+                              int64_t* launches) {
+  const int tb = ts_bits_for(cap);
+  const size_t smem = (size_t)(1 << tb) * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  // per-partition totals in out[4 ..), their sums in out[0..4)
+  k_part_count<<<P, QT, smem, s>>>(ka, offa, kb, offb, tb, out + 4);
+  k_part_sum<<<1, 1024, 0, s>>>(out + 4, P, out);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+size_t part_expand_smem(int cap) { return (size_t)(1 << ts_bits_for(cap)) * 16 + (size_t)cap * 8; }
+
+cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, const int64_t* offa,
+                               const unsigned long long* kb, const int32_t* hb, const int64_t* offb, int P, int cap,
+                               unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches) {
+  const int tb = ts_bits_for(cap);
+  const size_t smem = part_expand_smem(cap);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_part_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  k_part_expand<<<P, QT, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_max(const int64_t* offa, const int64_t* offb, int P, unsigned long long* out, cudaStream_t s,
+                            int64_t* launches) {
+  k_part_max<<<(P + 255) / 256, 256, 0, s>>>(offa, offb, P, out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace tcudb

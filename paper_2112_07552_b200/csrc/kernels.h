@@ -64,9 +64,10 @@ cudaError_t launch_rank_write(const unsigned long long* keys, const uint32_t* va
                               int64_t* launches);
 // One-block gather + bitonic sort + rank write for small hash domains (slot_code may alias code).
 bool small_rank_ok(int64_t count, int64_t cap);
+size_t small_rank_temp_bytes();
 cudaError_t launch_small_rank(const int32_t* code, const unsigned long long* slots, int64_t cap, int64_t count,
-                              long long minv, int32_t* slot_code, long long* dict, int32_t* remap, cudaStream_t s,
-                              int64_t* launches);
+                              long long minv, int32_t* slot_code, long long* dict, int32_t* remap, void* temp,
+                              cudaStream_t s, int64_t* launches);
 // codes[i] = remap[codes[i]] for codes >= 0 (per-tuple codes issued before the rank sort)
 cudaError_t launch_remap_codes(int32_t* codes, int64_t n, const int32_t* remap, cudaStream_t s, int64_t* launches);
 cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const DictView& kd,
@@ -203,6 +204,44 @@ cudaError_t launch_spa_fused(const SpaArgs& a, cudaStream_t s, int64_t* launches
 cudaError_t launch_band_weight_max(const SpaArgs& a, unsigned long long* out, cudaStream_t s, int64_t* launches);
 cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_spa_write(const SpaArgs& a, cudaStream_t s, int64_t* launches);
+
+// gcode[i] = code of grp[i] in the dictionary gd (final codes)
+cudaError_t launch_group_codes(const ColDesc& grp, const DictView& gd, int32_t* gcode, cudaStream_t s,
+                               int64_t* launches);
+
+// ---------------------------------------------------------------- hashpart.cu (a2 + a7, partitioned)
+// Hash-partitioned sparse COUNT for large hash-mode key domains: both tables are
+// radix-partitioned by the key hash so that each partition's key dictionary, per-key
+// counts and B buckets live in one CTA's shared memory.
+struct PartSide {
+  ColDesc key;            // raw join-key column (pass 1 input)
+  const int32_t* gcode;   // group codes of the rows (pass 1 input)
+  unsigned long long* k[2];  // ping-pong koff = key - kmin (u64)
+  int32_t* g[2];             // ping-pong group codes
+};
+size_t hashpart_temp_bytes(int64_t n, int nseg, int bits);
+// One radix pass over nseg segments (segment s = [seg_off[s], seg_off[s+1])): digit =
+// (fmix64(koff) >> shift) & (2^bits - 1); output segment-major, then digit. in_raw: pass 1
+// reads the raw key column and the gcode array instead of (k_in, g_in). seg_out (nseg *
+// 2^bits + 1) receives the new segment offsets.
+cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
+                             const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
+                             int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
+                             int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches);
+size_t part_expand_smem(int cap);
+// per partition: J_p = sum over its keys of cntA*cntB, D_p = #keys on both sides; out has
+// 4 + 4 P entries: totals out[0] (J), out[1] (K = sum D_p), out[2] (A tuples with a matched
+// key), out[3] (distinct B keys); per-partition values after them
+cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa, const unsigned long long* kb,
+                              const int64_t* offb, int P, int cap, unsigned long long* out, cudaStream_t s,
+                              int64_t* launches);
+// per partition: C[g][h] += 1 for every joined pair (u32 cells, row stride ldc)
+cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, const int64_t* offa,
+                               const unsigned long long* kb, const int32_t* hb, const int64_t* offb, int P, int cap,
+                               unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches);
+// largest partition (max over both sides) into *out (zeroed)
+cudaError_t launch_part_max(const int64_t* offa, const int64_t* offb, int P, unsigned long long* out, cudaStream_t s,
+                            int64_t* launches);
 
 // ---------------------------------------------------------------- reduce.cu (§8(f) f2)
 // One side ungrouped (Q3 P:785-823, Q4 P:842-850) or AVG: segmented reductions.

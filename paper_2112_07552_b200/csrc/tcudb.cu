@@ -237,7 +237,8 @@ void dict_finish_group(Arena& ar, Dict& d, int64_t* launches, int32_t* tuple_cod
   }
   if (small_rank_ok(d.count, (int64_t)d.span)) {
     int32_t* remap = ar.get<int32_t>(d.count);
-    CK(launch_small_rank(d.code, d.slots, (int64_t)d.span, d.count, d.minv, d.code, d.dict, remap, s, launches));
+    CK(launch_small_rank(d.code, d.slots, (int64_t)d.span, d.count, d.minv, d.code, d.dict, remap,
+                         ar.get<char>((int64_t)small_rank_temp_bytes()), s, launches));
     if (tuple_codes) CK(launch_remap_codes(tuple_codes, n, remap, s, launches));
     return;
   }
@@ -319,6 +320,138 @@ struct QueryOut {
   void *g = nullptr, *h = nullptr, *agg = nullptr;
 };
 
+// ---------------------------------------------------------------------------
+// Hash-partitioned sparse COUNT (hashpart.cu) for large hash-mode key domains (c5).
+// Returns false (nothing enqueued that matters) when the plan does not apply: the
+// caller then runs the general path. Steps: group dictionaries (a2) -> two radix
+// passes on the key hash per side -> per-partition count (J, K; a4 selector) ->
+// per-partition expand into C (a7) -> compaction (a8).
+bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb_table* B, const ColDesc& ak,
+                    const ColDesc& ag, const ColDesc& bk, const ColDesc& bh, const ColStats* hs, const double* est,
+                    long long kmin, tcudb_result* out, tcudb_stats& S, Timer& tm, int64_t* L, cudaStream_t s,
+                    bool timed) {
+  const int64_t nA = ak.n, nB = bk.n;
+  Dict DG, DH;
+  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
+  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2]);
+  {
+    int64_t* hp = static_cast<int64_t*>(ctx->pinned);
+    int* hov = reinterpret_cast<int*>(hp + 2);
+    hov[0] = hov[1] = 0;
+    CK(cudaMemcpyAsync(hp + 0, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 1, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    if (DG.ovf) CK(cudaMemcpyAsync(hov + 0, DG.ovf, 4, cudaMemcpyDeviceToHost, s));
+    if (DH.ovf) CK(cudaMemcpyAsync(hov + 1, DH.ovf, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hov[0] || hov[1]) return false;
+    DG.count = hp[0];
+    DH.count = hp[1];
+  }
+  const int64_t G = DG.count, H = DH.count, ldc = round_up(H, 4);
+  if ((double)G * (double)ldc * 4.0 > 0.3 * (double)ctx->mem_free0) return false;
+  dict_finish_group(ar, DG, L);
+  dict_finish_group(ar, DH, L);
+  int32_t* gA = ar.get<int32_t>(nA);
+  int32_t* hB = ar.get<int32_t>(nB);
+  CK(launch_group_codes(ag, DG.view(1), gA, s, L));
+  CK(launch_group_codes(bh, DH.view(1), hB, s, L));
+  // partitions: <= ~1 K tuples per side on average, two radix passes of <= 7 bits
+  int pbits = 1;
+  while (pbits < 14 && ((int64_t)1 << pbits) * 1024 < std::max(nA, nB)) ++pbits;
+  const int b1 = (pbits + 1) / 2, b2 = pbits - b1;
+  const int P = 1 << pbits;
+  struct Side { unsigned long long* k[2]; int32_t* g[2]; int64_t* seg1; int64_t* seg2; };
+  Side sd[2];
+  const ColDesc* keys[2] = {&ak, &bk};
+  const int32_t* grp[2] = {gA, hB};
+  const int64_t ns[2] = {nA, nB};
+  int64_t* seg0 = ar.get<int64_t>(4);
+  {
+    int64_t h0[4] = {0, nA, 0, nB};
+    std::memcpy(ctx->pinned, h0, sizeof(h0));
+    CK(cudaMemcpyAsync(seg0, ctx->pinned, sizeof(h0), cudaMemcpyHostToDevice, s));
+  }
+  for (int x = 0; x < 2; ++x) {
+    const int64_t n = ns[x];
+    sd[x].k[0] = ar.get<unsigned long long>(n); sd[x].k[1] = ar.get<unsigned long long>(n);
+    sd[x].g[0] = ar.get<int32_t>(n); sd[x].g[1] = ar.get<int32_t>(n);
+    sd[x].seg1 = ar.get<int64_t>(((int64_t)1 << b1) + 1);
+    sd[x].seg2 = ar.get<int64_t>((int64_t)P + 1);
+    void* t1 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1, b1));
+    CK(launch_part_pass(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
+                        sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L));
+    if (b2) {
+      void* t2 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1 << b1, b2));
+      CK(launch_part_pass(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
+                          sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, s, L));
+    }
+  }
+  const int fin = b2 ? 1 : 0;
+  unsigned long long* d_out = ar.zeros<unsigned long long>(4 + 4 * (int64_t)P);
+  unsigned long long* d_max = ar.zeros<unsigned long long>(1);
+  CK(launch_part_max(sd[0].seg2, sd[1].seg2, P, d_max, s, L));
+  const int64_t cap = (int64_t)*to_pinned<unsigned long long>(ctx, d_max, s);
+  if (cap <= 0 || part_expand_smem((int)std::min<int64_t>(cap, 1 << 20)) > 200 * 1024) return false;
+  CK(launch_part_count(sd[0].k[fin], sd[0].seg2, sd[1].k[fin], sd[1].seg2, P, (int)cap, d_out, s, L));
+  unsigned long long cnt[4];
+  CK(cudaMemcpyAsync(ctx->pinned, d_out, 32, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::memcpy(cnt, ctx->pinned, 32);
+  const unsigned long long J = cnt[0];
+  const int64_t K = (int64_t)cnt[1];
+  tm.mark(&S.ms_encode);
+  // a4 selector with the same cost model as the general path (COUNT)
+  const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), Kp = round_up(std::max<int64_t>(K, 1), 128);
+  const double t_dense = 2.0 * Gp * Hp * Kp / 2.0e15 + ((double)(Gp + Hp) * Kp * 3 + (double)Gp * Hp * 8) / 5.5e12;
+  const double t_sparse = (double)J / 1.2e10 + ((double)G * H * 8 + (double)(nA + nB) * 24) / 5.5e12;
+  if (J == 0 || K == 0) {
+    S.G = G; S.H = H; S.K = K; S.join_pairs = 0; S.path = 1; S.spa_mode = 4;
+    return true;  // empty result (out already zeroed)
+  }
+  if (t_dense <= t_sparse || J >= (1ull << 32)) return false;
+  unsigned* C = ar.zeros<unsigned>(G * ldc);
+  if (timed) cudaEventRecord(ctx->evk[0], s);
+  CK(launch_part_expand(sd[0].k[fin], sd[0].g[fin], sd[0].seg2, sd[1].k[fin], sd[1].g[fin], sd[1].seg2, P, (int)cap,
+                        C, ldc, s, L));
+  if (timed) cudaEventRecord(ctx->evk[1], s);
+  tm.mark(&S.ms_sparse);
+  // a8 compaction of C (u32 counts; codes are ascending ranks -> (g, h) order)
+  CompactArgs ca{};
+  ca.G = G; ca.H = H; ca.nseg = (H + 255) / 256; ca.seg_w = 256;
+  ca.E = C; ca.e_kind = 0; ca.lde = ldc; ca.V = C; ca.v_kind = 0; ca.ldv = ldc;
+  ca.dict_g = DG.dict; ca.dict_h = DH.dict;
+  ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
+  ca.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
+  ca.agg_out = 0;
+  void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
+  int64_t* d_nnz = ar.get<int64_t>(1);
+  CK(launch_compact_count(ca, nullptr, d_nnz, ctmp, s, L));
+  const int64_t nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+  const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
+  const size_t oh = ((size_t)nnz * gb + 255) / 256 * 256;
+  const size_t oa = oh + ((size_t)nnz * hb + 255) / 256 * 256;
+  char* base = static_cast<char*>(result_alloc(ctx, oa + (size_t)nnz * 8, s));
+  ca.out_g = base; ca.out_h = base + oh; ca.out_agg = base + oa;
+  try {
+    CK(launch_compact_write(ca, ctmp, s, L));
+    tm.mark(&S.ms_compact);
+    CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    result_release(ctx, base);
+    throw;
+  }
+  out->n = nnz; out->g = ca.out_g; out->h = ca.out_h; out->agg = ca.out_agg; out->base = base; out->on_host = 0;
+  S.G = G; S.H = H; S.K = K; S.K_union = (int64_t)est[0]; S.key_mode = 1;
+  S.join_pairs = (int64_t)J; S.n_result = nnz; S.path = 1; S.spa_mode = 4;
+  S.density_union = est[0] > 0 ? (double)nA / ((double)G * est[0]) : 0.0;
+  if (timed) {
+    cudaEventElapsedTime(&S.ms_kernel, ctx->evk[0], ctx->evk[1]);
+    // partitioned tuples read (12 B each side) + one 4-byte reduction per joined pair
+    S.kernel_bytes = 12.0 * (double)(nA + nB) + 4.0 * (double)J;
+  }
+  return true;
+}
+
 // internal status: AVG with both sides grouped -> the ABI entry composes SUM and COUNT
 constexpr tcudb_status kComposeAvg = static_cast<tcudb_status>(99);
 
@@ -381,6 +514,24 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       if (hk) est[0] = hll_estimate(hr);
       if (hg) est[1] = hll_estimate(hr + kHllM);
       if (hh) est[2] = hll_estimate(hr + 2 * kHllM);
+    }
+  }
+  {
+    // large hash-mode key domain, COUNT, both sides grouped: the hash-partitioned path
+    const char* no_hp = getenv("TCUDB_NO_HASHPART");
+    const char* force_hp = getenv("TCUDB_FORCE_HASHPART");  // tests: skip the size thresholds
+    const bool big = (est[0] >= (double)(1 << 19) && nA >= (1 << 20) && nB >= (1 << 20)) ||
+                     (force_hp && force_hp[0] == '1');
+    const bool hk = !dict_is_direct(nA + nB, kmin, kmax);
+    if (!is_sum && !absent && hk && big && !(q->flags & TCUDB_FORCE_DENSE) && !(no_hp && no_hp[0] == '1')) {
+      if (hashpart_query(ctx, ar, A, B, ak, ag, bk, bh, hs, est, kmin, out, S, tm, L, s, st != nullptr)) {
+        tm.finish();
+        S.n_launches = (int32_t)(ctx->launches - launches0);
+        S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+        return TCUDB_OK;
+      }
+      tm = Timer(ctx, s, st != nullptr);  // fallback: restart the stage clock
+      tm.mark(nullptr);
     }
   }
   unsigned long long* d_union = ar.zeros<unsigned long long>(1);

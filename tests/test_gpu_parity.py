@@ -503,6 +503,48 @@ def test_fused_compaction_matches(engine, torch_mod, oracle_mod, monkeypatch, ca
         assert np.array_equal(of[k], ou[k])
 
 
+@pytest.mark.parametrize("case", ["c5_64", "c5_16", "zipf", "int32_keys", "few_groups", "disjoint"])
+def test_hash_partitioned_count(engine, torch_mod, oracle_mod, monkeypatch, case):
+    """Hash-partitioned sparse COUNT (hashpart.cu; the default for c5-sized inputs) forced
+    on smaller inputs, and the general path, both exact against the oracle. zipf: skewed
+    keys (the plan may fall back when a partition outgrows shared memory)."""
+    rng = np.random.default_rng(55)
+    if case.startswith("c5"):
+        A, B, agg = datagen.make_config("c5", {"c5_64": 1 / 64, "c5_16": 1 / 16}[case])
+    elif case == "zipf":
+        n = 300000
+        A = datagen.Table(rng.zipf(1.2, n).astype(np.int64) * 7919 + (1 << 40), rng.integers(0, 500, n))
+        B = datagen.Table(rng.zipf(1.2, n).astype(np.int64) * 7919 + (1 << 40), rng.integers(0, 700, n))
+        agg = "count"
+    elif case == "int32_keys":
+        n = 200000
+        A = datagen.Table(rng.integers(-2**31, 2**31 - 1, n).astype(np.int32) // 64, rng.integers(0, 3000, n))
+        B = datagen.Table(rng.integers(-2**31, 2**31 - 1, n).astype(np.int32) // 64, rng.integers(0, 2000, n))
+        agg = "count"
+    elif case == "few_groups":
+        n = 250000
+        keys = rng.integers(0, 2**62, 60000)
+        A = datagen.Table(rng.choice(keys, n), rng.integers(0, 3, n) * 1000003)
+        B = datagen.Table(rng.choice(keys, n), rng.integers(0, 5, n) - 7)
+        agg = "count"
+    else:
+        n = 100000
+        A = datagen.Table(rng.integers(0, 2**40, n), rng.integers(0, 100, n))
+        B = datagen.Table(rng.integers(2**41, 2**42, n), rng.integers(0, 100, n))
+        agg = "count"
+    ref = oracle_mod.join_agg(A, B, agg)
+    monkeypatch.setenv("TCUDB_FORCE_HASHPART", "1")
+    out, st = run(engine, torch_mod, A, B, agg, 0)
+    compare(out, ref, agg)
+    if case in ("c5_64", "c5_16", "int32_keys"):
+        assert st["spa_mode"] == 4
+    monkeypatch.setenv("TCUDB_FORCE_HASHPART", "0")
+    monkeypatch.setenv("TCUDB_NO_HASHPART", "1")
+    out2, st2 = run(engine, torch_mod, A, B, agg, 0)
+    assert st2["spa_mode"] != 4
+    compare(out2, ref, agg)
+
+
 SHARD_SCRIPT = r"""
 import os, sys, numpy as np, torch, torch.distributed as dist
 sys.path.insert(0, os.getcwd())
