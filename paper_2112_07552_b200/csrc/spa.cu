@@ -285,14 +285,24 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
   }
   volatile unsigned long long* state = reinterpret_cast<volatile unsigned long long*>(a.lb_state);
   bool ovf = false;
+  // the next band's ticket is drawn one band ahead (thread 0), so the atomic's latency
+  // overlaps the current band's expansion instead of stalling the whole CTA
+  unsigned long long next_ticket = 0;
+  if (threadIdx.x == 0) next_ticket = atomicAdd(a.ticket, 1ull);
   for (;;) {
     __syncthreads();  // smem clear / previous band finished before the ticket is replaced
-    if (threadIdx.x == 0) s_band = (int64_t)atomicAdd(a.ticket, 1ull);
+    if (threadIdx.x == 0) {
+      s_band = (int64_t)next_ticket;
+      if ((int64_t)next_ticket < a.nbands) next_ticket = atomicAdd(a.ticket, 1ull);
+    }
     __syncthreads();
     const int64_t b = s_band;
     if (b >= a.nbands) break;
     const int64_t g0 = b * a.rows;
     const int nr = (int)min((int64_t)a.rows, a.G - g0);
+    // write pass: this band's row offsets, loaded now and consumed after the expansion
+    int64_t rowoff0 = 0;
+    if (a.row_out && threadIdx.x < nr) rowoff0 = a.row_out[g0 + threadIdx.x];
     spa_expand<(ACC >= 2)>(a, a.goff[b], a.goff[b + 1], g0, [&](int r, int h, int64_t pos, int32_t ai) {
       if constexpr (ACC == 0) {
         const int sh = (h & 1) * 16;
@@ -320,9 +330,9 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
       if (lane == 0) s_rowcnt[r] = c;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && a.row_out) {
+    if (a.row_out) {
       // write pass of the two-pass schedule: offsets from the count pass
-      for (int r = 0; r < nr; ++r) s_rowbase[r] = a.row_out[g0 + r];
+      if (threadIdx.x < nr) s_rowbase[threadIdx.x] = rowoff0;
     } else if (threadIdx.x == 0) {
       int64_t cnt = 0;
       for (int r = 0; r < nr; ++r) cnt += s_rowcnt[r];
