@@ -402,8 +402,8 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   tm.mark(&S.ms_encode);
   // a4 selector with the same cost model as the general path (COUNT)
   const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), Kp = round_up(std::max<int64_t>(K, 1), 128);
-  const double t_dense = 2.0 * Gp * Hp * Kp / 2.0e15 + ((double)(Gp + Hp) * Kp * 3 + (double)Gp * Hp * 8) / 5.5e12;
-  const double t_sparse = (double)J / 1.2e10 + ((double)G * H * 8 + (double)(nA + nB) * 24) / 5.5e12;
+  const double t_dense = 2.0 * Gp * Hp * Kp / 2.0e15 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / 5.5e12;
+  const double t_sparse = (double)J / 5.0e10 + ((double)G * H * 4 + (double)(nA + nB) * 32) / 5.5e12 + 40e-6;
   if (J == 0 || K == 0) {
     S.G = G; S.H = H; S.K = K; S.join_pairs = 0; S.path = 1; S.spa_mode = 4;
     return true;  // empty result (out already zeroed)
@@ -690,15 +690,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double dense_ops = 2.0 * (double)Gp * (double)Hp * (double)Kp;
   // the paper's input-matrix density: nnz(mat(A)) / (|A rows| x |dom(ID)|), ∪ domain
   S.density_union = S.K_union ? (double)nA / ((double)G * (double)S.K_union) : 0.0;
-  const double R_tc = is_float ? 1.0e15 : 2.0e15, BW = 5.5e12, R_sp = 1.2e10;
+  // Cost model (Eq. 3's CT = 2MNK / peak plus the bytes each path moves), calibrated on the
+  // B200 by scripts/selector_sweep.py (profiles/r01_selector_sweep.jsonl, §8(f) f4): the
+  // dense path touches its operand / scratch / C bytes ~3 times (fill, GEMM, compaction);
+  // the sparse path expands ~5e10 joined pairs/s and pays one more host sync (~40 us).
+  const double R_tc = is_float ? 1.0e15 : 2.0e15, BW = 5.5e12, R_sp = 5.0e10, T_sp0 = 40e-6;
   double planes_est = is_sum ? (is_float ? 1.0 : 2.0) : 1.0;
   if (need_exist) planes_est += 1.0;
-  const double t_dense = planes_est * dense_ops / R_tc + ((double)(Gp + Hp) * Kp * esz * 3 + (double)Gp * Hp * 8) / BW;
   const double csz = is_sum ? 8.0 : 4.0;
-  const double t_sparse = (double)J / R_sp + ((double)G * H * csz * 2 + (double)(nA + nB) * 24) / BW;
   const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 3 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
+  const double t_dense = planes_est * dense_ops / R_tc + 3.0 * dense_bytes / BW;
+  const double t_sparse = (double)J / R_sp + sparse_bytes / BW + T_sp0;
   // memory budget: the device's free memory when the context was created (a live
   // cudaMemGetInfo per query costs 0.3 ms to tens of ms of host time)
   const size_t free_b = ctx->mem_free0;
