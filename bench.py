@@ -339,6 +339,23 @@ def main():
         achieved = b / (g_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": "sparse stage", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None}
+    tri = None
+    if args.config == "c3" and not sharded:
+        # c3 also names the triangle query (a9): device-timed on the symmetrised graph
+        import datagen
+        s_np, d_np = datagen.c3_graph_edges()
+        S_, D_ = torch.from_numpy(s_np).to(dev), torch.from_numpy(d_np).to(dev)
+        for _ in range(2):
+            eng.triangle_count(S_, D_)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(5):
+            t_count, t_st = eng.triangle_count(S_, D_, with_stats=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tri = {"triangles": t_count, "ms": e0.elapsed_time(e1) / 5, "edges": int(len(s_np)),
+               "path": "sparse wedge check" if t_st["path"] == 1 else "dense masked GEMM"}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:  # the CPU baseline runs on rank 0 at N=1 only
         import oracle
@@ -364,6 +381,7 @@ def main():
         "stage_ms": {k: st[k] for k in ("ms_stats", "ms_encode", "ms_fill", "ms_gemm", "ms_sparse", "ms_compact")},
         "step_ms": [round(x, 4) for x in step_ms],
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+        **({"triangle_query": tri} if tri else {}),
         "context": PAPER_CONTEXT,
     }
     print(json.dumps(line))

@@ -243,6 +243,13 @@ cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, 
 cudaError_t launch_part_max(const int64_t* offa, const int64_t* offb, int P, unsigned long long* out, cudaStream_t s,
                             int64_t* launches);
 
+// ---------------------------------------------------------------- tri_sparse.cu (a9 sparse, §8(f) f3)
+size_t tri_sparse_temp_bytes(int64_t n, int64_t V);
+size_t tri_sparse_smem(int64_t V);  // bitmap bytes per CTA (V bits); <= 200 KB required
+// *out += number of triangles of the simple undirected graph on the coded edges (cu, cv < V)
+cudaError_t launch_tri_sparse(const int32_t* cu, const int32_t* cv, int64_t n, int64_t V, void* temp,
+                              unsigned long long* out, cudaStream_t s, int64_t* launches);
+
 // ---------------------------------------------------------------- reduce.cu (§8(f) f2)
 // One side ungrouped (Q3 P:785-823, Q4 P:842-850) or AVG: segmented reductions.
 struct SideOut {

@@ -1490,6 +1490,21 @@ tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* s
     int32_t* dummy = ar.zeros<int32_t>(V);
     CK(launch_probe(cs, cd, none, DV.view(), DV.view(), cu, cv, dummy, nullptr, V, s, L));
     const int64_t Vp = round_up(V, 256), Kp = round_up(V, 128);
+    // sparse wedge-check path (tri_sparse.cu) unless the dense product is small: 2·Vp³
+    // tensor operations vs ~m·sqrt(m) bitmap tests
+    const char* tri_env = getenv("TCUDB_TRI_PATH");  // "dense" / "sparse": tests
+    bool tri_sparse = Vp > 8192 && tri_sparse_smem(V) <= 200 * 1024;
+    if (tri_env && !strcmp(tri_env, "dense")) tri_sparse = false;
+    if (tri_env && !strcmp(tri_env, "sparse") && tri_sparse_smem(V) <= 200 * 1024) tri_sparse = true;
+    if (tri_sparse) {
+      unsigned long long* tri = ar.zeros<unsigned long long>(1);
+      CK(launch_tri_sparse(cu, cv, n_edges, V, ar.get<char>((int64_t)tri_sparse_temp_bytes(n_edges, V)), tri, s, L));
+      *triangles_out = (int64_t)*to_pinned<unsigned long long>(ctx, tri, s);
+      S.path = 1;
+      S.n_launches = (int32_t)(ctx->launches - launches0);
+      S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      return TCUDB_OK;
+    }
     uint8_t* adj = ar.zeros<uint8_t>(Vp * Kp);
     CK(launch_fill_sym_pattern(cu, cv, n_edges, adj, Kp, s, L));
     unsigned long long* tri = ar.zeros<unsigned long long>(1);

@@ -275,7 +275,11 @@ def test_dense_equals_sparse_bitwise(engine, torch_mod):
         assert np.array_equal(d[k], s[k])
 
 
-def test_triangles_textbook_and_random(engine, torch_mod, oracle_mod):
+@pytest.mark.parametrize("path", ["dense", "sparse"])
+def test_triangles_textbook_and_random(engine, torch_mod, oracle_mod, monkeypatch, path):
+    """a9 on both paths: the masked 2-hop GEMM (dense) and the oriented wedge check
+    (tri_sparse.cu) — textbook closed forms and a random multigraph with self-loops."""
+    monkeypatch.setenv("TCUDB_TRI_PATH", path)
     torch = torch_mod
     import math
     def tri(edges):
@@ -293,11 +297,31 @@ def test_triangles_textbook_and_random(engine, torch_mod, oracle_mod):
     assert got == oracle_mod.triangles(s, d)
 
 
-def test_c3_triangles_reduced(engine, torch_mod, oracle_mod):
+@pytest.mark.parametrize("path", ["dense", "sparse"])
+def test_c3_triangles_reduced(engine, torch_mod, oracle_mod, monkeypatch, path):
+    monkeypatch.setenv("TCUDB_TRI_PATH", path)
     torch = torch_mod
     s, d = datagen.c3_graph_edges(scale=12)
     got = engine.triangle_count(torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
     assert got == oracle_mod.triangles(s, d)
+
+
+def test_c3_triangles_full_sparse(engine, torch_mod, oracle_mod):
+    """The full c3 graph (R-MAT scale 16): the default (sparse) path vs the oracle, plus a
+    star-heavy graph whose hub exercises the degree orientation."""
+    torch = torch_mod
+    s, d = datagen.c3_graph_edges()
+    got, st = engine.triangle_count(torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(), with_stats=True)
+    assert st["path"] == 1
+    assert got == oracle_mod.triangles(s, d)
+    rng = np.random.default_rng(4)
+    hub = np.zeros(60000, np.int64)
+    leaves = rng.integers(1, 20000, 60000)
+    ring_a = rng.integers(1, 20000, 100000)
+    ring_b = rng.integers(1, 20000, 100000)
+    s2 = np.concatenate([hub, ring_a]); d2 = np.concatenate([leaves, ring_b])
+    got2 = engine.triangle_count(torch.from_numpy(s2).cuda(), torch.from_numpy(d2).cuda())
+    assert got2 == oracle_mod.triangles(s2, d2)
 
 
 # full-size configs in the launch configuration bench.py times (default flags)
