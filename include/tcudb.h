@@ -146,6 +146,24 @@ tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_ta
 tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B,
                                  const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, void* stream);
 
+/* Chain (3-way) join, §3.2 multi-way joins:
+ *
+ *     SELECT A.g, C.h, COUNT(*) | SUM(A.v * B.w * C.x)
+ *     FROM A, B, C WHERE A.k = B.key AND B.group = C.k
+ *     GROUP BY A.g, C.h
+ *
+ * B.key is B's first join attribute (ID_1), B.group its second (ID_2); B is
+ * projected out (the "chain exception"). Evaluated in the paper's join
+ * order A -> B -> C: T = (A ⋈ B) grouped by (A.g, B.ID_2) — the nonzero()
+ * re-encoding of mat(A)·mat(B)ᵀ into tuples, kept on the device — then
+ * T ⋈ C on ID_2 with SUM(T.agg · C.x). agg: COUNT or integer SUM (float values:
+ * E_UNSUPPORTED; the intermediate SUM would need fp64 columns). Result as for
+ * tcudb_join_agg: g has A.group's type, h has C.group's type, agg I64, sorted by
+ * (g, h); groups of A or C may not be absent. Errors as tcudb_join_agg. */
+tcudb_status tcudb_chain_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B,
+                                  const tcudb_table* C, const tcudb_query* q, tcudb_result* out,
+                                  tcudb_stats* stats, void* stream);
+
 /* Triangle count of the simple undirected graph of an edge list (self-loops
  * dropped, duplicates and direction ignored): T = trace(A³)/6 over the
  * symmetrised 0/1 adjacency A, evaluated as the 2-hop GEMM A·A with an epilogue

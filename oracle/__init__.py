@@ -155,6 +155,45 @@ def join_agg(A, B, agg="count", threads: int = 0):
         lib.oracle_free(ctypes.byref(res))
 
 
+def chain_join_agg(A, B, C, agg="count", threads: int = 0):
+    """SELECT A.g, C.h, agg FROM A, B, C WHERE A.k = B.k AND B.g = C.k GROUP BY A.g, C.h.
+
+    PAPER.md §3.2 multi-way joins, in the paper's join order A -> B -> C:
+    (1) A ⋈ B, (2) its nonzero() tuples (A.g, B.ID_2, agg) re-encoded as a table,
+    (3) that table ⋈ C. agg: "count" or "sum" (SUM(A.v * B.w * C.x), integer values).
+    B's "g" column is its second join attribute ID_2."""
+    t = join_agg(A, B, agg, threads)
+    T = {"k": t["h"], "g": t["g"], "v": t["cnt"] if agg == "count" else t["sum"]}
+    C2 = {"k": C["k"], "g": C["g"], "v": C.get("v") if agg == "sum" else None}
+    r = join_agg(T, C2, "sum", threads)
+    return {"g": r["g"], "h": r["h"], "cnt_triples": r["sum"] if agg == "count" else None,
+            "sum": r["sum"], "pairs": r["cnt"]}
+
+
+def chain_nested_loop(A, B, C, agg="count"):
+    """Brute force over all triples (i, j, l) — tiny inputs only."""
+    res = {}
+    av = A.get("v") if agg == "sum" else None
+    bw = B.get("v") if agg == "sum" else None
+    cx = C.get("v") if agg == "sum" else None
+    for i in range(len(A["k"])):
+        for j in range(len(B["k"])):
+            if int(A["k"][i]) != int(B["k"][j]):
+                continue
+            for l in range(len(C["k"])):
+                if int(B["g"][j]) != int(C["k"][l]):
+                    continue
+                key = (int(A["g"][i]), int(C["g"][l]))
+                x = 1
+                if agg == "sum":
+                    x = (int(av[i]) if av is not None else 1) * (int(bw[j]) if bw is not None else 1) * \
+                        (int(cx[l]) if cx is not None else 1)
+                res[key] = res.get(key, 0) + x
+    keys = sorted(res)
+    return {"g": np.array([k[0] for k in keys], np.int64), "h": np.array([k[1] for k in keys], np.int64),
+            "sum": np.array([res[k] for k in keys], np.int64)}
+
+
 def triangles(src, dst, threads: int = 0) -> int:
     """Number of triangles of the simple undirected graph on the edge list."""
     lib = _load()

@@ -25,7 +25,8 @@ COUNT, SUM, AVG = 0, 1, 2
 _AGG = {"count": COUNT, "sum": SUM, "avg": AVG}
 FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE, NO_FP4 = 1, 2, 4, 8, 16, 32
 
-EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_triangle_count", "tcudb_gemm",
+EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_chain_join_agg",
+                  "tcudb_triangle_count", "tcudb_gemm",
                   "tcudb_minmax", "tcudb_partition", "tcudb_result_free", "tcudb_result_free_host",
                   "tcudb_last_error", "tcudb_launch_count", "tcudb_destroy"])
 
@@ -96,6 +97,9 @@ def load(build_if_missing: bool = True):
     lib.tcudb_join_agg.restype = ctypes.c_int
     lib.tcudb_join_agg_host.argtypes = lib.tcudb_join_agg.argtypes
     lib.tcudb_join_agg_host.restype = ctypes.c_int
+    lib.tcudb_chain_join_agg.argtypes = [P, ctypes.POINTER(TableS), ctypes.POINTER(TableS), ctypes.POINTER(TableS),
+                                         ctypes.POINTER(Query), ctypes.POINTER(Result), ctypes.POINTER(Stats), P]
+    lib.tcudb_chain_join_agg.restype = ctypes.c_int
     lib.tcudb_triangle_count.argtypes = [P, ctypes.c_int64, P, P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
                                          ctypes.POINTER(Stats), P]
     lib.tcudb_triangle_count.restype = ctypes.c_int
@@ -312,6 +316,28 @@ class Engine:
                 continue  # ungrouped side: no output column
             dt = np.dtype(_TYPESTR[code])
             out[key] = np.zeros(0, dt) if res.n == 0 else np.asarray(_HostArray(owner, ptr, res.n, dt))
+        return (out, stats.to_dict()) if with_stats else out
+
+    def chain_join_agg(self, A, B, C, agg="count", flags=0, stream=None, with_stats=False):
+        """SELECT A.g, C.h, agg FROM A, B, C WHERE A.k = B.k AND B.g = C.k GROUP BY A.g, C.h
+        (B's "g" column is its second join attribute; agg: "count" or integer "sum")."""
+        torch = self._torch
+        ta, tb, tc = self._table_dev(A), self._table_dev(B), self._table_dev(C)
+        q = Query(_AGG[agg], int(flags))
+        res = Result()
+        stats = Stats()
+        st = self._lib.tcudb_chain_join_agg(self._ctx, ctypes.byref(ta), ctypes.byref(tb), ctypes.byref(tc),
+                                            ctypes.byref(q), ctypes.byref(res), ctypes.byref(stats),
+                                            self._stream(stream))
+        self._check(st)
+        owner = _Owner(self, res)
+        out = {}
+        for key, ptr, code in (("g", res.g, res.g_type), ("h", res.h, res.h_type), ("agg", res.agg, res.agg_type)):
+            if res.n == 0 or not ptr:
+                dt = {I32: torch.int32, I64: torch.int64, F32: torch.float32, F64: torch.float64}[code]
+                out[key] = torch.empty(0, dtype=dt, device=f"cuda:{self.device}")
+            else:
+                out[key] = torch.as_tensor(_DevArray(owner, ptr, res.n, code), device=f"cuda:{self.device}")
         return (out, stats.to_dict()) if with_stats else out
 
     def triangle_count(self, src, dst, stream=None, with_stats=False):

@@ -1456,6 +1456,39 @@ tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcu
   return TCUDB_OK;
 }
 
+tcudb_status tcudb_chain_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B,
+                                  const tcudb_table* C, const tcudb_query* q, tcudb_result* out,
+                                  tcudb_stats* stats, void* stream) {
+  if (!ctx || !out || !A || !B || !C || !q) return TCUDB_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  if (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM) return set_err(ctx, TCUDB_E_UNSUPPORTED, "chain: COUNT or SUM");
+  const bool vals = q->agg == TCUDB_SUM;
+  for (const tcudb_table* t : {A, B, C})
+    if (vals && t->value.data && t->value.type == TCUDB_F32)
+      return set_err(ctx, TCUDB_E_UNSUPPORTED, "chain: float values need an fp64 intermediate");
+  if ((A->n_rows > 0 && !A->group.data) || (B->n_rows > 0 && !B->group.data) || (C->n_rows > 0 && !C->group.data))
+    return set_err(ctx, TCUDB_E_INVALID, "chain: A.g, B.ID_2 and C.h are required");
+  // step 1: T = A ⋈ B grouped by (A.g, B.ID_2), COUNT or SUM(A.v · B.w)
+  tcudb_query q1 = *q;
+  tcudb_result T{};
+  tcudb_status st = tcudb_join_agg(ctx, A, B, &q1, &T, nullptr, stream);
+  if (st != TCUDB_OK) return st;
+  // step 2: T ⋈ C on ID_2, SUM(T.agg · C.x) grouped by (A.g, C.h): the intermediate stays
+  // on the device (nonzero() on the GPU, no host round trip)
+  tcudb_table tT{};
+  tT.n_rows = T.n;
+  tT.key = {T.h, T.h_type};
+  tT.group = {T.g, T.g_type};
+  tT.value = {T.agg, TCUDB_I64};
+  tcudb_table tC = *C;
+  if (!vals) tC.value = {nullptr, 0};
+  tcudb_query q2 = *q;
+  q2.agg = TCUDB_SUM;
+  st = tcudb_join_agg(ctx, &tT, &tC, &q2, out, stats, stream);
+  tcudb_result_free(ctx, &T);
+  return st;
+}
+
 tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* src, const void* dst,
                                   int32_t id_type, int64_t* triangles_out, tcudb_stats* stats, void* stream) {
   if (!ctx || !triangles_out || n_edges < 0 || (n_edges > 0 && (!src || !dst)) || !is_int_type(id_type))

@@ -373,3 +373,36 @@ def test_ungrouped_closed_forms(oracle_mod):
         SB[k] = SB.get(k, 0) + w
     q4 = oracle_mod.join_agg(A, _drop_g(B), "sum")
     assert q4["sum"].tolist() == [sum(SA[k] * SB.get(k, 0) for k in SA)]
+
+
+# ---------------------------------------------------------------- §8(f) f3: chain joins
+def test_chain_join_vs_triple_loop(oracle_mod):
+    """The chain oracle (join order A -> B -> C with the nonzero() re-encoding)
+    equals a brute-force loop over all triples (COUNT and integer SUM, duplicates,
+    negatives, empty and disjoint inputs)."""
+    rng = np.random.default_rng(31)
+    for _ in range(150):
+        A, B = datagen.random_tiny(rng, n_max=24, k_max=8, g_max=4, vkind="int", vmin=-4, vmax=4)
+        C, _ = datagen.random_tiny(rng, n_max=24, k_max=8, g_max=4, vkind="int", vmin=-4, vmax=4)
+        # B's second attribute joins C's key: draw it from C's key values (and some misses)
+        B = dict(B, g=rng.choice(np.concatenate([C["k"], [999]]), len(B["k"])) if len(C["k"]) else B["g"])
+        for agg in ("count", "sum"):
+            got = oracle_mod.chain_join_agg(A, B, C, agg)
+            ref = oracle_mod.chain_nested_loop(A, B, C, agg)
+            assert np.array_equal(got["g"], ref["g"]) and np.array_equal(got["h"], ref["h"])
+            assert np.array_equal(got["sum"], ref["sum"])
+
+
+def test_chain_three_hop_complete_graph(oracle_mod):
+    """3-hop walks on K_n: A^3 = (n^2 - 3n + 3) off the diagonal, (n-1)(n-2) on it
+    (A = J - I, A^2 = (n-2)A + (n-1)I)."""
+    n = 9
+    src, dst = zip(*[(i, j) for i in range(n) for j in range(n) if i != j])
+    src, dst = np.array(src), np.array(dst)
+    E1 = datagen.Table(dst, src)   # A: k = dst (the walk's next vertex), g = src
+    E2 = datagen.Table(src, dst)   # B: k = src, ID_2 = dst
+    E3 = datagen.Table(src, dst)   # C: k = src, h = dst
+    r = oracle_mod.chain_join_agg(E1, E2, E3, "count")
+    for g, h, c in zip(r["g"], r["h"], r["sum"]):
+        assert c == ((n - 1) * (n - 2) if g == h else n * n - 3 * n + 3)
+    assert len(r["g"]) == n * n
