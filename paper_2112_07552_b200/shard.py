@@ -55,9 +55,14 @@ def sharded_join_agg(eng, A, B, agg="count", with_stats=False, group=None):
     of device tensors); returns the full result on every rank."""
     import torch
     import torch.distributed as dist
+    if A.get("g") is None or B.get("g") is None:
+        # the row shards are A.g ranges: an ungrouped side (Q3 / Q4) would need a cross-rank
+        # reduction of partial groups, which this sharding does not do
+        raise NotImplementedError("sharded_join_agg needs both group columns (Q3/Q4 run on one GPU)")
     ws = dist.get_world_size(group)
     dev = A["k"].device
-    # 1. global A.g range
+    # 1. global A.g range (every group (g, h) lives on exactly one rank, so COUNT, SUM
+    #    and AVG are all complete locally)
     mn, mx = eng.minmax(A["g"])
     t = torch.tensor([mn, mx], dtype=torch.int64, device=dev)
     lo, hi = t[:1].clone(), t[1:].clone()
