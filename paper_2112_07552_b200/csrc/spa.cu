@@ -55,10 +55,13 @@ __device__ __forceinline__ int64_t warp_find(const int64_t* __restrict__ off, in
 // Calls f(row_in_band, h, bucket_pos, a_index) for every update of the CTA's band of
 // rows [g0, g0 + rows) (active tuples are grouped by band: goff[band]).
 // The band's update range is split evenly over the CTA's warps; each warp then works
-// alone (no CTA barriers): a window of 32 consecutive active tuples sits one per lane,
-// and for 32 consecutive updates the owning tuple of update base + p is
-//   (last tuple starting <= base) + #(tuple starts in (base, base + p]),
-// from one ballot and one OR-reduction of the window's start bits.
+// alone (no CTA barriers) on windows of 32 consecutive active tuples, one per lane, each
+// clamped to the warp's update range:
+//   long tuples (>= 32 updates in range): the warp walks the tuple's bucket together,
+//     32 consecutive bucket entries per step (coalesced, no per-update mapping);
+//   short tuples: their updates are numbered by a warp prefix sum, and update j + lane is
+//     located by a 5-step search over the lanes' prefixes.
+// (c3's 2-hop tuples average ~420 updates, so nearly all updates take the first form.)
 template <bool NEED_A, class F>
 __device__ __forceinline__ void spa_expand(const SpaArgs& a, int64_t t_begin, int64_t t_end, int64_t g0, F f) {
   const int lane = lane_id(), wid = warp_id(), nw = (int)(blockDim.x >> 5);
@@ -77,29 +80,60 @@ __device__ __forceinline__ void spa_expand(const SpaArgs& a, int64_t t_begin, in
     const int gr = valid ? a.act_g[tl] - (int)g0 : 0;
     const int ai = (NEED_A && valid) ? a.act_a[tl] : 0;
     const int64_t wend = min(uend, t + 32 < t_end ? a.act_off[t + 32] : U1);
-    for (; u < wend; u += 128) {
-      int64_t pp[4];
-      int rr[4], aa[4], hh[4];
-      bool ok[4];
+    // this lane's tuple, clamped to [u, wend)
+    int64_t onext = shfl64(o, (lane + 1) & 31);
+    if (lane == 31) onext = wend;
+    const int64_t lo = max(o, u), hi = min(onext, wend);
+    const int len = (valid && hi > lo) ? (int)(hi - lo) : 0;
+    // long tuples: the whole warp walks one bucket range at a time
+    unsigned lm = __ballot_sync(0xffffffffu, len >= 32);
+    while (lm) {
+      const int l = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int64_t xlo = shfl64(lo, l), xhi = shfl64(hi, l);
+      const int64_t delta = shfl64(b, l) - shfl64(o, l);  // bucket pos = update index + delta
+      const int r = __shfl_sync(0xffffffffu, gr, l);
+      const int aval = NEED_A ? __shfl_sync(0xffffffffu, ai, l) : 0;
+      for (int64_t x0 = xlo; x0 < xhi; x0 += 128) {
+        int hh[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t base = u + 32 * j;  // warp-uniform
-        ok[j] = base + lane < wend;
-        const unsigned le = __ballot_sync(0xffffffffu, o <= base);
-        const int l0 = 31 - __clz(le);
-        const int64_t d = o - base;
-        const unsigned st = __reduce_or_sync(0xffffffffu, (d > 0 && d < 32) ? (1u << (int)d) : 0u);
-        const int l = (l0 + __popc(st & ((2u << lane) - 1u))) & 31;
-        const int64_t ol = shfl64(o, l), bl = shfl64(b, l);
-        rr[j] = __shfl_sync(0xffffffffu, gr, l);
-        aa[j] = NEED_A ? __shfl_sync(0xffffffffu, ai, l) : 0;
-        pp[j] = bl + (base + lane - ol);
+        for (int j = 0; j < 4; ++j) {
+          const int64_t x = x0 + 32 * j + lane;
+          hh[j] = x < xhi ? __ldg(a.b_h + x + delta) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t x = x0 + 32 * j + lane;
+          if (x < xhi) f(r, hh[j], x + delta, aval);
+        }
       }
+    }
+    // short tuples: prefix-numbered updates, 32 per step
+    const int slen = len < 32 ? len : 0;
+    int incl = slen;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) hh[j] = ok[j] ? __ldg(a.b_h + pp[j]) : 0;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int sp = incl - slen;
+    const int S = __shfl_sync(0xffffffffu, incl, 31);
+    for (int j = 0; j < S; j += 32) {
+      const int k = j + lane;
+      int l = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (ok[j]) f(rr[j], hh[j], pp[j], aa[j]);
+      for (int step = 16; step > 0; step >>= 1) {
+        const int sps = __shfl_sync(0xffffffffu, sp, l + step);
+        if (sps <= k) l += step;
+      }
+      const int64_t xl = shfl64(lo, l), dl = shfl64(b, l) - shfl64(o, l);
+      const int spl = __shfl_sync(0xffffffffu, sp, l);
+      const int r = __shfl_sync(0xffffffffu, gr, l);
+      const int aval = NEED_A ? __shfl_sync(0xffffffffu, ai, l) : 0;
+      if (k < S) {
+        const int64_t pos = xl + (k - spl) + dl;
+        f(r, __ldg(a.b_h + pos), pos, aval);
+      }
     }
     u = wend;
     t += 32;
