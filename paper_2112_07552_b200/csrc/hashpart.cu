@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
   extern __shared__ __align__(16) uint8_t stage_raw[];
   unsigned long long* sk = reinterpret_cast<unsigned long long*>(stage_raw);  // [CH]
   int32_t* sg = reinterpret_cast<int32_t*>(sk + CH);                          // [CH]
+  uint8_t* sd = reinterpret_cast<uint8_t*>(sg + CH);                          // [CH] digit of each entry
   __shared__ int cnt[kMaxDigits], lstart[kMaxDigits];
   __shared__ int64_t gpos[kMaxDigits];
   const int64_t c = blockIdx.x;
@@ -162,16 +163,12 @@ __global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
       const int p = lstart[d[u]] + r[u];
       sk[p] = k[u];
       sg[p] = g[u];
+      sd[p] = (uint8_t)d[u];
     }
   __syncthreads();
   const int total = (int)(hi - lo);
   for (int p = threadIdx.x; p < total; p += PT) {
-    // digit of staged entry p: the last digit whose local start is <= p (binary search)
-    int a = 0, b = R - 1;
-    while (a < b) {
-      const int m = (a + b + 1) >> 1;
-      if (lstart[m] <= p) a = m; else b = m - 1;
-    }
+    const int a = sd[p];
     const int64_t o = gpos[a] + (p - lstart[a]);
     io.k_out[o] = sk[p];
     io.g_out[o] = sg[p];
@@ -393,7 +390,7 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   e = exclusive_scan_i32(counts, offs, cnts, nullptr, t, s, launches);
   if (e != cudaSuccess) return e;
   static bool attr = false;
-  constexpr int kStage = CH * 12;
+  constexpr int kStage = CH * 13;
   if (!attr) {
     e = cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kStage);
     if (e != cudaSuccess) return e;
