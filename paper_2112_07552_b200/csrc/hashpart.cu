@@ -403,9 +403,12 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   return cudaGetLastError();
 }
 
+// table slots: the next power of two >= 1.5 x the largest partition (load <= 2/3 for
+// linear probing), at least 2 K; smaller tables = more CTAs per SM for these latency-bound
+// per-partition kernels
 static int ts_bits_for(int cap) {
   int b = 11;
-  while ((1 << b) < 2 * cap) ++b;
+  while ((1 << b) < cap + cap / 2) ++b;
   return b;
 }
 
