@@ -189,7 +189,8 @@ __global__ void k_seg_out(const PassIO io) {
 }
 
 // ---- per-partition kernels: open-addressing table of TS slots in shared memory
-constexpr int QT = 512;
+constexpr int QT = 256;   // count kernel threads
+constexpr int QTE = 512;  // expand kernel threads
 
 TCUDB_DEV int slot_of(unsigned long long k, int ts_bits) {
   return (int)((k * 0x9E3779B97F4A7C15ull) >> (64 - ts_bits));
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(1024) k_part_sum(const unsigned long long* __r
   }
 }
 
-__global__ void __launch_bounds__(QT) k_part_expand(const unsigned long long* __restrict__ ka,
+__global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* __restrict__ ka,
                                                     const int32_t* __restrict__ ga,
                                                     const int64_t* __restrict__ offa,
                                                     const unsigned long long* __restrict__ kb,
@@ -288,27 +289,27 @@ __global__ void __launch_bounds__(QT) k_part_expand(const unsigned long long* __
                                                     const int64_t* __restrict__ offb, int ts_bits, int cap,
                                                     unsigned* __restrict__ C, int64_t ldc) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ int wsum[QT / 32];
+  __shared__ int wsum[QTE / 32];
   const int TS = 1 << ts_bits, mask = TS - 1;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
   int* cnt = reinterpret_cast<int*>(keys + TS);   // per slot: B tuples, then the bucket cursor
   int* start = cnt + TS;                          // per slot: bucket start
   int* bslot = start + TS;                        // per B tuple of the partition: its slot
   int* bh = bslot + cap;                          // B group codes bucketed by slot
-  for (int i = threadIdx.x; i < TS; i += QT) { keys[i] = ~0ull; cnt[i] = 0; }
+  for (int i = threadIdx.x; i < TS; i += QTE) { keys[i] = ~0ull; cnt[i] = 0; }
   __syncthreads();
   const int p = blockIdx.x;
   const int64_t b0 = offb[p];
   const int nb = (int)(offb[p + 1] - b0);
-  for (int i = threadIdx.x; i < nb; i += QT) {
+  for (int i = threadIdx.x; i < nb; i += QTE) {
     const int h = tab_insert(keys, mask, ts_bits, __ldcs(kb + b0 + i));
     bslot[i] = h;
     atomicAdd(cnt + h, 1);
   }
   __syncthreads();
-  // exclusive scan of cnt[0..TS) -> start (each thread a contiguous run of TS / QT slots)
+  // exclusive scan of cnt[0..TS) -> start (each thread a contiguous run of TS / QTE slots)
   {
-    const int per = TS / QT;
+    const int per = TS / QTE;
     const int s0 = threadIdx.x * per;
     int run = 0;
     for (int q = 0; q < per; ++q) run += cnt[s0 + q];
@@ -326,12 +327,12 @@ __global__ void __launch_bounds__(QT) k_part_expand(const unsigned long long* __
     for (int q = 0; q < per; ++q) { start[s0 + q] = x; x += cnt[s0 + q]; cnt[s0 + q] = 0; }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nb; i += QT) {
+  for (int i = threadIdx.x; i < nb; i += QTE) {
     const int h = bslot[i];
     bh[start[h] + atomicAdd(cnt + h, 1)] = __ldcs(hb + b0 + i);
   }
   __syncthreads();
-  for (int64_t i = offa[p] + threadIdx.x; i < offa[p + 1]; i += QT) {
+  for (int64_t i = offa[p] + threadIdx.x; i < offa[p + 1]; i += QTE) {
     const int h = tab_find(keys, mask, ts_bits, __ldcs(ka + i));
     if (h < 0) continue;
     const int n = cnt[h];
@@ -443,7 +444,7 @@ cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, 
     attr = true;
   }
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  k_part_expand<<<P, QT, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc);
+  k_part_expand<<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
