@@ -55,13 +55,65 @@ __device__ __forceinline__ void col_stats_finish(ColStats* s, long long mn, long
   }
 }
 
+// HyperLogLog register update (see k_hll): the same hash for int32 and int64 values
+TCUDB_DEV void hll_add(unsigned* s_reg, long long x) {
+  const unsigned long long h = fmix64((unsigned long long)x * 0x9E3779B97F4A7C15ull + 1);
+  const unsigned idx = (unsigned)(h >> (64 - kHllP));
+  const unsigned long long w = h << kHllP;
+  const unsigned rho = w ? (unsigned)__clzll(w) + 1u : (unsigned)(64 - kHllP + 1);
+  if (rho > s_reg[idx]) atomicMax(&s_reg[idx], rho);  // most updates stop at the read
+}
+
+// Sketch gate: 4,096 evenly spaced samples per int column (columns 0..3); a column is
+// sketched in the statistics pass iff its sampled span already exceeds the direct-offset
+// limit (max(4n, 65536): it will be a hash-mode domain). gate[c] = 1 / 0 (read back with
+// the statistics; a hash domain whose samples missed its span falls back to k_hll).
+__global__ void k_sketch_gate(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, int* __restrict__ gate) {
+  const ColDesc c = blockIdx.x == 0 ? c0 : blockIdx.x == 1 ? c1 : blockIdx.x == 2 ? c2 : c3;
+  __shared__ long long smn[32], smx[32];
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  if (c.data && c.n > 0)
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
+      const long long x = ld_int(c.data, c.type, (int64_t)((__int128)c.n * i / 4096));
+      mn = min(mn, x); mx = max(mx, x);
+    }
+  mn = warp_min_ll(mn); mx = warp_max_ll(mx);
+  if (lane_id() == 0) { smn[warp_id()] = mn; smx[warp_id()] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x / 32); ++w) { mn = min(mn, smn[w]); mx = max(mx, smx[w]); }
+    // the key domain spans both key columns: n of the pair
+    const int64_t n = blockIdx.x <= 1 ? c0.n + c1.n : c.n;
+    const unsigned long long span = (unsigned long long)mx - (unsigned long long)mn;
+    gate[blockIdx.x] = (mx >= mn && span + 1 > (unsigned long long)max((int64_t)4 * n, (int64_t)65536)) ? 1 : 0;
+  }
+}
+
 // blockIdx.y = column id. Integer columns: min / max (int64). Float columns:
-// min / max / min |x| (ordered-int encodings of fp32).
+// min / max / min |x| (ordered-int encodings of fp32). HLL: the #distinct sketches of the
+// key columns (0, 1 -> one union sketch), A.g (2) and B.h (3) are updated in the same pass
+// (sketch regs[3][kHllM], zeroed by the caller) — the #distinct metadata of P:1005-1008.
+template <bool HLL>
 __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColDesc c4, ColDesc c5,
-                            ColStats* __restrict__ st) {
+                            ColStats* __restrict__ st, unsigned* __restrict__ hll, const int* __restrict__ gate) {
+  __shared__ unsigned s_reg[HLL ? kHllM : 1];
   ColDesc c = blockIdx.y == 0 ? c0 : blockIdx.y == 1 ? c1 : blockIdx.y == 2 ? c2 : blockIdx.y == 3 ? c3
              : blockIdx.y == 4 ? c4 : c5;
   if (!c.data || c.n <= 0) return;
+  // key columns 0/1 share the union sketch: sketched if either sample says hash mode
+  const bool sk = HLL && blockIdx.y < 4 &&
+                  (blockIdx.y <= 1 ? (gate[0] | gate[1]) != 0 : gate[blockIdx.y] != 0);
+  if (sk) {
+    for (int i = threadIdx.x; i < kHllM; i += T) s_reg[i] = 0;
+    __syncthreads();
+  }
+  unsigned* gsk = sk ? hll + (blockIdx.y <= 1 ? 0 : (blockIdx.y - 1)) * kHllM : nullptr;
+  auto flush = [&]() {
+    if (!sk) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHllM; i += T)
+      if (s_reg[i]) atomicMax(gsk + i, s_reg[i]);
+  };
   ColStats* s = st + blockIdx.y;
   const int64_t stride = (int64_t)gridDim.x * T;
   const int64_t gtid = (int64_t)blockIdx.x * T + threadIdx.x;
@@ -100,6 +152,7 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     auto take = [&](int x) {
       mn = min(mn, x); mx = max(mx, x);
       mabs = min(mabs, x < 0 ? 0u - (unsigned)x : (unsigned)x);
+      if (sk) hll_add(s_reg, (long long)x);
     };
     for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
       int4 x[4];
@@ -109,6 +162,7 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
       for (int u = 0; u < 4; ++u) { take(x[u].x); take(x[u].y); take(x[u].z); take(x[u].w); }
     }
     for (int64_t i = n4 * 4 + gtid; i < c.n; i += stride) take(__ldcs(p + i));
+    flush();
     col_stats_finish(s, (long long)mn, (long long)mx, (long long)mabs, 0);
     return;
   }
@@ -126,8 +180,10 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
       mn = min(mn, x[u]); mx = max(mx, x[u]);
       const long long a = x[u] < 0 ? (x[u] == LLONG_MIN ? LLONG_MAX : -x[u]) : x[u];
       mabs = min(mabs, a);
+      if (sk) hll_add(s_reg, x[u]);
     }
   }
+  flush();
   col_stats_finish(s, mn, mx, mabs, 0);
 }
 
@@ -765,12 +821,20 @@ inline int grid_for(int64_t n, int per_block = T * 4) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, int64_t* launches) {
+cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, int64_t* launches, unsigned* hll,
+                             int* gate) {
   k_init_stats<<<1, 32, 0, s>>>(st, 6);
   int64_t nmax = 1;
   for (int i = 0; i < 6; ++i) if (cols[i].data && cols[i].n > nmax) nmax = cols[i].n;
   dim3 grid((unsigned)std::min<int64_t>(2 * kNumSMs, (nmax + T * 16 - 1) / (T * 16)), 6);
-  k_col_stats<<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st);
+  if (hll) {
+    k_sketch_gate<<<4, 256, 0, s>>>(cols[0], cols[1], cols[2], cols[3], gate);
+    k_col_stats<true><<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st, hll, gate);
+    if (launches) ++*launches;
+  } else {
+    k_col_stats<false><<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st, nullptr,
+                                          nullptr);
+  }
   if (launches) *launches += 2;
   return cudaGetLastError();
 }

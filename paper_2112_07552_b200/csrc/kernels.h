@@ -41,7 +41,11 @@ struct DictView {
 constexpr int kHllP = 13, kHllM = 1 << kHllP;  // HyperLogLog registers per sketch
 // max-merge the sketch of one int column into regs[kHllM] (regs zeroed by the caller)
 cudaError_t launch_hll(const ColDesc& c, unsigned* regs, cudaStream_t s, int64_t* launches);
-cudaError_t launch_col_stats(const ColDesc* cols6, ColStats* st, cudaStream_t s, int64_t* launches);
+// hll (optional, 3 x kHllM zeroed registers): #distinct sketches of the key columns (union),
+// A.g and B.h, updated in the same pass for the columns whose 4 K samples already span more
+// than a direct-offset dictionary allows; gate[4] (device) records which were sketched
+cudaError_t launch_col_stats(const ColDesc* cols6, ColStats* st, cudaStream_t s, int64_t* launches,
+                             unsigned* hll = nullptr, int* gate = nullptr);
 cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags, int64_t span, cudaStream_t s,
                                int64_t* launches);
 // Open-addressing insert of (x - minv); *overflow = 1 if the table is full; row_slot

@@ -483,11 +483,23 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   // ---------------- a1: statistics
   ColDesc cols[6] = {ak, bk, ag, bh, av, bw};
   ColStats* dstats = ar.get<ColStats>(6);
-  CK(launch_col_stats(cols, dstats, s, L));
+  // #distinct sketches (HyperLogLog) ride along with the statistics pass on large inputs;
+  // both come back in the same device->host read
+  constexpr int64_t kSketchMin = 1 << 20;
+  unsigned* hll_regs = (nA + nB >= kSketchMin) ? ar.zeros<unsigned>(3 * kHllM) : nullptr;
+  int* d_gate = hll_regs ? ar.zeros<int>(4) : nullptr;
+  CK(launch_col_stats(cols, dstats, s, L, hll_regs, d_gate));
   CK(cudaMemcpyAsync(ctx->pinned, dstats, sizeof(ColStats) * 6, cudaMemcpyDeviceToHost, s));
+  int* h_gate = reinterpret_cast<int*>(static_cast<char*>(ctx->pinned) + sizeof(ColStats) * 6);
+  if (hll_regs) {
+    CK(cudaMemcpyAsync(h_gate, d_gate, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->pinned_big, hll_regs, sizeof(unsigned) * 3 * kHllM, cudaMemcpyDeviceToHost, s));
+  }
   CK(cudaStreamSynchronize(s));
   ColStats hs[6];
   std::memcpy(hs, ctx->pinned, sizeof(hs));
+  int gate[4] = {0, 0, 0, 0};
+  if (hll_regs) std::memcpy(gate, h_gate, sizeof(gate));
   tm.mark(&S.ms_stats);
   // float values: reject non-finite
   for (int c = 4; c < 6; ++c)
@@ -497,24 +509,24 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const long long kmin = std::min(hs[0].mn, hs[1].mn), kmax = std::max(hs[0].mx, hs[1].mx);
   // #distinct metadata for the hash-mode domains: HyperLogLog sketches
   double est[3] = {0, 0, 0};
-  {
-    // (small inputs size their tables by the tuple count: the sketch pass would cost more)
-    constexpr int64_t kSketchMin = 1 << 20;
-    const bool hk = nA + nB >= kSketchMin && !dict_is_direct(nA + nB, kmin, kmax);
+  if (hll_regs) {
+    // (small inputs size their tables by the tuple count: no sketches)
+    const bool hk = !dict_is_direct(nA + nB, kmin, kmax);
     const bool hg = nA >= kSketchMin && !dict_is_direct(nA, hs[2].mn, hs[2].mx);
     const bool hh = nB >= kSketchMin && !dict_is_direct(nB, hs[3].mn, hs[3].mx);
-    if (hk || hg || hh) {
-      unsigned* regs = ar.zeros<unsigned>(3 * kHllM);
-      if (hk) { CK(launch_hll(ak, regs, s, L)); CK(launch_hll(bk, regs, s, L)); }  // union sketch
-      if (hg) CK(launch_hll(ag, regs + kHllM, s, L));
-      if (hh) CK(launch_hll(bh, regs + 2 * kHllM, s, L));
-      CK(cudaMemcpyAsync(ctx->pinned_big, regs, sizeof(unsigned) * 3 * kHllM, cudaMemcpyDeviceToHost, s));
+    const bool have[3] = {(gate[0] | gate[1]) != 0, gate[2] != 0, gate[3] != 0};
+    // a hash domain whose samples missed its span was not sketched in the stats pass
+    if ((hk && !have[0]) || (hg && !have[1]) || (hh && !have[2])) {
+      if (hk && !have[0]) { CK(launch_hll(ak, hll_regs, s, L)); CK(launch_hll(bk, hll_regs, s, L)); }
+      if (hg && !have[1]) CK(launch_hll(ag, hll_regs + kHllM, s, L));
+      if (hh && !have[2]) CK(launch_hll(bh, hll_regs + 2 * kHllM, s, L));
+      CK(cudaMemcpyAsync(ctx->pinned_big, hll_regs, sizeof(unsigned) * 3 * kHllM, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      const unsigned* hr = static_cast<const unsigned*>(ctx->pinned_big);
-      if (hk) est[0] = hll_estimate(hr);
-      if (hg) est[1] = hll_estimate(hr + kHllM);
-      if (hh) est[2] = hll_estimate(hr + 2 * kHllM);
     }
+    const unsigned* hr = static_cast<const unsigned*>(ctx->pinned_big);
+    if (hk) est[0] = hll_estimate(hr);
+    if (hg) est[1] = hll_estimate(hr + kHllM);
+    if (hh) est[2] = hll_estimate(hr + 2 * kHllM);
   }
   {
     // large hash-mode key domain, COUNT, both sides grouped: the hash-partitioned path
