@@ -409,8 +409,10 @@ __device__ __forceinline__ uint16_t bf16_bits(float x) {
 __device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
 
 // fp32 scratch -> bf16 hi (and optionally lo) segments; 8 cells per thread step.
+// hi = bf16(x) (RNE), lo = bf16(x - hi); hi goes to every K segment in hi_mask, lo to every
+// segment in lo_mask (segment i = columns [i·ld, (i+1)·ld) of the operand row)
 __global__ void k_pack_bf16(const float* __restrict__ scr, int64_t rows, int64_t ld, uint16_t* __restrict__ op,
-                            int64_t ld_op, int seg_hi, int seg_lo, FillStats* __restrict__ fs) {
+                            int64_t ld_op, int hi_mask, int lo_mask, FillStats* __restrict__ fs) {
   const int64_t per_row = ld / 8;
   const int64_t total = rows * per_row;
   const int64_t stride = (int64_t)gridDim.x * T;
@@ -432,8 +434,13 @@ __global__ void k_pack_bf16(const float* __restrict__ scr, int64_t rows, int64_t
       lo[j] = (uint32_t)bf16_bits(r0) | ((uint32_t)bf16_bits(r1) << 16);
     }
     uint16_t* row = op + r * ld_op;
-    *reinterpret_cast<uint4*>(row + (int64_t)seg_hi * ld + c8) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    if (seg_lo >= 0) *reinterpret_cast<uint4*>(row + (int64_t)seg_lo * ld + c8) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+#pragma unroll
+    for (int sg = 0; sg < 4; ++sg) {
+      if (hi_mask & (1 << sg))
+        *reinterpret_cast<uint4*>(row + (int64_t)sg * ld + c8) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      if (lo_mask & (1 << sg))
+        *reinterpret_cast<uint4*>(row + (int64_t)sg * ld + c8) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
   }
   inexact = __any_sync(0xffffffffu, inexact);
   nnz = warp_sum(nnz);
@@ -599,10 +606,10 @@ cudaError_t launch_pack_planes(const long long* scr, int64_t count, int planes, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int seg_hi,
-                             int seg_lo, FillStats* fs, cudaStream_t s, int64_t* launches) {
+cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int hi_mask,
+                             int lo_mask, FillStats* fs, cudaStream_t s, int64_t* launches) {
   if (rows <= 0) return cudaSuccess;
-  k_pack_bf16<<<grid_for(rows * (ld / 8), T * 4), T, 0, s>>>(scr, rows, ld, op, ld_op, seg_hi, seg_lo, fs);
+  k_pack_bf16<<<grid_for(rows * (ld / 8), T * 4), T, 0, s>>>(scr, rows, ld, op, ld_op, hi_mask, lo_mask, fs);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -136,10 +136,11 @@ cudaError_t launch_scratch_stats_i64(const long long* scr, int64_t count, FillSt
 // digits 0..P-2 are u8, the top digit is s8 when top_signed, else u8.
 cudaError_t launch_pack_planes(const long long* scr, int64_t count, int planes, int top_signed, uint8_t* op,
                                int64_t plane_stride, cudaStream_t s, int64_t* launches);
-// fp32 scratch [rows][ld] -> bf16 hi into op[row][seg_hi*ld + k], lo = bf16(x - hi) into
-// op[row][seg_lo*ld + k] (row stride ld_op elements); counts inexact cells.
-cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int seg_hi,
-                             int seg_lo, FillStats* fs, cudaStream_t s, int64_t* launches);
+// fp32 scratch [rows][ld] -> bf16 hi into op[row][i*ld + k] for every segment i in hi_mask,
+// lo = bf16(x - hi) into the segments in lo_mask (row stride ld_op elements); counts
+// inexact cells.
+cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int hi_mask,
+                             int lo_mask, FillStats* fs, cudaStream_t s, int64_t* launches);
 
 // ---------------------------------------------------------------- sparse.cu (a7)
 cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const ColDesc& w, int64_t n,

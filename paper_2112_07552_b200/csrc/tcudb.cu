@@ -710,7 +710,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   double planes_est = is_sum ? (is_float ? 1.0 : 2.0) : 1.0;
   if (need_exist) planes_est += 1.0;
   const double csz = is_sum ? 8.0 : 4.0;
-  const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 3 : (is_sum ? 8 : 1)) +
+  const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 4 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
   const double t_dense = planes_est * dense_ops / R_tc + 3.0 * dense_bytes / BW;
@@ -837,7 +837,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     bool bf16_direct = false;
     uint16_t *fA = nullptr, *fB = nullptr;
     if (is_float) {
-      ldop = 3 * Kp;
+      ldop = 4 * Kp;
       fA = ar.get<uint16_t>(Gp * ldop);
       fB = ar.get<uint16_t>(Hp * ldop);
       if (nA <= cellsA && nB <= cellsB) {
@@ -880,17 +880,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       float* scrB = ar.zeros<float>(cellsB);
       CK(launch_fill_f32(kA, gA, av, nA, scrA, Kp, s, L));
       CK(launch_fill_f32(kB, hB, bw, nB, scrB, Kp, s, L));
-      CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 0, -1, fs + 0, s, L));
-      CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 0, -1, fs + 1, s, L));
+      CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 1, 0, fs + 0, s, L));
+      CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 1, 0, fs + 1, s, L));
       CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       FillStats hf[2];
       std::memcpy(hf, ctx->pinned, sizeof(hf));
       if (hf[0].inexact || hf[1].inexact) {
         // 3-product split along K: A' = [hi | hi | lo], B' = [hi | lo | hi]
-        CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 1, 2, fs + 0, s, L));
-        CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 2, 1, fs + 1, s, L));
-        k_len = 3 * Kp;
+        // 4-product split along K: A' = [hi | hi | lo | lo], B' = [hi | lo | hi | lo]
+        // (the lo·lo term keeps the per-product error at the residual's 2·2^-18)
+        CK(launch_pack_bf16(scrA, Gp, Kp, fA, ldop, 0b0011, 0b1100, fs + 0, s, L));
+        CK(launch_pack_bf16(scrB, Hp, Kp, fB, ldop, 0b0101, 0b1010, fs + 1, s, L));
+        k_len = 4 * Kp;
         S.elem = 2;
       }
       opA = reinterpret_cast<uint8_t*>(fA);

@@ -654,3 +654,46 @@ def test_sharded_path_nccl_single_rank(tmp_path):
     assert line, r.stdout[-3000:] + r.stderr[-3000:]
     d = json.loads(line[-1])
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and "row-shard" in d["config"]["parallelism"]
+
+
+# ---------------------------------------------------------------- randomized sweep over the plans
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_all_plans(engine, torch_mod, oracle_mod, monkeypatch, seed):
+    """Random shapes (sizes, key/group spans and dtypes, skew, value kinds) through every
+    plan the selector can take — auto, FORCE_DENSE, FORCE_SPARSE, the one-pass band kernel,
+    the hash-partitioned path — and the f2 shapes; all against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    for it in range(6):
+        n_a, n_b = int(rng.integers(1, 60000)), int(rng.integers(1, 60000))
+        kspan = int(rng.choice([50, 3000, 10 ** 6, 2 ** 40]))
+        zipf = rng.random() < 0.3
+        def keys(n):
+            k = (rng.zipf(1.3, n) % kspan) if zipf else rng.integers(0, kspan, n)
+            return (k * int(rng.choice([1, 7919])) - kspan // 3).astype(rng.choice([np.int32, np.int64]) if kspan < 2 ** 30 else np.int64)
+        G, H = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+        vk = rng.choice(["none", "int", "float"])
+        def vals(n):
+            if vk == "none":
+                return None
+            if vk == "int":
+                return rng.integers(-30, 31, n).astype(rng.choice([np.int32, np.int64]))
+            return rng.uniform(-4, 4, n).astype(np.float32)
+        A = datagen.Table(keys(n_a), rng.integers(0, G, n_a) * 3 - 100, vals(n_a))
+        B = datagen.Table(keys(n_b), rng.integers(0, H, n_b) - 7, vals(n_b))
+        agg = "count" if vk == "none" else rng.choice(["sum", "avg"])
+        ref = oracle_mod.join_agg(A, B, agg)
+        for flags, env in ((0, {}), (1, {}), (2, {}), (2, {"TCUDB_SPA_ONE_PASS": "1"}),
+                           (0, {"TCUDB_FORCE_HASHPART": "1"})):
+            for k_, v_ in env.items():
+                monkeypatch.setenv(k_, v_)
+            out, st = run(engine, torch_mod, A, B, agg, flags)
+            compare(out, ref, agg, float_vals=(vk == "float"))
+            for k_ in env:
+                monkeypatch.delenv(k_)
+        # f2 shapes on the same tables
+        for shape in ("h_only", "none"):
+            A2 = dict(A, g=None)
+            B2 = B if shape == "h_only" else dict(B, g=None)
+            ref2 = oracle_mod.join_agg(A2, B2, agg)
+            out2, _ = run(engine, torch_mod, A2, B2, agg, 0)
+            compare(out2, ref2, agg, float_vals=(vk == "float"))
