@@ -910,7 +910,7 @@ cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, i
                               cudaStream_t s, int64_t* launches) {
   const int64_t nt = (n + PT - 1) / PT;
   if (n <= 0) return exclusive_scan_i32(nullptr, nullptr, 0, count_dev, temp, s, launches);
-  if (n <= 8192) {  // small spans: one launch; larger ones need the parallel 3-pass scan
+  if (n <= 32768) {  // spans up to 32 K: one launch (2 sweeps of one block); larger: the 3-pass scan
     k_pred_codes_1blk<<<1, 1024, 0, s>>>(fa, fb, n, code, count_dev, union_dev, dict, minv);
     if (launches) ++*launches;
     return cudaGetLastError();
