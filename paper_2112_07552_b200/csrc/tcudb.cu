@@ -784,7 +784,11 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     // is detected by the fill and sends the query down the u8 path.
     uint8_t *op4A = nullptr, *op4B = nullptr;
     const int64_t Kp4 = round_up(K, 256);  // 128-byte K blocks of packed nibbles
-    if (allow_fp4 && !is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24)) {
+    // (small products skip it: the e2m1 fill is optimistic, and a duplicate cell costs a second
+    // fill + GEMM + sync, while a u8 GEMM of < 1e11 operations takes a few microseconds)
+    const char* fp4_always = getenv("TCUDB_FP4_ALWAYS");  // tests: e2m1 on small products too
+    if (allow_fp4 && !is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24) &&
+        (dense_ops >= 1e11 || (fp4_always && fp4_always[0] == '1'))) {
       op4A = ar.zeros<uint8_t>(Gp * Kp4 / 2);
       op4B = ar.zeros<uint8_t>(Hp * Kp4 / 2);
       CK(launch_fill_count_fp4(kA, gA, nA, op4A, Kp4, fs + 0, s, L));

@@ -471,8 +471,9 @@ def test_gemm_fp4_large_sums_exact(engine, torch_mod):
 
 
 @pytest.mark.parametrize("name,scale", [("c2", 0.1), ("c3", 1 / 16), ("c5", 1 / 256)])
-def test_count_fp4_vs_u8_vs_oracle(engine, torch_mod, oracle_mod, name, scale):
+def test_count_fp4_vs_u8_vs_oracle(engine, torch_mod, oracle_mod, monkeypatch, name, scale):
     """Dense COUNT through e2m1 operands (default), u8 operands (NO_FP4) and the oracle agree."""
+    monkeypatch.setenv("TCUDB_FP4_ALWAYS", "1")  # these reduced products are below the e2m1 threshold
     A, B, agg = datagen.make_config(name, scale)
     ref = oracle_mod.join_agg(A, B, agg)
     o4, s4 = run(engine, torch_mod, A, B, agg, 1)
@@ -518,6 +519,7 @@ def test_fused_compaction_matches(engine, torch_mod, oracle_mod, monkeypatch, ca
         hb = rng.integers(0, 3000, len(kb))
         A, B, agg = datagen.Table(ka, ga), datagen.Table(kb, hb), "count"
     ref = oracle_mod.join_agg(A, B, agg)
+    monkeypatch.setenv("TCUDB_FP4_ALWAYS", "1")
     monkeypatch.setenv("TCUDB_FUSED_COMPACT", "1")
     of, sf = run(engine, torch_mod, A, B, agg, 1)
     assert sf["elem"] == 3 and sf["fused_compact"] == 1
