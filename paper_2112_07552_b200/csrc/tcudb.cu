@@ -762,9 +762,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   int64_t* d_nnz = nullptr;
   int64_t nnz = 0;
   FillStats* fs4 = nullptr;  // flags of the unchecked e2m1 fill
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  // attempts: 0 = e2m1 allowed, then u8; 1 = u8; 2 = the wide (int64 scratch) path. The
+  // e2m1 and (for Kp <= 32 K) u8 fills are optimistic: their overflow flags are read with
+  // the result size, and a failed check reruns the matrix stage one step wider.
+  bool force_wide = false;
+  FillStats* fs8 = nullptr;  // flags of the unchecked u8 fill
+  for (int attempt = 0; attempt < 3; ++attempt) {
   const bool allow_fp4 = attempt == 0;
   fs4 = nullptr;
+  fs8 = nullptr;
   S.elem = is_float ? 1 : 0;
   S.planes_a = S.planes_b = 1;
   S.kchunks = 1;
@@ -795,17 +801,24 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       CK(launch_fill_count_fp4(kB, hB, nB, op4B, Kp4, fs + 1, s, L));
       fs4 = fs;  // checked at the result-size read below
     }
-    if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE)) {
+    if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE) && !force_wide) {
       opA = ar.zeros<uint8_t>(cellsA);
       opB = ar.zeros<uint8_t>(cellsB);
       CK(launch_fill_count_u8(kA, gA, nA, opA, Kp, fs + 0, s, L));
       CK(launch_fill_count_u8(kB, hB, nB, opB, Kp, fs + 1, s, L));
-      CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      FillStats hf[2];
-      std::memcpy(hf, ctx->pinned, sizeof(hf));
-      if (hf[0].overflow || hf[1].overflow) { opA = opB = nullptr; CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s)); }
-      else { maxA = hf[0].max_abs; maxB = hf[1].max_abs; }
+      if (Kp <= 32768) {
+        // u8 cells <= 255: every int32 partial of one pass over Kp <= 32 K is exact
+        // (255·255·32768 < 2^31), so the GEMM need not wait for the cell maxima
+        maxA = maxB = 255;
+        fs8 = fs;
+      } else {
+        CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        FillStats hf[2];
+        std::memcpy(hf, ctx->pinned, sizeof(hf));
+        if (hf[0].overflow || hf[1].overflow) { opA = opB = nullptr; CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s)); }
+        else { maxA = hf[0].max_abs; maxB = hf[1].max_abs; }
+      }
     }
     if (!op4A && !opA && !is_float) {
       // wide integer path: int64 scratch -> stats -> digit planes (guard a3)
@@ -1186,13 +1199,17 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
     if (sparse_u16.acc_kind == 4) CK(cudaMemcpyAsync(hov, sparse_u16.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (fs4) CK(cudaMemcpyAsync(hfs, fs4, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+    if (fs8) CK(cudaMemcpyAsync(hfs, fs8, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     nnz = hp[0];
-    if (fs4 && (hfs[0].overflow || hfs[1].overflow)) {
-      // a (g, k) or (h, k) cell holds two tuples: not 0/1, so not e2m1 — rerun on u8
+    if ((fs4 || fs8) && (hfs[0].overflow || hfs[1].overflow)) {
+      // e2m1: a (g, k) or (h, k) cell holds two tuples (not 0/1) — rerun on u8;
+      // u8: a cell passed 255 — rerun on the wide path
+      if (fs8) { force_wide = true; attempt = 1; }
       seg_cnt = nullptr;
       if (ub_base) { result_release(ctx, ub_base); ub_base = nullptr; }
       dense_fc = false;
+      CK(cudaMemsetAsync(fs8 ? fs8 : fs4, 0, sizeof(FillStats) * 2, s));
       continue;
     }
     if (*hov) {
