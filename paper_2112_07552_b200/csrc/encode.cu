@@ -32,6 +32,17 @@ TCUDB_DEV unsigned long long fmix64(unsigned long long k) {
   k ^= k >> 33;
   return k;
 }
+TCUDB_DEV unsigned fmix32(unsigned k) {
+  k ^= k >> 16; k *= 0x85ebca6bu;
+  k ^= k >> 13; k *= 0xc2b2ae35u;
+  k ^= k >> 16;
+  return k;
+}
+// Hash-dictionary slot hash of an offset x - min: 32-bit finalizer when every offset fits
+// 32 bits (two 32-bit multiplies instead of two 64-bit ones), else the 64-bit one.
+TCUDB_DEV unsigned long long slot_hash(unsigned long long off, int wide) {
+  return wide ? fmix64(off) : (unsigned long long)fmix32((unsigned)off);
+}
 
 // ------------------------------------------------------------------ a1: statistics
 // Block-level reduction, then ONE set of atomics per block: same-address global
@@ -242,7 +253,7 @@ __global__ void __launch_bounds__(1024) k_mark_direct_smem(ColDesc c, long long 
 // are inserted once (warp aggregation). flags[slot] = 1 marks the side.
 __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __restrict__ slots,
                               unsigned long long mask, uint8_t* __restrict__ flags, int* __restrict__ overflow,
-                              int32_t* __restrict__ row_slot) {
+                              int32_t* __restrict__ row_slot, int wide) {
   constexpr int U = 4;  // elements per thread per iteration: the first-probe loads overlap
   const int64_t stride = (int64_t)gridDim.x * T;
   const int64_t n_round = (c.n + 31) & ~int64_t(31);
@@ -255,7 +266,7 @@ __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __r
       ok[u] = i < c.n;
       off[u] = ok[u] ? (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv
                      : ~0ull - 1 - lane_id();
-      h[u] = fmix64(off[u]) & mask;
+      h[u] = slot_hash(off[u], wide) & mask;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) cur[u] = ok[u] ? __ldcg(slots + h[u]) : 0ull;
@@ -294,7 +305,7 @@ __global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long 
                                                           unsigned long long* __restrict__ slots,
                                                           unsigned long long mask, uint8_t* __restrict__ flags,
                                                           int* __restrict__ overflow, int32_t* __restrict__ row_slot,
-                                                          int cap_s, int64_t chunk) {
+                                                          int cap_s, int64_t chunk, int wide) {
   extern __shared__ unsigned long long s_key[];
   int32_t* s_map = reinterpret_cast<int32_t*>(s_key + cap_s);
   __shared__ int s_n, s_bad;
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long 
   __syncthreads();
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(c.n, lo + chunk);
   auto sfind = [&](unsigned long long off, bool insert) -> int {
-    unsigned h = (unsigned)fmix64(off) & smask;
+    unsigned h = (unsigned)slot_hash(off, wide) & smask;
     for (int step = 0; step < cap_s; ++step) {
       const unsigned long long cur = s_key[h];
       if (cur == off) return (int)h;
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long 
   for (int sidx = threadIdx.x; sidx < cap_s; sidx += blockDim.x) {
     const unsigned long long off = s_key[sidx];
     if (off == ~0ull) continue;
-    unsigned long long hh = fmix64(off) & mask;
+    unsigned long long hh = slot_hash(off, wide) & mask;
     int32_t placed = -1;
     for (unsigned long long step = 0; step <= mask; ++step) {
       const unsigned long long cc = __ldcg(slots + hh);
@@ -562,7 +573,7 @@ __global__ void k_remap_codes(int32_t* __restrict__ codes, int64_t n, const int3
 TCUDB_DEV int32_t dict_lookup(const DictView& d, long long x) {
   const unsigned long long off = (unsigned long long)x - (unsigned long long)d.minv;
   if (d.mode == 0) return off < d.size ? d.code[off] : -1;
-  unsigned long long h = fmix64(off) & d.size;  // size = mask in hash mode
+  unsigned long long h = slot_hash(off, d.wide) & d.size;  // size = mask in hash mode
   while (true) {
     const unsigned long long k = d.slots[h];
     if (k == off) return d.code[h];
@@ -585,7 +596,7 @@ TCUDB_DEV void dict_lookup_batch(const DictView& d, const long long* x, const bo
   unsigned long long h[U], k[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    h[u] = fmix64(off[u]) & d.size;
+    h[u] = slot_hash(off[u], d.wide) & d.size;
     k[u] = ok[u] ? __ldg(d.slots + h[u]) : off[u];
   }
 #pragma unroll
@@ -874,8 +885,8 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 }
 
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, cudaStream_t s,
-                               int64_t* launches) {
+                               uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, int wide,
+                               cudaStream_t s, int64_t* launches) {
   if (c.n <= 0) return cudaSuccess;
   // shared-memory pre-aggregation when the estimated distinct count is small and
   // there are many tuples per distinct value (tables sized 2^ceil(log2(1.9 est)))
@@ -891,11 +902,12 @@ cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long l
     const int per_sm = smem <= 96 * 1024 ? 2 : 1;
     const int64_t nblk = std::min<int64_t>(per_sm * kNumSMs, (c.n + 32767) / 32768);
     const int64_t chunk = (c.n + nblk - 1) / nblk;
-    k_hash_insert_smem<<<(int)nblk, 1024, smem, s>>>(c, minv, slots, mask, flags, overflow, row_slot, cap_s, chunk);
+    k_hash_insert_smem<<<(int)nblk, 1024, smem, s>>>(c, minv, slots, mask, flags, overflow, row_slot, cap_s, chunk,
+                                                      wide);
     if (launches) ++*launches;
     return cudaGetLastError();
   }
-  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags, overflow, row_slot);
+  k_hash_insert<<<grid_for(c.n), T, 0, s>>>(c, minv, slots, mask, flags, overflow, row_slot, wide);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -35,6 +35,7 @@ struct DictView {
   // hash mode, optional: slot of each row of the column this view is probed with (written
   // by the insert): the lookup is then code[row_slot[i]], no rehash or table walk
   const int32_t* row_slot;
+  int wide;  // hash mode: offsets need 64 bits (fmix64 slot hash), else the 32-bit one
 };
 
 // ---------------------------------------------------------------- encode.cu
@@ -51,8 +52,8 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 // Open-addressing insert of (x - minv); *overflow = 1 if the table is full; row_slot
 // (optional, c.n entries) receives each row's slot.
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
-                               uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, cudaStream_t s,
-                               int64_t* launches);
+                               uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, int wide,
+                               cudaStream_t s, int64_t* launches);
 size_t pred_temp_bytes(int64_t n);
 // codes = exclusive scan of pred(i) (-1 where false); optional dict[code] = minv + i (direct
 // group domains: the sorted value dictionary comes out of the same pass).

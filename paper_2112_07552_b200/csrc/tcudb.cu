@@ -125,6 +125,7 @@ struct Dict {
   int* ovf = nullptr;         // hash mode: table-full flag (the estimate was too small)
   int32_t* slot1 = nullptr;   // hash mode: slot of each row of the first / second column
   int32_t* slot2 = nullptr;
+  int wide = 1;               // hash mode: offsets need 64 bits (slot hash fmix64 vs fmix32)
   DictView view(int col = 0) const {
     DictView v;
     v.mode = mode;
@@ -133,6 +134,7 @@ struct Dict {
     v.code = code;
     v.slots = slots;
     v.row_slot = col == 1 ? slot1 : col == 2 ? slot2 : nullptr;
+    v.wide = wide;
     return v;
   }
 };
@@ -197,6 +199,7 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
   } else {
     if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
     d.mode = 1;
+    d.wide = span > ((unsigned __int128)1 << 32) ? 1 : 0;  // some offset needs more than 32 bits
     unsigned long long want = (unsigned long long)(2 * n);
     if (est_distinct > 0) want = std::min(want, (unsigned long long)(1.9 * est_distinct) + 64);
     const unsigned long long cap = next_pow2(want);
@@ -207,14 +210,14 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.ovf = ar.zeros<int>(1);
     // per-row slots: the probe then reads code[slot] instead of rehashing and walking the table
     d.slot1 = ar.get<int32_t>(c1.n);
-    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, s, launches));
+    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, d.wide, s, launches));
     if (c2) {
       d.slot2 = ar.get<int32_t>(c2->n);
       if (intersect) {
         d.fb = ar.zeros<uint8_t>((int64_t)cap);
-        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, d.slot2, est_distinct, s, launches));
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fb, d.ovf, d.slot2, est_distinct, d.wide, s, launches));
       } else {
-        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot2, est_distinct, s, launches));
+        CK(launch_hash_insert(*c2, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot2, est_distinct, d.wide, s, launches));
       }
     }
     d.code = ar.get<int32_t>((int64_t)cap);
