@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
         const int64_t col = col0[q] + j * 32 + lane;
         const bool in = col < lim[q];
         e[q][j] = in ? __ldcs(E + row[q] * a.lde + col) : ET(0);
-        hv[q][j] = in ? __ldg(a.dict_h + col) : 0;
+        hv[q][j] = !in ? 0 : a.h_affine ? a.h_base + col : __ldg(a.dict_h + col);
       }
     }
 #pragma unroll

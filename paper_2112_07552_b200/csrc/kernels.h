@@ -300,6 +300,9 @@ struct CompactArgs {
   int g_out_type, h_out_type;                    // 0 I32, 1 I64
   int agg_out;                                   // 0 int64, 1 f64
   void* out_g; void* out_h; void* out_agg;
+  // affine h dictionary (a direct-offset domain with every value present: value = code + h_base):
+  // the decode is an add instead of a gather
+  int h_affine; long long h_base;
 };
 size_t compact_temp_bytes(int64_t G, int64_t nseg);
 cudaError_t launch_compact_count(const CompactArgs& a, const int32_t* precounted, int64_t* nnz_dev, void* temp,

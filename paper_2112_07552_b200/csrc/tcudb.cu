@@ -755,6 +755,9 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   } ub_guard{ctx, &ub_base};
   ca.G = G; ca.H = H;
   ca.dict_g = DG.dict; ca.dict_h = DH.dict;
+  // a direct-offset h domain with every value present decodes by an add (c2, c4)
+  ca.h_affine = DH.mode == 0 && (int64_t)DH.span == H;
+  ca.h_base = DH.minv;
   ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
   ca.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
   ca.agg_out = is_float ? 1 : 0;
