@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(NT) k_spa_write(const SpaArgs a) {
 // per band or two CTAs per SM on wide rows); a count reaching 65,535 raises *ovf and
 // the caller reruns the kernel with int32 cells.
 constexpr int NTF = 512;
-constexpr size_t kSmemFused = 108 * 1024;  // 2 CTAs per SM
+constexpr size_t kSmemFused = 96 * 1024;  // + ~17 KB static (stages): 2 CTAs per SM
 
 template <int ACC> struct FusedCell;
 template <> struct FusedCell<0> { using T = uint16_t; };            // COUNT, packed u16
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
   using T = typename FusedCell<ACC>::T;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int64_t s_base[NTF / 32 + 1];
-  __shared__ uint8_t s_stage[NTF / 32][256];
+  __shared__ uint16_t s_stage16[NTF / 32][16 * 32];
   __shared__ int64_t s_rowbase[64];
   __shared__ int s_rowcnt[64];
   __shared__ int64_t s_band;
@@ -390,18 +390,20 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
       for (int r = 0; r < nr; ++r) { s_rowbase[r] = run; run += s_rowcnt[r]; }
     }
     __syncthreads();
-    // write: per row, warps own contiguous slices of 8-word (256-cell) groups (see k_spa_write)
-    const int ngrp = (int)((W + 7) / 8);
-    const int per = (ngrp + nw - 1) / nw;
-    const int q0 = min(ngrp, wid * per), q1 = min(ngrp, q0 + per);
-    uint8_t* stage = s_stage[wid];
-    const int nbytes = (int)W * 4;
+    // write: per row, warps own contiguous slices of 16-word (512-cell) chunks; lanes 0-15
+    // hold one bitmap word each, a warp scan numbers the chunk's tuples, each lane lists its
+    // set bits into the warp's 512-entry stage, and the stage is written out 32 tuples per
+    // step (coalesced (g, h, agg) stores)
+    constexpr int CW = 16;
+    const int nch = (int)((W + CW - 1) / CW);
+    const int per = (nch + nw - 1) / nw;
+    const int q0 = min(nch, wid * per), q1 = min(nch, q0 + per);
+    uint16_t* stage = s_stage16[wid];
     for (int r = 0; r < nr; ++r) {
       const int64_t g = g0 + r;
       unsigned* rb = bits + r * W;
-      const uint8_t* rbytes = reinterpret_cast<const uint8_t*>(rb);
       int c = 0;
-      for (int i = q0 * 32 + lane; i < q1 * 32 && i < nbytes; i += 32) c += __popc(rbytes[i]);
+      for (int64_t wq = (int64_t)q0 * CW + lane; wq < (int64_t)q1 * CW && wq < W; wq += 32) c += __popc(rb[wq]);
       c = warp_sum(c);
       if (lane == 0) s_base[wid] = c;
       __syncthreads();
@@ -414,25 +416,28 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
       const long long gv = a.dict_g[g];
       T* arow = acc + (int64_t)r * ldc;
       for (int q = q0; q < q1; ++q) {
-        const int bi = q * 32 + lane;
-        unsigned m = bi < nbytes ? rbytes[bi] : 0u;
+        const int64_t wi = (int64_t)q * CW + lane;
+        unsigned m = (lane < CW && wi < W) ? rb[wi] : 0u;
         const int cnt = __popc(m);
         int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
+        for (int o = 1; o < CW; o <<= 1) {
           const int t = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += t;
         }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int total = __shfl_sync(0xffffffffu, incl, CW - 1);
         if (total == 0) continue;
         int p = incl - cnt;
-        while (m) {
-          const int bb = __ffs(m) - 1;
-          stage[p++] = (uint8_t)(lane * 8 + bb);
-          m &= m - 1;
+        if (lane < CW) {
+          while (m) {
+            const int bb = __ffs(m) - 1;
+            stage[p++] = (uint16_t)(lane * 32 + bb);
+            m &= m - 1;
+          }
+          if (wi < W) rb[wi] = 0u;  // this word is consumed
         }
         __syncwarp();
-        const int64_t hq = (int64_t)q * 256;
+        const int64_t hq = (int64_t)q * CW * 32;
         for (int j = lane; j < total; j += 32) {
           const int64_t h = hq + stage[j];
           const int64_t o = base + j;
@@ -449,8 +454,6 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
         __syncwarp();
         base += total;
       }
-      // clear this warp's slice of the row bitmap (all its bytes were read above)
-      for (int wq = q0 * 8 + lane; wq < q1 * 8 && wq < W; wq += 32) rb[wq] = 0u;
       __syncthreads();  // s_base reuse
     }
   }
