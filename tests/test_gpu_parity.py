@@ -701,3 +701,25 @@ def test_fuzz_all_plans(engine, torch_mod, oracle_mod, monkeypatch, seed):
             ref2 = oracle_mod.join_agg(A2, B2, agg)
             out2, _ = run(engine, torch_mod, A2, B2, agg, 0)
             compare(out2, ref2, agg, float_vals=(vk == "float"))
+
+
+def test_u8_count_long_k_and_wide_retry(engine, torch_mod, oracle_mod):
+    """Dense COUNT with K > 32 K keys (the u8 fill is checked before the GEMM and the int32
+    accumulation is chunked) and, separately, a cell past 255 caught by the optimistic u8
+    check (rerun on the int64 wide path)."""
+    rng = np.random.default_rng(8)
+    K = 40000
+    ka = np.concatenate([np.arange(K), rng.integers(0, K, 30000)])
+    A = datagen.Table(ka, rng.integers(0, 200, len(ka)))
+    B = datagen.Table(rng.integers(0, K, 50000), rng.integers(0, 300, 50000))
+    ref = oracle_mod.join_agg(A, B, "count")
+    out, st = run(engine, torch_mod, A, B, "count", 1)
+    assert st["path"] == 0 and st["elem"] == 0
+    compare(out, ref, "count")
+    # 300 copies of one (g, k) cell: the optimistic u8 fill overflows and the query reruns wide
+    A2 = datagen.Table(np.concatenate([np.full(300, 5), rng.integers(0, 100, 2000)]),
+                       np.concatenate([np.full(300, 1), rng.integers(0, 50, 2000)]))
+    B2 = datagen.Table(rng.integers(0, 100, 3000), rng.integers(0, 60, 3000))
+    ref2 = oracle_mod.join_agg(A2, B2, "count")
+    out2, st2 = run(engine, torch_mod, A2, B2, "count", 1)
+    compare(out2, ref2, "count")
