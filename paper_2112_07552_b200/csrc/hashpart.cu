@@ -61,7 +61,9 @@ __global__ void k_chunk_starts(const int64_t* __restrict__ seg_off, int nseg, in
 
 struct PassIO {
   const void* raw; int raw_type; long long kmin; const int32_t* g_raw;  // pass 1 (raw column)
+  const void* v_raw; int v_type;                                        // pass 1 values (SUM)
   const unsigned long long* k_in; const int32_t* g_in;
+  const long long* v_in; long long* v_out;                              // value payload (SUM)
   const int64_t* seg_off; int nseg; int shift; int bits;
   const int64_t* chunk_start;
   int32_t* counts;  // [total_chunks * R] in (segment, digit, chunk) order
@@ -77,6 +79,11 @@ TCUDB_DEV void load_tuple(const PassIO& io, int64_t i, unsigned long long& k, in
     k = io.k_in[i];
     g = io.g_in[i];
   }
+}
+TCUDB_DEV long long load_value(const PassIO& io, int64_t i) {
+  if (!io.v_out) return 0;
+  if (io.raw) return io.v_raw ? ld_int(io.v_raw, io.v_type, i) : 1;
+  return io.v_in[i];
 }
 
 __global__ void __launch_bounds__(PT) k_part_hist(const PassIO io) {
@@ -100,11 +107,13 @@ __global__ void __launch_bounds__(PT) k_part_hist(const PassIO io) {
   for (int d = threadIdx.x; d < R; d += PT) io.counts[base + (int64_t)d * nch + j] = h[d];
 }
 
-__global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
+template <bool VAL>
+__global__ void __launch_bounds__(PT, 2) k_part_scatter(const PassIO io) {  // 2 x 1,024 threads per SM
   extern __shared__ __align__(16) uint8_t stage_raw[];
   unsigned long long* sk = reinterpret_cast<unsigned long long*>(stage_raw);  // [CH]
   int32_t* sg = reinterpret_cast<int32_t*>(sk + CH);                          // [CH]
   uint8_t* sd = reinterpret_cast<uint8_t*>(sg + CH);                          // [CH] digit of each entry
+  long long* sv = reinterpret_cast<long long*>(sd + CH);                       // [CH] values (SUM only)
   __shared__ int cnt[kMaxDigits], lstart[kMaxDigits];
   __shared__ int64_t gpos[kMaxDigits];
   const int64_t c = blockIdx.x;
@@ -122,6 +131,7 @@ __global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
   const int64_t lo = io.seg_off[s] + j * CH, hi = min(io.seg_off[s + 1], lo + CH);
   unsigned long long k[4];
   int32_t g[4];
+  long long v[4];
   int d[4], r[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -129,6 +139,7 @@ __global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
     d[u] = -1;
     if (i < hi) {
       load_tuple(io, i, k[u], g[u]);
+      if (VAL) v[u] = load_value(io, i);
       d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
       r[u] = atomicAdd(&cnt[d[u]], 1);
     }
@@ -164,6 +175,7 @@ __global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
       sk[p] = k[u];
       sg[p] = g[u];
       sd[p] = (uint8_t)d[u];
+      if (VAL) sv[p] = v[u];
     }
   __syncthreads();
   const int total = (int)(hi - lo);
@@ -172,6 +184,7 @@ __global__ void __launch_bounds__(PT) k_part_scatter(const PassIO io) {
     const int64_t o = gpos[a] + (p - lstart[a]);
     io.k_out[o] = sk[p];
     io.g_out[o] = sg[p];
+    if (VAL) io.v_out[o] = sv[p];
   }
 }
 
@@ -281,13 +294,17 @@ __global__ void __launch_bounds__(1024) k_part_sum(const unsigned long long* __r
   }
 }
 
+template <bool SUM>
 __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* __restrict__ ka,
                                                     const int32_t* __restrict__ ga,
                                                     const int64_t* __restrict__ offa,
                                                     const unsigned long long* __restrict__ kb,
                                                     const int32_t* __restrict__ hb,
                                                     const int64_t* __restrict__ offb, int ts_bits, int cap,
-                                                    unsigned* __restrict__ C, int64_t ldc) {
+                                                    unsigned* __restrict__ C, int64_t ldc,
+                                                    const long long* __restrict__ va,
+                                                    const long long* __restrict__ vb,
+                                                    unsigned long long* __restrict__ C64) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int wsum[QTE / 32];
   const int TS = 1 << ts_bits, mask = TS - 1;
@@ -296,6 +313,7 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
   int* start = cnt + TS;                          // per slot: bucket start
   int* bslot = start + TS;                        // per B tuple of the partition: its slot
   int* bh = bslot + cap;                          // B group codes bucketed by slot
+  long long* bw = reinterpret_cast<long long*>(smem + (size_t)TS * 16 + (size_t)cap * 8);  // SUM: B values, bucketed
   for (int i = threadIdx.x; i < TS; i += QTE) { keys[i] = ~0ull; cnt[i] = 0; }
   __syncthreads();
   const int p = blockIdx.x;
@@ -329,7 +347,9 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += QTE) {
     const int h = bslot[i];
-    bh[start[h] + atomicAdd(cnt + h, 1)] = __ldcs(hb + b0 + i);
+    const int pos = start[h] + atomicAdd(cnt + h, 1);
+    bh[pos] = __ldcs(hb + b0 + i);
+    if (SUM) bw[pos] = __ldcs(vb + b0 + i);
   }
   __syncthreads();
   for (int64_t i = offa[p] + threadIdx.x; i < offa[p + 1]; i += QTE) {
@@ -337,9 +357,21 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
     if (h < 0) continue;
     const int n = cnt[h];
     if (n == 0) continue;
-    unsigned* row = C + (int64_t)__ldcs(ga + i) * ldc;
+    const int64_t r = (int64_t)__ldcs(ga + i) * ldc;
+    unsigned* row = C + r;
     const int e0 = start[h];
-    for (int e = 0; e < n; ++e) atomicAdd(row + bh[e0 + e], 1u);  // RED: no return value used
+    if (SUM) {
+      // integer SUM: wrapping products and sums (exact whenever the result fits int64; the
+      // caller has checked J·max|v|·max|w|), plus the COUNT plane for existence (R3)
+      const unsigned long long v = (unsigned long long)__ldcs(va + i);
+      unsigned long long* row64 = C64 + r;
+      for (int e = 0; e < n; ++e) {
+        atomicAdd(row64 + bh[e0 + e], v * (unsigned long long)bw[e0 + e]);
+        atomicAdd(row + bh[e0 + e], 1u);
+      }
+    } else {
+      for (int e = 0; e < n; ++e) atomicAdd(row + bh[e0 + e], 1u);  // RED: no return value used
+    }
   }
 }
 
@@ -366,7 +398,8 @@ size_t hashpart_temp_bytes(int64_t n, int nseg, int bits) {
 cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
                              const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
                              int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
-                             int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches) {
+                             int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
+                             const ColDesc* v_raw, const long long* v_in, long long* v_out) {
   if (bits < 1 || bits > 7 || n <= 0) return cudaErrorInvalidValue;
   const int R = 1 << bits;
   const int64_t chunks = max_chunks(n, nseg);
@@ -383,6 +416,8 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   io.k_in = k_in; io.g_in = g_in; io.seg_off = seg_off; io.nseg = nseg; io.shift = shift; io.bits = bits;
   io.chunk_start = chunk_start; io.counts = counts; io.offs = offs;
   io.k_out = k_out; io.g_out = g_out; io.seg_out = seg_out;
+  io.v_raw = v_raw ? v_raw->data : nullptr; io.v_type = v_raw ? v_raw->type : 0;
+  io.v_in = v_in; io.v_out = v_out;
   k_chunk_starts<<<1, 32, 0, s>>>(seg_off, nseg, chunk_start);
   // unused count slots (chunks past the real total) must scan as zero
   cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cnts * 4, s);
@@ -391,13 +426,16 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   e = exclusive_scan_i32(counts, offs, cnts, nullptr, t, s, launches);
   if (e != cudaSuccess) return e;
   static bool attr = false;
-  constexpr int kStage = CH * 13;
+  // staging per tuple: key 8 + group 4 + digit 1 (+ value 8 for SUM)
   if (!attr) {
-    e = cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kStage);
+    e = cudaFuncSetAttribute(k_part_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 21);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_part_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 13);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_part_scatter<<<(unsigned)chunks, PT, kStage, s>>>(io);
+  if (v_out) k_part_scatter<true><<<(unsigned)chunks, PT, CH * 21, s>>>(io);
+  else k_part_scatter<false><<<(unsigned)chunks, PT, CH * 13, s>>>(io);
   const int64_t so = (int64_t)nseg * R + 1;
   k_seg_out<<<(unsigned)std::min<int64_t>((so + 255) / 256, 1024), 256, 0, s>>>(io);
   if (launches) *launches += 4;
@@ -431,20 +469,25 @@ cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa,
   return cudaGetLastError();
 }
 
-size_t part_expand_smem(int cap) { return (size_t)(1 << ts_bits_for(cap)) * 16 + (size_t)cap * 8; }
+size_t part_expand_smem(int cap, bool sum) {
+  return (size_t)(1 << ts_bits_for(cap)) * 16 + (size_t)cap * (sum ? 16 : 8);
+}
 
 cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, const int64_t* offa,
                                const unsigned long long* kb, const int32_t* hb, const int64_t* offb, int P, int cap,
-                               unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches) {
+                               unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches, const long long* va,
+                               const long long* vb, unsigned long long* C64) {
   const int tb = ts_bits_for(cap);
-  const size_t smem = part_expand_smem(cap);
+  const size_t smem = part_expand_smem(cap, C64 != nullptr);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_part_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_part_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_part_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  k_part_expand<<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc);
+  if (C64) k_part_expand<true><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64);
+  else k_part_expand<false><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

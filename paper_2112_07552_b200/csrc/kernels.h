@@ -233,18 +233,23 @@ size_t hashpart_temp_bytes(int64_t n, int nseg, int bits);
 cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
                              const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
                              int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
-                             int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches);
-size_t part_expand_smem(int cap);
+                             int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
+                             const ColDesc* v_raw = nullptr, const long long* v_in = nullptr,
+                             long long* v_out = nullptr);  // value payload (integer SUM), optional
+size_t part_expand_smem(int cap, bool sum);
 // per partition: J_p = sum over its keys of cntA*cntB, D_p = #keys on both sides; out has
 // 4 + 4 P entries: totals out[0] (J), out[1] (K = sum D_p), out[2] (A tuples with a matched
 // key), out[3] (distinct B keys); per-partition values after them
 cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa, const unsigned long long* kb,
                               const int64_t* offb, int P, int cap, unsigned long long* out, cudaStream_t s,
                               int64_t* launches);
-// per partition: C[g][h] += 1 for every joined pair (u32 cells, row stride ldc)
+// per partition: C[g][h] += 1 for every joined pair (u32 cells, row stride ldc); with C64,
+// also C64[g][h] += va·vb (integer SUM, wrapping int64)
 cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, const int64_t* offa,
                                const unsigned long long* kb, const int32_t* hb, const int64_t* offb, int P, int cap,
-                               unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches);
+                               unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches,
+                               const long long* va = nullptr, const long long* vb = nullptr,
+                               unsigned long long* C64 = nullptr);
 // largest partition (max over both sides) into *out (zeroed)
 cudaError_t launch_part_max(const int64_t* offa, const int64_t* offb, int P, unsigned long long* out, cudaStream_t s,
                             int64_t* launches);

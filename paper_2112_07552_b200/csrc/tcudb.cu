@@ -332,7 +332,7 @@ struct QueryOut {
 bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb_table* B, const ColDesc& ak,
                     const ColDesc& ag, const ColDesc& bk, const ColDesc& bh, const ColStats* hs, const double* est,
                     long long kmin, tcudb_result* out, tcudb_stats& S, Timer& tm, int64_t* L, cudaStream_t s,
-                    bool timed) {
+                    bool timed, bool sum, const ColDesc& av, const ColDesc& bw) {
   const int64_t nA = ak.n, nB = bk.n;
   Dict DG, DH;
   dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
@@ -363,8 +363,9 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   while (pbits < 14 && ((int64_t)1 << pbits) * 1024 < std::max(nA, nB)) ++pbits;
   const int b1 = (pbits + 1) / 2, b2 = pbits - b1;
   const int P = 1 << pbits;
-  struct Side { unsigned long long* k[2]; int32_t* g[2]; int64_t* seg1; int64_t* seg2; };
+  struct Side { unsigned long long* k[2]; int32_t* g[2]; long long* v[2]; int64_t* seg1; int64_t* seg2; };
   Side sd[2];
+  const ColDesc* vals[2] = {&av, &bw};  // integer SUM: value payload (absent column = 1)
   const ColDesc* keys[2] = {&ak, &bk};
   const int32_t* grp[2] = {gA, hB};
   const int64_t ns[2] = {nA, nB};
@@ -378,15 +379,18 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
     const int64_t n = ns[x];
     sd[x].k[0] = ar.get<unsigned long long>(n); sd[x].k[1] = ar.get<unsigned long long>(n);
     sd[x].g[0] = ar.get<int32_t>(n); sd[x].g[1] = ar.get<int32_t>(n);
+    sd[x].v[0] = sum ? ar.get<long long>(n) : nullptr;
+    sd[x].v[1] = sum ? ar.get<long long>(n) : nullptr;
     sd[x].seg1 = ar.get<int64_t>(((int64_t)1 << b1) + 1);
     sd[x].seg2 = ar.get<int64_t>((int64_t)P + 1);
     void* t1 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1, b1));
     CK(launch_part_pass(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
-                        sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L));
+                        sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L, sum ? vals[x] : nullptr, nullptr,
+                        sd[x].v[0]));
     if (b2) {
       void* t2 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1 << b1, b2));
       CK(launch_part_pass(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
-                          sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, s, L));
+                          sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, s, L, nullptr, sd[x].v[0], sd[x].v[1]));
     }
   }
   const int fin = b2 ? 1 : 0;
@@ -394,7 +398,7 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   unsigned long long* d_max = ar.zeros<unsigned long long>(1);
   CK(launch_part_max(sd[0].seg2, sd[1].seg2, P, d_max, s, L));
   const int64_t cap = (int64_t)*to_pinned<unsigned long long>(ctx, d_max, s);
-  if (cap <= 0 || part_expand_smem((int)std::min<int64_t>(cap, 1 << 20)) > 200 * 1024) return false;
+  if (cap <= 0 || part_expand_smem((int)std::min<int64_t>(cap, 1 << 20), sum) > 200 * 1024) return false;
   CK(launch_part_count(sd[0].k[fin], sd[0].seg2, sd[1].k[fin], sd[1].seg2, P, (int)cap, d_out, s, L));
   unsigned long long cnt[4];
   CK(cudaMemcpyAsync(ctx->pinned, d_out, 32, cudaMemcpyDeviceToHost, s));
@@ -412,16 +416,26 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
     return true;  // empty result (out already zeroed)
   }
   if (t_dense <= t_sparse || J >= (1ull << 32)) return false;
+  if (sum) {
+    // int64 guard (a3): |SUM| <= J·max|v|·max|w|; beyond it the general path's finer bound decides
+    auto absmax = [&](const ColDesc& c, int i) -> long double {
+      if (!c.data) return 1.0L;
+      return std::max(std::fabs((long double)hs[i].mn), std::fabs((long double)hs[i].mx));
+    };
+    if ((long double)J * absmax(av, 4) * absmax(bw, 5) >= 9.2e18L) return false;
+  }
   unsigned* C = ar.zeros<unsigned>(G * ldc);
+  unsigned long long* C64 = sum ? ar.zeros<unsigned long long>(G * ldc) : nullptr;
   if (timed) cudaEventRecord(ctx->evk[0], s);
   CK(launch_part_expand(sd[0].k[fin], sd[0].g[fin], sd[0].seg2, sd[1].k[fin], sd[1].g[fin], sd[1].seg2, P, (int)cap,
-                        C, ldc, s, L));
+                        C, ldc, s, L, sd[0].v[fin], sd[1].v[fin], C64));
   if (timed) cudaEventRecord(ctx->evk[1], s);
   tm.mark(&S.ms_sparse);
   // a8 compaction of C (u32 counts; codes are ascending ranks -> (g, h) order)
   CompactArgs ca{};
   ca.G = G; ca.H = H; ca.nseg = (H + 255) / 256; ca.seg_w = 256;
   ca.E = C; ca.e_kind = 0; ca.lde = ldc; ca.V = C; ca.v_kind = 0; ca.ldv = ldc;
+  if (sum) { ca.V = C64; ca.v_kind = 1; }  // existence from the COUNT plane (R3), SUM from C64
   ca.dict_g = DG.dict; ca.dict_h = DH.dict;
   ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
   ca.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
@@ -538,8 +552,11 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     const bool big = (est[0] >= (double)(1 << 19) && nA >= (1 << 20) && nB >= (1 << 20)) ||
                      (force_hp && force_hp[0] == '1');
     const bool hk = !dict_is_direct(nA + nB, kmin, kmax);
-    if (!is_sum && !absent && hk && big && !(q->flags & TCUDB_FORCE_DENSE) && !(no_hp && no_hp[0] == '1')) {
-      if (hashpart_query(ctx, ar, A, B, ak, ag, bk, bh, hs, est, kmin, out, S, tm, L, s, st != nullptr)) {
+    // COUNT or integer SUM (AVG composes them below; float sums stay on the general path)
+    const bool hp_agg = q->agg == TCUDB_COUNT || (q->agg == TCUDB_SUM && !is_float);
+    if (hp_agg && !absent && hk && big && !(q->flags & TCUDB_FORCE_DENSE) && !(no_hp && no_hp[0] == '1')) {
+      if (hashpart_query(ctx, ar, A, B, ak, ag, bk, bh, hs, est, kmin, out, S, tm, L, s, st != nullptr,
+                         q->agg == TCUDB_SUM, av, bw)) {
         tm.finish();
         S.n_launches = (int32_t)(ctx->launches - launches0);
         S.ms_total = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
