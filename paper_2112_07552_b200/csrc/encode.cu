@@ -206,7 +206,7 @@ __global__ void k_init_stats(ColStats* st, int n) {
 // ------------------------------------------------------------------ #distinct sketch
 // PAPER.md §4.2.1 keeps "the number of distinct values" per column as
 // metadata. For hash-mode domains it is estimated on the device with a HyperLogLog
-// sketch (2^13 registers, ~1.2 % standard error) so the hash table is sized by the
+// sketch (2^12 registers, ~1.6 % standard error) so the hash table is sized by the
 // distinct count (L2-resident when small) instead of by the tuple count.
 __global__ void __launch_bounds__(1024) k_hll(ColDesc c, unsigned* __restrict__ regs) {
   __shared__ unsigned s_reg[kHllM];
