@@ -753,3 +753,27 @@ def test_hash_partitioned_int_sum(engine, torch_mod, oracle_mod, monkeypatch, ca
     out2, _ = run(engine, torch_mod, A, B, "sum", 0)
     for k in ("g", "h", "agg"):
         assert np.array_equal(out[k], out2[k])
+
+
+def test_abi_error_statuses(engine, torch_mod):
+    """Argument errors come back as status codes (never partial results): exclusive FORCE
+    flags -> E_INVALID; float keys, mixed int/float values, float chain values ->
+    E_UNSUPPORTED; and the context stays usable afterwards."""
+    torch = torch_mod
+    from paper_2112_07552_b200._lib import TcudbError
+    k = torch.arange(10, device="cuda", dtype=torch.int32)
+    A = {"k": k, "g": k}
+    with pytest.raises(TcudbError) as ei:
+        engine.join_agg(A, A, "count", flags=1 | 2)
+    assert ei.value.status == -1
+    with pytest.raises(TcudbError) as ei:
+        engine.join_agg({"k": k.float(), "g": k}, A, "count")
+    assert ei.value.status == -2
+    with pytest.raises(TcudbError) as ei:
+        engine.join_agg(dict(A, v=k.float()), dict(A, v=k), "sum")
+    assert ei.value.status == -2
+    with pytest.raises(TcudbError) as ei:
+        engine.chain_join_agg(dict(A, v=k.float()), A, A, "sum")
+    assert ei.value.status == -2
+    out = engine.join_agg(A, A, "count")
+    assert out["agg"].sum().item() == 10
