@@ -140,7 +140,8 @@ __device__ __forceinline__ void spa_expand(const SpaArgs& a, int64_t t_begin, in
   }
 }
 
-__global__ void __launch_bounds__(NT) k_spa_count(const SpaArgs a) {
+constexpr int NTC = 512;  // count pass: 2 CTAs per SM
+__global__ void __launch_bounds__(NTC, 2) k_spa_count(const SpaArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   // count_bands consecutive bands per CTA (their tuples are contiguous)
   const int64_t b0 = (int64_t)blockIdx.x * a.count_bands;
@@ -150,13 +151,13 @@ __global__ void __launch_bounds__(NT) k_spa_count(const SpaArgs a) {
   const int nr = (int)(g1 - g0);
   const int64_t W = a.words;
   unsigned* bits = reinterpret_cast<unsigned*>(smem);
-  for (int i = threadIdx.x; i < nr * (int)W; i += NT) bits[i] = 0u;
+  for (int i = threadIdx.x; i < nr * (int)W; i += NTC) bits[i] = 0u;
   __syncthreads();
   spa_expand<false>(a, a.goff[b0], a.goff[b1], g0, [&](int r, int h, int64_t, int32_t) {
     atomicOr(bits + r * W + (h >> 5), 1u << (h & 31));
   });
   __syncthreads();
-  for (int r = warp_id(); r < nr; r += NT / 32) {
+  for (int r = warp_id(); r < nr; r += NTC / 32) {
     int c = 0;
     for (int64_t w = lane_id(); w < W; w += 32) c += __popc(bits[r * W + w]);
     c = warp_sum(c);
@@ -568,7 +569,7 @@ cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_spa_count<<<(unsigned)((a.nbands + a.count_bands - 1) / a.count_bands), NT, sm, s>>>(a);
+  k_spa_count<<<(unsigned)((a.nbands + a.count_bands - 1) / a.count_bands), NTC, sm, s>>>(a);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
