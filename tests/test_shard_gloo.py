@@ -34,11 +34,24 @@ class CpuStandIn:
 
     def join_agg(self, A, B, agg, with_stats=False):
         import oracle
-        np_t = lambda T: datagen.Table(T["k"].numpy(), T["g"].numpy(), T["v"].numpy() if "v" in T else None)
+        col = lambda T, c: T[c].numpy() if T.get(c) is not None else None
+        np_t = lambda T: datagen.Table(T["k"].numpy(), col(T, "g"), col(T, "v"))
         r = oracle.join_agg(np_t(A), np_t(B), agg)
-        out = {"g": torch.from_numpy(r["g"]), "h": torch.from_numpy(r["h"]),
-               "agg": torch.from_numpy(r["cnt"] if agg == "count" else r["sum"])}
+        out = {c: torch.from_numpy(r[c]) for c in ("g", "h") if c in r}
+        out["agg"] = torch.from_numpy(r[_AGGKEY[agg]])
         return (out, {}) if with_stats else out
+
+
+_AGGKEY = {"count": "cnt", "sum": "sum", "avg": "avg"}
+
+
+def _variant(A, B, agg, drop):
+    """Q3 / Q4 variants of a config: drop="a" ungroups A, "b" ungroups B, "ab" both."""
+    if "a" in drop:
+        A = dict(A, g=None)
+    if "b" in drop:
+        B = dict(B, g=None)
+    return A, B
 
 
 def _free_port():
@@ -49,12 +62,19 @@ def _free_port():
     return p
 
 
+def _load(name):
+    base, _, rest = name.partition(":")
+    A, B, agg = datagen.make_config(base, 0.05) if base != "c1s" else datagen.make_config(base)
+    drop, _, ag = rest.partition(":")
+    return (*_variant(A, B, agg, drop), ag or agg)
+
+
 def _worker(rank, ws, port, name, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     try:
         from paper_2112_07552_b200.shard import local_slice, sharded_join_agg
-        A, B, agg = datagen.make_config(name, 0.05) if name != "c1s" else datagen.make_config(name)
+        A, B, agg = _load(name)
         tA = {k: torch.from_numpy(v) for k, v in local_slice(A, ws, rank).items() if v is not None}
         tB = {k: torch.from_numpy(v) for k, v in local_slice(B, ws, rank).items() if v is not None}
         out = sharded_join_agg(CpuStandIn(), tA, tB, agg)
@@ -63,7 +83,10 @@ def _worker(rank, ws, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["c1s", "c2", "c3"])
+# "config:ungrouped sides:agg" — Q3 by A.g / by B.h and Q4 shard on the grouped
+# side or reduce the per-rank partials with an allreduce
+@pytest.mark.parametrize("name", ["c1s", "c2", "c3", "c1s:b:sum", "c1s:a:avg", "c2:a:count",
+                                  "c1s:ab:sum", "c1s:ab:avg", "c3:ab:count"])
 def test_sharded_equals_single(oracle_mod, name):
     ws = 2
     ctx = mp.get_context("spawn")
@@ -76,12 +99,19 @@ def test_sharded_equals_single(oracle_mod, name):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    A, B, agg = datagen.make_config(name, 0.05) if name != "c1s" else datagen.make_config(name)
+    A, B, agg = _load(name)
     ref = oracle_mod.join_agg(A, B, agg)
     for r in range(ws):
-        assert np.array_equal(res[r]["g"], ref["g"])
-        assert np.array_equal(res[r]["h"], ref["h"])
-        assert np.array_equal(res[r]["agg"], ref["cnt"] if agg == "count" else ref["sum"])
+        assert set(res[r]) == {c for c in ("g", "h") if c in ref} | {"agg"}
+        for c in ("g", "h"):
+            if c in ref:
+                assert np.array_equal(res[r][c], ref[c])
+        want = ref[_AGGKEY[agg]]
+        if want.dtype == np.float64:
+            # Q4 adds the per-rank partials in another order than the one-pass oracle
+            assert np.allclose(res[r]["agg"], want, rtol=1e-12, atol=0)
+        else:
+            assert np.array_equal(res[r]["agg"], want)
 
 
 def test_range_bounds():
