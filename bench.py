@@ -123,6 +123,16 @@ def gemm_traffic_from_profiles(config, elem):
     return None
 
 
+def sparse_traffic_from_profiles(config, spa_mode):
+    """DRAM bytes per sparse-kernel launch from the committed ncu capture (same schedule only)."""
+    p = os.path.join(ROOT, "profiles", f"kernel_traffic_{config}.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("spa_mode") == spa_mode:
+            return d.get("dram_bytes_per_launch")
+    return None
+
+
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args):
     ws, rank, _ = dist_env()
@@ -331,7 +341,8 @@ def main():
                 "peak_source": f"{peaks['source']} copy bandwidth", "bytes_per_launch": st["kernel_bytes"],
                 "avg_launch_ms": k_ms, "spa_mode": {2: "count pass + band writer", 3: "one pass (look-back)",
                                                     4: "hash-partitioned"}.get(
-                    st["spa_mode"], st["spa_mode"]), "traffic": None}
+                    st["spa_mode"], st["spa_mode"]),
+                "traffic": sparse_traffic_from_profiles(args.config, st["spa_mode"])}
     else:
         # sparse or reduction path without the band kernel: stage time, 16 B per joined pair
         b = st["join_pairs"] * 16.0
