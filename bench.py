@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--shard-impl", default="native", choices=["native", "python"],
+                    help="multi-GPU path: collective libtcudb call (native) or shard.py over torch.distributed")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the multi-GPU row-sharded path even on one rank (NCCL group of 1; test hook)")
     args = ap.parse_args()
@@ -210,7 +212,10 @@ def main():
 
     A, B, agg = load_tables(args.config)
     n_tuples = len(A["k"]) + len(B["k"])
-    eng = Engine(local)
+    native = sharded and args.shard_impl == "native"
+    # native: the collective tcudb_join_agg (NCCL inside libtcudb, collective.cu);
+    # python: the same algorithm driven from shard.py over torch.distributed
+    eng = Engine(local, group=torch.distributed.group.WORLD) if native else Engine(local)
     stream = torch.cuda.current_stream(dev)
     to_dev = lambda T: {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in T.items() if v is not None}
     if not sharded:
@@ -219,7 +224,8 @@ def main():
     else:
         sA, sB = shard_mod.local_slice(A, ws, rank), shard_mod.local_slice(B, ws, rank)
         dA, dB = to_dev(sA), to_dev(sB)
-        step = lambda: shard_mod.sharded_join_agg(eng, dA, dB, agg, with_stats=True)
+        step = ((lambda: eng.join_agg(dA, dB, agg, with_stats=True)) if native
+                else (lambda: shard_mod.sharded_join_agg(eng, dA, dB, agg, with_stats=True)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     for _ in range(args.warmup):
@@ -262,13 +268,19 @@ def main():
         hB = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in sB.items() if v is not None}
         h2d = sum(v.numel() * v.element_size() for v in list(hA.values()) + list(hB.values()))
 
+        if native:
+            nA = {k: v.numpy() for k, v in hA.items()}
+            nB = {k: v.numpy() for k, v in hB.items()}
+
         def e2e_step():
+            if native:  # collective host API: slices in, full result out (pinned host)
+                return eng.join_agg_host(nA, nB, agg)
             gA = {k: v.to(dev, non_blocking=True) for k, v in hA.items()}
             gB = {k: v.to(dev, non_blocking=True) for k, v in hB.items()}
             r = shard_mod.sharded_join_agg(eng, gA, gB, agg)
             return {k: v.to("cpu") for k, v in r.items()}
         r = e2e_step()
-        d2h = sum(v.numel() * v.element_size() for v in r.values())
+        d2h = sum(v.nbytes if isinstance(v, np.ndarray) else v.numel() * v.element_size() for v in r.values())
         del r
         ts = []
         for _ in range(args.e2e_steps):
@@ -387,9 +399,11 @@ def main():
                    "G": st["G"], "H": st["H"], "K": st["K"], "join_pairs": st["join_pairs"],
                    "result_groups": st["n_result"], "path": "dense" if st["path"] == 0 else "sparse",
                    "parallelism": f"row-shard x{ws} (A routed by g range, B allgathered, results allgathered; "
+                                  f"{'collective libtcudb call over NCCL' if native else 'shard.py over torch.distributed'}; "
                                   f"G/H/K/stage_ms are rank 0's local query)" if sharded else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps"},
-        "stage_ms": {k: st[k] for k in ("ms_stats", "ms_encode", "ms_fill", "ms_gemm", "ms_sparse", "ms_compact")},
+        "stage_ms": {k: st[k] for k in ("ms_stats", "ms_encode", "ms_fill", "ms_gemm", "ms_sparse", "ms_compact")
+                     + (("ms_comm",) if native else ())},
         "step_ms": [round(x, 4) for x in step_ms],
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
         **({"triangle_query": tri} if tri else {}),

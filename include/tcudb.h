@@ -38,7 +38,7 @@ typedef enum {
   TCUDB_E_OVERFLOW = -4,    /* the precision guard proves an int64 result could overflow */
   TCUDB_E_NOMEM = -5,       /* device memory for operands / C / result exhausted */
   TCUDB_E_CUDA = -6,        /* CUDA runtime / launch error (sticky) */
-  TCUDB_E_COMM = -7         /* reserved for the collective path */
+  TCUDB_E_COMM = -7         /* collective path: NCCL / exchange failure */
 } tcudb_status;
 
 typedef enum { TCUDB_I32 = 0, TCUDB_I64 = 1, TCUDB_F32 = 2, TCUDB_F64 = 3 } tcudb_dtype;
@@ -66,7 +66,7 @@ typedef struct {
 enum {
   TCUDB_FORCE_DENSE = 1u << 0,  /* tensor-core GEMM path (a5, a6) */
   TCUDB_FORCE_SPARSE = 1u << 1, /* sparse-operand expand path (a7) */
-  TCUDB_GATHER_NONE = 1u << 2,  /* reserved (multi-GPU: keep row shards) */
+  TCUDB_GATHER_NONE = 1u << 2,  /* collective calls: return this rank's shard of the result */
   TCUDB_UNORDERED = 1u << 3,    /* reserved: output order unspecified */
   TCUDB_FORCE_WIDE = 1u << 4,   /* test hook: skip the packed fp4/u8 COUNT fills, use the
                                    int64 scratch + digit-plane guard path */
@@ -117,6 +117,7 @@ typedef struct {
   int32_t fused_compact; /* dense path: 1 if the compaction ran inside the GEMM kernel */
   float ms_kernel;       /* sparse path: CUDA-event time of the band kernel (k_spa_fused) */
   double kernel_bytes;   /* ... and its algorithmic bytes (4 J + 20 n_active + result bytes) */
+  float ms_comm;         /* collective calls: host wall time of the exchanges (NCCL + routing) */
 } tcudb_stats;
 
 typedef struct tcudb_ctx tcudb_ctx;
@@ -126,9 +127,19 @@ typedef struct tcudb_ctx tcudb_ctx;
 typedef void* (*tcudb_alloc_fn)(size_t bytes, void* stream, void* user);
 typedef void (*tcudb_free_fn)(void* ptr, void* stream, void* user);
 
-/* Create a context on `device`. nccl_comm is reserved (pass NULL); the
- * multi-GPU row sharding lives in the Python layer. Returns E_CUDA if the
- * device is not sm_100 or the CUDA runtime fails. */
+/* Create a context on `device`. nccl_comm: NULL, or an ncclComm_t (one rank per
+ * GPU; owned by the caller, e.g. torch's ProcessGroupNCCL communicator) — then every
+ * tcudb_join_agg / tcudb_join_agg_host on this context is COLLECTIVE (SURVEY §8(b)
+ * "Multi-GPU", §8(e)): each rank passes its local slices of A and B; output rows are
+ * sharded by ranges of the grouped side's group key (A.g; B.h for GROUP BY B.h only),
+ * that side's rows are routed to their owners (all-to-all-v), the other side is
+ * allgathered, each rank runs the local query, and the result is allgathered in rank
+ * order — on every rank identical to the single-GPU result — or, with
+ * TCUDB_GATHER_NONE, left as the rank's (g, h)-sorted shard. Without GROUP BY (Q4)
+ * the per-rank partial aggregates are combined with allreduces. NCCL (libnccl.so.2,
+ * the process's own) is resolved here with dlopen. Exchange failures: E_COMM.
+ * Returns E_CUDA if the device is not sm_100 or the CUDA runtime fails, E_COMM if
+ * the communicator is unusable. */
 tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_alloc_fn alloc_fn,
                           tcudb_free_fn free_fn, void* user);
 

@@ -6,7 +6,7 @@ The computation lives in libtcudb.so (hand-written sm_100a CUDA behind the C
 ABI in include/tcudb.h). This package is the thin Python binding (`Engine`)
 plus the multi-GPU row-sharding driver (`shard`).
 """
-from ._lib import (COUNT, FORCE_DENSE, FORCE_SPARSE, FORCE_WIDE, SUM, Engine, TcudbError,  # noqa: F401
+from ._lib import (COUNT, FORCE_DENSE, FORCE_SPARSE, FORCE_WIDE, GATHER_NONE, SUM, Engine, TcudbError,  # noqa: F401
                    load, LIB_PATH, EXPORTS)
 
-__all__ = ["Engine", "TcudbError", "load", "LIB_PATH", "EXPORTS", "FORCE_DENSE", "FORCE_SPARSE", "FORCE_WIDE"]
+__all__ = ["Engine", "TcudbError", "load", "LIB_PATH", "EXPORTS", "FORCE_DENSE", "FORCE_SPARSE", "FORCE_WIDE", "GATHER_NONE"]

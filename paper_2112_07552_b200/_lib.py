@@ -65,7 +65,8 @@ class Stats(ctypes.Structure):
                 ("ms_stats", ctypes.c_float), ("ms_encode", ctypes.c_float), ("ms_fill", ctypes.c_float),
                 ("ms_gemm", ctypes.c_float), ("ms_sparse", ctypes.c_float), ("ms_compact", ctypes.c_float),
                 ("ms_total", ctypes.c_float), ("spa_mode", ctypes.c_int32), ("spa_max_band", ctypes.c_int64),
-                ("fused_compact", ctypes.c_int32), ("ms_kernel", ctypes.c_float), ("kernel_bytes", ctypes.c_double)]
+                ("fused_compact", ctypes.c_int32), ("ms_kernel", ctypes.c_float), ("kernel_bytes", ctypes.c_double),
+                ("ms_comm", ctypes.c_float)]
 
     def to_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -192,10 +193,31 @@ class _DevArray:
                                          "stream": None}
 
 
+def nccl_comm_ptr(group, device: int) -> int:
+    """The ncclComm_t of a torch.distributed NCCL process group on `device` (created
+    eagerly by one tiny collective: ProcessGroupNCCL builds communicators lazily)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) != "nccl":
+        raise ValueError("the collective engine needs an NCCL process group")
+    t = torch.zeros(1, device=f"cuda:{device}")
+    dist.all_reduce(t, group=group)
+    torch.cuda.synchronize(device)
+    pg = group if group is not None else dist.group.WORLD
+    backend = pg._get_backend(torch.device("cuda", device))
+    ptr = int(backend._comm_ptr())
+    if not ptr:
+        raise RuntimeError("ProcessGroupNCCL has no communicator for this device")
+    return ptr
+
+
 class Engine:
     """One tcudb context on one CUDA device (sm_100a)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, group=None):
+        """group: None (single GPU), or a torch.distributed NCCL process group (e.g.
+        torch.distributed.group.WORLD) — then join_agg / join_agg_host are collective over
+        its ranks (one GPU per rank; see tcudb_create in include/tcudb.h)."""
         import torch
         self._torch = torch
         self._lib = load()
@@ -203,11 +225,13 @@ class Engine:
         torch.cuda.init()
         self._alloc_cb = ALLOC_FN(self._alloc)
         self._free_cb = FREE_FN(self._free)
+        comm = None if group is None else ctypes.c_void_p(nccl_comm_ptr(group, self.device))
         ctx = ctypes.c_void_p()
-        st = self._lib.tcudb_create(ctypes.byref(ctx), self.device, None, self._alloc_cb, self._free_cb, None)
+        st = self._lib.tcudb_create(ctypes.byref(ctx), self.device, comm, self._alloc_cb, self._free_cb, None)
         if st != TCUDB_OK:
-            raise TcudbError(st, "tcudb_create failed (needs an sm_100 GPU)")
+            raise TcudbError(st, "tcudb_create failed (needs an sm_100 GPU; with a group: a usable NCCL communicator)")
         self._ctx = ctx
+        self.collective = group is not None
 
     # allocator callbacks -> torch caching allocator (torch owns result memory)
     def _alloc(self, nbytes, stream, user):

@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <string>
+
+#include "../../include/tcudb.h"
 
 namespace tcudb {
 
@@ -67,5 +70,17 @@ size_t radix_temp_bytes(int64_t n);
 cudaError_t radix_sort_pairs(unsigned long long* keys, uint32_t* vals, unsigned long long* keys_alt,
                              uint32_t* vals_alt, int64_t n,
                              int bits, void* temp, cudaStream_t s, int64_t* launches, bool* result_in_alt);
+
+// ---------------------------------------------------------------- multi-GPU (collective.cu)
+struct NcclComm;
+NcclComm* nccl_attach(void* comm, std::string* err);
+void nccl_detach(NcclComm* c);
+tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* nc, const tcudb_table* A, const tcudb_table* B,
+                                 const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, cudaStream_t s,
+                                 float* ms_comm);
+// host-runtime helpers the collective path shares (tcudb.cu)
+void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s);
+void internal_result_release(tcudb_ctx* ctx, void* p);
+tcudb_status internal_set_err(tcudb_ctx* ctx, tcudb_status st, const char* msg);
 
 }  // namespace tcudb

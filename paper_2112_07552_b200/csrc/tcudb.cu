@@ -48,6 +48,8 @@ struct tcudb_ctx {
   std::map<void*, size_t> host_size;
   std::map<void*, bool> dev_from_cb;  // result pointer -> allocated through afn
   bool fp4 = true;                    // e2m1 COUNT operands allowed (env TCUDB_NO_FP4=1 disables)
+  tcudb::NcclComm* nc = nullptr;      // collective context (tcudb_create with an ncclComm_t)
+  bool in_collective = false;         // the local query inside a collective call
 };
 
 namespace {
@@ -1341,12 +1343,23 @@ tcudb_status fail_err(tcudb_ctx* ctx, const Fail& f) {
 
 }  // namespace
 
+namespace tcudb {
+void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s) {
+  try {
+    return result_alloc(ctx, bytes, s);
+  } catch (const Fail&) {
+    throw std::bad_alloc();
+  }
+}
+void internal_result_release(tcudb_ctx* ctx, void* p) { result_release(ctx, p); }
+tcudb_status internal_set_err(tcudb_ctx* ctx, tcudb_status st, const char* msg) { return set_err(ctx, st, msg); }
+}  // namespace tcudb
+
 // =========================================================================== C ABI
 extern "C" {
 
 tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_alloc_fn alloc_fn,
                           tcudb_free_fn free_fn, void* user) {
-  (void)nccl_comm;
   if (!out) return TCUDB_E_INVALID;
   *out = nullptr;
   int major = 0, minor = 0;
@@ -1376,6 +1389,14 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   for (auto& e : c->evk) cudaEventCreate(&e);
+  if (nccl_comm) {
+    std::string why;
+    c->nc = nccl_attach(nccl_comm, &why);
+    if (!c->nc) {
+      tcudb_destroy(c);
+      return TCUDB_E_COMM;
+    }
+  }
   *out = c;
   return TCUDB_OK;
 }
@@ -1397,6 +1418,23 @@ tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_ta
     return set_err(ctx, TCUDB_E_UNSUPPORTED, "mixed integer / float value columns");
   cudaSetDevice(ctx->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (ctx->nc && !ctx->in_collective) {
+    // collective call (collective.cu): routing + exchanges around the local query below
+    struct In { bool& f; explicit In(bool& x) : f(x) { f = true; } ~In() { f = false; } } in(ctx->in_collective);
+    float ms_comm = 0.f;
+    tcudb_status st;
+    try {
+      st = collective_join_agg(ctx, ctx->nc, A, B, q, out, stats, s, &ms_comm);
+    } catch (const Fail& f) {
+      std::memset(out, 0, sizeof(*out));
+      return fail_err(ctx, f);
+    } catch (const std::bad_alloc&) {
+      std::memset(out, 0, sizeof(*out));
+      return set_err(ctx, TCUDB_E_NOMEM, "collective result allocation");
+    }
+    if (stats) stats->ms_comm = ms_comm;
+    return st;
+  }
   // an absent group column = that side is not grouped (Q3 / Q4): a constant
   // column stands in (one group), and the result omits that column
   tcudb_table A2 = *A, B2 = *B;
@@ -1520,6 +1558,7 @@ tcudb_status tcudb_chain_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tc
   if (!ctx || !out || !A || !B || !C || !q) return TCUDB_E_INVALID;
   std::memset(out, 0, sizeof(*out));
   if (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM) return set_err(ctx, TCUDB_E_UNSUPPORTED, "chain: COUNT or SUM");
+  if (ctx->nc) return set_err(ctx, TCUDB_E_UNSUPPORTED, "chain joins run on a single-GPU context");
   const bool vals = q->agg == TCUDB_SUM;
   for (const tcudb_table* t : {A, B, C})
     if (vals && t->value.data && t->value.type == TCUDB_F32)
@@ -1726,6 +1765,7 @@ void tcudb_destroy(tcudb_ctx* ctx) {
   if (ctx->pinned_big) cudaFreeHost(ctx->pinned_big);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->evk) if (e) cudaEventDestroy(e);
+  if (ctx->nc) nccl_detach(ctx->nc);
   delete ctx;
 }
 

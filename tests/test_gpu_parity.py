@@ -643,6 +643,75 @@ print("SHARD_OK")
 """
 
 
+NATIVE_SCRIPT = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import datagen, oracle
+from paper_2112_07552_b200 import Engine, GATHER_NONE, TcudbError
+from paper_2112_07552_b200.shard import local_slice
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+e = Engine(0, group=dist.group.WORLD)
+assert e.collective
+ws, rk = dist.get_world_size(), dist.get_rank()
+KEY = {"count": "cnt", "sum": "sum", "avg": "avg"}
+def check(out, ref, agg, tag):
+    for c in ("g", "h"):
+        assert (c in out) == (c in ref), (tag, c)
+        if c in ref:
+            assert np.array_equal(np.asarray(out[c].cpu() if hasattr(out[c], "cpu") else out[c]), ref[c]), (tag, c)
+    got = np.asarray(out["agg"].cpu() if hasattr(out["agg"], "cpu") else out["agg"])
+    want = ref[KEY[agg]]
+    ok = np.allclose(got, want, rtol=1e-12, atol=0) if want.dtype == np.float64 else np.array_equal(got, want)
+    assert ok, tag
+for name, scale, drop, ag, flags in (("c1", 1.0, "", None, 0), ("c2", 0.1, "", None, 0), ("c1s", 1.0, "", None, 0),
+                                     ("c1s", 1.0, "", "avg", 0), ("c1s", 1.0, "b", "sum", 0),
+                                     ("c1s", 1.0, "a", "avg", 0), ("c1s", 1.0, "ab", "sum", 0),
+                                     ("c1s", 1.0, "ab", "avg", 0), ("c2", 0.1, "ab", "count", 0),
+                                     ("c1", 1.0, "", None, GATHER_NONE)):
+    A, B, agg = datagen.make_config(name, scale)
+    agg = ag or agg
+    if "a" in drop: A = dict(A, g=None)
+    if "b" in drop: B = dict(B, g=None)
+    sA, sB = local_slice(A, ws, rk), local_slice(B, ws, rk)
+    dev = lambda T: {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in T.items() if v is not None}
+    out, st = e.join_agg(dev(sA), dev(sB), agg, flags=flags, with_stats=True)
+    assert st["ms_comm"] >= 0
+    ref = oracle.join_agg(A, B, agg)
+    check(out, ref, agg, (name, drop, agg, flags))
+    # collective host API: host slices in, the full result out
+    hout = e.join_agg_host({k: v for k, v in sA.items() if v is not None},
+                           {k: v for k, v in sB.items() if v is not None}, agg, flags=flags)
+    check(hout, ref, agg, ("host", name, drop, agg))
+# chain joins are single-GPU only on a collective context
+A, B, _ = datagen.make_config("c1")
+try:
+    e.chain_join_agg(dev(A), dev(B), dev(B), "count")
+    raise SystemExit("chain on a collective context should fail")
+except TcudbError:
+    pass
+dist.destroy_process_group()
+print("NATIVE_OK")
+"""
+
+
+def test_native_collective_single_rank(tmp_path):
+    """The collective tcudb_join_agg (collective.cu: NCCL resolved by dlopen, torch's
+    communicator) on a 1-rank NCCL group: routing, all-to-all-v, allgather-v, Q3/Q4
+    allreduces, GATHER_NONE and the host API, against the oracle."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "native_check.py"
+    script.write_text(NATIVE_SCRIPT)
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(script)],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert "NATIVE_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_sharded_path_nccl_single_rank(tmp_path):
     """The multi-GPU driver (tcudb_minmax, tcudb_partition, NCCL all_to_all / allgather) on a
     1-rank NCCL group (one GPU in this environment), and bench.py --force-shard under torchrun."""
