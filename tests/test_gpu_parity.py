@@ -682,8 +682,16 @@ for name, scale, drop, ag, flags in (("c1", 1.0, "", None, 0), ("c2", 0.1, "", N
     hout = e.join_agg_host({k: v for k, v in sA.items() if v is not None},
                            {k: v for k, v in sB.items() if v is not None}, agg, flags=flags)
     check(hout, ref, agg, ("host", name, drop, agg))
-# chain joins are single-GPU only on a collective context
+# empty inputs on the collective path: empty result, no exchange errors
 A, B, _ = datagen.make_config("c1")
+Z = {k: v[:0] for k, v in A.items() if v is not None}
+for agg in ("count", "sum", "avg"):
+    for TA, TB in ((Z, B), (A, Z)):
+        out = e.join_agg(dev(TA), dev(TB), agg)
+        assert all(len(v) == 0 for v in out.values()), agg
+    out = e.join_agg(dev(dict(Z, g=None)), dev(dict(B, g=None)), agg)
+    assert len(out["agg"]) == 0, agg
+# chain joins are single-GPU only on a collective context
 try:
     e.chain_join_agg(dev(A), dev(B), dev(B), "count")
     raise SystemExit("chain on a collective context should fail")
