@@ -106,6 +106,68 @@ __global__ void k_fill_bf16_direct(const int32_t* __restrict__ kcode, const int3
   if (lane_id() == 0 && inexact) atomicOr(&fs->inexact, 1);
 }
 
+// Row-range pass of the direct fill (c4-sized operands exceed L2: scattered 2-byte stores
+// into HBM-resident lines cost a read-modify-write each). The caller zeroes rows [r0, r1)
+// (full lines, allocated in L2) and runs one pass per range sized to fit L2: the tuple
+// columns stream through with evict_first loads, the 2-byte stores carry an evict_last
+// policy, so each line is merged in L2 and written back once. A duplicate (row, k) cell
+// is detected afterwards: #nonzero cells == #tuples with nonzero bits (a zero-valued
+// duplicate cannot change a cell's correct value, any other duplicate loses a nonzero).
+__global__ void k_fill_bf16_rows(const int32_t* __restrict__ kcode, const int32_t* __restrict__ rcode,
+                                 const float* __restrict__ val, int64_t n, uint16_t* __restrict__ op, int64_t ld_op,
+                                 int32_t r0, int32_t r1, FillStats* __restrict__ fs) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * T;
+  int inexact = 0;
+  unsigned long long nz = 0;
+  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < n; i0 += U * stride) {
+    // all loads of the U tuples are issued before any store (three phases)
+    int32_t r[U], kc[U];
+    uint32_t b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = i0 + u * stride < n ? __ldcs(rcode + i0 + u * stride) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool in = r[u] >= r0 && r[u] < r1;
+      kc[u] = in ? __ldcs(kcode + i0 + u * stride) : -1;
+      b[u] = in && val ? __float_as_uint(__ldcs(val + i0 + u * stride)) : 0x3F800000u;  // absent value = 1.0
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kc[u] < 0) continue;
+      inexact |= (b[u] & 0xFFFFu) != 0u;
+      const unsigned short h = (unsigned short)(b[u] >> 16);
+      nz += h != 0;
+      asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(op + (int64_t)r[u] * ld_op + kc[u]), "h"(h),
+                   "l"(pol));
+    }
+  }
+  inexact = __any_sync(0xffffffffu, inexact);
+  nz = warp_sum(nz);
+  if (lane_id() == 0) {
+    if (inexact) atomicOr(&fs->inexact, 1);
+    if (nz) atomicAdd(&fs->nzt, nz);
+  }
+}
+
+__global__ void k_count_nonzero_u16(const uint16_t* __restrict__ op, int64_t ld_op, int64_t rows, int64_t cols,
+                                    unsigned long long* __restrict__ out) {
+  // cols % 8 == 0: 16-byte vectors, 8 cells each
+  const int64_t vpr = cols / 8, nv = rows * vpr;
+  unsigned long long c = 0;
+  for (int64_t v = (int64_t)blockIdx.x * T + threadIdx.x; v < nv; v += (int64_t)gridDim.x * T) {
+    const int64_t r = v / vpr, j = v - r * vpr;
+    const uint4 x = __ldcs(reinterpret_cast<const uint4*>(op + r * ld_op) + j);
+    const unsigned w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c += ((w[q] & 0xFFFFu) != 0) + ((w[q] >> 16) != 0);
+  }
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
 // ---- binned bf16 direct fill: the same result as k_fill_bf16_direct without the
 // scattered 2-byte stores into HBM. Rows are grouped into bands of R rows (a band is one
 // shared-memory tile of R x Kp bf16) and bands into coarse bins of P bands:
@@ -456,6 +518,24 @@ cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int
                                  FillStats* fs, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;
   k_fill_count_u8<<<grid_for(n), T, 0, s>>>(kcode, rcode, n, op, ld, fs);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_bf16_rows(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                  uint16_t* op, int64_t ld_op, int32_t r0, int32_t r1, FillStats* fs, cudaStream_t s,
+                                  int64_t* launches) {
+  if (n <= 0) return cudaSuccess;
+  k_fill_bf16_rows<<<kNumSMs * 8, T, 0, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, op, ld_op, r0, r1,
+                                            fs);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_nonzero_u16(const uint16_t* op, int64_t ld_op, int64_t rows, int64_t cols,
+                                     unsigned long long* out, cudaStream_t s, int64_t* launches) {
+  if (rows <= 0 || cols <= 0 || cols % 8) return cols % 8 ? cudaErrorInvalidValue : cudaSuccess;
+  k_count_nonzero_u16<<<kNumSMs * 8, T, 0, s>>>(op, ld_op, rows, cols, out);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -96,6 +96,7 @@ struct FillStats {
   int inexact;                 // float: some cell is not bf16-exact
   int neg;                     // some cell < 0
   int pad;
+  unsigned long long nzt;      // tuples with a nonzero bf16 (row-range direct fill)
 };
 // COUNT: packed u8 atomics directly into op[row][k] (row = code of the group).
 cudaError_t launch_fill_count_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
@@ -107,6 +108,13 @@ cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, in
 // Float SUM with <= 1 tuple per cell and bf16-exact values: bf16 bits stored straight into
 // op[r][k]; occ is a zeroed 1-bit occupancy map [rows][ld_occ bits] (a second tuple in a cell:
 // popcount(occ) < tuples written, checked by the caller); fs->inexact: value not bf16-exact.
+// Row-range passes of the direct bf16 fill: rows [r0, r1) only, stores kept in L2
+// (evict_last) over a range sized to fit it; then nonzero cells are counted.
+cudaError_t launch_fill_bf16_rows(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                  uint16_t* op, int64_t ld_op, int32_t r0, int32_t r1, FillStats* fs, cudaStream_t s,
+                                  int64_t* launches);
+cudaError_t launch_count_nonzero_u16(const uint16_t* op, int64_t ld_op, int64_t rows, int64_t cols,
+                                     unsigned long long* out, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                     uint16_t* op, int64_t ld_op, unsigned* occ, int64_t ld_occ, FillStats* fs,
                                     cudaStream_t s, int64_t* launches);

@@ -55,6 +55,7 @@ struct tcudb_ctx {
 namespace {
 
 constexpr size_t kPinnedBytes = 4096;
+constexpr int64_t kFillRangeBytes = 48ll << 20;  // operand rows per L2-resident fill range
 
 struct Fail {
   tcudb_status st;
@@ -886,13 +887,29 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         // optimistic: <= 1 tuple per cell and bf16-exact values -> the cells are the values
         // per side: binned (tile in shared memory, duplicate -> overflow) when the shape
         // fits, else scattered stores + occupancy bits whose popcount must equal the tuples
-        bool binned[2];
+        bool binned[2], ranged[2];
+        // row-range passes (each range's operand rows L2-resident, ~10.5 ps per tuple, bound by
+        // L2's scattered 2-byte store rate) while at most 3 ranges cover the operand; above
+        // that the re-reads of the tuple columns per range cost more than the binned fill
+        // (~13 ps per tuple at c4). TCUDB_FILL_PASSES=n forces n ranges, 0 the binned fill.
+        const char* fp_env = getenv("TCUDB_FILL_PASSES");
         auto direct_fill = [&](int side, const int32_t* kc, const int32_t* rc, const ColDesc& v, int64_t n,
                                int64_t rows, uint16_t* op) {
+          const int64_t auto_p = (rows * Kp * 2 + kFillRangeBytes - 1) / kFillRangeBytes;
+          const int fill_passes = fp_env ? atoi(fp_env) : (auto_p <= 3 && Kp % 8 == 0 ? (int)auto_p : 0);
           const char* nb = getenv("TCUDB_NO_BINNED_FILL");
           const size_t ws = (nb && nb[0] == '1') ? 0 : fill_bf16_binned_ws(n, rows, Kp);
-          binned[side] = ws != 0;
-          if (ws) {
+          binned[side] = ws != 0 && fill_passes <= 0;
+          ranged[side] = fill_passes > 0;
+          if (ranged[side]) {
+            const int64_t per = ((rows + fill_passes - 1) / fill_passes + 127) / 128 * 128;
+            for (int64_t r0 = 0; r0 < rows; r0 += per) {
+              const int64_t r1 = std::min(rows, r0 + per);
+              CK(cudaMemset2DAsync(op + r0 * ldop, ldop * 2, 0, Kp * 2, r1 - r0, s));
+              CK(launch_fill_bf16_rows(kc, rc, v, n, op, ldop, (int32_t)r0, (int32_t)r1, fs + side, s, L));
+            }
+            CK(launch_count_nonzero_u16(op, ldop, rows, Kp, &fs[side].nnz, s, L));
+          } else if (binned[side]) {
             CK(launch_fill_bf16_binned(kc, rc, v, n, rows, Kp, op, ldop, fs + side, ar.get<uint8_t>(ws), s, L));
           } else {
             CK(cudaMemset2DAsync(op, ldop * 2, 0, Kp * 2, rows, s));
@@ -908,7 +925,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         FillStats hf[2];
         std::memcpy(hf, ctx->pinned, sizeof(hf));
         auto no_dup = [&](int side, int64_t tuples) {
-          return binned[side] ? !hf[side].overflow : hf[side].nnz == tuples;
+          return ranged[side] ? hf[side].nnz == hf[side].nzt
+                 : binned[side] ? !hf[side].overflow : hf[side].nnz == tuples;
         };
         bf16_direct = no_dup(0, misc[3]) && no_dup(1, misc[4]) && !(hf[0].inexact | hf[1].inexact);
         if (!bf16_direct) CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));

@@ -864,3 +864,32 @@ def test_abi_error_statuses(engine, torch_mod):
     assert ei.value.status == -2
     out = engine.join_agg(A, A, "count")
     assert out["agg"].sum().item() == 10
+
+
+# ---------------------------------------------------------------- ranged bf16 fill (a5)
+@pytest.mark.parametrize("passes", [None, "1", "3"])
+@pytest.mark.parametrize("case", ["unique", "dup_nonzero", "dup_zero_after", "zero_values"])
+def test_bf16_range_fill_duplicates(engine, torch_mod, oracle_mod, monkeypatch, passes, case):
+    """The row-range direct fill trusts #nonzero cells == #nonzero-valued tuples: a duplicate
+    (row, k) cell that loses a nonzero value must send the guard to the fp32-scratch path,
+    zero-valued duplicates may not change a cell, so either way the result is the oracle's."""
+    if passes is not None:
+        monkeypatch.setenv("TCUDB_FILL_PASSES", passes)
+    rng = np.random.default_rng(11)
+    n = 96
+    cells = rng.permutation(n * n)
+    ag, ak = (cells // n).astype(np.int32), (cells % n).astype(np.int32)
+    av = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, n * n).astype(np.float32))
+    if case == "dup_nonzero":      # a second tuple in cell (ag[0], ak[0]) with another value
+        ag, ak, av = np.append(ag, ag[0]), np.append(ak, ak[0]), np.append(av, np.float32(0.5))
+    elif case == "dup_zero_after":  # ... with value 0, stored after the nonzero one
+        ag, ak, av = np.append(ag, ag[0]), np.append(ak, ak[0]), np.append(av, np.float32(0.0))
+    elif case == "zero_values":
+        av[::7] = 0.0
+    cells_b = rng.permutation(n * n)
+    bk, bh = (cells_b // n).astype(np.int32), (cells_b % n).astype(np.int32)
+    bw = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, n * n).astype(np.float32))
+    A, B = datagen.Table(ak, ag, av), datagen.Table(bk, bh, bw)
+    out, st = run(engine, torch_mod, A, B, "sum", flags=1)  # FORCE_DENSE: the fill under test
+    assert st["path"] == 0
+    compare(out, oracle_mod.join_agg(A, B, "sum"), "sum", float_vals=True)
