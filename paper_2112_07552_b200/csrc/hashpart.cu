@@ -27,7 +27,7 @@
 namespace tcudb {
 namespace {
 
-constexpr int PT = 1024;       // threads per partitioning block
+constexpr int PT = 512;        // threads per partitioning block (4 CTAs per SM)
 constexpr int CH = 4 * PT;     // tuples per partitioning chunk
 constexpr int kMaxDigits = 128;
 
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(PT) k_part_hist(const PassIO io) {
 }
 
 template <bool VAL>
-__global__ void __launch_bounds__(PT, 2) k_part_scatter(const PassIO io) {  // 2 x 1,024 threads per SM
+__global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io) {  // 2,048 threads per SM
   extern __shared__ __align__(16) uint8_t stage_raw[];
   unsigned long long* sk = reinterpret_cast<unsigned long long*>(stage_raw);  // [CH]
   int32_t* sg = reinterpret_cast<int32_t*>(sk + CH);                          // [CH]
