@@ -48,15 +48,40 @@ TCUDB_DEV int find_seg(const int64_t* __restrict__ chunk_start, int nseg, int64_
   return lo;
 }
 
-__global__ void k_chunk_starts(const int64_t* __restrict__ seg_off, int nseg, int64_t* __restrict__ chunk_start) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int64_t c = 0;
-    for (int s = 0; s < nseg; ++s) {
-      chunk_start[s] = c;
-      c += (seg_off[s + 1] - seg_off[s] + CH - 1) / CH;
-    }
-    chunk_start[nseg] = c;
+// one 1,024-thread block: each thread a contiguous run of segments, a block-wide scan of
+// the per-thread chunk totals (a single-thread loop cost ~7 us per pass)
+constexpr int kCsThreads = 1024;
+__global__ void __launch_bounds__(kCsThreads) k_chunk_starts(const int64_t* __restrict__ seg_off, int nseg,
+                                                            int64_t* __restrict__ chunk_start) {
+  __shared__ int64_t wsum[kCsThreads / 32];
+  const int per = (nseg + kCsThreads - 1) / kCsThreads;
+  const int s0 = threadIdx.x * per, s1 = min(nseg, s0 + per);
+  int64_t run = 0;
+  for (int s = s0; s < s1; ++s) run += (seg_off[s + 1] - seg_off[s] + CH - 1) / CH;
+  int64_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane_id() >= o) incl += t;
   }
+  if (lane_id() == 31) wsum[warp_id()] = incl;
+  __syncthreads();
+  if (warp_id() == 0) {
+    int64_t w = wsum[lane_id()], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane_id() >= o) wi += t;
+    }
+    wsum[lane_id()] = wi - w;  // exclusive prefix of the warp totals
+  }
+  __syncthreads();
+  int64_t c = wsum[warp_id()] + incl - run;
+  for (int s = s0; s < s1; ++s) {
+    chunk_start[s] = c;
+    c += (seg_off[s + 1] - seg_off[s] + CH - 1) / CH;
+  }
+  if (threadIdx.x == kCsThreads - 1) chunk_start[nseg] = c;
 }
 
 struct PassIO {
@@ -472,7 +497,7 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   io.k_out = k_out; io.g_out = g_out; io.seg_out = seg_out;
   io.v_raw = v_raw ? v_raw->data : nullptr; io.v_type = v_raw ? v_raw->type : 0;
   io.v_in = v_in; io.v_out = v_out;
-  k_chunk_starts<<<1, 32, 0, s>>>(seg_off, nseg, chunk_start);
+  k_chunk_starts<<<1, kCsThreads, 0, s>>>(seg_off, nseg, chunk_start);
   // unused count slots (chunks past the real total) must scan as zero
   cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cnts * 4, s);
   if (e != cudaSuccess) return e;
