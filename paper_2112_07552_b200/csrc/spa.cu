@@ -417,26 +417,26 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
       const long long gv = a.dict_g[g];
       T* arow = acc + (int64_t)r * ldc;
       for (int q = q0; q < q1; ++q) {
-        const int64_t wi = (int64_t)q * CW + lane;
-        unsigned m = (lane < CW && wi < W) ? rb[wi] : 0u;
+        // lane l takes half-word l & 1 of word l >> 1: all 32 lanes list set bits, at most 16 each
+        const int64_t wi = (int64_t)q * CW + (lane >> 1);
+        unsigned m = wi < W ? rb[wi] : 0u;
+        m = (lane & 1) ? (m >> 16) : (m & 0xFFFFu);
         const int cnt = __popc(m);
         int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < CW; o <<= 1) {
+        for (int o = 1; o < 32; o <<= 1) {
           const int t = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += t;
         }
-        const int total = __shfl_sync(0xffffffffu, incl, CW - 1);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total == 0) continue;
         int p = incl - cnt;
-        if (lane < CW) {
-          while (m) {
-            const int bb = __ffs(m) - 1;
-            stage[p++] = (uint16_t)(lane * 32 + bb);
-            m &= m - 1;
-          }
-          if (wi < W) rb[wi] = 0u;  // this word is consumed
+        while (m) {
+          const int bb = __ffs(m) - 1;
+          stage[p++] = (uint16_t)(lane * 16 + bb);
+          m &= m - 1;
         }
+        if (!(lane & 1) && wi < W) rb[wi] = 0u;  // this word is consumed (both halves were read above)
         __syncwarp();
         const int64_t hq = (int64_t)q * CW * 32;
         for (int j = lane; j < total; j += 32) {
