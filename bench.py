@@ -338,6 +338,9 @@ def main():
                 "frac": achieved / peak, "peak_sustained": peak_sus, "frac_of_sustained": achieved / peak_sus,
                 "peak_source": f"{peaks['source']} bf16 x {ratio:g} (nominal {kind.split()[0]}/bf16 ratio)",
                 "vs_int8_peak": achieved / int8_peak,
+                # B200 dense nominal (bf16 2.25 PF, int8 4.5 POPS, fp4 9 PF): frac above 1 only
+                # means the kernel reaches a larger share of ITS nominal than cuBLAS bf16 does
+                "nominal_peak": 2250.0 * ratio, "frac_of_nominal": achieved / (2250.0 * ratio),
                 "ops_per_launch": ops, "avg_launch_ms": g_ms,
                 "traffic": gemm_traffic_from_profiles(args.config, st["elem"])}
     elif st["ms_kernel"] > 0:
