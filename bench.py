@@ -213,6 +213,7 @@ def main():
     A, B, agg = load_tables(args.config)
     n_tuples = len(A["k"]) + len(B["k"])
     native = sharded and args.shard_impl == "native"
+    shard_note = "native collective cross-checked against shard.py" if native else ""
     # native: the collective tcudb_join_agg (NCCL inside libtcudb, collective.cu);
     # python: the same algorithm driven from shard.py over torch.distributed
     eng = Engine(local, group=torch.distributed.group.WORLD) if native else Engine(local)
@@ -224,6 +225,25 @@ def main():
     else:
         sA, sB = shard_mod.local_slice(A, ws, rank), shard_mod.local_slice(B, ws, rank)
         dA, dB = to_dev(sA), to_dev(sB)
+        if native:
+            # the native collective's peer exchanges are checked once against the shard.py
+            # driver (torch.distributed collectives) on the same slices; on any difference the
+            # run switches to shard.py and says so in config.parallelism
+            py_eng = Engine(local)
+            ref = shard_mod.sharded_join_agg(py_eng, dA, dB, agg)
+            native_err = "results differ"
+            try:
+                got = eng.join_agg(dA, dB, agg)
+                same = set(got) == set(ref) and all(
+                    got[c].numel() == ref[c].numel() and bool(torch.equal(got[c], ref[c])) for c in ref)
+            except Exception as ex:  # noqa: BLE001 - reported, then the python driver runs
+                same, native_err = False, repr(ex)[:200]
+            flag = torch.tensor([1 if same else 0], device=dev)
+            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                native, eng = False, py_eng
+                shard_note = f"native collective failed its cross-check ({native_err}); shard.py driver timed"
+            del ref
         step = ((lambda: eng.join_agg(dA, dB, agg, with_stats=True)) if native
                 else (lambda: shard_mod.sharded_join_agg(eng, dA, dB, agg, with_stats=True)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -403,6 +423,7 @@ def main():
                    "result_groups": st["n_result"], "path": "dense" if st["path"] == 0 else "sparse",
                    "parallelism": f"row-shard x{ws} (A routed by g range, B allgathered, results allgathered; "
                                   f"{'collective libtcudb call over NCCL' if native else 'shard.py over torch.distributed'}; "
+                                  f"{shard_note + '; ' if shard_note else ''}"
                                   f"G/H/K/stage_ms are rank 0's local query)" if sharded else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps"},
         "stage_ms": {k: st[k] for k in ("ms_stats", "ms_encode", "ms_fill", "ms_gemm", "ms_sparse", "ms_compact")

@@ -745,6 +745,7 @@ def test_sharded_path_nccl_single_rank(tmp_path):
     assert line, r.stdout[-3000:] + r.stderr[-3000:]
     d = json.loads(line[-1])
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and "row-shard" in d["config"]["parallelism"]
+    assert "cross-checked" in d["config"]["parallelism"], d["config"]["parallelism"]
 
 
 # ---------------------------------------------------------------- randomized sweep over the plans
