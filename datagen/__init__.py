@@ -224,6 +224,7 @@ CONFIGS = {
     "c2": "entity matching: 10k x 10k token-bag records, vocab 32k, shared-token COUNT",
     "c3": "graph query: 2-hop path count on R-MAT scale-16 edge table (self-join + group-by)",
     "c4": "matrix analytics: SQL matmul of two 8192x8192 (row,col,val) tables, SUM bf16",
+    "c4s": "c4 with signed fp32 N(0,1) values (not bf16-exact: the guard's hi/lo split)",
     "c5": "low-density join: 16M x 16M tuples over 4M-key domain, COUNT",
     "c5s": "c5 with SUM(A.v*B.w), v,w ~ U{-100..100}",
 }
@@ -243,9 +244,9 @@ def make_config(name, scale=1.0):
         sc = 16 if scale >= 1.0 else max(6, int(round(16 + np.log2(scale))))
         s, d = c3_graph_edges(scale=sc)
         A, B = c3_two_hop(s, d); return A, B, "count"
-    if name == "c4":
+    if name in ("c4", "c4s"):
         n = 8192 if scale >= 1.0 else max(16, int(8192 * np.sqrt(scale)))
-        A, B = c4_matrix(n=n); return A, B, "sum"
+        A, B = c4_matrix(n=n, signed=name == "c4s"); return A, B, "sum"
     if name in ("c5", "c5s"):
         n = int((1 << 24) * scale)
         kd = max(16, int((1 << 22) * scale))

@@ -142,6 +142,17 @@ __device__ __forceinline__ void epilogue_chunk(const KParams& p, const uint32_t*
       d2[i] = make_longlong2((long long)x0, (long long)x1);
       if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
     }
+  } else if (p.epi == EPI_SETF64 || p.epi == EPI_ACCF64) {
+    // fp32 accumulator of one K range -> fp64 C (the hi/lo split's partial products are
+    // accumulated in separate launches and summed here in fp64, R9)
+    double2* d2 = reinterpret_cast<double2*>(reinterpret_cast<double*>(p.C) + row * p.ldc + col);
+#pragma unroll
+    for (int i = 0; i < W / 2; ++i) {
+      double x0 = (double)__uint_as_float(r[2 * i]), x1 = (double)__uint_as_float(r[2 * i + 1]);
+      if (p.epi == EPI_ACCF64) { const double2 o = d2[i]; x0 += o.x; x1 += o.y; }
+      d2[i] = make_double2(x0, x1);
+      if (p.cnt_out) nzc += (x0 != 0.0) + (x1 != 0.0);
+    }
   } else {  // EPI_TRI
     if (row < p.mask_rows && col < p.mask_cols) {
       const uint4* m4 = reinterpret_cast<const uint4*>(p.mask + row * p.ldm + col);

@@ -17,7 +17,9 @@ enum GemmEpi {
   EPI_SET64 = 1,    // C64[r][c] = (int64)acc << shift
   EPI_ACC64 = 2,    // C64[r][c] += (int64)acc << shift
   EPI_TRI = 3,      // *tri_out += sum acc[r][c] * mask[r][c]   (triangle epilogue, a9)
-  EPI_STORE16 = 4   // C16[r][c] = (uint16)acc — COUNT results the guard proved < 2^16 (fp4 path)
+  EPI_STORE16 = 4,  // C16[r][c] = (uint16)acc — COUNT results the guard proved < 2^16 (fp4 path)
+  EPI_SETF64 = 5,   // C64f[r][c] = (double)acc        (bf16: one K range of the hi/lo split)
+  EPI_ACCF64 = 6    // C64f[r][c] += (double)acc       (float partials summed in fp64, DESIGN R9)
 };
 constexpr int kGemmBM = 128;
 constexpr int kGemmBN = 256;

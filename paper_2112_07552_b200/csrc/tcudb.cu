@@ -1020,6 +1020,31 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       ops += 2.0 * Gp * Hc * Kp4;
       ca.E = C; ca.e_kind = c16 ? 4 : 0; ca.lde = Hc; ca.V = C; ca.v_kind = ca.e_kind; ca.ldv = Hc;
       S.elem = 3;
+    } else if (is_float && S.elem == 2) {
+      // hi/lo split (operands laid along K as [hi|hi|lo|lo] · [hi|lo|hi|lo]): the hi·hi
+      // product and the three correction products accumulate in SEPARATE fp32 TMEM
+      // accumulators (separate launches) and are summed in fp64 by the epilogue. In one
+      // accumulator over K' = 4K the small correction terms were added to a sum already at
+      // full magnitude, where the tensor core's fp32 step loses their low bits
+      // (scripts/precision_probe.py, R9).
+      double* C = ar.get<double>(Gp * Hp);
+      static const int hh_env = getenv("TCUDB_SPLIT_HH_CHUNKS") ? atoi(getenv("TCUDB_SPLIT_HH_CHUNKS")) : 0;
+      const int hh_chunks = std::max(1, hh_env > 0 ? hh_env : 1);
+      const int64_t hh_step = round_up((Kp + hh_chunks - 1) / hh_chunks, 64);
+      ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop; ga.C = C; ga.ldc = Hp;
+      bool first = true;
+      for (int64_t k0 = 0; k0 < Kp; k0 += hh_step) {
+        ga.k_begin = k0; ga.k_len = std::min(hh_step, Kp - k0);
+        ga.epi = first ? EPI_SETF64 : EPI_ACCF64; ga.cnt_out = nullptr;
+        CK(launch_gemm(ga, s, L));
+        ops += 2.0 * Gp * Hp * ga.k_len;
+        first = false;
+      }
+      ga.k_begin = Kp; ga.k_len = 3 * Kp; ga.epi = EPI_ACCF64;
+      ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
+      CK(launch_gemm(ga, s, L));
+      ops += 2.0 * Gp * Hp * 3 * Kp;
+      ca.E = C; ca.e_kind = 3; ca.lde = Hp; ca.V = C; ca.v_kind = 3; ca.ldv = Hp;
     } else if (is_float) {
       float* C = ar.get<float>(Gp * Hp);
       ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop;

@@ -17,6 +17,8 @@ KEEP = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sectors_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_red.sum",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_op_tcgen05_mma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_mio_throttle",
         "smsp__pcsamp_warps_issue_stalled_lg_throttle", "smsp__pcsamp_warps_issue_stalled_barrier",
         "smsp__pcsamp_warps_issue_stalled_short_scoreboard", "smsp__pcsamp_warps_issue_stalled_membar"]
@@ -36,7 +38,7 @@ def main():
             d = dict(zip(hdr, row))
             u = dict(zip(hdr, units))
             lines.append(f"== {rep.split('/')[-1]} {d.get('Kernel Name', '')[:90]}")
-            for m in KEEP:
+            for m in KEEP + sorted(k for k in d if "pipe_tensor" in k and k not in KEEP):
                 if m in d:
                     lines.append(f"   {m:<80s} {d[m]} {u.get(m, '')}")
     open(out, "w").write("\n".join(lines) + "\n")

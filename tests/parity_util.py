@@ -1,14 +1,14 @@
 """Helpers shared by the GPU parity tests: table transfer and result comparison.
 
 Tolerance for float SUM (reading R9, from the north star's "1e-3
-relative"): |x_gpu - x| <= 1e-3 * max(|x|, 0.1 * S_abs), S_abs = sum |v*w| of
+relative"): |x_gpu - x| <= 1e-3 * max(|x|, 0.01 * S_abs), S_abs = sum |v*w| of
 the group (computed by the oracle). Integer results: bit-exact. Group sets and
 order: identical (existence = COUNT > 0, ascending (g, h)).
 """
 import numpy as np
 
 FLOAT_RTOL = 1e-3
-FLOOR = 0.1  # DESIGN.md R9: the dense float path's error is ~1e-5 S_abs (split + fp32 accumulation)
+FLOOR = 0.01  # DESIGN.md R9 = SURVEY §8(c) #9: the floor is 1e-5 S_abs (cancellation only)
 
 
 def to_dev(T, torch, device="cuda:0"):
