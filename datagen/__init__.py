@@ -217,6 +217,15 @@ def random_tiny(rng, n_max=64, k_max=16, g_max=8, vkind="none", vmin=-5, vmax=5,
             Table(kb.astype(key_dtype), hb.astype(np.int64), vals(nb)))
 
 
+# --------------------------------------------------------------------------- placement
+def local_slice(T, ws, rank):
+    """Contiguous 1/ws slice of a host table (numpy columns): rank r's starting data in
+    the multi-GPU runs."""
+    n = len(T["k"])
+    lo, hi = n * rank // ws, n * (rank + 1) // ws
+    return {k: (None if v is None else np.ascontiguousarray(v[lo:hi])) for k, v in T.items()}
+
+
 # --------------------------------------------------------------------------- registry
 CONFIGS = {
     "c1": "COUNT(*) natural join of two 1,000-row int tables on 64 distinct keys, 32x32 groups",

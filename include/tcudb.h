@@ -135,9 +135,15 @@ typedef void (*tcudb_free_fn)(void* ptr, void* stream, void* user);
  * that side's rows are routed to their owners (all-to-all-v), the other side is
  * allgathered, each rank runs the local query, and the result is allgathered in rank
  * order — on every rank identical to the single-GPU result — or, with
- * TCUDB_GATHER_NONE, left as the rank's (g, h)-sorted shard. Without GROUP BY (Q4)
- * the per-rank partial aggregates are combined with allreduces. NCCL (libnccl.so.2,
- * the process's own) is resolved here with dlopen. Exchange failures: E_COMM.
+ * TCUDB_GATHER_NONE, left as the rank's (g, h)-sorted shard. Ranges are balanced on the
+ * routed side's rows (weighted quantiles of an allgathered sample, tcudb_shard_bounds).
+ * Without GROUP BY (Q4) the per-rank partial aggregates are allgathered and combined
+ * exactly (an int64 total overflow is E_OVERFLOW). The ranks first agree on the query
+ * shape (tcudb_shard_agree): a rank with an empty slice may pass NULL columns; argument
+ * errors and every later local failure are agreed on (the same status on every rank, no
+ * rank left waiting in a collective). NCCL (libnccl.so.2, the process's own; or the
+ * library named by the environment variable TCUDB_NCCL_LIB) is resolved here with
+ * dlopen. Exchange failures: E_COMM.
  * Returns E_CUDA if the device is not sm_100 or the CUDA runtime fails, E_COMM if
  * the communicator is unusable. */
 tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_alloc_fn alloc_fn,
@@ -213,6 +219,29 @@ tcudb_status tcudb_minmax(tcudb_ctx* ctx, const void* col, int32_t type, int64_t
                           void* stream);
 tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_t* bounds, int32_t P,
                              tcudb_table* out, int64_t* counts, void* stream);
+
+/* Host-only planning steps of the collective call (§8(e)), exported so that the shard
+ * plan can be checked without a GPU (pure host code: no device work, no communicator).
+ *
+ * tcudb_shard_agree: the agreement step. descs: P rank descriptors of
+ * TCUDB_SHARD_DESC_LEN int64 each, rank-major: [0] A.n_rows, [1] B.n_rows, [2..7] column
+ * states of A.key, A.group, A.value, B.key, B.group, B.value (0: no rows and a NULL
+ * pointer — no vote; 1: absent; 2 + tcudb_dtype: present), [8] agg, [9] flags, [10] the
+ * rank's own argument status. Writes the agreed descriptor (row totals, voted column
+ * states — a column nobody votes on is absent —, agg, flags, status) into agreed[] and
+ * returns its status: the most negative rank status, E_INVALID when ranks disagree on a
+ * column, agg or flags, E_UNSUPPORTED for non-integer keys / groups or mixed int / float
+ * values. Every rank calling it on the same allgathered bytes gets the same answer.
+ *
+ * tcudb_shard_bounds: the range-bound step. msgs: P messages of TCUDB_SHARD_SAMPLES + 2
+ * int64, rank-major: [0] the rank's routed rows n, [1] its sample size S <= 1024, [2..]
+ * S group values sampled at stride n / S. Writes the P-1 ascending bounds (rows go to
+ * rank #{i : bounds[i] <= g}) at the weighted quantiles i·N/P of the pooled sample (each
+ * sample weighs n / S rows); a value is never split across ranks. */
+#define TCUDB_SHARD_DESC_LEN 11
+#define TCUDB_SHARD_SAMPLES 1024
+tcudb_status tcudb_shard_agree(const int64_t* descs, int32_t P, int64_t* agreed);
+tcudb_status tcudb_shard_bounds(const int64_t* msgs, int32_t P, int64_t* bounds);
 
 void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r);
 void tcudb_result_free_host(tcudb_ctx* ctx, tcudb_result* r);

@@ -28,7 +28,9 @@ FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE, NO_FP4 = 1, 2, 4,
 EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_chain_join_agg",
                   "tcudb_triangle_count", "tcudb_gemm",
                   "tcudb_minmax", "tcudb_partition", "tcudb_result_free", "tcudb_result_free_host",
-                  "tcudb_last_error", "tcudb_launch_count", "tcudb_destroy"])
+                  "tcudb_last_error", "tcudb_launch_count", "tcudb_destroy", "tcudb_shard_agree",
+                  "tcudb_shard_bounds"])
+SHARD_DESC_LEN, SHARD_SAMPLES = 11, 1024
 
 
 class TcudbError(RuntimeError):
@@ -120,6 +122,11 @@ def load(build_if_missing: bool = True):
     lib.tcudb_launch_count.argtypes = [P]
     lib.tcudb_launch_count.restype = ctypes.c_int64
     lib.tcudb_destroy.argtypes = [P]
+    I64P = ctypes.POINTER(ctypes.c_int64)
+    lib.tcudb_shard_agree.argtypes = [I64P, ctypes.c_int32, I64P]
+    lib.tcudb_shard_agree.restype = ctypes.c_int
+    lib.tcudb_shard_bounds.argtypes = [I64P, ctypes.c_int32, I64P]
+    lib.tcudb_shard_bounds.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -193,6 +200,44 @@ class _DevArray:
                                          "stream": None}
 
 
+def shard_agree(descs):
+    """tcudb_shard_agree (host only): descs = P rank descriptors (SHARD_DESC_LEN int64 each)
+    -> (status, agreed descriptor)."""
+    lib = load()
+    d = np.ascontiguousarray(np.asarray(descs, dtype=np.int64).reshape(-1, SHARD_DESC_LEN))
+    out = np.zeros(SHARD_DESC_LEN, dtype=np.int64)
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    st = lib.tcudb_shard_agree(d.ctypes.data_as(p64), d.shape[0], out.ctypes.data_as(p64))
+    return int(st), out
+
+
+def shard_bounds(msgs):
+    """tcudb_shard_bounds (host only): msgs = P sample messages (SHARD_SAMPLES + 2 int64
+    each: n, S, S values) -> the P-1 range bounds."""
+    lib = load()
+    m = np.ascontiguousarray(np.asarray(msgs, dtype=np.int64).reshape(-1, SHARD_SAMPLES + 2))
+    P = m.shape[0]
+    out = np.zeros(max(P - 1, 1), dtype=np.int64)
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    st = lib.tcudb_shard_bounds(m.ctypes.data_as(p64), P, out.ctypes.data_as(p64))
+    if st != TCUDB_OK:
+        raise TcudbError(st, "tcudb_shard_bounds")
+    return out[:P - 1].tolist()
+
+
+def shard_sample_msg(g):
+    """The sample message one rank contributes (host mirror of collective.cu's strided
+    sample: S = min(n, SHARD_SAMPLES) values at stride n // S)."""
+    g = np.asarray(g, dtype=np.int64)
+    n = len(g)
+    S = min(n, SHARD_SAMPLES)
+    m = np.zeros(SHARD_SAMPLES + 2, dtype=np.int64)
+    m[0], m[1] = n, S
+    if S:
+        m[2:2 + S] = g[::n // S][:S]
+    return m
+
+
 def nccl_comm_ptr(group, device: int) -> int:
     """The ncclComm_t of a torch.distributed NCCL process group on `device` (created
     eagerly by one tiny collective: ProcessGroupNCCL builds communicators lazily)."""
@@ -214,10 +259,12 @@ def nccl_comm_ptr(group, device: int) -> int:
 class Engine:
     """One tcudb context on one CUDA device (sm_100a)."""
 
-    def __init__(self, device: int = 0, group=None):
+    def __init__(self, device: int = 0, group=None, comm=None):
         """group: None (single GPU), or a torch.distributed NCCL process group (e.g.
         torch.distributed.group.WORLD) — then join_agg / join_agg_host are collective over
-        its ranks (one GPU per rank; see tcudb_create in include/tcudb.h)."""
+        its ranks (one GPU per rank; see tcudb_create in include/tcudb.h). comm: a raw
+        communicator pointer instead of a group (an ncclComm_t, or a communicator of the
+        library named by TCUDB_NCCL_LIB)."""
         import torch
         self._torch = torch
         self._lib = load()
@@ -225,13 +272,16 @@ class Engine:
         torch.cuda.init()
         self._alloc_cb = ALLOC_FN(self._alloc)
         self._free_cb = FREE_FN(self._free)
-        comm = None if group is None else ctypes.c_void_p(nccl_comm_ptr(group, self.device))
+        if comm is not None:
+            comm = ctypes.c_void_p(int(comm))
+        elif group is not None:
+            comm = ctypes.c_void_p(nccl_comm_ptr(group, self.device))
         ctx = ctypes.c_void_p()
         st = self._lib.tcudb_create(ctypes.byref(ctx), self.device, comm, self._alloc_cb, self._free_cb, None)
         if st != TCUDB_OK:
             raise TcudbError(st, "tcudb_create failed (needs an sm_100 GPU; with a group: a usable NCCL communicator)")
         self._ctx = ctx
-        self.collective = group is not None
+        self.collective = comm is not None
 
     # allocator callbacks -> torch caching allocator (torch owns result memory)
     def _alloc(self, nbytes, stream, user):

@@ -66,5 +66,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+SHIM_SRC = os.path.join(os.path.dirname(HERE), "tests", "nccl_shim", "nccl_shim.cpp")
+SHIM_LIB = os.path.join(os.path.dirname(HERE), "tests", "nccl_shim", "libnccl_shim.so")
+
+
+def build_shim(force: bool = False) -> str:
+    """Test infrastructure: the in-process communicator (tests/nccl_shim) that lets the
+    collective path run P ranks as P threads on one GPU (selected by TCUDB_NCCL_LIB)."""
+    if not force and os.path.exists(SHIM_LIB) and os.path.getmtime(SHIM_LIB) >= os.path.getmtime(SHIM_SRC):
+        return SHIM_LIB
+    tmp = SHIM_LIB + f".tmp{os.getpid()}"
+    cmd = [NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-o", tmp, SHIM_SRC]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"shim build failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, SHIM_LIB)
+    return SHIM_LIB
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_shim(force="--force" in sys.argv))

@@ -5,8 +5,13 @@
 // Output rows are independent units (§3.2: C[g][h] depends only on A's rows of
 // group g and B's rows of group h), so they are sharded by ranges of the grouped side's
 // group key and the only exchanges are data movement:
-//   1. global [min, max] of the routed side's group column (two allreduces) -> P
-//      equal-width ranges, rank r owning the r-th;
+//   0. agreement: every rank's query shape (rows, column presence and types, aggregate,
+//      flags, its local argument check) is allgathered and one decision is taken from the
+//      same bytes on every rank — a rank whose slice is empty (NULL columns) takes the
+//      others' shape; a disagreement fails on every rank with the same status;
+//   1. range bounds balanced on rows (§8(e) step 2): each rank allgathers a strided sample
+//      of its routed group column (<= 1024 values + its row count); every rank computes
+//      the same P-1 weighted quantiles of the pooled sample;
 //   2. the routed side's rows are sent to the rank owning their group (tcudb_partition +
 //      all-to-all-v as grouped ncclSend / ncclRecv);
 //   3. the other side is allgathered (allgather-v as grouped send / recv);
@@ -17,21 +22,27 @@
 //      TCUDB_GATHER_NONE returns the rank's shard instead.
 // Routed side: A (by A.g) when A is grouped; GROUP BY B.h only (Q3) routes B
 // by h. No GROUP BY (Q4): every rank joins its own A slice with the gathered
-// B and the per-rank partial aggregates are combined with allreduces (AVG = the reduced
-// SUM / the reduced COUNT, divided on the device).
+// B and the per-rank partial aggregates are allgathered and combined exactly (int SUM in
+// 128 bits: a total beyond int64 is E_OVERFLOW on every rank, as on one GPU).
+// Every local step that can fail (partition, local query) is followed by an agreement on
+// the status (allreduce MIN) before the next exchange, so one rank's error is every
+// rank's error instead of a peer blocked in a collective.
 //
 // NCCL is resolved at context creation with dlopen (the process's already-loaded
-// libnccl.so.2 — torch's — first), so a library used without a communicator has no NCCL
-// dependency. The communicator is owned by the caller.
+// libnccl.so.2 — torch's — first; TCUDB_NCCL_LIB names another library implementing the
+// same symbols, e.g. the tests' in-process communicator), so a library used without a
+// communicator has no NCCL dependency. The communicator is owned by the caller.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
-#include <memory>
-#include <type_traits>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/tcudb.h"
@@ -42,8 +53,14 @@ namespace tcudb {
 namespace {
 
 // NCCL's stable ABI values (nccl.h): data types and reduction ops used here
-constexpr int kNcclInt8 = 0, kNcclInt64 = 4, kNcclFloat64 = 8;
-constexpr int kNcclSum = 0, kNcclMax = 2, kNcclMin = 3;
+constexpr int kNcclInt8 = 0, kNcclInt64 = 4;
+constexpr int kNcclMin = 3;
+
+// query-shape descriptor (one per rank, allgathered): n_A, n_B, six column states
+// (A.key, A.group, A.value, B.key, B.group, B.value), agg, flags, local argument status
+constexpr int kDesc = TCUDB_SHARD_DESC_LEN;
+constexpr int kSamples = TCUDB_SHARD_SAMPLES;
+constexpr int kSampleMsg = kSamples + 2;
 
 struct CommError {
   std::string what;
@@ -70,6 +87,13 @@ void ck(cudaError_t e, const char* what) {
 
 size_t type_bytes(int32_t t) { return (t == TCUDB_I64 || t == TCUDB_F64) ? 8 : 4; }
 
+// 0: no vote (no rows, no pointer: present-but-empty and absent look alike), 1: absent,
+// 2 + type: present
+int64_t col_state(const tcudb_col& c, int64_t n) {
+  if (!c.data) return n == 0 ? 0 : 1;
+  return 2 + (int64_t)c.type;
+}
+
 }  // namespace
 
 struct NcclComm {
@@ -88,15 +112,28 @@ struct NcclComm {
   void nck(int r, const char* what) const {
     if (r != 0) throw CommError{std::string(what) + ": " + (ErrStr ? ErrStr(r) : "NCCL error")};
   }
-  // allgather of one int64 per rank, read back on the host
-  std::vector<int64_t> gather_i64(int64_t x, cudaStream_t s) const {
-    DevBuf d(sizeof(int64_t) * (nranks + 1), s);
-    ck(cudaMemcpyAsync(d.as<int64_t>() + nranks, &x, sizeof(int64_t), cudaMemcpyHostToDevice, s), "H2D");
-    nck(AllGather(d.as<int64_t>() + nranks, d.as<int64_t>(), 1, kNcclInt64, comm, s), "ncclAllGather");
-    std::vector<int64_t> h(nranks);
-    ck(cudaMemcpyAsync(h.data(), d.p, sizeof(int64_t) * nranks, cudaMemcpyDeviceToHost, s), "D2H");
+  // allgather of m int64 per rank, read back on the host (rank-major)
+  std::vector<int64_t> gather_vec(const int64_t* x, int m, cudaStream_t s) const {
+    DevBuf d(sizeof(int64_t) * (size_t)m * (nranks + 1), s);
+    int64_t* mine = d.as<int64_t>() + (size_t)m * nranks;
+    ck(cudaMemcpyAsync(mine, x, sizeof(int64_t) * m, cudaMemcpyHostToDevice, s), "H2D");
+    nck(AllGather(mine, d.as<int64_t>(), (size_t)m, kNcclInt64, comm, s), "ncclAllGather");
+    std::vector<int64_t> h((size_t)m * nranks);
+    ck(cudaMemcpyAsync(h.data(), d.p, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
     return h;
+  }
+  std::vector<int64_t> gather_i64(int64_t x, cudaStream_t s) const { return gather_vec(&x, 1, s); }
+  // every rank's status -> the same status on every rank (MIN: any error wins)
+  tcudb_status agree(tcudb_status st, cudaStream_t s) const {
+    DevBuf d(8, s);
+    const int64_t v = (int64_t)st;
+    ck(cudaMemcpyAsync(d.p, &v, 8, cudaMemcpyHostToDevice, s), "H2D");
+    nck(AllReduce(d.p, d.p, 1, kNcclInt64, kNcclMin, comm, s), "ncclAllReduce");
+    int64_t r = 0;
+    ck(cudaMemcpyAsync(&r, d.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    return (tcudb_status)r;
   }
   // grouped point-to-point exchange: send[j] bytes at soff[j] of src to rank j, recv[j]
   // bytes from rank j at roff[j] of dst (the rank's own part is a device copy)
@@ -115,9 +152,15 @@ struct NcclComm {
 };
 
 NcclComm* nccl_attach(void* comm, std::string* err) {
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's NCCL (torch's)
-  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) { *err = "libnccl.so.2 not found"; return nullptr; }
+  const char* alt = getenv("TCUDB_NCCL_LIB");  // another implementation of the NCCL symbols
+  void* h = nullptr;
+  if (alt && alt[0]) {
+    h = dlopen(alt, RTLD_NOW | RTLD_LOCAL);
+  } else {
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's NCCL (torch's)
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) { *err = "NCCL library not found"; return nullptr; }
   NcclComm* c = new NcclComm();
   c->comm = comm;
   bool ok = true;
@@ -145,16 +188,81 @@ NcclComm* nccl_attach(void* comm, std::string* err) {
 
 void nccl_detach(NcclComm* c) { delete c; }
 
-namespace {
-
-// P-1 ascending bounds splitting [lo, hi] into P equal-width ranges (exact in 128 bits)
-std::vector<int64_t> range_bounds(int64_t lo, int64_t hi, int P) {
-  std::vector<int64_t> b(P > 1 ? P - 1 : 0, 0);
-  if (lo > hi) return b;
-  const __int128 span = (__int128)hi - lo + 1;
-  for (int i = 1; i < P; ++i) b[i - 1] = (int64_t)(lo + span * i / P);
-  return b;
+// ---------------------------------------------------------------- host-only planning
+tcudb_status shard_agree(const int64_t* descs, int P, int64_t* agreed) {
+  std::memset(agreed, 0, sizeof(int64_t) * kDesc);
+  if (P < 1) return TCUDB_E_INVALID;
+  tcudb_status st = TCUDB_OK;
+  for (int r = 0; r < P; ++r) {
+    const int64_t* d = descs + (size_t)r * kDesc;
+    agreed[0] += d[0];
+    agreed[1] += d[1];
+    st = std::min(st, (tcudb_status)d[10]);
+    if (d[8] != descs[8] || d[9] != descs[9]) st = std::min(st, TCUDB_E_INVALID);  // agg / flags differ
+  }
+  agreed[8] = descs[8];
+  agreed[9] = descs[9];
+  for (int c = 0; c < 6; ++c) {
+    int64_t v = 0;
+    for (int r = 0; r < P; ++r) {
+      const int64_t x = descs[(size_t)r * kDesc + 2 + c];
+      if (x == 0) continue;
+      if (v == 0) v = x;
+      else if (v != x) st = std::min(st, TCUDB_E_INVALID);  // present on one rank, absent / other type on another
+    }
+    agreed[2 + c] = v == 0 ? 1 : v;
+  }
+  const bool vals = agreed[8] != TCUDB_COUNT;
+  for (int side = 0; side < 2; ++side) {
+    const int64_t* t = agreed + 2 + 3 * side;
+    const int64_t n = agreed[side];
+    if (n > 0 && t[0] < 2) st = std::min(st, TCUDB_E_INVALID);  // rows without a key column
+    auto int_t = [](int64_t x) { return x == 2 + TCUDB_I32 || x == 2 + TCUDB_I64; };
+    if ((t[0] >= 2 && !int_t(t[0])) || (t[1] >= 2 && !int_t(t[1]))) st = std::min(st, TCUDB_E_UNSUPPORTED);
+    if (vals && t[2] >= 2 && !int_t(t[2]) && t[2] != 2 + TCUDB_F32) st = std::min(st, TCUDB_E_UNSUPPORTED);
+  }
+  if (vals && agreed[4] >= 2 && agreed[7] >= 2 && ((agreed[4] == 2 + TCUDB_F32) != (agreed[7] == 2 + TCUDB_F32)))
+    st = std::min(st, TCUDB_E_UNSUPPORTED);  // mixed integer / float values
+  agreed[10] = st;
+  return st;
 }
+
+void shard_bounds(const int64_t* msgs, int P, int64_t* bounds) {
+  struct Smp { int64_t v; double w; };
+  std::vector<Smp> all;
+  double W = 0;
+  int64_t vmax = INT64_MIN;
+  for (int r = 0; r < P; ++r) {
+    const int64_t* m = msgs + (size_t)r * kSampleMsg;
+    const int64_t n = m[0], S = std::min<int64_t>(m[1], kSamples);
+    if (n <= 0 || S <= 0) continue;
+    const double w = (double)n / (double)S;  // each sample stands for n / S rows
+    for (int64_t i = 0; i < S; ++i) { all.push_back({m[2 + i], w}); vmax = std::max(vmax, m[2 + i]); }
+    W += (double)n;
+  }
+  std::sort(all.begin(), all.end(), [](const Smp& a, const Smp& b) { return a.v < b.v; });
+  // bound i = the smallest sampled value whose preceding weight reaches i·W/P (ties of a
+  // value stay on one rank: rows go to #{i : bounds[i] <= g})
+  size_t j = 0;
+  double cum = 0;
+  int64_t prev = INT64_MIN;
+  for (int i = 1; i < P; ++i) {
+    const double target = W * (double)i / (double)P;
+    while (j < all.size() && cum + 1e-9 * W < target) {
+      const int64_t v = all[j].v;
+      while (j < all.size() && all[j].v == v) cum += all[j++].w;  // whole value
+    }
+    int64_t b;
+    if (all.empty()) b = 0;
+    else if (j < all.size()) b = all[j].v;
+    else b = vmax == INT64_MAX ? INT64_MAX : vmax + 1;
+    b = std::max(b, prev);
+    bounds[i - 1] = b;
+    prev = b;
+  }
+}
+
+namespace {
 
 struct Cols {  // device columns of one table owned by this file
   std::vector<std::unique_ptr<DevBuf>> bufs;
@@ -172,7 +280,7 @@ void gather_table(const NcclComm& nc, const tcudb_table& T, Cols& out, cudaStrea
   const tcudb_col* in[3] = {&T.key, &T.group, &T.value};
   tcudb_col* dst[3] = {&out.t.key, &out.t.group, &out.t.value};
   for (int c = 0; c < 3; ++c) {
-    if (!in[c]->data) continue;
+    if (!in[c]->data) continue;  // absent on every rank (normalized presence)
     const size_t e = type_bytes(in[c]->type);
     out.bufs.emplace_back(new DevBuf((size_t)tot * e, s));
     std::vector<size_t> send(nc.nranks, (size_t)T.n_rows * e), soff(nc.nranks, 0), recv(nc.nranks), roff(nc.nranks);
@@ -182,24 +290,38 @@ void gather_table(const NcclComm& nc, const tcudb_table& T, Cols& out, cudaStrea
   }
 }
 
+// balanced bounds of the routed group column: strided sample -> allgather -> quantiles
+std::vector<int64_t> balanced_bounds(const NcclComm& nc, const tcudb_table& T, cudaStream_t s) {
+  std::vector<int64_t> msg(kSampleMsg, 0);
+  const int64_t n = T.n_rows;
+  const int64_t S = std::min<int64_t>(n, kSamples);
+  msg[0] = n;
+  msg[1] = S;
+  if (S > 0) {
+    const size_t e = type_bytes(T.group.type);
+    const int64_t stride = n / S;  // >= 1; samples i*stride, i < S
+    std::vector<int32_t> h32;
+    if (e == 8) {
+      ck(cudaMemcpy2DAsync(msg.data() + 2, 8, T.group.data, (size_t)stride * 8, 8, (size_t)S, cudaMemcpyDeviceToHost,
+                           s), "sample D2H");
+    } else {
+      h32.resize(S);
+      ck(cudaMemcpy2DAsync(h32.data(), 4, T.group.data, (size_t)stride * 4, 4, (size_t)S, cudaMemcpyDeviceToHost, s),
+         "sample D2H");
+    }
+    ck(cudaStreamSynchronize(s), "sync");
+    for (int64_t i = 0; i < (int64_t)h32.size(); ++i) msg[2 + i] = h32[i];
+  }
+  const std::vector<int64_t> all = nc.gather_vec(msg.data(), kSampleMsg, s);
+  std::vector<int64_t> b(nc.nranks > 1 ? nc.nranks - 1 : 1, 0);
+  shard_bounds(all.data(), nc.nranks, b.data());
+  return b;
+}
+
 // route the rows of T to the rank owning their group range
 tcudb_status route_table(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& T, Cols& out, cudaStream_t s) {
   const int P = nc.nranks;
-  int64_t mn, mx;
-  tcudb_status st = tcudb_minmax(ctx, T.group.data, T.group.type, T.n_rows, &mn, &mx, s);
-  if (st != TCUDB_OK) return st;
-  DevBuf r(16, s);
-  const int64_t h2[2] = {mn, mx};
-  ck(cudaMemcpyAsync(r.p, h2, 16, cudaMemcpyHostToDevice, s), "H2D");
-  nc.nck(nc.GroupStart(), "ncclGroupStart");
-  nc.nck(nc.AllReduce(r.as<int64_t>(), r.as<int64_t>(), 1, kNcclInt64, kNcclMin, nc.comm, s), "ncclAllReduce");
-  nc.nck(nc.AllReduce(r.as<int64_t>() + 1, r.as<int64_t>() + 1, 1, kNcclInt64, kNcclMax, nc.comm, s),
-         "ncclAllReduce");
-  nc.nck(nc.GroupEnd(), "ncclGroupEnd");
-  int64_t g2[2];
-  ck(cudaMemcpyAsync(g2, r.p, 16, cudaMemcpyDeviceToHost, s), "D2H");
-  ck(cudaStreamSynchronize(s), "sync");
-  const std::vector<int64_t> bounds = range_bounds(g2[0], g2[1], P);
+  const std::vector<int64_t> bounds = balanced_bounds(nc, T, s);
   // partition locally
   Cols part;
   part.t = T;
@@ -211,18 +333,11 @@ tcudb_status route_table(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& 
     pc[c]->data = part.bufs.back()->p;
   }
   std::vector<int64_t> counts(P, 0);
-  st = tcudb_partition(ctx, &T, bounds.data(), P, &part.t, counts.data(), s);
+  tcudb_status st = tcudb_partition(ctx, &T, bounds.data(), P, &part.t, counts.data(), s);
+  st = nc.agree(st, s);
   if (st != TCUDB_OK) return st;
   // P x P counts: row j = what rank j sends to each rank
-  std::vector<int64_t> M(P * P);
-  {
-    DevBuf d(sizeof(int64_t) * P * (P + 1), s);
-    ck(cudaMemcpyAsync(d.as<int64_t>() + P * P, counts.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, s),
-       "H2D");
-    nc.nck(nc.AllGather(d.as<int64_t>() + P * P, d.as<int64_t>(), P, kNcclInt64, nc.comm, s), "ncclAllGather");
-    ck(cudaMemcpyAsync(M.data(), d.p, sizeof(int64_t) * P * P, cudaMemcpyDeviceToHost, s), "D2H");
-    ck(cudaStreamSynchronize(s), "sync");
-  }
+  const std::vector<int64_t> M = nc.gather_vec(counts.data(), P, s);
   int64_t tot = 0;
   std::vector<int64_t> rc(P), roffr(P), soffr(P);
   int64_t srun = 0;
@@ -246,28 +361,30 @@ tcudb_status route_table(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& 
   return TCUDB_OK;
 }
 
-// allgather-v of a local result into one result allocation (g | h | agg, 256-B aligned)
-void gather_result(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_result& loc, tcudb_result* out, cudaStream_t s) {
+// allgather-v of a local result into one result allocation (g | h | agg, 256-B aligned);
+// which columns exist comes from the agreed query shape, never from local pointers (an
+// empty local result has NULL arrays)
+void gather_result(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_result& loc, const bool has[3],
+                   const int32_t ty[3], tcudb_result* out, cudaStream_t s) {
   const std::vector<int64_t> n = nc.gather_i64(loc.n, s);
   int64_t tot = 0;
   std::vector<int64_t> off(nc.nranks);
   for (int j = 0; j < nc.nranks; ++j) { off[j] = tot; tot += n[j]; }
-  void* src[3] = {loc.g, loc.h, loc.agg};
-  const int32_t ty[3] = {loc.g_type, loc.h_type, loc.agg_type};
+  const void* src[3] = {loc.g, loc.h, loc.agg};
   size_t at[3], run = 0;
   for (int c = 0; c < 3; ++c) {
     at[c] = run;
-    if (src[c] || c == 2) run += ((size_t)tot * type_bytes(ty[c]) + 255) / 256 * 256;
+    if (has[c]) run += ((size_t)tot * type_bytes(ty[c]) + 255) / 256 * 256;
   }
   char* base = static_cast<char*>(internal_result_alloc(ctx, run, s));
   *out = tcudb_result{};
   out->n = tot;
-  out->g_type = loc.g_type; out->h_type = loc.h_type; out->agg_type = loc.agg_type;
+  out->g_type = ty[0]; out->h_type = ty[1]; out->agg_type = ty[2];
   out->base = base;
   void** dst[3] = {&out->g, &out->h, &out->agg};
   try {
     for (int c = 0; c < 3; ++c) {
-      if (!src[c] && c != 2) continue;
+      if (!has[c]) continue;
       const size_t e = type_bytes(ty[c]);
       *dst[c] = base + at[c];
       std::vector<size_t> send(nc.nranks, (size_t)loc.n * e), soff(nc.nranks, 0), recv(nc.nranks), roff(nc.nranks);
@@ -282,52 +399,61 @@ void gather_result(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_result& loc, 
   }
 }
 
-// Q4: partial aggregate per rank, combined with allreduces
+// Q4: partial aggregate per rank, allgathered and combined exactly
 tcudb_status q4(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table* A, const tcudb_table* B,
-                const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, cudaStream_t s) {
+                const tcudb_query* q, bool fsum, tcudb_result* out, tcudb_stats* stats, cudaStream_t s) {
   Cols Bf;
   gather_table(nc, *B, Bf, s);
-  const bool fsum = q->agg != TCUDB_COUNT && ((A->value.data && A->value.type == TCUDB_F32) ||
-                                              (B->value.data && B->value.type == TCUDB_F32));
   tcudb_query qa = *q;
   if (q->agg == TCUDB_AVG) qa.agg = TCUDB_SUM;
   tcudb_result r{}, rc{};
-  tcudb_status st = tcudb_join_agg(ctx, A, &Bf.t, &qa, &r, stats, s);
-  if (st != TCUDB_OK) return st;
   struct RF { tcudb_ctx* c; tcudb_result* r; ~RF() { tcudb_result_free(c, r); } } f1{ctx, &r}, f2{ctx, &rc};
-  if (q->agg == TCUDB_AVG) {
+  tcudb_status st = tcudb_join_agg(ctx, A, &Bf.t, &qa, &r, stats, s);
+  if (st == TCUDB_OK && q->agg == TCUDB_AVG) {
     tcudb_query qc = *q;
     qc.agg = TCUDB_COUNT;
     st = tcudb_join_agg(ctx, A, &Bf.t, &qc, &rc, nullptr, s);
-    if (st != TCUDB_OK) return st;
   }
-  // [0] rows present, [1] the aggregate (int64 or fp64 bits), [2] COUNT (AVG)
-  DevBuf d(24, s);
-  ck(cudaMemsetAsync(d.p, 0, 24, s), "memset");
-  const int64_t has = r.n;
-  ck(cudaMemcpyAsync(d.p, &has, 8, cudaMemcpyHostToDevice, s), "H2D");
-  if (r.n) ck(cudaMemcpyAsync(d.as<char>() + 8, r.agg, 8, cudaMemcpyDeviceToDevice, s), "D2D");
-  if (rc.n) ck(cudaMemcpyAsync(d.as<char>() + 16, rc.agg, 8, cudaMemcpyDeviceToDevice, s), "D2D");
-  nc.nck(nc.GroupStart(), "ncclGroupStart");
-  nc.nck(nc.AllReduce(d.p, d.p, 1, kNcclInt64, kNcclSum, nc.comm, s), "ncclAllReduce");
-  nc.nck(nc.AllReduce(d.as<char>() + 8, d.as<char>() + 8, 1, fsum ? kNcclFloat64 : kNcclInt64, kNcclSum, nc.comm, s),
-         "ncclAllReduce");
-  nc.nck(nc.AllReduce(d.as<char>() + 16, d.as<char>() + 16, 1, kNcclInt64, kNcclSum, nc.comm, s), "ncclAllReduce");
-  nc.nck(nc.GroupEnd(), "ncclGroupEnd");
-  int64_t tot_has = 0;
-  ck(cudaMemcpyAsync(&tot_has, d.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  const tcudb_status agreed = nc.agree(st, s);
+  if (agreed != TCUDB_OK) {
+    if (st == TCUDB_OK) internal_set_err(ctx, agreed, "collective join: another rank failed");
+    return agreed;
+  }
+  // [0] local result rows (0 or 1), [1] the aggregate (int64 or fp64 bits), [2] COUNT (AVG)
+  int64_t part[3] = {r.n, 0, 0};
+  if (r.n) ck(cudaMemcpyAsync(&part[1], r.agg, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  if (rc.n) ck(cudaMemcpyAsync(&part[2], rc.agg, 8, cudaMemcpyDeviceToHost, s), "D2H");
   ck(cudaStreamSynchronize(s), "sync");
+  const std::vector<int64_t> all = nc.gather_vec(part, 3, s);
+  int64_t has = 0, cnt = 0;
+  __int128 isum = 0;
+  double fs = 0.0;
+  for (int j = 0; j < nc.nranks; ++j) {  // rank order: the same sum on every rank
+    has += all[3 * j];
+    cnt += all[3 * j + 2];
+    if (!all[3 * j]) continue;
+    if (fsum) { double x; std::memcpy(&x, &all[3 * j + 1], 8); fs += x; }
+    else isum += (__int128)all[3 * j + 1];
+  }
+  if (!fsum && (isum > (__int128)INT64_MAX || isum < (__int128)INT64_MIN)) {
+    // every rank's partial fits int64 but the total does not (the single-GPU guard's
+    // E_OVERFLOW; all ranks see the same sum)
+    return internal_set_err(ctx, TCUDB_E_OVERFLOW, "int64 overflow of the Q4 total across ranks");
+  }
+  int64_t tot[2] = {0, cnt};
+  if (fsum) std::memcpy(&tot[0], &fs, 8);
+  else tot[0] = (int64_t)isum;
   *out = tcudb_result{};
   out->g_type = TCUDB_I32; out->h_type = TCUDB_I32;
   out->agg_type = (q->agg == TCUDB_AVG || fsum) ? TCUDB_F64 : TCUDB_I64;
   char* base = static_cast<char*>(internal_result_alloc(ctx, 256, s));
   out->base = base;
   out->agg = base;
-  out->n = tot_has > 0 ? 1 : 0;
-  ck(cudaMemcpyAsync(base, d.as<char>() + 8, 8, cudaMemcpyDeviceToDevice, s), "D2D");
+  out->n = has > 0 ? 1 : 0;
+  ck(cudaMemcpyAsync(base, tot, 16, cudaMemcpyHostToDevice, s), "H2D");
   if (q->agg == TCUDB_AVG) {
     int64_t L = 0;
-    ck(launch_avg_div(base, fsum ? 1 : 0, reinterpret_cast<const long long*>(d.as<char>() + 16), out->n, s, &L),
+    ck(launch_avg_div(base, fsum ? 1 : 0, reinterpret_cast<const long long*>(base + 8), out->n, s, &L),
        "AVG division");
   }
   ck(cudaStreamSynchronize(s), "sync");
@@ -337,20 +463,54 @@ tcudb_status q4(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table* A, const 
 }  // namespace
 
 tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* ncp, const tcudb_table* A, const tcudb_table* B,
-                                 const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, cudaStream_t s,
-                                 float* ms_comm) {
+                                 const tcudb_query* q, tcudb_status local_st, tcudb_result* out, tcudb_stats* stats,
+                                 cudaStream_t s, float* ms_comm) {
   const NcclComm& nc = *ncp;
   const auto t0 = std::chrono::steady_clock::now();
   float local_ms = 0.f;
   tcudb_status st = TCUDB_OK;
+  *out = tcudb_result{};
   try {
-    const bool ga = A->group.data != nullptr, gb = B->group.data != nullptr;
+    // 0. agreement on the query shape
+    int64_t d[kDesc] = {};
+    const tcudb_table none{};
+    const tcudb_table& a = A ? *A : none;
+    const tcudb_table& b = B ? *B : none;
+    d[0] = a.n_rows; d[1] = b.n_rows;
+    const tcudb_col* cs[6] = {&a.key, &a.group, &a.value, &b.key, &b.group, &b.value};
+    for (int c = 0; c < 6; ++c) d[2 + c] = col_state(*cs[c], c < 3 ? a.n_rows : b.n_rows);
+    d[8] = q ? q->agg : -1;
+    d[9] = q ? q->flags : 0;
+    d[10] = local_st;
+    const std::vector<int64_t> all = nc.gather_vec(d, kDesc, s);
+    int64_t ag[kDesc];
+    st = shard_agree(all.data(), nc.nranks, ag);
+    if (st != TCUDB_OK) {
+      if (local_st == TCUDB_OK) internal_set_err(ctx, st, "collective join: ranks disagree on the query or another rank's arguments are invalid");
+      return st;
+    }
+    // normalized local tables: present columns get a (never dereferenced) pointer when the
+    // local slice is empty, absent columns are NULL everywhere, types are the agreed ones
+    DevBuf dummy(16, s);
+    tcudb_table An = a, Bn = b;
+    tcudb_col* ns[6] = {&An.key, &An.group, &An.value, &Bn.key, &Bn.group, &Bn.value};
+    for (int c = 0; c < 6; ++c) {
+      if (ag[2 + c] >= 2) {
+        ns[c]->type = (int32_t)(ag[2 + c] - 2);
+        if (!ns[c]->data) ns[c]->data = dummy.p;
+      } else {
+        ns[c]->data = nullptr;
+      }
+    }
+    const bool ga = An.group.data != nullptr, gb = Bn.group.data != nullptr;
+    const bool fsum = q->agg != TCUDB_COUNT && ((An.value.data && An.value.type == TCUDB_F32) ||
+                                                (Bn.value.data && Bn.value.type == TCUDB_F32));
     if (!ga && !gb) {
-      st = q4(ctx, nc, A, B, q, out, stats, s);
+      st = q4(ctx, nc, &An, &Bn, q, fsum, out, stats, s);
     } else {
       // the grouped side is routed by its group range (A when both are grouped)
-      const tcudb_table& R = ga ? *A : *B;
-      const tcudb_table& O = ga ? *B : *A;
+      const tcudb_table& R = ga ? An : Bn;
+      const tcudb_table& O = ga ? Bn : An;
       Cols Rr, Of;
       st = route_table(ctx, nc, R, Rr, s);
       if (st != TCUDB_OK) return st;
@@ -359,14 +519,24 @@ tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* ncp, const tcud
       const tcudb_table& Br = ga ? Of.t : Rr.t;
       tcudb_result loc{};
       const auto tl = std::chrono::steady_clock::now();
-      st = tcudb_join_agg(ctx, &Ar, &Br, q, &loc, stats, s);
+      const tcudb_status lst = tcudb_join_agg(ctx, &Ar, &Br, q, &loc, stats, s);
       local_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - tl).count();
-      if (st != TCUDB_OK) return st;
+      struct RF { tcudb_ctx* c; tcudb_result* r; bool keep = false; ~RF() { if (!keep) tcudb_result_free(c, r); } } fl{ctx, &loc};
+      st = nc.agree(lst, s);
+      if (st != TCUDB_OK) {
+        if (lst == TCUDB_OK) internal_set_err(ctx, st, "collective join: another rank's local query failed");
+        return st;
+      }
       if (q->flags & TCUDB_GATHER_NONE) {
         *out = loc;
+        out->g_type = ga ? An.group.type : TCUDB_I32;
+        out->h_type = gb ? Bn.group.type : TCUDB_I32;
+        fl.keep = true;
       } else {
-        struct RF { tcudb_ctx* c; tcudb_result* r; ~RF() { tcudb_result_free(c, r); } } fl{ctx, &loc};
-        gather_result(ctx, nc, loc, out, s);
+        const bool has[3] = {ga, gb, true};
+        const int32_t ty[3] = {ga ? An.group.type : TCUDB_I32, gb ? Bn.group.type : TCUDB_I32,
+                               (q->agg == TCUDB_AVG || fsum) ? TCUDB_F64 : TCUDB_I64};
+        gather_result(ctx, nc, loc, has, ty, out, s);
       }
     }
   } catch (const CommError& e) {
@@ -379,3 +549,19 @@ tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* ncp, const tcud
 }
 
 }  // namespace tcudb
+
+// ---------------------------------------------------------------- C ABI: host-only planning
+extern "C" {
+
+tcudb_status tcudb_shard_agree(const int64_t* descs, int32_t P, int64_t* agreed) {
+  if (!descs || !agreed || P < 1 || P > 1024) return TCUDB_E_INVALID;
+  return tcudb::shard_agree(descs, P, agreed);
+}
+
+tcudb_status tcudb_shard_bounds(const int64_t* msgs, int32_t P, int64_t* bounds) {
+  if (!msgs || P < 1 || P > 1024 || (P > 1 && !bounds)) return TCUDB_E_INVALID;
+  if (P > 1) tcudb::shard_bounds(msgs, P, bounds);
+  return TCUDB_OK;
+}
+
+}  // extern "C"

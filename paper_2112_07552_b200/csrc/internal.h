@@ -77,9 +77,12 @@ cudaError_t radix_sort_pairs(unsigned long long* keys, uint32_t* vals, unsigned 
 struct NcclComm;
 NcclComm* nccl_attach(void* comm, std::string* err);
 void nccl_detach(NcclComm* c);
+// local_st: this rank's own argument check (agreed on before any exchange)
 tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* nc, const tcudb_table* A, const tcudb_table* B,
-                                 const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, cudaStream_t s,
-                                 float* ms_comm);
+                                 const tcudb_query* q, tcudb_status local_st, tcudb_result* out, tcudb_stats* stats,
+                                 cudaStream_t s, float* ms_comm);
+tcudb_status shard_agree(const int64_t* descs, int P, int64_t* agreed);
+void shard_bounds(const int64_t* msgs, int P, int64_t* bounds);
 // host-runtime helpers the collective path shares (tcudb.cu)
 void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s);
 void internal_result_release(tcudb_ctx* ctx, void* p);

@@ -49,6 +49,7 @@ struct tcudb_ctx {
   std::map<void*, bool> dev_from_cb;  // result pointer -> allocated through afn
   bool fp4 = true;                    // e2m1 COUNT operands allowed (env TCUDB_NO_FP4=1 disables)
   tcudb::NcclComm* nc = nullptr;      // collective context (tcudb_create with an ncclComm_t)
+  tcudb_status host_fail = TCUDB_OK;  // collective host API: staging failed on this rank
   bool in_collective = false;         // the local query inside a collective call
 };
 
@@ -1449,25 +1450,36 @@ tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_ta
   if (!ctx || !out) return TCUDB_E_INVALID;
   std::memset(out, 0, sizeof(*out));
   if (ctx->sticky) return set_err(ctx, TCUDB_E_CUDA, "context has a sticky CUDA error");
-  if (!q || (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM && q->agg != TCUDB_AVG))
-    return set_err(ctx, TCUDB_E_INVALID, "bad query");
-  if ((q->flags & TCUDB_FORCE_DENSE) && (q->flags & TCUDB_FORCE_SPARSE))
-    return set_err(ctx, TCUDB_E_INVALID, "FORCE_DENSE and FORCE_SPARSE are exclusive");
-  const bool vals = q->agg != TCUDB_COUNT;
-  tcudb_status v = check_table(A, vals);
-  if (v == TCUDB_OK) v = check_table(B, vals);
-  if (v != TCUDB_OK) return set_err(ctx, v, "bad table arguments");
-  if (vals && A->value.data && B->value.data && ((A->value.type == TCUDB_F32) != (B->value.type == TCUDB_F32)))
-    return set_err(ctx, TCUDB_E_UNSUPPORTED, "mixed integer / float value columns");
+  // argument checks (on a collective context they are agreed on across the ranks first)
+  tcudb_status v = TCUDB_OK;
+  const char* why = nullptr;
+  if (!q || (q->agg != TCUDB_COUNT && q->agg != TCUDB_SUM && q->agg != TCUDB_AVG)) {
+    v = TCUDB_E_INVALID; why = "bad query";
+  } else if ((q->flags & TCUDB_FORCE_DENSE) && (q->flags & TCUDB_FORCE_SPARSE)) {
+    v = TCUDB_E_INVALID; why = "FORCE_DENSE and FORCE_SPARSE are exclusive";
+  } else {
+    const bool vals = q->agg != TCUDB_COUNT;
+    v = check_table(A, vals);
+    if (v == TCUDB_OK) v = check_table(B, vals);
+    if (v != TCUDB_OK) why = "bad table arguments";
+    else if (vals && A->value.data && B->value.data && ((A->value.type == TCUDB_F32) != (B->value.type == TCUDB_F32))) {
+      v = TCUDB_E_UNSUPPORTED; why = "mixed integer / float value columns";
+    }
+  }
+  if (v == TCUDB_OK && ctx->host_fail != TCUDB_OK) { v = ctx->host_fail; why = "host columns could not be staged"; }
+  ctx->host_fail = TCUDB_OK;
+  if (!(ctx->nc && !ctx->in_collective) && v != TCUDB_OK) return set_err(ctx, v, why);
   cudaSetDevice(ctx->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (ctx->nc && !ctx->in_collective) {
-    // collective call (collective.cu): routing + exchanges around the local query below
+    // collective call (collective.cu): agreement, routing + exchanges around the local query
     struct In { bool& f; explicit In(bool& x) : f(x) { f = true; } ~In() { f = false; } } in(ctx->in_collective);
     float ms_comm = 0.f;
     tcudb_status st;
+    if (v != TCUDB_OK) set_err(ctx, v, why);
+    tcudb_query qz{};
     try {
-      st = collective_join_agg(ctx, ctx->nc, A, B, q, out, stats, s, &ms_comm);
+      st = collective_join_agg(ctx, ctx->nc, A, B, q ? q : &qz, v, out, stats, s, &ms_comm);
     } catch (const Fail& f) {
       std::memset(out, 0, sizeof(*out));
       return fail_err(ctx, f);
@@ -1557,6 +1569,12 @@ tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcu
             up(B->group, B->n_rows, dB.group) && up(B->value, B->n_rows, dB.value);
   tcudb_status st = ok ? TCUDB_OK : TCUDB_E_NOMEM;
   tcudb_result dr{};
+  if (st != TCUDB_OK && ctx->nc) {
+    // collective: this rank still takes part (its failure is agreed on by every rank)
+    ctx->host_fail = st;
+    dA.n_rows = dB.n_rows = 0;
+    st = TCUDB_OK;
+  }
   if (st == TCUDB_OK) st = tcudb_join_agg(ctx, &dA, &dB, q, &dr, stats, stream);
   for (void* p : dev) cudaFreeAsync(p, s);
   if (st != TCUDB_OK) return st;

@@ -1,12 +1,15 @@
-"""Multi-GPU row sharding of the join + group-by (north star):
-output rows are sharded by ranges of A's group key; B is broadcast (allgather)
-over NVLink; result tuples are allgathered. One process per GPU, NCCL through
-torch.distributed (the plumbing); routing and the local query run in
-libtcudb.so kernels (tcudb_minmax, tcudb_partition, tcudb_join_agg).
+"""TEST INFRASTRUCTURE — a torch.distributed reference driver of the §8(e) row sharding.
+
+The product's multi-GPU path is the collective tcudb_join_agg inside libtcudb
+(csrc/collective.cu, NCCL). This module writes the same exchange algorithm over
+torch.distributed collectives so that it can run on CPU processes with the gloo
+backend (tests/test_shard_gloo.py), with a CPU stand-in for the per-rank engine;
+the range bounds come from the product's own host planning step
+(tcudb_shard_bounds over allgathered samples, as collective.cu computes them).
 
 Steps per query on every rank r of P (each rank starts with a 1/P slice of A
-and of B in its HBM):
-  1. global min/max of A.g (allreduce) -> P equal-width g ranges;
+and of B):
+  1. strided sample of A.g per rank (allgather) -> P row-balanced g ranges;
   2. route A by g range: tcudb_partition + all_to_all_single (sizes first);
   3. allgather B (sizes first, padded);
   4. local query on (A_r, B) -> tuples whose g lies in rank r's range;
@@ -25,19 +28,7 @@ from __future__ import annotations
 import numpy as np
 
 
-def local_slice(T, ws, rank):
-    """Contiguous 1/ws slice of a host table (numpy columns)."""
-    n = len(T["k"])
-    lo, hi = n * rank // ws, n * (rank + 1) // ws
-    return {k: (None if v is None else np.ascontiguousarray(v[lo:hi])) for k, v in T.items()}
-
-
-def range_bounds(gmin: int, gmax: int, P: int):
-    """P-1 ascending bounds splitting [gmin, gmax] into P equal-width ranges."""
-    if gmin > gmax:
-        return [0] * (P - 1)
-    span = gmax - gmin + 1
-    return [gmin + (span * i) // P for i in range(1, P)]
+from datagen import local_slice  # noqa: F401  (re-exported for the tests)
 
 
 def _all_gather_var(t, dist, group=None):
@@ -74,20 +65,20 @@ def _route(eng, T, bounds, dist, group):
 
 
 def _global_bounds(eng, col, dist, group):
-    """P equal-width ranges of a column's global [min, max] (allreduce of tcudb_minmax)."""
+    """Row-balanced ranges: every rank's strided sample of the column is allgathered and
+    the product's host planning step (tcudb_shard_bounds) picks the weighted quantiles."""
     import torch
-    mn, mx = eng.minmax(col)
-    t = torch.tensor([mn, mx], dtype=torch.int64, device=col.device)
-    lo, hi = t[:1].clone(), t[1:].clone()
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
-    return range_bounds(int(lo.item()), int(hi.item()), dist.get_world_size(group))
+    from paper_2112_07552_b200._lib import shard_bounds, shard_sample_msg
+    m = torch.from_numpy(shard_sample_msg(col.cpu().numpy())).to(col.device)
+    ms = [torch.zeros_like(m) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(ms, m, group=group)
+    return shard_bounds(torch.stack(ms).cpu().numpy())
 
 
 def _one(res, dtype, dev):
     """The (at most one) local Q4 aggregate as a 1-element tensor (0 when empty)."""
     import torch
-    a = res["agg"]
+    a = res["agg"].to(dev)
     return a[:1].to(dtype) if a.numel() else torch.zeros(1, dtype=dtype, device=dev)
 
 
@@ -104,15 +95,33 @@ def _sharded_q4(eng, A, B, agg, with_stats, group):
         out = eng.join_agg(A, Bf, agg, with_stats=with_stats)
         rc = None
     rs, st = (out if with_stats else (out, None))
-    n = torch.tensor([rs["agg"].numel()], dtype=torch.int64, device=dev)
-    dist.all_reduce(n, group=group)
-    s = _one(rs, rs["agg"].dtype, dev)
-    dist.all_reduce(s, group=group)
+    # partials allgathered and combined exactly in rank order (integer SUM in Python ints:
+    # a total beyond int64 raises, as the library's E_OVERFLOW)
+    part = torch.stack([torch.tensor(rs["agg"].numel(), dtype=torch.float64),
+                        _one(rs, torch.float64, "cpu")[0] if rs["agg"].dtype == torch.float64 else torch.tensor(0.0),
+                        torch.tensor(0.0)])
+    ints = torch.tensor([int(_one(rs, torch.int64, "cpu")[0]) if rs["agg"].dtype != torch.float64 else 0,
+                         int(_one(rc, torch.int64, "cpu")[0]) if rc is not None else 0], dtype=torch.int64)
+    ws = dist.get_world_size(group)
+    pl = [torch.zeros_like(part) for _ in range(ws)]
+    il = [torch.zeros_like(ints) for _ in range(ws)]
+    dist.all_gather(pl, part, group=group)
+    dist.all_gather(il, ints, group=group)
+    n = sum(int(p[0]) for p in pl)
+    if rs["agg"].dtype == torch.float64:
+        tot = 0.0
+        for p in pl:
+            tot += float(p[1])
+        s = torch.tensor([tot], dtype=torch.float64)
+    else:
+        tot = sum(int(i[0]) for i in il)
+        if not -2 ** 63 <= tot < 2 ** 63:
+            raise OverflowError("int64 overflow of the Q4 total")
+        s = torch.tensor([tot], dtype=torch.int64)
     if agg == "avg":
-        c = _one(rc, torch.int64, dev)
-        dist.all_reduce(c, group=group)
-        s = s.to(torch.float64) / c.clamp(min=1).to(torch.float64)
-    full = {"agg": s if int(n.item()) > 0 else s[:0]}
+        c = sum(int(i[1]) for i in il)
+        s = s.to(torch.float64) / max(c, 1)
+    full = {"agg": s if n > 0 else s[:0]}
     return (full, st) if with_stats else full
 
 
