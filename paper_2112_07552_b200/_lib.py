@@ -29,7 +29,7 @@ EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcud
                   "tcudb_triangle_count", "tcudb_gemm",
                   "tcudb_minmax", "tcudb_partition", "tcudb_result_free", "tcudb_result_free_host",
                   "tcudb_last_error", "tcudb_launch_count", "tcudb_destroy", "tcudb_shard_agree",
-                  "tcudb_shard_bounds"])
+                  "tcudb_shard_bounds", "tcudb_calibration"])
 SHARD_DESC_LEN, SHARD_SAMPLES = 11, 1024
 
 
@@ -122,6 +122,8 @@ def load(build_if_missing: bool = True):
     lib.tcudb_launch_count.argtypes = [P]
     lib.tcudb_launch_count.restype = ctypes.c_int64
     lib.tcudb_destroy.argtypes = [P]
+    lib.tcudb_calibration.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
+    lib.tcudb_calibration.restype = ctypes.c_int32
     I64P = ctypes.POINTER(ctypes.c_int64)
     lib.tcudb_shard_agree.argtypes = [I64P, ctypes.c_int32, I64P]
     lib.tcudb_shard_agree.restype = ctypes.c_int
@@ -303,6 +305,14 @@ class Engine:
 
     def last_error(self):
         return self._lib.tcudb_last_error(self._ctx).decode()
+
+    @property
+    def calibration(self) -> dict:
+        """Selector constants measured at tcudb_create (tcudb_calibration)."""
+        v = (ctypes.c_double * 7)()
+        m = self._lib.tcudb_calibration(self._ctx, v)
+        keys = ("R_i8", "R_bf16", "R_fp4", "BW", "R_sp", "T_sp0", "ms")
+        return dict(zip(keys, list(v)), measured=bool(m))
 
     @property
     def launch_count(self) -> int:

@@ -323,3 +323,11 @@ cudaError_t launch_compact_count(const CompactArgs& a, const int32_t* precounted
 cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t s, int64_t* launches);
 
 }  // namespace tcudb
+
+namespace tcudb {
+// ---------------------------------------------------------------- calib.cu
+// synthetic int32 columns for the create-time calibration: k uniform over [0, keys),
+// g uniform over [0, groups)
+cudaError_t launch_gen_cols(int32_t* k, int32_t* g, int64_t n, uint32_t keys, uint32_t groups, uint32_t seed,
+                            cudaStream_t s, int64_t* launches);
+}  // namespace tcudb

@@ -28,8 +28,20 @@
 
 using namespace tcudb;
 
+// Selector cost-model constants (a4, Eq. 3 CT = 2MNK / peak plus the bytes each path
+// moves). Defaults = the round-1 fit of scripts/selector_sweep.py; tcudb_create replaces
+// them by a one-time measurement per device and process (calibrate()).
+struct Calib {
+  double R_i8 = 2.0e15, R_bf16 = 1.0e15, R_fp4 = 4.0e15;  // dense GEMM ops/s per kind
+  double BW = 5.5e12;                                       // device copy bytes/s (read + write)
+  double R_sp = 5.0e10, T_sp0 = 40e-6;                      // sparse path: joined pairs/s, fixed cost
+  int measured = 0;
+  float ms = 0.f;                                           // calibration wall time
+};
+
 struct tcudb_ctx {
   int device = 0;
+  Calib cal;
   cudaMemPool_t pool = nullptr;
   tcudb_alloc_fn afn = nullptr;
   tcudb_free_fn ffn = nullptr;
@@ -413,8 +425,10 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   tm.mark(&S.ms_encode);
   // a4 selector with the same cost model as the general path (COUNT)
   const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), Kp = round_up(std::max<int64_t>(K, 1), 128);
-  const double t_dense = 2.0 * Gp * Hp * Kp / 2.0e15 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / 5.5e12;
-  const double t_sparse = (double)J / 5.0e10 + ((double)G * H * 4 + (double)(nA + nB) * 32) / 5.5e12 + 40e-6;
+  const Calib& cb = ctx->cal;
+  const double t_dense = 2.0 * Gp * Hp * Kp / cb.R_i8 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / cb.BW;
+  // the partitioned expand's own rate (one L2 reduction per joined pair: ~1.4e11/s on c5)
+  const double t_sparse = (double)J / 5.0e10 + ((double)G * H * 4 + (double)(nA + nB) * 32) / cb.BW + cb.T_sp0;
   if (J == 0 || K == 0) {
     S.G = G; S.H = H; S.K = K; S.join_pairs = 0; S.path = 1; S.spa_mode = 4;
     return true;  // empty result (out already zeroed)
@@ -730,7 +744,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   // B200 by scripts/selector_sweep.py (profiles/r01_selector_sweep.jsonl, §8(f) f4): the
   // dense path touches its operand / scratch / C bytes ~3 times (fill, GEMM, compaction);
   // the sparse path expands ~5e10 joined pairs/s and pays one more host sync (~40 us).
-  const double R_tc = is_float ? 1.0e15 : 2.0e15, BW = 5.5e12, R_sp = 5.0e10, T_sp0 = 40e-6;
+  const Calib& cb = ctx->cal;  // measured at tcudb_create (calibrate())
+  const bool fp4_likely = !is_sum && ctx->fp4 && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && dense_ops >= 1e11;
+  const double R_tc = is_float ? cb.R_bf16 : (fp4_likely ? cb.R_fp4 : cb.R_i8), BW = cb.BW, R_sp = cb.R_sp,
+               T_sp0 = cb.T_sp0;
   double planes_est = is_sum ? (is_float ? 1.0 : 2.0) : 1.0;
   if (need_exist) planes_est += 1.0;
   const double csz = is_sum ? 8.0 : 4.0;
@@ -739,9 +756,21 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
   const double t_dense = planes_est * dense_ops / R_tc + 3.0 * dense_bytes / BW;
   const double t_sparse = (double)J / R_sp + sparse_bytes / BW + T_sp0;
-  // memory budget: the device's free memory when the context was created (a live
-  // cudaMemGetInfo per query costs 0.3 ms to tens of ms of host time)
-  const size_t free_b = ctx->mem_free0;
+  // memory budget: the device's free memory when the context was created, re-read live
+  // (cudaMemGetInfo: 0.3 ms to tens of ms of host time) only when a path's footprint comes
+  // within reach of it
+  size_t free_b = ctx->mem_free0;
+  if (std::max(dense_bytes, sparse_bytes) > 0.25 * (double)free_b) {
+    size_t fb = 0, tb = 0;
+    if (cudaMemGetInfo(&fb, &tb) == cudaSuccess) {
+      size_t reserved = 0, used = 0;
+      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      free_b = fb + (reserved > used ? reserved - used : 0);  // + what our pool holds unused
+    } else {
+      cudaGetLastError();
+    }
+  }
   bool dense;
   if (q->flags & TCUDB_FORCE_DENSE) dense = true;
   else if (q->flags & TCUDB_FORCE_SPARSE) dense = false;
@@ -1352,6 +1381,137 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   return TCUDB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// One-time selector calibration (SURVEY §8(b) tcudb_create "runs calibration (A19)";
+// PAPER.md §4.2.2: the cost model needs the device's rates; the paper samples
+// them once). Measured per device, once per process, on a private stream:
+//   BW     — a 128 MiB device-to-device copy (read + write bytes / s), best of 3;
+//   R_i8 / R_bf16 / R_fp4 — the a6 GEMM kernels on 4096 x 4096 x 4096 (fp4: x 8192) operands;
+//   R_sp, T_sp0 — two forced-sparse COUNT queries on generated tables (J = 2^20 and 2^23
+//          joined pairs): t = J / R_sp + bytes / BW + T_sp0 solved for R_sp and T_sp0.
+// Each figure is clamped to [1/4, 4] x its default so a disturbed measurement cannot
+// derail the selector. TCUDB_CALIBRATE=0 keeps the defaults.
+std::mutex g_calib_mu;
+std::map<int, Calib> g_calib;
+
+void calibrate(tcudb_ctx* c) {
+  {
+    std::lock_guard<std::mutex> g(g_calib_mu);
+    auto it = g_calib.find(c->device);
+    if (it != g_calib.end()) { c->cal = it->second; return; }
+  }
+  const char* env = getenv("TCUDB_CALIBRATE");
+  if (env && env[0] == '0') return;
+  const auto t0 = std::chrono::steady_clock::now();
+  Calib cal;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) { cudaGetLastError(); return; }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto timed = [&](auto&& fn, int reps) -> double {  // best of reps, seconds
+    double best = 1e30;
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(e0, s);
+      fn();
+      cudaEventRecord(e1, s);
+      if (cudaEventSynchronize(e1) != cudaSuccess) return -1.0;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = std::min(best, (double)ms * 1e-3);
+    }
+    return best;
+  };
+  auto clamp = [](double x, double def) { return x > 0 ? std::min(std::max(x, 0.25 * def), 4.0 * def) : def; };
+  bool ok = true;
+  try {
+    Arena ar(s);
+    int64_t L = 0;
+    {
+      const size_t bytes = 128ull << 20;
+      char* a = ar.get<char>((int64_t)bytes);
+      char* b = ar.get<char>((int64_t)bytes);
+      CK(cudaMemsetAsync(a, 1, bytes, s));
+      const double t = timed([&] { cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice, s); }, 3);
+      cal.BW = clamp(2.0 * (double)bytes / t, cal.BW);
+    }
+    {
+      const int64_t M = 4096, N = 4096, K = 4096;
+      uint8_t* A = ar.get<uint8_t>(M * K * 2);
+      uint8_t* B = ar.get<uint8_t>(N * K * 2);
+      void* C = ar.get<char>(M * N * 4);
+      CK(cudaMemsetAsync(A, 0x11, M * K * 2, s));
+      CK(cudaMemsetAsync(B, 0x11, N * K * 2, s));
+      GemmArgs ga{};
+      ga.M = M; ga.N = N; ga.A = A; ga.B = B; ga.C = C; ga.ldc = N; ga.epi = EPI_STORE32;
+      ga.elem = ELEM_I8; ga.lda = ga.ldb = K; ga.k_begin = 0; ga.k_len = K;
+      const double ti = timed([&] { launch_gemm(ga, s, &L); }, 3);
+      cal.R_i8 = clamp(2.0 * M * N * K / ti, cal.R_i8);
+      ga.elem = ELEM_BF16;
+      const double tb = timed([&] { launch_gemm(ga, s, &L); }, 3);
+      cal.R_bf16 = clamp(2.0 * M * N * K / tb, cal.R_bf16);
+      // e2m1: K = 8192 elements in 4096 bytes per row, N a multiple of 240
+      ga.elem = ELEM_FP4; ga.N = 3840; ga.lda = ga.ldb = K; ga.k_len = K;
+      const double tf = timed([&] { launch_gemm(ga, s, &L); }, 3);
+      cal.R_fp4 = clamp(2.0 * M * 3840.0 * (2.0 * K) / tf, cal.R_fp4);
+    }
+    if (cudaGetLastError() != cudaSuccess) ok = false;
+    // sparse path: two forced-sparse COUNT queries
+    double t_pt[2] = {0, 0}, J_pt[2] = {0, 0}, b_pt[2] = {0, 0};
+    const int64_t n_pt[2] = {1 << 17, 1 << 20};
+    const uint32_t keys_pt[2] = {1u << 14, 1u << 17}, groups = 4096;
+    for (int pt = 0; pt < 2 && ok; ++pt) {
+      const int64_t n = n_pt[pt];
+      int32_t* ka = ar.get<int32_t>(n);
+      int32_t* ga_ = ar.get<int32_t>(n);
+      int32_t* kb = ar.get<int32_t>(n);
+      int32_t* hb = ar.get<int32_t>(n);
+      CK(launch_gen_cols(ka, ga_, n, keys_pt[pt], groups, 17u + (uint32_t)pt, s, &L));
+      CK(launch_gen_cols(kb, hb, n, keys_pt[pt], groups, 91u + (uint32_t)pt, s, &L));
+      tcudb_table TA{}, TB{};
+      TA.n_rows = TB.n_rows = n;
+      TA.key = {ka, TCUDB_I32}; TA.group = {ga_, TCUDB_I32};
+      TB.key = {kb, TCUDB_I32}; TB.group = {hb, TCUDB_I32};
+      tcudb_query q{TCUDB_COUNT, TCUDB_FORCE_SPARSE};
+      double best = 1e30;
+      tcudb_stats st{};
+      for (int r = 0; r < 3; ++r) {
+        tcudb_result out{};
+        const auto h0 = std::chrono::steady_clock::now();
+        if (run_join_agg(c, &TA, &TB, &q, &out, &st, s) != TCUDB_OK) { ok = false; break; }
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+        result_release(c, out.base ? out.base : out.g);
+        if (r > 0) best = std::min(best, dt);  // the first run pays one-time setup
+      }
+      t_pt[pt] = best;
+      J_pt[pt] = (double)st.join_pairs;
+      b_pt[pt] = (double)st.G * (double)st.H * 4.0 + 2.0 * (double)n * 32.0;
+    }
+    if (ok && J_pt[1] > J_pt[0] * 2) {
+      const double y0 = t_pt[0] - b_pt[0] / cal.BW, y1 = t_pt[1] - b_pt[1] / cal.BW;
+      const double slope = (y1 - y0) / (J_pt[1] - J_pt[0]);
+      if (slope > 0) {
+        cal.R_sp = clamp(1.0 / slope, cal.R_sp);
+        cal.T_sp0 = std::min(std::max(y0 - J_pt[0] / cal.R_sp, 10e-6), 400e-6);
+      }
+    }
+    CK(cudaStreamSynchronize(s));
+  } catch (const Fail&) {
+    ok = false;
+  }
+  cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (!ok) return;  // defaults stay
+  cal.measured = 1;
+  cal.ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->cal = cal;
+  std::lock_guard<std::mutex> g(g_calib_mu);
+  g_calib[c->device] = cal;
+}
+
 tcudb_status check_table(const tcudb_table* t, bool need_value_ok) {
   if (!t || t->n_rows < 0) return TCUDB_E_INVALID;
   if (t->n_rows > 0 && !t->key.data) return TCUDB_E_INVALID;
@@ -1433,6 +1593,7 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   for (auto& e : c->evk) cudaEventCreate(&e);
+  calibrate(c);  // selector constants (A19); cached per device and process
   if (nccl_comm) {
     std::string why;
     c->nc = nccl_attach(nccl_comm, &why);
@@ -1816,6 +1977,14 @@ void tcudb_result_free_host(tcudb_ctx* ctx, tcudb_result* r) {
 const char* tcudb_last_error(const tcudb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t tcudb_launch_count(const tcudb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t tcudb_calibration(const tcudb_ctx* ctx, double* out7) {
+  if (!ctx || !out7) return 0;
+  const Calib& c = ctx->cal;
+  const double v[7] = {c.R_i8, c.R_bf16, c.R_fp4, c.BW, c.R_sp, c.T_sp0, (double)c.ms};
+  std::memcpy(out7, v, sizeof(v));
+  return c.measured;
+}
 
 void tcudb_destroy(tcudb_ctx* ctx) {
   if (!ctx) return;

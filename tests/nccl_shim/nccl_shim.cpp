@@ -7,20 +7,24 @@
 // q4 and every exchange) at P = 2, 4, 8 on a single B200. Selected at tcudb_create by
 // TCUDB_NCCL_LIB=<path of this library>.
 //
-// Semantics: every call (or ncclGroupStart..ncclGroupEnd block) is one rendezvous of all
-// P ranks: each rank synchronizes the streams of its calls, posts its operation list,
-// waits for the others (barrier 1), stages what it receives into host memory (sends are
-// matched to receives per (source, destination) pair in call order, collectives by
-// position; sizes, types and ops must agree), waits (barrier 2), then writes its receive
-// buffers. A mismatch or a barrier timeout breaks the world: that call and every later
-// call on it return an error on every rank (the library turns it into E_COMM) instead of
-// hanging. Counters record the calls and bytes per rank.
+// Semantics (those of NCCL, executed eagerly on the host): point-to-point sends are
+// copied out at call time (after the stream's earlier work) into a mailbox per
+// (source, destination) pair; a receive takes the next message of its pair, in call order,
+// and checks its size. Collectives are numbered per rank; the n-th collective of every
+// rank must be the same operation (kind, count, type, reduction) — each rank posts its
+// contribution and waits for all P. Inside ncclGroupStart..End the sends run first, then
+// the collectives, then the receives (a group is concurrent in NCCL, so any order that
+// cannot deadlock is faithful). A mismatch or a wait beyond the timeout breaks the world:
+// that call and every later call on it return an error on every rank (the library turns
+// it into E_COMM) instead of hanging. Counters record the calls and bytes per rank.
 #include <cuda_runtime.h>
 
 #include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <deque>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -46,48 +50,41 @@ struct Op {
   cudaStream_t stream;
 };
 
+struct Coll {
+  int kind = -1, dtype = -1, redop = -1;
+  size_t count = 0;
+  std::vector<std::vector<char>> data;
+  int have = 0, done = 0;
+};
+
 struct World {
   int P;
   double timeout_s;
   std::mutex mu;
   std::condition_variable cv;
-  int arrived = 0;
-  long long gen = 0;
   bool broken = false;
   std::string why;
-  std::vector<std::vector<Op>> posted;
+  std::map<std::pair<int, int>, std::deque<std::vector<char>>> mail;  // (src, dst) -> messages
+  std::map<long long, Coll> coll;                                     // collective sequence -> slot
+  std::vector<long long> seq;                                         // next collective per rank
   std::vector<Comm> comms;
   std::vector<long long> calls, bytes_in;
-  explicit World(int p, double t) : P(p), timeout_s(t), posted(p), calls(p, 0), bytes_in(p, 0) {
+  explicit World(int p, double t) : P(p), timeout_s(t), seq(p, 0), calls(p, 0), bytes_in(p, 0) {
     comms.resize(p);
     for (int r = 0; r < p; ++r) comms[r] = Comm{this, r};
   }
-  // returns false when the world is (or becomes) broken
-  bool barrier() {
-    std::unique_lock<std::mutex> lk(mu);
-    if (broken) return false;
-    const long long g = gen;
-    if (++arrived == P) {
-      arrived = 0;
-      ++gen;
-      cv.notify_all();
-      return true;
-    }
-    const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g || broken; });
-    if (broken) return false;
-    if (!ok) {
-      broken = true;
-      why = "barrier timeout (a rank did not reach the collective)";
-      cv.notify_all();
-      return false;
-    }
-    return true;
-  }
-  void fail(const std::string& w) {
-    std::lock_guard<std::mutex> lk(mu);
+  void fail_locked(const std::string& w) {
     if (!broken) why = w;
     broken = true;
     cv.notify_all();
+  }
+  // wait (lock held) until pred() or broken; false on broken / timeout (which breaks)
+  template <typename Pred>
+  bool wait(std::unique_lock<std::mutex>& lk, Pred pred, const char* what) {
+    const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return broken || pred(); });
+    if (broken) return false;
+    if (!ok) { fail_locked(std::string("timeout waiting for ") + what); return false; }
+    return true;
   }
 };
 
@@ -137,91 +134,102 @@ std::vector<char> d2h(const void* p, size_t bytes) {
   return h;
 }
 
-// one rendezvous over the calling rank's operation list
+void h2d(void* p, const std::vector<char>& h) {
+  if (!h.empty()) cudaMemcpy(p, h.data(), h.size(), cudaMemcpyHostToDevice);
+}
+
+// the calling rank's operations of one call or group
 int run_group(std::vector<Op>& ops) {
   if (ops.empty()) return 0;
   World* w = ops[0].comm->w;
   const int me = ops[0].comm->rank;
-  for (const Op& o : ops) {
-    if (o.comm->w != w || o.comm->rank != me) { w->fail("one group spans two communicators"); return kInvalidUsage; }
-    if (!dsize(o.dtype)) { w->fail("unsupported data type"); return kInvalidArgument; }
-  }
-  for (const Op& o : ops) cudaStreamSynchronize(o.stream);
   {
-    std::lock_guard<std::mutex> lk(w->mu);
-    w->posted[me] = ops;
+    std::unique_lock<std::mutex> lk(w->mu);
+    if (w->broken) return kSystemError;
+    for (const Op& o : ops) {
+      if (o.comm->w != w || o.comm->rank != me) { w->fail_locked("one group spans two communicators"); return kInvalidUsage; }
+      if (!dsize(o.dtype)) { w->fail_locked("unsupported data type"); return kInvalidArgument; }
+      if ((o.kind == OP_SEND || o.kind == OP_RECV) && (o.peer < 0 || o.peer >= w->P || o.peer == me)) {
+        w->fail_locked("point-to-point with an invalid peer");
+        return kInvalidArgument;
+      }
+    }
     w->calls[me] += (long long)ops.size();
   }
-  if (!w->barrier()) return kSystemError;
-  // stage what this rank receives
-  struct Stage { void* dst; std::vector<char> data; };
-  std::vector<Stage> stage;
-  std::string err;
-  std::vector<int> coll_idx(w->P, 0);
-  int my_coll = 0;
-  for (size_t i = 0; i < ops.size() && err.empty(); ++i) {
-    const Op& o = ops[i];
-    const size_t bytes = o.count * dsize(o.dtype);
-    if (o.kind == OP_SEND) continue;
-    if (o.kind == OP_RECV) {
-      // k-th receive from peer p matches p's k-th send to me
-      int k = 0;
-      for (size_t j = 0; j < i; ++j) k += ops[j].kind == OP_RECV && ops[j].peer == o.peer;
-      if (o.peer < 0 || o.peer >= w->P) { err = "receive from an invalid peer"; break; }
-      const std::vector<Op>& po = w->posted[o.peer];
-      const Op* match = nullptr;
-      int seen = 0;
-      for (const Op& x : po)
-        if (x.kind == OP_SEND && x.peer == me && seen++ == k) { match = &x; break; }
-      if (!match) { err = "receive without a matching send"; break; }
-      if (match->count * dsize(match->dtype) != bytes) { err = "send / receive sizes differ"; break; }
-      stage.push_back({o.dst, d2h(match->src, bytes)});
-      continue;
-    }
-    // collective: the my_coll-th collective of every rank must be the same operation
-    std::vector<const Op*> peers(w->P, nullptr);
-    for (int r = 0; r < w->P; ++r) {
-      int seen = 0;
-      for (const Op& x : w->posted[r])
-        if ((x.kind == OP_ALLREDUCE || x.kind == OP_ALLGATHER) && seen++ == my_coll) { peers[r] = &x; break; }
-      if (!peers[r] || peers[r]->kind != o.kind || peers[r]->count != o.count || peers[r]->dtype != o.dtype ||
-          (o.kind == OP_ALLREDUCE && peers[r]->redop != o.redop)) {
-        err = "collective mismatch across ranks";
-        break;
-      }
-    }
-    ++my_coll;
-    if (!err.empty()) break;
-    if (o.kind == OP_ALLGATHER) {
-      std::vector<char> all(bytes * w->P);
-      for (int r = 0; r < w->P; ++r) {
-        std::vector<char> x = d2h(peers[r]->src, bytes);
-        if (bytes) std::memcpy(all.data() + bytes * r, x.data(), bytes);
-      }
-      stage.push_back({o.dst, std::move(all)});
-    } else {
-      std::vector<char> acc = d2h(peers[0]->src, bytes);
-      for (int r = 1; r < w->P; ++r)
-        if (!reduce_any(acc, d2h(peers[r]->src, bytes), o.count, o.dtype, o.redop)) { err = "unsupported reduction"; break; }
-      stage.push_back({o.dst, std::move(acc)});
-    }
-  }
-  if (!err.empty()) w->fail(err);
-  if (!w->barrier()) return kSystemError;
+  for (const Op& o : ops) cudaStreamSynchronize(o.stream);
   long long in = 0;
-  for (Stage& st : stage) {
-    if (!st.data.empty()) cudaMemcpy(st.dst, st.data.data(), st.data.size(), cudaMemcpyHostToDevice);
-    in += (long long)st.data.size();
+  // 1. sends: copied out now (eager)
+  for (const Op& o : ops) {
+    if (o.kind != OP_SEND) continue;
+    std::vector<char> m = d2h(o.src, o.count * dsize(o.dtype));
+    std::lock_guard<std::mutex> lk(w->mu);
+    w->mail[{me, o.peer}].push_back(std::move(m));
+    w->cv.notify_all();
+  }
+  // 2. collectives, in call order
+  for (const Op& o : ops) {
+    if (o.kind != OP_ALLREDUCE && o.kind != OP_ALLGATHER) continue;
+    const size_t bytes = o.count * dsize(o.dtype);
+    std::vector<char> mine = d2h(o.src, bytes);
+    std::vector<char> out;
+    {
+      std::unique_lock<std::mutex> lk(w->mu);
+      const long long q = w->seq[me]++;
+      Coll& c = w->coll[q];
+      if (c.kind < 0) {
+        c.kind = o.kind; c.count = o.count; c.dtype = o.dtype; c.redop = o.redop;
+        c.data.resize(w->P);
+      } else if (c.kind != o.kind || c.count != o.count || c.dtype != o.dtype ||
+                 (o.kind == OP_ALLREDUCE && c.redop != o.redop)) {
+        w->fail_locked("collective mismatch across ranks");
+        return kSystemError;
+      }
+      c.data[me] = std::move(mine);
+      ++c.have;
+      w->cv.notify_all();
+      if (!w->wait(lk, [&] { return c.have == w->P; }, "a collective")) return kSystemError;
+      if (o.kind == OP_ALLGATHER) {
+        out.resize(bytes * w->P);
+        for (int r = 0; r < w->P; ++r)
+          if (bytes) std::memcpy(out.data() + bytes * r, c.data[r].data(), bytes);
+      } else {
+        out = c.data[0];
+        for (int r = 1; r < w->P; ++r)
+          if (!reduce_any(out, c.data[r], o.count, o.dtype, o.redop)) {
+            w->fail_locked("unsupported reduction");
+            return kSystemError;
+          }
+      }
+      if (++c.done == w->P) w->coll.erase(q);
+    }
+    h2d(o.dst, out);
+    in += (long long)out.size();
+  }
+  // 3. receives: the next message of each (peer, me) pair, in call order
+  for (const Op& o : ops) {
+    if (o.kind != OP_RECV) continue;
+    const size_t bytes = o.count * dsize(o.dtype);
+    std::vector<char> m;
+    {
+      std::unique_lock<std::mutex> lk(w->mu);
+      auto& box = w->mail[{o.peer, me}];
+      if (!w->wait(lk, [&] { return !box.empty(); }, "a matching send")) return kSystemError;
+      m = std::move(box.front());
+      box.pop_front();
+      if (m.size() != bytes) { w->fail_locked("send / receive sizes differ"); return kSystemError; }
+    }
+    h2d(o.dst, m);
+    in += (long long)m.size();
   }
   {
     std::lock_guard<std::mutex> lk(w->mu);
     w->bytes_in[me] += in;
+    if (w->broken) return kSystemError;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int submit(const Op& o) {
-  if (o.comm->w->broken) return kSystemError;
   if (t_depth > 0) { t_ops.push_back(o); return 0; }
   std::vector<Op> one{o};
   return run_group(one);
@@ -270,7 +278,6 @@ int ncclGroupEnd() {
   if (--t_depth > 0) return 0;
   std::vector<Op> ops;
   ops.swap(t_ops);
-  if (!ops.empty() && ops[0].comm->w->broken) return kSystemError;
   return run_group(ops);
 }
 const char* ncclGetErrorString(int r) {

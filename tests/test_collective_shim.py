@@ -84,7 +84,7 @@ def run_ranks(shim, P, slices, agg, flags=0, host=False, timeout=120.0):
         assert not t.is_alive(), "rank thread hung"
     calls = [shim.shim_calls(world, r) for r in range(P)]
     nbytes = [shim.shim_bytes_in(world, r) for r in range(P)]
-    broken = shim.shim_world_broken(world)
+    broken = shim.shim_world_why(world).decode() if shim.shim_world_broken(world) else ""
     shim.shim_world_destroy(world)
     return res, err, calls, nbytes, broken
 
@@ -101,8 +101,8 @@ def variant(A, B, drop):
     return A, B
 
 
-def check_all(res, err, ref, agg, float_vals):
-    assert all(e is None for e in err), err
+def check_all(res, err, ref, agg, float_vals, broken=""):
+    assert all(e is None for e in err), (err, broken)
     for r, out in enumerate(res):
         compare(out, ref, agg, float_vals=float_vals)
 
@@ -176,8 +176,8 @@ def test_collective_empty_and_skewed_ranks(shim, oracle_mod, agg):
         sl.append((a, b))
     assert n > 0
     ref = oracle_mod.join_agg(A, B, agg)
-    res, err, *_ = run_ranks(shim, P, sl, agg)
-    check_all(res, err, ref, agg, False)
+    res, err, _, _, broken = run_ranks(shim, P, sl, agg)
+    check_all(res, err, ref, agg, False, broken)
     # no joined pairs at all on the routed side's owners: disjoint keys
     B2 = dict(B, k=B["k"] + 10 ** 6)
     ref2 = oracle_mod.join_agg(A, B2, agg)

@@ -897,3 +897,13 @@ def test_bf16_range_fill_duplicates(engine, torch_mod, oracle_mod, monkeypatch, 
     out, st = run(engine, torch_mod, A, B, "sum", flags=1)  # FORCE_DENSE: the fill under test
     assert st["path"] == 0
     compare(out, oracle_mod.join_agg(A, B, "sum"), "sum", float_vals=True)
+
+
+def test_selector_calibration_measured(engine):
+    """tcudb_create measured the selector's constants (A19) on this device: rates in the
+    B200's range (the clamps allow 1/4..4x of the defaults; these bounds are tighter)."""
+    c = engine.calibration
+    assert c["measured"], c
+    assert 1.0e15 < c["R_i8"] < 5.0e15 and 0.5e15 < c["R_bf16"] < 2.5e15 and 2.0e15 < c["R_fp4"] < 1.0e16, c
+    assert 3.0e12 < c["BW"] < 9.0e12, c
+    assert 1.25e10 <= c["R_sp"] <= 2.0e11 and 10e-6 <= c["T_sp0"] <= 400e-6, c
