@@ -70,7 +70,7 @@ struct DevBuf {  // stream-ordered device buffer
   void* p = nullptr;
   cudaStream_t s;
   DevBuf(size_t bytes, cudaStream_t st) : s(st) {
-    if (cudaMallocAsync(&p, bytes ? bytes : 8, s) != cudaSuccess) {
+    if (pool_malloc(&p, bytes ? bytes : 8, s) != cudaSuccess) {
       cudaGetLastError();
       throw CommError{"device allocation for the exchange"};
     }

@@ -877,11 +877,7 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
   // threads): mark in shared memory instead whenever the span fits, so each block
   // stores each set flag once.
   if (span <= 64 * 1024 && c.n >= 4096) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_mark_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr = true;
-    }
+    set_func_attr(k_mark_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     // enough tuples per block to amortize zeroing and flushing the span
     int64_t blocks = c.n / std::max<int64_t>(4096, span / 4);
     if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
@@ -905,11 +901,7 @@ cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long l
   if (est_distinct > 0 && row_slot && cap <= 16384 && c.n >= 64 * cap) {
     const int cap_s = (int)cap;  // >= 1.9 x the global distinct count, so >= any block's
     const size_t smem = (size_t)cap_s * 12;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_hash_insert_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 12);
-      attr = true;
-    }
+    set_func_attr(k_hash_insert_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 12);
     const int per_sm = smem <= 96 * 1024 ? 2 : 1;
     const int64_t nblk = std::min<int64_t>(per_sm * kNumSMs, (c.n + 32767) / 32768);
     const int64_t chunk = (c.n + nblk - 1) / nblk;
@@ -1011,11 +1003,7 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
   if (!rowabs_g && K > 0 && key.n >= 4 * K && key.type == 0 && grp.type == 0 && kd.mode == 0 && gd.mode == 0 &&
       fits_i32(kd.minv) && fits_i32(gd.minv) && smem_d <= 100 * 1024 && al16(key.data) && al16(grp.data) &&
       al16(kcode) && al16(gcode)) {
-    static bool attr_d = false;
-    if (!attr_d) {
-      cudaFuncSetAttribute(k_probe_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      attr_d = true;
-    }
+    set_func_attr(k_probe_direct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     int64_t blocks = key.n / 4096;
     if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
     if (blocks < 1) blocks = 1;
@@ -1026,11 +1014,7 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
     return cudaGetLastError();
   }
   if (!rowabs_g && K > 0 && smem <= 200 * 1024 && key.n >= 4 * K) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_probe_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
+    set_func_attr(k_probe_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int64_t blocks = key.n / 2048;  // >= 2 tuples per thread; the flush is K / 1024 steps per block
     if (blocks > kNumSMs) blocks = kNumSMs;
     if (blocks < 1) blocks = 1;

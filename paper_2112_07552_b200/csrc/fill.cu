@@ -616,13 +616,9 @@ cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, 
   k_bin_scatter<<<p.nblk, kBinThreads, 0, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, p.chunk, p.R,
                                                p.P, p.ncoarse, Kp, coffs, ent8, fs);
   k_bin_split<<<p.ncoarse, kBinThreads, 0, s>>>(ent8, coffs, p.nblk, p.P, p.nband, boffs, ent4);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_bin_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kBinTileBytes + kBinTileBytes / 16);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = set_func_attr(k_bin_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kBinTileBytes + kBinTileBytes / 16);
+  if (e != cudaSuccess) return e;
   const int tile_smem = (int)(p.R * Kp * 2 + p.R * Kp / 8);
   k_bin_tile<<<p.nband, kBinTileThreads, tile_smem, s>>>(ent4, boffs, p.R, Kp, rows, op, ld_op, fs);
   if (launches) *launches += 4;

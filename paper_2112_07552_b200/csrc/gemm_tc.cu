@@ -663,16 +663,12 @@ int pick_group_m(int tiles_m, int64_t rows_per_mblock, int64_t k_bytes) {
 // Builds the tensor maps and launches the 1-CTA kernel for the chosen stage width.
 template <int BN_, bool FP4, bool CMP = false>
 cudaError_t run_1cta(const GemmArgs& a, const KParams& p, int map_elem, int kb, cudaStream_t s, int64_t* launches) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 128, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Geo<BN_, 128>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_gemm_tc<BN_, FP4, 64, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)Geo<BN_, 64>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_func_attr(k_gemm_tc<BN_, FP4, 128, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Geo<BN_, 128>::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  e = set_func_attr(k_gemm_tc<BN_, FP4, 64, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)Geo<BN_, 64>::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
   constexpr int NT_ = CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREADS;
   const int64_t kcols = a.k_begin + a.k_len;
   CUtensorMap mA, mB;
@@ -732,12 +728,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
   if (a.M % BM || a.N % BN || (a.k_len * esz) % BKB || (a.k_begin * esz) % BKB) return cudaErrorInvalidValue;
   if ((a.lda * esz) % 16 || (a.ldb * esz) % 16) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_func_attr(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
+  if (e != cudaSuccess) return e;
   // Kernel choice: the 1-CTA 128x256 kernel is the default (measured faster on c2: 1.31 vs
   // 1.40 ms; both MMA-bound at ~65-70 % tensor-pipe activity). TCUDB_GEMM_PAIR=1 selects the
   // CTA-pair (cta_group::2) kernel when M splits into 256-row pair tiles.

@@ -504,15 +504,11 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   k_part_hist<<<(unsigned)chunks, PT, 0, s>>>(io);
   e = exclusive_scan_i32(counts, offs, cnts, nullptr, t, s, launches);
   if (e != cudaSuccess) return e;
-  static bool attr = false;
   // staging per tuple: key 8 + group 4 + digit 1 (+ value 8 for SUM)
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_part_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 21);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_part_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 13);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = set_func_attr(k_part_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 21);
+  if (e != cudaSuccess) return e;
+  e = set_func_attr(k_part_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 13);
+  if (e != cudaSuccess) return e;
   if (v_out) k_part_scatter<true><<<(unsigned)chunks, PT, CH * 21, s>>>(io);
   else k_part_scatter<false><<<(unsigned)chunks, PT, CH * 13, s>>>(io);
   const int64_t so = (int64_t)nseg * R + 1;
@@ -535,11 +531,7 @@ cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa,
                               int64_t* launches) {
   const int tb = ts_bits_for(cap);
   const size_t smem = (size_t)(1 << tb) * 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  set_func_attr(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   // per-partition totals in out[4 ..), their sums in out[0..4)
   k_part_count<<<P, QT, smem, s>>>(ka, offa, kb, offb, tb, out + 4);
@@ -558,12 +550,8 @@ cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, 
                                const long long* vb, unsigned long long* C64) {
   const int tb = ts_bits_for(cap);
   const size_t smem = part_expand_smem(cap, C64 != nullptr);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_part_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_part_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  set_func_attr(k_part_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  set_func_attr(k_part_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   if (C64) k_part_expand<true><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64);
   else k_part_expand<false><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64);

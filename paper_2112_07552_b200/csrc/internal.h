@@ -83,6 +83,17 @@ tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* nc, const tcudb
                                  cudaStream_t s, float* ms_comm);
 tcudb_status shard_agree(const int64_t* descs, int P, int64_t* agreed);
 void shard_bounds(const int64_t* msgs, int P, int64_t* bounds);
+// Stream-ordered scratch from the calling context's own memory pool (tcudb_create makes a
+// private pool: the process's default pool and its release threshold stay the caller's).
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s);
+// ABI entry scope: the context's device and pool for the call; the caller's current device
+// is restored on exit (nested entries restore in order)
+struct CtxScope {
+  int prev_dev = -1;
+  void* prev_pool = nullptr;
+  CtxScope(int device, void* pool);
+  ~CtxScope();
+};
 // host-runtime helpers the collective path shares (tcudb.cu)
 void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s);
 void internal_result_release(tcudb_ctx* ctx, void* p);

@@ -503,13 +503,9 @@ static size_t fused_smem(const SpaArgs& a) {
 
 template <int ACC>
 static cudaError_t launch_fused_t(const SpaArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_spa_fused<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kSmemFused);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = set_func_attr(k_spa_fused<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSmemFused);
+  if (e != cudaSuccess) return e;
   const int64_t grid = std::min<int64_t>(a.nbands, 2 * kNumSMs);
   k_spa_fused<ACC><<<(unsigned)grid, NTF, fused_smem(a), s>>>(a);
   return cudaGetLastError();
@@ -563,12 +559,8 @@ static size_t write_smem(const SpaArgs& a) {
 cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.G <= 0) return cudaSuccess;
   const size_t sm = count_smem(a);
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_spa_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = set_func_attr(k_spa_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  if (e != cudaSuccess) return e;
   k_spa_count<<<(unsigned)((a.nbands + a.count_bands - 1) / a.count_bands), NTC, sm, s>>>(a);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -576,13 +568,9 @@ cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches
 
 template <int ACC>
 static cudaError_t launch_write_t(const SpaArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_spa_write<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kSmemMax);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = set_func_attr(k_spa_write<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSmemMax);
+  if (e != cudaSuccess) return e;
   k_spa_write<ACC><<<(unsigned)((a.G + a.rows - 1) / a.rows), NT, write_smem(a), s>>>(a);
   return cudaGetLastError();
 }

@@ -284,11 +284,7 @@ cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const
   if (n <= 0) return cudaSuccess;
   const int nb = (G + R - 1) / R;  // bands
   const bool smem = (int64_t)nb * 4 <= 160 * 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_active_g_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
+  set_func_attr(k_active_g_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   int64_t blocks = n / std::max<int64_t>(4096, nb / 2);
   if (blocks > kNumSMs) blocks = kNumSMs;
   if (blocks < 1) blocks = 1;
@@ -300,11 +296,7 @@ cudaError_t launch_active_by_g(const int32_t* kcode, const int32_t* gcode, const
   // band; the CTA's run per band is long enough to fill whole sectors); else one global
   // atomic per tuple (many bands: little contention)
   if (nb <= 1024 && n >= (1 << 20)) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(k_active_g_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 12);
-      attr2 = true;
-    }
+    set_func_attr(k_active_g_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 12);
     const int64_t nblk = std::min<int64_t>(2 * kNumSMs, (n + 16383) / 16384);
     const int64_t chunk = (n + nblk - 1) / nblk;
     k_active_g_scatter_smem<<<(int)nblk, 1024, (size_t)nb * 12, s>>>(kcode, gcode, cnt_b, n, chunk, nb, R, goff,

@@ -90,7 +90,7 @@ struct Arena {
   T* get(int64_t count) {
     if (count <= 0) count = 1;
     void* p = nullptr;
-    const cudaError_t e = cudaMallocAsync(&p, (size_t)count * sizeof(T), s);
+    const cudaError_t e = pool_malloc(&p, (size_t)count * sizeof(T), s);
     if (e != cudaSuccess) {
       cudaGetLastError();
       throw Fail{e == cudaErrorMemoryAllocation ? TCUDB_E_NOMEM : TCUDB_E_CUDA, "cudaMallocAsync", e};
@@ -315,7 +315,7 @@ void* result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s) {
     std::lock_guard<std::mutex> g(ctx->mu);
     ctx->dev_from_cb[p] = true;
   } else {
-    const cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    const cudaError_t e = pool_malloc(&p, bytes, s);
     if (e != cudaSuccess) { cudaGetLastError(); throw Fail{TCUDB_E_NOMEM}; }
   }
   return p;
@@ -1548,6 +1548,25 @@ tcudb_status fail_err(tcudb_ctx* ctx, const Fail& f) {
 }  // namespace
 
 namespace tcudb {
+thread_local cudaMemPool_t t_pool = nullptr;  // the pool of the context whose call is running
+
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s) {
+  if (t_pool) return cudaMallocFromPoolAsync(p, bytes, t_pool, s);
+  return cudaMallocAsync(p, bytes, s);
+}
+
+CtxScope::CtxScope(int device, void* pool) {
+  if (cudaGetDevice(&prev_dev) != cudaSuccess) { cudaGetLastError(); prev_dev = -1; }
+  if (prev_dev != device) cudaSetDevice(device);
+  prev_pool = t_pool;
+  t_pool = static_cast<cudaMemPool_t>(pool);
+}
+CtxScope::~CtxScope() {
+  t_pool = static_cast<cudaMemPool_t>(prev_pool);
+  int cur = -1;
+  if (prev_dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev_dev) cudaSetDevice(prev_dev);
+}
+
 void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s) {
   try {
     return result_alloc(ctx, bytes, s);
@@ -1566,8 +1585,8 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
                           tcudb_free_fn free_fn, void* user) {
   if (!out) return TCUDB_E_INVALID;
   *out = nullptr;
-  int major = 0, minor = 0;
-  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return TCUDB_E_CUDA; }
+  int major = 0, minor = 0, ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) { cudaGetLastError(); return TCUDB_E_CUDA; }
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
   if (major != 10 || minor != 0) return TCUDB_E_CUDA;  // built for sm_100a only
@@ -1577,9 +1596,18 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   c->afn = alloc_fn;
   c->ffn = free_fn;
   c->user = user;
-  if (cudaDeviceGetDefaultMemPool(&c->pool, device) != cudaSuccess) { delete c; return TCUDB_E_CUDA; }
-  unsigned long long thr = ~0ull;
-  cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  {
+    // a private stream-ordered pool (scratch is recycled across queries without returning
+    // to the driver; the caller's default pool and its release threshold are untouched)
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&c->pool, &props) != cudaSuccess) { cudaGetLastError(); delete c; return TCUDB_E_CUDA; }
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  CtxScope scope(device, c->pool);
   if (cudaMallocHost(&c->pinned, kPinnedBytes) != cudaSuccess) { delete c; return TCUDB_E_CUDA; }
   {
     size_t fb = 0, tb = 0;
@@ -1630,7 +1658,7 @@ tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_ta
   if (v == TCUDB_OK && ctx->host_fail != TCUDB_OK) { v = ctx->host_fail; why = "host columns could not be staged"; }
   ctx->host_fail = TCUDB_OK;
   if (!(ctx->nc && !ctx->in_collective) && v != TCUDB_OK) return set_err(ctx, v, why);
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (ctx->nc && !ctx->in_collective) {
     // collective call (collective.cu): agreement, routing + exchanges around the local query
@@ -1662,7 +1690,7 @@ tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_ta
     absent |= 1u << side;
     t.group.type = TCUDB_I32;
     if (t.n_rows == 0) continue;
-    if (cudaMallocAsync(&zcol[side], (size_t)t.n_rows * 4, s) != cudaSuccess ||
+    if (pool_malloc(&zcol[side], (size_t)t.n_rows * 4, s) != cudaSuccess ||
         cudaMemsetAsync(zcol[side], 0, (size_t)t.n_rows * 4, s) != cudaSuccess) {
       cudaGetLastError();
       for (void* p : zcol) if (p) cudaFreeAsync(p, s);
@@ -1711,14 +1739,14 @@ tcudb_status tcudb_join_agg_host(tcudb_ctx* ctx, const tcudb_table* A, const tcu
   if (!ctx || !out || !A || !B || !q) return TCUDB_E_INVALID;
   std::memset(out, 0, sizeof(*out));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   std::vector<void*> dev;
   auto up = [&](const tcudb_col& c, int64_t n, tcudb_col& d) -> bool {
     d = c;
     if (!c.data || n == 0) return true;
     const size_t bytes = (size_t)n * ((c.type == TCUDB_I64 || c.type == TCUDB_F64) ? 8 : 4);
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) { cudaGetLastError(); return false; }
+    if (pool_malloc(&p, bytes, s) != cudaSuccess) { cudaGetLastError(); return false; }
     dev.push_back(p);
     if (cudaMemcpyAsync(p, c.data, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return false;
     d.data = p;
@@ -1815,7 +1843,7 @@ tcudb_status tcudb_triangle_count(tcudb_ctx* ctx, int64_t n_edges, const void* s
   if (ctx->sticky) return set_err(ctx, TCUDB_E_CUDA, "context has a sticky CUDA error");
   *triangles_out = 0;
   if (n_edges == 0) return TCUDB_OK;
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   tcudb_stats local{};
   tcudb_stats& S = stats ? *stats : local;
@@ -1882,7 +1910,7 @@ tcudb_status tcudb_gemm(tcudb_ctx* ctx, int32_t elem, int32_t a_signed, int32_t 
                         void* stream) {
   if (!ctx || !A || !B || !C || elem < 0 || elem > 2) return TCUDB_E_INVALID;
   if (elem == 2 && (K % 256 || lda % 2 || ldb % 2 || N % kGemmBNFp4)) return TCUDB_E_INVALID;
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   GemmArgs ga{};
   ga.elem = elem; ga.a_signed = a_signed; ga.b_signed = b_signed; ga.M = M; ga.N = N; ga.k_begin = 0; ga.k_len = K;
   ga.A = A; ga.lda = lda; ga.B = B; ga.ldb = ldb; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = ldc;
@@ -1899,7 +1927,7 @@ tcudb_status tcudb_minmax(tcudb_ctx* ctx, const void* col, int32_t type, int64_t
   *mn = INT64_MAX;
   *mx = INT64_MIN;
   if (n == 0) return TCUDB_OK;
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   try {
     Arena ar(s);
@@ -1924,7 +1952,7 @@ tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_
     return TCUDB_E_INVALID;
   for (int i = 0; i < P; ++i) counts[i] = 0;
   if (in->n_rows == 0) return TCUDB_OK;
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   try {
     Arena ar(s);
@@ -1988,7 +2016,7 @@ int32_t tcudb_calibration(const tcudb_ctx* ctx, double* out7) {
 
 void tcudb_destroy(tcudb_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
+  CtxScope scope(ctx->device, ctx->pool);
   cudaDeviceSynchronize();
   for (auto& kv : ctx->host_size) cudaFreeHost(kv.first);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -1996,6 +2024,8 @@ void tcudb_destroy(tcudb_ctx* ctx) {
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->evk) if (e) cudaEventDestroy(e);
   if (ctx->nc) nccl_detach(ctx->nc);
+  cudaDeviceSynchronize();
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }
 

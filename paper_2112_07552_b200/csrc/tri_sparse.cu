@@ -185,13 +185,9 @@ cudaError_t launch_tri_sparse(const int32_t* cu, const int32_t* cv, int64_t n, i
     k_tri_orient<<<grid_for(m), T, 0, s>>>(eu, ev, m, deg, odeg, nullptr, nullptr, nullptr, 0);
     if ((e = exclusive_scan_i32(odeg, ooff, V, ooff + V, stmp, s, launches)) != cudaSuccess) return e;
     k_tri_orient<<<grid_for(m), T, 0, s>>>(eu, ev, m, deg, nullptr, ooff, ocur, adj, 1);
-    static bool attr = false;
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(k_tri_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) !=
-          cudaSuccess)
-        return e;
-      attr = true;
-    }
+    if ((e = set_func_attr(k_tri_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) !=
+        cudaSuccess)
+      return e;
     unsigned long long* ticket = reinterpret_cast<unsigned long long*>(ocur);  // reused: 8 bytes, zeroed below
     if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) return e;
     const int per_sm = smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
