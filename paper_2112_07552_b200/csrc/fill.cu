@@ -625,6 +625,258 @@ cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, 
   return cudaGetLastError();
 }
 
+// ---- tiled bf16 direct fill (one binning level): the operand is cut into tiles of
+// 65,536 cells (R rows x KW columns, KW = a power of two <= 8192); every tuple becomes a
+// 4-byte entry (cell in tile << 16 | bf16 bits) binned by tile in ONE pass — large batches
+// (16 K tuples per CTA) staged in shared memory so each tile's entries leave as runs — and
+// one CTA per tile builds the tile in shared memory and writes it out coalesced, zeros
+// included. Per tuple: 4-8 B (hist) + 12 B read + 4 B written (bin) + 4 B read + 2 B
+// written (tile), vs the scattered 2-byte stores of the direct / row-range fills that
+// are bound by L2's partial-sector store rate.
+namespace {
+constexpr int kT2Threads = 1024;
+constexpr int kT2Batch = 16 * kT2Threads;
+constexpr int kT2MaxTiles = 4096;
+constexpr int kT2TileCells = 65536;
+struct T2Plan {
+  int KW = 0, R = 0, nkt = 0, ntiles = 0, nblk = 0, kw_bits = 0;
+  int64_t chunk = 0;
+  size_t off_counts = 0, off_offs = 0, off_temp = 0, off_ent = 0, bytes = 0;
+};
+T2Plan t2_plan(int64_t n, int64_t rows, int64_t Kp) {
+  T2Plan p;
+  if (n < (1 << 20) || Kp % 8) return p;
+  int KW = 128, kb = 7;
+  while (KW < Kp && KW < 8192) { KW *= 2; ++kb; }
+  const int R = kT2TileCells / KW;
+  const int64_t nkt = (Kp + KW - 1) / KW, nrt = (rows + R - 1) / R;
+  if (nkt * nrt > kT2MaxTiles) return p;
+  p.KW = KW; p.kw_bits = kb; p.R = R; p.nkt = (int)nkt; p.ntiles = (int)(nkt * nrt);
+  p.nblk = (int)std::min<int64_t>(kNumSMs, (n + kT2Batch - 1) / kT2Batch);
+  p.chunk = ((n + p.nblk - 1) / p.nblk + 3) & ~int64_t(3);  // 16-byte aligned chunks
+  const int64_t m = (int64_t)p.ntiles * p.nblk;
+  p.off_counts = 0;
+  p.off_offs = al256(m * 4);
+  p.off_temp = p.off_offs + al256((m + 1) * 8);
+  p.off_ent = p.off_temp + al256(scan_temp_bytes(m));
+  p.bytes = p.off_ent + al256(n * 4);
+  return p;
+}
+
+TCUDB_DEV int t2_tile(int r, int kc, int R, int kw_bits, int nkt) { return (r / R) * nkt + (kc >> kw_bits); }
+
+// per-(tile, block) counts, tile-major (the scan gives each block its run per tile)
+__global__ void __launch_bounds__(kT2Threads) k_t2_hist(const int32_t* __restrict__ kcode,
+                                                        const int32_t* __restrict__ rcode, int64_t n, int64_t chunk,
+                                                        int R, int kw_bits, int nkt, int ntiles,
+                                                        int32_t* __restrict__ counts) {
+  __shared__ int hist[kT2MaxTiles];
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = max(lo, min(n, lo + chunk));
+  auto one = [&](int kc, int r) { if (kc >= 0) atomicAdd(&hist[t2_tile(r, kc, R, kw_bits, nkt)], 1); };
+  const int64_t v1 = hi / 4;
+  for (int64_t v = lo / 4 + threadIdx.x; v < v1; v += blockDim.x) {
+    const int4 k = __ldcs(reinterpret_cast<const int4*>(kcode) + v);
+    const int4 r = __ldcs(reinterpret_cast<const int4*>(rcode) + v);
+    one(k.x, r.x); one(k.y, r.y); one(k.z, r.z); one(k.w, r.w);
+  }
+  for (int64_t i = v1 * 4 + threadIdx.x; i < hi; i += blockDim.x) one(kcode[i], rcode[i]);
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(int64_t)t * gridDim.x + blockIdx.x] = hist[t];
+}
+
+__global__ void __launch_bounds__(kT2Threads, 1) k_t2_bin(const int32_t* __restrict__ kcode,
+                                                         const int32_t* __restrict__ rcode,
+                                                         const float* __restrict__ val, int64_t n, int64_t chunk,
+                                                         int R, int KW, int kw_bits, int nkt, int ntiles,
+                                                         const int64_t* __restrict__ offs,
+                                                         uint32_t* __restrict__ ent, FillStats* __restrict__ fs) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem);                       // [kT2Batch]
+  uint16_t* stile = reinterpret_cast<uint16_t*>(stage + kT2Batch);           // [kT2Batch]
+  int64_t* gcur = reinterpret_cast<int64_t*>(stile + kT2Batch);             // [ntiles]
+  int* cnt = reinterpret_cast<int*>(gcur + ntiles);                          // [ntiles]
+  int* bstart = cnt + ntiles;                                                // [ntiles]
+  __shared__ int wsum[kT2Threads / 32];
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    gcur[t] = offs[(int64_t)t * gridDim.x + blockIdx.x];
+    cnt[t] = 0;
+  }
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = max(lo, min(n, lo + chunk));
+  const bool vec_val = val && (reinterpret_cast<uintptr_t>(val) & 15) == 0;
+  const int per = (ntiles + kT2Threads - 1) / kT2Threads;  // counters per thread in the scan
+  int inexact = 0;
+  for (int64_t b0 = lo; b0 < hi; b0 += kT2Batch) {
+    constexpr int U = kT2Batch / kT2Threads / 4;  // int4 vectors per thread per column
+    uint32_t e[4 * U];
+    int tl[4 * U], rk[4 * U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = b0 + ((int64_t)u * kT2Threads + threadIdx.x) * 4;
+      int kc[4] = {-1, -1, -1, -1}, r[4] = {0, 0, 0, 0};
+      uint32_t bv[4] = {0x3F800000u, 0x3F800000u, 0x3F800000u, 0x3F800000u};  // absent value = 1.0
+      if (i + 3 < hi) {
+        const int4 k4 = __ldcs(reinterpret_cast<const int4*>(kcode + i));
+        const int4 r4 = __ldcs(reinterpret_cast<const int4*>(rcode + i));
+        kc[0] = k4.x; kc[1] = k4.y; kc[2] = k4.z; kc[3] = k4.w;
+        r[0] = r4.x; r[1] = r4.y; r[2] = r4.z; r[3] = r4.w;
+        if (vec_val) {
+          const uint4 b4 = __ldcs(reinterpret_cast<const uint4*>(val + i));
+          bv[0] = b4.x; bv[1] = b4.y; bv[2] = b4.z; bv[3] = b4.w;
+        } else if (val) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) bv[q] = __float_as_uint(val[i + q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i + q < hi) {
+            kc[q] = kcode[i + q];
+            r[q] = rcode[i + q];
+            if (val) bv[q] = __float_as_uint(val[i + q]);
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int x = 4 * u + q;
+        tl[x] = -1;
+        if (kc[q] < 0) continue;
+        inexact |= (bv[q] & 0xFFFFu) != 0u;
+        tl[x] = t2_tile(r[q], kc[q], R, kw_bits, nkt);
+        const uint32_t cell = (uint32_t)((r[q] % R) * KW + (kc[q] & (KW - 1)));  // < 65536
+        e[x] = (cell << 16) | (bv[q] >> 16);
+        rk[x] = atomicAdd(&cnt[tl[x]], 1);
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the ntiles counts: each thread a contiguous run of `per`
+    {
+      const int t0 = threadIdx.x * per;
+      int run = 0;
+      for (int q = 0; q < per; ++q) run += t0 + q < ntiles ? cnt[t0 + q] : 0;
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane_id() >= o) incl += t;
+      }
+      if (lane_id() == 31) wsum[warp_id()] = incl;
+      __syncthreads();
+      if (warp_id() == 0) {
+        const int w = wsum[lane_id()];
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane_id() >= o) wi += t;
+        }
+        wsum[lane_id()] = wi - w;
+      }
+      __syncthreads();
+      int x = wsum[warp_id()] + incl - run;
+      for (int q = 0; q < per; ++q)
+        if (t0 + q < ntiles) { bstart[t0 + q] = x; x += cnt[t0 + q]; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 4 * U; ++x)
+      if (tl[x] >= 0) {
+        const int j = bstart[tl[x]] + rk[x];
+        stage[j] = e[x];
+        stile[j] = (uint16_t)tl[x];
+      }
+    __syncthreads();
+    const int total = bstart[ntiles - 1] + cnt[ntiles - 1];
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      const int t = stile[j];
+      __stcg(ent + gcur[t] + (j - bstart[t]), stage[j]);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+      gcur[t] += cnt[t];
+      cnt[t] = 0;
+    }
+    __syncthreads();
+  }
+  inexact = __syncthreads_or(inexact);
+  if (threadIdx.x == 0 && inexact) atomicOr(&fs->inexact, 1);
+}
+
+// one CTA per tile: R x KW bf16 cells + occupancy bits in shared memory
+__global__ void __launch_bounds__(kT2Threads, 1) k_t2_tile(const uint32_t* __restrict__ ent,
+                                                          const int64_t* __restrict__ offs, int nblk, int R, int KW,
+                                                          int nkt, int64_t rows, int64_t Kp,
+                                                          uint16_t* __restrict__ op, int64_t ld_op,
+                                                          FillStats* __restrict__ fs) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
+  unsigned* occ = reinterpret_cast<unsigned*>(smem + (size_t)kT2TileCells * 2);
+  for (int i = threadIdx.x; i < kT2TileCells / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(tile)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < kT2TileCells / 32; i += blockDim.x) occ[i] = 0;
+  __syncthreads();
+  const int t = blockIdx.x;
+  const int64_t lo = offs[(int64_t)t * nblk], hi = offs[(int64_t)(t + 1) * nblk];
+  int dup = 0;
+  constexpr int U = 4;
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)U * blockDim.x) {
+    uint32_t e[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      e[u] = i < hi ? __ldcs(ent + i) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + (int64_t)u * blockDim.x >= hi) continue;
+      const uint32_t c = e[u] >> 16;
+      tile[c] = (uint16_t)(e[u] & 0xFFFFu);
+      dup |= (int)((atomicOr(&occ[c >> 5], 1u << (c & 31)) >> (c & 31)) & 1u);
+    }
+  }
+  __syncthreads();
+  const int64_t r0 = (int64_t)(t / nkt) * R, c0 = (int64_t)(t % nkt) * KW;
+  const int nrow = (int)min((int64_t)R, rows - r0);
+  const int ncol = (int)min((int64_t)KW, Kp - c0);  // multiple of 8
+  const int v8 = ncol / 8;
+  for (int i = threadIdx.x; i < nrow * v8; i += blockDim.x) {
+    const int r = i / v8, c = i - r * v8;
+    __stcs(reinterpret_cast<uint4*>(op + (r0 + r) * ld_op + c0) + c,
+           reinterpret_cast<const uint4*>(tile + (int64_t)r * KW)[c]);
+  }
+  dup = __syncthreads_or(dup);
+  if (threadIdx.x == 0 && dup) atomicOr(&fs->overflow, 1);
+}
+}  // namespace
+
+size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp) { return t2_plan(n, rows, Kp).bytes; }
+
+cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                   int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
+                                   cudaStream_t s, int64_t* launches) {
+  const T2Plan p = t2_plan(n, rows, Kp);
+  if (!p.bytes) return cudaErrorInvalidValue;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int32_t* counts = reinterpret_cast<int32_t*>(w + p.off_counts);
+  int64_t* offs = reinterpret_cast<int64_t*>(w + p.off_offs);
+  uint32_t* ent = reinterpret_cast<uint32_t*>(w + p.off_ent);
+  const int64_t m = (int64_t)p.ntiles * p.nblk;
+  k_t2_hist<<<p.nblk, kT2Threads, 0, s>>>(kcode, rcode, n, p.chunk, p.R, p.kw_bits, p.nkt, p.ntiles, counts);
+  cudaError_t e = exclusive_scan_i32(counts, offs, m, offs + m, w + p.off_temp, s, launches);
+  if (e != cudaSuccess) return e;
+  const int bin_smem = kT2Batch * 6 + p.ntiles * 16;
+  if ((e = set_func_attr(k_t2_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, bin_smem)) != cudaSuccess) return e;
+  k_t2_bin<<<p.nblk, kT2Threads, bin_smem, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, p.chunk, p.R,
+                                                p.KW, p.kw_bits, p.nkt, p.ntiles, offs, ent, fs);
+  const int tile_smem = kT2TileCells * 2 + kT2TileCells / 8;
+  if ((e = set_func_attr(k_t2_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem)) != cudaSuccess) return e;
+  k_t2_tile<<<p.ntiles, kT2Threads, tile_smem, s>>>(ent, offs, p.nblk, p.R, p.KW, p.nkt, rows, Kp, op, ld_op, fs);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,
                                   int64_t ld_elems, FillStats* fs, cudaStream_t s, int64_t* launches) {
   if (n <= 0) return cudaSuccess;

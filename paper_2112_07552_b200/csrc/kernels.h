@@ -123,6 +123,12 @@ cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, 
 // shape does not fit the scheme (caller uses the direct fill). Duplicate cells set
 // fs->overflow; inexact values set fs->inexact.
 size_t fill_bf16_binned_ws(int64_t n, int64_t rows, int64_t Kp);
+// Tiled direct fill (one binning level into 65,536-cell tiles, then one CTA per tile);
+// workspace bytes (0: shape not supported), fs->inexact / fs->overflow as the binned fill.
+size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp);
+cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                   int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
+                                   cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                     int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
                                     cudaStream_t s, int64_t* launches);

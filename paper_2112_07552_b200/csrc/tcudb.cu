@@ -291,6 +291,7 @@ struct Timer {
   // elapsed between consecutive marks is written into the slot of the later mark
   void finish() {
     if (!on) return;
+    if (n > 0) cudaEventSynchronize(ctx->ev[n - 1]);  // an early return may not have synced past it
     for (int i = 1; i < n; ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]);
@@ -923,12 +924,25 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         // that the re-reads of the tuple columns per range cost more than the binned fill
         // (~13 ps per tuple at c4). TCUDB_FILL_PASSES=n forces n ranges, 0 the binned fill.
         const char* fp_env = getenv("TCUDB_FILL_PASSES");
+        // The tiled fill (one binning level into 65,536-cell tiles written coalesced from
+        // shared memory) is the default whenever its tile count fits; TCUDB_FILL_MODE=range /
+        // binned / direct selects the earlier fills (kept for comparison and small shapes).
+        const char* fm_env = getenv("TCUDB_FILL_MODE");
+        const std::string fill_mode = fm_env ? fm_env : "";
         auto direct_fill = [&](int side, const int32_t* kc, const int32_t* rc, const ColDesc& v, int64_t n,
                                int64_t rows, uint16_t* op) {
+          const size_t ws_t = (fill_mode.empty() || fill_mode == "tiled") ? fill_bf16_tiled_ws(n, rows, Kp) : 0;
+          if (ws_t) {
+            binned[side] = true;  // duplicate check: fs.overflow (occupancy bits)
+            ranged[side] = false;
+            CK(launch_fill_bf16_tiled(kc, rc, v, n, rows, Kp, op, ldop, fs + side, ar.get<uint8_t>((int64_t)ws_t), s, L));
+            return;
+          }
           const int64_t auto_p = (rows * Kp * 2 + kFillRangeBytes - 1) / kFillRangeBytes;
-          const int fill_passes = fp_env ? atoi(fp_env) : (auto_p <= 3 && Kp % 8 == 0 ? (int)auto_p : 0);
+          const int fill_passes = fp_env ? atoi(fp_env) : fill_mode == "binned" || fill_mode == "direct" ? 0
+                                  : (auto_p <= 3 && Kp % 8 == 0 ? (int)auto_p : 0);
           const char* nb = getenv("TCUDB_NO_BINNED_FILL");
-          const size_t ws = (nb && nb[0] == '1') ? 0 : fill_bf16_binned_ws(n, rows, Kp);
+          const size_t ws = (nb && nb[0] == '1') || fill_mode == "direct" ? 0 : fill_bf16_binned_ws(n, rows, Kp);
           binned[side] = ws != 0 && fill_passes <= 0;
           ranged[side] = fill_passes > 0;
           if (ranged[side]) {

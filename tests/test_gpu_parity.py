@@ -907,3 +907,32 @@ def test_selector_calibration_measured(engine):
     assert 1.0e15 < c["R_i8"] < 5.0e15 and 0.5e15 < c["R_bf16"] < 2.5e15 and 2.0e15 < c["R_fp4"] < 1.0e16, c
     assert 3.0e12 < c["BW"] < 9.0e12, c
     assert 1.25e10 <= c["R_sp"] <= 2.0e11 and 10e-6 <= c["T_sp0"] <= 400e-6, c
+
+
+@pytest.mark.parametrize("mode", ["tiled", "range", "binned"])
+@pytest.mark.parametrize("case", ["unique", "dup_nonzero", "dup_zero_after", "zero_values", "inexact"])
+def test_bf16_fill_modes_large(engine, torch_mod, oracle_mod, monkeypatch, mode, case):
+    """The bf16 direct fills on >= 2^20 tuples (the tiled fill's size): 1024 x 1024 cells in
+    shuffled order, ragged G (1000 rows), a duplicate cell (nonzero / zero second value),
+    zero values, a non-bf16-exact value (-> fp32 scratch path). All equal the oracle."""
+    monkeypatch.setenv("TCUDB_FILL_MODE", mode)
+    rng = np.random.default_rng(12)
+    n, m = 1000, 1088
+    cells = rng.permutation(n * m)
+    ag, ak = (cells // m).astype(np.int32), (cells % m).astype(np.int32)
+    av = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, n * m).astype(np.float32))
+    if case == "dup_nonzero":
+        ag, ak, av = np.append(ag, ag[5]), np.append(ak, ak[5]), np.append(av, np.float32(0.5))
+    elif case == "dup_zero_after":
+        ag, ak, av = np.append(ag, ag[5]), np.append(ak, ak[5]), np.append(av, np.float32(0.0))
+    elif case == "zero_values":
+        av[::7] = 0.0
+    elif case == "inexact":
+        av[123] = np.float32(0.1)
+    bk = np.tile(np.arange(m, dtype=np.int32), 3)
+    bh = np.repeat(np.arange(3, dtype=np.int32), m)
+    bw = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, 3 * m).astype(np.float32))
+    A, B = datagen.Table(ak, ag, av), datagen.Table(bk, bh, bw)
+    out, st = run(engine, torch_mod, A, B, "sum", flags=1)
+    assert st["path"] == 0
+    compare(out, oracle_mod.join_agg(A, B, "sum"), "sum", float_vals=True)
