@@ -20,29 +20,12 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "dict.cuh"
 
 namespace tcudb {
 namespace {
 
 constexpr int T = 256;
-
-TCUDB_DEV unsigned long long fmix64(unsigned long long k) {
-  k ^= k >> 33; k *= 0xff51afd7ed558ccdULL;
-  k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ULL;
-  k ^= k >> 33;
-  return k;
-}
-TCUDB_DEV unsigned fmix32(unsigned k) {
-  k ^= k >> 16; k *= 0x85ebca6bu;
-  k ^= k >> 13; k *= 0xc2b2ae35u;
-  k ^= k >> 16;
-  return k;
-}
-// Hash-dictionary slot hash of an offset x - min: 32-bit finalizer when every offset fits
-// 32 bits (two 32-bit multiplies instead of two 64-bit ones), else the 64-bit one.
-TCUDB_DEV unsigned long long slot_hash(unsigned long long off, int wide) {
-  return wide ? fmix64(off) : (unsigned long long)fmix32((unsigned)off);
-}
 
 // ------------------------------------------------------------------ a1: statistics
 // Block-level reduction, then ONE set of atomics per block: same-address global
@@ -356,6 +339,7 @@ __global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long 
     if (placed < 0) *overflow = 1;
     else if (!flags[placed]) flags[placed] = 1;
   }
+  if (!row_slot) return;  // dictionary only: the caller looks values up itself
   __syncthreads();
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const unsigned long long off = (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv;
@@ -581,46 +565,6 @@ __global__ void k_remap_codes(int32_t* __restrict__ codes, int64_t n, const int3
 }
 
 // ------------------------------------------------------------------ probe (codes per tuple)
-TCUDB_DEV int32_t dict_lookup(const DictView& d, long long x) {
-  const unsigned long long off = (unsigned long long)x - (unsigned long long)d.minv;
-  if (d.mode == 0) return off < d.size ? d.code[off] : -1;
-  unsigned long long h = slot_hash(off, d.wide) & d.size;  // size = mask in hash mode
-  while (true) {
-    const unsigned long long k = d.slots[h];
-    if (k == off) return d.code[h];
-    if (k == ~0ull) return -1;
-    h = (h + 1) & d.size;
-  }
-}
-
-// U lookups with their first loads issued together (the probe is latency-bound).
-template <int U>
-TCUDB_DEV void dict_lookup_batch(const DictView& d, const long long* x, const bool* ok, int32_t* out) {
-  unsigned long long off[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) off[u] = (unsigned long long)x[u] - (unsigned long long)d.minv;
-  if (d.mode == 0) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) out[u] = (ok[u] && off[u] < d.size) ? __ldg(d.code + off[u]) : -1;
-    return;
-  }
-  unsigned long long h[U], k[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    h[u] = slot_hash(off[u], d.wide) & d.size;
-    k[u] = ok[u] ? __ldg(d.slots + h[u]) : off[u];
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    while (k[u] != off[u] && k[u] != ~0ull) {
-      h[u] = (h[u] + 1) & d.size;
-      k[u] = __ldg(d.slots + h[u]);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) out[u] = (ok[u] && k[u] == off[u]) ? __ldg(d.code + h[u]) : -1;
-}
-
 // Codes of rows i0 + u * stride: through the insert's per-row slots when present
 // (code[row_slot[i]], one gather from an L2-sized table), else by value.
 template <int U>
@@ -898,7 +842,7 @@ cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long l
   // shared-memory pre-aggregation when the estimated distinct count is small and
   // there are many tuples per distinct value (tables sized 2^ceil(log2(1.9 est)))
   const int64_t cap = (int64_t)mask + 1;
-  if (est_distinct > 0 && row_slot && cap <= 16384 && c.n >= 64 * cap) {
+  if (est_distinct > 0 && cap <= 16384 && c.n >= 64 * cap) {
     const int cap_s = (int)cap;  // >= 1.9 x the global distinct count, so >= any block's
     const size_t smem = (size_t)cap_s * 12;
     set_func_attr(k_hash_insert_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 12);

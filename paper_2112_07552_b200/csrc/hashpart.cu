@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "dict.cuh"
 
 namespace tcudb {
 namespace {
@@ -85,7 +86,8 @@ __global__ void __launch_bounds__(kCsThreads) k_chunk_starts(const int64_t* __re
 }
 
 struct PassIO {
-  const void* raw; int raw_type; long long kmin; const int32_t* g_raw;  // pass 1 (raw column)
+  const void* raw; int raw_type; long long kmin;                        // pass 1 (raw key column)
+  ColDesc gcol; DictView gd;                                            // pass 1: raw groups -> codes
   const void* v_raw; int v_type;                                        // pass 1 values (SUM)
   const unsigned long long* k_in; const int32_t* g_in;
   const long long* v_in; long long* v_out;                              // value payload (SUM)
@@ -96,15 +98,6 @@ struct PassIO {
   unsigned long long* k_out; int32_t* g_out; int64_t* seg_out;
 };
 
-TCUDB_DEV void load_tuple(const PassIO& io, int64_t i, unsigned long long& k, int32_t& g) {
-  if (io.raw) {
-    k = (unsigned long long)ld_int(io.raw, io.raw_type, i) - (unsigned long long)io.kmin;
-    g = io.g_raw[i];
-  } else {
-    k = io.k_in[i];
-    g = io.g_in[i];
-  }
-}
 TCUDB_DEV long long load_value(const PassIO& io, int64_t i) {
   if (!io.v_out) return 0;
   if (io.raw) return io.v_raw ? ld_int(io.v_raw, io.v_type, i) : 1;
@@ -166,16 +159,35 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
   int32_t g[4];
   long long v[4];
   int d[4], r[4];
+  bool ok[4];
+  long long graw[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int64_t i = lo + threadIdx.x + u * PT;
+    ok[u] = i < hi;
     d[u] = -1;
-    if (i < hi) {
-      load_tuple(io, i, k[u], g[u]);
+    k[u] = 0;
+    g[u] = 0;
+    graw[u] = 0;
+    if (ok[u]) {
+      if (io.raw) {
+        k[u] = (unsigned long long)ld_int(io.raw, io.raw_type, i) - (unsigned long long)io.kmin;
+        graw[u] = ld_int(io.gcol.data, io.gcol.type, i);
+      } else {
+        k[u] = io.k_in[i];
+        g[u] = io.g_in[i];
+      }
       if (VAL) v[u] = load_value(io, i);
-      d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
-      r[u] = atomicAdd(&cnt[d[u]], 1);
     }
+  }
+  // pass 1: group codes straight from the finished group dictionary (L2-resident), so the
+  // per-tuple code column is never written and read back
+  if (io.raw) dict_lookup_batch<4>(io.gd, graw, ok, g);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (!ok[u]) continue;
+    d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
+    r[u] = atomicAdd(&cnt[d[u]], 1);
   }
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of <= 128 digit counts, 4 per lane
@@ -269,7 +281,7 @@ TCUDB_DEV int tab_find(const unsigned long long* keys, int mask, int ts_bits, un
 __global__ void __launch_bounds__(QT) k_part_count(const unsigned long long* __restrict__ ka,
                                                    const int64_t* __restrict__ offa,
                                                    const unsigned long long* __restrict__ kb,
-                                                   const int64_t* __restrict__ offb, int ts_bits,
+                                                   const int64_t* __restrict__ offb, int ts_bits, int stride,
                                                    unsigned long long* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int TS = 1 << ts_bits, mask = TS - 1;
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(QT) k_part_count(const unsigned long long* __r
   int* cb = ca + TS;
   for (int i = threadIdx.x; i < TS; i += QT) { keys[i] = ~0ull; ca[i] = 0; cb[i] = 0; }
   __syncthreads();
-  const int p = blockIdx.x;
+  const int p = blockIdx.x * stride;  // stride > 1: a sample of the partitions (the selector's estimate)
   // 4 key loads in flight per thread ahead of the shared-memory probes
   constexpr int NU = 4;
   for (int64_t i0 = offb[p] + threadIdx.x, e = offb[p + 1]; i0 < e; i0 += NU * QT) {
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(QT) k_part_count(const unsigned long long* __r
   if (threadIdx.x < 4) {
     unsigned long long t = 0;
     for (int w = 0; w < QT / 32; ++w) t += red[threadIdx.x][w];
-    out[(int64_t)p * 4 + threadIdx.x] = t;
+    out[(int64_t)blockIdx.x * 4 + threadIdx.x] = t;
   }
 }
 
@@ -367,9 +379,12 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
                                                     unsigned* __restrict__ C, int64_t ldc,
                                                     const long long* __restrict__ va,
                                                     const long long* __restrict__ vb,
-                                                    unsigned long long* __restrict__ C64) {
+                                                    unsigned long long* __restrict__ C64,
+                                                    unsigned long long* __restrict__ jk) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int wsum[QTE / 32];
+  __shared__ unsigned long long jred[QTE / 32];
+  __shared__ int kred;
   const int TS = 1 << ts_bits, mask = TS - 1;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
   int* cnt = reinterpret_cast<int*>(keys + TS);   // per slot: B tuples, then the bucket cursor
@@ -377,7 +392,10 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
   int* bslot = start + TS;                        // per B tuple of the partition: its slot
   int* bh = bslot + cap;                          // B group codes bucketed by slot
   long long* bw = reinterpret_cast<long long*>(smem + (size_t)TS * 16 + (size_t)cap * 8);  // SUM: B values, bucketed
+  unsigned* hit = reinterpret_cast<unsigned*>(smem + (size_t)TS * 16 + (size_t)cap * (SUM ? 16 : 8));  // [TS / 32]
   for (int i = threadIdx.x; i < TS; i += QTE) { keys[i] = ~0ull; cnt[i] = 0; }
+  for (int i = threadIdx.x; i < TS / 32; i += QTE) hit[i] = 0;
+  if (threadIdx.x == 0) kred = 0;
   __syncthreads();
   const int p = blockIdx.x;
   const int64_t b0 = offb[p];
@@ -416,6 +434,7 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
   }
   __syncthreads();
   const unsigned long long pol = l2_keep_policy();
+  unsigned long long jp = 0;  // this thread's joined pairs (the exact J_p of the partition)
   constexpr int U = 4;  // A keys and group codes loaded ahead of the probes
   const int64_t ea = offa[p + 1];
   for (int64_t i0 = offa[p] + threadIdx.x; i0 < ea; i0 += U * QTE) {
@@ -435,6 +454,8 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
     if (h < 0) continue;
     const int n = cnt[h];
     if (n == 0) continue;
+    jp += (unsigned long long)n;
+    if (!(hit[h >> 5] & (1u << (h & 31)))) atomicOr(hit + (h >> 5), 1u << (h & 31));
     const int64_t r = (int64_t)gg[u] * ldc;
     unsigned* row = C + r;
     const int e0 = start[h];
@@ -451,6 +472,23 @@ __global__ void __launch_bounds__(QTE) k_part_expand(const unsigned long long* _
       for (int e = 0; e < n; ++e) red_keep(row + bh[e0 + e], 1u, pol);
     }
    }
+  }
+  // J_p and K_p (keys with a B bucket and at least one A tuple) for the stats and guards
+  jp = warp_sum(jp);
+  if (lane_id() == 0) jred[warp_id()] = jp;
+  __syncthreads();
+  int kc = 0;
+  for (int i = threadIdx.x; i < TS / 32; i += QTE) kc += __popc(hit[i]);
+  kc = warp_sum(kc);
+  if (lane_id() == 0 && kc) atomicAdd(&kred, kc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < QTE / 32; ++w) t += jred[w];
+    jk[(int64_t)p * 4 + 0] = t;
+    jk[(int64_t)p * 4 + 1] = (unsigned long long)kred;
+    jk[(int64_t)p * 4 + 2] = 0;
+    jk[(int64_t)p * 4 + 3] = 0;
   }
 }
 
@@ -474,7 +512,7 @@ size_t hashpart_temp_bytes(int64_t n, int nseg, int bits) {
          ((size_t)(cnts + 1) * 8 + 255) / 256 * 256 + scan_temp_bytes(cnts);
 }
 
-cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
+cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const ColDesc* g_col, const DictView* gd,
                              const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
                              int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
                              int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
@@ -491,7 +529,8 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   int64_t* offs = reinterpret_cast<int64_t*>(t);
   t += ((size_t)(cnts + 1) * 8 + 255) / 256 * 256;
   PassIO io{};
-  io.raw = raw ? raw->data : nullptr; io.raw_type = raw ? raw->type : 0; io.kmin = kmin; io.g_raw = g_raw;
+  io.raw = raw ? raw->data : nullptr; io.raw_type = raw ? raw->type : 0; io.kmin = kmin;
+  if (raw) { io.gcol = *g_col; io.gd = *gd; }
   io.k_in = k_in; io.g_in = g_in; io.seg_off = seg_off; io.nseg = nseg; io.shift = shift; io.bits = bits;
   io.chunk_start = chunk_start; io.counts = counts; io.offs = offs;
   io.k_out = k_out; io.g_out = g_out; io.seg_out = seg_out;
@@ -528,34 +567,37 @@ static int ts_bits_for(int cap) {
 
 cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa, const unsigned long long* kb,
                               const int64_t* offb, int P, int cap, unsigned long long* out, cudaStream_t s,
-                              int64_t* launches) {
+                              int64_t* launches, int stride) {
   const int tb = ts_bits_for(cap);
   const size_t smem = (size_t)(1 << tb) * 16;
   set_func_attr(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   // per-partition totals in out[4 ..), their sums in out[0..4)
-  k_part_count<<<P, QT, smem, s>>>(ka, offa, kb, offb, tb, out + 4);
-  k_part_sum<<<1, 1024, 0, s>>>(out + 4, P, out);
+  const int np = (P + stride - 1) / stride;
+  k_part_count<<<np, QT, smem, s>>>(ka, offa, kb, offb, tb, stride, out + 4);
+  k_part_sum<<<1, 1024, 0, s>>>(out + 4, np, out);
   if (launches) *launches += 2;
   return cudaGetLastError();
 }
 
 size_t part_expand_smem(int cap, bool sum) {
-  return (size_t)(1 << ts_bits_for(cap)) * 16 + (size_t)cap * (sum ? 16 : 8);
+  return (size_t)(1 << ts_bits_for(cap)) * 16 + (size_t)cap * (sum ? 16 : 8) + (size_t)(1 << ts_bits_for(cap)) / 8;
 }
 
 cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, const int64_t* offa,
                                const unsigned long long* kb, const int32_t* hb, const int64_t* offb, int P, int cap,
                                unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches, const long long* va,
-                               const long long* vb, unsigned long long* C64) {
+                               const long long* vb, unsigned long long* C64, unsigned long long* jk) {
   const int tb = ts_bits_for(cap);
   const size_t smem = part_expand_smem(cap, C64 != nullptr);
   set_func_attr(k_part_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   set_func_attr(k_part_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (C64) k_part_expand<true><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64);
-  else k_part_expand<false><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64);
-  if (launches) ++*launches;
+  // jk: 4 + 4 P entries (per-partition J_p, K_p after the 4 totals, summed below)
+  if (C64) k_part_expand<true><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64, jk + 4);
+  else k_part_expand<false><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64, jk + 4);
+  k_part_sum<<<1, 1024, 0, s>>>(jk + 4, P, jk);
+  if (launches) *launches += 2;
   return cudaGetLastError();
 }
 

@@ -244,7 +244,9 @@ size_t hashpart_temp_bytes(int64_t n, int nseg, int bits);
 // (fmix64(koff) >> shift) & (2^bits - 1); output segment-major, then digit. in_raw: pass 1
 // reads the raw key column and the gcode array instead of (k_in, g_in). seg_out (nseg *
 // 2^bits + 1) receives the new segment offsets.
-cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
+// pass 1 (raw != NULL): raw key column + raw group column g_col with its finished
+// dictionary gd (group codes looked up in the pass); later passes: k_in / g_in
+cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const ColDesc* g_col, const DictView* gd,
                              const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
                              int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
                              int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
@@ -254,16 +256,20 @@ size_t part_expand_smem(int cap, bool sum);
 // per partition: J_p = sum over its keys of cntA*cntB, D_p = #keys on both sides; out has
 // 4 + 4 P entries: totals out[0] (J), out[1] (K = sum D_p), out[2] (A tuples with a matched
 // key), out[3] (distinct B keys); per-partition values after them
+// stride > 1: only partitions 0, stride, 2 stride, ... (a sample for the selector's
+// estimate; the per-partition values are then those of the sampled partitions)
 cudaError_t launch_part_count(const unsigned long long* ka, const int64_t* offa, const unsigned long long* kb,
                               const int64_t* offb, int P, int cap, unsigned long long* out, cudaStream_t s,
-                              int64_t* launches);
+                              int64_t* launches, int stride = 1);
 // per partition: C[g][h] += 1 for every joined pair (u32 cells, row stride ldc); with C64,
 // also C64[g][h] += va·vb (integer SUM, wrapping int64)
 cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, const int64_t* offa,
                                const unsigned long long* kb, const int32_t* hb, const int64_t* offb, int P, int cap,
                                unsigned* C, int64_t ldc, cudaStream_t s, int64_t* launches,
                                const long long* va = nullptr, const long long* vb = nullptr,
-                               unsigned long long* C64 = nullptr);
+                               unsigned long long* C64 = nullptr, unsigned long long* jk = nullptr);
+// jk (4 + 4 P entries, required): the exact join size J = jk[0] and K = jk[1] (keys with
+// pairs), measured while expanding
 // largest partition (max over both sides) into *out (zeroed)
 cudaError_t launch_part_max(const int64_t* offa, const int64_t* offb, int P, unsigned long long* out, cudaStream_t s,
                             int64_t* launches);

@@ -184,7 +184,7 @@ double hll_estimate(const unsigned* r) {
 // est_distinct (> 0) sizes the hash table: 2^ceil(log2(1.9 x estimate)), never above 2n
 // (load <= ~0.53; c5's 4.2 M keys fit 2^23 slots = 64 MB, L2-resident).
 void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long long mn, long long mx, bool intersect,
-                unsigned long long* union_dev, int64_t* launches, double est_distinct = 0) {
+                unsigned long long* union_dev, int64_t* launches, double est_distinct = 0, bool row_slots = true) {
   cudaStream_t s = ar.s;
   const int64_t n = c1.n + (c2 ? c2->n : 0);
   const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
@@ -225,7 +225,7 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.fa = ar.zeros<uint8_t>((int64_t)cap);
     d.ovf = ar.zeros<int>(1);
     // per-row slots: the probe then reads code[slot] instead of rehashing and walking the table
-    d.slot1 = ar.get<int32_t>(c1.n);
+    d.slot1 = row_slots ? ar.get<int32_t>(c1.n) : nullptr;
     CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, d.wide, s, launches));
     if (c2) {
       d.slot2 = ar.get<int32_t>(c2->n);
@@ -352,8 +352,10 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
                     bool timed, bool sum, const ColDesc& av, const ColDesc& bw) {
   const int64_t nA = ak.n, nB = bk.n;
   Dict DG, DH;
-  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
-  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2]);
+  // group dictionaries only (no per-row slots): pass 1 of the partitioning looks each
+  // tuple's group code up in the finished dictionary
+  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false);
+  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], false);
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
     int* hov = reinterpret_cast<int*>(hp + 2);
@@ -371,10 +373,8 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   if ((double)G * (double)ldc * 4.0 > 0.3 * (double)ctx->mem_free0) return false;
   dict_finish_group(ar, DG, L);
   dict_finish_group(ar, DH, L);
-  int32_t* gA = ar.get<int32_t>(nA);
-  int32_t* hB = ar.get<int32_t>(nB);
-  CK(launch_group_codes(ag, DG.view(1), gA, s, L));
-  CK(launch_group_codes(bh, DH.view(1), hB, s, L));
+  const DictView gdv[2] = {DG.view(), DH.view()};
+  const ColDesc* gcols[2] = {&ag, &bh};
   // partitions: <= ~1 K tuples per side on average, two radix passes of <= 7 bits
   int pbits = 1;
   while (pbits < 14 && ((int64_t)1 << pbits) * 1024 < std::max(nA, nB)) ++pbits;
@@ -384,7 +384,6 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   Side sd[2];
   const ColDesc* vals[2] = {&av, &bw};  // integer SUM: value payload (absent column = 1)
   const ColDesc* keys[2] = {&ak, &bk};
-  const int32_t* grp[2] = {gA, hB};
   const int64_t ns[2] = {nA, nB};
   int64_t* seg0 = ar.get<int64_t>(4);
   {
@@ -401,12 +400,12 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
     sd[x].seg1 = ar.get<int64_t>(((int64_t)1 << b1) + 1);
     sd[x].seg2 = ar.get<int64_t>((int64_t)P + 1);
     void* t1 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1, b1));
-    CK(launch_part_pass(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
+    CK(launch_part_pass(keys[x], kmin, gcols[x], &gdv[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
                         sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L, sum ? vals[x] : nullptr, nullptr,
                         sd[x].v[0]));
     if (b2) {
       void* t2 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1 << b1, b2));
-      CK(launch_part_pass(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
+      CK(launch_part_pass(nullptr, 0, nullptr, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
                           sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, s, L, nullptr, sd[x].v[0], sd[x].v[1]));
     }
   }
@@ -416,38 +415,60 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   CK(launch_part_max(sd[0].seg2, sd[1].seg2, P, d_max, s, L));
   const int64_t cap = (int64_t)*to_pinned<unsigned long long>(ctx, d_max, s);
   if (cap <= 0 || part_expand_smem((int)std::min<int64_t>(cap, 1 << 20), sum) > 200 * 1024) return false;
-  CK(launch_part_count(sd[0].k[fin], sd[0].seg2, sd[1].k[fin], sd[1].seg2, P, (int)cap, d_out, s, L));
-  unsigned long long cnt[4];
-  CK(cudaMemcpyAsync(ctx->pinned, d_out, 32, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  std::memcpy(cnt, ctx->pinned, 32);
-  const unsigned long long J = cnt[0];
-  const int64_t K = (int64_t)cnt[1];
-  tm.mark(&S.ms_encode);
-  // a4 selector with the same cost model as the general path (COUNT)
-  const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), Kp = round_up(std::max<int64_t>(K, 1), 128);
+  // a4 selector on the join size J = sum_k cntA(k)·cntB(k). With many partitions a sample of
+  // them (every 16th: keys are hashed, so each holds an unbiased 1/P of the key domain) gives
+  // the estimate; the exact J and K come out of the expand itself. A close call, or a J near
+  // a guard bound (u32 cells, the int64 SUM bound), counts every partition first.
+  auto absmax = [&](const ColDesc& c, int i) -> long double {
+    if (!c.data) return 1.0L;
+    return std::max(std::fabs((long double)hs[i].mn), std::fabs((long double)hs[i].mx));
+  };
+  const long double vmax = sum ? absmax(av, 4) * absmax(bw, 5) : 1.0L;
   const Calib& cb = ctx->cal;
-  const double t_dense = 2.0 * Gp * Hp * Kp / cb.R_i8 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / cb.BW;
-  // the partitioned expand's own rate (one L2 reduction per joined pair: ~1.4e11/s on c5)
-  const double t_sparse = (double)J / 5.0e10 + ((double)G * H * 4 + (double)(nA + nB) * 32) / cb.BW + cb.T_sp0;
-  if (J == 0 || K == 0) {
+  auto costs = [&](double J, double K, double* td, double* tsp) {
+    const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), Kp = round_up(std::max<int64_t>((int64_t)K, 1), 128);
+    *td = 2.0 * Gp * Hp * Kp / cb.R_i8 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / cb.BW;
+    // the partitioned expand's own rate (one L2 reduction per joined pair: ~1.4e11/s on c5)
+    *tsp = J / 5.0e10 + ((double)G * H * 4 + (double)(nA + nB) * 32) / cb.BW + cb.T_sp0;
+  };
+  const char* hp_exact = getenv("TCUDB_HASHPART_EXACT_COUNT");  // tests: always count every partition
+  int stride = (P >= 1024 && !(hp_exact && hp_exact[0] == '1')) ? 16 : 1;
+  unsigned long long J = 0;
+  int64_t K = 0;
+  for (;;) {
+    CK(launch_part_count(sd[0].k[fin], sd[0].seg2, sd[1].k[fin], sd[1].seg2, P, (int)cap, d_out, s, L, stride));
+    unsigned long long cnt[4];
+    CK(cudaMemcpyAsync(ctx->pinned, d_out, 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(cnt, ctx->pinned, 32);
+    J = cnt[0] * (unsigned long long)stride;
+    K = (int64_t)cnt[1] * stride;
+    if (stride == 1) break;
+    double td, tsp;
+    costs((double)J, (double)K, &td, &tsp);
+    const bool close = td <= 4.0 * tsp;
+    const bool near_guard = J == 0 || J >= (1ull << 30) || (sum && (long double)J * vmax >= 9.2e17L);
+    if (!close && !near_guard) break;
+    stride = 1;  // decide on the exact count
+  }
+  tm.mark(&S.ms_encode);
+  if (stride == 1 && (J == 0 || K == 0)) {
     S.G = G; S.H = H; S.K = K; S.join_pairs = 0; S.path = 1; S.spa_mode = 4;
     return true;  // empty result (out already zeroed)
   }
-  if (t_dense <= t_sparse || J >= (1ull << 32)) return false;
-  if (sum) {
+  {
+    double td, tsp;
+    costs((double)J, (double)K, &td, &tsp);
+    if (td <= tsp || J >= (1ull << 32)) return false;
     // int64 guard (a3): |SUM| <= J·max|v|·max|w|; beyond it the general path's finer bound decides
-    auto absmax = [&](const ColDesc& c, int i) -> long double {
-      if (!c.data) return 1.0L;
-      return std::max(std::fabs((long double)hs[i].mn), std::fabs((long double)hs[i].mx));
-    };
-    if ((long double)J * absmax(av, 4) * absmax(bw, 5) >= 9.2e18L) return false;
+    if (sum && (long double)J * vmax >= 9.2e18L) return false;
   }
   unsigned* C = ar.zeros<unsigned>(G * ldc);
   unsigned long long* C64 = sum ? ar.zeros<unsigned long long>(G * ldc) : nullptr;
+  unsigned long long* d_jk = ar.get<unsigned long long>(4 + 4 * (int64_t)P);
   if (timed) cudaEventRecord(ctx->evk[0], s);
   CK(launch_part_expand(sd[0].k[fin], sd[0].g[fin], sd[0].seg2, sd[1].k[fin], sd[1].g[fin], sd[1].seg2, P, (int)cap,
-                        C, ldc, s, L, sd[0].v[fin], sd[1].v[fin], C64));
+                        C, ldc, s, L, sd[0].v[fin], sd[1].v[fin], C64, d_jk));
   if (timed) cudaEventRecord(ctx->evk[1], s);
   tm.mark(&S.ms_sparse);
   // a8 compaction of C (u32 counts; codes are ascending ranks -> (g, h) order)
@@ -462,7 +483,20 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
   int64_t* d_nnz = ar.get<int64_t>(1);
   CK(launch_compact_count(ca, nullptr, d_nnz, ctmp, s, L));
-  const int64_t nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+  int64_t nnz = 0;
+  {
+    // nnz and the exact J, K measured by the expand, in one read
+    int64_t* hp = static_cast<int64_t*>(ctx->pinned);
+    CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 1, d_jk, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nnz = hp[0];
+    J = (unsigned long long)hp[1];
+    K = hp[2];
+  }
+  // the estimate was wrong past a guard bound: the cells may have wrapped — decide again on
+  // the general path (nothing is returned from this one)
+  if (J >= (1ull << 32) || (sum && (long double)J * vmax >= 9.2e18L)) return false;
   const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
   const size_t oh = ((size_t)nnz * gb + 255) / 256 * 256;
   const size_t oa = oh + ((size_t)nnz * hb + 255) / 256 * 256;

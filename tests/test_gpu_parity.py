@@ -607,6 +607,8 @@ def test_hash_partitioned_count(engine, torch_mod, oracle_mod, monkeypatch, case
     compare(out, ref, agg)
     if case in ("c5_64", "c5_16"):  # (elsewhere the selector may prefer the dense path)
         assert st["spa_mode"] == 4
+    if st["spa_mode"] == 4:  # the exact join size measured by the expand (c5_16: sampled count)
+        assert st["join_pairs"] == int(ref["cnt"].sum())
     monkeypatch.setenv("TCUDB_FORCE_HASHPART", "0")
     monkeypatch.setenv("TCUDB_NO_HASHPART", "1")
     out2, st2 = run(engine, torch_mod, A, B, agg, 0)
