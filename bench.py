@@ -48,6 +48,10 @@ WORKLOADS = {
     "c4": "c4: SQL matmul of two 8192x8192 (row,col,val) tables, SUM(A.v*B.w), bf16-exact values",
     "c4s": "c4s: c4 with signed fp32 N(0,1) values (not bf16-exact: hi/lo split)",
     "c5": "c5: low-density COUNT(*) join, 2^24 x 2^24 tuples over a 2^22 scrambled int64 key domain",
+    "c5s": "c5s: c5 with SUM(A.v*B.w), v,w ~ U{-100..100}",
+    "c1s": "c1s: c1 with SUM(A.v*B.w), v,w ~ U{-100..100}",
+    "c2b": ("c2b: blocked entity matching (not a BASELINE config; the f4 block-sparse path's input): "
+            "100 blocks x 100 records per side, L ~ U{100..200} tokens from a 400-token block vocabulary"),
 }
 
 
@@ -374,6 +378,10 @@ def measure(eng, torch, dev, config, steps, warmup, ws, rank, sharded, flush, st
     ms = total_ms / steps
     qroof = query_roofline(st, input_bytes(A) + input_bytes(B), peaks)
     qroof["frac"] = qroof["t_roof_ms"] / ms
+    if config in ("c1", "c1s"):
+        # latency-bound (T_roof < 1 us); a roofline fraction says nothing here
+        qroof["frac"] = None
+        qroof["note"] = "launch/latency-bound: T_roof < 1 us, fraction not meaningful (SURVEY 8(d) c1)"
     qroof["peak_source"] = f"{peaks['source']} (bf16 x dtype ratio, copy bandwidth)"
     if sharded:
         qroof["note"] = "single-GPU roofline of the whole query vs the N-GPU query time"

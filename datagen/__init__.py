@@ -94,6 +94,30 @@ def c2_entity_matching(n_records=10_000, vocab=32_768, lmin=10, lmax=30, s=1.0, 
     return Table(ta, ra), Table(tb, rb)
 
 
+def c2_blocked(n_records=10_000, n_blocks=100, block_vocab=400, lmin=100, lmax=200, seeds=(21, 22)):
+    """Blocked entity matching (the paper's EM blocking, as a block-structured
+    input for the §8(f) f4 block-sparse path; not one of BASELINE's five configs): records
+    numbered block by block (a table sorted by its blocking key), n_blocks blocks, each
+    record a set of L ~ U{lmin..lmax} distinct tokens drawn uniformly from its block's own
+    vocabulary of block_vocab tokens; token ids are a random permutation of the whole
+    vocabulary (so the block structure is invisible in key order). k = tok, g / h = rid,
+    COUNT(*) = shared tokens; pairs only inside blocks."""
+    V = n_blocks * block_vocab
+    perm = np.random.default_rng(seeds[0] * 7 + 1).permutation(V).astype(np.int32)
+
+    def side(seed):
+        rng = np.random.default_rng(seed)
+        lens = rng.integers(lmin, lmax + 1, n_records)
+        block = (np.arange(n_records) * n_blocks) // n_records
+        order = np.argsort(rng.random((n_records, block_vocab)), axis=1)[:, :lmax]
+        keep = np.arange(lmax)[None, :] < lens[:, None]
+        local = order[keep]
+        rid = np.repeat(np.arange(n_records, dtype=np.int32), lens)
+        tok = perm[np.repeat(block, lens) * block_vocab + local]
+        return Table(tok.astype(np.int32), rid)
+    return side(seeds[0]), side(seeds[1])
+
+
 # --------------------------------------------------------------------------- c3
 def c3_graph_edges(scale=16, edge_factor=16, abcd=(0.57, 0.19, 0.19, 0.05), seed=4):
     """R-MAT edge list (Chakrabarti et al.): scale 16 (65,536 ids), edge factor
@@ -231,6 +255,7 @@ CONFIGS = {
     "c1": "COUNT(*) natural join of two 1,000-row int tables on 64 distinct keys, 32x32 groups",
     "c1s": "c1 with SUM(A.v*B.w), v,w ~ U{-100..100}",
     "c2": "entity matching: 10k x 10k token-bag records, vocab 32k, shared-token COUNT",
+    "c2b": "blocked entity matching (f4 block-sparse input): 100 blocks x 100 records, 400-token block vocabularies",
     "c3": "graph query: 2-hop path count on R-MAT scale-16 edge table (self-join + group-by)",
     "c4": "matrix analytics: SQL matmul of two 8192x8192 (row,col,val) tables, SUM bf16",
     "c4s": "c4 with signed fp32 N(0,1) values (not bf16-exact: the guard's hi/lo split)",
@@ -249,6 +274,9 @@ def make_config(name, scale=1.0):
     if name == "c2":
         n = max(16, int(10_000 * scale))
         A, B = c2_entity_matching(n_records=n); return A, B, "count"
+    if name == "c2b":
+        n = max(100, int(10_000 * scale))
+        A, B = c2_blocked(n_records=n, n_blocks=max(1, n // 100)); return A, B, "count"
     if name == "c3":
         sc = 16 if scale >= 1.0 else max(6, int(round(16 + np.log2(scale))))
         s, d = c3_graph_edges(scale=sc)

@@ -118,6 +118,8 @@ typedef struct {
   float ms_kernel;       /* sparse path: CUDA-event time of the band kernel (k_spa_fused) */
   double kernel_bytes;   /* ... and its algorithmic bytes (4 J + 20 n_active + result bytes) */
   float ms_comm;         /* collective calls: host wall time of the exchanges (NCCL + routing) */
+  double block_active;   /* dense path, block-sparse GEMM (§8(f) f4): share of (tile, K-block)
+                            products with tuples on both sides (the rest skipped); 0: dense GEMM */
 } tcudb_stats;
 
 typedef struct tcudb_ctx tcudb_ctx;

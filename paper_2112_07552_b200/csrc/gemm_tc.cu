@@ -63,7 +63,43 @@ struct KParams {
   int32_t* cnt_out; int64_t ldcnt;
   int group_m;       // M-blocks per raster band
   FusedCompact fc;   // fused compaction (CMP kernels only)
+  // block-sparse (§8(f) f4, TCU-SpMM's zero-tile skipping P:1241-1251): per M-tile / N-tile
+  // bitmaps over the absolute K-blocks (bmw 64-bit words per tile); a K-block enters the
+  // product of tile (mb, nb) only when both bits are set. NULL: dense.
+  const unsigned long long* bmA;
+  const unsigned long long* bmB;
+  int bmw;
 };
+
+// Calls f(kb, first) for the K-blocks of tile (mb, nb) in ascending order: all of them
+// (dense), or those active in both operands' block bitmaps. Returns the count.
+template <typename F>
+__device__ __forceinline__ int for_active_kb(const KParams& p, int mb, int nb, F&& f) {
+  if (!p.bmA) {
+    for (int kb = 0; kb < p.num_kb; ++kb) f(kb, kb == 0);
+    return p.num_kb;
+  }
+  const unsigned long long* a = p.bmA + (int64_t)mb * p.bmw;
+  const unsigned long long* b = p.bmB + (int64_t)nb * p.bmw;
+  const int k0 = p.kb_begin, k1 = p.kb_begin + p.num_kb;
+  int n = 0;
+  for (int w = k0 >> 6; w <= ((k1 - 1) >> 6); ++w) {
+    unsigned long long m = __ldg(a + w) & __ldg(b + w);
+    if (w == (k0 >> 6) && (k0 & 63)) m &= ~0ull << (k0 & 63);
+    if (w == ((k1 - 1) >> 6) && (k1 & 63)) m &= ~0ull >> (64 - (k1 & 63));
+    while (m) {
+      const int bit = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      f(w * 64 + bit - k0, n == 0);
+      ++n;
+    }
+  }
+  return n;
+}
+__device__ __forceinline__ bool tile_active(const KParams& p, int mb, int nb) {
+  if (!p.bmA) return true;
+  return for_active_kb(p, mb, nb, [](int, bool) {}) > 0;
+}
 
 // Grouped raster: bands of group_m M-blocks, N-blocks swept inside a band, so a band's
 // A panel stays L2-resident while B streams through once per band.
@@ -171,19 +207,40 @@ __device__ __forceinline__ void epilogue_chunk(const KParams& p, const uint32_t*
 // Epilogue for one accumulator tile: this thread owns one row (its TMEM lane) and
 // the BN_ accumulator columns at taddr. Returns the row's nonzero count.
 template <int BN_, bool FP4>
-__device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, int64_t row, int nb, long long& tri) {
+__device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, int64_t row, int nb, long long& tri,
+                                             bool zero = false) {
   int nzc = 0;  // nonzeros of this row inside the BN_-column tile (compaction count, a8)
+  // zero: a block-sparse tile with no active K-block — its zeros are written without a
+  // TMEM accumulator (accumulating epilogues add nothing, so they skip it)
+  if (zero && (p.epi == EPI_ACC64 || p.epi == EPI_ACCF64 || p.epi == EPI_TRI)) {
+    if (p.epi == EPI_ACC64 && p.cnt_out) {
+      for (int c = 0; c < BN_; ++c) nzc += reinterpret_cast<const long long*>(p.C)[row * p.ldc + (int64_t)nb * BN_ + c] != 0;
+    } else if (p.epi == EPI_ACCF64 && p.cnt_out) {
+      for (int c = 0; c < BN_; ++c) nzc += reinterpret_cast<const double*>(p.C)[row * p.ldc + (int64_t)nb * BN_ + c] != 0.0;
+    }
+    return nzc;
+  }
 #pragma unroll 1
   for (int c = 0; c < BN_ / 32; ++c) {
     uint32_t r[32];
-    tmem_ld_32x32b_x32(taddr + c * 32, r);
-    tmem_ld_wait();
+    if (zero) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = 0u;
+    } else {
+      tmem_ld_32x32b_x32(taddr + c * 32, r);
+      tmem_ld_wait();
+    }
     epilogue_chunk<32, FP4>(p, r, row, (int64_t)nb * BN_ + c * 32, nzc, tri);
   }
   if (BN_ % 32) {
     uint32_t r[16];
-    tmem_ld_32x32b_x16(taddr + (BN_ / 32) * 32, r);
-    tmem_ld_wait();
+    if (zero) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = 0u;
+    } else {
+      tmem_ld_32x32b_x16(taddr + (BN_ / 32) * 32, r);
+      tmem_ld_wait();
+    }
     epilogue_chunk<16, FP4>(p, r, row, (int64_t)nb * BN_ + (BN_ / 32) * 32, nzc, tri);
   }
   return nzc;
@@ -378,14 +435,14 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
       int stage = 0; uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for_active_kb(p, mb, nb, [&](int kb, bool) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
           const int kc = (p.kb_begin + kb) * p.elems_per_kb;
           tma_load_2d(&tmA, sA + stage * A_STAGE_BYTES, &full[stage], kc, mb * BM, pol);
           tma_load_2d(&tmB, sB + stage * G::B_STAGE_BYTES, &full[stage], kc, nb * BN_, pol);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
+        });
       }
     }
   } else if (warp == 1) {
@@ -394,17 +451,22 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb = 0, nb = 0;
+        if (p.bmA) {
+          tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
+          if (!tile_active(p, mb, nb)) continue;  // an all-zero tile: no accumulator (epilogue writes zeros)
+        }
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN_;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for_active_kb(p, mb, nb, [&](int, bool first) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = sw_desc<KB_>(smem_u32(sA + stage * A_STAGE_BYTES));
           const uint64_t bdesc = sw_desc<KB_>(smem_u32(sB + stage * G::B_STAGE_BYTES));
 #pragma unroll
           for (int kk = 0; kk < KB_ / 32; ++kk) {  // 32 bytes of K per MMA
-            const uint32_t accum = (kb | kk) != 0;
+            const uint32_t accum = (!first || kk != 0) ? 1u : 0u;
             if (FP4) mma_mxf4(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, tmem_base + SF_COL,
                               tmem_base + SF_COL + 16, accum);
             else if (p.is_bf16) mma_f16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
@@ -412,7 +474,7 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
           }
           mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
+        });
         mma_commit(&tfull[acc]);      // accumulator ready for the epilogue
         acc ^= 1; if (acc == 0) acc_phase ^= 1;
       }
@@ -424,9 +486,14 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
     long long tri = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
+      const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
+      if (!tile_active(p, mb, nb)) {  // block-sparse: no accumulator for this tile
+        const int nzc = epilogue_rows<BN_, FP4>(p, 0, row, nb, tri, true);
+        if (!CMP && p.cnt_out) p.cnt_out[row * p.ldcnt + nb] = nzc;
+        continue;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN_;
       const int nzc = epilogue_rows<BN_, FP4>(p, taddr, row, nb, tri);
       tc_fence_before();
@@ -695,7 +762,7 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
     return cudaErrorInvalidValue;
   const int64_t tiles_n = (a.N + BNF - 1) / BNF;
   if (a.ldc < tiles_n * BNF) return cudaErrorInvalidValue;
-  const int kb = pick_kb();
+  const int kb = a.bmA ? BKB : pick_kb();  // bitmaps are over 128-byte K-blocks
   KParams p{};
   p.M = a.M; p.N = a.N;
   p.tiles_m = (int)(a.M / BM); p.tiles_n = (int)tiles_n;
@@ -711,6 +778,8 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   p.epi = a.epi; p.C = a.C; p.ldc = a.ldc; p.shift = 0;
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   p.group_m = pick_group_m(p.tiles_m, BM, a.k_len);
+  p.bmA = a.bmA; p.bmB = a.bmB; p.bmw = a.bmw;
+  if (a.cmp && a.bmA) return cudaErrorInvalidValue;  // fused compaction needs every tile's epilogue
   if (a.cmp) {
     // M-blocks must complete early for their compaction to overlap later tiles: bands of
     // 2 M-blocks (measured best of 1..40 on c2)
@@ -734,8 +803,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   // 1.40 ms; both MMA-bound at ~65-70 % tensor-pipe activity). TCUDB_GEMM_PAIR=1 selects the
   // CTA-pair (cta_group::2) kernel when M splits into 256-row pair tiles.
   static const bool want_pair = getenv("TCUDB_GEMM_PAIR") && getenv("TCUDB_GEMM_PAIR")[0] == '1';
-  const bool pair = want_pair && a.M % 256 == 0;
-  const int kb = pair ? BKB : pick_kb();
+  const bool pair = want_pair && a.M % 256 == 0 && !a.bmA;
+  const int kb = (pair || a.bmA) ? BKB : pick_kb();  // bitmaps are over 128-byte K-blocks
   KParams p{};
   p.M = a.M; p.N = a.N;
   p.tiles_m = (int)(a.M / (pair ? 256 : BM)); p.tiles_n = (int)(a.N / BN);
@@ -756,6 +825,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   p.mask = a.mask; p.ldm = a.ldm; p.mask_rows = a.mask_rows; p.mask_cols = a.mask_cols; p.tri_out = a.tri_out;
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   p.group_m = pick_group_m(p.tiles_m, pair ? 256 : BM, a.k_len * esz);
+  p.bmA = a.bmA; p.bmB = a.bmB; p.bmw = a.bmw;
   if (!pair) return run_1cta<BN, false>(a, p, a.elem, kb, s, launches);
   const int64_t kcols = a.k_begin + a.k_len;
   CUtensorMap mA, mB;

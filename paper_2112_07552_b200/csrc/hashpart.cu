@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(kCsThreads) k_chunk_starts(const int64_t* __re
 }
 
 struct PassIO {
-  const void* raw; int raw_type; long long kmin;                        // pass 1 (raw key column)
-  ColDesc gcol; DictView gd;                                            // pass 1: raw groups -> codes
+  const void* raw; int raw_type; long long kmin; const int32_t* g_raw;  // pass 1 (raw key column, group codes)
   const void* v_raw; int v_type;                                        // pass 1 values (SUM)
   const unsigned long long* k_in; const int32_t* g_in;
   const long long* v_in; long long* v_out;                              // value payload (SUM)
@@ -159,35 +158,22 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
   int32_t g[4];
   long long v[4];
   int d[4], r[4];
-  bool ok[4];
-  long long graw[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int64_t i = lo + threadIdx.x + u * PT;
-    ok[u] = i < hi;
     d[u] = -1;
-    k[u] = 0;
-    g[u] = 0;
-    graw[u] = 0;
-    if (ok[u]) {
+    if (i < hi) {
       if (io.raw) {
         k[u] = (unsigned long long)ld_int(io.raw, io.raw_type, i) - (unsigned long long)io.kmin;
-        graw[u] = ld_int(io.gcol.data, io.gcol.type, i);
+        g[u] = io.g_raw[i];
       } else {
         k[u] = io.k_in[i];
         g[u] = io.g_in[i];
       }
       if (VAL) v[u] = load_value(io, i);
+      d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
+      r[u] = atomicAdd(&cnt[d[u]], 1);
     }
-  }
-  // pass 1: group codes straight from the finished group dictionary (L2-resident), so the
-  // per-tuple code column is never written and read back
-  if (io.raw) dict_lookup_batch<4>(io.gd, graw, ok, g);
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    if (!ok[u]) continue;
-    d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
-    r[u] = atomicAdd(&cnt[d[u]], 1);
   }
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of <= 128 digit counts, 4 per lane
@@ -512,7 +498,7 @@ size_t hashpart_temp_bytes(int64_t n, int nseg, int bits) {
          ((size_t)(cnts + 1) * 8 + 255) / 256 * 256 + scan_temp_bytes(cnts);
 }
 
-cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const ColDesc* g_col, const DictView* gd,
+cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
                              const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
                              int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
                              int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
@@ -529,8 +515,7 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const ColDesc* 
   int64_t* offs = reinterpret_cast<int64_t*>(t);
   t += ((size_t)(cnts + 1) * 8 + 255) / 256 * 256;
   PassIO io{};
-  io.raw = raw ? raw->data : nullptr; io.raw_type = raw ? raw->type : 0; io.kmin = kmin;
-  if (raw) { io.gcol = *g_col; io.gd = *gd; }
+  io.raw = raw ? raw->data : nullptr; io.raw_type = raw ? raw->type : 0; io.kmin = kmin; io.g_raw = g_raw;
   io.k_in = k_in; io.g_in = g_in; io.seg_off = seg_off; io.nseg = nseg; io.shift = shift; io.bits = bits;
   io.chunk_start = chunk_start; io.counts = counts; io.offs = offs;
   io.k_out = k_out; io.g_out = g_out; io.seg_out = seg_out;

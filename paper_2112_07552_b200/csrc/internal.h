@@ -44,6 +44,11 @@ struct GemmArgs {
   // the result tuples are written in (g, h) order by compaction warps while later tiles
   // are still being multiplied (see gemm_tc.cu). Scratch arrays are zeroed by the caller.
   const void* cmp = nullptr;        // const FusedCompact* (device-visible fields by value)
+  // optional block-sparse bitmaps (blocksparse.cu): per 128-row A tile / BN-row B tile, bmw
+  // 64-bit words over the absolute K-blocks of the stage width; 1-CTA kernel, no cmp
+  const unsigned long long* bmA = nullptr;
+  const unsigned long long* bmB = nullptr;
+  int bmw = 0;
 };
 // Fused-compaction parameters (gemm_tc.cu, EPI_STORE16 + fp4 only).
 struct FusedCompact {

@@ -244,9 +244,8 @@ size_t hashpart_temp_bytes(int64_t n, int nseg, int bits);
 // (fmix64(koff) >> shift) & (2^bits - 1); output segment-major, then digit. in_raw: pass 1
 // reads the raw key column and the gcode array instead of (k_in, g_in). seg_out (nseg *
 // 2^bits + 1) receives the new segment offsets.
-// pass 1 (raw != NULL): raw key column + raw group column g_col with its finished
-// dictionary gd (group codes looked up in the pass); later passes: k_in / g_in
-cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const ColDesc* g_col, const DictView* gd,
+// pass 1 (raw != NULL): raw key column + per-tuple group codes g_raw; later passes: k_in / g_in
+cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* g_raw,
                              const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off, int nseg,
                              int64_t n, int shift, int bits, unsigned long long* k_out, int32_t* g_out,
                              int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
@@ -342,4 +341,25 @@ namespace tcudb {
 // g uniform over [0, groups)
 cudaError_t launch_gen_cols(int32_t* k, int32_t* g, int64_t n, uint32_t keys, uint32_t groups, uint32_t seed,
                             cudaStream_t s, int64_t* launches);
+}  // namespace tcudb
+
+namespace tcudb {
+// ---------------------------------------------------------------- blocksparse.cu (§8(f) f4)
+// Re-code the join keys in order of their smallest A row (kA / kB and the per-key counts
+// are rewritten in place).
+size_t bs_reorder_temp_bytes(int64_t K);
+cudaError_t launch_bs_reorder(int32_t* kA, const int32_t* gA, int64_t nA, int32_t* kB, int64_t nB, int32_t* cntA,
+                              int32_t* cntB, int64_t K, void* temp, cudaStream_t s, int64_t* launches);
+// base occupancy bitmap (zeroed by the caller): 16-row x 64-key blocks, W words per row group
+cudaError_t launch_bs_mark(const int32_t* kcode, const int32_t* rcode, int64_t n, int W, unsigned long long* bm,
+                           cudaStream_t s, int64_t* launches);
+// tile bitmaps for one GEMM launch: rows_per_tile (multiple of 16) rows per tile, f key groups
+// of 64 per K-block, K-block kb maps to key group (kb mod period_kb) * f (the hi/lo split
+// repeats the key space along K), Wout words per tile
+cudaError_t launch_bs_derive(const unsigned long long* base, int base_rows, int W, int rows_per_tile, int f,
+                             int64_t period_kb, int64_t total_kb, int ntiles, int Wout, unsigned long long* out,
+                             cudaStream_t s, int64_t* launches);
+// *out += active (tile pair, K-block) products
+cudaError_t launch_bs_active(const unsigned long long* a, const unsigned long long* b, int tiles_m, int tiles_n,
+                             int Wt, unsigned long long* out, cudaStream_t s, int64_t* launches);
 }  // namespace tcudb

@@ -352,8 +352,7 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
                     bool timed, bool sum, const ColDesc& av, const ColDesc& bw) {
   const int64_t nA = ak.n, nB = bk.n;
   Dict DG, DH;
-  // group dictionaries only (no per-row slots): pass 1 of the partitioning looks each
-  // tuple's group code up in the finished dictionary
+  // group dictionaries only (no per-row slots: one read of each group column)
   dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false);
   dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], false);
   {
@@ -373,8 +372,14 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   if ((double)G * (double)ldc * 4.0 > 0.3 * (double)ctx->mem_free0) return false;
   dict_finish_group(ar, DG, L);
   dict_finish_group(ar, DH, L);
-  const DictView gdv[2] = {DG.view(), DH.view()};
-  const ColDesc* gcols[2] = {&ag, &bh};
+  // per-tuple group codes by value from the finished dictionaries (a lookup inside the
+  // partition pass measured slower: +0.2 ms on c5, the dependent table loads stall the
+  // latency-bound scatter; here four lookups per thread are in flight)
+  int32_t* gA = ar.get<int32_t>(nA);
+  int32_t* hB = ar.get<int32_t>(nB);
+  CK(launch_group_codes(ag, DG.view(), gA, s, L));
+  CK(launch_group_codes(bh, DH.view(), hB, s, L));
+  const int32_t* grp[2] = {gA, hB};
   // partitions: <= ~1 K tuples per side on average, two radix passes of <= 7 bits
   int pbits = 1;
   while (pbits < 14 && ((int64_t)1 << pbits) * 1024 < std::max(nA, nB)) ++pbits;
@@ -400,12 +405,12 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
     sd[x].seg1 = ar.get<int64_t>(((int64_t)1 << b1) + 1);
     sd[x].seg2 = ar.get<int64_t>((int64_t)P + 1);
     void* t1 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1, b1));
-    CK(launch_part_pass(keys[x], kmin, gcols[x], &gdv[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
+    CK(launch_part_pass(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
                         sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L, sum ? vals[x] : nullptr, nullptr,
                         sd[x].v[0]));
     if (b2) {
       void* t2 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1 << b1, b2));
-      CK(launch_part_pass(nullptr, 0, nullptr, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
+      CK(launch_part_pass(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
                           sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, s, L, nullptr, sd[x].v[0], sd[x].v[1]));
     }
   }
@@ -773,6 +778,64 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   // planes) and 2 x 128-byte blocks for bf16.
   const int64_t Kp = round_up(K, 128);
   const double dense_ops = 2.0 * (double)Gp * (double)Hp * (double)Kp;
+
+  // ---------------- §8(f) f4: block-sparse analysis (blocksparse.cu). When the dense product
+  // is large, re-code the keys by their first A row and measure the share of (tile, K-block)
+  // products with tuples on both sides; the GEMM then skips the empty ones and the
+  // selector's dense cost shrinks by that share. TCUDB_BLOCK_SPARSE=0 off, =1 forced.
+  const char* bs_env = getenv("TCUDB_BLOCK_SPARSE");
+  const bool bs_force = bs_env && bs_env[0] == '1', bs_off = bs_env && bs_env[0] == '0';
+  double bs_frac = 1.0;
+  unsigned long long *bs_baseA = nullptr, *bs_baseB = nullptr;
+  int bs_W = 0;
+  if (!bs_off && (bs_force || dense_ops >= 2e12) && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
+    CK(launch_bs_reorder(kA, gA, nA, kB, nB, cntA, cntB, K, ar.get<char>((int64_t)bs_reorder_temp_bytes(K)), s, L));
+    const int64_t kgroups = (Kp * 4 + 63) / 64;  // 64-key groups over the widest K' (the split's 4 Kp)
+    bs_W = (int)((kgroups + 63) / 64);
+    bs_baseA = ar.zeros<unsigned long long>(Gp / 16 * bs_W);
+    bs_baseB = ar.zeros<unsigned long long>(Hp / 16 * bs_W);
+    CK(launch_bs_mark(kA, gA, nA, bs_W, bs_baseA, s, L));
+    CK(launch_bs_mark(kB, hB, nB, bs_W, bs_baseB, s, L));
+    // the share at kind::i8 granularity (128-row A tiles, 256-row B tiles, 128-key blocks)
+    const int tm = (int)(Gp / 128), tn = (int)(Hp / 256);
+    const int64_t nkb = Kp / 128;
+    const int Wt = (int)((nkb + 63) / 64);
+    unsigned long long* ta = ar.get<unsigned long long>((int64_t)tm * Wt);
+    unsigned long long* tb = ar.get<unsigned long long>((int64_t)tn * Wt);
+    CK(launch_bs_derive(bs_baseA, (int)(Gp / 16), bs_W, 128, 2, nkb, nkb, tm, Wt, ta, s, L));
+    CK(launch_bs_derive(bs_baseB, (int)(Hp / 16), bs_W, 256, 2, nkb, nkb, tn, Wt, tb, s, L));
+    unsigned long long* act = ar.zeros<unsigned long long>(1);
+    CK(launch_bs_active(ta, tb, tm, tn, Wt, act, s, L));
+    const unsigned long long a = *to_pinned<unsigned long long>(ctx, act, s);
+    bs_frac = (double)a / ((double)tm * (double)tn * (double)nkb);
+  }
+  const bool use_bs = bs_baseA && (bs_force || bs_frac <= 0.85);
+  S.block_active = use_bs ? bs_frac : 0.0;
+  // tile bitmaps of one GEMM launch kind (cached): rows per B tile, 64-key groups per K-block,
+  // K-blocks of the launch's K' space and the period of the key space along it
+  struct BsMaps { const unsigned long long *a = nullptr, *b = nullptr; int w = 0; };
+  std::map<int, BsMaps> bs_cache;
+  auto bs_maps = [&](int kind /*0 i8, 1 bf16, 2 bf16 split, 3 e2m1*/, int64_t total_kb, int64_t period_kb) {
+    BsMaps m;
+    if (!use_bs) return m;
+    auto it = bs_cache.find(kind);
+    if (it != bs_cache.end()) return it->second;
+    const int bn = kind == 3 ? kGemmBNFp4 : 256;
+    const int f = kind == 3 ? 4 : kind == 0 ? 2 : 1;
+    const int tm = (int)(Gp / 128), tn = (int)((Hp + bn - 1) / bn);
+    m.w = (int)((total_kb + 63) / 64);
+    unsigned long long* ta = ar.get<unsigned long long>((int64_t)tm * m.w);
+    unsigned long long* tb = ar.get<unsigned long long>((int64_t)tn * m.w);
+    CK(launch_bs_derive(bs_baseA, (int)(Gp / 16), bs_W, 128, f, period_kb, total_kb, tm, m.w, ta, s, L));
+    CK(launch_bs_derive(bs_baseB, (int)(Hp / 16), bs_W, bn, f, period_kb, total_kb, tn, m.w, tb, s, L));
+    m.a = ta; m.b = tb;
+    bs_cache[kind] = m;
+    return m;
+  };
+  auto with_bs = [&](GemmArgs& g, int kind, int64_t total_kb, int64_t period_kb) {
+    const BsMaps m = bs_maps(kind, total_kb, period_kb);
+    g.bmA = m.a; g.bmB = m.b; g.bmw = m.w;
+  };
   // the paper's input-matrix density: nnz(mat(A)) / (|A rows| x |dom(ID)|), ∪ domain
   S.density_union = S.K_union ? (double)nA / ((double)G * (double)S.K_union) : 0.0;
   // Cost model (Eq. 3's CT = 2MNK / peak plus the bytes each path moves), calibrated on the
@@ -789,7 +852,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 4 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
-  const double t_dense = planes_est * dense_ops / R_tc + 3.0 * dense_bytes / BW;
+  const double t_dense = planes_est * dense_ops * (use_bs ? bs_frac : 1.0) / R_tc + 3.0 * dense_bytes / BW;
   const double t_sparse = (double)J / R_sp + sparse_bytes / BW + T_sp0;
   // memory budget: the device's free memory when the context was created, re-read live
   // (cudaMemGetInfo: 0.3 ms to tens of ms of host time) only when a path's footprint comes
@@ -1073,7 +1136,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       const char* want_fc = getenv("TCUDB_FUSED_COMPACT");
       const double ub_t = std::min((double)G * (double)H, (double)J);
       FusedCompact fcmp{};
-      if (c16 && want_fc && want_fc[0] == '1' && ub_t * (double)(res_gb + res_hb + 8) <= 0.3 * (double)ctx->mem_free0) {
+      if (c16 && !use_bs && want_fc && want_fc[0] == '1' &&
+          ub_t * (double)(res_gb + res_hb + 8) <= 0.3 * (double)ctx->mem_free0) {
         const int64_t ub = (int64_t)ub_t;
         const size_t oh = ((size_t)ub * res_gb + 255) / 256 * 256;
         const size_t oa = oh + ((size_t)ub * res_hb + 255) / 256 * 256;
@@ -1094,6 +1158,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         fc_out[0] = fcmp.out_g; fc_out[1] = fcmp.out_h; fc_out[2] = fcmp.out_agg;
         d_fc_total = fcmp.total;
       }
+      if (!ga.cmp) with_bs(ga, 3, Kp4 / 256, Kp4 / 256);
       CK(launch_gemm(ga, s, L));
       ops += 2.0 * Gp * Hc * Kp4;
       ca.E = C; ca.e_kind = c16 ? 4 : 0; ca.lde = Hc; ca.V = C; ca.v_kind = ca.e_kind; ca.ldv = Hc;
@@ -1110,6 +1175,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       const int hh_chunks = std::max(1, hh_env > 0 ? hh_env : 1);
       const int64_t hh_step = round_up((Kp + hh_chunks - 1) / hh_chunks, 64);
       ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop; ga.C = C; ga.ldc = Hp;
+      with_bs(ga, 2, 4 * Kp / 64, Kp / 64);  // the key space repeats along K' = [hi|hi|lo|lo]
       bool first = true;
       for (int64_t k0 = 0; k0 < Kp; k0 += hh_step) {
         ga.k_begin = k0; ga.k_len = std::min(hh_step, Kp - k0);
@@ -1128,6 +1194,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       ga.elem = ELEM_BF16; ga.A = opA; ga.lda = ldop; ga.B = opB; ga.ldb = ldop;
       ga.k_begin = 0; ga.k_len = k_len; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
       ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
+      with_bs(ga, 1, k_len / 64, Kp / 64);
       CK(launch_gemm(ga, s, L));
       ops += 2.0 * Gp * Hp * k_len;
       ca.E = C; ca.e_kind = 2; ca.lde = Hp; ca.V = C; ca.v_kind = 2; ca.ldv = Hp;
@@ -1142,6 +1209,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         ga.A = opA; ga.lda = Kp; ga.B = opB; ga.ldb = Kp;
         ga.k_begin = 0; ga.k_len = Kp; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
         ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
+        with_bs(ga, 0, Kp / 128, Kp / 128);
         CK(launch_gemm(ga, s, L));
         ops += dense_ops;
         ca.E = C; ca.e_kind = 0; ca.lde = Hp; ca.V = C; ca.v_kind = 0; ca.ldv = Hp;
@@ -1161,6 +1229,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
               ga.B = opB + (int64_t)j * cellsB; ga.ldb = Kp;
               ga.k_begin = k0; ga.k_len = std::min<int64_t>(kc, Kp - k0);
               ga.epi = first ? EPI_SET64 : EPI_ACC64; ga.C = C; ga.ldc = Hp; ga.shift = 8 * (i + j);
+              with_bs(ga, 0, Kp / 128, Kp / 128);
               CK(launch_gemm(ga, s, L));
               ops += 2.0 * Gp * Hp * ga.k_len;
               first = false;
@@ -1176,11 +1245,14 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       ge.M = Gp; ge.N = Hp; ge.elem = ELEM_I8; ge.A = patA; ge.lda = Kp; ge.B = patB; ge.ldb = Kp;
       ge.k_begin = 0; ge.k_len = Kp; ge.epi = EPI_STORE32; ge.C = E; ge.ldc = Hp;
       ge.cnt_out = seg_cnt; ge.ldcnt = ca.nseg;
+      with_bs(ge, 0, Kp / 128, Kp / 128);
       CK(launch_gemm(ge, s, L));
       ops += dense_ops;
       ca.E = E; ca.e_kind = 0; ca.lde = Hp;
     }
-    S.gemm_ops = ops;
+    // executed work: the block-sparse GEMM skips (1 - share) of the products (share measured at
+    // kind::i8 granularity)
+    S.gemm_ops = ops * (use_bs ? bs_frac : 1.0);
     tm.mark(&S.ms_gemm);
   } else {
     // ---------------- a7 sparse expand
