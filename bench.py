@@ -408,7 +408,7 @@ def measure(eng, torch, dev, config, steps, warmup, ws, rank, sharded, flush, st
                   ("f64" if agg == "sum" and A["v"] is not None and A["v"].dtype == np.float32 else "int64")),
         "config": {"workload": WORKLOADS[config], "n_A": len(A["k"]), "n_B": len(B["k"]),
                    "G": st["G"], "H": st["H"], "K": st["K"], "join_pairs": st["join_pairs"],
-                   "result_groups": st["n_result"], "path": {0: "dense", 1: "sparse", 2: "segmented"}[st["path"]],
+                   "result_groups": st["n_result"], "path": {0: "dense", 1: "sparse", 2: "segmented", 3: "key-partitioned"}[st["path"]],
                    "l2": "flushed (256 MiB write) between timed steps"},
         "stage_ms": {k: st[k] for k in ("ms_stats", "ms_encode", "ms_fill", "ms_gemm", "ms_sparse", "ms_compact")
                      + (("ms_comm",) if sharded else ())},

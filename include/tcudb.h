@@ -70,8 +70,13 @@ enum {
   TCUDB_UNORDERED = 1u << 3,    /* reserved: output order unspecified */
   TCUDB_FORCE_WIDE = 1u << 4,   /* test hook: skip the packed fp4/u8 COUNT fills, use the
                                    int64 scratch + digit-plane guard path */
-  TCUDB_NO_FP4 = 1u << 5        /* COUNT: do not use e2m1 (fp4) 0/1 operands (kind::mxf4);
+  TCUDB_NO_FP4 = 1u << 5,       /* COUNT: do not use e2m1 (fp4) 0/1 operands (kind::mxf4);
                                    use u8 operands (kind::i8) */
+  TCUDB_KEY_PARTITIONED = 1u << 6, /* collective calls, COUNT / integer SUM with both sides grouped:
+                                      the key-partitioned path (both sides routed by a hash of the
+                                      join key, partial groups merged by g range; §8(f) f4). Default
+                                      when B has >= 4 M rows in total. */
+  TCUDB_ROW_SHARDED = 1u << 7   /* collective calls: always the row-sharded path (north star) */
 };
 
 typedef struct {

@@ -24,6 +24,7 @@ I32, I64, F32, F64 = 0, 1, 2, 3
 COUNT, SUM, AVG = 0, 1, 2
 _AGG = {"count": COUNT, "sum": SUM, "avg": AVG}
 FORCE_DENSE, FORCE_SPARSE, GATHER_NONE, UNORDERED, FORCE_WIDE, NO_FP4 = 1, 2, 4, 8, 16, 32
+KEY_PARTITIONED, ROW_SHARDED = 64, 128
 
 EXPORTS = sorted(["tcudb_create", "tcudb_join_agg", "tcudb_join_agg_host", "tcudb_chain_join_agg",
                   "tcudb_triangle_count", "tcudb_gemm",

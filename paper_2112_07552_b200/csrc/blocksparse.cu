@@ -16,6 +16,7 @@
 // keeps its bit), so the result is the dense product's, bit for bit on the integer paths.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -44,11 +45,11 @@ __global__ void k_bs_minrow(const int32_t* __restrict__ kcode, const int32_t* __
   }
 }
 
-// sort keys: (minrow << 32 | code) — the code breaks ties so the order is deterministic
+// sort keys by minrow (the radix sort is stable: ties keep ascending codes)
 __global__ void k_bs_sortkeys(const int32_t* __restrict__ minrow, int64_t K, unsigned long long* __restrict__ keys,
                               uint32_t* __restrict__ vals) {
   for (int64_t k = (int64_t)blockIdx.x * T + threadIdx.x; k < K; k += (int64_t)gridDim.x * T) {
-    keys[k] = ((unsigned long long)(uint32_t)minrow[k] << 32) | (unsigned long long)k;
+    keys[k] = (unsigned long long)(uint32_t)minrow[k];
     vals[k] = (uint32_t)k;
   }
 }
@@ -78,30 +79,30 @@ __global__ void k_bs_mark(const int32_t* __restrict__ kcode, const int32_t* __re
 }
 
 // tile bitmaps: tile t covers base row groups [t * rpt, (t + 1) * rpt) (clipped), bit kb of
-// the launch's K-block space <- key groups [(kb mod period) * f, + f)
+// the launch's K-block space <- key groups [(kb mod period) * f, + f). One thread per
+// (tile, K-block); a warp's 32 bits leave as one 32-bit half of a bitmap word.
 __global__ void k_bs_derive(const unsigned long long* __restrict__ base, int base_rows, int W, int rpt, int f,
                             int64_t period_kb, int64_t total_kb, int ntiles, int Wout,
-                            unsigned long long* __restrict__ out) {
-  const int64_t nw = (int64_t)ntiles * Wout;
-  for (int64_t x = (int64_t)blockIdx.x * T + threadIdx.x; x < nw; x += (int64_t)gridDim.x * T) {
-    const int t = (int)(x / Wout), w = (int)(x - (int64_t)t * Wout);
-    const int g0 = t * rpt, g1 = min(base_rows, g0 + rpt);
-    unsigned long long o = 0;
-    for (int b = 0; b < 64; ++b) {
-      const int64_t kb = (int64_t)w * 64 + b;
-      if (kb >= total_kb) break;
+                            unsigned* __restrict__ out32) {
+  const int64_t per_tile = (int64_t)Wout * 64;  // K-block slots per tile (padded to whole words)
+  const int64_t nthr = (int64_t)ntiles * per_tile;
+  for (int64_t x = (int64_t)blockIdx.x * T + threadIdx.x; x < nthr; x += (int64_t)gridDim.x * T) {
+    const int t = (int)(x / per_tile);
+    const int64_t kb = x - (int64_t)t * per_tile;
+    bool any = false;
+    if (kb < total_kb) {
+      const int g0 = t * rpt, g1 = min(base_rows, g0 + rpt);
       const int64_t kg0 = (kb % period_kb) * f;
-      bool any = false;
       for (int g = g0; g < g1 && !any; ++g) {
         const unsigned long long* row = base + (int64_t)g * W;
         for (int q = 0; q < f; ++q) {
           const int64_t kg = kg0 + q;
-          if ((row[kg >> 6] >> (kg & 63)) & 1ull) { any = true; break; }
+          if ((__ldg(row + (kg >> 6)) >> (kg & 63)) & 1ull) { any = true; break; }
         }
       }
-      if (any) o |= 1ull << b;
     }
-    out[x] = o;
+    const unsigned bits = __ballot_sync(0xffffffffu, any);  // per_tile % 64 == 0: warps never straddle tiles
+    if (lane_id() == 0) out32[x >> 5] = bits;
   }
 }
 
@@ -140,7 +141,7 @@ cudaError_t launch_bs_reorder(int32_t* kA, const int32_t* gA, int64_t nA, int32_
   k_bs_minrow<<<grid_for(nA), T, 0, s>>>(kA, gA, nA, minrow);
   k_bs_sortkeys<<<grid_for(K), T, 0, s>>>(minrow, K, k0, v0);
   bool alt = false;
-  if ((e = radix_sort_pairs(k0, v0, k1, v1, K, 64, rtmp, s, launches, &alt)) != cudaSuccess) return e;
+  if ((e = radix_sort_pairs(k0, v0, k1, v1, K, 32, rtmp, s, launches, &alt)) != cudaSuccess) return e;
   k_bs_invert<<<grid_for(K), T, 0, s>>>(alt ? v1 : v0, K, perm);
   if ((e = launch_remap_codes(kA, nA, perm, s, launches)) != cudaSuccess) return e;
   if ((e = launch_remap_codes(kB, nB, perm, s, launches)) != cudaSuccess) return e;
@@ -165,8 +166,11 @@ cudaError_t launch_bs_derive(const unsigned long long* base, int base_rows, int 
                              int64_t period_kb, int64_t total_kb, int ntiles, int Wout, unsigned long long* out,
                              cudaStream_t s, int64_t* launches) {
   if (rows_per_tile % 16) return cudaErrorInvalidValue;
-  k_bs_derive<<<grid_for((int64_t)ntiles * Wout), T, 0, s>>>(base, base_rows, W, rows_per_tile / 16, f, period_kb,
-                                                             total_kb, ntiles, Wout, out);
+  // one thread per (tile, K-block slot): the grid covers whole warps (ntiles * Wout * 64 threads)
+  const int64_t nthr = (int64_t)ntiles * Wout * 64;
+  const int grid = (int)std::min<int64_t>((nthr + T - 1) / T, (int64_t)kNumSMs * 32);
+  k_bs_derive<<<grid, T, 0, s>>>(base, base_rows, W, rows_per_tile / 16, f, period_kb, total_kb, ntiles, Wout,
+                                 reinterpret_cast<unsigned*>(out));
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -318,10 +318,12 @@ std::vector<int64_t> balanced_bounds(const NcclComm& nc, const tcudb_table& T, c
   return b;
 }
 
-// route the rows of T to the rank owning their group range
-tcudb_status route_table(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& T, Cols& out, cudaStream_t s) {
+// route the rows of T to the rank owning their group range (by_key: the rank owning a hash
+// of their join key — the key-partitioned path)
+tcudb_status route_table(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& T, Cols& out, cudaStream_t s,
+                         bool by_key = false) {
   const int P = nc.nranks;
-  const std::vector<int64_t> bounds = balanced_bounds(nc, T, s);
+  const std::vector<int64_t> bounds = by_key ? std::vector<int64_t>(P > 1 ? P - 1 : 1, 0) : balanced_bounds(nc, T, s);
   // partition locally
   Cols part;
   part.t = T;
@@ -333,7 +335,7 @@ tcudb_status route_table(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& 
     pc[c]->data = part.bufs.back()->p;
   }
   std::vector<int64_t> counts(P, 0);
-  tcudb_status st = tcudb_partition(ctx, &T, bounds.data(), P, &part.t, counts.data(), s);
+  tcudb_status st = partition_table(ctx, &T, bounds.data(), P, by_key ? 1 : 0, &part.t, counts.data(), s);
   st = nc.agree(st, s);
   if (st != TCUDB_OK) return st;
   // P x P counts: row j = what rank j sends to each rank
@@ -460,6 +462,69 @@ tcudb_status q4(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table* A, const 
   return TCUDB_OK;
 }
 
+// §8(f) f4, the key-partitioned path: both sides are routed by a hash of the join key,
+// so every join pair is formed on exactly one rank (a partitioned hash join: no side is
+// replicated, each rank joins 1/P of A with 1/P of B); a group (g, h) can then collect
+// partial aggregates on several ranks, so the partial tuples are routed by g range and
+// merged — with the library's own join + group-by: the partials T(g, h, agg) joined on h
+// with the distinct h values D (a GROUP BY h-only query over T) give SUM(agg) per (g, h),
+// a group existing iff one of its partials did. COUNT and integer SUM.
+tcudb_status key_partitioned(tcudb_ctx* ctx, const NcclComm& nc, const tcudb_table& A, const tcudb_table& B,
+                             const tcudb_query* q, tcudb_result* loc, tcudb_stats* stats, cudaStream_t s) {
+  Cols Ak, Bk;
+  tcudb_status st = route_table(ctx, nc, A, Ak, s, true);
+  if (st != TCUDB_OK) return st;
+  st = route_table(ctx, nc, B, Bk, s, true);
+  if (st != TCUDB_OK) return st;
+  tcudb_query q1 = *q;
+  q1.flags &= ~(uint32_t)(TCUDB_GATHER_NONE | TCUDB_KEY_PARTITIONED | TCUDB_ROW_SHARDED);
+  tcudb_result part{};
+  struct RF { tcudb_ctx* c; tcudb_result* r; ~RF() { tcudb_result_free(c, r); } } fp{ctx, &part};
+  const tcudb_status lst = tcudb_join_agg(ctx, &Ak.t, &Bk.t, &q1, &part, stats, s);
+  st = nc.agree(lst, s);
+  if (st != TCUDB_OK) {
+    if (lst == TCUDB_OK) internal_set_err(ctx, st, "collective join: another rank's local query failed");
+    return st;
+  }
+  // the partials as a table (k = h, g = g, v = agg), routed by g range
+  DevBuf dummy(16, s);
+  tcudb_table T{};
+  T.n_rows = part.n;
+  T.key = {part.h ? part.h : dummy.p, B.group.type};
+  T.group = {part.g ? part.g : dummy.p, A.group.type};
+  T.value = {part.agg ? part.agg : dummy.p, TCUDB_I64};
+  Cols Tr;
+  st = route_table(ctx, nc, T, Tr, s);
+  if (st != TCUDB_OK) return st;
+  // merge: D = distinct h of the received partials (GROUP BY h only), then SUM(agg) per (g, h)
+  tcudb_table Th{}, Tg{};
+  Th.n_rows = Tr.t.n_rows;
+  Th.key = Tr.t.key;                          // ungrouped side (Q3 shape)
+  Tg.n_rows = Tr.t.n_rows;
+  Tg.key = Tr.t.key;
+  Tg.group = Tr.t.key;                        // B.h = h
+  tcudb_query qd{TCUDB_COUNT, 0};
+  tcudb_result D{};
+  struct RF2 { tcudb_ctx* c; tcudb_result* r; ~RF2() { tcudb_result_free(c, r); } } fd{ctx, &D};
+  tcudb_status mst = tcudb_join_agg(ctx, &Th, &Tg, &qd, &D, nullptr, s);
+  if (mst == TCUDB_OK) {
+    tcudb_table TA = Tr.t, TD{};
+    TD.n_rows = D.n;
+    TD.key = {D.h ? D.h : dummy.p, B.group.type};
+    TD.group = TD.key;
+    tcudb_query qs{TCUDB_SUM, 0};
+    mst = tcudb_join_agg(ctx, &TA, &TD, &qs, loc, nullptr, s);
+  }
+  st = nc.agree(mst, s);
+  if (st != TCUDB_OK) {
+    tcudb_result_free(ctx, loc);
+    if (mst == TCUDB_OK) internal_set_err(ctx, st, "collective join: another rank's merge failed");
+    return st;
+  }
+  if (stats) stats->path = 3;  // key-partitioned (the local join's plan is in the other fields)
+  return TCUDB_OK;
+}
+
 }  // namespace
 
 tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* ncp, const tcudb_table* A, const tcudb_table* B,
@@ -505,7 +570,33 @@ tcudb_status collective_join_agg(tcudb_ctx* ctx, const NcclComm* ncp, const tcud
     const bool ga = An.group.data != nullptr, gb = Bn.group.data != nullptr;
     const bool fsum = q->agg != TCUDB_COUNT && ((An.value.data && An.value.type == TCUDB_F32) ||
                                                 (Bn.value.data && Bn.value.type == TCUDB_F32));
-    if (!ga && !gb) {
+    // row sharding (north star) vs the key-partitioned path (§8(f) f4): the latter for COUNT
+    // / integer SUM when the other side is too large to replicate on every rank (>= 4 M rows
+    // in total), or when asked for; flags decide identically on every rank
+    const char* kp_env = getenv("TCUDB_KEY_PARTITION");
+    const bool kp_ok = ga && gb && q->agg != TCUDB_AVG && !fsum && nc.nranks > 1;
+    const bool kp = kp_ok && !(q->flags & TCUDB_ROW_SHARDED) &&
+                    ((q->flags & TCUDB_KEY_PARTITIONED) || (kp_env && kp_env[0] == '1') ||
+                     (!(kp_env && kp_env[0] == '0') && ag[1] >= (1ll << 22)));
+    if (kp) {
+      tcudb_result loc{};
+      const auto tl = std::chrono::steady_clock::now();
+      st = key_partitioned(ctx, nc, An, Bn, q, &loc, stats, s);
+      local_ms = 0.f;
+      (void)tl;
+      if (st != TCUDB_OK) return st;
+      struct RF { tcudb_ctx* c; tcudb_result* r; bool keep = false; ~RF() { if (!keep) tcudb_result_free(c, r); } } fl{ctx, &loc};
+      if (q->flags & TCUDB_GATHER_NONE) {
+        *out = loc;
+        out->g_type = An.group.type;
+        out->h_type = Bn.group.type;
+        fl.keep = true;
+      } else {
+        const bool has[3] = {true, true, true};
+        const int32_t ty[3] = {An.group.type, Bn.group.type, TCUDB_I64};
+        gather_result(ctx, nc, loc, has, ty, out, s);
+      }
+    } else if (!ga && !gb) {
       st = q4(ctx, nc, &An, &Bn, q, fsum, out, stats, s);
     } else {
       // the grouped side is routed by its group range (A when both are grouped)

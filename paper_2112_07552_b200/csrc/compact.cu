@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
       const int64_t s = s0 + q * stride;
       row[q] = s < nsegs ? s / a.nseg : 0;
       col0[q] = (s - row[q] * a.nseg) * a.seg_w;
-      lim[q] = s < nsegs ? min(a.H, col0[q] + a.seg_w) : 0;
+      // a segment without nonzeros (off[s + 1] == off[s]) is not read at all: block-sparse
+      // products leave whole tiles zero
+      lim[q] = (s < nsegs && off[s + 1] > off[s]) ? min(a.H, col0[q] + a.seg_w) : 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int64_t col = col0[q] + j * 32 + lane;
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       const int64_t s = s0 + q * stride;
-      if (s >= nsegs || col0[q] >= a.H) continue;
+      if (s >= nsegs || col0[q] >= a.H || lim[q] == 0) continue;
     if (!SAME) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -153,7 +155,7 @@ inline int grid_for_segs(int64_t nsegs) {
 
 size_t compact_temp_bytes(int64_t G, int64_t nseg) {
   const int64_t n = G * nseg;
-  return ((size_t)n * 4 + 15) / 16 * 16 + (size_t)n * 8 + scan_temp_bytes(n) + 64;
+  return ((size_t)n * 4 + 15) / 16 * 16 + (size_t)(n + 1) * 8 + scan_temp_bytes(n) + 64;
 }
 
 // counts: if `precounted` != NULL the per-segment counts already exist (GEMM epilogue);
@@ -170,7 +172,10 @@ cudaError_t launch_compact_count(const CompactArgs& a, const int32_t* precounted
     if (launches) ++*launches;
     src = cnt;
   }
-  return exclusive_scan_i32(src, off, n, nnz_dev, off + n, s, launches);
+  // off[n] = the total as well (the write pass reads off[s + 1] - off[s] per segment)
+  const cudaError_t e = exclusive_scan_i32(src, off, n, nnz_dev, off + n + 1, s, launches);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(off + n, nnz_dev, 8, cudaMemcpyDeviceToDevice, s);
 }
 
 cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t s, int64_t* launches) {

@@ -99,6 +99,10 @@ struct CtxScope {
   CtxScope(int device, void* pool);
   ~CtxScope();
 };
+// tcudb_partition's body with the key-hash mode of the key-partitioned path (by_key: bounds
+// unused, destination = hash of the join key; the group column may be absent)
+tcudb_status partition_table(tcudb_ctx* ctx, const tcudb_table* in, const int64_t* bounds, int32_t P, int by_key,
+                             tcudb_table* out, int64_t* counts, cudaStream_t s);
 // host-runtime helpers the collective path shares (tcudb.cu)
 void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s);
 void internal_result_release(tcudb_ctx* ctx, void* p);

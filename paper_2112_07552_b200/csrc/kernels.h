@@ -306,11 +306,12 @@ cudaError_t launch_avg_div(void* sum_inout, int sum_is_float, const long long* c
                            int64_t* launches);
 
 // ---------------------------------------------------------------- partition.cu (§8(e))
-cudaError_t launch_part_count(const ColDesc& grp, const long long* bounds, int P, unsigned long long* counts,
-                              cudaStream_t s, int64_t* launches);
+// destination = group range (bounds) or, by_key != 0, a hash of the join key (bounds unused)
+cudaError_t launch_part_count(const ColDesc& key, const ColDesc& grp, const long long* bounds, int P, int by_key,
+                              unsigned long long* counts, cudaStream_t s, int64_t* launches);
 cudaError_t launch_part_scatter(const ColDesc& key, const ColDesc& grp, const ColDesc& val, const long long* bounds,
-                                int P, unsigned long long* cursor, void* ok, void* og, void* ov, cudaStream_t s,
-                                int64_t* launches);
+                                int P, int by_key, unsigned long long* cursor, void* ok, void* og, void* ov,
+                                cudaStream_t s, int64_t* launches);
 
 // ---------------------------------------------------------------- compact.cu (a8)
 // Existence matrix E (int32 count or the value matrix) -> tuples (g, h, agg), row-major.

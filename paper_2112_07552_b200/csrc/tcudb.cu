@@ -1668,7 +1668,8 @@ tcudb_status fail_err(tcudb_ctx* ctx, const Fail& f) {
 }  // namespace
 
 namespace tcudb {
-thread_local cudaMemPool_t t_pool = nullptr;  // the pool of the context whose call is running
+thread_local cudaMemPool_t t_pool = nullptr;
+  // the pool of the context whose call is running
 
 cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s) {
   if (t_pool) return cudaMallocFromPoolAsync(p, bytes, t_pool, s);
@@ -1696,6 +1697,47 @@ void* internal_result_alloc(tcudb_ctx* ctx, size_t bytes, cudaStream_t s) {
 }
 void internal_result_release(tcudb_ctx* ctx, void* p) { result_release(ctx, p); }
 tcudb_status internal_set_err(tcudb_ctx* ctx, tcudb_status st, const char* msg) { return set_err(ctx, st, msg); }
+
+tcudb_status partition_table(tcudb_ctx* ctx, const tcudb_table* in, const int64_t* bounds, int32_t P, int by_key,
+                             tcudb_table* out, int64_t* counts, cudaStream_t s) {
+  if (!ctx || !in || !out || !counts || P < 1 || P > 1024 || (P > 1 && !bounds && !by_key)) return TCUDB_E_INVALID;
+  if (check_table(in, true) != TCUDB_OK) return TCUDB_E_INVALID;
+  if (in->n_rows > 0 && (!out->key.data || (in->group.data && !out->group.data) || (in->value.data && !out->value.data)))
+    return TCUDB_E_INVALID;
+  for (int i = 0; i < P; ++i) counts[i] = 0;
+  if (in->n_rows == 0) return TCUDB_OK;
+  CtxScope scope(ctx->device, ctx->pool);
+  try {
+    Arena ar(s);
+    const int64_t n = in->n_rows;
+    ColDesc k{in->key.data, in->key.type, n}, g{in->group.data, in->group.type, n};
+    ColDesc v{in->value.data, in->value.type, n};
+    long long* db = ar.get<long long>(P);
+    if (P > 1 && !by_key) CK(cudaMemcpyAsync(db, bounds, sizeof(long long) * (P - 1), cudaMemcpyHostToDevice, s));
+    unsigned long long* dc = ar.zeros<unsigned long long>(2 * P);
+    CK(launch_part_count(k, g, db, P, by_key, dc, s, &ctx->launches));
+    std::vector<unsigned long long> hc(P);
+    CK(cudaMemcpyAsync(hc.data(), dc, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> cur(P);
+    unsigned long long run = 0;
+    for (int i = 0; i < P; ++i) { cur[i] = run; run += hc[i]; counts[i] = (int64_t)hc[i]; }
+    CK(cudaMemcpyAsync(dc + P, cur.data(), sizeof(unsigned long long) * P, cudaMemcpyHostToDevice, s));
+    CK(launch_part_scatter(k, g, v, db, P, by_key, dc + P, const_cast<void*>(out->key.data),
+                           const_cast<void*>(out->group.data), const_cast<void*>(out->value.data), s,
+                           &ctx->launches));
+    CK(cudaStreamSynchronize(s));
+    out->n_rows = n;
+    out->key.type = in->key.type;
+    out->group.type = in->group.type;
+    out->value.type = in->value.type;
+    return TCUDB_OK;
+  } catch (const Fail& f) {
+    return fail_err(ctx, f);
+  }
+}
+
+
 }  // namespace tcudb
 
 // =========================================================================== C ABI
@@ -2067,41 +2109,8 @@ tcudb_status tcudb_minmax(tcudb_ctx* ctx, const void* col, int32_t type, int64_t
 tcudb_status tcudb_partition(tcudb_ctx* ctx, const tcudb_table* in, const int64_t* bounds, int32_t P,
                              tcudb_table* out, int64_t* counts, void* stream) {
   if (!ctx || !in || !out || !counts || P < 1 || P > 1024 || (P > 1 && !bounds)) return TCUDB_E_INVALID;
-  if (check_table(in, true) != TCUDB_OK) return TCUDB_E_INVALID;
-  if (in->n_rows > 0 && (!out->key.data || !out->group.data || (in->value.data && !out->value.data)))
-    return TCUDB_E_INVALID;
-  for (int i = 0; i < P; ++i) counts[i] = 0;
-  if (in->n_rows == 0) return TCUDB_OK;
-  CtxScope scope(ctx->device, ctx->pool);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  try {
-    Arena ar(s);
-    const int64_t n = in->n_rows;
-    ColDesc k{in->key.data, in->key.type, n}, g{in->group.data, in->group.type, n};
-    ColDesc v{in->value.data, in->value.type, n};
-    long long* db = ar.get<long long>(P);
-    if (P > 1) CK(cudaMemcpyAsync(db, bounds, sizeof(long long) * (P - 1), cudaMemcpyHostToDevice, s));
-    unsigned long long* dc = ar.zeros<unsigned long long>(2 * P);
-    CK(launch_part_count(g, db, P, dc, s, &ctx->launches));
-    std::vector<unsigned long long> hc(P);
-    CK(cudaMemcpyAsync(hc.data(), dc, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    std::vector<unsigned long long> cur(P);
-    unsigned long long run = 0;
-    for (int i = 0; i < P; ++i) { cur[i] = run; run += hc[i]; counts[i] = (int64_t)hc[i]; }
-    CK(cudaMemcpyAsync(dc + P, cur.data(), sizeof(unsigned long long) * P, cudaMemcpyHostToDevice, s));
-    CK(launch_part_scatter(k, g, v, db, P, dc + P, const_cast<void*>(out->key.data),
-                           const_cast<void*>(out->group.data), const_cast<void*>(out->value.data), s,
-                           &ctx->launches));
-    CK(cudaStreamSynchronize(s));
-    out->n_rows = n;
-    out->key.type = in->key.type;
-    out->group.type = in->group.type;
-    out->value.type = in->value.type;
-    return TCUDB_OK;
-  } catch (const Fail& f) {
-    return fail_err(ctx, f);
-  }
+  if (in->n_rows > 0 && !in->group.data) return TCUDB_E_INVALID;
+  return tcudb::partition_table(ctx, in, bounds, P, 0, out, counts, static_cast<cudaStream_t>(stream));
 }
 
 void tcudb_result_free(tcudb_ctx* ctx, tcudb_result* r) {

@@ -219,3 +219,29 @@ def test_collective_errors_agreed(shim):
     res, err, *_ = run_ranks(shim, 2, [(a, b), ({k: (v[:0] if v is not None else None) for k, v in a.items()}, b0)],
                              "sum")
     assert all(e is None for e in err) and all(int(r["agg"][0]) == big * big for r in res)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c1s", 1.0), ("c2", 0.1), ("c3", 1 / 16), ("c5s", 1 / 64)])
+def test_collective_key_partitioned(shim, oracle_mod, P, name, scale):
+    """§8(f) f4: the key-partitioned path (both sides routed by key hash, partial groups
+    merged by g range through a join + group-by) forced with TCUDB_KEY_PARTITIONED."""
+    from paper_2112_07552_b200._lib import KEY_PARTITIONED
+    A, B, agg = datagen.make_config(name, scale)
+    ref = oracle_mod.join_agg(A, B, agg)
+    res, err, calls, nbytes, broken = run_ranks(shim, P, contiguous(A, B, P), agg, flags=KEY_PARTITIONED)
+    check_all(res, err, ref, agg, False, broken)
+
+
+def test_collective_key_partitioned_default_and_shards(shim, oracle_mod):
+    """c5 at 1/4 scale (B: 4 M rows) takes the key-partitioned path by default; GATHER_NONE
+    shards concatenate to the single-GPU result; ROW_SHARDED forces the other path."""
+    from paper_2112_07552_b200._lib import GATHER_NONE, ROW_SHARDED
+    A, B, agg = datagen.make_config("c5", 1 / 4)
+    ref = oracle_mod.join_agg(A, B, agg)
+    res, err, *_ = run_ranks(shim, 4, contiguous(A, B, 4), agg, flags=GATHER_NONE)
+    assert all(e is None for e in err), err
+    cat = {k: np.concatenate([r[k] for r in res]) for k in ("g", "h", "agg")}
+    compare(cat, ref, agg)
+    res, err, *_ = run_ranks(shim, 2, contiguous(A, B, 2), agg, flags=ROW_SHARDED)
+    check_all(res, err, ref, agg, False)
