@@ -54,6 +54,11 @@ __global__ void k_bs_sortkeys(const int32_t* __restrict__ minrow, int64_t K, uns
   }
 }
 
+__global__ void k_bs_clamp(unsigned long long* __restrict__ keys, int64_t K, unsigned long long G) {
+  for (int64_t k = (int64_t)blockIdx.x * T + threadIdx.x; k < K; k += (int64_t)gridDim.x * T)
+    if (keys[k] > G) keys[k] = G;
+}
+
 __global__ void k_bs_invert(const uint32_t* __restrict__ sorted_vals, int64_t K, int32_t* __restrict__ perm) {
   for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < K; i += (int64_t)gridDim.x * T)
     perm[sorted_vals[i]] = (int32_t)i;
@@ -125,7 +130,7 @@ size_t bs_reorder_temp_bytes(int64_t K) {
 }
 
 cudaError_t launch_bs_reorder(int32_t* kA, const int32_t* gA, int64_t nA, int32_t* kB, int64_t nB, int32_t* cntA,
-                              int32_t* cntB, int64_t K, void* temp, cudaStream_t s, int64_t* launches) {
+                              int32_t* cntB, int64_t K, int64_t G, void* temp, cudaStream_t s, int64_t* launches) {
   if (K <= 0) return cudaSuccess;
   char* t = static_cast<char*>(temp);
   auto take = [&](size_t bytes) { char* p = t; t += (bytes + 255) / 256 * 256; return p; };
@@ -141,7 +146,15 @@ cudaError_t launch_bs_reorder(int32_t* kA, const int32_t* gA, int64_t nA, int32_
   k_bs_minrow<<<grid_for(nA), T, 0, s>>>(kA, gA, nA, minrow);
   k_bs_sortkeys<<<grid_for(K), T, 0, s>>>(minrow, K, k0, v0);
   bool alt = false;
-  if ((e = radix_sort_pairs(k0, v0, k1, v1, K, 32, rtmp, s, launches, &alt)) != cudaSuccess) return e;
+  // minrow < G, or the "no A row" marker 0x7F7F7F7F: sort only the bits that can differ
+  int bits = 32;
+  if (G < (1ll << 24)) {
+    // keys without an A tuple sort last either way: clamp their marker to G
+    bits = 8;
+    while (bits < 32 && ((int64_t)1 << bits) <= G) bits += 8;
+    k_bs_clamp<<<grid_for(K), T, 0, s>>>(k0, K, (unsigned long long)G);
+  }
+  if ((e = radix_sort_pairs(k0, v0, k1, v1, K, bits, rtmp, s, launches, &alt)) != cudaSuccess) return e;
   k_bs_invert<<<grid_for(K), T, 0, s>>>(alt ? v1 : v0, K, perm);
   if ((e = launch_remap_codes(kA, nA, perm, s, launches)) != cudaSuccess) return e;
   if ((e = launch_remap_codes(kB, nB, perm, s, launches)) != cudaSuccess) return e;

@@ -193,12 +193,23 @@ cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t 
       default: launch_write_t<3, 3, true>(a, off, grid, s);
     }
   } else {
-    if (a.e_kind != 0) return cudaErrorInvalidValue;  // separate existence planes are int32 counts
-    switch (a.v_kind) {
-      case 0: launch_write_t<0, 0, false>(a, off, grid, s); break;
-      case 1: launch_write_t<0, 1, false>(a, off, grid, s); break;
-      case 2: launch_write_t<0, 2, false>(a, off, grid, s); break;
-      default: launch_write_t<0, 3, false>(a, off, grid, s);
+    // separate existence planes: int32 counts (u8 pattern GEMM) or u16 (e2m1 pattern GEMM)
+    if (a.e_kind == 0) {
+      switch (a.v_kind) {
+        case 0: launch_write_t<0, 0, false>(a, off, grid, s); break;
+        case 1: launch_write_t<0, 1, false>(a, off, grid, s); break;
+        case 2: launch_write_t<0, 2, false>(a, off, grid, s); break;
+        default: launch_write_t<0, 3, false>(a, off, grid, s);
+      }
+    } else if (a.e_kind == 4) {
+      switch (a.v_kind) {
+        case 0: launch_write_t<4, 0, false>(a, off, grid, s); break;
+        case 1: launch_write_t<4, 1, false>(a, off, grid, s); break;
+        case 2: launch_write_t<4, 2, false>(a, off, grid, s); break;
+        default: launch_write_t<4, 3, false>(a, off, grid, s);
+      }
+    } else {
+      return cudaErrorInvalidValue;
     }
   }
   if (launches) ++*launches;

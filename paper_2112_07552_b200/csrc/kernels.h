@@ -350,7 +350,7 @@ namespace tcudb {
 // are rewritten in place).
 size_t bs_reorder_temp_bytes(int64_t K);
 cudaError_t launch_bs_reorder(int32_t* kA, const int32_t* gA, int64_t nA, int32_t* kB, int64_t nB, int32_t* cntA,
-                              int32_t* cntB, int64_t K, void* temp, cudaStream_t s, int64_t* launches);
+                              int32_t* cntB, int64_t K, int64_t G, void* temp, cudaStream_t s, int64_t* launches);
 // base occupancy bitmap (zeroed by the caller): 16-row x 64-key blocks, W words per row group
 cudaError_t launch_bs_mark(const int32_t* kcode, const int32_t* rcode, int64_t n, int W, unsigned long long* bm,
                            cudaStream_t s, int64_t* launches);

@@ -788,38 +788,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   double bs_frac = 1.0;
   unsigned long long *bs_baseA = nullptr, *bs_baseB = nullptr;
   int bs_W = 0;
-  if (!bs_off && (bs_force || dense_ops >= 2e12) && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
-    CK(launch_bs_reorder(kA, gA, nA, kB, nB, cntA, cntB, K, ar.get<char>((int64_t)bs_reorder_temp_bytes(K)), s, L));
-    const int64_t kgroups = (Kp * 4 + 63) / 64;  // 64-key groups over the widest K' (the split's 4 Kp)
-    bs_W = (int)((kgroups + 63) / 64);
-    bs_baseA = ar.zeros<unsigned long long>(Gp / 16 * bs_W);
-    bs_baseB = ar.zeros<unsigned long long>(Hp / 16 * bs_W);
-    CK(launch_bs_mark(kA, gA, nA, bs_W, bs_baseA, s, L));
-    CK(launch_bs_mark(kB, hB, nB, bs_W, bs_baseB, s, L));
-    // the share at kind::i8 granularity (128-row A tiles, 256-row B tiles, 128-key blocks)
-    const int tm = (int)(Gp / 128), tn = (int)(Hp / 256);
-    const int64_t nkb = Kp / 128;
-    const int Wt = (int)((nkb + 63) / 64);
-    unsigned long long* ta = ar.get<unsigned long long>((int64_t)tm * Wt);
-    unsigned long long* tb = ar.get<unsigned long long>((int64_t)tn * Wt);
-    CK(launch_bs_derive(bs_baseA, (int)(Gp / 16), bs_W, 128, 2, nkb, nkb, tm, Wt, ta, s, L));
-    CK(launch_bs_derive(bs_baseB, (int)(Hp / 16), bs_W, 256, 2, nkb, nkb, tn, Wt, tb, s, L));
-    unsigned long long* act = ar.zeros<unsigned long long>(1);
-    CK(launch_bs_active(ta, tb, tm, tn, Wt, act, s, L));
-    const unsigned long long a = *to_pinned<unsigned long long>(ctx, act, s);
-    bs_frac = (double)a / ((double)tm * (double)tn * (double)nkb);
-  }
-  const bool use_bs = bs_baseA && (bs_force || bs_frac <= 0.85);
-  S.block_active = use_bs ? bs_frac : 0.0;
-  // tile bitmaps of one GEMM launch kind (cached): rows per B tile, 64-key groups per K-block,
-  // K-blocks of the launch's K' space and the period of the key space along it
+  // the GEMM kind the fill will most likely take (its tile bitmaps measure the share and are
+  // reused by the launch): e2m1 COUNT, u8 otherwise, bf16 for floats
+  const bool fp4_guess = !is_sum && ctx->fp4 && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && K < (1 << 24) &&
+                         dense_ops >= 1e11;
+  const double gemm_rate = is_float ? ctx->cal.R_bf16 : fp4_guess ? ctx->cal.R_fp4 : ctx->cal.R_i8;
   struct BsMaps { const unsigned long long *a = nullptr, *b = nullptr; int w = 0; };
   std::map<int, BsMaps> bs_cache;
-  auto bs_maps = [&](int kind /*0 i8, 1 bf16, 2 bf16 split, 3 e2m1*/, int64_t total_kb, int64_t period_kb) {
-    BsMaps m;
-    if (!use_bs) return m;
+  // tile bitmaps of one GEMM launch kind (cached): rows per B tile, 64-key groups per K-block,
+  // K-blocks of the launch's K' space and the period of the key space along it
+  auto bs_derive = [&](int kind /*0 i8, 1 bf16, 2 bf16 split, 3 e2m1*/, int64_t total_kb, int64_t period_kb) {
     auto it = bs_cache.find(kind);
     if (it != bs_cache.end()) return it->second;
+    BsMaps m;
     const int bn = kind == 3 ? kGemmBNFp4 : 256;
     const int f = kind == 3 ? 4 : kind == 0 ? 2 : 1;
     const int tm = (int)(Gp / 128), tn = (int)((Hp + bn - 1) / bn);
@@ -831,6 +812,37 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     m.a = ta; m.b = tb;
     bs_cache[kind] = m;
     return m;
+  };
+  // the analysis costs ~0.2 ms (a key sort, two marking passes, a host sync): only when the
+  // dense product would take >= 1 ms at the device's measured rate
+  if (!bs_off && (bs_force || dense_ops / gemm_rate >= 1e-3) && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
+    CK(launch_bs_reorder(kA, gA, nA, kB, nB, cntA, cntB, K, G, ar.get<char>((int64_t)bs_reorder_temp_bytes(K)), s,
+                         L));
+    const int64_t kgroups = (Kp * 4 + 63) / 64;  // 64-key groups over the widest K' (the split's 4 Kp)
+    bs_W = (int)((kgroups + 63) / 64);
+    bs_baseA = ar.zeros<unsigned long long>(Gp / 16 * bs_W);
+    bs_baseB = ar.zeros<unsigned long long>(Hp / 16 * bs_W);
+    CK(launch_bs_mark(kA, gA, nA, bs_W, bs_baseA, s, L));
+    CK(launch_bs_mark(kB, hB, nB, bs_W, bs_baseB, s, L));
+    const int kind = is_float ? 1 : fp4_guess ? 3 : 0;
+    const int64_t Kp4g = round_up(K, 256);
+    const int64_t nkb = kind == 3 ? Kp4g / 256 : kind == 1 ? Kp / 64 : Kp / 128;
+    const BsMaps m = bs_derive(kind, nkb, nkb);
+    const int bn = kind == 3 ? kGemmBNFp4 : 256;
+    const int tm = (int)(Gp / 128), tn = (int)((Hp + bn - 1) / bn);
+    unsigned long long* act = ar.zeros<unsigned long long>(1);
+    CK(launch_bs_active(m.a, m.b, tm, tn, m.w, act, s, L));
+    const unsigned long long a = *to_pinned<unsigned long long>(ctx, act, s);
+    bs_frac = (double)a / ((double)tm * (double)tn * (double)nkb);
+  }
+  const bool use_bs = bs_baseA && (bs_force || bs_frac <= 0.85);
+  S.block_active = use_bs ? bs_frac : 0.0;
+  auto bs_maps = [&](int kind, int64_t total_kb, int64_t period_kb) {
+    BsMaps m;
+    if (!use_bs) return m;
+    auto it = bs_cache.find(kind);
+    if (it != bs_cache.end()) return it->second;
+    return bs_derive(kind, total_kb, period_kb);
   };
   auto with_bs = [&](GemmArgs& g, int kind, int64_t total_kb, int64_t period_kb) {
     const BsMaps m = bs_maps(kind, total_kb, period_kb);
@@ -932,6 +944,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     // ---------------- a5 fill
     uint8_t *opA = nullptr, *opB = nullptr;        // value planes (int8) or bf16 operands
     uint8_t *patA = nullptr, *patB = nullptr;      // existence pattern planes
+    bool pat4 = false;                              // ... as e2m1 0/1 operands
     int PA = 1, PB = 1, sA = 0, sB = 0;
     unsigned long long maxA = 1, maxB = 1;          // max |digit-plane value| for the int32 chunk bound
     FillStats* fs = ar.zeros<FillStats>(2);
@@ -1100,10 +1113,21 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       opB = reinterpret_cast<uint8_t*>(fB);
     }
     if (need_exist) {
-      patA = ar.zeros<uint8_t>(cellsA);
-      patB = ar.zeros<uint8_t>(cellsB);
-      CK(launch_fill_pattern_u8(kA, gA, nA, patA, Kp, s, L));
-      CK(launch_fill_pattern_u8(kB, hB, nB, patB, Kp, s, L));
+      // existence pattern (R3): 0/1 cells -> e2m1 operands (kind::mxf4, exact for K < 2^24,
+      // half the operand bytes and twice the kind::i8 rate); u8 when e2m1 is off
+      if (ctx->fp4 && !(q->flags & TCUDB_NO_FP4) && K < (1 << 24)) {
+        pat4 = true;
+        patA = ar.zeros<uint8_t>(Gp * Kp4 / 2);
+        patB = ar.zeros<uint8_t>(Hp * Kp4 / 2);
+        FillStats* fsp = ar.zeros<FillStats>(2);  // duplicate cells are fine for a pattern (OR)
+        CK(launch_fill_count_fp4(kA, gA, nA, patA, Kp4, fsp + 0, s, L));
+        CK(launch_fill_count_fp4(kB, hB, nB, patB, Kp4, fsp + 1, s, L));
+      } else {
+        patA = ar.zeros<uint8_t>(cellsA);
+        patB = ar.zeros<uint8_t>(cellsB);
+        CK(launch_fill_pattern_u8(kA, gA, nA, patA, Kp, s, L));
+        CK(launch_fill_pattern_u8(kB, hB, nB, patB, Kp, s, L));
+      }
     }
     tm.mark(&S.ms_fill);
 
@@ -1114,7 +1138,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     // the GEMM that produces the existence matrix also emits per-(row, N-tile) nonzero counts
     ca.nseg = Hp / 256;
     ca.seg_w = 256;
-    if (op4A) {
+    if (op4A || pat4) {  // segments follow the e2m1 GEMM's 240-column N tiles
       ca.nseg = (Hp + kGemmBNFp4 - 1) / kGemmBNFp4;
       ca.seg_w = kGemmBNFp4;
     }
@@ -1239,7 +1263,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         ca.E = C; ca.e_kind = 1; ca.lde = Hp; ca.V = C; ca.v_kind = 1; ca.ldv = Hp;
       }
     }
-    if (need_exist) {
+    if (need_exist && pat4) {
+      const int64_t Hc = ca.nseg * kGemmBNFp4;
+      const bool c16 = K < 65536;  // a pattern count is <= K
+      void* E = c16 ? (void*)ar.get<uint16_t>(Gp * Hc) : (void*)ar.get<int32_t>(Gp * Hc);
+      GemmArgs ge{};
+      ge.M = Gp; ge.N = Hp; ge.elem = ELEM_FP4; ge.A = patA; ge.lda = Kp4 / 2; ge.B = patB; ge.ldb = Kp4 / 2;
+      ge.k_begin = 0; ge.k_len = Kp4 / 2; ge.epi = c16 ? EPI_STORE16 : EPI_STORE32; ge.C = E; ge.ldc = Hc;
+      ge.cnt_out = seg_cnt; ge.ldcnt = ca.nseg;
+      with_bs(ge, 3, Kp4 / 256, Kp4 / 256);
+      CK(launch_gemm(ge, s, L));
+      ops += 2.0 * Gp * Hc * Kp4;
+      ca.E = E; ca.e_kind = c16 ? 4 : 0; ca.lde = Hc;
+    } else if (need_exist) {
       int32_t* E = ar.get<int32_t>(Gp * Hp);
       GemmArgs ge{};
       ge.M = Gp; ge.N = Hp; ge.elem = ELEM_I8; ge.A = patA; ge.lda = Kp; ge.B = patB; ge.ldb = Kp;
@@ -1632,6 +1668,172 @@ void calibrate(tcudb_ctx* c) {
   g_calib[c->device] = cal;
 }
 
+// ---------------------------------------------------------------------------
+// Digit-plane product (a6 wide path): C64 = sum_ij 256^(i+j) X_i · Y_j^T over K chunks
+// that keep every int32 partial exact; the last launch emits the per-segment nonzero counts.
+struct Planes {
+  uint8_t* op = nullptr;
+  int P = 1, top_signed = 0;
+  unsigned long long maxv = 255;  // max |plane value| (255 once multi-plane)
+  int64_t cells = 0;              // elements per plane
+};
+
+// int64 scratch [rows][Kp] -> stats -> digit planes (guard a3)
+Planes make_planes(tcudb_ctx* ctx, Arena& ar, long long* scr, int64_t cells, FillStats* fs, int64_t* L) {
+  cudaStream_t s = ar.s;
+  CK(launch_scratch_stats_i64(scr, cells, fs, s, L));
+  FillStats hf = *to_pinned<FillStats>(ctx, fs, s);
+  Planes p;
+  p.top_signed = hf.neg ? 1 : 0;
+  p.P = 1;
+  if (hf.neg) { while (p.P < 8 && hf.max_abs > ((1ull << (8 * p.P - 1)) - 1)) ++p.P; }
+  else { while (p.P < 8 && hf.max_abs > ((1ull << (8 * p.P)) - 1)) ++p.P; }
+  p.maxv = p.P == 1 ? std::max<unsigned long long>(hf.max_abs, 1) : 255;
+  p.cells = cells;
+  p.op = ar.get<uint8_t>(cells * p.P);
+  CK(launch_pack_planes(scr, cells, p.P, p.top_signed, p.op, cells, s, L));
+  return p;
+}
+
+double gemm_planes(Arena& ar, const Planes& X, const Planes& Y, int64_t M, int64_t N, int64_t Kp, long long* C,
+                   int64_t ldc, int32_t* cnt_out, int64_t ldcnt, int64_t* L) {
+  const unsigned long long prod = X.maxv * Y.maxv ? X.maxv * Y.maxv : 1;
+  int64_t kc = (int64_t)((2147483647ull / prod) / 128 * 128);
+  if (kc < 128) kc = 128;
+  const int total = X.P * Y.P * (int)((Kp + kc - 1) / kc);
+  int n = 0;
+  double ops = 0;
+  GemmArgs ga{};
+  ga.M = M; ga.N = N; ga.elem = ELEM_I8; ga.C = C; ga.ldc = ldc;
+  for (int i = 0; i < X.P; ++i)
+    for (int j = 0; j < Y.P; ++j)
+      for (int64_t k0 = 0; k0 < Kp; k0 += kc) {
+        ga.a_signed = (i == X.P - 1) && X.top_signed;
+        ga.b_signed = (j == Y.P - 1) && Y.top_signed;
+        ga.A = X.op + (int64_t)i * X.cells; ga.lda = Kp;
+        ga.B = Y.op + (int64_t)j * Y.cells; ga.ldb = Kp;
+        ga.k_begin = k0; ga.k_len = std::min<int64_t>(kc, Kp - k0);
+        ga.epi = n == 0 ? EPI_SET64 : EPI_ACC64; ga.shift = 8 * (i + j);
+        ga.cnt_out = n == total - 1 ? cnt_out : nullptr; ga.ldcnt = ldcnt;
+        CK(launch_gemm(ga, ar.s, L));
+        ops += 2.0 * M * N * ga.k_len;
+        ++n;
+      }
+  return ops;
+}
+
+// §8(f) f3, the chain exception (§3.2): when B is projected out, the
+// 3-way join A -> B -> C is the matrix chain mat(A) × mat(B)^T × mat(C)^T — no nonzero()
+// table conversion of the intermediate. Here: T = A_op · B_op^T (G x K2, int64, digit
+// planes), T itself re-packed as digit planes (it is already K2-major: row g over ID_2),
+// R = T · C_op^T (G x H), compacted. COUNT only (with values the intermediate would carry
+// SUM(A.v·B.w) per (g, ID_2), the same product with valued operands — out of scope here).
+// Returns false (nothing returned) when the shapes make the chain unattractive: the caller
+// then runs the table route.
+bool chain_dense(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B, const tcudb_table* C, bool forced,
+                 tcudb_result* out, tcudb_stats& S, cudaStream_t s) {
+  int64_t* L = &ctx->launches;
+  const int64_t nA = A->n_rows, nB = B->n_rows, nC = C->n_rows;
+  if (nA == 0 || nB == 0 || nC == 0) return false;
+  Arena ar(s);
+  ColDesc ak{A->key.data, A->key.type, nA}, ag{A->group.data, A->group.type, nA};
+  ColDesc bk{B->key.data, B->key.type, nB}, bg{B->group.data, B->group.type, nB};
+  ColDesc ck{C->key.data, C->key.type, nC}, ch{C->group.data, C->group.type, nC};
+  ColDesc none{nullptr, 0, 0};
+  ColStats* dst = ar.get<ColStats>(12);
+  ColDesc c1[6] = {ak, bk, ag, ch, none, none}, c2[6] = {bg, ck, none, none, none, none};
+  CK(launch_col_stats(c1, dst, s, L));
+  CK(launch_col_stats(c2, dst + 6, s, L));
+  CK(cudaMemcpyAsync(ctx->pinned, dst, sizeof(ColStats) * 12, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ColStats hs[12];
+  std::memcpy(hs, ctx->pinned, sizeof(hs));
+  Dict D1, D2, DG, DH;
+  dict_build(ar, D1, ak, &bk, std::min(hs[0].mn, hs[1].mn), std::max(hs[0].mx, hs[1].mx), true, nullptr, L);
+  dict_build(ar, D2, bg, &ck, std::min(hs[6].mn, hs[7].mn), std::max(hs[6].mx, hs[7].mx), false, nullptr, L);
+  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L);
+  dict_build(ar, DH, ch, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L);
+  {
+    int64_t* hp = static_cast<int64_t*>(ctx->pinned);
+    int* hov = reinterpret_cast<int*>(hp + 4);
+    hov[0] = 0;
+    CK(cudaMemcpyAsync(hp + 0, D1.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 1, D2.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 2, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + 3, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
+    for (Dict* d : {&D1, &D2, &DG, &DH})
+      if (d->ovf) CK(cudaMemcpyAsync(hov, d->ovf, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hov[0]) return false;  // a hash dictionary outgrew its estimate: the table route
+    D1.count = hp[0]; D2.count = hp[1]; DG.count = hp[2]; DH.count = hp[3];
+  }
+  const int64_t K1 = D1.count, K2 = D2.count, G = DG.count, H = DH.count;
+  if (K1 == 0 || K2 == 0) return false;
+  const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), K1p = round_up(K1, 128), K2p = round_up(K2, 256);
+  const double ops = 2.0 * Gp * K2p * K1p + 2.0 * Gp * Hp * K2p;
+  const double bytes = (double)Gp * K2p * 8 * 2 + (double)(Gp + K2p) * K1p * 8 + (double)(Hp + Gp) * K2p * 8 +
+                       (double)Gp * Hp * 8;
+  if (!forced && (ops > 5e12 || bytes > 0.25 * (double)ctx->mem_free0)) return false;
+  if (bytes > 0.6 * (double)ctx->mem_free0) return false;
+  dict_finish_group(ar, DG, L);
+  dict_finish_group(ar, DH, L);
+  // per-tuple codes: A (k1, g), B (k1, k2), C (k2, h)
+  int32_t *kA = ar.get<int32_t>(nA), *gA = ar.get<int32_t>(nA);
+  int32_t *k1B = ar.get<int32_t>(nB), *k2B = ar.get<int32_t>(nB);
+  int32_t *kC = ar.get<int32_t>(nC), *hC = ar.get<int32_t>(nC);
+  int32_t* dummy = ar.zeros<int32_t>(std::max<int64_t>(std::max<int64_t>(D1.span, D2.span), 1));
+  CK(launch_probe(ak, ag, none, D1.view(1), DG.view(1), kA, gA, dummy, nullptr, (int64_t)D1.span, s, L));
+  CK(launch_probe(bk, bg, none, D1.view(2), D2.view(1), k1B, k2B, dummy, nullptr, (int64_t)D1.span, s, L));
+  CK(launch_probe(ck, ch, none, D2.view(2), DH.view(1), kC, hC, dummy, nullptr, (int64_t)D2.span, s, L));
+  // operands: counts in int64 scratch -> digit planes (any multiplicity is exact)
+  FillStats* fs = ar.zeros<FillStats>(4);
+  long long* sA = ar.zeros<long long>(Gp * K1p);
+  long long* sB = ar.zeros<long long>(K2p * K1p);
+  long long* sC = ar.zeros<long long>(Hp * K2p);
+  CK(launch_fill_i64(kA, gA, none, nA, sA, K1p, s, L));
+  CK(launch_fill_i64(k1B, k2B, none, nB, sB, K1p, s, L));
+  CK(launch_fill_i64(kC, hC, none, nC, sC, K2p, s, L));
+  const Planes PA = make_planes(ctx, ar, sA, Gp * K1p, fs + 0, L);
+  const Planes PB = make_planes(ctx, ar, sB, K2p * K1p, fs + 1, L);
+  const Planes PC = make_planes(ctx, ar, sC, Hp * K2p, fs + 2, L);
+  // T = mat(A) × mat(B)^T : G x K2 path counts through B (int64, K2-major rows)
+  long long* T = ar.get<long long>(Gp * K2p);
+  double done_ops = gemm_planes(ar, PA, PB, Gp, K2p, K1p, T, K2p, nullptr, 0, L);
+  // T re-packed as digit planes: the left operand of the second product (no table in between)
+  const Planes PT = make_planes(ctx, ar, T, Gp * K2p, fs + 3, L);
+  CompactArgs ca{};
+  ca.G = G; ca.H = H; ca.nseg = Hp / 256; ca.seg_w = 256;
+  int32_t* seg_cnt = ar.get<int32_t>(Gp * ca.nseg);
+  long long* R = ar.get<long long>(Gp * Hp);
+  done_ops += gemm_planes(ar, PT, PC, Gp, Hp, K2p, R, Hp, seg_cnt, ca.nseg, L);
+  // existence = path count > 0 (COUNT)
+  ca.E = R; ca.e_kind = 1; ca.lde = Hp; ca.V = R; ca.v_kind = 1; ca.ldv = Hp;
+  ca.dict_g = DG.dict; ca.dict_h = DH.dict;
+  ca.g_out_type = A->group.type == TCUDB_I64 ? 1 : 0;
+  ca.h_out_type = C->group.type == TCUDB_I64 ? 1 : 0;
+  void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
+  int64_t* d_nnz = ar.get<int64_t>(1);
+  CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
+  const int64_t nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+  const size_t gb = ca.g_out_type ? 8 : 4, hb = ca.h_out_type ? 8 : 4;
+  const size_t oh = ((size_t)nnz * gb + 255) / 256 * 256;
+  const size_t oa = oh + ((size_t)nnz * hb + 255) / 256 * 256;
+  char* base = static_cast<char*>(result_alloc(ctx, oa + (size_t)nnz * 8, s));
+  ca.out_g = base; ca.out_h = base + oh; ca.out_agg = base + oa;
+  try {
+    CK(launch_compact_write(ca, ctmp, s, L));
+    CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    result_release(ctx, base);
+    throw;
+  }
+  out->n = nnz; out->g = ca.out_g; out->h = ca.out_h; out->agg = ca.out_agg; out->base = base; out->on_host = 0;
+  out->g_type = A->group.type; out->h_type = C->group.type; out->agg_type = TCUDB_I64;
+  S.path = 0; S.G = G; S.H = H; S.K = K2; S.n_result = nnz; S.gemm_ops = done_ops;
+  S.planes_a = PT.P; S.planes_b = PC.P;
+  return true;
+}
+
 tcudb_status check_table(const tcudb_table* t, bool need_value_ok) {
   if (!t || t->n_rows < 0) return TCUDB_E_INVALID;
   if (t->n_rows > 0 && !t->key.data) return TCUDB_E_INVALID;
@@ -1977,6 +2179,22 @@ tcudb_status tcudb_chain_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tc
       return set_err(ctx, TCUDB_E_UNSUPPORTED, "chain: float values need an fp64 intermediate");
   if ((A->n_rows > 0 && !A->group.data) || (B->n_rows > 0 && !B->group.data) || (C->n_rows > 0 && !C->group.data))
     return set_err(ctx, TCUDB_E_INVALID, "chain: A.g, B.ID_2 and C.h are required");
+  // the chain exception: COUNT with B projected out -> mat(A)·mat(B)^T·mat(C)^T
+  // on the tensor cores, the intermediate kept as a matrix (no table conversion) — chosen
+  // when both products are small enough (or FORCE_DENSE); FORCE_SPARSE: the table route
+  if (q->agg == TCUDB_COUNT && !(q->flags & TCUDB_FORCE_SPARSE)) {
+    CtxScope scope(ctx->device, ctx->pool);
+    tcudb_stats local{};
+    tcudb_stats& S = stats ? *stats : local;
+    std::memset(&S, 0, sizeof(S));
+    try {
+      if (chain_dense(ctx, A, B, C, (q->flags & TCUDB_FORCE_DENSE) != 0, out, S, static_cast<cudaStream_t>(stream)))
+        return TCUDB_OK;
+    } catch (const Fail& f) {
+      std::memset(out, 0, sizeof(*out));
+      return fail_err(ctx, f);
+    }
+  }
   // step 1: T = A ⋈ B grouped by (A.g, B.ID_2), COUNT or SUM(A.v · B.w)
   tcudb_query q1 = *q;
   tcudb_result T{};

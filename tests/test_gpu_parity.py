@@ -617,39 +617,44 @@ def test_hash_partitioned_count(engine, torch_mod, oracle_mod, monkeypatch, case
 
 
 # ---------------------------------------------------------------- §8(f) f3: chain joins
-def _chain_run(engine, torch_mod, A, B, C, agg):
-    out = engine.chain_join_agg(to_dev(A, torch_mod), to_dev(B, torch_mod), to_dev(C, torch_mod), agg)
+def _chain_run(engine, torch_mod, A, B, C, agg, flags=0):
+    out = engine.chain_join_agg(to_dev(A, torch_mod), to_dev(B, torch_mod), to_dev(C, torch_mod), agg, flags=flags)
     return res_np(out)
 
 
-def test_chain_join_tiny_vs_triple_loop(engine, torch_mod, oracle_mod):
+# flags: default (COUNT takes the chain exception when small), FORCE_DENSE (the matrix
+# chain mat(A)·mat(B)^T·mat(C)^T), FORCE_SPARSE (the table route through nonzero())
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_chain_join_tiny_vs_triple_loop(engine, torch_mod, oracle_mod, flags):
     rng = np.random.default_rng(32)
     for _ in range(40):
         A, B = datagen.random_tiny(rng, n_max=40, k_max=8, g_max=4, vkind="int", vmin=-4, vmax=4, allow_empty=False)
         C, _ = datagen.random_tiny(rng, n_max=40, k_max=8, g_max=4, vkind="int", vmin=-4, vmax=4, allow_empty=False)
         B = dict(B, g=rng.choice(np.concatenate([C["k"], [999]]), len(B["k"])))
         for agg in ("count", "sum"):
-            got = _chain_run(engine, torch_mod, A, B, C, agg)
+            got = _chain_run(engine, torch_mod, A, B, C, agg, flags)
             ref = oracle_mod.chain_nested_loop(A, B, C, agg)
             assert np.array_equal(got["g"].astype(np.int64), ref["g"])
             assert np.array_equal(got["h"].astype(np.int64), ref["h"])
             assert np.array_equal(got["agg"], ref["sum"])
 
 
-def test_chain_three_hop_graphs(engine, torch_mod, oracle_mod):
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_chain_three_hop_graphs(engine, torch_mod, oracle_mod, flags):
     """3-hop path counts (A -> B -> C over the edge table): K_9 closed form and the c3
-    graph at 1/16 scale vs the oracle's join-order evaluation."""
+    graph at 1/16 scale vs the oracle's join-order evaluation, on the chain exception
+    (matrix chain, default / FORCE_DENSE) and the table route (FORCE_SPARSE)."""
     n = 9
     src, dst = (np.array(x) for x in zip(*[(i, j) for i in range(n) for j in range(n) if i != j]))
     E1, E2 = datagen.Table(dst, src), datagen.Table(src, dst)
-    r = _chain_run(engine, torch_mod, E1, E2, E2, "count")
+    r = _chain_run(engine, torch_mod, E1, E2, E2, "count", flags)
     assert len(r["g"]) == n * n
     for g, h, c in zip(r["g"], r["h"], r["agg"]):
         assert c == ((n - 1) * (n - 2) if g == h else n * n - 3 * n + 3)
     A, B, _ = datagen.make_config("c3", 1 / 16)
     C = {"k": B["k"], "g": B["g"], "v": None}
     B2 = {"k": B["k"], "g": B["g"], "v": None}
-    got = _chain_run(engine, torch_mod, A, B2, C, "count")
+    got = _chain_run(engine, torch_mod, A, B2, C, "count", flags)
     ref = oracle_mod.chain_join_agg(A, B2, C, "count")
     assert np.array_equal(got["g"].astype(np.int64), ref["g"]) and np.array_equal(got["h"].astype(np.int64), ref["h"])
     assert np.array_equal(got["agg"], ref["sum"])
