@@ -483,6 +483,7 @@ def main():
         "roofline": head["roofline"], "query_roofline": head["query_roofline"],
         "cpu_baseline": head["cpu_baseline"], "e2e": head["e2e"], "clocks": clocks,
         "gpu_launches": head["gpu_launches"],
+        "selector_calibration": eng.calibration,
         "configs": {c: {k: v for k, v in r.items()} for c, r in others.items()},
         "context": PAPER_CONTEXT,
     }

@@ -95,6 +95,9 @@ struct PassIO {
   int32_t* counts;  // [total_chunks * R] in (segment, digit, chunk) order
   const int64_t* offs;  // exclusive scan of counts
   unsigned long long* k_out; int32_t* g_out; int64_t* seg_out;
+  // atomic-reservation passes: per (segment, digit) output cursors (start offsets known from
+  // the one-pass 2^pbits histogram); NULL: the per-chunk offsets of the hist + scan passes
+  unsigned long long* cursor;
 };
 
 TCUDB_DEV long long load_value(const PassIO& io, int64_t i) {
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
   const int64_t base = io.chunk_start[s] * R;
   for (int d = threadIdx.x; d < R; d += PT) {
     cnt[d] = 0;
-    gpos[d] = io.offs[base + (int64_t)d * nch + j];
+    if (!io.cursor) gpos[d] = io.offs[base + (int64_t)d * nch + j];
   }
   __syncthreads();
   const int64_t lo = io.seg_off[s] + j * CH, hi = min(io.seg_off[s + 1], lo + CH);
@@ -176,6 +179,10 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
     }
   }
   __syncthreads();
+  // atomic reservation of this chunk's run per digit (order inside a partition is free)
+  if (io.cursor)
+    for (int dd = threadIdx.x; dd < R; dd += PT)
+      gpos[dd] = cnt[dd] ? (int64_t)atomicAdd(io.cursor + (int64_t)s * R + dd, (unsigned long long)cnt[dd]) : 0;
   if (threadIdx.x < 32) {  // exclusive scan of <= 128 digit counts, 4 per lane
     int v[4], sum = 0;
 #pragma unroll
@@ -217,6 +224,35 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
     io.g_out[o] = sg[p];
     if (VAL) io.v_out[o] = sv[p];
   }
+}
+
+// One pass over a side's raw keys: the histogram of the full partition index (the top
+// pbits of the key hash, both radix digits at once) — every segment and partition start is
+// known before the first scatter, which then reserves its runs with one atomic per digit
+// (no per-pass histogram / count-scan passes). Persistent CTAs, shared-memory bins.
+constexpr int HT = 1024;
+__global__ void __launch_bounds__(HT) k_part_hist_all(const void* __restrict__ raw, int raw_type, long long kmin,
+                                                      int64_t n, int pbits, unsigned* __restrict__ hist) {
+  extern __shared__ unsigned bins[];
+  const int P = 1 << pbits;
+  for (int i = threadIdx.x; i < P; i += HT) bins[i] = 0u;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * HT;
+  constexpr int U = 4;
+  for (int64_t i0 = (int64_t)blockIdx.x * HT + threadIdx.x; i0 < n; i0 += U * stride) {
+    unsigned long long k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      k[u] = i < n ? (unsigned long long)ld_int(raw, raw_type, i) - (unsigned long long)kmin : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) atomicAdd(&bins[(int)(mix64(k[u]) >> (64 - pbits))], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += HT)
+    if (bins[i]) atomicAdd(hist + i, bins[i]);
 }
 
 // new segment offsets: seg_out[s * R + d] = start of digit d of segment s (empty segments
@@ -538,6 +574,48 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
   const int64_t so = (int64_t)nseg * R + 1;
   k_seg_out<<<(unsigned)std::min<int64_t>((so + 255) / 256, 1024), 256, 0, s>>>(io);
   if (launches) *launches += 4;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_hist_all(const ColDesc& raw, long long kmin, int pbits, unsigned* hist, cudaStream_t s,
+                                 int64_t* launches) {
+  if (raw.n <= 0) return cudaSuccess;
+  const size_t smem = sizeof(unsigned) << pbits;
+  cudaError_t e = set_func_attr(k_part_hist_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = std::min<int64_t>(2 * kNumSMs, (raw.n + HT * 16 - 1) / (HT * 16));
+  k_part_hist_all<<<(unsigned)std::max<int64_t>(blocks, 1), HT, smem, s>>>(raw.data, raw.type, kmin, raw.n, pbits,
+                                                                           hist);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+size_t hashpart_atomic_temp_bytes(int nseg) { return ((size_t)(nseg + 1) * 8 + 255) / 256 * 256; }
+
+cudaError_t launch_part_pass_atomic(const ColDesc* raw, long long kmin, const int32_t* g_raw,
+                                    const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off,
+                                    int nseg, int64_t n, int shift, int bits, unsigned long long* cursor,
+                                    unsigned long long* k_out, int32_t* g_out, void* temp, cudaStream_t s,
+                                    int64_t* launches, const ColDesc* v_raw, const long long* v_in,
+                                    long long* v_out) {
+  if (bits < 1 || bits > 7 || n <= 0) return cudaErrorInvalidValue;
+  const int64_t chunks = max_chunks(n, nseg);
+  int64_t* chunk_start = static_cast<int64_t*>(temp);
+  PassIO io{};
+  io.raw = raw ? raw->data : nullptr; io.raw_type = raw ? raw->type : 0; io.kmin = kmin; io.g_raw = g_raw;
+  io.k_in = k_in; io.g_in = g_in; io.seg_off = seg_off; io.nseg = nseg; io.shift = shift; io.bits = bits;
+  io.chunk_start = chunk_start; io.cursor = cursor;
+  io.k_out = k_out; io.g_out = g_out;
+  io.v_raw = v_raw ? v_raw->data : nullptr; io.v_type = v_raw ? v_raw->type : 0;
+  io.v_in = v_in; io.v_out = v_out;
+  k_chunk_starts<<<1, kCsThreads, 0, s>>>(seg_off, nseg, chunk_start);
+  cudaError_t e = set_func_attr(k_part_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 21);
+  if (e != cudaSuccess) return e;
+  e = set_func_attr(k_part_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * 13);
+  if (e != cudaSuccess) return e;
+  if (v_out) k_part_scatter<true><<<(unsigned)chunks, PT, CH * 21, s>>>(io);
+  else k_part_scatter<false><<<(unsigned)chunks, PT, CH * 13, s>>>(io);
+  if (launches) *launches += 2;
   return cudaGetLastError();
 }
 

@@ -251,6 +251,18 @@ cudaError_t launch_part_pass(const ColDesc* raw, long long kmin, const int32_t* 
                              int64_t* seg_out, void* temp, cudaStream_t s, int64_t* launches,
                              const ColDesc* v_raw = nullptr, const long long* v_in = nullptr,
                              long long* v_out = nullptr);  // value payload (integer SUM), optional
+// histogram of the top pbits (<= 14) of the key hash over one side's raw keys (hist zeroed)
+cudaError_t launch_part_hist_all(const ColDesc& raw, long long kmin, int pbits, unsigned* hist, cudaStream_t s,
+                                 int64_t* launches);
+// one radix pass with atomic run reservation: cursor[s * 2^bits + d] = the next free slot of
+// digit d of segment s (initialized to its start by the caller)
+size_t hashpart_atomic_temp_bytes(int nseg);
+cudaError_t launch_part_pass_atomic(const ColDesc* raw, long long kmin, const int32_t* g_raw,
+                                    const unsigned long long* k_in, const int32_t* g_in, const int64_t* seg_off,
+                                    int nseg, int64_t n, int shift, int bits, unsigned long long* cursor,
+                                    unsigned long long* k_out, int32_t* g_out, void* temp, cudaStream_t s,
+                                    int64_t* launches, const ColDesc* v_raw = nullptr, const long long* v_in = nullptr,
+                                    long long* v_out = nullptr);
 size_t part_expand_smem(int cap, bool sum);
 // per partition: J_p = sum over its keys of cntA*cntB, D_p = #keys on both sides; out has
 // 4 + 4 P entries: totals out[0] (J), out[1] (K = sum D_p), out[2] (A tuples with a matched

@@ -396,6 +396,8 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
     std::memcpy(ctx->pinned, h0, sizeof(h0));
     CK(cudaMemcpyAsync(seg0, ctx->pinned, sizeof(h0), cudaMemcpyHostToDevice, s));
   }
+  const char* hs_env = getenv("TCUDB_HASHPART_HISTSCAN");  // 1: the per-pass hist + scan partitioning
+  const bool atomic_parts = !(hs_env && hs_env[0] == '1');
   for (int x = 0; x < 2; ++x) {
     const int64_t n = ns[x];
     sd[x].k[0] = ar.get<unsigned long long>(n); sd[x].k[1] = ar.get<unsigned long long>(n);
@@ -404,6 +406,33 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
     sd[x].v[1] = sum ? ar.get<long long>(n) : nullptr;
     sd[x].seg1 = ar.get<int64_t>(((int64_t)1 << b1) + 1);
     sd[x].seg2 = ar.get<int64_t>((int64_t)P + 1);
+    if (atomic_parts) {
+      // one histogram pass over the full partition index gives every segment / partition
+      // start; both radix passes then reserve their runs with atomics (no per-pass
+      // histogram and count scans; the order inside a partition is free)
+      unsigned* hist = ar.zeros<unsigned>(P);
+      CK(launch_part_hist_all(*keys[x], kmin, pbits, hist, s, L));
+      CK(exclusive_scan_i32(reinterpret_cast<const int32_t*>(hist), sd[x].seg2, P, sd[x].seg2 + P,
+                            ar.get<char>((int64_t)scan_temp_bytes(P)), s, L));
+      CK(cudaMemcpy2DAsync(sd[x].seg1, 8, sd[x].seg2, (size_t)8 << b2, 8, ((size_t)1 << b1) + 1,
+                           cudaMemcpyDeviceToDevice, s));
+      unsigned long long* cur2 = ar.get<unsigned long long>(P);
+      CK(cudaMemcpyAsync(cur2, sd[x].seg2, (size_t)P * 8, cudaMemcpyDeviceToDevice, s));
+      unsigned long long* cur1 = cur2;
+      if (b2) {
+        cur1 = ar.get<unsigned long long>((int64_t)1 << b1);
+        CK(cudaMemcpyAsync(cur1, sd[x].seg1, ((size_t)1 << b1) * 8, cudaMemcpyDeviceToDevice, s));
+      }
+      CK(launch_part_pass_atomic(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, cur1,
+                                 sd[x].k[0], sd[x].g[0], ar.get<char>((int64_t)hashpart_atomic_temp_bytes(1)), s, L,
+                                 sum ? vals[x] : nullptr, nullptr, sd[x].v[0]));
+      if (b2)
+        CK(launch_part_pass_atomic(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits,
+                                   b2, cur2, sd[x].k[1], sd[x].g[1],
+                                   ar.get<char>((int64_t)hashpart_atomic_temp_bytes(1 << b1)), s, L, nullptr,
+                                   sd[x].v[0], sd[x].v[1]));
+      continue;
+    }
     void* t1 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1, b1));
     CK(launch_part_pass(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
                         sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L, sum ? vals[x] : nullptr, nullptr,
@@ -813,9 +842,16 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     bs_cache[kind] = m;
     return m;
   };
-  // the analysis costs ~0.2 ms (a key sort, two marking passes, a host sync): only when the
-  // dense product would take >= 1 ms at the device's measured rate
-  if (!bs_off && (bs_force || dense_ops / gemm_rate >= 1e-3) && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
+  // the analysis costs ~0.1-0.2 ms (a key sort, two marking passes, a host sync): only when
+  // the dense product would take >= 1.5 ms at the device's measured rate, and when the dense
+  // path could win at all (its byte traffic alone below the sparse estimate)
+  bool bs_worth = bs_force;
+  if (!bs_force && dense_ops / gemm_rate >= 1.5e-3) {
+    const double bytes = (double)(Gp + Hp) * Kp * (is_float ? 2.0 : 1.0) + (double)Gp * Hp * (is_sum ? 8.0 : 2.0);
+    const double t_sp = (double)J / ctx->cal.R_sp + ctx->cal.T_sp0;
+    bs_worth = 3.0 * bytes / ctx->cal.BW < t_sp;
+  }
+  if (!bs_off && bs_worth && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
     CK(launch_bs_reorder(kA, gA, nA, kB, nB, cntA, cntB, K, G, ar.get<char>((int64_t)bs_reorder_temp_bytes(K)), s,
                          L));
     const int64_t kgroups = (Kp * 4 + 63) / 64;  // 64-key groups over the widest K' (the split's 4 Kp)

@@ -1,12 +1,15 @@
 #!/bin/bash
 # full ncu captures of selected kernels: args are "config:regex:count" triples
+# (TCUDB_CALIBRATE=0: the create-time calibration would otherwise be the first GEMM / sparse
+#  launches the regex matches)
 mkdir -p gpurun_out
+export TCUDB_CALIBRATE=0
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 for spec in "$@"; do
   IFS=: read c re n <<< "$spec"
   tag=$(echo "$re" | tr -c 'a-zA-Z0-9_\n' '_')
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$re" -c ${n:-1} \
-     -o gpurun_out/prof_${c}_${tag} -f python bench.py --config $c --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 \
+     -o gpurun_out/prof_${c}_${tag} -f python bench.py --config $c --also "" --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 \
      > gpurun_out/ncu_${c}_${tag}.log 2>&1
   tail -2 gpurun_out/ncu_${c}_${tag}.log
 done

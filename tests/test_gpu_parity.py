@@ -943,3 +943,19 @@ def test_bf16_fill_modes_large(engine, torch_mod, oracle_mod, monkeypatch, mode,
     out, st = run(engine, torch_mod, A, B, "sum", flags=1)
     assert st["path"] == 0
     compare(out, oracle_mod.join_agg(A, B, "sum"), "sum", float_vals=True)
+
+
+@pytest.mark.parametrize("mode", ["atomic", "histscan"])
+@pytest.mark.parametrize("name", ["c5", "c5s"])
+def test_hash_partition_pass_modes(engine, torch_mod, oracle_mod, monkeypatch, mode, name):
+    """Both partitioning schemes of the hash-partitioned path (one histogram + atomic run
+    reservation, default; per-pass histogram + scan) against the oracle at 1/16 scale
+    (1 M tuples per side: two radix passes, 1,024 partitions, the sampled selector)."""
+    if mode == "histscan":
+        monkeypatch.setenv("TCUDB_HASHPART_HISTSCAN", "1")
+    monkeypatch.setenv("TCUDB_FORCE_HASHPART", "1")
+    A, B, agg = datagen.make_config(name, 1 / 16)
+    ref = oracle_mod.join_agg(A, B, agg)
+    out, st = run(engine, torch_mod, A, B, agg, 0)
+    assert st["spa_mode"] == 4
+    compare(out, ref, agg)
