@@ -265,7 +265,9 @@ def kernel_roofline(st, gemm_ms, kernel_ms, config, peaks):
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "peak_source": f"{peaks['source']} copy bandwidth", "bytes_per_launch": st["kernel_bytes"],
                 "avg_launch_ms": k_ms, "spa_mode": {2: "count pass + band writer", 3: "one pass (look-back)",
-                                                    4: "hash-partitioned"}.get(st["spa_mode"], st["spa_mode"]),
+                                                    4: "hash-partitioned",
+                                                    5: "hub-band count pass + one pass (look-back)"}.get(
+                    st["spa_mode"], st["spa_mode"]),
                 "traffic": sparse_traffic_from_profiles(config, st["spa_mode"])}
     # sparse or reduction path without the band kernel: stage time, 16 B per joined pair
     b = st["join_pairs"] * 16.0

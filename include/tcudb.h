@@ -117,7 +117,8 @@ typedef struct {
   double gemm_ops;      /* 2 * Gp * Hp * Kp summed over GEMM launches (dense path) */
   float ms_stats, ms_encode, ms_fill, ms_gemm, ms_sparse, ms_compact, ms_total;
   int32_t spa_mode;     /* sparse path: 0 C matrix (or dense path), 1 count + write passes,
-                           2 count pass + persistent band writer, 3 one persistent pass */
+                           2 count pass + persistent band writer, 3 one persistent pass,
+                           4 hash-partitioned, 5 hub-band count pass + one persistent pass */
   int64_t spa_max_band; /* sparse path: most updates of one band of result rows */
   int32_t fused_compact; /* dense path: 1 if the compaction ran inside the GEMM kernel */
   float ms_kernel;       /* sparse path: CUDA-event time of the band kernel (k_spa_fused) */
@@ -125,6 +126,7 @@ typedef struct {
   float ms_comm;         /* collective calls: host wall time of the exchanges (NCCL + routing) */
   double block_active;   /* dense path, block-sparse GEMM (§8(f) f4): share of (tile, K-block)
                             products with tuples on both sides (the rest skipped); 0: dense GEMM */
+  int64_t spa_hubs;      /* sparse path, hybrid one-pass schedule: bands counted ahead (hubs) */
 } tcudb_stats;
 
 typedef struct tcudb_ctx tcudb_ctx;

@@ -69,7 +69,8 @@ class Stats(ctypes.Structure):
                 ("ms_gemm", ctypes.c_float), ("ms_sparse", ctypes.c_float), ("ms_compact", ctypes.c_float),
                 ("ms_total", ctypes.c_float), ("spa_mode", ctypes.c_int32), ("spa_max_band", ctypes.c_int64),
                 ("fused_compact", ctypes.c_int32), ("ms_kernel", ctypes.c_float), ("kernel_bytes", ctypes.c_double),
-                ("ms_comm", ctypes.c_float), ("block_active", ctypes.c_double)]
+                ("ms_comm", ctypes.c_float), ("block_active", ctypes.c_double),
+                ("spa_hubs", ctypes.c_int64)]
 
     def to_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

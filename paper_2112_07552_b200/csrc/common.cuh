@@ -4,7 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <mutex>
-#include <set>
+#include <map>
 #include <tuple>
 
 #define TCUDB_DEV __device__ __forceinline__
@@ -238,19 +238,21 @@ TCUDB_DEV long long warp_min_ll(long long v) {
   for (int o = 16; o > 0; o >>= 1) v = min(v, (long long)__shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-// cudaFuncSetAttribute once per (kernel, device, attribute, value), thread-safe. The
-// attribute is a per-device property: a process-wide "already set" flag would skip the
+// cudaFuncSetAttribute per (kernel, device, attribute), thread-safe, keeping the largest value
+// requested so far (the attributes used here are upper bounds: MaxDynamicSharedMemorySize).
+// The attribute is a per-device property: a process-wide "already set" flag would skip the
 // second device (and race between threads); one inline function => one table per library.
 inline cudaError_t set_func_attr_void(const void* f, cudaFuncAttribute attr, int value) {
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int, int>> done;
+  static std::map<std::tuple<const void*, int, int>, int> cur;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
-  const auto key = std::make_tuple(f, dev, (int)attr, value);
+  const auto key = std::make_tuple(f, dev, (int)attr);
   std::lock_guard<std::mutex> g(mu);
-  if (done.count(key)) return cudaSuccess;
+  auto it = cur.find(key);
+  if (it != cur.end() && it->second >= value) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(f, attr, value);
-  if (e == cudaSuccess) done.insert(key);
+  if (e == cudaSuccess) cur[key] = value;
   return e;
 }
 template <typename K>

@@ -214,7 +214,17 @@ struct SpaArgs {
   unsigned long long* lb_state;  // nbands, zeroed: look-back (flag | tuple count) per band
   int64_t* total;              // out: number of result tuples
   int* ovf;                    // out (zeroed): a u16 COUNT cell reached 65,535
+  // count pass over a subset of bands (the hub bands of the hybrid schedule): band_list[i]
+  // for i < n_list, one band per CTA; NULL: every band
+  const int32_t* band_list;
+  int64_t n_list;
 };
+// Hybrid one-pass schedule: the bands heavier than thr updates (hubs) -> list (count in
+// *n_out); after their count pass, their tuple counts are published in lb_state (look-back
+// aggregates) so that no later band's look-back waits for a hub's expansion.
+cudaError_t launch_hub_list(const SpaArgs& a, unsigned long long thr, int32_t* list, unsigned long long* n_out,
+                            cudaStream_t s, int64_t* launches);
+cudaError_t launch_hub_publish(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 // false when one result row does not fit in shared memory (the caller keeps the C path)
 bool spa_plan(SpaArgs& a);
 bool spa_fused_plan(SpaArgs& a);

@@ -143,9 +143,9 @@ __device__ __forceinline__ void spa_expand(const SpaArgs& a, int64_t t_begin, in
 constexpr int NTC = 512;  // count pass: 2 CTAs per SM
 __global__ void __launch_bounds__(NTC, 2) k_spa_count(const SpaArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  // count_bands consecutive bands per CTA (their tuples are contiguous)
-  const int64_t b0 = (int64_t)blockIdx.x * a.count_bands;
-  const int64_t b1 = min(a.nbands, b0 + a.count_bands);
+  // count_bands consecutive bands per CTA (their tuples are contiguous), or one listed band
+  const int64_t b0 = a.band_list ? (int64_t)a.band_list[blockIdx.x] : (int64_t)blockIdx.x * a.count_bands;
+  const int64_t b1 = a.band_list ? b0 + 1 : min(a.nbands, b0 + a.count_bands);
   const int64_t g0 = b0 * a.rows;
   const int64_t g1 = min(a.G, b1 * a.rows);
   const int nr = (int)(g1 - g0);
@@ -473,6 +473,40 @@ __global__ void k_band_weight_max(const int64_t* __restrict__ goff, const int64_
   if (lane_id() == 0 && m) atomicMax(out, m);
 }
 
+__global__ void k_hub_list(const int64_t* __restrict__ goff, const int64_t* __restrict__ act_off, int64_t nbands,
+                           unsigned long long thr, int32_t* __restrict__ list, unsigned long long* __restrict__ n) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbands; b += (int64_t)gridDim.x * blockDim.x)
+    if ((unsigned long long)(act_off[goff[b + 1]] - act_off[goff[b]]) > thr)
+      list[atomicAdd(n, 1ull)] = (int32_t)b;
+}
+
+__global__ void k_hub_publish(const int32_t* __restrict__ list, int64_t n_list, const int32_t* __restrict__ row_nnz,
+                              int rows, int64_t G, unsigned long long* __restrict__ lb_state) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_list; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = list[i], g0 = b * rows, g1 = min(G, g0 + rows);
+    unsigned long long c = 0;
+    for (int64_t g = g0; g < g1; ++g) c += (unsigned long long)row_nnz[g];
+    lb_state[b] = kLbAgg | c;  // the band's aggregate, before any CTA takes a ticket
+  }
+}
+
+cudaError_t launch_hub_list(const SpaArgs& a, unsigned long long thr, int32_t* list, unsigned long long* n_out,
+                            cudaStream_t s, int64_t* launches) {
+  if (a.nbands <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(2 * kNumSMs, (a.nbands + 255) / 256);
+  k_hub_list<<<(unsigned)blocks, 256, 0, s>>>(a.goff, a.act_off, a.nbands, thr, list, n_out);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hub_publish(const SpaArgs& a, cudaStream_t s, int64_t* launches) {
+  if (a.n_list <= 0) return cudaSuccess;
+  k_hub_publish<<<(unsigned)std::min<int64_t>(kNumSMs, (a.n_list + 255) / 256), 256, 0, s>>>(
+      a.band_list, a.n_list, a.row_nnz, a.rows, a.G, a.lb_state);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_band_weight_max(const SpaArgs& a, unsigned long long* out, cudaStream_t s, int64_t* launches) {
   if (a.nbands <= 0) return cudaSuccess;
   const int64_t blocks = std::min<int64_t>(2 * kNumSMs, (a.nbands + 255) / 256);
@@ -561,7 +595,9 @@ cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches
   const size_t sm = count_smem(a);
   const cudaError_t e = set_func_attr(k_spa_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   if (e != cudaSuccess) return e;
-  k_spa_count<<<(unsigned)((a.nbands + a.count_bands - 1) / a.count_bands), NTC, sm, s>>>(a);
+  const int64_t grid = a.band_list ? a.n_list : (a.nbands + a.count_bands - 1) / a.count_bands;
+  if (grid <= 0) return cudaSuccess;
+  k_spa_count<<<(unsigned)grid, NTC, sm, s>>>(a);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

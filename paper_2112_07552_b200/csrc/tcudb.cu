@@ -939,6 +939,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   bool spa_fw = false;         // ... on the persistent band kernel (spa.cu k_spa_fused)
   bool spa_one = false;        // ... in one pass (no count pass)
   bool spa_timed = false;      // evk[] bracket the band kernel
+  bool spa_hub = false;        // ... one pass after a count pass over the hub bands only
+  unsigned long long hub_thr = 0;
   bool dense_fc = false;       // dense path: compaction fused into the GEMM (f1)
   void* fc_out[3] = {nullptr, nullptr, nullptr};
   int64_t* d_fc_total = nullptr;
@@ -1390,6 +1392,18 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         spa_one = ub_bytes <= 0.3 * (double)ctx->mem_free0 && (is_sum || u16_safe) &&
                   ((double)max_w <= 4.0 * avg_w + 65536.0 || (force_one && force_one[0] == '1'));
         S.spa_max_band = (int64_t)max_w;
+        // hybrid (COUNT, u16 cells): a count pass over the hub bands only, their counts
+        // published up front, then the one-pass kernel for everything — no band's look-back
+        // waits for a hub's expansion, and the other bands are expanded once. A u16 cell
+        // reaching 65,535 (possible: a hub band has >= 65,535 updates) falls back to the
+        // two-pass schedule below.
+        const char* no_hub = getenv("TCUDB_SPA_NO_HUB");
+        if (!spa_one && !is_sum && sa.acc_kind == 4 && ub_bytes <= 0.3 * (double)ctx->mem_free0 &&
+            !(no_hub && no_hub[0] == '1')) {
+          spa_hub = true;
+          spa_one = true;
+          hub_thr = (unsigned long long)(4.0 * avg_w + 65536.0);
+        }
       }
       if (spa_one) {
         // expand + count + ordered write in one launch, into the upper-bound result buffer
@@ -1406,6 +1420,21 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         sa.total = ar.zeros<int64_t>(1);
         sa.ovf = ar.zeros<int>(1);
         sa.row_out = nullptr;
+        if (spa_hub) {
+          int32_t* list = ar.get<int32_t>(sa.nbands);
+          unsigned long long* d_n = ar.zeros<unsigned long long>(1);
+          CK(launch_hub_list(sa, hub_thr, list, d_n, s, L));
+          const int64_t n_hub = (int64_t)*to_pinned<unsigned long long>(ctx, d_n, s);
+          sa.row_nnz = ar.get<int32_t>(G);
+          sa.band_list = list;
+          sa.n_list = n_hub;
+          sa.count_bands = 1;
+          CK(launch_spa_count(sa, s, L));
+          CK(launch_hub_publish(sa, s, L));
+          sa.band_list = nullptr;
+          sa.n_list = 0;
+          S.spa_hubs = n_hub;
+        }
         if (st) cudaEventRecord(ctx->evk[0], s);
         CK(launch_spa_fused(sa, s, L));
         if (st) cudaEventRecord(ctx->evk[1], s);
@@ -1488,6 +1517,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     *hov = 0;
     CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
     if (sparse_u16.acc_kind == 4) CK(cudaMemcpyAsync(hov, sparse_u16.ovf, 4, cudaMemcpyDeviceToHost, s));
+    if (spa_hub) CK(cudaMemcpyAsync(hov, sa.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (fs4) CK(cudaMemcpyAsync(hfs, fs4, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
     if (fs8) CK(cudaMemcpyAsync(hfs, fs8, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1502,7 +1532,24 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       CK(cudaMemsetAsync(fs8 ? fs8 : fs4, 0, sizeof(FillStats) * 2, s));
       continue;
     }
-    if (*hov) {
+    if (*hov && spa_hub) {
+      // a u16 cell of the hybrid one-pass kernel passed 65,535: the two-pass schedule (count
+      // pass over every band, then the write pass, rerun in int32 cells on its own overflow)
+      result_release(ctx, ub_base);
+      ub_base = nullptr;
+      spa_one = false;
+      spa_hub = false;
+      int64_t* row_out = ar.get<int64_t>(G + 1);
+      spa_count_plan(sa);
+      CK(launch_spa_count(sa, s, L));
+      void* tmpg = ar.get<char>((int64_t)scan_temp_bytes(std::max<int64_t>(G, 1)));
+      CK(exclusive_scan_i32(sa.row_nnz, row_out, G, row_out + G, tmpg, s, L));
+      sa.row_out = row_out;
+      sa.ticket = ar.zeros<unsigned long long>(1);
+      sa.ovf = ar.zeros<int>(1);
+      d_nnz = row_out + G;
+      nnz = *to_pinned<int64_t>(ctx, d_nnz, s);
+    } else if (*hov) {
       // some (g, h) count passed 65535: redo the expand with 32/64-bit cells
       ExpandArgs ea = sparse_u16;
       ea.ovf = nullptr;
@@ -1560,7 +1607,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   tm.finish();
   out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->base = r.g; out->on_host = 0;
   S.n_result = nnz;
-  S.spa_mode = !spa ? 0 : spa_one ? 3 : spa_fw ? 2 : 1;
+  S.spa_mode = !spa ? 0 : spa_hub ? 5 : spa_one ? 3 : spa_fw ? 2 : 1;
   if (st && spa_timed) {
     // band kernel: algorithmic bytes = bucket entries read (4 B per joined pair) + the
     // active A tuples' (offset, bucket, row) read (20 B each) + result tuples written
