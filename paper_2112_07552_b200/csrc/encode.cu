@@ -35,7 +35,7 @@ __device__ __forceinline__ void col_stats_finish(ColStats* s, long long mn, long
   __shared__ long long smn[T / 32], smx[T / 32], sab[T / 32];
   __shared__ int sfl[T / 32];
   mn = warp_min_ll(mn); mx = warp_max_ll(mx); mabs = warp_min_ll(mabs);
-  flags = __any_sync(0xffffffffu, flags);
+  flags = (int)__reduce_or_sync(0xffffffffu, (unsigned)flags);  // every flag bit, not just "any"
   if (lane_id() == 0) { smn[warp_id()] = mn; smx[warp_id()] = mx; sab[warp_id()] = mabs; sfl[warp_id()] = flags; }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -45,7 +45,7 @@ __device__ __forceinline__ void col_stats_finish(ColStats* s, long long mn, long
     atomicMin(&s->mn, mn);
     atomicMax(&s->mx, mx);
     atomicMin(&s->min_abs, mabs);
-    if (flags) atomicOr(&s->flags, 1);
+    if (flags) atomicOr(&s->flags, flags);
   }
 }
 
@@ -118,8 +118,10 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     int nonfinite = 0;
     const float* p = static_cast<const float*>(c.data);
     const float4* p4 = static_cast<const float4*>(c.data);
+    int inexact = 0;  // some value is not bf16-representable (flags bit 1)
     auto take = [&](float x) {
       if (!isfinite(x)) nonfinite = 1;
+      inexact |= (__float_as_uint(x) & 0xFFFFu) != 0u;
       mn = fminf(mn, x); mx = fmaxf(mx, x); mabs = fminf(mabs, fabsf(x));
     };
     for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
@@ -135,7 +137,7 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     for (int64_t i = n4 * 4 + gtid; i < c.n; i += stride) take(__ldcs(p + i));
     // fp32 -> order-preserving int: flip for negatives
     auto ord = [](float f) { int b = __float_as_int(f); return b >= 0 ? (long long)b : (long long)(b ^ 0x7fffffff); };
-    col_stats_finish(s, ord(mn), ord(mx), ord(mabs), nonfinite);
+    col_stats_finish(s, ord(mn), ord(mx), ord(mabs), nonfinite | (inexact << 1));
     return;
   }
   if (c.type == 0) {  // int32: 32-bit compares, widened once at the end

@@ -16,7 +16,8 @@ struct ColDesc {
 };
 
 // Column statistics (a1 / D2). Integer columns: mn, mx, min_abs as int64.
-// Float columns: order-preserving int encodings of fp32 (see decode_ord), flags bit0 = non-finite seen.
+// Float columns: order-preserving int encodings of fp32 (see decode_ord), flags bit0 = non-finite seen,
+// bit1 = some value is not bf16-representable.
 struct ColStats {
   long long mn, mx, min_abs;
   int flags;

@@ -1062,7 +1062,9 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       ldop = 4 * Kp;
       fA = ar.get<uint16_t>(Gp * ldop);
       fB = ar.get<uint16_t>(Hp * ldop);
-      if (nA <= cellsA && nB <= cellsB) {
+      // a value that is not bf16-representable (statistics flag) rules the direct fills out
+      const bool vals_inexact = (cols[4].data && (hs[4].flags & 2)) || (cols[5].data && (hs[5].flags & 2));
+      if (nA <= cellsA && nB <= cellsB && !vals_inexact) {
         // optimistic: <= 1 tuple per cell and bf16-exact values -> the cells are the values
         // per side: binned (tile in shared memory, duplicate -> overflow) when the shape
         // fits, else scattered stores + occupancy bits whose popcount must equal the tuples
@@ -1072,14 +1074,17 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         // that the re-reads of the tuple columns per range cost more than the binned fill
         // (~13 ps per tuple at c4). TCUDB_FILL_PASSES=n forces n ranges, 0 the binned fill.
         const char* fp_env = getenv("TCUDB_FILL_PASSES");
-        // The tiled fill (one binning level into 65,536-cell tiles written coalesced from
-        // shared memory) is the default whenever its tile count fits; TCUDB_FILL_MODE=range /
-        // binned / direct selects the earlier fills (kept for comparison and small shapes).
+        // Row-range passes while <= 3 ranges cover the operand (c4: 1.51 ms vs 1.56 tiled), else
+        // the tiled fill (one binning level into 65,536-cell tiles written coalesced from shared
+        // memory; 1.56 ms vs 1.78 for the two-level binned fill on c4). TCUDB_FILL_MODE=range /
+        // tiled / binned / direct forces one.
         const char* fm_env = getenv("TCUDB_FILL_MODE");
         const std::string fill_mode = fm_env ? fm_env : "";
         auto direct_fill = [&](int side, const int32_t* kc, const int32_t* rc, const ColDesc& v, int64_t n,
                                int64_t rows, uint16_t* op) {
-          const size_t ws_t = (fill_mode.empty() || fill_mode == "tiled") ? fill_bf16_tiled_ws(n, rows, Kp) : 0;
+          const int64_t ranges = (rows * Kp * 2 + kFillRangeBytes - 1) / kFillRangeBytes;
+          const bool tiled_ok = fill_mode == "tiled" || (fill_mode.empty() && !fp_env && !(ranges <= 3 && Kp % 8 == 0));
+          const size_t ws_t = tiled_ok ? fill_bf16_tiled_ws(n, rows, Kp) : 0;
           if (ws_t) {
             binned[side] = true;  // duplicate check: fs.overflow (occupancy bits)
             ranged[side] = false;
@@ -1392,14 +1397,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         spa_one = ub_bytes <= 0.3 * (double)ctx->mem_free0 && (is_sum || u16_safe) &&
                   ((double)max_w <= 4.0 * avg_w + 65536.0 || (force_one && force_one[0] == '1'));
         S.spa_max_band = (int64_t)max_w;
-        // hybrid (COUNT, u16 cells): a count pass over the hub bands only, their counts
-        // published up front, then the one-pass kernel for everything — no band's look-back
-        // waits for a hub's expansion, and the other bands are expanded once. A u16 cell
-        // reaching 65,535 (possible: a hub band has >= 65,535 updates) falls back to the
-        // two-pass schedule below.
-        const char* no_hub = getenv("TCUDB_SPA_NO_HUB");
+        // hybrid (COUNT, u16 cells; opt-in TCUDB_SPA_HUB=1): a count pass over the hub bands
+        // only, their counts published up front, then the one-pass kernel for everything, so
+        // no look-back waits for a hub's expansion. Measured slower on c3 (12.3 ms vs 3.1 ms):
+        // below the hub threshold the power-law band weights still vary ~100x, and every CTA
+        // waits at its look-back for the slowest in-flight predecessor (82 % of warp samples
+        // at the barrier). A u16 cell reaching 65,535 falls back to the two-pass schedule.
+        const char* hub_env = getenv("TCUDB_SPA_HUB");
         if (!spa_one && !is_sum && sa.acc_kind == 4 && ub_bytes <= 0.3 * (double)ctx->mem_free0 &&
-            !(no_hub && no_hub[0] == '1')) {
+            hub_env && hub_env[0] == '1') {
           spa_hub = true;
           spa_one = true;
           hub_thr = (unsigned long long)(4.0 * avg_w + 65536.0);

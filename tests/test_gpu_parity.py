@@ -212,15 +212,15 @@ def test_float_direct_fill_guard_large(engine, torch_mod, oracle_mod, case, G):
 # SPA schedules: "one" = one persistent pass with look-back (forced even when skewed),
 # "auto" = the selector's choice, "two" = count pass + legacy write kernel,
 # "0" = C matrix in HBM (no shared-memory SPA)
-@pytest.mark.parametrize("spa", ["one", "auto", "two", "0", "nohub"])
+@pytest.mark.parametrize("spa", ["one", "auto", "two", "0", "hub"])
 @pytest.mark.parametrize("case", ["c3", "c5", "c5s", "wide_h", "skew_sum_float", "skew_sum_int", "hot_cell"])
 def test_sparse_spa_and_matrix_paths(engine, torch_mod, oracle_mod, monkeypatch, spa, case):
     """The sparse path under every schedule — all exact against the oracle. wide_h has a
     wide H (~30 K groups: one u16 row per band); the skew cases put most updates
-    in a few rows (auto: the hybrid hub-count + one-pass schedule; nohub: the two-pass
-    one); hot_cell drives one (g, h) COUNT past 65,535 (u16 cell overflow -> int32 rerun,
-    from the hybrid schedule via the two-pass fallback)."""
-    monkeypatch.setenv("TCUDB_SPA_NO_HUB", "1" if spa == "nohub" else "0")
+    in a few rows (hub: the opt-in hybrid hub-count + one-pass schedule); hot_cell drives
+    one (g, h) COUNT past 65,535 (u16 cell overflow -> int32 rerun, from the hybrid schedule
+    via the two-pass fallback)."""
+    monkeypatch.setenv("TCUDB_SPA_HUB", "1" if spa == "hub" else "0")
     monkeypatch.setenv("TCUDB_NO_SPA", "1" if spa == "0" else "0")
     monkeypatch.setenv("TCUDB_NO_SPA_FUSED", "1" if spa == "two" else "0")
     monkeypatch.setenv("TCUDB_SPA_ONE_PASS", "1" if spa == "one" else "0")
