@@ -338,11 +338,20 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
     // write pass: this band's row offsets, loaded now and consumed after the expansion
     int64_t rowoff0 = 0;
     if (a.row_out && threadIdx.x < nr) rowoff0 = a.row_out[g0 + threadIdx.x];
+    // a u16 cell can only reach 65,535 in a band with >= 65,535 updates: lighter bands use
+    // fire-and-forget reductions (the returning atomic's latency was ~15 % of the band
+    // kernel's warp samples on c3)
+    const bool check16 = ACC == 0 && a.act_off[a.goff[b + 1]] - a.act_off[a.goff[b]] >= 65535;
     spa_expand<(ACC >= 2)>(a, a.goff[b], a.goff[b + 1], g0, [&](int r, int h, int64_t pos, int32_t ai) {
       if constexpr (ACC == 0) {
         const int sh = (h & 1) * 16;
-        const unsigned old = atomicAdd(reinterpret_cast<unsigned*>(acc) + ((r * ldc + h) >> 1), 1u << sh);
-        if (((old >> sh) & 0xFFFFu) == 0xFFFFu) ovf = true;
+        unsigned* cell = reinterpret_cast<unsigned*>(acc) + ((r * ldc + h) >> 1);
+        if (check16) {
+          const unsigned old = atomicAdd(cell, 1u << sh);
+          if (((old >> sh) & 0xFFFFu) == 0xFFFFu) ovf = true;
+        } else {
+          atomicAdd(cell, 1u << sh);  // result unused: a shared-memory reduction
+        }
       } else if constexpr (ACC == 1) {
         atomicAdd(acc + r * ldc + h, 1);
       } else if constexpr (ACC == 2) {
@@ -439,18 +448,32 @@ __global__ void __launch_bounds__(NTF, 2) k_spa_fused(const SpaArgs a) {
         if (!(lane & 1) && wi < W) rb[wi] = 0u;  // this word is consumed (both halves were read above)
         __syncwarp();
         const int64_t hq = (int64_t)q * CW * 32;
-        for (int j = lane; j < total; j += 32) {
-          const int64_t h = hq + stage[j];
-          const int64_t o = base + j;
-          const long long hv = __ldg(a.dict_h + h);
-          if (a.g_out_type) __stcs(static_cast<long long*>(a.out_g) + o, gv);
-          else __stcs(static_cast<int*>(a.out_g) + o, (int)gv);
-          if (a.h_out_type) __stcs(static_cast<long long*>(a.out_h) + o, hv);
-          else __stcs(static_cast<int*>(a.out_h) + o, (int)hv);
-          const T x = arow[h];
-          arow[h] = (T)0;  // zero on read: the next band starts from a clear accumulator
-          if constexpr (ACC == 3) __stcs(static_cast<double*>(a.out_agg) + o, x);
-          else __stcs(static_cast<long long*>(a.out_agg) + o, (long long)x);
+        // two tuples per lane per step: both dictionary gathers are in flight before the
+        // stores that consume them (the h store stalled on its gather)
+        for (int j0 = lane; j0 < total; j0 += 64) {
+          const int j1 = j0 + 32;
+          const bool v1 = j1 < total;
+          const int64_t h0 = hq + stage[j0];
+          const int64_t h1 = v1 ? hq + stage[j1] : h0;
+          const long long hv0 = __ldg(a.dict_h + h0);
+          const long long hv1 = __ldg(a.dict_h + h1);
+          const T x0 = arow[h0];
+          const T x1 = arow[h1];
+          arow[h0] = (T)0;  // zero on read: the next band starts from a clear accumulator
+          if (v1) arow[h1] = (T)0;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !v1) break;
+            const int64_t o = base + (u ? j1 : j0);
+            const long long hv = u ? hv1 : hv0;
+            const T x = u ? x1 : x0;
+            if (a.g_out_type) __stcs(static_cast<long long*>(a.out_g) + o, gv);
+            else __stcs(static_cast<int*>(a.out_g) + o, (int)gv);
+            if (a.h_out_type) __stcs(static_cast<long long*>(a.out_h) + o, hv);
+            else __stcs(static_cast<int*>(a.out_h) + o, (int)hv);
+            if constexpr (ACC == 3) __stcs(static_cast<double*>(a.out_agg) + o, x);
+            else __stcs(static_cast<long long*>(a.out_agg) + o, (long long)x);
+          }
         }
         __syncwarp();
         base += total;
