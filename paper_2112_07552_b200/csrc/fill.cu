@@ -634,8 +634,9 @@ cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, 
 // written (tile), vs the scattered 2-byte stores of the direct / row-range fills that
 // are bound by L2's partial-sector store rate.
 namespace {
-constexpr int kT2Threads = 1024;
-constexpr int kT2Batch = 16 * kT2Threads;
+constexpr int kT2Threads = 1024;     // hist / tile kernels
+constexpr int kT2BinThreads = 512;   // bin kernel: 2 CTAs per SM, so one CTA's barrier phases
+constexpr int kT2Batch = 16 * kT2BinThreads;  //   overlap the other's loads
 constexpr int kT2MaxTiles = 4096;
 constexpr int kT2TileCells = 65536;
 struct T2Plan {
@@ -652,7 +653,7 @@ T2Plan t2_plan(int64_t n, int64_t rows, int64_t Kp) {
   const int64_t nkt = (Kp + KW - 1) / KW, nrt = (rows + R - 1) / R;
   if (nkt * nrt > kT2MaxTiles) return p;
   p.KW = KW; p.kw_bits = kb; p.R = R; p.nkt = (int)nkt; p.ntiles = (int)(nkt * nrt);
-  p.nblk = (int)std::min<int64_t>(kNumSMs, (n + kT2Batch - 1) / kT2Batch);
+  p.nblk = (int)std::min<int64_t>(2 * kNumSMs, (n + kT2Batch - 1) / kT2Batch);
   p.chunk = ((n + p.nblk - 1) / p.nblk + 3) & ~int64_t(3);  // 16-byte aligned chunks
   const int64_t m = (int64_t)p.ntiles * p.nblk;
   p.off_counts = 0;
@@ -686,7 +687,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2_hist(const int32_t* __restric
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(int64_t)t * gridDim.x + blockIdx.x] = hist[t];
 }
 
-__global__ void __launch_bounds__(kT2Threads, 1) k_t2_bin(const int32_t* __restrict__ kcode,
+__global__ void __launch_bounds__(kT2BinThreads, 2) k_t2_bin(const int32_t* __restrict__ kcode,
                                                          const int32_t* __restrict__ rcode,
                                                          const float* __restrict__ val, int64_t n, int64_t chunk,
                                                          int R, int KW, int kw_bits, int nkt, int ntiles,
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_t2_bin(const int32_t* __restr
   int64_t* gcur = reinterpret_cast<int64_t*>(stile + kT2Batch);             // [ntiles]
   int* cnt = reinterpret_cast<int*>(gcur + ntiles);                          // [ntiles]
   int* bstart = cnt + ntiles;                                                // [ntiles]
-  __shared__ int wsum[kT2Threads / 32];
+  __shared__ int wsum[kT2BinThreads / 32];
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
     gcur[t] = offs[(int64_t)t * gridDim.x + blockIdx.x];
     cnt[t] = 0;
@@ -706,15 +707,15 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_t2_bin(const int32_t* __restr
   __syncthreads();
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = max(lo, min(n, lo + chunk));
   const bool vec_val = val && (reinterpret_cast<uintptr_t>(val) & 15) == 0;
-  const int per = (ntiles + kT2Threads - 1) / kT2Threads;  // counters per thread in the scan
+  const int per = (ntiles + kT2BinThreads - 1) / kT2BinThreads;  // counters per thread in the scan
   int inexact = 0;
   for (int64_t b0 = lo; b0 < hi; b0 += kT2Batch) {
-    constexpr int U = kT2Batch / kT2Threads / 4;  // int4 vectors per thread per column
+    constexpr int U = kT2Batch / kT2BinThreads / 4;  // int4 vectors per thread per column
     uint32_t e[4 * U];
     int tl[4 * U], rk[4 * U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t i = b0 + ((int64_t)u * kT2Threads + threadIdx.x) * 4;
+      const int64_t i = b0 + ((int64_t)u * kT2BinThreads + threadIdx.x) * 4;
       int kc[4] = {-1, -1, -1, -1}, r[4] = {0, 0, 0, 0};
       uint32_t bv[4] = {0x3F800000u, 0x3F800000u, 0x3F800000u, 0x3F800000u};  // absent value = 1.0
       if (i + 3 < hi) {
@@ -765,14 +766,14 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_t2_bin(const int32_t* __restr
       if (lane_id() == 31) wsum[warp_id()] = incl;
       __syncthreads();
       if (warp_id() == 0) {
-        const int w = wsum[lane_id()];
+        const int w = lane_id() < kT2BinThreads / 32 ? wsum[lane_id()] : 0;
         int wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int t = __shfl_up_sync(0xffffffffu, wi, o);
           if (lane_id() >= o) wi += t;
         }
-        wsum[lane_id()] = wi - w;
+        if (lane_id() < kT2BinThreads / 32) wsum[lane_id()] = wi - w;
       }
       __syncthreads();
       int x = wsum[warp_id()] + incl - run;
@@ -868,7 +869,7 @@ cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, c
   if (e != cudaSuccess) return e;
   const int bin_smem = kT2Batch * 6 + p.ntiles * 16;
   if ((e = set_func_attr(k_t2_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, bin_smem)) != cudaSuccess) return e;
-  k_t2_bin<<<p.nblk, kT2Threads, bin_smem, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, p.chunk, p.R,
+  k_t2_bin<<<p.nblk, kT2BinThreads, bin_smem, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, p.chunk, p.R,
                                                 p.KW, p.kw_bits, p.nkt, p.ntiles, offs, ent, fs);
   const int tile_smem = kT2TileCells * 2 + kT2TileCells / 8;
   if ((e = set_func_attr(k_t2_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem)) != cudaSuccess) return e;
