@@ -635,8 +635,8 @@ cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, 
 // are bound by L2's partial-sector store rate.
 namespace {
 constexpr int kT2Threads = 1024;     // hist / tile kernels
-constexpr int kT2BinThreads = 512;   // bin kernel: 2 CTAs per SM, so one CTA's barrier phases
-constexpr int kT2Batch = 16 * kT2BinThreads;  //   overlap the other's loads
+constexpr int kT2BinThreads = 1024;  // bin kernel, one CTA per SM (512 x 2 CTAs measured slower on
+constexpr int kT2Batch = 16 * kT2BinThreads;  //   c4: 1.68 vs 1.56 ms — shorter runs per tile)
 constexpr int kT2MaxTiles = 4096;
 constexpr int kT2TileCells = 65536;
 struct T2Plan {
@@ -653,7 +653,7 @@ T2Plan t2_plan(int64_t n, int64_t rows, int64_t Kp) {
   const int64_t nkt = (Kp + KW - 1) / KW, nrt = (rows + R - 1) / R;
   if (nkt * nrt > kT2MaxTiles) return p;
   p.KW = KW; p.kw_bits = kb; p.R = R; p.nkt = (int)nkt; p.ntiles = (int)(nkt * nrt);
-  p.nblk = (int)std::min<int64_t>(2 * kNumSMs, (n + kT2Batch - 1) / kT2Batch);
+  p.nblk = (int)std::min<int64_t>(kNumSMs, (n + kT2Batch - 1) / kT2Batch);
   p.chunk = ((n + p.nblk - 1) / p.nblk + 3) & ~int64_t(3);  // 16-byte aligned chunks
   const int64_t m = (int64_t)p.ntiles * p.nblk;
   p.off_counts = 0;
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2_hist(const int32_t* __restric
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(int64_t)t * gridDim.x + blockIdx.x] = hist[t];
 }
 
-__global__ void __launch_bounds__(kT2BinThreads, 2) k_t2_bin(const int32_t* __restrict__ kcode,
+__global__ void __launch_bounds__(kT2BinThreads, 1) k_t2_bin(const int32_t* __restrict__ kcode,
                                                          const int32_t* __restrict__ rcode,
                                                          const float* __restrict__ val, int64_t n, int64_t chunk,
                                                          int R, int KW, int kw_bits, int nkt, int ntiles,

@@ -846,7 +846,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   // the dense product would take >= 1.5 ms at the device's measured rate, and when the dense
   // path could win at all (its byte traffic alone below the sparse estimate)
   bool bs_worth = bs_force;
-  if (!bs_force && dense_ops / gemm_rate >= 1.5e-3) {
+  // the analysis itself: ~15 ps per tuple (marking + re-coding passes) + ~0.1 ms of small
+  // launches and one host sync; it must be a small share of the product it may shrink
+  const double t_analysis = (double)(nA + nB) * 15e-12 + 100e-6;
+  if (!bs_force && dense_ops / gemm_rate >= std::max(1.5e-3, 4.0 * t_analysis)) {
     const double bytes = (double)(Gp + Hp) * Kp * (is_float ? 2.0 : 1.0) + (double)Gp * Hp * (is_sum ? 8.0 : 2.0);
     const double t_sp = (double)J / ctx->cal.R_sp + ctx->cal.T_sp0;
     bs_worth = 3.0 * bytes / ctx->cal.BW < t_sp;
