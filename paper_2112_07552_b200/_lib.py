@@ -314,7 +314,7 @@ class Engine:
         v = (ctypes.c_double * 7)()
         m = self._lib.tcudb_calibration(self._ctx, v)
         keys = ("R_i8", "R_bf16", "R_fp4", "BW", "R_sp", "T_sp0", "ms")
-        return dict(zip(keys, list(v)), measured=bool(m))
+        return dict(zip(keys, list(v)), measured=bool(m), injected=m == 2)
 
     @property
     def launch_count(self) -> int:

@@ -1650,6 +1650,18 @@ void calibrate(tcudb_ctx* c) {
   }
   const char* env = getenv("TCUDB_CALIBRATE");
   if (env && env[0] == '0') return;
+  // constants measured by an earlier run (e.g. the bench line's selector_calibration), for runs
+  // whose own timing is distorted (under a profiler): "R_i8,R_bf16,R_fp4,BW,R_sp,T_sp0"
+  if (const char* vals = getenv("TCUDB_CALIBRATION_VALUES")) {
+    Calib cal;
+    double v[6];
+    if (sscanf(vals, "%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) == 6) {
+      cal.R_i8 = v[0]; cal.R_bf16 = v[1]; cal.R_fp4 = v[2]; cal.BW = v[3]; cal.R_sp = v[4]; cal.T_sp0 = v[5];
+      cal.measured = 2;  // injected
+      c->cal = cal;
+      return;
+    }
+  }
   const auto t0 = std::chrono::steady_clock::now();
   Calib cal;
   cudaStream_t s = nullptr;

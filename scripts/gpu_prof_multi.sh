@@ -1,9 +1,10 @@
 #!/bin/bash
 # full ncu captures of selected kernels: args are "config:regex:count" triples
-# (TCUDB_CALIBRATE=0: the create-time calibration would otherwise be the first GEMM / sparse
-#  launches the regex matches)
+# (the create-time calibration would otherwise be the first GEMM / sparse launches the regex
+#  matches, and its timing under ncu is distorted: pass the constants of a normal run in
+#  TCUDB_CALIBRATION_VALUES, else the compiled defaults are used)
 mkdir -p gpurun_out
-export TCUDB_CALIBRATE=0
+if [ -z "$TCUDB_CALIBRATION_VALUES" ]; then export TCUDB_CALIBRATE=0; fi
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 for spec in "$@"; do
   IFS=: read c re n <<< "$spec"
