@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 
 #include "common.cuh"
@@ -639,28 +640,37 @@ constexpr int kT2BinThreads = 1024;  // bin kernel, one CTA per SM (512 x 2 CTAs
 constexpr int kT2Batch = 16 * kT2BinThreads;  //   c4: 1.68 vs 1.56 ms — shorter runs per tile)
 constexpr int kT2MaxTiles = 4096;
 constexpr int kT2TileCells = 65536;
+// SPLIT (values that are not bf16-exact): 8-byte entries (cell << 32 | fp32 bits), fp32 tiles of
+// 32,768 cells, and the tile CTA writes bf16 hi / lo = bf16(x - hi) into the segments of the
+// split layout ([hi|hi|lo|lo] for A, [hi|lo|hi|lo] for B) — no fp32 scratch, no atomics
+template <bool SPLIT> struct T2 {
+  using Ent = typename std::conditional<SPLIT, unsigned long long, uint32_t>::type;
+  static constexpr int kCells = SPLIT ? 32768 : kT2TileCells;
+  static constexpr int kBatch = SPLIT ? 8 * kT2BinThreads : kT2Batch;
+};
 struct T2Plan {
   int KW = 0, R = 0, nkt = 0, ntiles = 0, nblk = 0, kw_bits = 0;
   int64_t chunk = 0;
   size_t off_counts = 0, off_offs = 0, off_temp = 0, off_ent = 0, bytes = 0;
 };
-T2Plan t2_plan(int64_t n, int64_t rows, int64_t Kp) {
+T2Plan t2_plan(int64_t n, int64_t rows, int64_t Kp, bool split = false) {
   T2Plan p;
   if (n < (1 << 20) || Kp % 8) return p;
   int KW = 128, kb = 7;
   while (KW < Kp && KW < 8192) { KW *= 2; ++kb; }
-  const int R = kT2TileCells / KW;
+  const int R = (split ? 32768 : kT2TileCells) / KW;
   const int64_t nkt = (Kp + KW - 1) / KW, nrt = (rows + R - 1) / R;
   if (nkt * nrt > kT2MaxTiles) return p;
   p.KW = KW; p.kw_bits = kb; p.R = R; p.nkt = (int)nkt; p.ntiles = (int)(nkt * nrt);
-  p.nblk = (int)std::min<int64_t>(kNumSMs, (n + kT2Batch - 1) / kT2Batch);
+  const int batch = split ? 8 * kT2BinThreads : kT2Batch;
+  p.nblk = (int)std::min<int64_t>(kNumSMs, (n + batch - 1) / batch);
   p.chunk = ((n + p.nblk - 1) / p.nblk + 3) & ~int64_t(3);  // 16-byte aligned chunks
   const int64_t m = (int64_t)p.ntiles * p.nblk;
   p.off_counts = 0;
   p.off_offs = al256(m * 4);
   p.off_temp = p.off_offs + al256((m + 1) * 8);
   p.off_ent = p.off_temp + al256(scan_temp_bytes(m));
-  p.bytes = p.off_ent + al256(n * 4);
+  p.bytes = p.off_ent + al256(n * (split ? 8 : 4));
   return p;
 }
 
@@ -687,16 +697,20 @@ __global__ void __launch_bounds__(kT2Threads) k_t2_hist(const int32_t* __restric
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(int64_t)t * gridDim.x + blockIdx.x] = hist[t];
 }
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(kT2BinThreads, 1) k_t2_bin(const int32_t* __restrict__ kcode,
                                                          const int32_t* __restrict__ rcode,
                                                          const float* __restrict__ val, int64_t n, int64_t chunk,
                                                          int R, int KW, int kw_bits, int nkt, int ntiles,
                                                          const int64_t* __restrict__ offs,
-                                                         uint32_t* __restrict__ ent, FillStats* __restrict__ fs) {
+                                                         typename T2<SPLIT>::Ent* __restrict__ ent,
+                                                         FillStats* __restrict__ fs) {
+  using Ent = typename T2<SPLIT>::Ent;
+  constexpr int kBatch = T2<SPLIT>::kBatch;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* stage = reinterpret_cast<uint32_t*>(smem);                       // [kT2Batch]
-  uint16_t* stile = reinterpret_cast<uint16_t*>(stage + kT2Batch);           // [kT2Batch]
-  int64_t* gcur = reinterpret_cast<int64_t*>(stile + kT2Batch);             // [ntiles]
+  Ent* stage = reinterpret_cast<Ent*>(smem);                                 // [kBatch]
+  uint16_t* stile = reinterpret_cast<uint16_t*>(stage + kBatch);             // [kBatch]
+  int64_t* gcur = reinterpret_cast<int64_t*>(stile + kBatch);               // [ntiles]
   int* cnt = reinterpret_cast<int*>(gcur + ntiles);                          // [ntiles]
   int* bstart = cnt + ntiles;                                                // [ntiles]
   __shared__ int wsum[kT2BinThreads / 32];
@@ -709,9 +723,9 @@ __global__ void __launch_bounds__(kT2BinThreads, 1) k_t2_bin(const int32_t* __re
   const bool vec_val = val && (reinterpret_cast<uintptr_t>(val) & 15) == 0;
   const int per = (ntiles + kT2BinThreads - 1) / kT2BinThreads;  // counters per thread in the scan
   int inexact = 0;
-  for (int64_t b0 = lo; b0 < hi; b0 += kT2Batch) {
-    constexpr int U = kT2Batch / kT2BinThreads / 4;  // int4 vectors per thread per column
-    uint32_t e[4 * U];
+  for (int64_t b0 = lo; b0 < hi; b0 += kBatch) {
+    constexpr int U = kBatch / kT2BinThreads / 4;  // int4 vectors per thread per column
+    Ent e[4 * U];
     int tl[4 * U], rk[4 * U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -746,8 +760,9 @@ __global__ void __launch_bounds__(kT2BinThreads, 1) k_t2_bin(const int32_t* __re
         if (kc[q] < 0) continue;
         inexact |= (bv[q] & 0xFFFFu) != 0u;
         tl[x] = t2_tile(r[q], kc[q], R, kw_bits, nkt);
-        const uint32_t cell = (uint32_t)((r[q] % R) * KW + (kc[q] & (KW - 1)));  // < 65536
-        e[x] = (cell << 16) | (bv[q] >> 16);
+        const uint32_t cell = (uint32_t)((r[q] % R) * KW + (kc[q] & (KW - 1)));  // < tile cells
+        if constexpr (SPLIT) e[x] = ((unsigned long long)cell << 32) | bv[q];
+        else e[x] = (cell << 16) | (bv[q] >> 16);
         rk[x] = atomicAdd(&cnt[tl[x]], 1);
       }
     }
@@ -805,35 +820,40 @@ __global__ void __launch_bounds__(kT2BinThreads, 1) k_t2_bin(const int32_t* __re
   if (threadIdx.x == 0 && inexact) atomicOr(&fs->inexact, 1);
 }
 
-// one CTA per tile: R x KW bf16 cells + occupancy bits in shared memory
-__global__ void __launch_bounds__(kT2Threads, 1) k_t2_tile(const uint32_t* __restrict__ ent,
+// one CTA per tile: R x KW bf16 cells (SPLIT: fp32 cells, written as bf16 hi / lo into the
+// segments hi_mask / lo_mask of the split layout, segment stride Kp) + occupancy bits
+template <bool SPLIT>
+__global__ void __launch_bounds__(kT2Threads, 1) k_t2_tile(const typename T2<SPLIT>::Ent* __restrict__ ent,
                                                           const int64_t* __restrict__ offs, int nblk, int R, int KW,
                                                           int nkt, int64_t rows, int64_t Kp,
-                                                          uint16_t* __restrict__ op, int64_t ld_op,
-                                                          FillStats* __restrict__ fs) {
+                                                          uint16_t* __restrict__ op, int64_t ld_op, int hi_mask,
+                                                          int lo_mask, FillStats* __restrict__ fs) {
+  using Ent = typename T2<SPLIT>::Ent;
+  constexpr int kCells = T2<SPLIT>::kCells;
+  using Cell = typename std::conditional<SPLIT, uint32_t, uint16_t>::type;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
-  unsigned* occ = reinterpret_cast<unsigned*>(smem + (size_t)kT2TileCells * 2);
-  for (int i = threadIdx.x; i < kT2TileCells / 8; i += blockDim.x)
+  Cell* tile = reinterpret_cast<Cell*>(smem);
+  unsigned* occ = reinterpret_cast<unsigned*>(smem + (size_t)kCells * sizeof(Cell));
+  for (int i = threadIdx.x; i < kCells * (int)sizeof(Cell) / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(tile)[i] = make_uint4(0, 0, 0, 0);
-  for (int i = threadIdx.x; i < kT2TileCells / 32; i += blockDim.x) occ[i] = 0;
+  for (int i = threadIdx.x; i < kCells / 32; i += blockDim.x) occ[i] = 0;
   __syncthreads();
   const int t = blockIdx.x;
   const int64_t lo = offs[(int64_t)t * nblk], hi = offs[(int64_t)(t + 1) * nblk];
   int dup = 0;
   constexpr int U = 4;
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)U * blockDim.x) {
-    uint32_t e[U];
+    Ent e[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + (int64_t)u * blockDim.x;
-      e[u] = i < hi ? __ldcs(ent + i) : 0xFFFFFFFFu;
+      e[u] = i < hi ? __ldcs(ent + i) : (Ent)0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (i0 + (int64_t)u * blockDim.x >= hi) continue;
-      const uint32_t c = e[u] >> 16;
-      tile[c] = (uint16_t)(e[u] & 0xFFFFu);
+      const uint32_t c = SPLIT ? (uint32_t)((unsigned long long)e[u] >> 32) : (uint32_t)e[u] >> 16;
+      tile[c] = SPLIT ? (Cell)((unsigned long long)e[u] & 0xFFFFFFFFull) : (Cell)((uint32_t)e[u] & 0xFFFFu);
       dup |= (int)((atomicOr(&occ[c >> 5], 1u << (c & 31)) >> (c & 31)) & 1u);
     }
   }
@@ -844,38 +864,77 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_t2_tile(const uint32_t* __res
   const int v8 = ncol / 8;
   for (int i = threadIdx.x; i < nrow * v8; i += blockDim.x) {
     const int r = i / v8, c = i - r * v8;
-    __stcs(reinterpret_cast<uint4*>(op + (r0 + r) * ld_op + c0) + c,
-           reinterpret_cast<const uint4*>(tile + (int64_t)r * KW)[c]);
+    if constexpr (!SPLIT) {
+      __stcs(reinterpret_cast<uint4*>(op + (r0 + r) * ld_op + c0) + c,
+             reinterpret_cast<const uint4*>(tile + (int64_t)r * KW)[c]);
+    } else {
+      const float4 a = reinterpret_cast<const float4*>(tile + (int64_t)r * KW)[2 * c];
+      const float4 b = reinterpret_cast<const float4*>(tile + (int64_t)r * KW)[2 * c + 1];
+      const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint16_t h0 = bf16_bits(x[2 * j]), h1 = bf16_bits(x[2 * j + 1]);
+        hw[j] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+        lw[j] = (uint32_t)bf16_bits(x[2 * j] - bf16_val(h0)) | ((uint32_t)bf16_bits(x[2 * j + 1] - bf16_val(h1)) << 16);
+      }
+      uint16_t* row = op + (r0 + r) * ld_op + c0 + (int64_t)c * 8;
+#pragma unroll
+      for (int sg = 0; sg < 4; ++sg) {
+        if (hi_mask & (1 << sg)) __stcs(reinterpret_cast<uint4*>(row + (int64_t)sg * Kp), make_uint4(hw[0], hw[1], hw[2], hw[3]));
+        if (lo_mask & (1 << sg)) __stcs(reinterpret_cast<uint4*>(row + (int64_t)sg * Kp), make_uint4(lw[0], lw[1], lw[2], lw[3]));
+      }
+    }
   }
   dup = __syncthreads_or(dup);
   if (threadIdx.x == 0 && dup) atomicOr(&fs->overflow, 1);
 }
 }  // namespace
 
-size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp) { return t2_plan(n, rows, Kp).bytes; }
+size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp, bool split) {
+  return t2_plan(n, rows, Kp, split).bytes;
+}
 
-cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
-                                   int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
-                                   cudaStream_t s, int64_t* launches) {
-  const T2Plan p = t2_plan(n, rows, Kp);
+template <bool SPLIT>
+static cudaError_t run_t2(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n, int64_t rows,
+                          int64_t Kp, uint16_t* op, int64_t ld_op, int hi_mask, int lo_mask, FillStats* fs, void* ws,
+                          cudaStream_t s, int64_t* launches) {
+  using Ent = typename T2<SPLIT>::Ent;
+  const T2Plan p = t2_plan(n, rows, Kp, SPLIT);
   if (!p.bytes) return cudaErrorInvalidValue;
   uint8_t* w = static_cast<uint8_t*>(ws);
   int32_t* counts = reinterpret_cast<int32_t*>(w + p.off_counts);
   int64_t* offs = reinterpret_cast<int64_t*>(w + p.off_offs);
-  uint32_t* ent = reinterpret_cast<uint32_t*>(w + p.off_ent);
+  Ent* ent = reinterpret_cast<Ent*>(w + p.off_ent);
   const int64_t m = (int64_t)p.ntiles * p.nblk;
   k_t2_hist<<<p.nblk, kT2Threads, 0, s>>>(kcode, rcode, n, p.chunk, p.R, p.kw_bits, p.nkt, p.ntiles, counts);
   cudaError_t e = exclusive_scan_i32(counts, offs, m, offs + m, w + p.off_temp, s, launches);
   if (e != cudaSuccess) return e;
-  const int bin_smem = kT2Batch * 6 + p.ntiles * 16;
-  if ((e = set_func_attr(k_t2_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, bin_smem)) != cudaSuccess) return e;
-  k_t2_bin<<<p.nblk, kT2BinThreads, bin_smem, s>>>(kcode, rcode, static_cast<const float*>(val.data), n, p.chunk, p.R,
-                                                p.KW, p.kw_bits, p.nkt, p.ntiles, offs, ent, fs);
-  const int tile_smem = kT2TileCells * 2 + kT2TileCells / 8;
-  if ((e = set_func_attr(k_t2_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem)) != cudaSuccess) return e;
-  k_t2_tile<<<p.ntiles, kT2Threads, tile_smem, s>>>(ent, offs, p.nblk, p.R, p.KW, p.nkt, rows, Kp, op, ld_op, fs);
+  const int bin_smem = T2<SPLIT>::kBatch * (int)(sizeof(Ent) + 2) + p.ntiles * 16;
+  if ((e = set_func_attr(k_t2_bin<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bin_smem)) != cudaSuccess)
+    return e;
+  k_t2_bin<SPLIT><<<p.nblk, kT2BinThreads, bin_smem, s>>>(kcode, rcode, static_cast<const float*>(val.data), n,
+                                                          p.chunk, p.R, p.KW, p.kw_bits, p.nkt, p.ntiles, offs, ent,
+                                                          fs);
+  const int tile_smem = T2<SPLIT>::kCells * (SPLIT ? 4 : 2) + T2<SPLIT>::kCells / 8;
+  if ((e = set_func_attr(k_t2_tile<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem)) != cudaSuccess)
+    return e;
+  k_t2_tile<SPLIT><<<p.ntiles, kT2Threads, tile_smem, s>>>(ent, offs, p.nblk, p.R, p.KW, p.nkt, rows, Kp, op, ld_op,
+                                                           hi_mask, lo_mask, fs);
   if (launches) *launches += 3;
   return cudaGetLastError();
+}
+
+cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                   int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
+                                   cudaStream_t s, int64_t* launches) {
+  return run_t2<false>(kcode, rcode, val, n, rows, Kp, op, ld_op, 1, 0, fs, ws, s, launches);
+}
+
+cudaError_t launch_fill_bf16_split_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                         int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, int hi_mask,
+                                         int lo_mask, FillStats* fs, void* ws, cudaStream_t s, int64_t* launches) {
+  return run_t2<true>(kcode, rcode, val, n, rows, Kp, op, ld_op, hi_mask, lo_mask, fs, ws, s, launches);
 }
 
 cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,

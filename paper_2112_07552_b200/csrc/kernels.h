@@ -126,7 +126,13 @@ cudaError_t launch_fill_bf16_direct(const int32_t* kcode, const int32_t* rcode, 
 size_t fill_bf16_binned_ws(int64_t n, int64_t rows, int64_t Kp);
 // Tiled direct fill (one binning level into 65,536-cell tiles, then one CTA per tile);
 // workspace bytes (0: shape not supported), fs->inexact / fs->overflow as the binned fill.
-size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp);
+size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp, bool split = false);
+// The same for values that are not bf16-exact: fp32 tiles, written as bf16 hi / lo = bf16(x - hi)
+// into the segments hi_mask / lo_mask of the hi/lo split layout (segment stride Kp, row stride
+// ld_op); duplicate cells set fs->overflow (the caller then takes the fp32-scratch path).
+cudaError_t launch_fill_bf16_split_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
+                                         int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, int hi_mask,
+                                         int lo_mask, FillStats* fs, void* ws, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                    int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
                                    cudaStream_t s, int64_t* launches);

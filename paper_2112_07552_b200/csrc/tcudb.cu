@@ -1061,12 +1061,12 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     }
     bool bf16_direct = false;
     uint16_t *fA = nullptr, *fB = nullptr;
+    const bool vals_inexact = is_float && ((cols[4].data && (hs[4].flags & 2)) || (cols[5].data && (hs[5].flags & 2)));
     if (is_float) {
       ldop = 4 * Kp;
       fA = ar.get<uint16_t>(Gp * ldop);
       fB = ar.get<uint16_t>(Hp * ldop);
       // a value that is not bf16-representable (statistics flag) rules the direct fills out
-      const bool vals_inexact = (cols[4].data && (hs[4].flags & 2)) || (cols[5].data && (hs[5].flags & 2));
       if (nA <= cellsA && nB <= cellsB && !vals_inexact) {
         // optimistic: <= 1 tuple per cell and bf16-exact values -> the cells are the values
         // per side: binned (tile in shared memory, duplicate -> overflow) when the shape
@@ -1133,6 +1133,30 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       }
     }
     if (is_float && bf16_direct) {
+      opA = reinterpret_cast<uint8_t*>(fA);
+      opB = reinterpret_cast<uint8_t*>(fB);
+    } else if (is_float && vals_inexact && !(q->flags & TCUDB_FORCE_WIDE) && nA <= cellsA && nB <= cellsB &&
+               fill_bf16_tiled_ws(nA, Gp, Kp, true) && fill_bf16_tiled_ws(nB, Hp, Kp, true) &&
+               [&] {
+                 // optimistic: <= 1 tuple per cell -> the tiled fill writes bf16 hi / lo straight
+                 // into the split layout A' = [hi|hi|lo|lo], B' = [hi|lo|hi|lo] (no fp32 scratch,
+                 // no atomics); a duplicate cell falls through to the scratch path below
+                 const size_t ws = std::max(fill_bf16_tiled_ws(nA, Gp, Kp, true), fill_bf16_tiled_ws(nB, Hp, Kp, true));
+                 uint8_t* w = ar.get<uint8_t>((int64_t)ws);
+                 CK(launch_fill_bf16_split_tiled(kA, gA, av, nA, Gp, Kp, fA, ldop, 0b0011, 0b1100, fs + 0, w, s, L));
+                 CK(launch_fill_bf16_split_tiled(kB, hB, bw, nB, Hp, Kp, fB, ldop, 0b0101, 0b1010, fs + 1, w, s, L));
+                 CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+                 CK(cudaStreamSynchronize(s));
+                 FillStats hf[2];
+                 std::memcpy(hf, ctx->pinned, sizeof(hf));
+                 if (hf[0].overflow || hf[1].overflow) {
+                   CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
+                   return false;
+                 }
+                 return true;
+               }()) {
+      k_len = 4 * Kp;
+      S.elem = 2;
       opA = reinterpret_cast<uint8_t*>(fA);
       opB = reinterpret_cast<uint8_t*>(fB);
     } else if (is_float) {

@@ -919,7 +919,8 @@ def test_selector_calibration_measured(engine):
 
 
 @pytest.mark.parametrize("mode", ["tiled", "range", "binned"])
-@pytest.mark.parametrize("case", ["unique", "dup_nonzero", "dup_zero_after", "zero_values", "inexact"])
+@pytest.mark.parametrize("case", ["unique", "dup_nonzero", "dup_zero_after", "zero_values", "inexact",
+                                  "inexact_dup"])
 def test_bf16_fill_modes_large(engine, torch_mod, oracle_mod, monkeypatch, mode, case):
     """The bf16 direct fills on >= 2^20 tuples (the tiled fill's size): 1024 x 1024 cells in
     shuffled order, ragged G (1000 rows), a duplicate cell (nonzero / zero second value),
@@ -936,8 +937,11 @@ def test_bf16_fill_modes_large(engine, torch_mod, oracle_mod, monkeypatch, mode,
         ag, ak, av = np.append(ag, ag[5]), np.append(ak, ak[5]), np.append(av, np.float32(0.0))
     elif case == "zero_values":
         av[::7] = 0.0
-    elif case == "inexact":
+    elif case == "inexact":          # -> the tiled hi/lo split fill (unique cells)
         av[123] = np.float32(0.1)
+    elif case == "inexact_dup":      # -> split fill sees the duplicate -> fp32 scratch path
+        av[123] = np.float32(0.1)
+        ag, ak, av = np.append(ag, ag[5]), np.append(ak, ak[5]), np.append(av, np.float32(0.3))
     bk = np.tile(np.arange(m, dtype=np.int32), 3)
     bh = np.repeat(np.arange(3, dtype=np.int32), m)
     bw = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, 3 * m).astype(np.float32))
