@@ -110,7 +110,8 @@ typedef struct {
   int32_t planes_b;
   int32_t existence;  /* 0: existence from C itself, 1: separate COUNT plane */
   int32_t kchunks;    /* K chunks accumulated in int64 (1 = single int32 pass) */
-  int32_t key_mode;   /* 0 direct-offset dictionary, 1 hash dictionary (join key) */
+  int32_t key_mode;   /* 0 direct-offset dictionary, 1 hash dictionary (join key), 2 direct-offset with
+                         the codes looked up inside the fused dense fill (no per-tuple code columns) */
   int32_t n_launches; /* kernels launched by this call */
   int64_t G, H, K, K_union, join_pairs, n_result;
   double density_union; /* nnz cells / (G * K_union): the paper's density */

@@ -139,6 +139,28 @@ cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, c
 cudaError_t launch_fill_bf16_binned(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                     int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
                                     cudaStream_t s, int64_t* launches);
+// ---- fill_direct.cu: a2 + a5 fused for direct-offset dictionaries over int32 columns (c4 class)
+constexpr int kDirectSpanMax = 16384;  // key / group spans whose u16 code tables the fill keeps in smem
+// One side: cnt_span[x - kmin] += #tuples with key x; kflag[x - kmin] = 1, gflag[g - gmin] = 1
+// (zeroed by the caller). 16-byte aligned columns; kspan * 4 + gspan <= 160 KB.
+bool direct_count_ok(int64_t kspan, int64_t gspan);
+cudaError_t launch_direct_count(const int32_t* key, const int32_t* grp, int64_t n, long long kmin, int64_t kspan,
+                                long long gmin, int64_t gspan, int32_t* cnt_span, uint8_t* kflag, uint8_t* gflag,
+                                cudaStream_t s, int64_t* launches);
+struct DtFill {
+  const int32_t* key; const int32_t* grp; const float* val; int64_t n;  // val NULL: 1.0
+  long long kmin; int kspan; const int32_t* kcode;  // code table over the key span (-1: not in the ∩ domain)
+  long long gmin; int gspan; const int32_t* gcode;  // row-code table over the group span
+  int64_t rows, Kp;                                 // operand rows (multiple of 8) and K columns (of 128)
+  uint16_t* op; int64_t ld_op;                      // bf16 operand [rows][ld_op] (elements)
+  int hi_mask, lo_mask;                             // split: segments (stride Kp) receiving hi / lo
+  uint8_t* pat; int64_t ld_pat;                     // optional e2m1 existence pattern [rows][ld_pat bytes]
+  FillStats* fs;                                    // fs->overflow: a cell with two tuples
+};
+bool fill_direct_ok(const DtFill& f, bool split);
+size_t fill_direct_ws(int64_t rows, int64_t Kp, bool split);
+// split = false: bf16-exact values, cells written as bf16; true: fp32 cells -> hi / lo segments
+cudaError_t launch_fill_direct(const DtFill& f, bool split, void* ws, cudaStream_t s, int64_t* launches);
 // Pattern plane op[r][k] = 1 where a cell holds >= 1 tuple; symmetric adjacency for triangles.
 cudaError_t launch_fill_pattern_u8(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op, int64_t ld,
                                    cudaStream_t s, int64_t* launches);

@@ -179,6 +179,27 @@ double hll_estimate(const unsigned* r) {
   return e;
 }
 
+// Direct-offset dictionary in two halves around its marks: allocation (zeroed flags over
+// [mn, mx]; fb for the second side of an ∩ domain; the sorted value array of a group domain)
+// and the codes (exclusive scan of the flags; a group domain's ascending values come out of
+// the same scan). The marks are k_mark_direct's, or k_direct_count's (fill_direct.cu).
+void dict_direct_alloc(Arena& ar, Dict& d, long long mn, long long mx, bool two_cols, bool intersect) {
+  d.mode = 0;
+  d.minv = mn;
+  if (!d.count_dev) d.count_dev = ar.get<int64_t>(1);
+  d.span = (unsigned long long)((unsigned long long)mx - (unsigned long long)mn) + 1;
+  const int64_t sp = (int64_t)d.span;
+  d.fa = ar.zeros<uint8_t>(sp);
+  d.fb = intersect ? ar.zeros<uint8_t>(sp) : nullptr;
+  d.code = ar.get<int32_t>(sp);
+  d.dict = two_cols ? nullptr : ar.get<long long>(sp);
+}
+void dict_direct_codes(Arena& ar, Dict& d, unsigned long long* union_dev, int64_t* launches) {
+  void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)d.span));
+  CK(launch_pred_codes(d.fa, d.fb, (int64_t)d.span, d.code, d.count_dev, union_dev, d.dict, d.minv, tmp, ar.s,
+                       launches));
+}
+
 // Build phase 1 of a dictionary over one or two columns (marks + codes / compaction).
 // intersect: K domain, code only keys present on both sides (∩); otherwise the union.
 // est_distinct (> 0) sizes the hash table: 2^ceil(log2(1.9 x estimate)), never above 2n
@@ -197,21 +218,11 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.bits = b;
   }
   if (dict_is_direct(n, mn, mx)) {
-    d.mode = 0;
-    d.span = (unsigned long long)span;
-    d.fa = ar.zeros<uint8_t>((int64_t)d.span);
+    dict_direct_alloc(ar, d, mn, mx, c2 != nullptr, c2 && intersect);
     const int64_t sp = (int64_t)d.span;
     CK(launch_mark_direct(c1, mn, d.fa, sp, s, launches));
-    if (c2) {
-      if (intersect) { d.fb = ar.zeros<uint8_t>(sp); CK(launch_mark_direct(*c2, mn, d.fb, sp, s, launches)); }
-      else CK(launch_mark_direct(*c2, mn, d.fa, sp, s, launches));
-    }
-    d.code = ar.get<int32_t>((int64_t)d.span);
-    void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)d.span));
-    // group domains (single column): the ascending value dictionary comes out of the same scan
-    if (!c2) d.dict = ar.get<long long>(sp);
-    CK(launch_pred_codes(d.fa, d.fb, (int64_t)d.span, d.code, d.count_dev, union_dev, d.dict, mn, tmp, s,
-                         launches));
+    if (c2) CK(launch_mark_direct(*c2, mn, intersect ? d.fb : d.fa, sp, s, launches));
+    dict_direct_codes(ar, d, union_dev, launches);
   } else {
     if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
     d.mode = 1;
@@ -663,19 +674,62 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   int32_t *cntA = nullptr, *cntB = nullptr;
   // J, max rowabs A, max rowabs B, A tuples with a ∩ key, B tuples with a ∩ key
   unsigned long long misc[6] = {0, 0, 0, 0, 0, 0};
+  // Deferred per-tuple codes (fill_direct.cu): float SUM over int32 columns whose three
+  // dictionaries are direct with spans that fit shared memory, large inputs (the c4 class).
+  // One pass per side marks the dictionaries and counts tuples per key (cntA / cntB over the
+  // key span: J is the same sum); the dense fill looks the codes up itself, and any other
+  // consumer materializes them first (need_codes below).
+  bool lazy = false;
+  int64_t Ku_lazy = 0;
+  {
+    const char* nl = getenv("TCUDB_NO_LAZY_CODES");
+    const char* fl = getenv("TCUDB_LAZY_CODES");  // tests: skip the size thresholds
+    const bool big = (nA >= (1 << 22) && nB >= (1 << 22)) || (fl && fl[0] == '1');
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    auto span_of = [](long long mn, long long mx) {
+      return (int64_t)std::min<unsigned long long>((unsigned long long)mx - (unsigned long long)mn + 1, 1ull << 40);
+    };
+    const int64_t ksp = span_of(kmin, kmax), gsp = span_of(hs[2].mn, hs[2].mx), hsp = span_of(hs[3].mn, hs[3].mx);
+    lazy = is_float && !absent && !(nl && nl[0] == '1') && !(q->flags & TCUDB_FORCE_SPARSE) && ag.data && bh.data &&
+           big && ak.type == TCUDB_I32 && bk.type == TCUDB_I32 &&
+           ag.type == TCUDB_I32 && bh.type == TCUDB_I32 && al16(ak.data) && al16(bk.data) && al16(ag.data) &&
+           al16(bh.data) && dict_is_direct(nA + nB, kmin, kmax) && dict_is_direct(nA, hs[2].mn, hs[2].mx) &&
+           dict_is_direct(nB, hs[3].mn, hs[3].mx) && ksp <= kDirectSpanMax && gsp <= kDirectSpanMax &&
+           hsp <= kDirectSpanMax && direct_count_ok(ksp, std::max(gsp, hsp));
+  }
   for (int attempt = 0; attempt < 2; ++attempt) {
+    double* rowA = nullptr;
+    double* rowB = nullptr;
+    int64_t Ku, Gu = 0, Hu = 0;
+    if (lazy) {
+      dict_direct_alloc(ar, DK, kmin, kmax, true, true);
+      dict_direct_alloc(ar, DG, hs[2].mn, hs[2].mx, false, false);
+      dict_direct_alloc(ar, DH, hs[3].mn, hs[3].mx, false, false);
+      Ku = Ku_lazy = (int64_t)DK.span;
+      cntA = ar.zeros<int32_t>(Ku);  // indexed by key offset here (by code once materialized)
+      cntB = ar.zeros<int32_t>(Ku);
+      CK(launch_direct_count(static_cast<const int32_t*>(ak.data), static_cast<const int32_t*>(ag.data), nA, kmin,
+                             Ku, DG.minv, (int64_t)DG.span, cntA, DK.fa, DG.fa, s, L));
+      CK(launch_direct_count(static_cast<const int32_t*>(bk.data), static_cast<const int32_t*>(bh.data), nB, kmin,
+                             Ku, DH.minv, (int64_t)DH.span, cntB, DK.fb, DH.fa, s, L));
+      dict_direct_codes(ar, DK, d_union, L);
+      dict_direct_codes(ar, DG, nullptr, L);
+      dict_direct_codes(ar, DH, nullptr, L);
+    } else {
     dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0]);
     dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
     dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2]);
     // probe right away with upper-bound sizes (codes < span / capacity), so the dictionary
     // sizes and the join size J come back in ONE device->host read
-    const int64_t Ku = (int64_t)DK.span, Gu = (int64_t)DG.span, Hu = (int64_t)DH.span;
+    Ku = (int64_t)DK.span;
+    Gu = (int64_t)DG.span; Hu = (int64_t)DH.span;
     cntA = ar.zeros<int32_t>(Ku);
     cntB = ar.zeros<int32_t>(Ku);
-    double* rowA = int_sum ? ar.zeros<double>(Gu) : nullptr;
-    double* rowB = int_sum ? ar.zeros<double>(Hu) : nullptr;
+    rowA = int_sum ? ar.zeros<double>(Gu) : nullptr;
+    rowB = int_sum ? ar.zeros<double>(Hu) : nullptr;
     CK(launch_probe(ak, ag, av, DK.view(1), DG.view(1), kA, gA, cntA, rowA, Ku, s, L));
     CK(launch_probe(bk, bh, bw, DK.view(2), DH.view(1), kB, hB, cntB, rowB, Ku, s, L));
+    }
     unsigned long long* d_misc = ar.zeros<unsigned long long>(6);
     CK(launch_join_size(cntA, cntB, Ku, d_misc + 0, s, L));
     if (int_sum) {
@@ -704,6 +758,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     DK = Dict(); DG = Dict(); DH = Dict();
   }
   const int64_t K = DK.count, G = DG.count, H = DH.count;
+  // deferred codes: the per-tuple codes and per-code counts for every path but the fused fill
+  auto need_codes = [&]() {
+    if (!lazy) return;
+    lazy = false;
+    cntA = ar.zeros<int32_t>(Ku_lazy);
+    cntB = ar.zeros<int32_t>(Ku_lazy);
+    CK(launch_probe(ak, ag, av, DK.view(1), DG.view(1), kA, gA, cntA, nullptr, Ku_lazy, s, L));
+    CK(launch_probe(bk, bh, bw, DK.view(2), DH.view(1), kB, hB, cntB, nullptr, Ku_lazy, s, L));
+  };
   S.K = K; S.G = G; S.H = H;
   S.key_mode = DK.mode;
   tm.mark(&S.ms_encode);
@@ -736,6 +799,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   // (a single distinct group on a grouped side takes it too, unless a path is forced)
   if (absent || ((G == 1 || H == 1) && !(q->flags & (TCUDB_FORCE_DENSE | TCUDB_FORCE_SPARSE)))) {
     S.path = 2;
+    need_codes();
     const bool by_h = G == 1;  // reduce B's tuples into H groups with A's per-key (count, sum)
     const int32_t* k_this = by_h ? kB : kA;
     const int32_t* g_this = by_h ? hB : gA;
@@ -855,6 +919,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     bs_worth = 3.0 * bytes / ctx->cal.BW < t_sp;
   }
   if (!bs_off && bs_worth && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
+    need_codes();
     CK(launch_bs_reorder(kA, gA, nA, kB, nB, cntA, cntB, K, G, ar.get<char>((int64_t)bs_reorder_temp_bytes(K)), s,
                          L));
     const int64_t kgroups = (Kp * 4 + 63) / 64;  // 64-key groups over the widest K' (the split's 4 Kp)
@@ -929,6 +994,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     if (!dense && sparse_bytes > 0.85 * free_b && dense_bytes <= 0.85 * free_b) dense = true;
   }
   S.path = dense ? 0 : 1;
+  if (!dense || !is_float) need_codes();
   S.elem = is_float ? 1 : 0;
   S.planes_a = S.planes_b = 1;
   S.kchunks = 1;
@@ -1062,12 +1128,69 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     bool bf16_direct = false;
     uint16_t *fA = nullptr, *fB = nullptr;
     const bool vals_inexact = is_float && ((cols[4].data && (hs[4].flags & 2)) || (cols[5].data && (hs[5].flags & 2)));
+    bool fused_split = false;  // the fused fill wrote the hi / lo split
+    bool pat_done = false;     // ... and the e2m1 existence pattern
     if (is_float) {
       ldop = 4 * Kp;
       fA = ar.get<uint16_t>(Gp * ldop);
       fB = ar.get<uint16_t>(Hp * ldop);
+      if (lazy) {
+        // a2 + a5 fused (fill_direct.cu): codes looked up inside the fill; optimistic (<= 1
+        // tuple per cell: the tiles' occupancy bits check it), the existence pattern (R3)
+        // comes from the same occupancy bits; any failure materializes the codes and
+        // continues on the general fills below
+        const bool split = vals_inexact;
+        const bool pat_ok = need_exist && ctx->fp4 && !(q->flags & TCUDB_NO_FP4) && K < (1 << 24);
+        DtFill f[2];
+        for (int side = 0; side < 2; ++side) {
+          DtFill& x = f[side];
+          x = DtFill{};
+          const ColDesc& kc = side ? bk : ak;
+          const ColDesc& gc = side ? bh : ag;
+          const ColDesc& vc = side ? bw : av;
+          const Dict& D = side ? DH : DG;
+          x.key = static_cast<const int32_t*>(kc.data);
+          x.grp = static_cast<const int32_t*>(gc.data);
+          x.val = vc.data && vc.type == TCUDB_F32 ? static_cast<const float*>(vc.data) : nullptr;
+          x.n = side ? nB : nA;
+          x.kmin = DK.minv; x.kspan = (int)DK.span; x.kcode = DK.code;
+          x.gmin = D.minv; x.gspan = (int)D.span; x.gcode = D.code;
+          x.rows = side ? Hp : Gp; x.Kp = Kp;
+          x.op = side ? fB : fA; x.ld_op = ldop;
+          x.hi_mask = side ? 0b0101 : 0b0011;
+          x.lo_mask = side ? 0b1010 : 0b1100;
+          x.fs = fs + side;
+        }
+        const bool vals_ok = (!av.data || av.type == TCUDB_F32) && (!bw.data || bw.type == TCUDB_F32);
+        if (vals_ok && nA <= cellsA && nB <= cellsB && fill_direct_ok(f[0], split) && fill_direct_ok(f[1], split)) {
+          if (pat_ok) {
+            patA = ar.zeros<uint8_t>(Gp * Kp4 / 2);
+            patB = ar.zeros<uint8_t>(Hp * Kp4 / 2);
+            f[0].pat = patA; f[1].pat = patB;
+            f[0].ld_pat = f[1].ld_pat = Kp4 / 2;
+          }
+          const size_t ws = std::max(fill_direct_ws(Gp, Kp, split), fill_direct_ws(Hp, Kp, split));
+          void* w = ar.get<uint8_t>((int64_t)ws);
+          CK(launch_fill_direct(f[0], split, w, s, L));
+          CK(launch_fill_direct(f[1], split, w, s, L));
+          CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
+          FillStats hf[2];
+          std::memcpy(hf, ctx->pinned, sizeof(hf));
+          if (!hf[0].overflow && !hf[1].overflow) {
+            S.key_mode = 2;
+            if (split) fused_split = true;
+            else bf16_direct = true;
+            if (pat_ok) { pat_done = true; pat4 = true; }
+          } else {
+            CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
+            patA = patB = nullptr;
+          }
+        }
+        if (!bf16_direct && !fused_split) need_codes();
+      }
       // a value that is not bf16-representable (statistics flag) rules the direct fills out
-      if (nA <= cellsA && nB <= cellsB && !vals_inexact) {
+      if (!bf16_direct && !fused_split && nA <= cellsA && nB <= cellsB && !vals_inexact) {
         // optimistic: <= 1 tuple per cell and bf16-exact values -> the cells are the values
         // per side: binned (tile in shared memory, duplicate -> overflow) when the shape
         // fits, else scattered stores + occupancy bits whose popcount must equal the tuples
@@ -1132,7 +1255,12 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         if (!bf16_direct) CK(cudaMemsetAsync(fs, 0, sizeof(FillStats) * 2, s));
       }
     }
-    if (is_float && bf16_direct) {
+    if (is_float && fused_split) {
+      k_len = 4 * Kp;
+      S.elem = 2;
+      opA = reinterpret_cast<uint8_t*>(fA);
+      opB = reinterpret_cast<uint8_t*>(fB);
+    } else if (is_float && bf16_direct) {
       opA = reinterpret_cast<uint8_t*>(fA);
       opB = reinterpret_cast<uint8_t*>(fB);
     } else if (is_float && vals_inexact && !(q->flags & TCUDB_FORCE_WIDE) && nA <= cellsA && nB <= cellsB &&
@@ -1182,7 +1310,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       opA = reinterpret_cast<uint8_t*>(fA);
       opB = reinterpret_cast<uint8_t*>(fB);
     }
-    if (need_exist) {
+    if (need_exist && !pat_done) {
+      need_codes();
       // existence pattern (R3): 0/1 cells -> e2m1 operands (kind::mxf4, exact for K < 2^24,
       // half the operand bytes and twice the kind::i8 rate); u8 when e2m1 is off
       if (ctx->fp4 && !(q->flags & TCUDB_NO_FP4) && K < (1 << 24)) {

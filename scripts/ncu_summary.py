@@ -38,7 +38,10 @@ def main():
             d = dict(zip(hdr, row))
             u = dict(zip(hdr, units))
             lines.append(f"== {rep.split('/')[-1]} {d.get('Kernel Name', '')[:90]}")
-            for m in KEEP + sorted(k for k in d if "pipe_tensor" in k and k not in KEEP):
+            extra = sorted(k for k in d if k not in KEEP and ("pipe_tensor" in k or k.startswith(
+                "smsp__pcsamp_warps_issue_stalled_") or k in ("smsp__pcsamp_sample_count",
+                "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct")))
+            for m in KEEP + extra:
                 if m in d:
                     lines.append(f"   {m:<80s} {d[m]} {u.get(m, '')}")
     open(out, "w").write("\n".join(lines) + "\n")

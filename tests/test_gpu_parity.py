@@ -965,3 +965,53 @@ def test_hash_partition_pass_modes(engine, torch_mod, oracle_mod, monkeypatch, m
     out, st = run(engine, torch_mod, A, B, agg, 0)
     assert st["spa_mode"] == 4
     compare(out, ref, agg)
+
+
+# ---------------------------------------------------------------- a2 + a5 fused (fill_direct.cu)
+@pytest.mark.parametrize("case", ["dense_exact", "holes", "signed_exact", "signed_split", "dup", "dup_split",
+                                  "one_side_value", "ragged_kp"])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_fused_direct_fill(engine, torch_mod, oracle_mod, monkeypatch, case, flags):
+    """Deferred per-tuple codes (the c4 class, TCUDB_LAZY_CODES=1 lifts the size threshold):
+    the counting pass marks the direct dictionaries and counts per key, the fused fill looks
+    the codes up itself (key_mode 2) — bf16 cells, the hi/lo split for non-bf16 values, the
+    e2m1 existence pattern from the tiles' occupancy bits for signed values. Keys present on
+    one side only (∩ domain), group values with gaps, duplicate cells (-> the codes are
+    materialized and the scratch path runs), an absent value column, a K that is not a power
+    of two. Auto flags may pick the sparse path (codes materialized). All equal the oracle."""
+    monkeypatch.setenv("TCUDB_LAZY_CODES", "1")
+    rng = np.random.default_rng(["dense_exact", "holes", "signed_exact", "signed_split", "dup", "dup_split",
+                                 "one_side_value", "ragged_kp"].index(case) + 40)
+    G, K = 600, (1000 if case == "ragged_kp" else 1024)
+    cells = rng.permutation(G * K)
+    ag, ak = (cells // K).astype(np.int32), (cells % K).astype(np.int32)
+    exact = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, G * K).astype(np.float32))
+    av = exact
+    if case == "holes":       # groups 3g + 7, keys only on even codes + 100 (B covers a shifted range)
+        keep = ak % 2 == 0
+        ag, ak, av = 3 * ag[keep] + 7, ak[keep] + 100, av[keep]
+    elif case == "signed_exact":
+        av = (rng.integers(-16, 17, G * K) / 8).astype(np.float32)
+    elif case in ("signed_split", "dup_split"):
+        av = rng.standard_normal(G * K).astype(np.float32)
+    if case in ("dup", "dup_split"):
+        ag, ak, av = np.append(ag, ag[7]), np.append(ak, ak[7]), np.append(av, av[3])
+    H = 40
+    bk = np.tile(np.arange(K, dtype=np.int32), H)
+    bh = np.repeat(np.arange(H, dtype=np.int32) * 5, K).astype(np.int32)
+    if case == "holes":
+        bk = bk + 150
+    bw = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, H * K).astype(np.float32))
+    if case in ("signed_exact", "signed_split"):
+        bw = -bw
+    perm = rng.permutation(len(bk))
+    A = datagen.Table(ak.astype(np.int32), ag.astype(np.int32), av)
+    B = datagen.Table(bk[perm].astype(np.int32), bh[perm], None if case == "one_side_value" else bw[perm])
+    ref = oracle_mod.join_agg(A, B, "sum")
+    out, st = run(engine, torch_mod, A, B, "sum", flags)
+    compare(out, ref, "sum", float_vals=True)
+    if flags == 1:
+        assert st["path"] == 0
+        assert st["key_mode"] == (0 if case.startswith("dup") else 2), st["key_mode"]
+        if case in ("signed_split",):
+            assert st["elem"] == 2 and st["existence"] == 1
