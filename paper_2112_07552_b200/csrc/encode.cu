@@ -279,6 +279,104 @@ __global__ void k_hash_insert(ColDesc c, long long minv, unsigned long long* __r
   }
 }
 
+// Small int32 domains, dictionary only (no per-row slots; c5's group columns: 16.7 M values
+// over 4,096 distinct): a sparse block-local set of 32-bit offsets (32,768 slots, stored as
+// offset + 1, 0 = empty; load <= 1/8 for the <= 4 K keys a block may hold, so the longest
+// probe among a warp's 32 lanes stays short — the linear-probing divergence of a half-full
+// table cost ~150 instructions per tuple), 16-byte vector loads four in flight, then the
+// block's distinct keys into the global table (same slots and flags as k_hash_insert).
+constexpr int kSdThreads = 1024;
+constexpr int kSdBits = 15;
+__global__ void __launch_bounds__(kSdThreads) k_small_distinct(ColDesc c, long long minv,
+                                                               unsigned long long* __restrict__ slots,
+                                                               unsigned long long mask, uint8_t* __restrict__ flags,
+                                                               int* __restrict__ overflow, int64_t chunk,
+                                                               int64_t step) {
+  extern __shared__ uint32_t s_set[];
+  constexpr int TS = 1 << kSdBits;
+  __shared__ int s_n, s_top;
+  for (int i = threadIdx.x; i < TS; i += kSdThreads) s_set[i] = 0u;
+  if (threadIdx.x == 0) { s_n = 0; s_top = 0; }
+  __syncthreads();
+  const uint32_t mn = (uint32_t)minv;
+  auto ins = [&](int x) {
+    const uint32_t k1 = ((uint32_t)x - mn) + 1u;  // offset + 1; offset 2^32 - 1 is kept aside
+    if (k1 == 0u) { s_top = 1; return; }
+    uint32_t h = (k1 * 0x9E3779B1u) >> (32 - kSdBits);
+    while (true) {
+      const uint32_t cur = s_set[h];
+      if (cur == k1) return;
+      if (cur == 0u) {
+        const uint32_t prev = atomicCAS(s_set + h, 0u, k1);
+        if (prev == 0u) { atomicAdd(&s_n, 1); return; }
+        if (prev == k1) return;
+      }
+      h = (h + 1) & (TS - 1);
+    }
+  };
+  const int32_t* col = static_cast<const int32_t*>(c.data);
+  if (step > 1) {
+    // sample: tuples 0, step, 2 step, ... (the caller checks every tuple against the result)
+    const int64_t m = (c.n + step - 1) / step;
+    const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(m, lo + chunk);
+    constexpr int U = 8;
+    // warp-uniform trip counts: the __syncwarp below needs every lane of the warp
+    for (int64_t jw = lo + (threadIdx.x & ~31); jw < hi; jw += U * kSdThreads) {
+      const int64_t j0 = jw + lane_id();
+      int x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = j0 + u * kSdThreads < hi ? __ldcs(col + (j0 + u * kSdThreads) * step) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (j0 + u * kSdThreads < hi) ins(x[u]);
+        __syncwarp();
+      }
+    }
+  }
+  const int64_t lo = step > 1 ? 0 : (int64_t)blockIdx.x * chunk, hi = step > 1 ? 0 : min(c.n, lo + chunk);  // chunk % 4 == 0
+  const int4* c4 = reinterpret_cast<const int4*>(c.data);
+  const int64_t v_lo = lo >> 2, v_hi = hi >> 2;
+  constexpr int U = 4;
+  for (int64_t vw = v_lo + (threadIdx.x & ~31); vw < v_hi; vw += U * kSdThreads) {  // warp-uniform trips
+    const int64_t v0 = vw + lane_id();
+    int4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = v0 + u * kSdThreads < v_hi ? __ldcs(c4 + v0 + u * kSdThreads) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (v0 + u * kSdThreads < v_hi) { ins(x[u].x); ins(x[u].y); ins(x[u].z); ins(x[u].w); }
+      // reconverge: lanes leaving the probe loops at different steps otherwise run the
+      // following iterations in separate groups (measured ~11 of 32 lanes active)
+      __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, s_n > TS / 4)) break;  // > 8 K distinct values in a block: the caller rebuilds by n
+  }
+  for (int64_t i = (v_hi << 2) + threadIdx.x; i < hi; i += kSdThreads) ins(col[i]);
+  __syncthreads();
+  if (s_n > TS / 4) {
+    if (threadIdx.x == 0) *overflow = 1;
+    return;
+  }
+  for (int sidx = threadIdx.x; sidx <= TS; sidx += kSdThreads) {
+    const uint32_t k1 = sidx < TS ? s_set[sidx] : (s_top ? 0u : 1u);  // sidx == TS: offset 2^32 - 1
+    if (sidx < TS ? !k1 : k1) continue;
+    const unsigned long long off = (unsigned long long)(uint32_t)(k1 - 1u);
+    unsigned long long hh = slot_hash(off, 0) & mask;
+    int32_t placed = -1;
+    for (unsigned long long step = 0; step <= mask; ++step) {
+      const unsigned long long cc = __ldcg(slots + hh);
+      if (cc == off) { placed = (int32_t)hh; break; }
+      if (cc == ~0ull) {
+        const unsigned long long prev = atomicCAS(slots + hh, ~0ull, off);
+        if (prev == ~0ull || prev == off) { placed = (int32_t)hh; break; }
+      }
+      hh = (hh + 1) & mask;
+    }
+    if (placed < 0) *overflow = 1;
+    else if (!flags[placed]) flags[placed] = 1;
+  }
+}
+
 // Small domains with many tuples per value (c5: 16.7 M group values over 4,096
 // distinct): every tuple of k_hash_insert reads a slot of a tiny global table, and
 // those L2 requests (not bytes) bound it. Here each block first de-duplicates its
@@ -314,7 +412,32 @@ __global__ void __launch_bounds__(1024) k_hash_insert_smem(ColDesc c, long long 
     }
     return -1;
   };
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+  int64_t i_tail = lo;
+  if (c.type == 0 && !(reinterpret_cast<uintptr_t>(c.data) & 15) && !(lo & 3)) {
+    // int32 column: 16-byte vectors, four in flight per thread (one scalar load at a time
+    // kept ~1 K loads in flight per SM: latency-bound at ~0.6 TB/s)
+    const int4* c4 = reinterpret_cast<const int4*>(c.data);
+    const int64_t v_lo = lo >> 2, v_hi = hi >> 2;
+    constexpr int U = 4;
+    for (int64_t vw = v_lo + (threadIdx.x & ~31); vw < v_hi; vw += U * blockDim.x) {  // warp-uniform trips
+      const int64_t v0 = vw + lane_id();
+      int4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = v0 + u * blockDim.x < v_hi ? __ldcs(c4 + v0 + u * blockDim.x) : make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (v0 + u * blockDim.x < v_hi) {
+          const int xs[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (sfind((unsigned long long)(long long)xs[q] - (unsigned long long)minv, true) < 0) s_bad = 1;
+        }
+        __syncwarp();  // reconverge after the probe loops
+      }
+    }
+    i_tail = v_hi << 2;
+  }
+  for (int64_t i = i_tail + threadIdx.x; i < hi; i += blockDim.x) {
     const unsigned long long off = (unsigned long long)ld_int(c.data, c.type, i) - (unsigned long long)minv;
     if (sfind(off, true) < 0) s_bad = 1;
   }
@@ -718,8 +841,64 @@ __global__ void k_probe(ColDesc key, ColDesc grp, ColDesc val, DictView kd, Dict
   }
 }
 
+// Group codes from a small finished hash dictionary (<= 16 K slots, offsets of 32 bits, int32
+// column): each CTA copies the slots (as 32-bit offsets) and their codes into shared memory
+// and maps 16-byte vectors of the column (a global-table probe per tuple was L2-latency-bound).
+constexpr int kGcThreads = 1024;
+constexpr int kGcMaxCap = 16384;
+constexpr int kGcBits = 14;  // 16,384 shared slots: load <= 1/4 for <= 4 K groups
+__global__ void __launch_bounds__(kGcThreads) k_group_codes_smem(ColDesc grp, DictView gd, int32_t* __restrict__ gcode,
+                                                                 int* __restrict__ miss) {
+  extern __shared__ __align__(16) unsigned long long s_gt[];  // (offset << 32 | code), ~0 = empty
+  constexpr int TS = 1 << kGcBits;
+  for (int i = threadIdx.x; i < TS; i += kGcThreads) s_gt[i] = ~0ull;
+  __syncthreads();
+  auto sh = [](uint32_t off) { return (off * 0x9E3779B1u) >> (32 - kGcBits); };
+  const int cap = (int)gd.size + 1;  // hash mode: size = mask
+  for (int i = threadIdx.x; i < cap; i += kGcThreads) {
+    const unsigned long long k = __ldg(gd.slots + i);
+    if (k == ~0ull) continue;
+    const unsigned long long w = (k << 32) | (uint32_t)__ldg(gd.code + i);
+    uint32_t h = sh((uint32_t)k);
+    while (atomicCAS(s_gt + h, ~0ull, w) != ~0ull) h = (h + 1) & (TS - 1);
+  }
+  __syncthreads();
+  const unsigned mn = (unsigned)gd.minv;
+  int missed = 0;
+  auto look = [&](int x) -> int32_t {
+    const uint32_t off = (uint32_t)x - mn;
+    uint32_t h = sh(off);
+    while (true) {
+      const unsigned long long w = s_gt[h];
+      if ((uint32_t)(w >> 32) == off && w != ~0ull) return (int32_t)(uint32_t)w;
+      if (w == ~0ull) { missed = 1; return -1; }
+      h = (h + 1) & (TS - 1);
+    }
+  };
+  const int64_t nv = grp.n / 4;
+  const int4* g4 = reinterpret_cast<const int4*>(grp.data);
+  int4* o4 = reinterpret_cast<int4*>(gcode);
+  const int64_t stride = (int64_t)gridDim.x * kGcThreads;
+  constexpr int U = 4;
+  for (int64_t vw = (int64_t)blockIdx.x * kGcThreads + (threadIdx.x & ~31); vw < nv; vw += U * stride) {  // warp-uniform
+    const int64_t v0 = vw + lane_id();
+    int4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = v0 + u * stride < nv ? __ldcs(g4 + v0 + u * stride) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (v0 + u * stride < nv) __stcg(o4 + v0 + u * stride, make_int4(look(x[u].x), look(x[u].y), look(x[u].z), look(x[u].w)));
+      __syncwarp();  // reconverge after the probe loops
+    }
+  }
+  for (int64_t i = nv * 4 + (int64_t)blockIdx.x * kGcThreads + threadIdx.x; i < grp.n; i += stride)
+    gcode[i] = look(static_cast<const int32_t*>(grp.data)[i]);
+  if (miss && __any_sync(0xffffffffu, missed) && lane_id() == 0) atomicOr(miss, 1);
+}
+
 // Group codes only (the hash-partitioned sparse path encodes the join key itself).
-__global__ void k_group_codes(ColDesc grp, DictView gd, int32_t* __restrict__ gcode) {
+__global__ void k_group_codes(ColDesc grp, DictView gd, int32_t* __restrict__ gcode, int* __restrict__ miss) {
+  int missed = 0;
   constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * T;
   for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < grp.n; i0 += U * stride) {
@@ -735,8 +914,9 @@ __global__ void k_group_codes(ColDesc grp, DictView gd, int32_t* __restrict__ gc
     rows_lookup<U>(gd, x, ok, i0, stride, c);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (ok[u]) gcode[i0 + u * stride] = c[u];
+      if (ok[u]) { gcode[i0 + u * stride] = c[u]; missed |= c[u] < 0; }
   }
+  if (miss && missed) atomicOr(miss, 1);
 }
 
 // J = sum_k cntA[k] * cntB[k] (join size, a4) and max per-key counts.
@@ -837,20 +1017,40 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
   return cudaGetLastError();
 }
 
+
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
                                uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, int wide,
-                               cudaStream_t s, int64_t* launches) {
+                               cudaStream_t s, int64_t* launches, int64_t sample_step) {
   if (c.n <= 0) return cudaSuccess;
   // shared-memory pre-aggregation when the estimated distinct count is small and
   // there are many tuples per distinct value (tables sized 2^ceil(log2(1.9 est)))
   const int64_t cap = (int64_t)mask + 1;
+  if (est_distinct > 0 && cap <= 16384 && c.n >= 64 * cap && !row_slot && !wide && c.type == 0 &&
+      !(reinterpret_cast<uintptr_t>(c.data) & 15)) {
+    constexpr int smem = (1 << kSdBits) * 4;
+    cudaError_t e = set_func_attr(k_small_distinct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    // one block per SM (TCUDB_SD_BLOCKS overrides: experiments)
+    // every block ends by inserting each distinct key it saw into the global table (all of a
+    // small domain's keys, typically; those few L2 lines serialize the merges): sampled builds
+    // use 16 blocks (measured 2 / 4 / 8 / 16 on c5's groups: 213 / 140 / 103 / 95 us)
+    static const int env_nb = getenv("TCUDB_SD_BLOCKS") ? atoi(getenv("TCUDB_SD_BLOCKS")) : 0;
+    const int64_t step = sample_step > 1 ? sample_step : 1;
+    const int64_t m = (c.n + step - 1) / step;
+    const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(env_nb > 0 ? env_nb : (step > 1 ? 16 : kNumSMs),
+                                                                (m + 16383) / 16384));
+    const int64_t chunk = ((m + nblk - 1) / nblk + 3) & ~int64_t(3);
+    k_small_distinct<<<(int)nblk, kSdThreads, smem, s>>>(c, minv, slots, mask, flags, overflow, chunk, step);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   if (est_distinct > 0 && cap <= 16384 && c.n >= 64 * cap) {
     const int cap_s = (int)cap;  // >= 1.9 x the global distinct count, so >= any block's
     const size_t smem = (size_t)cap_s * 12;
     set_func_attr(k_hash_insert_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 12);
     const int per_sm = smem <= 96 * 1024 ? 2 : 1;
     const int64_t nblk = std::min<int64_t>(per_sm * kNumSMs, (c.n + 32767) / 32768);
-    const int64_t chunk = (c.n + nblk - 1) / nblk;
+    const int64_t chunk = ((c.n + nblk - 1) / nblk + 3) & ~int64_t(3);  // 16-byte aligned chunks
     k_hash_insert_smem<<<(int)nblk, 1024, smem, s>>>(c, minv, slots, mask, flags, overflow, row_slot, cap_s, chunk,
                                                       wide);
     if (launches) ++*launches;
@@ -974,9 +1174,22 @@ cudaError_t launch_probe(const ColDesc& key, const ColDesc& grp, const ColDesc& 
 }
 
 cudaError_t launch_group_codes(const ColDesc& grp, const DictView& gd, int32_t* gcode, cudaStream_t s,
-                               int64_t* launches) {
+                               int64_t* launches, int* miss) {
   if (grp.n <= 0) return cudaSuccess;
-  k_group_codes<<<grid_for(grp.n), T, 0, s>>>(grp, gd, gcode);
+  if (gd.mode == 1 && !gd.wide && !gd.row_slot && grp.type == 0 && gd.size + 1 <= (unsigned long long)kGcMaxCap &&
+      gd.size + 1 <= (1ull << kGcBits) / 2 &&
+      !(reinterpret_cast<uintptr_t>(grp.data) & 15) && !(reinterpret_cast<uintptr_t>(gcode) & 15) &&
+      grp.n >= 64 * (int64_t)(gd.size + 1)) {
+    const int smem = (1 << kGcBits) * 8;
+    cudaError_t e = set_func_attr(k_group_codes_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const int per_sm = smem <= 100 * 1024 ? 2 : 1;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * kNumSMs, grp.n / 16384));
+    k_group_codes_smem<<<(int)blocks, kGcThreads, smem, s>>>(grp, gd, gcode, miss);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
+  k_group_codes<<<grid_for(grp.n), T, 0, s>>>(grp, gd, gcode, miss);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -28,8 +28,9 @@
 namespace tcudb {
 namespace {
 
-constexpr int PT = 512;        // threads per partitioning block (4 CTAs per SM)
-constexpr int CH = 4 * PT;     // tuples per partitioning chunk
+constexpr int PT = 512;        // threads per partitioning block (2 CTAs per SM)
+constexpr int PER = 8;         // tuples per thread and chunk
+constexpr int CH = PER * PT;   // tuples per partitioning chunk
 constexpr int kMaxDigits = 128;
 
 TCUDB_DEV unsigned long long mix64(unsigned long long k) {
@@ -129,14 +130,15 @@ __global__ void __launch_bounds__(PT) k_part_hist(const PassIO io) {
   }
 #pragma unroll
   for (int u = 0; u < CH / PT; ++u)
-    if (lo + threadIdx.x + (int64_t)u * PT < hi) atomicAdd(&h[(int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1))], 1);
+    if (lo + threadIdx.x + (int64_t)u * PT < hi)
+      atomicAdd(&h[(int)(((io.raw ? mix64(k[u]) : k[u]) >> io.shift) & (unsigned)(R - 1))], 1);
   __syncthreads();
   const int64_t base = io.chunk_start[s] * R;
   for (int d = threadIdx.x; d < R; d += PT) io.counts[base + (int64_t)d * nch + j] = h[d];
 }
 
 template <bool VAL>
-__global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io) {  // 2,048 threads per SM
+__global__ void __launch_bounds__(PT, 2) k_part_scatter(const PassIO io) {  // 2,048 threads per SM
   extern __shared__ __align__(16) uint8_t stage_raw[];
   unsigned long long* sk = reinterpret_cast<unsigned long long*>(stage_raw);  // [CH]
   int32_t* sg = reinterpret_cast<int32_t*>(sk + CH);                          // [CH]
@@ -157,24 +159,34 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
   }
   __syncthreads();
   const int64_t lo = io.seg_off[s] + j * CH, hi = min(io.seg_off[s + 1], lo + CH);
-  unsigned long long k[4];
-  int32_t g[4];
-  long long v[4];
-  int d[4], r[4];
+  unsigned long long k[PER];
+  int32_t g[PER];
+  long long v[PER];
+  int d[PER], r[PER];
+  // the chunk's loads first (all four per thread in flight), then the digits and ranks
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < PER; ++u) {
     const int64_t i = lo + threadIdx.x + u * PT;
-    d[u] = -1;
+    k[u] = 0; g[u] = 0;
     if (i < hi) {
       if (io.raw) {
         k[u] = (unsigned long long)ld_int(io.raw, io.raw_type, i) - (unsigned long long)io.kmin;
-        g[u] = io.g_raw[i];
+        g[u] = __ldcs(io.g_raw + i);
       } else {
-        k[u] = io.k_in[i];
-        g[u] = io.g_in[i];
+        k[u] = __ldcs(io.k_in + i);
+        g[u] = __ldcs(io.g_in + i);
       }
       if (VAL) v[u] = load_value(io, i);
-      d[u] = (int)((mix64(k[u]) >> io.shift) & (unsigned)(R - 1));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    d[u] = -1;
+    if (lo + threadIdx.x + u * PT < hi) {
+      // pass 1 replaces the key offset by its hash (a bijection: equal keys <=> equal
+      // hashes), so later passes and the per-partition tables never rehash
+      if (io.raw) k[u] = mix64(k[u]);
+      d[u] = (int)((k[u] >> io.shift) & (unsigned)(R - 1));
       r[u] = atomicAdd(&cnt[d[u]], 1);
     }
   }
@@ -207,7 +219,7 @@ __global__ void __launch_bounds__(PT, 2048 / PT) k_part_scatter(const PassIO io)
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < PER; ++u)
     if (d[u] >= 0) {
       const int p = lstart[d[u]] + r[u];
       sk[p] = k[u];
@@ -653,9 +665,9 @@ cudaError_t launch_part_expand(const unsigned long long* ka, const int32_t* ga, 
                                const long long* vb, unsigned long long* C64, unsigned long long* jk) {
   const int tb = ts_bits_for(cap);
   const size_t smem = part_expand_smem(cap, C64 != nullptr);
-  set_func_attr(k_part_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  set_func_attr(k_part_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  set_func_attr(k_part_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 186 * 1024);
+  set_func_attr(k_part_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 186 * 1024);
+  if (smem > 186 * 1024) return cudaErrorInvalidValue;
   // jk: 4 + 4 P entries (per-partition J_p, K_p after the 4 totals, summed below)
   if (C64) k_part_expand<true><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64, jk + 4);
   else k_part_expand<false><<<P, QTE, smem, s>>>(ka, ga, offa, kb, hb, offb, tb, cap, C, ldc, va, vb, C64, jk + 4);

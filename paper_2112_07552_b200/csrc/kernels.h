@@ -54,7 +54,7 @@ cudaError_t launch_mark_direct(const ColDesc& c, long long minv, uint8_t* flags,
 // (optional, c.n entries) receives each row's slot.
 cudaError_t launch_hash_insert(const ColDesc& c, long long minv, unsigned long long* slots, unsigned long long mask,
                                uint8_t* flags, int* overflow, int32_t* row_slot, double est_distinct, int wide,
-                               cudaStream_t s, int64_t* launches);
+                               cudaStream_t s, int64_t* launches, int64_t sample_step = 1);
 size_t pred_temp_bytes(int64_t n);
 // codes = exclusive scan of pred(i) (-1 where false); optional dict[code] = minv + i (direct
 // group domains: the sorted value dictionary comes out of the same pass).
@@ -265,8 +265,10 @@ cudaError_t launch_spa_count(const SpaArgs& a, cudaStream_t s, int64_t* launches
 cudaError_t launch_spa_write(const SpaArgs& a, cudaStream_t s, int64_t* launches);
 
 // gcode[i] = code of grp[i] in the dictionary gd (final codes)
+// per-tuple group codes; miss (optional): set when a value is not in the dictionary (a sampled
+// build missed it: the caller rebuilds)
 cudaError_t launch_group_codes(const ColDesc& grp, const DictView& gd, int32_t* gcode, cudaStream_t s,
-                               int64_t* launches);
+                               int64_t* launches, int* miss = nullptr);
 
 // ---------------------------------------------------------------- hashpart.cu (a2 + a7, partitioned)
 // Hash-partitioned sparse COUNT for large hash-mode key domains: both tables are

@@ -205,7 +205,8 @@ void dict_direct_codes(Arena& ar, Dict& d, unsigned long long* union_dev, int64_
 // est_distinct (> 0) sizes the hash table: 2^ceil(log2(1.9 x estimate)), never above 2n
 // (load <= ~0.53; c5's 4.2 M keys fit 2^23 slots = 64 MB, L2-resident).
 void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long long mn, long long mx, bool intersect,
-                unsigned long long* union_dev, int64_t* launches, double est_distinct = 0, bool row_slots = true) {
+                unsigned long long* union_dev, int64_t* launches, double est_distinct = 0, bool row_slots = true,
+                int64_t sample_step = 1) {
   cudaStream_t s = ar.s;
   const int64_t n = c1.n + (c2 ? c2->n : 0);
   const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
@@ -237,7 +238,8 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.ovf = ar.zeros<int>(1);
     // per-row slots: the probe then reads code[slot] instead of rehashing and walking the table
     d.slot1 = row_slots ? ar.get<int32_t>(c1.n) : nullptr;
-    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, d.wide, s, launches));
+    CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, d.wide, s, launches,
+                          c2 ? 1 : sample_step));
     if (c2) {
       d.slot2 = ar.get<int32_t>(c2->n);
       if (intersect) {
@@ -363,9 +365,15 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
                     bool timed, bool sum, const ColDesc& av, const ColDesc& bw) {
   const int64_t nA = ak.n, nB = bk.n;
   Dict DG, DH;
-  // group dictionaries only (no per-row slots: one read of each group column)
-  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false);
-  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], false);
+  // group dictionaries only (no per-row slots). Small domains over many tuples are built from
+  // a strided sample of ~256 K values (c5: 64 occurrences of each of 4,096 values expected in
+  // it); every tuple is then looked up by the code pass, and a value the sample missed sends
+  // the query to the general path (checked with the partition sizes below)
+  auto step_for = [](int64_t n) -> int64_t { return n >= (1 << 22) ? n >> 18 : 1; };
+  const char* ns_env = getenv("TCUDB_NO_DICT_SAMPLE");
+  const bool sample = !(ns_env && ns_env[0] == '1');
+  dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false, sample ? step_for(nA) : 1);
+  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], false, sample ? step_for(nB) : 1);
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
     int* hov = reinterpret_cast<int*>(hp + 2);
@@ -388,8 +396,10 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   // latency-bound scatter; here four lookups per thread are in flight)
   int32_t* gA = ar.get<int32_t>(nA);
   int32_t* hB = ar.get<int32_t>(nB);
-  CK(launch_group_codes(ag, DG.view(), gA, s, L));
-  CK(launch_group_codes(bh, DH.view(), hB, s, L));
+  unsigned long long* d_max_miss = ar.zeros<unsigned long long>(2);  // [0] largest partition, [1] missed value
+  int* d_miss = reinterpret_cast<int*>(d_max_miss + 1);
+  CK(launch_group_codes(ag, DG.view(), gA, s, L, d_miss));
+  CK(launch_group_codes(bh, DH.view(), hB, s, L, d_miss));
   const int32_t* grp[2] = {gA, hB};
   // partitions: <= ~1 K tuples per side on average, two radix passes of <= 7 bits
   int pbits = 1;
@@ -456,10 +466,15 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   }
   const int fin = b2 ? 1 : 0;
   unsigned long long* d_out = ar.zeros<unsigned long long>(4 + 4 * (int64_t)P);
-  unsigned long long* d_max = ar.zeros<unsigned long long>(1);
+  unsigned long long* d_max = d_max_miss;
   CK(launch_part_max(sd[0].seg2, sd[1].seg2, P, d_max, s, L));
-  const int64_t cap = (int64_t)*to_pinned<unsigned long long>(ctx, d_max, s);
-  if (cap <= 0 || part_expand_smem((int)std::min<int64_t>(cap, 1 << 20), sum) > 200 * 1024) return false;
+  CK(cudaMemcpyAsync(ctx->pinned, d_max_miss, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  unsigned long long hmm[2];
+  std::memcpy(hmm, ctx->pinned, 16);
+  if (hmm[1]) return false;  // a group value outside the sampled dictionary: the general path
+  const int64_t cap = (int64_t)hmm[0];
+  if (cap <= 0 || part_expand_smem((int)std::min<int64_t>(cap, 1 << 20), sum) > 186 * 1024) return false;
   // a4 selector on the join size J = sum_k cntA(k)·cntB(k). With many partitions a sample of
   // them (every 16th: keys are hashed, so each holds an unbiased 1/P of the key domain) gives
   // the estimate; the exact J and K come out of the expand itself. A close call, or a J near

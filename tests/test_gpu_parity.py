@@ -1015,3 +1015,35 @@ def test_fused_direct_fill(engine, torch_mod, oracle_mod, monkeypatch, case, fla
         assert st["key_mode"] == (0 if case.startswith("dup") else 2), st["key_mode"]
         if case in ("signed_split",):
             assert st["elem"] == 2 and st["existence"] == 1
+
+
+@pytest.mark.parametrize("case", ["complete", "rare_value_a", "rare_value_b"])
+def test_hash_partitioned_sampled_group_dictionary(engine, torch_mod, oracle_mod, monkeypatch, case):
+    """Small group domains over >= 2^22 tuples are built from a strided sample (every
+    n/2^18-th value); every tuple is looked up afterwards and a value the sample missed sends
+    the query to the general path. A value that occurs once, off the sample grid, on either
+    side: the result still equals the oracle (and the hash-partitioned plan is not taken)."""
+    rng = np.random.default_rng(77)
+    n = 1 << 22
+    pool_a, pool_b = datagen._pool(rng, 1500), datagen._pool(rng, 900)
+    ga = pool_a[rng.integers(0, len(pool_a), n)]
+    hb = pool_b[rng.integers(0, len(pool_b), n)]
+    ka = datagen.scramble(rng.integers(0, 1 << 21, n, dtype=np.int64).astype(np.uint64))
+    kb = datagen.scramble(rng.integers(0, 1 << 21, n, dtype=np.int64).astype(np.uint64))
+    rare = np.int32(123456789)
+    assert rare not in pool_a and rare not in pool_b
+    if case == "rare_value_a":
+        ga[12345] = rare   # 12345 is not a multiple of the sample step (16)
+        kb[7] = ka[12345]  # ... and it joins
+    elif case == "rare_value_b":
+        hb[54321] = rare
+        ka[9] = kb[54321]
+    A, B = datagen.Table(ka, ga), datagen.Table(kb, hb)
+    ref = oracle_mod.join_agg(A, B, "count")
+    monkeypatch.setenv("TCUDB_FORCE_HASHPART", "1")
+    out, st = run(engine, torch_mod, A, B, "count", 0)
+    compare(out, ref, "count")
+    if case == "complete":
+        assert st["spa_mode"] == 4
+    else:
+        assert st["spa_mode"] != 4
