@@ -19,7 +19,8 @@ LIB = os.path.join(HERE, "libtcudb.so")
 OBJDIR = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC] + \
+    os.environ.get("TCUDB_NVCC_EXTRA", "").split()  # experiments: -D knobs
 
 
 def _sources():

@@ -26,6 +26,14 @@ constexpr int A_STAGE_BYTES = BM * BKB;  // 16 KB
 constexpr int NUM_THREADS = 192;         // 6 warps
 constexpr int TMEM_COLS = 512;           // 2 accumulators x 256 fp32/s32 columns (fp4: 2 x 240 + scales)
 constexpr int GROUP_M = 16;              // tile raster: 16 M-blocks per band
+#ifndef TCUDB_CMP_WARPS
+#define TCUDB_CMP_WARPS 8
+#endif
+#ifndef TCUDB_CMP_GROUP_M
+#define TCUDB_CMP_GROUP_M 2
+#endif
+constexpr int kCmpWarps = TCUDB_CMP_WARPS;
+constexpr int kCmpGroupM = TCUDB_CMP_GROUP_M;
 
 // Per-BN kernel geometry (BN = 256 for kind::i8 / kind::f16, 240 for kind::mxf4 so
 // that two accumulators plus the block-scale columns fit the 512 TMEM columns).
@@ -260,7 +268,7 @@ __device__ __forceinline__ int epilogue_rows(const KParams& p, uint32_t taddr, i
 //     over the AGG / INC states (every AGG comes from an epilogue warp, so the wait ends).
 //     A row's tuples in the tile go to P(mb) + rowbase[row] + tcnt[nb][row], in column
 //     order: the output is (g, h)-sorted exactly as the separate compaction kernel's.
-constexpr int CMP_WARPS = 4;
+constexpr int CMP_WARPS = kCmpWarps;  // groups of 4 (TCUDB build-time knob)
 constexpr unsigned long long kMbAgg = 1ull << 62, kMbInc = 2ull << 62, kMbVal = (1ull << 62) - 1;
 
 __device__ __noinline__ void mblock_finish(const KParams& p, int mb) {
@@ -520,11 +528,12 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
       if (lane == 0 && tri != 0) atomicAdd(p.tri_out, (unsigned long long)tri);
     }
   } else if (CMP) {
-    // ===================== compaction warps 6..9 =====================
-    const int cw = warp - 6;
+    // ===================== compaction warps 6.. (groups of 4, one tile each in turn) =====
+    const int cw = (warp - 6) & 3, grp = (warp - 6) >> 2;
+    constexpr int NG = CMP_WARPS / 4;
     int cached_mb = -1;
     int64_t P = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x + grp * gridDim.x; t < num_tiles; t += NG * gridDim.x) {
       int mb, nb; tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, mb, nb);
       if (mb != cached_mb) {
         int64_t v = 0;
@@ -783,7 +792,7 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   if (a.cmp) {
     // M-blocks must complete early for their compaction to overlap later tiles: bands of
     // 2 M-blocks (measured best of 1..40 on c2)
-    if (!getenv("TCUDB_GEMM_GROUP_M")) p.group_m = p.tiles_m < 2 ? p.tiles_m : 2;
+    if (!getenv("TCUDB_GEMM_GROUP_M")) p.group_m = p.tiles_m < kCmpGroupM ? p.tiles_m : kCmpGroupM;
     p.fc = *static_cast<const FusedCompact*>(a.cmp);
     p.cnt_out = p.fc.tcnt;  // non-null: the epilogue counts nonzeros (stored as tcnt[nb][row])
     return run_1cta<BNF, true, true>(a, p, ELEM_I8, kb, s, launches);
