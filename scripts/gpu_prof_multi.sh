@@ -9,7 +9,7 @@ python __graft_entry__.py > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.
 for spec in "$@"; do
   IFS=: read c re n <<< "$spec"
   tag=$(echo "$re" | tr -c 'a-zA-Z0-9_\n' '_')
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$re" -c ${n:-1} \
+  timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"$re" -c ${n:-1} \
      -o gpurun_out/prof_${c}_${tag} -f python bench.py --config $c --also "" --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 \
      > gpurun_out/ncu_${c}_${tag}.log 2>&1
   tail -2 gpurun_out/ncu_${c}_${tag}.log

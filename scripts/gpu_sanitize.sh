@@ -6,7 +6,7 @@ export TCUDB_CALIBRATE=0   # keep the sanitized runs small (the calibration is c
 for tool in memcheck racecheck synccheck; do
   extra=""
   [ $tool = memcheck ] && extra="--leak-check no"
-  timeout 2400 compute-sanitizer --tool $tool $extra --error-exitcode 9 --print-limit 50 \
+  timeout -s KILL 1500 compute-sanitizer --tool $tool $extra --error-exitcode 9 --print-limit 50 \
       python scripts/sanitize_cases.py quick > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool rc=$?"; grep -E "ERROR SUMMARY|SANITIZE_CASES_OK|RACECHECK SUMMARY" gpurun_out/sanitize_$tool.log | tail -3
 done

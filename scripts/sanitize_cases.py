@@ -4,7 +4,7 @@ usage: compute-sanitizer --tool <tool> python scripts/sanitize_cases.py [quick]
 Covers: c1 / c1s (COUNT, SUM, AVG, Q3, Q4) on the selector's path and forced dense /
 sparse, the wide (int64 scratch) path, e2m1 forced on small products, the band-SPA
 schedules (one pass, count + write), the hash-partitioned path, float SUM (bf16 direct,
-hi/lo split), random tiny instances, triangles (both paths), the chain join and the
+hi/lo split; the fused direct fill), sampled group dictionaries, random tiny instances, triangles (both paths), the chain join and the
 a6 GEMM kinds. Every result is checked against the oracle (test infrastructure).
 """
 import os
@@ -68,6 +68,13 @@ check(A, B, agg, 0, float_vals=True)
 check(A, B, agg, 2, float_vals=True)
 A, B, agg = datagen.make_config("c4", 1 / 4096)
 check(A, B, agg, 0, float_vals=True)
+# a2 + a5 fused (deferred codes, fill_direct.cu): bf16 cells, hi/lo split + e2m1 pattern
+check(A, B, agg, 1, {"TCUDB_LAZY_CODES": "1"}, float_vals=True)
+A, B, agg = datagen.make_config("c4s", 1 / 4096)
+check(A, B, agg, 1, {"TCUDB_LAZY_CODES": "1"}, float_vals=True)
+# sampled group dictionaries + shared-memory code lookup (hash-partitioned path, 2^22 tuples)
+A, B, agg = datagen.make_config("c5", 1 / 4)
+check(A, B, agg, 0, {"TCUDB_FORCE_HASHPART": "1"})
 rng = np.random.default_rng(7)
 for i in range(6 if quick else 24):
     vk = ("none", "int", "float")[i % 3]
