@@ -104,7 +104,7 @@ typedef struct {
  * on the query stream; ms_total is host wall clock of the whole call. */
 typedef struct {
   int32_t path;       /* 0 dense (tensor cores), 1 sparse expand */
-  int32_t elem;       /* dense operand type: 0 u8/s8 (kind::i8), 1 bf16, 2 bf16 hi/lo split (4 products),
+  int32_t elem;       /* dense operand type: 0 u8/s8 (kind::i8), 1 bf16, 2 bf16 hi/mid/lo split (6 products),
                          3 e2m1 0/1 COUNT operands (kind::mxf4, unit scales) */
   int32_t planes_a;   /* base-256 digit planes of A_op (int SUM) */
   int32_t planes_b;

@@ -221,6 +221,42 @@ TCUDB_DEV uint64_t policy_evict_first() {
   return p;
 }
 
+// ------------------------------------------------------------------ bf16 three-way split
+// 8 consecutive fp32 cells -> bf16 hi / mid / lo (RNE, reading R8/R9) stored as 16-byte vectors
+// into every K segment (stride seg_stride elements) by its 2-bit role (kernels.h kRoles*).
+TCUDB_DEV uint16_t bf16_rn_bits(float x) {
+  uint16_t b;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(b) : "f"(x));
+  return b;
+}
+TCUDB_DEV float bf16_bits_val(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+template <bool STREAM>
+TCUDB_DEV void store_split8(uint16_t* row, int64_t seg_stride, const float* x, int roles, int nsegs) {
+  uint32_t w[3][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint16_t p[3][2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float v = x[2 * j + e];
+      p[0][e] = bf16_rn_bits(v);
+      const float r1 = v - bf16_bits_val(p[0][e]);
+      p[1][e] = bf16_rn_bits(r1);
+      p[2][e] = bf16_rn_bits(r1 - bf16_bits_val(p[1][e]));
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) w[q][j] = (uint32_t)p[q][0] | ((uint32_t)p[q][1] << 16);
+  }
+  for (int sg = 0; sg < nsegs; ++sg) {
+    const int role = (roles >> (2 * sg)) & 3;
+    if (role == 3) continue;
+    const uint4 v = make_uint4(w[role][0], w[role][1], w[role][2], w[role][3]);
+    uint4* dst = reinterpret_cast<uint4*>(row + (int64_t)sg * seg_stride);
+    if (STREAM) __stcs(dst, v);
+    else *dst = v;
+  }
+}
+
 // ------------------------------------------------------------------ reductions
 template <typename T>
 TCUDB_DEV T warp_sum(T v) {

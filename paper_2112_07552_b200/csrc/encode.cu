@@ -58,6 +58,16 @@ TCUDB_DEV void hll_add(unsigned* s_reg, long long x) {
   if (rho > s_reg[idx]) atomicMax(&s_reg[idx], rho);  // most updates stop at the read
 }
 
+// 32-bit variant for the sketches of int32 GROUP columns (each has its own sketch; the key
+// columns share the union sketch and keep the 64-bit hash so int32 and int64 keys agree)
+TCUDB_DEV void hll_add32(unsigned* s_reg, int x) {
+  const unsigned h = fmix32((unsigned)x * 0x9E3779B1u + 1u);
+  const unsigned idx = h >> (32 - kHllP);
+  const unsigned w = h << kHllP;
+  const unsigned rho = w ? (unsigned)__clz(w) + 1u : (unsigned)(32 - kHllP + 1);
+  if (rho > s_reg[idx]) atomicMax(&s_reg[idx], rho);
+}
+
 // Sketch gate: 4,096 evenly spaced samples per int column (columns 0..3); a column is
 // sketched in the statistics pass iff its sampled span already exceeds the direct-offset
 // limit (max(4n, 65536): it will be a hash-mode domain). gate[c] = 1 / 0 (read back with
@@ -145,10 +155,14 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     unsigned mabs = UINT_MAX;
     const int* p = static_cast<const int*>(c.data);
     const int4* p4 = static_cast<const int4*>(c.data);
+    const bool key_col = blockIdx.y <= 1;
     auto take = [&](int x) {
       mn = min(mn, x); mx = max(mx, x);
       mabs = min(mabs, x < 0 ? 0u - (unsigned)x : (unsigned)x);
-      if (sk) hll_add(s_reg, (long long)x);
+      if (sk) {
+        if (key_col) hll_add(s_reg, (long long)x);
+        else hll_add32(s_reg, x);
+      }
     };
     for (int64_t i0 = gtid; i0 < n4; i0 += 4 * stride) {
       int4 x[4];
@@ -163,22 +177,26 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
     return;
   }
   long long mn = LLONG_MAX, mx = LLONG_MIN, mabs = LLONG_MAX;
-  for (int64_t i0 = (int64_t)blockIdx.x * T + threadIdx.x; i0 < c.n; i0 += 4 * stride) {
-    long long x[4];
+  auto take64 = [&](long long x) {
+    mn = min(mn, x); mx = max(mx, x);
+    const long long a = x < 0 ? (x == LLONG_MIN ? LLONG_MAX : -x) : x;
+    mabs = min(mabs, a);
+    if (sk) hll_add(s_reg, x);
+  };
+  // 16-byte vectors (two values), four in flight per thread; the odd tail after
+  const int64_t n2 = (reinterpret_cast<uintptr_t>(c.data) & 15) ? 0 : c.n / 2;
+  const longlong2* p2 = static_cast<const longlong2*>(c.data);
+  for (int64_t i0 = gtid; i0 < n2; i0 += 4 * stride) {
+    longlong2 x[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = i0 + u * stride;
-      x[u] = i < c.n ? ld_int(c.data, c.type, i) : 0;
+    for (int u = 0; u < 4; ++u) {  // clamped index: a repeat is harmless for min / max / a sketch
+      const int4 t = ld_stream_v4(p2 + min(i0 + u * stride, n2 - 1));
+      x[u] = make_longlong2(((long long)(unsigned)t.y << 32) | (unsigned)t.x, ((long long)(unsigned)t.w << 32) | (unsigned)t.z);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (i0 + u * stride >= c.n) break;
-      mn = min(mn, x[u]); mx = max(mx, x[u]);
-      const long long a = x[u] < 0 ? (x[u] == LLONG_MIN ? LLONG_MAX : -x[u]) : x[u];
-      mabs = min(mabs, a);
-      if (sk) hll_add(s_reg, x[u]);
-    }
+    for (int u = 0; u < 4; ++u) { take64(x[u].x); take64(x[u].y); }
   }
+  for (int64_t i = n2 * 2 + gtid; i < c.n; i += stride) take64(__ldcs(static_cast<const long long*>(c.data) + i));
   flush();
   col_stats_finish(s, mn, mx, mabs, 0);
 }

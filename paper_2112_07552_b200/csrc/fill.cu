@@ -471,11 +471,11 @@ __device__ __forceinline__ uint16_t bf16_bits(float x) {
 }
 __device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
 
-// fp32 scratch -> bf16 hi (and optionally lo) segments; 8 cells per thread step.
-// hi = bf16(x) (RNE), lo = bf16(x - hi); hi goes to every K segment in hi_mask, lo to every
-// segment in lo_mask (segment i = columns [i·ld, (i+1)·ld) of the operand row)
+// fp32 scratch -> bf16 segments; 8 cells per thread step: the three-way split (hi, mid, lo)
+// written into the K segments of the operand row by their roles (kernels.h kRoles*; kRolesHi:
+// hi into segment 0 only); inexact = some cell is not bf16-exact (x - hi != 0)
 __global__ void k_pack_bf16(const float* __restrict__ scr, int64_t rows, int64_t ld, uint16_t* __restrict__ op,
-                            int64_t ld_op, int hi_mask, int lo_mask, FillStats* __restrict__ fs) {
+                            int64_t ld_op, int roles, FillStats* __restrict__ fs) {
   const int64_t per_row = ld / 8;
   const int64_t total = rows * per_row;
   const int64_t stride = (int64_t)gridDim.x * T;
@@ -486,24 +486,12 @@ __global__ void k_pack_bf16(const float* __restrict__ scr, int64_t rows, int64_t
     const float4 a = *reinterpret_cast<const float4*>(scr + r * ld + c8);
     const float4 b = *reinterpret_cast<const float4*>(scr + r * ld + c8 + 4);
     const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    uint32_t hi[4], lo[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint16_t h0 = bf16_bits(x[2 * j]), h1 = bf16_bits(x[2 * j + 1]);
-      const float r0 = x[2 * j] - bf16_val(h0), r1 = x[2 * j + 1] - bf16_val(h1);
-      inexact |= (r0 != 0.f) | (r1 != 0.f);
-      nnz += (x[2 * j] != 0.f) + (x[2 * j + 1] != 0.f);
-      hi[j] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-      lo[j] = (uint32_t)bf16_bits(r0) | ((uint32_t)bf16_bits(r1) << 16);
+    for (int j = 0; j < 8; ++j) {
+      inexact |= (x[j] - bf16_val(bf16_bits(x[j]))) != 0.f;
+      nnz += x[j] != 0.f;
     }
-    uint16_t* row = op + r * ld_op;
-#pragma unroll
-    for (int sg = 0; sg < 4; ++sg) {
-      if (hi_mask & (1 << sg))
-        *reinterpret_cast<uint4*>(row + (int64_t)sg * ld + c8) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      if (lo_mask & (1 << sg))
-        *reinterpret_cast<uint4*>(row + (int64_t)sg * ld + c8) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    }
+    store_split8<false>(op + r * ld_op + c8, ld, x, roles, kSplitSegs);
   }
   inexact = __any_sync(0xffffffffu, inexact);
   nnz = warp_sum(nnz);
@@ -642,7 +630,7 @@ constexpr int kT2MaxTiles = 4096;
 constexpr int kT2TileCells = 65536;
 // SPLIT (values that are not bf16-exact): 8-byte entries (cell << 32 | fp32 bits), fp32 tiles of
 // 32,768 cells, and the tile CTA writes bf16 hi / lo = bf16(x - hi) into the segments of the
-// split layout ([hi|hi|lo|lo] for A, [hi|lo|hi|lo] for B) — no fp32 scratch, no atomics
+// three-way split layout (kernels.h kRolesA / kRolesB) — no fp32 scratch, no atomics
 template <bool SPLIT> struct T2 {
   using Ent = typename std::conditional<SPLIT, unsigned long long, uint32_t>::type;
   static constexpr int kCells = SPLIT ? 32768 : kT2TileCells;
@@ -820,14 +808,14 @@ __global__ void __launch_bounds__(kT2BinThreads, 1) k_t2_bin(const int32_t* __re
   if (threadIdx.x == 0 && inexact) atomicOr(&fs->inexact, 1);
 }
 
-// one CTA per tile: R x KW bf16 cells (SPLIT: fp32 cells, written as bf16 hi / lo into the
-// segments hi_mask / lo_mask of the split layout, segment stride Kp) + occupancy bits
+// one CTA per tile: R x KW bf16 cells (SPLIT: fp32 cells, written as the three-way bf16 split
+// into the segments of the split layout by their roles, segment stride Kp) + occupancy bits
 template <bool SPLIT>
 __global__ void __launch_bounds__(kT2Threads, 1) k_t2_tile(const typename T2<SPLIT>::Ent* __restrict__ ent,
                                                           const int64_t* __restrict__ offs, int nblk, int R, int KW,
                                                           int nkt, int64_t rows, int64_t Kp,
-                                                          uint16_t* __restrict__ op, int64_t ld_op, int hi_mask,
-                                                          int lo_mask, FillStats* __restrict__ fs) {
+                                                          uint16_t* __restrict__ op, int64_t ld_op, int roles,
+                                                          FillStats* __restrict__ fs) {
   using Ent = typename T2<SPLIT>::Ent;
   constexpr int kCells = T2<SPLIT>::kCells;
   using Cell = typename std::conditional<SPLIT, uint32_t, uint16_t>::type;
@@ -871,19 +859,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_t2_tile(const typename T2<SPL
       const float4 a = reinterpret_cast<const float4*>(tile + (int64_t)r * KW)[2 * c];
       const float4 b = reinterpret_cast<const float4*>(tile + (int64_t)r * KW)[2 * c + 1];
       const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t hw[4], lw[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint16_t h0 = bf16_bits(x[2 * j]), h1 = bf16_bits(x[2 * j + 1]);
-        hw[j] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-        lw[j] = (uint32_t)bf16_bits(x[2 * j] - bf16_val(h0)) | ((uint32_t)bf16_bits(x[2 * j + 1] - bf16_val(h1)) << 16);
-      }
-      uint16_t* row = op + (r0 + r) * ld_op + c0 + (int64_t)c * 8;
-#pragma unroll
-      for (int sg = 0; sg < 4; ++sg) {
-        if (hi_mask & (1 << sg)) __stcs(reinterpret_cast<uint4*>(row + (int64_t)sg * Kp), make_uint4(hw[0], hw[1], hw[2], hw[3]));
-        if (lo_mask & (1 << sg)) __stcs(reinterpret_cast<uint4*>(row + (int64_t)sg * Kp), make_uint4(lw[0], lw[1], lw[2], lw[3]));
-      }
+      store_split8<true>(op + (r0 + r) * ld_op + c0 + (int64_t)c * 8, Kp, x, roles, kSplitSegs);
     }
   }
   dup = __syncthreads_or(dup);
@@ -897,7 +873,7 @@ size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp, bool split) {
 
 template <bool SPLIT>
 static cudaError_t run_t2(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n, int64_t rows,
-                          int64_t Kp, uint16_t* op, int64_t ld_op, int hi_mask, int lo_mask, FillStats* fs, void* ws,
+                          int64_t Kp, uint16_t* op, int64_t ld_op, int roles, FillStats* fs, void* ws,
                           cudaStream_t s, int64_t* launches) {
   using Ent = typename T2<SPLIT>::Ent;
   const T2Plan p = t2_plan(n, rows, Kp, SPLIT);
@@ -920,7 +896,7 @@ static cudaError_t run_t2(const int32_t* kcode, const int32_t* rcode, const ColD
   if ((e = set_func_attr(k_t2_tile<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem)) != cudaSuccess)
     return e;
   k_t2_tile<SPLIT><<<p.ntiles, kT2Threads, tile_smem, s>>>(ent, offs, p.nblk, p.R, p.KW, p.nkt, rows, Kp, op, ld_op,
-                                                           hi_mask, lo_mask, fs);
+                                                           roles, fs);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
@@ -928,13 +904,13 @@ static cudaError_t run_t2(const int32_t* kcode, const int32_t* rcode, const ColD
 cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                    int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
                                    cudaStream_t s, int64_t* launches) {
-  return run_t2<false>(kcode, rcode, val, n, rows, Kp, op, ld_op, 1, 0, fs, ws, s, launches);
+  return run_t2<false>(kcode, rcode, val, n, rows, Kp, op, ld_op, kRolesHi, fs, ws, s, launches);
 }
 
 cudaError_t launch_fill_bf16_split_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
-                                         int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, int hi_mask,
-                                         int lo_mask, FillStats* fs, void* ws, cudaStream_t s, int64_t* launches) {
-  return run_t2<true>(kcode, rcode, val, n, rows, Kp, op, ld_op, hi_mask, lo_mask, fs, ws, s, launches);
+                                         int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, int roles,
+                                         FillStats* fs, void* ws, cudaStream_t s, int64_t* launches) {
+  return run_t2<true>(kcode, rcode, val, n, rows, Kp, op, ld_op, roles, fs, ws, s, launches);
 }
 
 cudaError_t launch_fill_count_fp4(const int32_t* kcode, const int32_t* rcode, int64_t n, uint8_t* op,
@@ -994,10 +970,10 @@ cudaError_t launch_pack_planes(const long long* scr, int64_t count, int planes, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int hi_mask,
-                             int lo_mask, FillStats* fs, cudaStream_t s, int64_t* launches) {
+cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int roles,
+                             FillStats* fs, cudaStream_t s, int64_t* launches) {
   if (rows <= 0) return cudaSuccess;
-  k_pack_bf16<<<grid_for(rows * (ld / 8), T * 4), T, 0, s>>>(scr, rows, ld, op, ld_op, hi_mask, lo_mask, fs);
+  k_pack_bf16<<<grid_for(rows * (ld / 8), T * 4), T, 0, s>>>(scr, rows, ld, op, ld_op, roles, fs);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

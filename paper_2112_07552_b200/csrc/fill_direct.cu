@@ -17,8 +17,8 @@
 //   k_dt_tile       one CTA per tile builds the tile in shared memory (occupancy bits
 //                   detect a duplicate cell -> fs->overflow; the caller then takes the
 //                   scratch path) and writes it coalesced, zeros included — bf16 cells, or
-//                   fp32 cells written as the hi / lo split (R8: hi = bf16(x), lo =
-//                   bf16(x - hi)) — plus, optionally, the e2m1 existence pattern (R3).
+//                   fp32 cells written as the three-way split (R8/R9: hi = bf16(x),
+//                   mid = bf16(x - hi), lo = bf16(x - hi - mid)) — plus, optionally, the e2m1 existence pattern (R3).
 // Bytes per tuple: 8 (count) + 12 read + 4|8 written (bin) + 4|8 read + cells written (tile).
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -265,8 +265,6 @@ __global__ void __launch_bounds__(kDtThreads, 2) k_dt_bin(const DtFill f, const 
   if (threadIdx.x == 0 && ovf) atomicOr(&f.fs->overflow, 1);
 }
 
-TCUDB_DEV uint16_t dt_bf16(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
-TCUDB_DEV float dt_bf16_val(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
 
 template <bool SPLIT>
 __global__ void __launch_bounds__(kDtTileThreads, 1) k_dt_tile(const DtFill f, const DtPlan p,
@@ -327,19 +325,7 @@ __global__ void __launch_bounds__(kDtTileThreads, 1) k_dt_tile(const DtFill f, c
       const float4 a = reinterpret_cast<const float4*>(tile + (int64_t)r * p.KW)[2 * c];
       const float4 b = reinterpret_cast<const float4*>(tile + (int64_t)r * p.KW)[2 * c + 1];
       const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t hw[4], lw[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint16_t h0 = dt_bf16(x[2 * j]), h1 = dt_bf16(x[2 * j + 1]);
-        hw[j] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-        lw[j] = (uint32_t)dt_bf16(x[2 * j] - dt_bf16_val(h0)) | ((uint32_t)dt_bf16(x[2 * j + 1] - dt_bf16_val(h1)) << 16);
-      }
-      uint16_t* row = f.op + (r0 + r) * f.ld_op + c0 + (int64_t)c * 8;
-#pragma unroll
-      for (int sg = 0; sg < 4; ++sg) {
-        if (f.hi_mask & (1 << sg)) __stcs(reinterpret_cast<uint4*>(row + (int64_t)sg * f.Kp), make_uint4(hw[0], hw[1], hw[2], hw[3]));
-        if (f.lo_mask & (1 << sg)) __stcs(reinterpret_cast<uint4*>(row + (int64_t)sg * f.Kp), make_uint4(lw[0], lw[1], lw[2], lw[3]));
-      }
+      store_split8<true>(f.op + (r0 + r) * f.ld_op + c0 + (int64_t)c * 8, f.Kp, x, f.roles, kSplitSegs);
     }
   }
   if (f.pat) {

@@ -187,7 +187,7 @@ __device__ __forceinline__ void epilogue_chunk(const KParams& p, const uint32_t*
       if (p.cnt_out) nzc += (x0 != 0ull) + (x1 != 0ull);
     }
   } else if (p.epi == EPI_SETF64 || p.epi == EPI_ACCF64) {
-    // fp32 accumulator of one K range -> fp64 C (the hi/lo split's partial products are
+    // fp32 accumulator of one K range -> fp64 C (the bf16 split's partial products are
     // accumulated in separate launches and summed here in fp64, R9)
     double2* d2 = reinterpret_cast<double2*>(reinterpret_cast<double*>(p.C) + row * p.ldc + col);
 #pragma unroll

@@ -88,6 +88,18 @@ cudaError_t launch_popcount(const unsigned* w, int64_t n, unsigned mask, unsigne
 cudaError_t launch_max_u64(const unsigned long long* x, int64_t n, unsigned long long* out, cudaStream_t s,
                            int64_t* launches);
 
+// ---------------------------------------------------------------- float split layout (reading R9)
+// A value that is not bf16-exact is split three ways, x = hi + mid + lo + r with hi = bf16(x),
+// mid = bf16(x - hi), lo = bf16(x - hi - mid), |r| <= 2^-24 |x|. Along K the operands hold
+// kSplitSegs segments of Kp columns: A' = [hi|hi|hi|mid|mid|lo], B' = [hi|mid|lo|hi|mid|hi], so
+// the product sums hi·hi (segment 0, its own fp32 accumulator) and the corrections hi·mid,
+// hi·lo, mid·hi, mid·mid, lo·hi (every term down to 2^-16 of |v·w|). A segment's role is 2 bits
+// of a `roles` word: 0 hi, 1 mid, 2 lo, 3 not written.
+constexpr int kSplitSegs = 6;
+constexpr int kRolesA = 0 | (0 << 2) | (0 << 4) | (1 << 6) | (1 << 8) | (2 << 10);
+constexpr int kRolesB = 0 | (1 << 2) | (2 << 4) | (0 << 6) | (1 << 8) | (0 << 10);
+constexpr int kRolesHi = 0xFFC;  // hi into segment 0 only (bf16 without the split)
+
 // ---------------------------------------------------------------- fill.cu (a5)
 // Device-side fill statistics read by the precision guard (a3).
 struct FillStats {
@@ -131,8 +143,8 @@ size_t fill_bf16_tiled_ws(int64_t n, int64_t rows, int64_t Kp, bool split = fals
 // into the segments hi_mask / lo_mask of the hi/lo split layout (segment stride Kp, row stride
 // ld_op); duplicate cells set fs->overflow (the caller then takes the fp32-scratch path).
 cudaError_t launch_fill_bf16_split_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
-                                         int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, int hi_mask,
-                                         int lo_mask, FillStats* fs, void* ws, cudaStream_t s, int64_t* launches);
+                                         int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, int roles,
+                                         FillStats* fs, void* ws, cudaStream_t s, int64_t* launches);
 cudaError_t launch_fill_bf16_tiled(const int32_t* kcode, const int32_t* rcode, const ColDesc& val, int64_t n,
                                    int64_t rows, int64_t Kp, uint16_t* op, int64_t ld_op, FillStats* fs, void* ws,
                                    cudaStream_t s, int64_t* launches);
@@ -153,7 +165,7 @@ struct DtFill {
   long long gmin; int gspan; const int32_t* gcode;  // row-code table over the group span
   int64_t rows, Kp;                                 // operand rows (multiple of 8) and K columns (of 128)
   uint16_t* op; int64_t ld_op;                      // bf16 operand [rows][ld_op] (elements)
-  int hi_mask, lo_mask;                             // split: segments (stride Kp) receiving hi / lo
+  int roles;                                        // split: role of each K segment (stride Kp)
   uint8_t* pat; int64_t ld_pat;                     // optional e2m1 existence pattern [rows][ld_pat bytes]
   FillStats* fs;                                    // fs->overflow: a cell with two tuples
 };
@@ -183,8 +195,8 @@ cudaError_t launch_pack_planes(const long long* scr, int64_t count, int planes, 
 // fp32 scratch [rows][ld] -> bf16 hi into op[row][i*ld + k] for every segment i in hi_mask,
 // lo = bf16(x - hi) into the segments in lo_mask (row stride ld_op elements); counts
 // inexact cells.
-cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int hi_mask,
-                             int lo_mask, FillStats* fs, cudaStream_t s, int64_t* launches);
+cudaError_t launch_pack_bf16(const float* scr, int64_t rows, int64_t ld, uint16_t* op, int64_t ld_op, int roles,
+                             FillStats* fs, cudaStream_t s, int64_t* launches);
 
 // ---------------------------------------------------------------- sparse.cu (a7)
 cudaError_t launch_bucket_fill(const int32_t* kcode, const int32_t* hcode, const ColDesc& w, int64_t n,

@@ -761,7 +761,10 @@ def test_bench_collective_single_rank():
 
 
 # ---------------------------------------------------------------- randomized sweep over the plans
-@pytest.mark.parametrize("seed", range(int(os.environ.get("TCUDB_FUZZ_SEEDS", "6"))))
+# (plus the seeds of the 300-seed sweep that exposed the two-way split's residual: groups of a
+# few float products missing the 1e-5 S_abs floor by up to 2x; fixed by the three-way split)
+@pytest.mark.parametrize("seed", sorted(set(range(int(os.environ.get("TCUDB_FUZZ_SEEDS", "6"))))
+                                        | {101, 108, 192, 215, 221, 235, 250}))
 def test_fuzz_all_plans(engine, torch_mod, oracle_mod, monkeypatch, seed):
     """Random shapes (sizes, key/group spans and dtypes, skew, value kinds) through every
     plan the selector can take — auto, FORCE_DENSE, FORCE_SPARSE, the one-pass band kernel,
