@@ -259,14 +259,14 @@ const char* tcudb_last_error(const tcudb_ctx* ctx);
 /* Kernel launches recorded since the context was created (evidence counter). */
 int64_t tcudb_launch_count(const tcudb_ctx* ctx);
 /* The dense-vs-sparse selector's cost-model constants (a4; Eq. 3 P:1172-1175,
- * §4.2.2): out7 = {dense GEMM rate kind::i8, kind::f16 (bf16), kind::mxf4
+ * §4.2.2): out8 = {dense GEMM rate kind::i8, kind::f16 (bf16), kind::mxf4
  * (ops/s), device copy bandwidth (bytes/s), sparse-path joined pairs/s, sparse-path fixed
- * cost (s), calibration wall time (ms)}. tcudb_create measures them once per device and
- * process (environment TCUDB_CALIBRATE=0: the compiled defaults; TCUDB_CALIBRATION_VALUES=
- * "R_i8,R_bf16,R_fp4,BW,R_sp,T_sp0": constants measured by an earlier run, for runs whose own
- * timing is distorted, e.g. under a profiler). Returns 1 if measured, 2 if injected, 0 for
- * the defaults. */
-int32_t tcudb_calibration(const tcudb_ctx* ctx, double* out7);
+ * cost (s), calibration wall time (ms), dense-path fixed cost (s)}. tcudb_create measures them
+ * once per device and process (environment TCUDB_CALIBRATE=0: the compiled defaults;
+ * TCUDB_CALIBRATION_VALUES="R_i8,R_bf16,R_fp4,BW,R_sp,T_sp0[,T_d0]": constants measured by an
+ * earlier run, for runs whose own timing is distorted, e.g. under a profiler). Returns 1 if
+ * measured, 2 if injected, 0 for the defaults. */
+int32_t tcudb_calibration(const tcudb_ctx* ctx, double* out8);
 void tcudb_destroy(tcudb_ctx* ctx);
 
 #ifdef __cplusplus

@@ -311,9 +311,9 @@ class Engine:
     @property
     def calibration(self) -> dict:
         """Selector constants measured at tcudb_create (tcudb_calibration)."""
-        v = (ctypes.c_double * 7)()
+        v = (ctypes.c_double * 8)()
         m = self._lib.tcudb_calibration(self._ctx, v)
-        keys = ("R_i8", "R_bf16", "R_fp4", "BW", "R_sp", "T_sp0", "ms")
+        keys = ("R_i8", "R_bf16", "R_fp4", "BW", "R_sp", "T_sp0", "ms", "T_d0")
         return dict(zip(keys, list(v)), measured=bool(m), injected=m == 2)
 
     @property

@@ -35,6 +35,7 @@ struct Calib {
   double R_i8 = 2.0e15, R_bf16 = 1.0e15, R_fp4 = 4.0e15;  // dense GEMM ops/s per kind
   double BW = 5.5e12;                                       // device copy bytes/s (read + write)
   double R_sp = 5.0e10, T_sp0 = 40e-6;                      // sparse path: joined pairs/s, fixed cost
+  double T_d0 = 150e-6;                                     // dense path: fixed cost (syncs, scans, launches)
   int measured = 0;
   float ms = 0.f;                                           // calibration wall time
 };
@@ -487,7 +488,7 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   const Calib& cb = ctx->cal;
   auto costs = [&](double J, double K, double* td, double* tsp) {
     const int64_t Gp = round_up(G, 256), Hp = round_up(H, 256), Kp = round_up(std::max<int64_t>((int64_t)K, 1), 128);
-    *td = 2.0 * Gp * Hp * Kp / cb.R_i8 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / cb.BW;
+    *td = 2.0 * Gp * Hp * Kp / cb.R_i8 + 3.0 * ((double)(Gp + Hp) * Kp + (double)Gp * Hp * 8) / cb.BW + cb.T_d0;
     // the partitioned expand's own rate (one L2 reduction per joined pair: ~1.4e11/s on c5)
     *tsp = J / 5.0e10 + ((double)G * H * 4 + (double)(nA + nB) * 32) / cb.BW + cb.T_sp0;
   };
@@ -983,7 +984,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 4 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
-  const double t_dense = planes_est * dense_ops * (use_bs ? bs_frac : 1.0) / R_tc + 3.0 * dense_bytes / BW;
+  const double t_dense = planes_est * dense_ops * (use_bs ? bs_frac : 1.0) / R_tc + 3.0 * dense_bytes / BW + cb.T_d0;
   const double t_sparse = (double)J / R_sp + sparse_bytes / BW + T_sp0;
   // memory budget: the device's free memory when the context was created, re-read live
   // (cudaMemGetInfo: 0.3 ms to tens of ms of host time) only when a path's footprint comes
@@ -1820,12 +1821,14 @@ void calibrate(tcudb_ctx* c) {
   const char* env = getenv("TCUDB_CALIBRATE");
   if (env && env[0] == '0') return;
   // constants measured by an earlier run (e.g. the bench line's selector_calibration), for runs
-  // whose own timing is distorted (under a profiler): "R_i8,R_bf16,R_fp4,BW,R_sp,T_sp0"
+  // whose own timing is distorted (under a profiler): "R_i8,R_bf16,R_fp4,BW,R_sp,T_sp0[,T_d0]"
   if (const char* vals = getenv("TCUDB_CALIBRATION_VALUES")) {
     Calib cal;
-    double v[6];
-    if (sscanf(vals, "%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) == 6) {
+    double v[7];
+    const int nv = sscanf(vals, "%lf,%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6]);
+    if (nv >= 6) {
       cal.R_i8 = v[0]; cal.R_bf16 = v[1]; cal.R_fp4 = v[2]; cal.BW = v[3]; cal.R_sp = v[4]; cal.T_sp0 = v[5];
+      if (nv == 7) cal.T_d0 = v[6];
       cal.measured = 2;  // injected
       c->cal = cal;
       return;
@@ -1922,6 +1925,42 @@ void calibrate(tcudb_ctx* c) {
       if (slope > 0) {
         cal.R_sp = clamp(1.0 / slope, cal.R_sp);
         cal.T_sp0 = std::min(std::max(y0 - J_pt[0] / cal.R_sp, 10e-6), 400e-6);
+      }
+    }
+    // dense path's fixed cost: the smaller point forced dense (G = H = 4,096, K ~ 16 K, COUNT),
+    // minus the model's GEMM and byte terms — the host syncs, result-size read,
+    // scans and small launches the byte / flop terms do not see
+    if (ok) {
+      const int64_t n = n_pt[0];
+      int32_t* ka = ar.get<int32_t>(n);
+      int32_t* ga_ = ar.get<int32_t>(n);
+      int32_t* kb = ar.get<int32_t>(n);
+      int32_t* hb = ar.get<int32_t>(n);
+      CK(launch_gen_cols(ka, ga_, n, keys_pt[0], groups, 17u, s, &L));
+      CK(launch_gen_cols(kb, hb, n, keys_pt[0], groups, 91u, s, &L));
+      tcudb_table TA{}, TB{};
+      TA.n_rows = TB.n_rows = n;
+      TA.key = {ka, TCUDB_I32}; TA.group = {ga_, TCUDB_I32};
+      TB.key = {kb, TCUDB_I32}; TB.group = {hb, TCUDB_I32};
+      // (u8 operands: random cells collide, and an e2m1 fill would rerun on u8 — a retry the
+      // fixed cost must not absorb)
+      tcudb_query q{TCUDB_COUNT, TCUDB_FORCE_DENSE | TCUDB_NO_FP4};
+      double best = 1e30;
+      tcudb_stats st{};
+      for (int r = 0; r < 3 && ok; ++r) {
+        tcudb_result out{};
+        const auto h0 = std::chrono::steady_clock::now();
+        if (run_join_agg(c, &TA, &TB, &q, &out, &st, s) != TCUDB_OK) { ok = false; break; }
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+        result_release(c, out.base ? out.base : out.g);
+        if (r > 0) best = std::min(best, dt);
+      }
+      if (ok) {
+        const double Gp = (double)round_up(st.G, 256), Hp = (double)round_up(st.H, 256);
+        const double Kp = (double)round_up(st.K, 128);
+        const double R = st.elem == 3 ? cal.R_fp4 : cal.R_i8;
+        const double model = 2.0 * Gp * Hp * Kp / R + 3.0 * ((Gp + Hp) * Kp + Gp * Hp * 8) / cal.BW;
+        cal.T_d0 = std::min(std::max(best - model, 10e-6), 2e-3);
       }
     }
     CK(cudaStreamSynchronize(s));
@@ -2626,11 +2665,11 @@ const char* tcudb_last_error(const tcudb_ctx* ctx) { return ctx ? ctx->err.c_str
 
 int64_t tcudb_launch_count(const tcudb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-int32_t tcudb_calibration(const tcudb_ctx* ctx, double* out7) {
-  if (!ctx || !out7) return 0;
+int32_t tcudb_calibration(const tcudb_ctx* ctx, double* out8) {
+  if (!ctx || !out8) return 0;
   const Calib& c = ctx->cal;
-  const double v[7] = {c.R_i8, c.R_bf16, c.R_fp4, c.BW, c.R_sp, c.T_sp0, (double)c.ms};
-  std::memcpy(out7, v, sizeof(v));
+  const double v[8] = {c.R_i8, c.R_bf16, c.R_fp4, c.BW, c.R_sp, c.T_sp0, (double)c.ms, c.T_d0};
+  std::memcpy(out8, v, sizeof(v));
   return c.measured;
 }
 

@@ -10,7 +10,7 @@ export TAG=${TAG:-r02}
 tail -3 gpurun_out/${TAG}_bench.time
 export TCUDB_CALIBRATION_VALUES=$(python -c "
 import json; c=json.load(open('gpurun_out/${TAG}_bench.json'))['selector_calibration']
-print(','.join(repr(c[k]) for k in ('R_i8','R_bf16','R_fp4','BW','R_sp','T_sp0')))")
+print(','.join(repr(c[k]) for k in ('R_i8','R_bf16','R_fp4','BW','R_sp','T_sp0','T_d0')))")
 echo "calibration: $TCUDB_CALIBRATION_VALUES"
 python - <<'PY'
 import json, os

@@ -919,6 +919,7 @@ def test_selector_calibration_measured(engine):
     assert 1.0e15 < c["R_i8"] < 5.0e15 and 0.5e15 < c["R_bf16"] < 2.5e15 and 2.0e15 < c["R_fp4"] < 1.0e16, c
     assert 3.0e12 < c["BW"] < 9.0e12, c
     assert 1.25e10 <= c["R_sp"] <= 2.0e11 and 10e-6 <= c["T_sp0"] <= 400e-6, c
+    assert 10e-6 <= c["T_d0"] <= 2e-3, c
 
 
 @pytest.mark.parametrize("mode", ["tiled", "range", "binned"])
