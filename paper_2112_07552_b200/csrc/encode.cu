@@ -76,11 +76,19 @@ __global__ void k_sketch_gate(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, in
   const ColDesc c = blockIdx.x == 0 ? c0 : blockIdx.x == 1 ? c1 : blockIdx.x == 2 ? c2 : c3;
   __shared__ long long smn[32], smx[32];
   long long mn = LLONG_MAX, mx = LLONG_MIN;
-  if (c.data && c.n > 0)
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
-      const long long x = ld_int(c.data, c.type, (int64_t)((__int128)c.n * i / 4096));
-      mn = min(mn, x); mx = max(mx, x);
+  if (c.data && c.n > 0) {
+    // n * i < 2^63 for n < 2^51: 64-bit index math (a 128-bit division per sample cost ~15 us)
+    long long x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = threadIdx.x + u * (int)blockDim.x;
+      x[u] = i < 4096 ? ld_int(c.data, c.type, (int64_t)(c.n < (1ll << 51) ? c.n * i / 4096
+                                                                         : (int64_t)((__int128)c.n * i / 4096)))
+                      : x[0];
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { mn = min(mn, x[u]); mx = max(mx, x[u]); }
+  }
   mn = warp_min_ll(mn); mx = warp_max_ll(mx);
   if (lane_id() == 0) { smn[warp_id()] = mn; smx[warp_id()] = mx; }
   __syncthreads();
@@ -203,7 +211,7 @@ __global__ void k_col_stats(ColDesc c0, ColDesc c1, ColDesc c2, ColDesc c3, ColD
 
 __global__ void k_init_stats(ColStats* st, int n) {
   const int i = threadIdx.x;
-  if (i < n) { st[i].mn = LLONG_MAX; st[i].mx = LLONG_MIN; st[i].min_abs = LLONG_MAX; st[i].flags = 0; }
+  if (i < n) { st[i].mn = LLONG_MAX; st[i].mx = LLONG_MIN; st[i].min_abs = LLONG_MAX; st[i].flags = 0; st[i].pad = 0; }
 }
 
 // ------------------------------------------------------------------ #distinct sketch
@@ -521,7 +529,7 @@ __global__ void k_pred_count(const uint8_t* __restrict__ fa, const uint8_t* __re
 // Single-block variant for spans up to ~1 M flags (one launch instead of count +
 // scan + codes): 1024 threads sweep the flags in 16 K chunks with a running offset;
 // also writes the total, the ∪ count, and (direct group domains) dict[code] = min + x.
-__global__ void __launch_bounds__(1024) k_pred_codes_1blk(const uint8_t* __restrict__ fa,
+__device__ __forceinline__ void pred_codes_1blk_body(const uint8_t* __restrict__ fa,
                                                           const uint8_t* __restrict__ fb, int64_t n,
                                                           int32_t* __restrict__ code, int64_t* __restrict__ count,
                                                           unsigned long long* __restrict__ union_cnt,
@@ -589,6 +597,21 @@ __global__ void __launch_bounds__(1024) k_pred_codes_1blk(const uint8_t* __restr
     u = warp_sum(u);
     if (lane_id() == 0 && u) atomicAdd(union_cnt, (unsigned long long)u);
   }
+}
+
+__global__ void __launch_bounds__(1024) k_pred_codes_1blk(const uint8_t* __restrict__ fa,
+                                                          const uint8_t* __restrict__ fb, int64_t n,
+                                                          int32_t* __restrict__ code, int64_t* __restrict__ count,
+                                                          unsigned long long* __restrict__ union_cnt,
+                                                          long long* __restrict__ dict, long long minv) {
+  pred_codes_1blk_body(fa, fb, n, code, count, union_cnt, dict, minv);
+}
+
+// up to three small dictionaries' codes in one launch (one block each: the key, A.g and B.h
+// dictionaries of a query), instead of three dependent single-block launches
+__global__ void __launch_bounds__(1024) k_pred_codes_1blk_multi(PredJob j0, PredJob j1, PredJob j2) {
+  const PredJob& j = blockIdx.x == 0 ? j0 : blockIdx.x == 1 ? j1 : j2;
+  pred_codes_1blk_body(j.fa, j.fb, j.n, j.code, j.count, j.union_cnt, j.dict, j.minv);
 }
 
 __global__ void k_pred_codes(const uint8_t* __restrict__ fa, const uint8_t* __restrict__ fb, int64_t n,
@@ -994,7 +1017,7 @@ cudaError_t launch_col_stats(const ColDesc* cols, ColStats* st, cudaStream_t s, 
   for (int i = 0; i < 6; ++i) if (cols[i].data && cols[i].n > nmax) nmax = cols[i].n;
   dim3 grid((unsigned)std::min<int64_t>(2 * kNumSMs, (nmax + T * 16 - 1) / (T * 16)), 6);
   if (hll) {
-    k_sketch_gate<<<4, 256, 0, s>>>(cols[0], cols[1], cols[2], cols[3], gate);
+    k_sketch_gate<<<4, 1024, 0, s>>>(cols[0], cols[1], cols[2], cols[3], gate);
     k_col_stats<true><<<grid, T, 0, s>>>(cols[0], cols[1], cols[2], cols[3], cols[4], cols[5], st, hll, gate);
     if (launches) ++*launches;
   } else {
@@ -1104,6 +1127,25 @@ cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, i
   k_pred_codes<<<(unsigned)nt, T, 0, s>>>(fa, fb, n, toff, code, dict, minv);
   if (launches) ++*launches;
   return cudaGetLastError();
+}
+
+cudaError_t launch_pred_codes_multi(const PredJob* jobs, int nj, void* const* temps, cudaStream_t s,
+                                    int64_t* launches) {
+  bool small = nj >= 1 && nj <= 3;
+  for (int i = 0; i < nj && small; ++i) small = jobs[i].n > 0 && jobs[i].n <= 32768;
+  if (small) {
+    const PredJob none{};
+    k_pred_codes_1blk_multi<<<nj, 1024, 0, s>>>(jobs[0], nj > 1 ? jobs[1] : none, nj > 2 ? jobs[2] : none);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
+  for (int i = 0; i < nj; ++i) {
+    const PredJob& j = jobs[i];
+    const cudaError_t e = launch_pred_codes(j.fa, j.fb, j.n, j.code, j.count, j.union_cnt, j.dict, j.minv, temps[i],
+                                            s, launches);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_direct_dict(const int32_t* code, int64_t range, long long minv, long long* dict, cudaStream_t s,

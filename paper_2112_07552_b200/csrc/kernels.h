@@ -61,6 +61,14 @@ size_t pred_temp_bytes(int64_t n);
 cudaError_t launch_pred_codes(const uint8_t* fa, const uint8_t* fb, int64_t n, int32_t* code, int64_t* count_dev,
                               unsigned long long* union_dev, long long* dict, long long minv, void* temp,
                               cudaStream_t s, int64_t* launches);
+// one dictionary's code scan (launch_pred_codes' arguments); launch_pred_codes_multi runs up
+// to three small ones (n <= 32 K) as one launch, larger ones one by one (temps[i] each)
+struct PredJob {
+  const uint8_t* fa; const uint8_t* fb; int64_t n; int32_t* code; int64_t* count;
+  unsigned long long* union_cnt; long long* dict; long long minv;
+};
+cudaError_t launch_pred_codes_multi(const PredJob* jobs, int nj, void* const* temps, cudaStream_t s,
+                                    int64_t* launches);
 cudaError_t launch_direct_dict(const int32_t* code, int64_t range, long long minv, long long* dict, cudaStream_t s,
                                int64_t* launches);
 cudaError_t launch_gather_slots(const int32_t* tmp_code, const unsigned long long* slots, int64_t cap,

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -143,6 +144,8 @@ struct Dict {
   int32_t* slot1 = nullptr;   // hash mode: slot of each row of the first / second column
   int32_t* slot2 = nullptr;
   int wide = 1;               // hash mode: offsets need 64 bits (slot hash fmix64 vs fmix32)
+  bool pending = false;       // direct mode: marks done, code scan deferred (flush_codes)
+  unsigned long long* pending_union = nullptr;
   DictView view(int col = 0) const {
     DictView v;
     v.mode = mode;
@@ -200,6 +203,20 @@ void dict_direct_codes(Arena& ar, Dict& d, unsigned long long* union_dev, int64_
   CK(launch_pred_codes(d.fa, d.fb, (int64_t)d.span, d.code, d.count_dev, union_dev, d.dict, d.minv, tmp, ar.s,
                        launches));
 }
+// the deferred code scans of up to three direct dictionaries in one launch when they are small
+void flush_codes(Arena& ar, std::initializer_list<Dict*> ds, int64_t* launches) {
+  PredJob jobs[3];
+  void* temps[3];
+  int nj = 0;
+  for (Dict* d : ds) {
+    if (!d->pending || nj == 3) continue;
+    jobs[nj] = PredJob{d->fa, d->fb, (int64_t)d->span, d->code, d->count_dev, d->pending_union, d->dict, d->minv};
+    temps[nj] = ar.get<char>((int64_t)pred_temp_bytes((int64_t)d->span));
+    d->pending = false;
+    ++nj;
+  }
+  if (nj) CK(launch_pred_codes_multi(jobs, nj, temps, ar.s, launches));
+}
 
 // Build phase 1 of a dictionary over one or two columns (marks + codes / compaction).
 // intersect: K domain, code only keys present on both sides (∩); otherwise the union.
@@ -207,7 +224,7 @@ void dict_direct_codes(Arena& ar, Dict& d, unsigned long long* union_dev, int64_
 // (load <= ~0.53; c5's 4.2 M keys fit 2^23 slots = 64 MB, L2-resident).
 void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long long mn, long long mx, bool intersect,
                 unsigned long long* union_dev, int64_t* launches, double est_distinct = 0, bool row_slots = true,
-                int64_t sample_step = 1) {
+                int64_t sample_step = 1, bool defer_codes = false) {
   cudaStream_t s = ar.s;
   const int64_t n = c1.n + (c2 ? c2->n : 0);
   const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
@@ -224,7 +241,8 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     const int64_t sp = (int64_t)d.span;
     CK(launch_mark_direct(c1, mn, d.fa, sp, s, launches));
     if (c2) CK(launch_mark_direct(*c2, mn, intersect ? d.fb : d.fa, sp, s, launches));
-    dict_direct_codes(ar, d, union_dev, launches);
+    if (defer_codes) { d.pending = true; d.pending_union = union_dev; }
+    else dict_direct_codes(ar, d, union_dev, launches);
   } else {
     if (span > (unsigned __int128)~0ull) throw Fail{TCUDB_E_UNSUPPORTED};  // full 2^64 key span
     d.mode = 1;
@@ -728,13 +746,14 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
                              Ku, DG.minv, (int64_t)DG.span, cntA, DK.fa, DG.fa, s, L));
       CK(launch_direct_count(static_cast<const int32_t*>(bk.data), static_cast<const int32_t*>(bh.data), nB, kmin,
                              Ku, DH.minv, (int64_t)DH.span, cntB, DK.fb, DH.fa, s, L));
-      dict_direct_codes(ar, DK, d_union, L);
-      dict_direct_codes(ar, DG, nullptr, L);
-      dict_direct_codes(ar, DH, nullptr, L);
+      DK.pending = DG.pending = DH.pending = true;
+      DK.pending_union = d_union;
+      flush_codes(ar, {&DK, &DG, &DH}, L);
     } else {
-    dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0]);
-    dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1]);
-    dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2]);
+    dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0], true, 1, true);
+    dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], true, 1, true);
+    dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], true, 1, true);
+    flush_codes(ar, {&DK, &DG, &DH}, L);  // direct dictionaries' code scans, batched
     // probe right away with upper-bound sizes (codes < span / capacity), so the dictionary
     // sizes and the join size J come back in ONE device->host read
     Ku = (int64_t)DK.span;

@@ -101,10 +101,28 @@ def variant(A, B, drop):
     return A, B
 
 
+def _diff_report(r, out, ref):
+    """which (g, h) groups a rank's result has that the oracle lacks (and vice versa)"""
+    import json
+    got = set(zip(np.asarray(out["g"]).tolist(), np.asarray(out["h"]).tolist())) if "g" in out and "h" in out else set()
+    want = set(zip(ref["g"].tolist(), ref["h"].tolist())) if "g" in ref and "h" in ref else set()
+    extra, missing = sorted(got - want)[:20], sorted(want - got)[:20]
+    dup = len(out["agg"]) - len(got)
+    rep = {"rank": r, "n": int(len(out["agg"])), "n_ref": int(len(ref["cnt"])), "duplicates": int(dup),
+           "extra": [list(map(int, x)) for x in extra], "missing": [list(map(int, x)) for x in missing]}
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(os.path.join("gpurun_out", "collective_diff.jsonl"), "a") as f:
+        f.write(json.dumps(rep) + "\n")
+    return rep
+
+
 def check_all(res, err, ref, agg, float_vals, broken=""):
     assert all(e is None for e in err), (err, broken)
     for r, out in enumerate(res):
-        compare(out, ref, agg, float_vals=float_vals)
+        try:
+            compare(out, ref, agg, float_vals=float_vals)
+        except AssertionError as e:
+            raise AssertionError(f"rank {r}: {e}; {_diff_report(r, out, ref)}") from None
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
