@@ -561,14 +561,34 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
 // tcgen05.mma.cta_group::2 (M = 256) and its commits multicast to both CTAs'
 // barriers. Per SM this halves the B bytes staged per MMA compared with the
 // 1-CTA 128 x 256 tile (L2 -> SM traffic per MAC drops by 1/3).
-constexpr int STAGES2 = 6;
-constexpr int A2_BYTES = 128 * BKB;  // 16 KB (this CTA's 128 rows of A)
-constexpr int B2_BYTES = 128 * BKB;  // 16 KB (this CTA's half of the 256 N rows)
-constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr size_t SMEM2_BYTES = (size_t)STAGES2 * STAGE2_BYTES + 1024 + 256;
+// kind::mxf4 (c2's e2m1 COUNT product): a 256 x 240 pair tile, 120 B rows per CTA (two 240-column
+// accumulators + the block-scale columns fill the 512 TMEM columns, as in the 1-CTA kernel).
+template <int BN_, bool FP4>
+struct Geo2 {
+  static constexpr int STAGES = FP4 ? 7 : 6;
+  static constexpr int A_BYTES = 128 * BKB;             // 16 KB (this CTA's 128 rows of A)
+  static constexpr int B_BYTES = (BN_ / 2) * BKB;       // this CTA's half of the BN_ rows of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+};
 
+TCUDB_DEV void mma_mxf4_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t sfa,
+                             uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+      : "memory");
+}
+
+template <int BN_, bool FP4>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KParams p) {
+  using G2 = Geo2<BN_, FP4>;
+  constexpr int STAGES2 = G2::STAGES, A2_BYTES = G2::A_BYTES, B2_BYTES = G2::B_BYTES;
+  constexpr int STAGE2_BYTES = G2::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -584,7 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  const int num_tiles = p.tiles_m * p.tiles_n;  // pair tiles (256 x 256)
+  const int num_tiles = p.tiles_m * p.tiles_n;  // pair tiles (256 x BN_)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -595,10 +615,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncwarp();
-  cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (FP4) {
+    // unit block scales (UE8M0 0x7F) in both CTAs' scale columns [480, 512), all 128 lanes:
+    // whichever lanes / columns the pair MMA reads for SFA and SFB hold 2^0
+    if (warp >= 2 && warp < 6) {
+      const uint32_t q = (uint32_t)((warp & 3) * 32) << 16;
+      tmem_st_32x32b_x16(tmem_base + q + SF_COL, 0x7F7F7F7Fu);
+      tmem_st_32x32b_x16(tmem_base + q + SF_COL + 16, 0x7F7F7F7Fu);
+      tmem_st_wait();
+    }
+    tc_fence_before();
+  }
+  __syncwarp();
+  cluster_sync();  // barriers (and the scale columns) of both CTAs initialised before any remote arrive / MMA
+  tc_fence_after();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -615,7 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
           const int kc = (p.kb_begin + kb) * p.elems_per_kb;
           tma_load_2d_pair(&tmA, sA + stage * A2_BYTES, leader_full + 8 * stage, kc, mb * 256 + rank * 128, pol);
-          tma_load_2d_pair(&tmB, sB + stage * B2_BYTES, leader_full + 8 * stage, kc, nb * 256 + rank * 128, pol);
+          tma_load_2d_pair(&tmB, sB + stage * B2_BYTES, leader_full + 8 * stage, kc, nb * BN_ + rank * (BN_ / 2), pol);
           if (++stage == STAGES2) { stage = 0; phase ^= 1; }
         }
       }
@@ -627,7 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int t = cid; t < num_tiles; t += ncl) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BN_;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -636,7 +669,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t accum = (kb | kk) != 0;
-            if (p.is_bf16) mma_f16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
+            if (FP4) mma_mxf4_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, tmem_base + SF_COL,
+                                   tmem_base + SF_COL + 16, accum);
+            else if (p.is_bf16) mma_f16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
             else mma_i8_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, p.idesc, accum);
           }
           mma_commit_pair(&empty[stage], 0x3);  // frees this stage in both CTAs
@@ -656,8 +691,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t row = (int64_t)mb * 256 + rank * 128 + quarter * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      const int nzc = epilogue_rows<BN, false>(p, taddr, row, nb, tri);
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN_;
+      const int nzc = epilogue_rows<BN_, FP4>(p, taddr, row, nb, tri);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -789,6 +824,29 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   p.group_m = pick_group_m(p.tiles_m, BM, a.k_len);
   p.bmA = a.bmA; p.bmB = a.bmB; p.bmw = a.bmw;
   if (a.cmp && a.bmA) return cudaErrorInvalidValue;  // fused compaction needs every tile's epilogue
+  // CTA-pair kernel (cta_group::2, 256 x 240 pair tiles): each SM stages 128 A rows + 120 B rows
+  // per K-block instead of 128 + 240 (a third less L2 -> SM traffic per MAC). Default when M
+  // splits into 256-row pair tiles; TCUDB_GEMM_PAIR4=0 keeps the 1-CTA kernel.
+  static const bool no_pair4 = getenv("TCUDB_GEMM_PAIR4") && getenv("TCUDB_GEMM_PAIR4")[0] == '0';
+  if (!no_pair4 && !a.cmp && !a.bmA && a.M % 256 == 0 && kb == BKB) {
+    using G2 = Geo2<BNF, true>;
+    cudaError_t e = set_func_attr(k_gemm_tc2<BNF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)G2::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    p.tiles_m = (int)(a.M / 256);
+    p.idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24);
+    p.group_m = pick_group_m(p.tiles_m, 256, a.k_len);
+    const int64_t kcols = a.k_begin + a.k_len;
+    CUtensorMap mA, mB;
+    if (!make_map(&mA, a.A, ELEM_I8, a.M, kcols, a.lda, 128) ||
+        !make_map(&mB, a.B, ELEM_I8, a.N, kcols, a.ldb, BNF / 2))
+      return cudaErrorInvalidValue;
+    const int tiles = p.tiles_m * p.tiles_n;
+    const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+    k_gemm_tc2<BNF, true><<<grid, NUM_THREADS, G2::SMEM_BYTES, s>>>(mA, mB, p);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   if (a.cmp) {
     // M-blocks must complete early for their compaction to overlap later tiles: bands of
     // 2 M-blocks (measured best of 1..40 on c2)
@@ -806,7 +864,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   if (a.M <= 0 || a.N <= 0 || a.k_len <= 0) return cudaSuccess;
   if (a.M % BM || a.N % BN || (a.k_len * esz) % BKB || (a.k_begin * esz) % BKB) return cudaErrorInvalidValue;
   if ((a.lda * esz) % 16 || (a.ldb * esz) % 16) return cudaErrorInvalidValue;
-  cudaError_t e = set_func_attr(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
+  cudaError_t e = set_func_attr(k_gemm_tc2<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Geo2<BN, false>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   // Kernel choice: the 1-CTA 128x256 kernel is the default (measured faster on c2: 1.31 vs
   // 1.40 ms; both MMA-bound at ~65-70 % tensor-pipe activity). TCUDB_GEMM_PAIR=1 selects the
@@ -842,7 +901,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
     return cudaErrorInvalidValue;
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-  k_gemm_tc2<<<grid, NUM_THREADS, SMEM2_BYTES, s>>>(mA, mB, p);
+  k_gemm_tc2<BN, false><<<grid, NUM_THREADS, Geo2<BN, false>::SMEM_BYTES, s>>>(mA, mB, p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
