@@ -162,8 +162,10 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
 /* The join + group-by query. A, B: device columns, read-only,
  * any alignment. On success *out holds device arrays (caller owns). Blocks the
  * host on at most 4 small device->host reads (statistics, sizes, join size,
- * nnz); results are valid once `stream` passes the call. One query in flight
- * per context. `stats` may be NULL. */
+ * nnz); results are valid once `stream` passes the call: without `stats` the call
+ * returns while the result write is still running on `stream` (with `stats`, and on
+ * the collective path, it returns after it; asynchronous kernel faults surface on a
+ * later call as E_CUDA). One query in flight per context. `stats` may be NULL. */
 tcudb_status tcudb_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_table* B,
                             const tcudb_query* q, tcudb_result* out, tcudb_stats* stats, void* stream);
 

@@ -367,8 +367,10 @@ class Engine:
         q = Query(_AGG[agg], int(flags))
         res = Result()
         stats = Stats()
+        # without stats the call returns while the result write still runs on the stream (tcudb.h)
         st = self._lib.tcudb_join_agg(self._ctx, ctypes.byref(ta), ctypes.byref(tb), ctypes.byref(q),
-                                      ctypes.byref(res), ctypes.byref(stats), self._stream(stream))
+                                      ctypes.byref(res), ctypes.byref(stats) if with_stats else None,
+                                      self._stream(stream))
         self._check(st)
         owner = _Owner(self, res)
         out = {}

@@ -332,6 +332,12 @@ struct Timer {
   }
 };
 
+// The last kernels of a query (the ordered result write) are left running when the call
+// returns: the result is valid once the stream passes the call (tcudb.h, Synchronisation), so
+// the host does not wait for the write. Stats (their event timings) and the collective path
+// (exchanges after the local query) wait.
+inline bool end_sync(const tcudb_ctx* ctx, bool timed) { return timed || ctx->in_collective; }
+
 template <typename T>
 T* to_pinned(tcudb_ctx* ctx, const void* dev, cudaStream_t s) {
   Arena::ck(cudaMemcpyAsync(ctx->pinned, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -584,7 +590,7 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   try {
     CK(launch_compact_write(ca, ctmp, s, L));
     tm.mark(&S.ms_compact);
-    CK(cudaStreamSynchronize(s));
+    if (end_sync(ctx, timed)) CK(cudaStreamSynchronize(s));
   } catch (...) {
     result_release(ctx, base);
     throw;
@@ -877,7 +883,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     const int agg_kind = is_avg ? (kind == 2 ? 4 : 3) : kind;
     CK(launch_side_write(cnt_g, sum_g, pos, NG, agg_kind, o, s, L));
     tm.mark(&S.ms_compact);
-    CK(cudaStreamSynchronize(s));
+    if (end_sync(ctx, st != nullptr)) CK(cudaStreamSynchronize(s));
     tm.finish();
     out->n = n_res; out->g = gp; out->h = hp_; out->agg = o.agg; out->base = base; out->on_host = 0;
     S.n_result = n_res;
@@ -1801,7 +1807,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     throw;
   }
   tm.mark(&S.ms_compact);
-  CK(cudaStreamSynchronize(s));
+  if (end_sync(ctx, st != nullptr)) CK(cudaStreamSynchronize(s));
   tm.finish();
   out->n = nnz; out->g = r.g; out->h = r.h; out->agg = r.agg; out->base = r.g; out->on_host = 0;
   S.n_result = nnz;
