@@ -56,6 +56,12 @@ struct tcudb_ctx {
   size_t mem_free0 = 0;        // free device memory at creation (path-selection budget)
   cudaEvent_t ev[8] = {};
   cudaEvent_t evk[2] = {};   // the sparse path's band kernel (roofline timing)
+  // query scratch: small allocations are bumped from one device block (no allocator call per
+  // array: a small query makes ~50 of them); reused by the next query after scr_ev
+  char* scr = nullptr;
+  size_t scr_cap = 0, scr_used = 0;
+  cudaEvent_t scr_ev = nullptr;
+  bool scr_ev_set = false;
   std::mutex mu;
   // pinned host block cache for host-API results: size -> free blocks
   std::multimap<size_t, void*> host_free;
@@ -81,16 +87,39 @@ struct Fail {
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // Query-scoped arena: stream-ordered allocations, all released at scope exit.
+constexpr size_t kScratchBytes = 32ull << 20;  // per-context bump region
+constexpr size_t kBumpMax = 4ull << 20;        // larger arrays come from the pool
+
 struct Arena {
   cudaStream_t s;
   std::vector<void*> ptrs;
-  explicit Arena(cudaStream_t st) : s(st) {}
+  tcudb_ctx* ctx = nullptr;  // non-null: small arrays from the context's bump region
+  size_t mark = 0;           // the region's fill level when this arena opened (stack order)
+  explicit Arena(cudaStream_t st, tcudb_ctx* c = nullptr) : s(st), ctx(c && c->scr ? c : nullptr) {
+    if (!ctx) return;
+    mark = ctx->scr_used;
+    // the previous query's kernels may still read their scratch (the call returns before its
+    // last kernels finish): the region is reused only after them
+    if (mark == 0 && ctx->scr_ev_set) cudaStreamWaitEvent(s, ctx->scr_ev, 0);
+  }
   ~Arena() {
     for (void* p : ptrs) cudaFreeAsync(p, s);
+    if (!ctx) return;
+    ctx->scr_used = mark;
+    if (mark == 0) {
+      cudaEventRecord(ctx->scr_ev, s);
+      ctx->scr_ev_set = true;
+    }
   }
   template <typename T>
   T* get(int64_t count) {
     if (count <= 0) count = 1;
+    const size_t bytes = ((size_t)count * sizeof(T) + 255) / 256 * 256;
+    if (ctx && bytes <= kBumpMax && ctx->scr_used + bytes <= ctx->scr_cap) {
+      T* q = reinterpret_cast<T*>(ctx->scr + ctx->scr_used);
+      ctx->scr_used += bytes;
+      return q;
+    }
     void* p = nullptr;
     const cudaError_t e = pool_malloc(&p, (size_t)count * sizeof(T), s);
     if (e != cudaSuccess) {
@@ -313,10 +342,12 @@ struct Timer {
   bool on;
   int n = 0;
   float* slots[8] = {};
+  std::chrono::steady_clock::time_point host[8];  // host clock at each mark (TCUDB_HOST_TRACE=1)
   Timer(tcudb_ctx* c, cudaStream_t st, bool enable) : ctx(c), s(st), on(enable) {}
   void mark(float* out_ms) {
     if (!on || n >= 8) return;
     cudaEventRecord(ctx->ev[n], s);
+    host[n] = std::chrono::steady_clock::now();
     slots[n] = out_ms;
     ++n;
   }
@@ -324,10 +355,14 @@ struct Timer {
   void finish() {
     if (!on) return;
     if (n > 0) cudaEventSynchronize(ctx->ev[n - 1]);  // an early return may not have synced past it
+    static const bool trace = getenv("TCUDB_HOST_TRACE") && getenv("TCUDB_HOST_TRACE")[0] == '1';
     for (int i = 1; i < n; ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]);
       if (slots[i]) *slots[i] += ms;
+      if (trace)
+        fprintf(stderr, "tcudb trace: mark %d  device %.1f us  host %.1f us\n", i, ms * 1e3,
+                std::chrono::duration<double, std::micro>(host[i] - host[i - 1]).count());
     }
   }
 };
@@ -633,7 +668,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   out->agg_type = (is_float || is_avg) ? TCUDB_F64 : TCUDB_I64;
   if (nA == 0 || nB == 0) return TCUDB_OK;
 
-  Arena ar(s);
+  Arena ar(s, ctx);
   tm.mark(nullptr);
   // ---------------- a1: statistics
   ColDesc cols[6] = {ak, bk, ag, bh, av, bw};
@@ -2322,6 +2357,9 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   for (auto& e : c->evk) cudaEventCreate(&e);
+  cudaEventCreateWithFlags(&c->scr_ev, cudaEventDisableTiming);
+  if (cudaMalloc(&c->scr, kScratchBytes) == cudaSuccess) c->scr_cap = kScratchBytes;
+  else { cudaGetLastError(); c->scr = nullptr; }
   calibrate(c);  // selector constants (A19); cached per device and process
   if (nccl_comm) {
     std::string why;
@@ -2707,6 +2745,8 @@ void tcudb_destroy(tcudb_ctx* ctx) {
   if (ctx->pinned_big) cudaFreeHost(ctx->pinned_big);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->evk) if (e) cudaEventDestroy(e);
+  if (ctx->scr_ev) cudaEventDestroy(ctx->scr_ev);
+  if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->nc) nccl_detach(ctx->nc);
   cudaDeviceSynchronize();
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
