@@ -1051,3 +1051,40 @@ def test_hash_partitioned_sampled_group_dictionary(engine, torch_mod, oracle_mod
         assert st["spa_mode"] == 4
     else:
         assert st["spa_mode"] != 4
+
+
+# ---------------------------------------------------------------- asynchronous return
+# Without stats tcudb_join_agg returns while the result write still runs on the stream
+# (tcudb.h); the next query's scratch (the context's bump region) waits for the previous
+# query's event. Results must be right when read in stream order, across streams once the
+# reader's stream waits on the writer's, and for back-to-back queries on different streams.
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c1s", 1.0), ("c2", 0.2), ("c3", 1 / 16), ("c4", 1 / 1024),
+                                        ("c5", 1 / 64), ("c5s", 1 / 256)])
+def test_no_stats_async_return(engine, torch_mod, oracle_mod, name, scale):
+    A, B, agg = datagen.make_config(name, scale)
+    ref = oracle_mod.join_agg(A, B, agg)
+    out = engine.join_agg(to_dev(A, torch_mod), to_dev(B, torch_mod), agg)  # no stats: no final sync
+    compare(res_np(out), ref, agg, float_vals=name.startswith("c4"))
+
+
+def test_no_stats_back_to_back_streams(engine, torch_mod, oracle_mod):
+    torch = torch_mod
+    cases = [datagen.make_config("c2", 0.3), datagen.make_config("c1", 1.0), datagen.make_config("c5", 1 / 64),
+             datagen.make_config("c1s", 1.0)]
+    refs = [oracle_mod.join_agg(A, B, agg) for A, B, agg in cases]
+    dev = [(to_dev(A, torch), to_dev(B, torch), agg) for A, B, agg in cases]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for rep in range(3):
+        outs = []
+        for i, (dA, dB, agg) in enumerate(dev):  # alternate streams, no host sync in between
+            s = streams[i % 2]
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                outs.append(engine.join_agg(dA, dB, agg, stream=s))
+        # read every result on the default stream after it waits on both writers
+        cur = torch.cuda.current_stream()
+        for s in streams:
+            cur.wait_stream(s)
+        for out, ref, (_, _, agg) in zip(outs, refs, dev):
+            compare(res_np(out), ref, agg)
