@@ -56,6 +56,10 @@ struct tcudb_ctx {
   size_t mem_free0 = 0;        // free device memory at creation (path-selection budget)
   cudaEvent_t ev[8] = {};
   cudaEvent_t evk[2] = {};   // the sparse path's band kernel (roofline timing)
+  // side stream: the two tables' independent per-side work (hash-partitioned path: group
+  // dictionaries, group codes, partition passes) runs on the query stream and s2 at once
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t evf[2] = {};   // fork (query stream -> s2), join (s2 -> query stream)
   // query scratch: small allocations are bumped from one device block (no allocator call per
   // array: a small query makes ~50 of them); reused by the next query after scr_ev
   char* scr = nullptr;
@@ -419,6 +423,38 @@ struct QueryOut {
 // caller then runs the general path. Steps: group dictionaries (a2) -> two radix
 // passes on the key hash per side -> per-partition count (J, K; a4 selector) ->
 // per-partition expand into C (a7) -> compaction (a8).
+// Fork / join of the context's side stream around one table's independent work: s2 waits for
+// everything enqueued on the query stream so far (fork), the query stream for everything on
+// s2 (join). SideStream swaps the arena's stream inside its scope, so that table's launches,
+// memsets and pool allocations go to s2 (the arena still frees on the query stream, after the
+// join). Without a side stream both run on the query stream.
+struct SideStream {
+  Arena& ar;
+  cudaStream_t prev;
+  SideStream(Arena& a, cudaStream_t s2) : ar(a), prev(a.s) { if (s2) ar.s = s2; }
+  ~SideStream() { ar.s = prev; }
+};
+void side_fork(tcudb_ctx* ctx, cudaStream_t s) {
+  if (!ctx->s2) return;
+  Arena::ck(cudaEventRecord(ctx->evf[0], s));
+  Arena::ck(cudaStreamWaitEvent(ctx->s2, ctx->evf[0], 0));
+}
+void side_join(tcudb_ctx* ctx, cudaStream_t s) {
+  if (!ctx->s2) return;
+  Arena::ck(cudaEventRecord(ctx->evf[1], ctx->s2));
+  Arena::ck(cudaStreamWaitEvent(s, ctx->evf[1], 0));
+}
+// an error between fork and join: the query stream still waits for the side stream's work
+// before the arena's stream-ordered frees (no throw from the destructor)
+struct SideJoinGuard {
+  tcudb_ctx* ctx; cudaStream_t s; bool armed = false;
+  ~SideJoinGuard() {
+    if (!armed || !ctx->s2) return;
+    if (cudaEventRecord(ctx->evf[1], ctx->s2) == cudaSuccess) cudaStreamWaitEvent(s, ctx->evf[1], 0);
+    cudaGetLastError();
+  }
+};
+
 bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb_table* B, const ColDesc& ak,
                     const ColDesc& ag, const ColDesc& bk, const ColDesc& bh, const ColStats* hs, const double* est,
                     long long kmin, tcudb_result* out, tcudb_stats& S, Timer& tm, int64_t* L, cudaStream_t s,
@@ -432,8 +468,17 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   auto step_for = [](int64_t n) -> int64_t { return n >= (1 << 22) ? n >> 18 : 1; };
   const char* ns_env = getenv("TCUDB_NO_DICT_SAMPLE");
   const bool sample = !(ns_env && ns_env[0] == '1');
+  // A's dictionary on the query stream, B's on the side stream (two latency-bound builds at once)
+  const char* nss = getenv("TCUDB_NO_SIDE_STREAM");
+  cudaStream_t s2 = (nss && nss[0] == '1') ? nullptr : ctx->s2;
+  SideJoinGuard sjg{ctx, s};
+  if (s2) { side_fork(ctx, s); sjg.armed = true; }
   dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false, sample ? step_for(nA) : 1);
-  dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], false, sample ? step_for(nB) : 1);
+  {
+    SideStream side(ar, s2);
+    dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], false, sample ? step_for(nB) : 1);
+  }
+  if (s2) { side_join(ctx, s); sjg.armed = false; }
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
     int* hov = reinterpret_cast<int*>(hp + 2);
@@ -449,18 +494,11 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   }
   const int64_t G = DG.count, H = DH.count, ldc = round_up(H, 4);
   if ((double)G * (double)ldc * 4.0 > 0.3 * (double)ctx->mem_free0) return false;
-  dict_finish_group(ar, DG, L);
-  dict_finish_group(ar, DH, L);
   // per-tuple group codes by value from the finished dictionaries (a lookup inside the
   // partition pass measured slower: +0.2 ms on c5, the dependent table loads stall the
   // latency-bound scatter; here four lookups per thread are in flight)
-  int32_t* gA = ar.get<int32_t>(nA);
-  int32_t* hB = ar.get<int32_t>(nB);
   unsigned long long* d_max_miss = ar.zeros<unsigned long long>(2);  // [0] largest partition, [1] missed value
   int* d_miss = reinterpret_cast<int*>(d_max_miss + 1);
-  CK(launch_group_codes(ag, DG.view(), gA, s, L, d_miss));
-  CK(launch_group_codes(bh, DH.view(), hB, s, L, d_miss));
-  const int32_t* grp[2] = {gA, hB};
   // partitions: <= ~1 K tuples per side on average, two radix passes of <= 7 bits
   int pbits = 1;
   while (pbits < 14 && ((int64_t)1 << pbits) * 1024 < std::max(nA, nB)) ++pbits;
@@ -470,6 +508,8 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   Side sd[2];
   const ColDesc* vals[2] = {&av, &bw};  // integer SUM: value payload (absent column = 1)
   const ColDesc* keys[2] = {&ak, &bk};
+  const ColDesc* grpc[2] = {&ag, &bh};
+  Dict* dicts[2] = {&DG, &DH};
   const int64_t ns[2] = {nA, nB};
   int64_t* seg0 = ar.get<int64_t>(4);
   {
@@ -479,8 +519,16 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   }
   const char* hs_env = getenv("TCUDB_HASHPART_HISTSCAN");  // 1: the per-pass hist + scan partitioning
   const bool atomic_parts = !(hs_env && hs_env[0] == '1');
+  // each table's dictionary ranks, group codes and partition passes: A on the query stream,
+  // B on the side stream
+  if (s2) { side_fork(ctx, s); sjg.armed = true; }
   for (int x = 0; x < 2; ++x) {
+    SideStream side(ar, x ? s2 : nullptr);
+    const cudaStream_t ss = ar.s;
     const int64_t n = ns[x];
+    dict_finish_group(ar, *dicts[x], L);
+    int32_t* gcode = ar.get<int32_t>(n);
+    CK(launch_group_codes(*grpc[x], dicts[x]->view(), gcode, ss, L, d_miss));
     sd[x].k[0] = ar.get<unsigned long long>(n); sd[x].k[1] = ar.get<unsigned long long>(n);
     sd[x].g[0] = ar.get<int32_t>(n); sd[x].g[1] = ar.get<int32_t>(n);
     sd[x].v[0] = sum ? ar.get<long long>(n) : nullptr;
@@ -492,38 +540,39 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
       // start; both radix passes then reserve their runs with atomics (no per-pass
       // histogram and count scans; the order inside a partition is free)
       unsigned* hist = ar.zeros<unsigned>(P);
-      CK(launch_part_hist_all(*keys[x], kmin, pbits, hist, s, L));
+      CK(launch_part_hist_all(*keys[x], kmin, pbits, hist, ss, L));
       CK(exclusive_scan_i32(reinterpret_cast<const int32_t*>(hist), sd[x].seg2, P, sd[x].seg2 + P,
-                            ar.get<char>((int64_t)scan_temp_bytes(P)), s, L));
+                            ar.get<char>((int64_t)scan_temp_bytes(P)), ss, L));
       CK(cudaMemcpy2DAsync(sd[x].seg1, 8, sd[x].seg2, (size_t)8 << b2, 8, ((size_t)1 << b1) + 1,
-                           cudaMemcpyDeviceToDevice, s));
+                           cudaMemcpyDeviceToDevice, ss));
       unsigned long long* cur2 = ar.get<unsigned long long>(P);
-      CK(cudaMemcpyAsync(cur2, sd[x].seg2, (size_t)P * 8, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(cur2, sd[x].seg2, (size_t)P * 8, cudaMemcpyDeviceToDevice, ss));
       unsigned long long* cur1 = cur2;
       if (b2) {
         cur1 = ar.get<unsigned long long>((int64_t)1 << b1);
-        CK(cudaMemcpyAsync(cur1, sd[x].seg1, ((size_t)1 << b1) * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(cur1, sd[x].seg1, ((size_t)1 << b1) * 8, cudaMemcpyDeviceToDevice, ss));
       }
-      CK(launch_part_pass_atomic(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, cur1,
-                                 sd[x].k[0], sd[x].g[0], ar.get<char>((int64_t)hashpart_atomic_temp_bytes(1)), s, L,
+      CK(launch_part_pass_atomic(keys[x], kmin, gcode, nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, cur1,
+                                 sd[x].k[0], sd[x].g[0], ar.get<char>((int64_t)hashpart_atomic_temp_bytes(1)), ss, L,
                                  sum ? vals[x] : nullptr, nullptr, sd[x].v[0]));
       if (b2)
         CK(launch_part_pass_atomic(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits,
                                    b2, cur2, sd[x].k[1], sd[x].g[1],
-                                   ar.get<char>((int64_t)hashpart_atomic_temp_bytes(1 << b1)), s, L, nullptr,
+                                   ar.get<char>((int64_t)hashpart_atomic_temp_bytes(1 << b1)), ss, L, nullptr,
                                    sd[x].v[0], sd[x].v[1]));
       continue;
     }
     void* t1 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1, b1));
-    CK(launch_part_pass(keys[x], kmin, grp[x], nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
-                        sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, s, L, sum ? vals[x] : nullptr, nullptr,
+    CK(launch_part_pass(keys[x], kmin, gcode, nullptr, nullptr, seg0 + 2 * x, 1, n, 64 - b1, b1, sd[x].k[0],
+                        sd[x].g[0], b2 ? sd[x].seg1 : sd[x].seg2, t1, ss, L, sum ? vals[x] : nullptr, nullptr,
                         sd[x].v[0]));
     if (b2) {
       void* t2 = ar.get<char>((int64_t)hashpart_temp_bytes(n, 1 << b1, b2));
       CK(launch_part_pass(nullptr, 0, nullptr, sd[x].k[0], sd[x].g[0], sd[x].seg1, 1 << b1, n, 64 - pbits, b2,
-                          sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, s, L, nullptr, sd[x].v[0], sd[x].v[1]));
+                          sd[x].k[1], sd[x].g[1], sd[x].seg2, t2, ss, L, nullptr, sd[x].v[0], sd[x].v[1]));
     }
   }
+  if (s2) { side_join(ctx, s); sjg.armed = false; }
   const int fin = b2 ? 1 : 0;
   unsigned long long* d_out = ar.zeros<unsigned long long>(4 + 4 * (int64_t)P);
   unsigned long long* d_max = d_max_miss;
@@ -2358,6 +2407,8 @@ tcudb_status tcudb_create(tcudb_ctx** out, int device, void* nccl_comm, tcudb_al
   for (auto& e : c->ev) cudaEventCreate(&e);
   for (auto& e : c->evk) cudaEventCreate(&e);
   cudaEventCreateWithFlags(&c->scr_ev, cudaEventDisableTiming);
+  for (auto& e : c->evf) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess) { cudaGetLastError(); c->s2 = nullptr; }
   if (cudaMalloc(&c->scr, kScratchBytes) == cudaSuccess) c->scr_cap = kScratchBytes;
   else { cudaGetLastError(); c->scr = nullptr; }
   calibrate(c);  // selector constants (A19); cached per device and process
@@ -2746,6 +2797,8 @@ void tcudb_destroy(tcudb_ctx* ctx) {
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->evk) if (e) cudaEventDestroy(e);
   if (ctx->scr_ev) cudaEventDestroy(ctx->scr_ev);
+  for (auto& e : ctx->evf) if (e) cudaEventDestroy(e);
+  if (ctx->s2) cudaStreamDestroy(ctx->s2);
   if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->nc) nccl_detach(ctx->nc);
   cudaDeviceSynchronize();

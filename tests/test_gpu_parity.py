@@ -973,7 +973,7 @@ def test_hash_partition_pass_modes(engine, torch_mod, oracle_mod, monkeypatch, m
 
 # ---------------------------------------------------------------- a2 + a5 fused (fill_direct.cu)
 @pytest.mark.parametrize("case", ["dense_exact", "holes", "signed_exact", "signed_split", "dup", "dup_split",
-                                  "one_side_value", "ragged_kp"])
+                                  "one_side_value", "ragged_kp", "shifted_keys", "negative_groups"])
 @pytest.mark.parametrize("flags", [0, 1])
 def test_fused_direct_fill(engine, torch_mod, oracle_mod, monkeypatch, case, flags):
     """Deferred per-tuple codes (the c4 class, TCUDB_LAZY_CODES=1 lifts the size threshold):
@@ -985,7 +985,7 @@ def test_fused_direct_fill(engine, torch_mod, oracle_mod, monkeypatch, case, fla
     of two. Auto flags may pick the sparse path (codes materialized). All equal the oracle."""
     monkeypatch.setenv("TCUDB_LAZY_CODES", "1")
     rng = np.random.default_rng(["dense_exact", "holes", "signed_exact", "signed_split", "dup", "dup_split",
-                                 "one_side_value", "ragged_kp"].index(case) + 40)
+                                 "one_side_value", "ragged_kp", "shifted_keys", "negative_groups"].index(case) + 40)
     G, K = 600, (1000 if case == "ragged_kp" else 1024)
     cells = rng.permutation(G * K)
     ag, ak = (cells // K).astype(np.int32), (cells % K).astype(np.int32)
@@ -1008,6 +1008,10 @@ def test_fused_direct_fill(engine, torch_mod, oracle_mod, monkeypatch, case, fla
     bw = datagen._bf16_representable(rng.uniform(2.0 ** -8, 1.0, H * K).astype(np.float32))
     if case in ("signed_exact", "signed_split"):
         bw = -bw
+    if case == "shifted_keys":
+        ak, bk = ak + 50_000, bk + 50_000
+    elif case == "negative_groups":
+        ag, bh = ag - 5_000, bh - 70_000
     perm = rng.permutation(len(bk))
     A = datagen.Table(ak.astype(np.int32), ag.astype(np.int32), av)
     B = datagen.Table(bk[perm].astype(np.int32), bh[perm], None if case == "one_side_value" else bw[perm])
