@@ -840,9 +840,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       DK.pending_union = d_union;
       flush_codes(ar, {&DK, &DG, &DH}, L);
     } else {
+    // B's group dictionary and B's probe run on the side stream beside A's (small launches,
+    // each far from filling the device)
+    const char* nss = getenv("TCUDB_NO_SIDE_STREAM");
+    const cudaStream_t s2 = (nss && nss[0] == '1') ? nullptr : ctx->s2;
+    SideJoinGuard sjg{ctx, s};
+    if (s2) { side_fork(ctx, s); sjg.armed = true; }
     dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0], true, 1, true);
     dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], true, 1, true);
-    dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], true, 1, true);
+    {
+      SideStream side(ar, s2);
+      dict_build(ar, DH, bh, nullptr, hs[3].mn, hs[3].mx, false, nullptr, L, est[2], true, 1, true);
+    }
+    if (s2) { side_join(ctx, s); sjg.armed = false; }
     flush_codes(ar, {&DK, &DG, &DH}, L);  // direct dictionaries' code scans, batched
     // probe right away with upper-bound sizes (codes < span / capacity), so the dictionary
     // sizes and the join size J come back in ONE device->host read
@@ -852,8 +862,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     cntB = ar.zeros<int32_t>(Ku);
     rowA = int_sum ? ar.zeros<double>(Gu) : nullptr;
     rowB = int_sum ? ar.zeros<double>(Hu) : nullptr;
+    if (s2) { side_fork(ctx, s); sjg.armed = true; }
     CK(launch_probe(ak, ag, av, DK.view(1), DG.view(1), kA, gA, cntA, rowA, Ku, s, L));
-    CK(launch_probe(bk, bh, bw, DK.view(2), DH.view(1), kB, hB, cntB, rowB, Ku, s, L));
+    CK(launch_probe(bk, bh, bw, DK.view(2), DH.view(1), kB, hB, cntB, rowB, Ku, s2 ? s2 : s, L));
+    if (s2) { side_join(ctx, s); sjg.armed = false; }
     }
     unsigned long long* d_misc = ar.zeros<unsigned long long>(6);
     CK(launch_join_size(cntA, cntB, Ku, d_misc + 0, s, L));
@@ -1040,7 +1052,13 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double t_analysis = (double)(nA + nB) * 15e-12 + 100e-6;
   if (!bs_force && dense_ops / gemm_rate >= std::max(1.5e-3, 4.0 * t_analysis)) {
     const double bytes = (double)(Gp + Hp) * Kp * (is_float ? 2.0 : 1.0) + (double)Gp * Hp * (is_sum ? 8.0 : 2.0);
-    const double t_sp = (double)J / ctx->cal.R_sp + ctx->cal.T_sp0;
+    // the sparse paths' rate on large joins: the calibrated R_sp comes from J <= 2^23 pairs,
+    // where fixed costs weigh; at 10^8 pairs the band and partitioned kernels expand ~4-5x
+    // faster (c3 1.4e11, c5 1.3e11 pairs/s vs R_sp ~3.7e10). The analysis (~0.26 ms on c3) is
+    // skipped when block-sparse could not win even with no GEMM at all against that rate
+    // (c3: ~3 ms of operand + C bytes vs a 2.8 ms sparse query; the blocked c2b still runs it).
+    constexpr double kLargeJoinSpeedup = 5.0;
+    const double t_sp = (double)J / (kLargeJoinSpeedup * ctx->cal.R_sp) + ctx->cal.T_sp0;
     bs_worth = 3.0 * bytes / ctx->cal.BW < t_sp;
   }
   if (!bs_off && bs_worth && !(q->flags & TCUDB_FORCE_SPARSE) && K >= 64) {
