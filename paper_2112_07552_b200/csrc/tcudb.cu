@@ -1212,10 +1212,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     const char* fp4_always = getenv("TCUDB_FP4_ALWAYS");  // tests: e2m1 on small products too
     if (allow_fp4 && !is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24) &&
         (dense_ops >= 1e11 || (fp4_always && fp4_always[0] == '1'))) {
+      // A's operand zeroed and filled on the query stream, B's on the side stream
+      const char* nss = getenv("TCUDB_NO_SIDE_STREAM");
+      const cudaStream_t s2 = (nss && nss[0] == '1') ? nullptr : ctx->s2;
+      SideJoinGuard sjg{ctx, s};
+      if (s2) { side_fork(ctx, s); sjg.armed = true; }
       op4A = ar.zeros<uint8_t>(Gp * Kp4 / 2);
-      op4B = ar.zeros<uint8_t>(Hp * Kp4 / 2);
       CK(launch_fill_count_fp4(kA, gA, nA, op4A, Kp4, fs + 0, s, L));
-      CK(launch_fill_count_fp4(kB, hB, nB, op4B, Kp4, fs + 1, s, L));
+      {
+        SideStream side(ar, s2);
+        op4B = ar.zeros<uint8_t>(Hp * Kp4 / 2);
+        CK(launch_fill_count_fp4(kB, hB, nB, op4B, Kp4, fs + 1, ar.s, L));
+      }
+      if (s2) { side_join(ctx, s); sjg.armed = false; }
       fs4 = fs;  // checked at the result-size read below
     }
     if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE) && !force_wide) {
