@@ -16,7 +16,9 @@
 // Codes are ascending dense ranks, so row-major order is (g, h) order and the
 // ORDER BY comes for free (§3.4). Decode: g = dict_g[i], h = dict_h[j].
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
       }
     }
     int64_t base = off[s];
-    const long long gval = a.dict_g[row[q]];
+    const long long gval = GT < 2 ? a.dict_g[row[q]] : 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const bool nz = Cell<EK>::nz(e[q][j]);
@@ -121,8 +123,9 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
         const int64_t pos = base + __popc(m & lt);
         const long long hval = hv[q][j];
         // streaming (evict-first) stores: the result tuples are not re-read by the GPU
+        // (GT 2 / 3: the g column is written by k_fill_g, one vectorised run per row)
         if (GT == 1) __stcs(static_cast<long long*>(a.out_g) + pos, gval);
-        else __stcs(static_cast<int*>(a.out_g) + pos, (int)gval);
+        else if (GT == 0) __stcs(static_cast<int*>(a.out_g) + pos, (int)gval);
         if (HT == 1) __stcs(static_cast<long long*>(a.out_h) + pos, hval);
         else __stcs(static_cast<int*>(a.out_h) + pos, (int)hval);
         const VT x = SAME ? (VT)e[q][j] : v[q][j];
@@ -135,13 +138,58 @@ __global__ void __launch_bounds__(T) k_seg_write(const CompactArgs a, const int6
   }
 }
 
+// The g column of the result is constant along each row: row r's tuples occupy
+// [off[r * nseg], off[(r + 1) * nseg]) and all carry dict_g[r]. One warp per row writes that
+// run with aligned 16-byte stores (scalar head / tail), so the ordered write pass above stores
+// only h and agg.
+template <typename GV>
+__global__ void __launch_bounds__(T) k_fill_g(const CompactArgs a, const int64_t* __restrict__ off) {
+  constexpr int PER16 = 16 / sizeof(GV);
+  const int lane = lane_id();
+  GV* out = static_cast<GV*>(a.out_g);
+  for (int64_t r = (int64_t)blockIdx.x * WPB + warp_id(); r < a.G; r += (int64_t)gridDim.x * WPB) {
+    const int64_t b = off[r * a.nseg], e = off[(r + 1) * a.nseg];
+    if (b >= e) continue;
+    const GV g = (GV)a.dict_g[r];
+    // head up to 16-byte alignment, aligned body, tail
+    const int64_t mis = (int64_t)((reinterpret_cast<uintptr_t>(out + b) & 15) / sizeof(GV));
+    const int64_t b16 = min(e, b + (mis ? PER16 - mis : 0));
+    if (b + lane < b16) __stcs(out + b + lane, g);
+    const int64_t nv = (e - b16) / PER16;
+    uint4 w;
+    if (sizeof(GV) == 4) w = make_uint4((unsigned)g, (unsigned)g, (unsigned)g, (unsigned)g);
+    else w = make_uint4((unsigned)(long long)g, (unsigned)((unsigned long long)(long long)g >> 32),
+                        (unsigned)(long long)g, (unsigned)((unsigned long long)(long long)g >> 32));
+    uint4* o4 = reinterpret_cast<uint4*>(out + b16);
+    for (int64_t i = lane; i < nv; i += 32) __stcs(o4 + i, w);
+    for (int64_t i = b16 + nv * PER16 + lane; i < e; i += 32) __stcs(out + i, g);
+  }
+}
+
 template <int EK, int VK, bool SAME>
-void launch_write_t(const CompactArgs& a, const int64_t* off, int grid, cudaStream_t s) {
-  const int sel = a.g_out_type * 2 + a.h_out_type;
-  if (sel == 0) k_seg_write<EK, VK, SAME, 0, 0><<<grid, T, 0, s>>>(a, off);
-  else if (sel == 1) k_seg_write<EK, VK, SAME, 0, 1><<<grid, T, 0, s>>>(a, off);
-  else if (sel == 2) k_seg_write<EK, VK, SAME, 1, 0><<<grid, T, 0, s>>>(a, off);
-  else k_seg_write<EK, VK, SAME, 1, 1><<<grid, T, 0, s>>>(a, off);
+int launch_write_t(const CompactArgs& a, const int64_t* off, int grid, cudaStream_t s) {
+  // g in its own pass for the dense e2m1 COUNT results (u16 cells, long rows): aligned vector
+  // runs instead of a 4 / 8-byte store per tuple (c2: compaction 0.378 -> 0.370 ms; on c4 / c5
+  // measured within noise, so only here — scripts/gpu_fillg.sh)
+  static const bool no_fg = getenv("TCUDB_NO_FILL_G") && getenv("TCUDB_NO_FILL_G")[0] == '1';
+  const bool fill_g = !no_fg && EK == 4 && a.nseg >= 8;
+  const int sel = (fill_g ? 4 : 0) + a.g_out_type * 2 + a.h_out_type;
+  switch (sel) {
+    case 0: k_seg_write<EK, VK, SAME, 0, 0><<<grid, T, 0, s>>>(a, off); break;
+    case 1: k_seg_write<EK, VK, SAME, 0, 1><<<grid, T, 0, s>>>(a, off); break;
+    case 2: k_seg_write<EK, VK, SAME, 1, 0><<<grid, T, 0, s>>>(a, off); break;
+    case 3: k_seg_write<EK, VK, SAME, 1, 1><<<grid, T, 0, s>>>(a, off); break;
+    case 4: k_seg_write<EK, VK, SAME, 2, 0><<<grid, T, 0, s>>>(a, off); break;
+    case 5: k_seg_write<EK, VK, SAME, 2, 1><<<grid, T, 0, s>>>(a, off); break;
+    case 6: k_seg_write<EK, VK, SAME, 3, 0><<<grid, T, 0, s>>>(a, off); break;
+    default: k_seg_write<EK, VK, SAME, 3, 1><<<grid, T, 0, s>>>(a, off); break;
+  }
+  if (fill_g) {
+    const int gg = (int)std::min<int64_t>((a.G + WPB - 1) / WPB, (int64_t)kNumSMs * 8);
+    if (a.g_out_type) k_fill_g<long long><<<std::max(gg, 1), T, 0, s>>>(a, off);
+    else k_fill_g<int><<<std::max(gg, 1), T, 0, s>>>(a, off);
+  }
+  return fill_g ? 2 : 1;  // kernels launched
 }
 
 inline int grid_for_segs(int64_t nsegs) {
@@ -184,35 +232,36 @@ cudaError_t launch_compact_write(const CompactArgs& a, void* temp, cudaStream_t 
   const int64_t* off = reinterpret_cast<const int64_t*>(static_cast<char*>(temp) + ((size_t)n * 4 + 15) / 16 * 16);
   const int grid = grid_for_segs(n);
   const bool same = a.E == a.V && a.e_kind == a.v_kind && a.lde == a.ldv;
+  int nk = 1;
   if (same) {
     switch (a.e_kind) {
-      case 0: launch_write_t<0, 0, true>(a, off, grid, s); break;
-      case 1: launch_write_t<1, 1, true>(a, off, grid, s); break;
-      case 2: launch_write_t<2, 2, true>(a, off, grid, s); break;
-      case 4: launch_write_t<4, 4, true>(a, off, grid, s); break;
-      default: launch_write_t<3, 3, true>(a, off, grid, s);
+      case 0: nk = launch_write_t<0, 0, true>(a, off, grid, s); break;
+      case 1: nk = launch_write_t<1, 1, true>(a, off, grid, s); break;
+      case 2: nk = launch_write_t<2, 2, true>(a, off, grid, s); break;
+      case 4: nk = launch_write_t<4, 4, true>(a, off, grid, s); break;
+      default: nk = launch_write_t<3, 3, true>(a, off, grid, s);
     }
   } else {
     // separate existence planes: int32 counts (u8 pattern GEMM) or u16 (e2m1 pattern GEMM)
     if (a.e_kind == 0) {
       switch (a.v_kind) {
-        case 0: launch_write_t<0, 0, false>(a, off, grid, s); break;
-        case 1: launch_write_t<0, 1, false>(a, off, grid, s); break;
-        case 2: launch_write_t<0, 2, false>(a, off, grid, s); break;
-        default: launch_write_t<0, 3, false>(a, off, grid, s);
+        case 0: nk = launch_write_t<0, 0, false>(a, off, grid, s); break;
+        case 1: nk = launch_write_t<0, 1, false>(a, off, grid, s); break;
+        case 2: nk = launch_write_t<0, 2, false>(a, off, grid, s); break;
+        default: nk = launch_write_t<0, 3, false>(a, off, grid, s);
       }
     } else if (a.e_kind == 4) {
       switch (a.v_kind) {
-        case 0: launch_write_t<4, 0, false>(a, off, grid, s); break;
-        case 1: launch_write_t<4, 1, false>(a, off, grid, s); break;
-        case 2: launch_write_t<4, 2, false>(a, off, grid, s); break;
-        default: launch_write_t<4, 3, false>(a, off, grid, s);
+        case 0: nk = launch_write_t<4, 0, false>(a, off, grid, s); break;
+        case 1: nk = launch_write_t<4, 1, false>(a, off, grid, s); break;
+        case 2: nk = launch_write_t<4, 2, false>(a, off, grid, s); break;
+        default: nk = launch_write_t<4, 3, false>(a, off, grid, s);
       }
     } else {
       return cudaErrorInvalidValue;
     }
   }
-  if (launches) ++*launches;
+  if (launches) *launches += nk;
   return cudaGetLastError();
 }
 
