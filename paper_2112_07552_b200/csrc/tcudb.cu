@@ -1655,7 +1655,18 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       w_kind = is_float ? 2 : 1;
       b_w = is_float ? (void*)ar.get<float>(nB) : (void*)ar.get<long long>(nB);
     }
-    CK(launch_bucket_fill(kB, hB, bw, nB, bstart, cursor, b_h, b_w, w_kind, s, L));
+    // B's buckets on the side stream while A's active tuples are gathered on the query stream
+    // (joined before the first kernel that reads the buckets)
+    const char* nss_b = getenv("TCUDB_NO_SIDE_STREAM");
+    const cudaStream_t s2b = (nss_b && nss_b[0] == '1') ? nullptr : ctx->s2;
+    SideJoinGuard bucket_guard{ctx, s};
+    if (s2b) { side_fork(ctx, s); bucket_guard.armed = true; }
+    CK(launch_bucket_fill(kB, hB, bw, nB, bstart, cursor, b_h, b_w, w_kind, s2b ? s2b : s, L));
+    auto join_buckets = [&]() {
+      if (!bucket_guard.armed) return;
+      side_join(ctx, s);
+      bucket_guard.armed = false;
+    };
     int32_t* act_a = ar.get<int32_t>(nA);
     int32_t* act_w = ar.zeros<int32_t>(nA);
     const int64_t ldc_ = round_up(H, 4);
@@ -1685,6 +1696,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       sa.act_b = act_b; sa.act_g = act_g;
       int64_t* act_off = ar.get<int64_t>(nA + 1);
       CK(exclusive_scan_i32(act_w, act_off, nA, act_off + nA, tmp, s, L));
+      join_buckets();
       sa.goff = goff; sa.act_a = act_a; sa.act_off = act_off;
       sa.kcodeA = kA; sa.gcodeA = gA; sa.va = av;
       sa.bstart = bstart; sa.b_h = b_h; sa.b_w = b_w; sa.w_kind = w_kind;
@@ -1788,6 +1800,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       CK(launch_compact_active(work, pos, nA, act_a, act_w, s, L));
     }
     if (!spa) {
+    join_buckets();
     int64_t* act_off = ar.get<int64_t>(nA);
     CK(exclusive_scan_i32(act_w, act_off, nA, nullptr, tmp, s, L));
     const int64_t ldc = round_up(H, 4);
