@@ -77,7 +77,14 @@ struct KParams {
   const unsigned long long* bmA;
   const unsigned long long* bmB;
   int bmw;
+  const int* abort_a; const int* abort_b;  // GemmArgs::abort_a / abort_b
 };
+
+// the optimistic fill failed (GemmArgs::abort_a / abort_b): every thread of every CTA sees the
+// same flags, so the whole grid leaves before any barrier, TMEM allocation or cluster sync
+__device__ __forceinline__ bool gemm_aborted(const KParams& p) {
+  return p.abort_a && (__ldcg(p.abort_a) | __ldcg(p.abort_b)) != 0;
+}
 
 // Calls f(kb, first) for the K-blocks of tile (mb, nb) in ascending order: all of them
 // (dense), or those active in both operands' block bitmaps. Returns the count.
@@ -409,6 +416,7 @@ __global__ void __launch_bounds__(CMP ? NUM_THREADS + 32 * CMP_WARPS : NUM_THREA
 
   const int warp = warp_id(), lane = lane_id();
   const int num_tiles = p.tiles_m * p.tiles_n;
+  if (gemm_aborted(p)) return;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -605,6 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const bool leader = rank == 0;
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
   const int num_tiles = p.tiles_m * p.tiles_n;  // pair tiles (256 x BN_)
+  if (gemm_aborted(p)) return;  // both CTAs of the pair read the same flags
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -823,6 +832,7 @@ cudaError_t launch_gemm_fp4(const GemmArgs& a, cudaStream_t s, int64_t* launches
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   p.group_m = pick_group_m(p.tiles_m, BM, a.k_len);
   p.bmA = a.bmA; p.bmB = a.bmB; p.bmw = a.bmw;
+  p.abort_a = a.abort_a; p.abort_b = a.abort_b ? a.abort_b : a.abort_a;
   if (a.cmp && a.bmA) return cudaErrorInvalidValue;  // fused compaction needs every tile's epilogue
   // CTA-pair kernel (cta_group::2, 256 x 240 pair tiles): each SM stages 128 A rows + 120 B rows
   // per K-block instead of 128 + 240 (a third less L2 -> SM traffic per MAC). Default when M
@@ -894,6 +904,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s, int64_t* launches) {
   p.cnt_out = a.cnt_out; p.ldcnt = a.ldcnt;
   p.group_m = pick_group_m(p.tiles_m, pair ? 256 : BM, a.k_len * esz);
   p.bmA = a.bmA; p.bmB = a.bmB; p.bmw = a.bmw;
+  p.abort_a = a.abort_a; p.abort_b = a.abort_b ? a.abort_b : a.abort_a;
   if (!pair) return run_1cta<BN, false>(a, p, a.elem, kb, s, launches);
   const int64_t kcols = a.k_begin + a.k_len;
   CUtensorMap mA, mB;

@@ -40,6 +40,10 @@ struct GemmArgs {
   // optional: per (row, 256-column N tile) count of nonzero results, cnt[row * ldcnt + n_tile]
   // (feeds the compaction scan, a8; only on the launch that produces the final matrix)
   int32_t* cnt_out = nullptr; int64_t ldcnt = 0;
+  // optional: the optimistic fill's overflow flags (device ints). When either is set the
+  // operands are not exact, the host reruns the matrix stage one type wider, and this launch
+  // exits at once instead of multiplying them
+  const int* abort_a = nullptr; const int* abort_b = nullptr;
   // optional (fp4 COUNT with EPI_STORE16): compaction (a8) fused into the GEMM kernel —
   // the result tuples are written in (g, h) order by compaction warps while later tiles
   // are still being multiplied (see gemm_tc.cu). Scratch arrays are zeroed by the caller.

@@ -1111,7 +1111,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   const double dense_bytes = (double)(Gp + Hp) * Kp * esz * (is_float ? 4 : (is_sum ? 8 : 1)) +
                              (double)(Gp + Hp) * Kp * (is_sum ? (is_float ? 4 : 8) : 0) + (double)Gp * Hp * 8;
   const double sparse_bytes = (double)G * H * csz * (need_exist ? 1.5 : 1.0) + (double)(nA + nB) * 32;
-  const double t_dense = planes_est * dense_ops * (use_bs ? bs_frac : 1.0) / R_tc + 3.0 * dense_bytes / BW + cb.T_d0;
+  // every plane past the first (digit planes, the existence pattern) is another fill, GEMM
+  // launch and int64 accumulation pass: T_d0 (measured on a one-plane COUNT) per plane
+  const double t_dense = planes_est * dense_ops * (use_bs ? bs_frac : 1.0) / R_tc + 3.0 * dense_bytes / BW +
+                         planes_est * cb.T_d0;
   const double t_sparse = (double)J / R_sp + sparse_bytes / BW + T_sp0;
   // memory budget: the device's free memory when the context was created, re-read live
   // (cudaMemGetInfo: 0.3 ms to tens of ms of host time) only when a path's footprint comes
@@ -1533,7 +1536,9 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         d_fc_total = fcmp.total;
       }
       if (!ga.cmp) with_bs(ga, 3, Kp4 / 256, Kp4 / 256);
+      ga.abort_a = &fs4[0].overflow; ga.abort_b = &fs4[1].overflow;  // a duplicate cell: u8 rerun
       CK(launch_gemm(ga, s, L));
+      ga.abort_a = ga.abort_b = nullptr;
       ops += 2.0 * Gp * Hc * Kp4;
       ca.E = C; ca.e_kind = c16 ? 4 : 0; ca.lde = Hc; ca.V = C; ca.v_kind = ca.e_kind; ca.ldv = Hc;
       S.elem = 3;
@@ -1586,7 +1591,9 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
         ga.k_begin = 0; ga.k_len = Kp; ga.epi = EPI_STORE32; ga.C = C; ga.ldc = Hp;
         ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
         with_bs(ga, 0, Kp / 128, Kp / 128);
+        if (fs8) { ga.abort_a = &fs8[0].overflow; ga.abort_b = &fs8[1].overflow; }  // a u8 carry: wide rerun
         CK(launch_gemm(ga, s, L));
+        ga.abort_a = ga.abort_b = nullptr;
         ops += dense_ops;
         ca.E = C; ca.e_kind = 0; ca.lde = Hp; ca.V = C; ca.v_kind = 0; ca.ldv = Hp;
       } else {
