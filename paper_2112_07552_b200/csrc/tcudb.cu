@@ -302,8 +302,13 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
       }
     }
     d.code = ar.get<int32_t>((int64_t)cap);
-    void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)cap));
-    CK(launch_pred_codes(d.fa, d.fb, (int64_t)cap, d.code, d.count_dev, union_dev, nullptr, 0, tmp, s, launches));
+    if (defer_codes) {  // batched with the other dictionaries' code scans (flush_codes)
+      d.pending = true;
+      d.pending_union = union_dev;
+    } else {
+      void* tmp = ar.get<char>((int64_t)pred_temp_bytes((int64_t)cap));
+      CK(launch_pred_codes(d.fa, d.fb, (int64_t)cap, d.code, d.count_dev, union_dev, nullptr, 0, tmp, s, launches));
+    }
   }
 }
 
@@ -444,6 +449,12 @@ void side_join(tcudb_ctx* ctx, cudaStream_t s) {
   Arena::ck(cudaEventRecord(ctx->evf[1], ctx->s2));
   Arena::ck(cudaStreamWaitEvent(s, ctx->evf[1], 0));
 }
+// The side stream for a query of n tuples: the fork / join costs host calls (event record +
+// wait, ~2 x 2 us) that only pay off when the per-table kernels are not tiny
+inline cudaStream_t side_stream_for(const tcudb_ctx* ctx, int64_t n) {
+  static const bool off = getenv("TCUDB_NO_SIDE_STREAM") && getenv("TCUDB_NO_SIDE_STREAM")[0] == '1';
+  return (off || n < (1 << 16)) ? nullptr : ctx->s2;
+}
 // an error between fork and join: the query stream still waits for the side stream's work
 // before the arena's stream-ordered frees (no throw from the destructor)
 struct SideJoinGuard {
@@ -469,8 +480,7 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   const char* ns_env = getenv("TCUDB_NO_DICT_SAMPLE");
   const bool sample = !(ns_env && ns_env[0] == '1');
   // A's dictionary on the query stream, B's on the side stream (two latency-bound builds at once)
-  const char* nss = getenv("TCUDB_NO_SIDE_STREAM");
-  cudaStream_t s2 = (nss && nss[0] == '1') ? nullptr : ctx->s2;
+  cudaStream_t s2 = side_stream_for(ctx, nA + nB);
   SideJoinGuard sjg{ctx, s};
   if (s2) { side_fork(ctx, s); sjg.armed = true; }
   dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false, sample ? step_for(nA) : 1);
@@ -842,8 +852,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     } else {
     // B's group dictionary and B's probe run on the side stream beside A's (small launches,
     // each far from filling the device)
-    const char* nss = getenv("TCUDB_NO_SIDE_STREAM");
-    const cudaStream_t s2 = (nss && nss[0] == '1') ? nullptr : ctx->s2;
+    const cudaStream_t s2 = side_stream_for(ctx, nA + nB);
     SideJoinGuard sjg{ctx, s};
     if (s2) { side_fork(ctx, s); sjg.armed = true; }
     dict_build(ar, DK, ak, &bk, kmin, kmax, true, d_union, L, est[0], true, 1, true);
@@ -912,8 +921,18 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   if (K == 0 || J == 0) { tm.finish(); return TCUDB_OK; }
   // hash-mode group domains: ascending ranks; the per-tuple codes issued by the probe
   // (compaction order) are remapped so row/column order = (g, h) order
-  dict_finish_group(ar, DG, L, gA, nA);
-  dict_finish_group(ar, DH, L, hB, nB);
+  {
+    // B's group ranks on the side stream beside A's
+    const cudaStream_t s2 = side_stream_for(ctx, nA + nB);
+    SideJoinGuard sjg{ctx, s};
+    if (s2) { side_fork(ctx, s); sjg.armed = true; }
+    dict_finish_group(ar, DG, L, gA, nA);
+    {
+      SideStream side(ar, s2);
+      dict_finish_group(ar, DH, L, hB, nB);
+    }
+    if (s2) { side_join(ctx, s); sjg.armed = false; }
+  }
 
   // ---------------- a3 (integer bound) + a4 selector
   auto col_absmax = [&](int c) -> long double {
@@ -1216,8 +1235,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     if (allow_fp4 && !is_sum && !(q->flags & (TCUDB_FORCE_WIDE | TCUDB_NO_FP4)) && ctx->fp4 && K < (1 << 24) &&
         (dense_ops >= 1e11 || (fp4_always && fp4_always[0] == '1'))) {
       // A's operand zeroed and filled on the query stream, B's on the side stream
-      const char* nss = getenv("TCUDB_NO_SIDE_STREAM");
-      const cudaStream_t s2 = (nss && nss[0] == '1') ? nullptr : ctx->s2;
+      const cudaStream_t s2 = side_stream_for(ctx, nA + nB);
       SideJoinGuard sjg{ctx, s};
       if (s2) { side_fork(ctx, s); sjg.armed = true; }
       op4A = ar.zeros<uint8_t>(Gp * Kp4 / 2);
@@ -1231,10 +1249,19 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       fs4 = fs;  // checked at the result-size read below
     }
     if (!op4A && !is_sum && !(q->flags & TCUDB_FORCE_WIDE) && !force_wide) {
-      opA = ar.zeros<uint8_t>(cellsA);
-      opB = ar.zeros<uint8_t>(cellsB);
-      CK(launch_fill_count_u8(kA, gA, nA, opA, Kp, fs + 0, s, L));
-      CK(launch_fill_count_u8(kB, hB, nB, opB, Kp, fs + 1, s, L));
+      {
+        const cudaStream_t s2 = side_stream_for(ctx, nA + nB);
+        SideJoinGuard sjg{ctx, s};
+        if (s2) { side_fork(ctx, s); sjg.armed = true; }
+        opA = ar.zeros<uint8_t>(cellsA);
+        CK(launch_fill_count_u8(kA, gA, nA, opA, Kp, fs + 0, s, L));
+        {
+          SideStream side(ar, s2);
+          opB = ar.zeros<uint8_t>(cellsB);
+          CK(launch_fill_count_u8(kB, hB, nB, opB, Kp, fs + 1, ar.s, L));
+        }
+        if (s2) { side_join(ctx, s); sjg.armed = false; }
+      }
       if (Kp <= 32768) {
         // u8 cells <= 255: every int32 partial of one pass over Kp <= 32 K is exact
         // (255·255·32768 < 2^31), so the GEMM need not wait for the cell maxima
@@ -1664,8 +1691,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     }
     // B's buckets on the side stream while A's active tuples are gathered on the query stream
     // (joined before the first kernel that reads the buckets)
-    const char* nss_b = getenv("TCUDB_NO_SIDE_STREAM");
-    const cudaStream_t s2b = (nss_b && nss_b[0] == '1') ? nullptr : ctx->s2;
+    const cudaStream_t s2b = side_stream_for(ctx, nA + nB);
     SideJoinGuard bucket_guard{ctx, s};
     if (s2b) { side_fork(ctx, s); bucket_guard.armed = true; }
     CK(launch_bucket_fill(kB, hB, bw, nB, bstart, cursor, b_h, b_w, w_kind, s2b ? s2b : s, L));
