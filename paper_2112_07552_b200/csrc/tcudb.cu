@@ -262,7 +262,7 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
   const int64_t n = c1.n + (c2 ? c2->n : 0);
   const unsigned __int128 span = (unsigned __int128)((unsigned long long)mx - (unsigned long long)mn) + 1;
   d.minv = mn;
-  d.count_dev = ar.get<int64_t>(1);
+  if (!d.count_dev) d.count_dev = ar.get<int64_t>(1);
   {
     const unsigned long long sm1 = (unsigned long long)mx - (unsigned long long)mn;
     int b = 8;
@@ -287,7 +287,7 @@ void dict_build(Arena& ar, Dict& d, const ColDesc& c1, const ColDesc* c2, long l
     d.slots = ar.get<unsigned long long>((int64_t)cap);
     CK(cudaMemsetAsync(d.slots, 0xFF, cap * sizeof(unsigned long long), s));
     d.fa = ar.zeros<uint8_t>((int64_t)cap);
-    d.ovf = ar.zeros<int>(1);
+    if (!d.ovf) d.ovf = ar.zeros<int>(1);
     // per-row slots: the probe then reads code[slot] instead of rehashing and walking the table
     d.slot1 = row_slots ? ar.get<int32_t>(c1.n) : nullptr;
     CK(launch_hash_insert(c1, mn, d.slots, cap - 1, d.fa, d.ovf, d.slot1, est_distinct, d.wide, s, launches,
@@ -798,7 +798,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       tm.mark(nullptr);
     }
   }
-  unsigned long long* d_union = ar.zeros<unsigned long long>(1);
+  unsigned long long* d_union = nullptr;  // |∪ keys| counter (in the encode block below)
   Dict DK, DG, DH;
   // sum |v| per group: the integer-SUM overflow bound of the guard (fp64; non-negative, so
   // its bit pattern orders like an unsigned integer for the max reduction)
@@ -832,6 +832,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
            hsp <= kDirectSpanMax && direct_count_ok(ksp, std::max(gsp, hsp));
   }
   for (int attempt = 0; attempt < 2; ++attempt) {
+    // the sizes, join size, guard bounds and overflow flags the host reads after the encode
+    // sit in one zeroed block: one device->host copy instead of eight
+    // [0..2] K, G, H counts | [3] |∪ keys| | [4..9] misc | [10..11] three int overflow flags
+    int64_t* eblk = ar.zeros<int64_t>(12);
+    DK.count_dev = eblk + 0; DG.count_dev = eblk + 1; DH.count_dev = eblk + 2;
+    DK.ovf = reinterpret_cast<int*>(eblk + 10);
+    DG.ovf = DK.ovf + 1;
+    DH.ovf = DK.ovf + 2;
+    d_union = reinterpret_cast<unsigned long long*>(eblk + 3);
     double* rowA = nullptr;
     double* rowB = nullptr;
     int64_t Ku, Gu = 0, Hu = 0;
@@ -876,23 +885,15 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     CK(launch_probe(bk, bh, bw, DK.view(2), DH.view(1), kB, hB, cntB, rowB, Ku, s2 ? s2 : s, L));
     if (s2) { side_join(ctx, s); sjg.armed = false; }
     }
-    unsigned long long* d_misc = ar.zeros<unsigned long long>(6);
+    unsigned long long* d_misc = reinterpret_cast<unsigned long long*>(eblk + 4);
     CK(launch_join_size(cntA, cntB, Ku, d_misc + 0, s, L));
     if (int_sum) {
       CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowA), Gu, d_misc + 1, s, L));
       CK(launch_max_u64(reinterpret_cast<unsigned long long*>(rowB), Hu, d_misc + 2, s, L));
     }
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
-    int* hov = reinterpret_cast<int*>(hp + 12);
-    hov[0] = hov[1] = hov[2] = 0;
-    CK(cudaMemcpyAsync(hp + 0, DK.count_dev, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 1, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 2, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 3, d_union, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 4, d_misc, 48, cudaMemcpyDeviceToHost, s));
-    if (DK.ovf) CK(cudaMemcpyAsync(hov + 0, DK.ovf, 4, cudaMemcpyDeviceToHost, s));
-    if (DG.ovf) CK(cudaMemcpyAsync(hov + 1, DG.ovf, 4, cudaMemcpyDeviceToHost, s));
-    if (DH.ovf) CK(cudaMemcpyAsync(hov + 2, DH.ovf, 4, cudaMemcpyDeviceToHost, s));
+    const int* hov = reinterpret_cast<const int*>(hp + 10);
+    CK(cudaMemcpyAsync(hp, eblk, 12 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     DK.count = hp[0]; DG.count = hp[1]; DH.count = hp[2];
     S.K_union = hp[3];
@@ -900,7 +901,6 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     if (!hov[0] && !hov[1] && !hov[2]) break;
     // an estimate was far too small (table full): rebuild sized by the tuple counts
     est[0] = est[1] = est[2] = 0;
-    CK(cudaMemsetAsync(d_union, 0, 8, s));
     DK = Dict(); DG = Dict(); DH = Dict();
   }
   const int64_t K = DK.count, G = DG.count, H = DH.count;
