@@ -481,6 +481,11 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   const bool sample = !(ns_env && ns_env[0] == '1');
   // A's dictionary on the query stream, B's on the side stream (two latency-bound builds at once)
   cudaStream_t s2 = side_stream_for(ctx, nA + nB);
+  // both dictionaries' sizes and overflow flags in one zeroed block: one host read
+  int64_t* hblk = ar.zeros<int64_t>(3);
+  DG.count_dev = hblk; DH.count_dev = hblk + 1;
+  DG.ovf = reinterpret_cast<int*>(hblk + 2);
+  DH.ovf = DG.ovf + 1;
   SideJoinGuard sjg{ctx, s};
   if (s2) { side_fork(ctx, s); sjg.armed = true; }
   dict_build(ar, DG, ag, nullptr, hs[2].mn, hs[2].mx, false, nullptr, L, est[1], false, sample ? step_for(nA) : 1);
@@ -491,12 +496,8 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   if (s2) { side_join(ctx, s); sjg.armed = false; }
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
-    int* hov = reinterpret_cast<int*>(hp + 2);
-    hov[0] = hov[1] = 0;
-    CK(cudaMemcpyAsync(hp + 0, DG.count_dev, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 1, DH.count_dev, 8, cudaMemcpyDeviceToHost, s));
-    if (DG.ovf) CK(cudaMemcpyAsync(hov + 0, DG.ovf, 4, cudaMemcpyDeviceToHost, s));
-    if (DH.ovf) CK(cudaMemcpyAsync(hov + 1, DH.ovf, 4, cudaMemcpyDeviceToHost, s));
+    const int* hov = reinterpret_cast<const int*>(hp + 2);
+    CK(cudaMemcpyAsync(hp, hblk, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (hov[0] || hov[1]) return false;
     DG.count = hp[0];
@@ -1219,7 +1220,8 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     bool pat4 = false;                              // ... as e2m1 0/1 operands
     int PA = 1, PB = 1, sA = 0, sB = 0;
     unsigned long long maxA = 1, maxB = 1;          // max |digit-plane value| for the int32 chunk bound
-    FillStats* fs = ar.zeros<FillStats>(2);
+    // fill flags of A and B; the third slot receives the result size (one host read, below)
+    FillStats* fs = ar.zeros<FillStats>(3);
     int64_t ldop = Kp;                              // elements per operand row
     int64_t k_len = Kp;
     const int64_t cellsA = Gp * Kp, cellsB = Hp * Kp;
@@ -1869,19 +1871,28 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
 
   // ---------------- a8 compaction
   ctmp = (spa || dense_fc) ? nullptr : ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
-  d_nnz = dense_fc ? d_fc_total : spa_one ? sa.total : spa ? const_cast<int64_t*>(sa.row_out) + G : ar.get<int64_t>(1);
+  // the optimistic fills' flags and the result size in one host read: the scan writes the
+  // size into the flags' third slot
+  FillStats* fsx = fs4 ? fs4 : fs8;
+  const bool nnz_in_fs = fsx && !spa && !dense_fc;
+  d_nnz = dense_fc ? d_fc_total : spa_one ? sa.total : spa ? const_cast<int64_t*>(sa.row_out) + G
+        : nnz_in_fs ? reinterpret_cast<int64_t*>(fsx + 2) : ar.get<int64_t>(1);
   if (!spa && !dense_fc) CK(launch_compact_count(ca, seg_cnt, d_nnz, ctmp, s, L));
   {
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
     int* hov = reinterpret_cast<int*>(hp + 1);
     FillStats* hfs = reinterpret_cast<FillStats*>(hp + 2);
     *hov = 0;
-    CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
+    if (nnz_in_fs) {
+      CK(cudaMemcpyAsync(hfs, fsx, sizeof(FillStats) * 3, cudaMemcpyDeviceToHost, s));
+    } else {
+      CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
+      if (fsx) CK(cudaMemcpyAsync(hfs, fsx, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
+    }
     if (sparse_u16.acc_kind == 4) CK(cudaMemcpyAsync(hov, sparse_u16.ovf, 4, cudaMemcpyDeviceToHost, s));
     if (spa_hub) CK(cudaMemcpyAsync(hov, sa.ovf, 4, cudaMemcpyDeviceToHost, s));
-    if (fs4) CK(cudaMemcpyAsync(hfs, fs4, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
-    if (fs8) CK(cudaMemcpyAsync(hfs, fs8, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (nnz_in_fs) std::memcpy(hp, hfs + 2, sizeof(int64_t));
     nnz = hp[0];
     if ((fs4 || fs8) && (hfs[0].overflow || hfs[1].overflow)) {
       // e2m1: a (g, k) or (h, k) cell holds two tuples (not 0/1) — rerun on u8;
