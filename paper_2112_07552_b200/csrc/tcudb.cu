@@ -1520,8 +1520,10 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
     // the GEMM that produces the existence matrix also emits per-(row, N-tile) nonzero counts
     ca.nseg = Hp / 256;
     ca.seg_w = 256;
-    if (op4A || pat4) {  // segments follow the e2m1 GEMM's 240-column N tiles
-      ca.nseg = (Hp + kGemmBNFp4 - 1) / kGemmBNFp4;
+    if (op4A || pat4) {  // segments follow the e2m1 GEMM's 240-column N tiles, over the H real
+      // columns (a tile of Hp's padding alone would be a whole tile of zero products: c2's
+      // 43rd of 43)
+      ca.nseg = (std::max<int64_t>(H, 1) + kGemmBNFp4 - 1) / kGemmBNFp4;
       ca.seg_w = kGemmBNFp4;
     }
     seg_cnt = ar.get<int32_t>(Gp * ca.nseg);
@@ -1531,6 +1533,9 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       // 0/1 cells: every count <= K; below 2^16 the epilogue stores u16 (halves C traffic)
       const bool c16 = K < 65536;
       void* C = c16 ? (void*)ar.get<uint16_t>(Gp * Hc) : (void*)ar.get<int32_t>(Gp * Hc);
+      // N tiles over the H real columns only; rows H..N of B are zero (allocated up to Hp,
+      // min(Hc, Hp) >= 240 keeps the 240-row box inside the tensor map)
+      ga.N = std::min(Hc, Hp);
       ga.elem = ELEM_FP4; ga.A = op4A; ga.lda = Kp4 / 2; ga.B = op4B; ga.ldb = Kp4 / 2;
       ga.k_begin = 0; ga.k_len = Kp4 / 2; ga.epi = c16 ? EPI_STORE16 : EPI_STORE32; ga.C = C; ga.ldc = Hc;
       ga.cnt_out = value_cnt; ga.ldcnt = ca.nseg;
@@ -1656,7 +1661,7 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
       const bool c16 = K < 65536;  // a pattern count is <= K
       void* E = c16 ? (void*)ar.get<uint16_t>(Gp * Hc) : (void*)ar.get<int32_t>(Gp * Hc);
       GemmArgs ge{};
-      ge.M = Gp; ge.N = Hp; ge.elem = ELEM_FP4; ge.A = patA; ge.lda = Kp4 / 2; ge.B = patB; ge.ldb = Kp4 / 2;
+      ge.M = Gp; ge.N = std::min(Hc, Hp); ge.elem = ELEM_FP4; ge.A = patA; ge.lda = Kp4 / 2; ge.B = patB; ge.ldb = Kp4 / 2;
       ge.k_begin = 0; ge.k_len = Kp4 / 2; ge.epi = c16 ? EPI_STORE16 : EPI_STORE32; ge.C = E; ge.ldc = Hc;
       ge.cnt_out = seg_cnt; ge.ldcnt = ca.nseg;
       with_bs(ge, 3, Kp4 / 256, Kp4 / 256);
