@@ -661,18 +661,17 @@ bool hashpart_query(tcudb_ctx* ctx, Arena& ar, const tcudb_table* A, const tcudb
   ca.h_out_type = B->group.type == TCUDB_I64 ? 1 : 0;
   ca.agg_out = 0;
   void* ctmp = ar.get<char>((int64_t)compact_temp_bytes(G, ca.nseg));
-  int64_t* d_nnz = ar.get<int64_t>(1);
+  // the result size lands next to the exact J, K the expand summed (d_jk[0..1]): one read
+  int64_t* d_nnz = reinterpret_cast<int64_t*>(d_jk + 2);
   CK(launch_compact_count(ca, nullptr, d_nnz, ctmp, s, L));
   int64_t nnz = 0;
   {
-    // nnz and the exact J, K measured by the expand, in one read
     int64_t* hp = static_cast<int64_t*>(ctx->pinned);
-    CK(cudaMemcpyAsync(hp, d_nnz, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + 1, d_jk, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp, d_jk, 24, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    nnz = hp[0];
-    J = (unsigned long long)hp[1];
-    K = hp[2];
+    J = (unsigned long long)hp[0];
+    K = hp[1];
+    nnz = hp[2];
   }
   // the estimate was wrong past a guard bound: the cells may have wrapped — decide again on
   // the general path (nothing is returned from this one)
@@ -732,19 +731,20 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
   tm.mark(nullptr);
   // ---------------- a1: statistics
   ColDesc cols[6] = {ak, bk, ag, bh, av, bw};
-  ColStats* dstats = ar.get<ColStats>(6);
+  // the column statistics and the sketch gate flags in one block (one host read)
+  char* sblk = ar.get<char>((int64_t)(sizeof(ColStats) * 6 + 16));
+  ColStats* dstats = reinterpret_cast<ColStats*>(sblk);
   // #distinct sketches (HyperLogLog) ride along with the statistics pass on large inputs;
   // both come back in the same device->host read
   constexpr int64_t kSketchMin = 1 << 20;
   unsigned* hll_regs = (nA + nB >= kSketchMin) ? ar.zeros<unsigned>(3 * kHllM) : nullptr;
-  int* d_gate = hll_regs ? ar.zeros<int>(4) : nullptr;
+  int* d_gate = hll_regs ? reinterpret_cast<int*>(sblk + sizeof(ColStats) * 6) : nullptr;
+  if (d_gate) CK(cudaMemsetAsync(d_gate, 0, 16, s));
   CK(launch_col_stats(cols, dstats, s, L, hll_regs, d_gate));
-  CK(cudaMemcpyAsync(ctx->pinned, dstats, sizeof(ColStats) * 6, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->pinned, dstats, sizeof(ColStats) * 6 + (hll_regs ? 16 : 0), cudaMemcpyDeviceToHost, s));
   int* h_gate = reinterpret_cast<int*>(static_cast<char*>(ctx->pinned) + sizeof(ColStats) * 6);
-  if (hll_regs) {
-    CK(cudaMemcpyAsync(h_gate, d_gate, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+  if (hll_regs)
     CK(cudaMemcpyAsync(ctx->pinned_big, hll_regs, sizeof(unsigned) * 3 * kHllM, cudaMemcpyDeviceToHost, s));
-  }
   CK(cudaStreamSynchronize(s));
   ColStats hs[6];
   std::memcpy(hs, ctx->pinned, sizeof(hs));
