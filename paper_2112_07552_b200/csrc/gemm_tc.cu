@@ -9,7 +9,9 @@
 //   * TMA 2D tile loads with 128-byte swizzle into a 4-stage mbarrier ring;
 //   * persistent CTAs (grid = #SMs) walking a grouped tile order;
 //   * warp roles: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-5 epilogue.
-// Tile 128 x 256 x (128 bytes of K) per stage.
+// Tile 128 x 256 x (128 bytes of K) per stage (1-CTA kernel, kind::i8 / kind::f16); the e2m1
+// product runs on the CTA-pair kernel k_gemm_tc2 (cta_group::2, 256 x 240 pair tiles, each CTA
+// staging 128 A rows + 120 B rows per stage), which halves B's L2 -> SM bytes per MAC.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
