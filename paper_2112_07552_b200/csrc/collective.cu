@@ -38,6 +38,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -315,6 +317,17 @@ std::vector<int64_t> balanced_bounds(const NcclComm& nc, const tcudb_table& T, c
   const std::vector<int64_t> all = nc.gather_vec(msg.data(), kSampleMsg, s);
   std::vector<int64_t> b(nc.nranks > 1 ? nc.nranks - 1 : 1, 0);
   shard_bounds(all.data(), nc.nranks, b.data());
+  // every rank must route by the SAME bounds (a group range split over two ranks would come
+  // back twice): rank 0's bounds are allgathered and used everywhere; a rank whose own
+  // computation differed reports it (TCUDB_DEBUG_BOUNDS=1)
+  const std::vector<int64_t> ball = nc.gather_vec(b.data(), (int)b.size(), s);
+  bool same = true;
+  for (size_t i = 0; i < b.size(); ++i) same = same && ball[i] == b[i];
+  if (!same) {
+    static const bool dbg = getenv("TCUDB_DEBUG_BOUNDS") && getenv("TCUDB_DEBUG_BOUNDS")[0] == '1';
+    if (dbg) fprintf(stderr, "tcudb: rank %d range bounds differ from rank 0's (using rank 0's)\n", nc.rank);
+    for (size_t i = 0; i < b.size(); ++i) b[i] = ball[i];
+  }
   return b;
 }
 

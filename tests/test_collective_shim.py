@@ -110,6 +110,12 @@ def _diff_report(r, out, ref):
     dup = len(out["agg"]) - len(got)
     rep = {"rank": r, "n": int(len(out["agg"])), "n_ref": int(len(ref["cnt"])), "duplicates": int(dup),
            "extra": [list(map(int, x)) for x in extra], "missing": [list(map(int, x)) for x in missing]}
+    if dup and "g" in out and "h" in out:
+        # where the repeated groups sit: (g, h) order breaks at the start of a repeated run
+        g, h = np.asarray(out["g"]).astype(np.int64), np.asarray(out["h"]).astype(np.int64)
+        brk = np.nonzero((g[1:] < g[:-1]) | ((g[1:] == g[:-1]) & (h[1:] <= h[:-1])))[0]
+        rep["order_breaks"] = [[int(i + 1), int(g[i]), int(h[i]), int(g[i + 1]), int(h[i + 1])] for i in brk[:20]]
+        rep["n_order_breaks"] = int(len(brk))
     os.makedirs("gpurun_out", exist_ok=True)
     with open(os.path.join("gpurun_out", "collective_diff.jsonl"), "a") as f:
         f.write(json.dumps(rep) + "\n")
