@@ -1352,10 +1352,16 @@ tcudb_status run_join_agg(tcudb_ctx* ctx, const tcudb_table* A, const tcudb_tabl
             f[0].pat = patA; f[1].pat = patB;
             f[0].ld_pat = f[1].ld_pat = Kp4 / 2;
           }
-          const size_t ws = std::max(fill_direct_ws(Gp, Kp, split), fill_direct_ws(Hp, Kp, split));
-          void* w = ar.get<uint8_t>((int64_t)ws);
+          // A's fill on the query stream, B's on the side stream (own binning workspace): the
+          // second fill's bin kernel starts while the first one's tail and tile pass run
+          const cudaStream_t s2 = side_stream_for(ctx, nA + nB);
+          void* w = ar.get<uint8_t>((int64_t)fill_direct_ws(Gp, Kp, split));
+          void* w2 = s2 ? ar.get<uint8_t>((int64_t)fill_direct_ws(Hp, Kp, split)) : w;
+          SideJoinGuard sjg{ctx, s};
+          if (s2) { side_fork(ctx, s); sjg.armed = true; }
           CK(launch_fill_direct(f[0], split, w, s, L));
-          CK(launch_fill_direct(f[1], split, w, s, L));
+          CK(launch_fill_direct(f[1], split, w2, s2 ? s2 : s, L));
+          if (s2) { side_join(ctx, s); sjg.armed = false; }
           CK(cudaMemcpyAsync(ctx->pinned, fs, sizeof(FillStats) * 2, cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
           FillStats hf[2];
